@@ -1,0 +1,230 @@
+/*
+ * lowdiff.h -- C ABI of the B200-native LowDiff hot path (arXiv 2509.04084, SC'25).
+ *
+ * LowDiff reuses the compressed gradients of data-parallel training as differential
+ * checkpoints (Finding 1; Alg. 1).  This library is the
+ * data-parallel hot path of that method on sm_100a:
+ *   lowdiff_compress       per-layer top-k with error feedback       Alg. 1 l.4
+ *   lowdiff_exchange       allgather of fixed-K blocks + merge       Alg. 1 l.5,7 PAPER.md:231,235
+ *   lowdiff_batch_persist  reuse queue -> pinned ring -> batched file Alg. 1 l.6,12-14
+ *   lowdiff_full_ckpt      sharded full checkpoint C^F               Alg. 1 l.15
+ *   lowdiff_recover        chain scan + fused replay onto C^F        Alg. 1 l.16-24 PAPER.md:248-259
+ * plus the LowDiff+ layer-wise dense snapshot (Alg. 2 l.19) and a
+ * device-resident replay entry point used by recover and by the benchmark.
+ *
+ * Conventions (all calls):
+ *  - Every call returns lowdiff_status; none throws, aborts or exits.  A CUDA or NCCL
+ *    failure poisons the context: every later call returns the same code.
+ *  - Device pointers are plain CUDA device addresses (e.g. torch tensor data_ptr()),
+ *    contiguous, 16-byte aligned (else LOWDIFF_E_INVALID).  The CALLER owns every
+ *    device buffer; the library never frees or reallocates caller memory.
+ *  - `stream` arguments are cudaStream_t handles passed as void*.  Calls that take a
+ *    stream enqueue work on it and return without a host synchronisation unless
+ *    stated otherwise.
+ *  - The LIBRARY owns the context, its NCCL communicator, side streams and events,
+ *    pinned host ring, device scratch (sized at create; no allocation on the
+ *    compress/exchange hot path), the writer thread, and the files it writes.
+ *  - One context per (process, GPU); one host thread drives a context.
+ * File formats and the numerical readings are specified in DESIGN.md.
+ */
+#ifndef LOWDIFF_H_
+#define LOWDIFF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LOWDIFF_OK = 0,
+  LOWDIFF_E_INVALID = 1,  /* bad argument: NULL, misaligned, out of range            */
+  LOWDIFF_E_DIM = 2,      /* size mismatch ("dimension error")        */
+  LOWDIFF_E_NUMERIC = 3,  /* non-finite accumulated gradient           */
+  LOWDIFF_E_CUDA = 4,     /* CUDA runtime failure (context poisoned)                */
+  LOWDIFF_E_NCCL = 5,     /* NCCL failure (context poisoned)                        */
+  LOWDIFF_E_IO = 6,       /* storage failure                          */
+  LOWDIFF_E_CORRUPT = 7,  /* CRC / format / header mismatch       */
+  LOWDIFF_E_GAP = 8,      /* missing full checkpoint or diff in the chain */
+  LOWDIFF_E_STATE = 9     /* call out of order (iteration not consecutive, FIFO S:249) */
+} lowdiff_status;
+
+typedef enum { LOWDIFF_SGD = 0, LOWDIFF_ADAM = 1 } lowdiff_optim;
+
+/* Per-iteration optimizer scalars, derived on the host in double and rounded once
+ * (R-11); stored in every differential block so replay never re-derives them. */
+typedef struct { float lr, bc1_inv, bc2_inv; } lowdiff_step_scalars;
+
+/* Adam constants {beta1, 1-beta1, beta2, 1-beta2, eps}, each rounded once from double. */
+typedef struct { float beta1, one_minus_beta1, beta2, one_minus_beta2, eps; } lowdiff_adam_consts;
+
+typedef struct {
+  int32_t n_layers;            /* entries of the layer table (one per parameter tensor)        */
+  const int64_t *numel;        /* [n_layers] sizes, forward order; Psi = sum < 2^32            */
+  uint32_t density_ppm;        /* 1..1e6; k_l = max(1, min(n_l, floor(n_l*ppm/1e6)))  (R-3)    */
+  int32_t error_feedback;      /* 1: acc = residual + grad, residual' = unsent part (default)  */
+  int32_t mean;                /* 1: merged G = sum / world (default); 0: sum                  */
+  int32_t rank, world;         /* data-parallel rank and world size                            */
+  const void *nccl_unique_id;  /* 128-byte ncclUniqueId from rank 0 (world > 1).  NULL: no
+                                  communicator -- a recovery/merge-only context (exchange then
+                                  returns LOWDIFF_E_STATE)                                     */
+  int32_t device;              /* CUDA device ordinal this context drives                      */
+  const char *ckpt_dir;        /* directory for .ldb/.ldf files; NULL disables persistence     */
+  int32_t batch_size;          /* b >= 1 differentials per .ldb file            */
+  int32_t ring_slots;          /* pinned ring slots R >= b (0 -> 2b)                           */
+  int32_t write_files;         /* 1: writer thread writes files; 0: D2H only (ring recycled)   */
+  int32_t fsync;               /* 1: fsync each file before rename                             */
+  int32_t optim;               /* lowdiff_optim recorded in the files and used by recover      */
+  lowdiff_adam_consts adam;    /* recorded in the files and used by recover                    */
+} lowdiff_config;
+
+typedef struct lowdiff_ctx lowdiff_ctx;
+
+/* Create a context: validates the layer table, builds the chunk plan, allocates device
+ * scratch and the pinned ring, initialises NCCL (world > 1) and starts the writer thread.
+ * Synchronous.  *out is NULL on failure. */
+lowdiff_status lowdiff_create(const lowdiff_config *cfg, lowdiff_ctx **out);
+
+/* Drain all pending work (implies lowdiff_sync), stop the writer, free library resources.
+ * Returns the first deferred error, if any.  ctx may be NULL. */
+lowdiff_status lowdiff_destroy(lowdiff_ctx *ctx);
+
+/* Psi and K = sum_l k_l. */
+lowdiff_status lowdiff_query(const lowdiff_ctx *ctx, int64_t *psi, int64_t *k_tot);
+
+/* k_l and koff_l (offset of layer l's entries inside a send block). */
+lowdiff_status lowdiff_layer_k(const lowdiff_ctx *ctx, int32_t layer, int64_t *k, int64_t *koff);
+
+/* 1. Compress (Alg. 1 line 4).  For every layer l:
+ *      acc = residual + grad (error_feedback = 1) or grad;
+ *      select the k_l entries with the largest key = bits(acc) & 0x7FFFFFFF, ties to the
+ *      LOWER index; write them index-ascending into `send` at koff_l:
+ *      send = idx u32[K] (global flat index) || val f32-bits u32[K];
+ *      residual' = acc with the selected entries set to +0.0f.
+ *    grad: device f32[Psi] (read).  residual: device f32[Psi] (read/write; ignored and may
+ *    be NULL when error_feedback = 0).  send: device u32[2K] (written).
+ *    A non-finite acc sets a device flag; the next persist/sync returns LOWDIFF_E_NUMERIC.
+ *    If `send` is still being copied out by a previous lowdiff_batch_persist, the stream
+ *    waits for that copy (write-after-read). */
+lowdiff_status lowdiff_compress(lowdiff_ctx *ctx, const float *grad, float *residual,
+                                uint32_t *send, void *stream);
+
+/* 2. Exchange (Alg. 1 lines 5 and 7): ncclAllGather of the fixed-size
+ *    blocks (rank r's block lands at gathered + r*2K), then the merge
+ *      G[j] = ((((+0 + v_0[j]) + v_1[j]) + ... ) + v_{N-1}[j]) / N   (rank order, IEEE divide)
+ *    where v_r[j] is rank r's value when j is among its indices.  No atomics: deterministic.
+ *    send: device u32[2K].  gathered: device u32[world*2K] (may be NULL when world == 1).
+ *    dense_out: device f32[Psi] (written entirely). */
+lowdiff_status lowdiff_exchange(lowdiff_ctx *ctx, const uint32_t *send, uint32_t *gathered,
+                                float *dense_out, void *stream);
+
+/* Merge only (the second half of lowdiff_exchange) for a gathered buffer of `world`
+ *    blocks that the caller assembled itself.  world >= 1; same arithmetic as above. */
+lowdiff_status lowdiff_merge(lowdiff_ctx *ctx, int32_t world, const uint32_t *gathered,
+                             float *dense_out, void *stream);
+
+/* 3. Batch persist (Alg. 1 line 6 Q.put, lines 12-14; Steps 1-3).
+ *    Records an event on `producer`; a library side stream waits on it and copies this
+ *    rank's own send block (8K bytes) into a pinned-host ring slot.  The writer thread
+ *    groups b consecutive iterations into one .ldb file written with one writev
+ *    (`*.tmp`, then rename).  `iteration` must be the previous call's + 1 (else
+ *    LOWDIFF_E_STATE).  Blocks on the host only while the ring is full (backpressure);
+ *    the blocked time is reported by lowdiff_stats.  scalars: host pointer. */
+lowdiff_status lowdiff_batch_persist(lowdiff_ctx *ctx, int64_t iteration,
+                                     const lowdiff_step_scalars *scalars, const uint32_t *send,
+                                     void *producer);
+
+/* 4. Full checkpoint (Alg. 1 line 15): this rank's shard
+ *    [floor(rank*Psi/world), floor((rank+1)*Psi/world)) of p, m, v (m, v may be NULL ->
+ *    zeros), copied D2H on a side stream after an event on `producer`; `producer` then
+ *    waits (device-side) for the copy, so the caller's next update cannot overwrite the
+ *    snapshot (write-after-read).  Persisted asynchronously as .ldf.
+ *    `iteration` = optimizer steps applied to (p, m, v). */
+lowdiff_status lowdiff_full_ckpt(lowdiff_ctx *ctx, int64_t iteration, const float *p,
+                                 const float *m, const float *v, void *producer);
+
+/* 5. Recover (Alg. 1 recovery process; Eq. 2):
+ *    F = latest iteration <= target (-1: no bound) with all `world` .ldf shards present;
+ *    then blocks F+1..target of every rank must exist (LOWDIFF_E_GAP) and verify
+ *    (LOWDIFF_E_CORRUPT); target = -1 replays the longest gap-free chain.  Loads C^F into
+ *    p, m, v (device f32[Psi]; m, v may be NULL for SGD), replays the blocks through the
+ *    optimizer recorded in the files with the fused replay kernel, and stores the
+ *    iteration reached in *recovered.  Synchronous (returns after the replay finished). */
+lowdiff_status lowdiff_recover(lowdiff_ctx *ctx, int64_t target, float *p, float *m, float *v,
+                               int64_t *recovered, void *stream);
+
+/* Fused replay of n_steps differentials that are already in device memory:
+ *    diffs: device u32[n_steps][world][2K] (the gathered blocks of each step, rank order);
+ *    scalars: host [n_steps]; optim: lowdiff_optim.  For each step t in order,
+ *    G_t = merge(diffs[t]) then p, m, v <- SGD/Adam(G_t, scalars[t]).  Every element's
+ *    result equals applying the steps one at a time.  Asynchronous on `stream`. */
+lowdiff_status lowdiff_replay(lowdiff_ctx *ctx, int32_t optim, int32_t world, int64_t n_steps,
+                              const uint32_t *diffs, const lowdiff_step_scalars *scalars,
+                              float *p, float *m, float *v, void *stream);
+
+/* LowDiff+ layer-wise snapshot (Sec. 5.1; Alg. 2 l.19):
+ *    after the caller's gradient sync of layers [first_layer, first_layer+n_layers)
+ *    (contiguous in the flat gradient; grad_bucket points at layer first_layer), copy
+ *    them D2H on a side stream into the pinned buffer of `iteration` (double-buffered:
+ *    iterations t and t+1 may be in flight). */
+lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx *ctx, int64_t iteration, int32_t first_layer,
+                                      int32_t n_layers, const float *grad_bucket, void *producer);
+
+/* Wait until every layer of `iteration` has been snapshotted; *host_grad = pinned
+ *    f32[Psi] valid until iteration + 2 is first snapshotted.  LOWDIFF_E_STATE if some
+ *    layer of that iteration was never submitted. */
+lowdiff_status lowdiff_snapshot_wait(lowdiff_ctx *ctx, int64_t iteration, const float **host_grad);
+
+/* Drain D2H copies and the writer (flushing a final partial batch) and
+ * surface deferred errors. */
+lowdiff_status lowdiff_sync(lowdiff_ctx *ctx);
+
+typedef struct {
+  int64_t files_written, bytes_written;
+  int64_t ring_stall_ns;       /* host time lowdiff_batch_persist spent blocked on a full ring */
+  int64_t writer_busy_ns;      /* writer thread time spent building + writing files            */
+  int64_t spec_hits, spec_misses;   /* large layers selected from the speculative band / refilled */
+} lowdiff_stats;
+lowdiff_status lowdiff_get_stats(const lowdiff_ctx *ctx, lowdiff_stats *out);
+
+/* Per-kernel device timing (CUDA events recorded on the launching stream).  enable != 0
+ * starts recording; lowdiff_prof_read synchronises and returns the summed milliseconds
+ * and launch count of kernel `name` since enabling ("" = all). */
+lowdiff_status lowdiff_prof_enable(lowdiff_ctx *ctx, int32_t enable);
+lowdiff_status lowdiff_prof_read(lowdiff_ctx *ctx, const char *name, double *total_ms,
+                                 int64_t *launches);
+
+/* Number of kernels this library launched on behalf of ctx since creation. */
+int64_t lowdiff_kernel_launches(const lowdiff_ctx *ctx);
+
+const char *lowdiff_last_error(const lowdiff_ctx *ctx);
+
+/* ---- host helpers (no context, no GPU needed) ---- */
+/* Write a fresh 128-byte ncclUniqueId into out (rank 0 calls this, then broadcasts). */
+lowdiff_status lowdiff_nccl_unique_id(void *out128);
+/* {lr, 1/(1-beta1^t), 1/(1-beta2^t)} in double with beta^t by t repeated products, rounded once. */
+lowdiff_status lowdiff_derive_step_scalars(int64_t t, double lr, double beta1, double beta2,
+                                           lowdiff_step_scalars *out);
+lowdiff_status lowdiff_derive_adam_consts(double beta1, double beta2, double eps,
+                                          lowdiff_adam_consts *out);
+/* CRC-32C (Castagnoli) of len bytes, as stored in the file trailers. */
+uint32_t lowdiff_crc32c(const void *data, size_t len);
+/* Locate the recoverable chain in cfg->ckpt_dir without loading it (host only):
+ *    *full_iter = F, *last_iter = last replayable iteration (target rules as recover). */
+lowdiff_status lowdiff_chain_scan(const lowdiff_config *cfg, int64_t target, int64_t *full_iter,
+                                  int64_t *last_iter);
+/* Serialise a batch file from host blocks exactly as the writer thread does (host only;
+ *    used by multi-rank host tests): blocks = n_iters x 2K u32, scalars = n_iters. */
+lowdiff_status lowdiff_write_batch_host(const lowdiff_config *cfg, int64_t first_iter,
+                                        int32_t n_iters, const lowdiff_step_scalars *scalars,
+                                        const uint32_t *blocks);
+/* Serialise this rank's full-checkpoint shard from host arrays of length Psi (host only). */
+lowdiff_status lowdiff_write_full_host(const lowdiff_config *cfg, int64_t iteration, const float *p,
+                                       const float *m, const float *v);
+int32_t lowdiff_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOWDIFF_H_ */

@@ -1,0 +1,992 @@
+// C-ABI implementation of liblowdiff: context, NCCL exchange, reuse queue -> pinned ring ->
+// writer thread, full checkpoints, chain scan + recovery, LowDiff+ snapshots.
+// The GPU kernels live in compress.cu and merge_replay.cu.  See include/lowdiff.h.
+#include <dirent.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <map>
+
+#include "internal.h"
+
+using ld::DevPlan;
+
+namespace {
+
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+lowdiff_status fail(lowdiff_ctx* c, lowdiff_status st, const std::string& msg) {
+  std::lock_guard<std::mutex> g(c->err_mu);
+  c->last_error = msg;
+  if (st == LOWDIFF_E_CUDA || st == LOWDIFF_E_NCCL) c->poisoned = st;
+  return st;
+}
+
+lowdiff_status cuda_fail(lowdiff_ctx* c, cudaError_t e, const char* what) {
+  return fail(c, LOWDIFF_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(c, e_, #call); \
+  } while (0)
+
+lowdiff_status entry(lowdiff_ctx* c) {
+  if (!c) return LOWDIFF_E_INVALID;
+  if (c->poisoned != LOWDIFF_OK) return c->poisoned;
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
+  return LOWDIFF_OK;
+}
+
+lowdiff_status take_deferred(lowdiff_ctx* c) {
+  std::lock_guard<std::mutex> g(c->err_mu);
+  lowdiff_status d = c->deferred;
+  c->deferred = LOWDIFF_OK;
+  return d;
+}
+
+void set_deferred(lowdiff_ctx* c, lowdiff_status st, const std::string& msg) {
+  std::lock_guard<std::mutex> g(c->err_mu);
+  if (c->deferred == LOWDIFF_OK) c->deferred = st;
+  c->last_error = msg;
+  if (st == LOWDIFF_E_CUDA) c->poisoned = st;
+}
+
+uint64_t k_rule(uint64_t n, uint32_t ppm) {   // DESIGN.md R-3
+  uint64_t k = n * ppm / 1000000ull;
+  return std::max<uint64_t>(1, std::min(k, n));
+}
+
+template <class T>
+lowdiff_status upload(lowdiff_ctx* c, const std::vector<T>& h, T** d) {
+  void* p = nullptr;
+  size_t bytes = std::max<size_t>(1, h.size()) * sizeof(T);
+  CK(cudaMalloc(&p, bytes));
+  c->dev_allocs.push_back(p);
+  if (!h.empty()) CK(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  *d = static_cast<T*>(p);
+  return LOWDIFF_OK;
+}
+
+lowdiff_status dalloc(lowdiff_ctx* c, size_t bytes, void** d) {
+  CK(cudaMalloc(d, std::max<size_t>(bytes, 16)));
+  c->dev_allocs.push_back(*d);
+  return LOWDIFF_OK;
+}
+
+// ---------------------------------------------------------------- chunk plan
+lowdiff_status build_plan(lowdiff_ctx* c) {
+  const int L = c->cfg.n_layers;
+  std::vector<uint64_t> off(L + 1), koff(L);
+  std::vector<uint32_t> kk(L);
+  std::vector<int32_t> small, large, chunk0, cslot;
+  std::vector<uint64_t> cbase, clo, chi;
+  for (int l = 0; l < L; ++l) {
+    off[l + 1] = off[l] + (uint64_t)c->numel[l];
+    kk[l] = (uint32_t)k_rule((uint64_t)c->numel[l], c->cfg.density_ppm);
+    koff[l] = l ? koff[l - 1] + kk[l - 1] : 0;
+  }
+  for (int l = 0; l < L; ++l) {
+    const uint64_t lo = off[l], hi = off[l + 1];
+    if (hi - lo <= (uint64_t)ld::kSmallMax) { small.push_back(l); continue; }
+    const int slot = (int)large.size();
+    large.push_back(l);
+    chunk0.push_back((int32_t)cslot.size());
+    for (uint64_t b = lo & ~3ull; b < hi; b += ld::kChunk) {
+      cslot.push_back(slot);
+      cbase.push_back(b);
+      clo.push_back(std::max(b, lo));
+      chi.push_back(std::min(b + ld::kChunk, hi));
+    }
+  }
+  chunk0.push_back((int32_t)cslot.size());
+  c->off = off;
+  c->koff = koff;
+  c->k = kk;
+  c->psi = (int64_t)off[L];
+  c->K = (int64_t)(koff[L - 1] + kk[L - 1]);
+
+  DevPlan& P = c->plan;
+  P.n_layers = L;
+  P.n_small = (int)small.size();
+  P.n_large = (int)large.size();
+  P.n_chunks = (int)cslot.size();
+  lowdiff_status st;
+  uint64_t* d_off; uint32_t* d_k; uint64_t* d_koff; int32_t *d_small, *d_large, *d_c0, *d_cslot;
+  uint64_t *d_cb, *d_clo, *d_chi;
+  if ((st = upload(c, off, &d_off)) || (st = upload(c, kk, &d_k)) || (st = upload(c, koff, &d_koff)) ||
+      (st = upload(c, small, &d_small)) || (st = upload(c, large, &d_large)) || (st = upload(c, chunk0, &d_c0)) ||
+      (st = upload(c, cslot, &d_cslot)) || (st = upload(c, cbase, &d_cb)) || (st = upload(c, clo, &d_clo)) ||
+      (st = upload(c, chi, &d_chi)))
+    return st;
+  P.layer_off = d_off; P.layer_k = d_k; P.layer_koff = d_koff;
+  P.small_layers = d_small; P.large_layers = d_large; P.large_chunk0 = d_c0;
+  P.chunk_slot = d_cslot; P.chunk_base = d_cb; P.chunk_lo = d_clo; P.chunk_hi = d_chi;
+  const size_t nc = (size_t)std::max(1, P.n_chunks), nl = (size_t)std::max(1, P.n_large);
+  void* p;
+  if ((st = dalloc(c, nc * ld::kChunk * 4, &p))) return st; P.cand_idx = (uint32_t*)p;
+  if ((st = dalloc(c, nc * ld::kChunk * 4, &p))) return st; P.cand_val = (uint32_t*)p;
+  if ((st = dalloc(c, nc * 4 * 6, &p))) return st;
+  P.chunk_count = (uint32_t*)p; P.chunk_gt = P.chunk_count + nc; P.chunk_eq = P.chunk_gt + nc;
+  P.chunk_out = P.chunk_eq + nc; P.chunk_take = P.chunk_out + nc; P.refill_list = P.chunk_take + nc;
+  if ((st = dalloc(c, nl * (2048 + 2048 + 512) * 4, &p))) return st; P.hist = (uint32_t*)p;
+  if ((st = dalloc(c, nl * sizeof(ld::LayerSel), &p))) return st; P.sel = (ld::LayerSel*)p;
+  if ((st = dalloc(c, nl * 4, &p))) return st; P.thr = (uint32_t*)p;
+  CK(cudaMemset(P.thr, 0xFF, nl * 4));   // no speculative band before the first call
+  if ((st = dalloc(c, 8 * 4, &p))) return st; P.counters = (uint32_t*)p;
+  if ((st = dalloc(c, 4 * 4, &p))) return st; P.err = (uint32_t*)p;
+  CK(cudaMemset(P.err, 0, 16));
+  CK(cudaMemset(P.err + 1, 0xFF, 4));
+  return LOWDIFF_OK;
+}
+
+// ---------------------------------------------------------------- writer thread
+void write_batch(lowdiff_ctx* c, const std::vector<int>& batch) {
+  if (!c->cfg.write_files || batch.empty()) return;
+  const int64_t t0 = now_ns();
+  std::vector<uint8_t> pre = c->prefix;
+  const uint64_t first = (uint64_t)c->slots[batch[0]].iteration;
+  const uint32_t n = (uint32_t)batch.size();
+  std::memcpy(pre.data() + 16, &first, 8);
+  std::memcpy(pre.data() + 24, &n, 4);
+  std::vector<std::pair<const void*, size_t>> parts;
+  parts.push_back({pre.data(), pre.size()});
+  uint32_t crc = ld::crc32c_update(0xFFFFFFFFu, pre.data(), pre.size());
+  const size_t blk = 32 + 8 * (size_t)c->K;
+  for (int s : batch) {
+    parts.push_back({c->slots[s].host, blk});
+    crc = ld::crc32c_update(crc, c->slots[s].host, blk);
+  }
+  crc ^= 0xFFFFFFFFu;
+  parts.push_back({&crc, 4});
+  std::string err;
+  lowdiff_status st = ld::write_file_atomic(ld::batch_name(c->ckpt_dir, c->cfg.rank, (int64_t)first), parts,
+                                            c->cfg.fsync != 0, &err);
+  if (st != LOWDIFF_OK) {
+    set_deferred(c, st, err);
+  } else {
+    c->files_written += 1;
+    size_t tot = 0;
+    for (auto& p : parts) tot += p.second;
+    c->bytes_written += (int64_t)tot;
+  }
+  c->writer_ns += now_ns() - t0;
+}
+
+void release(lowdiff_ctx* c, std::vector<int>& batch) {
+  std::lock_guard<std::mutex> g(c->mu);
+  for (int s : batch) c->free_slots.push_back(s);
+  batch.clear();
+  c->cv_free.notify_all();
+}
+
+
+void writer_loop(lowdiff_ctx* c) {
+  std::vector<int> batch;
+  uint32_t err_seen = 0;
+  cudaSetDevice(c->device);
+  for (;;) {
+    int slot = -1;
+    bool do_flush = false, quit = false;
+    {
+      std::unique_lock<std::mutex> lk(c->mu);
+      c->cv_work.wait(lk, [&] { return c->stop || c->flush_req || !c->queued.empty(); });
+      if (!c->queued.empty()) {
+        slot = c->queued.front();
+        c->queued.pop_front();
+        c->writer_busy = 1;
+      } else if (c->flush_req) {
+        do_flush = true;
+        c->writer_busy = 1;
+      } else {
+        quit = true;
+      }
+    }
+    if (slot >= 0) {
+      ld::Slot& S = c->slots[slot];
+      cudaError_t e = cudaEventSynchronize(S.done);
+      bool drop = false;
+      if (e != cudaSuccess) {
+        set_deferred(c, LOWDIFF_E_CUDA, std::string("D2H of a differential: ") + cudaGetErrorString(e));
+        drop = true;
+      } else if (S.err_host[0] != err_seen) {
+        err_seen = S.err_host[0];
+        char msg[160];
+        std::snprintf(msg, sizeof msg, "non-finite accumulated gradient before iteration %lld (first layer %u)",
+                      (long long)S.iteration, S.err_host[1]);
+        set_deferred(c, LOWDIFF_E_NUMERIC, msg);
+        drop = true;
+      }
+      if (drop) {
+        write_batch(c, batch);      // keep what is consecutive; the chain stops before this iteration
+        release(c, batch);
+        std::vector<int> one{slot};
+        release(c, one);
+      } else {
+        batch.push_back(slot);
+        if ((int)batch.size() == c->b) {
+          write_batch(c, batch);
+          release(c, batch);
+        }
+      }
+    } else if (do_flush) {
+      write_batch(c, batch);
+      release(c, batch);
+      std::lock_guard<std::mutex> g(c->mu);
+      c->flush_req = false;
+    } else if (quit) {
+      write_batch(c, batch);
+      release(c, batch);
+      return;
+    }
+    std::lock_guard<std::mutex> g(c->mu);
+    c->writer_busy = 0;
+    c->cv_idle.notify_all();
+  }
+}
+
+// ---------------------------------------------------------------- chain scan (recovery)
+struct Chain {
+  int64_t F = -1, last = -1;
+  std::vector<std::string> full_paths;                               // [world]
+  std::vector<std::map<int64_t, std::pair<std::string, uint32_t>>> where;  // rank -> t -> (file, block)
+};
+
+bool parse_name(const char* name, const char* kind, const char* ext, unsigned* rank, long long* it) {
+  // ld_<kind>_r%03u_%012lld.<ext>
+  char pat[64];
+  std::snprintf(pat, sizeof pat, "ld_%s_r%%3u_%%12lld.%%3s", kind);
+  char tail[8] = {0};
+  if (std::strlen(name) != 29) return false;
+  if (std::sscanf(name, pat, rank, it, tail) != 3) return false;
+  return std::strcmp(tail, ext) == 0;
+}
+
+bool read_all(const std::string& path, std::vector<uint8_t>& out) {
+  int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+  if (fd < 0) return false;
+  struct stat sb;
+  if (fstat(fd, &sb) != 0) { ::close(fd); return false; }
+  out.resize((size_t)sb.st_size);
+  size_t got = 0;
+  while (got < out.size()) {
+    ssize_t r = ::pread(fd, out.data() + got, out.size() - got, (off_t)got);
+    if (r <= 0) { ::close(fd); return false; }
+    got += (size_t)r;
+  }
+  ::close(fd);
+  return true;
+}
+
+bool read_head(const std::string& path, uint8_t* buf, size_t n, size_t* fsize) {
+  int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+  if (fd < 0) return false;
+  struct stat sb;
+  bool ok = fstat(fd, &sb) == 0 && ::pread(fd, buf, n, 0) == (ssize_t)n;
+  *fsize = ok ? (size_t)sb.st_size : 0;
+  ::close(fd);
+  return ok;
+}
+
+template <class T> T rd(const uint8_t* p) { T v; std::memcpy(&v, p, sizeof v); return v; }
+
+lowdiff_status scan_chain(const lowdiff_config& cfg, int64_t target, Chain* ch, std::string* err) {
+  const uint32_t world = (uint32_t)cfg.world;
+  std::map<int64_t, std::map<uint32_t, std::string>> fulls;
+  std::vector<std::map<int64_t, std::string>> diffs(world);
+  DIR* d = opendir(cfg.ckpt_dir);
+  if (!d) { *err = std::string("cannot open ") + cfg.ckpt_dir; return LOWDIFF_E_IO; }
+  while (dirent* de = readdir(d)) {
+    unsigned r; long long it;
+    if (parse_name(de->d_name, "full", "ldf", &r, &it) && r < world)
+      fulls[it][r] = std::string(cfg.ckpt_dir) + "/" + de->d_name;
+    else if (parse_name(de->d_name, "diff", "ldb", &r, &it) && r < world)
+      diffs[r][it] = std::string(cfg.ckpt_dir) + "/" + de->d_name;
+  }
+  closedir(d);
+  ch->F = -1;
+  for (auto it = fulls.rbegin(); it != fulls.rend(); ++it) {
+    if (target >= 0 && it->first > target) continue;
+    if (it->second.size() == world) {
+      ch->F = it->first;
+      ch->full_paths.clear();
+      for (uint32_t r = 0; r < world; ++r) ch->full_paths.push_back(it->second[r]);
+      break;
+    }
+  }
+  if (ch->F < 0) { *err = "no complete full checkpoint <= target"; return LOWDIFF_E_GAP; }
+  ch->where.assign(world, {});
+  for (uint32_t r = 0; r < world; ++r) {
+    for (auto& fe : diffs[r]) {     // ascending first iteration: later files win
+      uint8_t h[64];
+      size_t fsz = 0;
+      if (!read_head(fe.second, h, 64, &fsz) || std::memcmp(h, "LDB1", 4) != 0) {
+        *err = "unreadable batch file " + fe.second;
+        return LOWDIFF_E_CORRUPT;
+      }
+      const uint32_t n = rd<uint32_t>(h + 24);
+      for (uint32_t i = 0; i < n; ++i) ch->where[r][fe.first + i] = {fe.second, i};
+    }
+  }
+  int64_t last = ch->F;
+  for (;;) {
+    const int64_t t = last + 1;
+    if (target >= 0 && t > target) break;
+    bool all = true;
+    for (uint32_t r = 0; r < world && all; ++r) all = ch->where[r].count(t) > 0;
+    if (!all) break;
+    last = t;
+  }
+  if (target >= 0 && last < target) {
+    *err = "differential chain has a gap after iteration " + std::to_string(last);
+    return LOWDIFF_E_GAP;
+  }
+  ch->last = last;
+  return LOWDIFF_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- profiling helpers
+namespace ld {
+void prof_begin(lowdiff_ctx* c, const char* name, cudaStream_t s, int* handle) {
+  *handle = -1;
+  if (!c->prof) return;
+  ProfRec r{name, nullptr, nullptr};
+  if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
+  cudaEventRecord(r.a, s);
+  c->prof_recs.push_back(r);
+  *handle = (int)c->prof_recs.size() - 1;
+}
+void prof_end(lowdiff_ctx* c, int handle, cudaStream_t s) {
+  if (handle < 0 || !c->prof) return;
+  cudaEventRecord(c->prof_recs[handle].b, s);
+}
+}  // namespace ld
+
+extern "C" {
+
+int32_t lowdiff_abi_version(void) { return 1; }
+
+lowdiff_status lowdiff_nccl_unique_id(void* out128) {
+  if (!out128) return LOWDIFF_E_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return LOWDIFF_E_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, 128);
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_derive_step_scalars(int64_t t, double lr, double beta1, double beta2,
+                                           lowdiff_step_scalars* out) {
+  if (!out || t < 1) return LOWDIFF_E_INVALID;
+  double b1t = 1.0, b2t = 1.0;   // beta^t by t repeated double products (R-11)
+  for (int64_t i = 0; i < t; ++i) { b1t *= beta1; b2t *= beta2; }
+  out->lr = (float)lr;
+  out->bc1_inv = (float)(1.0 / (1.0 - b1t));
+  out->bc2_inv = (float)(1.0 / (1.0 - b2t));
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_derive_adam_consts(double beta1, double beta2, double eps, lowdiff_adam_consts* out) {
+  if (!out) return LOWDIFF_E_INVALID;
+  out->beta1 = (float)beta1;
+  out->one_minus_beta1 = (float)(1.0 - beta1);
+  out->beta2 = (float)beta2;
+  out->one_minus_beta2 = (float)(1.0 - beta2);
+  out->eps = (float)eps;
+  return LOWDIFF_OK;
+}
+
+uint32_t lowdiff_crc32c(const void* data, size_t len) {
+  return ld::crc32c_update(0xFFFFFFFFu, data, len) ^ 0xFFFFFFFFu;
+}
+
+static lowdiff_status validate_cfg(const lowdiff_config* cfg) {
+  if (!cfg || cfg->n_layers <= 0 || !cfg->numel) return LOWDIFF_E_INVALID;
+  if (cfg->density_ppm < 1 || cfg->density_ppm > 1000000) return LOWDIFF_E_INVALID;
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return LOWDIFF_E_INVALID;
+  if (cfg->optim != LOWDIFF_SGD && cfg->optim != LOWDIFF_ADAM) return LOWDIFF_E_INVALID;
+  uint64_t psi = 0;
+  for (int l = 0; l < cfg->n_layers; ++l) {
+    if (cfg->numel[l] <= 0) return LOWDIFF_E_DIM;
+    psi += (uint64_t)cfg->numel[l];
+  }
+  if (psi >= (1ull << 32)) return LOWDIFF_E_DIM;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_create(const lowdiff_config* cfg, lowdiff_ctx** out) {
+  if (!out) return LOWDIFF_E_INVALID;
+  *out = nullptr;
+  lowdiff_status st = validate_cfg(cfg);
+  if (st) return st;
+  lowdiff_ctx* c = new lowdiff_ctx();
+  c->cfg = *cfg;
+  c->numel.assign(cfg->numel, cfg->numel + cfg->n_layers);
+  c->cfg.numel = c->numel.data();
+  c->cfg.nccl_unique_id = nullptr;
+  if (cfg->ckpt_dir) c->ckpt_dir = cfg->ckpt_dir;
+  c->cfg.ckpt_dir = cfg->ckpt_dir ? c->ckpt_dir.c_str() : nullptr;
+  c->device = cfg->device;
+  c->b = std::max(1, cfg->batch_size);
+  c->R = cfg->ring_slots > 0 ? std::max(cfg->ring_slots, c->b) : 2 * c->b;
+  auto bail = [&](lowdiff_status s) { lowdiff_destroy(c); return s; };
+  if ((st = entry(c))) return bail(st);
+  if ((st = build_plan(c))) return bail(st);
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_tmp, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->last_d2h, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->full_done, cudaEventDisableTiming) != cudaSuccess)
+    return bail(LOWDIFF_E_CUDA);
+  for (int i = 0; i < 2; ++i)
+    if (cudaEventCreateWithFlags(&c->snap_done[i], cudaEventDisableTiming) != cudaSuccess) return bail(LOWDIFF_E_CUDA);
+  if (cfg->world > 1 && cfg->nccl_unique_id) {   // no id: recovery / merge-only context
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
+    if (ncclCommInitRank(&c->comm, cfg->world, id, cfg->rank) != ncclSuccess) return bail(LOWDIFF_E_NCCL);
+  }
+  // pinned ring: R slots of (32-byte block header + 8K payload), 4 KiB aligned
+  c->slot_bytes = ((32 + 8 * (size_t)c->K) + 4095) & ~(size_t)4095;
+  if (cudaHostAlloc((void**)&c->ring, c->slot_bytes * c->R, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->err_pinned, sizeof(uint32_t) * 2 * c->R, cudaHostAllocDefault) != cudaSuccess)
+    return bail(LOWDIFF_E_CUDA);
+  std::memset(c->err_pinned, 0, sizeof(uint32_t) * 2 * c->R);
+  c->slots.resize(c->R);
+  for (int s = 0; s < c->R; ++s) {
+    c->slots[s].host = c->ring + s * c->slot_bytes;
+    c->slots[s].err_host = c->err_pinned + 2 * s;
+    if (cudaEventCreateWithFlags(&c->slots[s].done, cudaEventDisableTiming) != cudaSuccess) return bail(LOWDIFF_E_CUDA);
+    c->free_slots.push_back(s);
+  }
+  ld::build_prefix(c->cfg, c->numel, c->psi, c->K, c->prefix);
+  if (c->cfg.ckpt_dir && c->cfg.write_files) ::mkdir(c->cfg.ckpt_dir, 0755);
+  c->writer = std::thread(writer_loop, c);
+  *out = c;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_sync(lowdiff_ctx* c) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  {
+    std::unique_lock<std::mutex> lk(c->mu);
+    c->flush_req = true;
+    c->cv_work.notify_all();
+    c->cv_idle.wait(lk, [&] { return c->queued.empty() && !c->flush_req && !c->writer_busy; });
+  }
+  if (c->full_writer.joinable()) c->full_writer.join();
+  CK(cudaStreamSynchronize(c->side));
+  uint32_t err[2];
+  CK(cudaMemcpy(err, c->plan.err, 8, cudaMemcpyDeviceToHost));
+  lowdiff_status d = take_deferred(c);
+  if (d) return d;
+  if (err[0] != 0) {
+    // counter semantics: reset after reporting so the next sync reports only new events
+    CK(cudaMemset(c->plan.err, 0, 4));
+    return fail(c, LOWDIFF_E_NUMERIC, "non-finite accumulated gradient (first layer " + std::to_string(err[1]) + ")");
+  }
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
+  if (!c) return LOWDIFF_OK;
+  lowdiff_status st = LOWDIFF_OK;
+  if (c->writer.joinable()) {
+    if (c->poisoned == LOWDIFF_OK) st = lowdiff_sync(c);
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      c->stop = true;
+      c->cv_work.notify_all();
+    }
+    c->writer.join();
+  }
+  if (c->full_writer.joinable()) c->full_writer.join();
+  cudaSetDevice(c->device);
+  if (c->side) cudaStreamSynchronize(c->side);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (auto& s : c->slots) if (s.done) cudaEventDestroy(s.done);
+  for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  if (c->ring) cudaFreeHost(c->ring);
+  if (c->err_pinned) cudaFreeHost(c->err_pinned);
+  if (c->full_host) cudaFreeHost(c->full_host);
+  for (auto* p : c->snap_host) if (p) cudaFreeHost(p);
+  for (auto* p : c->dev_allocs) cudaFree(p);
+  if (c->replay_scratch) cudaFree(c->replay_scratch);
+  if (c->merge_scratch) cudaFree(c->merge_scratch);
+  for (auto e : {c->ev_tmp, c->last_d2h, c->full_done, c->snap_done[0], c->snap_done[1]}) if (e) cudaEventDestroy(e);
+  if (c->side) cudaStreamDestroy(c->side);
+  delete c;
+  return st;
+}
+
+lowdiff_status lowdiff_query(const lowdiff_ctx* c, int64_t* psi, int64_t* k_tot) {
+  if (!c) return LOWDIFF_E_INVALID;
+  if (psi) *psi = c->psi;
+  if (k_tot) *k_tot = c->K;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_layer_k(const lowdiff_ctx* c, int32_t layer, int64_t* k, int64_t* koff) {
+  if (!c || layer < 0 || layer >= c->cfg.n_layers) return LOWDIFF_E_INVALID;
+  if (k) *k = c->k[layer];
+  if (koff) *koff = (int64_t)c->koff[layer];
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send, void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!grad || !send || (c->cfg.error_feedback && !residual)) return fail(c, LOWDIFF_E_INVALID, "compress: NULL buffer");
+  if (!aligned16(grad) || !aligned16(send) || (residual && !aligned16(residual)))
+    return fail(c, LOWDIFF_E_INVALID, "compress: buffers must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->last_d2h_src == send) CK(cudaStreamWaitEvent(s, c->last_d2h, 0));   // WAR on the send block
+  CK(ld::launch_compress(c, grad, c->cfg.error_feedback ? residual : nullptr, send, s));
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_merge(lowdiff_ctx* c, int32_t world, const uint32_t* gathered, float* dense_out, void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (world < 1 || !gathered || !dense_out) return fail(c, LOWDIFF_E_INVALID, "merge: bad argument");
+  if (!aligned16(gathered) || !aligned16(dense_out)) return fail(c, LOWDIFF_E_INVALID, "merge: buffers must be 16-byte aligned");
+  CK(ld::launch_merge(c, world, gathered, dense_out, static_cast<cudaStream_t>(stream)));
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_exchange(lowdiff_ctx* c, const uint32_t* send, uint32_t* gathered, float* dense_out,
+                                void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!send || !dense_out || (c->cfg.world > 1 && !gathered)) return fail(c, LOWDIFF_E_INVALID, "exchange: NULL buffer");
+  const size_t blk = 2 * (size_t)c->K;
+  if (c->cfg.world > 1) {
+    if (!c->comm) return fail(c, LOWDIFF_E_STATE, "exchange: context was created without an NCCL id");
+    int h;
+    ld::prof_begin(c, "allgather", s, &h);
+    ncclResult_t r = ncclAllGather(send, gathered, blk, ncclUint32, c->comm, s);
+    ld::prof_end(c, h, s);
+    if (r != ncclSuccess) return fail(c, LOWDIFF_E_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    return lowdiff_merge(c, c->cfg.world, gathered, dense_out, stream);
+  }
+  if (gathered && gathered != send) CK(cudaMemcpyAsync(gathered, send, blk * 4, cudaMemcpyDeviceToDevice, s));
+  return lowdiff_merge(c, 1, send, dense_out, stream);
+}
+
+lowdiff_status lowdiff_batch_persist(lowdiff_ctx* c, int64_t iteration, const lowdiff_step_scalars* scalars,
+                                     const uint32_t* send, void* producer) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if ((st = take_deferred(c))) return st;
+  if (!scalars || !send) return fail(c, LOWDIFF_E_INVALID, "batch_persist: NULL argument");
+  if (c->next_iter >= 0 && iteration != c->next_iter)
+    return fail(c, LOWDIFF_E_STATE, "batch_persist: iteration " + std::to_string(iteration) + " after " +
+                                        std::to_string(c->next_iter - 1) + " (must be consecutive)");
+  int slot;
+  {
+    std::unique_lock<std::mutex> lk(c->mu);
+    if (c->free_slots.empty()) {
+      const int64_t t0 = now_ns();
+      c->cv_free.wait(lk, [&] { return !c->free_slots.empty(); });
+      c->stall_ns += now_ns() - t0;
+    }
+    slot = c->free_slots.front();
+    c->free_slots.pop_front();
+  }
+  c->next_iter = iteration + 1;
+  ld::Slot& S = c->slots[slot];
+  S.iteration = iteration;
+  uint8_t* h = S.host;                          // 32-byte block header
+  std::memset(h, 0, 32);
+  const uint64_t it = (uint64_t)iteration;
+  std::memcpy(h, &it, 8);
+  std::memcpy(h + 8, &scalars->lr, 4);
+  std::memcpy(h + 12, &scalars->bc1_inv, 4);
+  std::memcpy(h + 16, &scalars->bc2_inv, 4);
+  cudaStream_t p = static_cast<cudaStream_t>(producer);
+  int hnd;
+  CK(cudaEventRecord(c->ev_tmp, p));
+  CK(cudaStreamWaitEvent(c->side, c->ev_tmp, 0));
+  ld::prof_begin(c, "d2h", c->side, &hnd);
+  CK(cudaMemcpyAsync(h + 32, send, 8 * (size_t)c->K, cudaMemcpyDeviceToHost, c->side));
+  ld::prof_end(c, hnd, c->side);
+  CK(cudaMemcpyAsync(S.err_host, c->plan.err, 8, cudaMemcpyDeviceToHost, c->side));
+  CK(cudaEventRecord(S.done, c->side));
+  CK(cudaEventRecord(c->last_d2h, c->side));
+  c->last_d2h_src = send;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    c->queued.push_back(slot);
+    c->cv_work.notify_all();
+  }
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_full_ckpt(lowdiff_ctx* c, int64_t iteration, const float* p, const float* m, const float* v,
+                                 void* producer) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if ((st = take_deferred(c))) return st;
+  if (!p || iteration < 0) return fail(c, LOWDIFF_E_INVALID, "full_ckpt: bad argument");
+  if (c->full_writer.joinable()) c->full_writer.join();   // one full checkpoint in flight
+  const uint64_t sb = (uint64_t)c->psi * c->cfg.rank / c->cfg.world;
+  const uint64_t se = (uint64_t)c->psi * (c->cfg.rank + 1) / c->cfg.world;
+  const size_t S = se - sb;
+  if (c->full_cap < 3 * S) {
+    if (c->full_host) cudaFreeHost(c->full_host);
+    c->full_host = nullptr;
+    c->full_cap = 0;
+    CK(cudaHostAlloc((void**)&c->full_host, std::max<size_t>(1, 3 * S) * 4, cudaHostAllocDefault));
+    c->full_cap = 3 * S;
+  }
+  cudaStream_t pr = static_cast<cudaStream_t>(producer);
+  CK(cudaEventRecord(c->ev_tmp, pr));
+  CK(cudaStreamWaitEvent(c->side, c->ev_tmp, 0));
+  const float* src[3] = {p, m, v};
+  for (int a = 0; a < 3; ++a) {
+    if (src[a]) CK(cudaMemcpyAsync(c->full_host + a * S, src[a] + sb, S * 4, cudaMemcpyDeviceToHost, c->side));
+    else std::memset(c->full_host + a * S, 0, S * 4);
+  }
+  CK(cudaEventRecord(c->full_done, c->side));
+  CK(cudaStreamWaitEvent(pr, c->full_done, 0));   // the next update waits for the snapshot (WAR)
+  if (!c->cfg.ckpt_dir || !c->cfg.write_files) return LOWDIFF_OK;
+  c->full_writer = std::thread([c, iteration, sb, se, S]() {
+    cudaSetDevice(c->device);
+    cudaError_t e = cudaEventSynchronize(c->full_done);
+    if (e != cudaSuccess) { set_deferred(c, LOWDIFF_E_CUDA, cudaGetErrorString(e)); return; }
+    const int64_t t0 = now_ns();
+    std::vector<uint8_t> hdr(96, 0);
+    std::memcpy(hdr.data(), "LDF1", 4);
+    const uint16_t ver = 1, flags = (uint16_t)((c->cfg.error_feedback ? 1 : 0) | (c->cfg.mean ? 2 : 0));
+    std::memcpy(hdr.data() + 4, &ver, 2);
+    std::memcpy(hdr.data() + 6, &flags, 2);
+    const uint32_t rk = (uint32_t)c->cfg.rank, wd = (uint32_t)c->cfg.world, opt = (uint32_t)c->cfg.optim;
+    const uint64_t itu = (uint64_t)iteration, psi = (uint64_t)c->psi;
+    std::memcpy(hdr.data() + 8, &rk, 4);
+    std::memcpy(hdr.data() + 12, &wd, 4);
+    std::memcpy(hdr.data() + 16, &itu, 8);
+    std::memcpy(hdr.data() + 24, &psi, 8);
+    std::memcpy(hdr.data() + 32, &sb, 8);
+    std::memcpy(hdr.data() + 40, &se, 8);
+    std::memcpy(hdr.data() + 48, &opt, 4);
+    std::memcpy(hdr.data() + 64, &c->cfg.adam, 20);
+    uint32_t crc = ld::crc32c_update(0xFFFFFFFFu, hdr.data(), hdr.size());
+    crc = ld::crc32c_update(crc, c->full_host, 3 * S * 4) ^ 0xFFFFFFFFu;
+    std::string err;
+    lowdiff_status s2 = ld::write_file_atomic(ld::full_name(c->ckpt_dir, c->cfg.rank, iteration),
+                                              {{hdr.data(), hdr.size()}, {c->full_host, 3 * S * 4}, {&crc, 4}},
+                                              c->cfg.fsync != 0, &err);
+    if (s2) set_deferred(c, s2, err);
+    else { c->files_written += 1; c->bytes_written += (int64_t)(100 + 12 * S); }
+    c->writer_ns += now_ns() - t0;
+  });
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_replay(lowdiff_ctx* c, int32_t optim, int32_t world, int64_t n_steps, const uint32_t* diffs,
+                              const lowdiff_step_scalars* scalars, float* p, float* m, float* v, void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (world < 1 || n_steps < 0 || (n_steps && (!diffs || !scalars)) || !p ||
+      (optim == LOWDIFF_ADAM && (!m || !v)) || (optim != LOWDIFF_ADAM && optim != LOWDIFF_SGD))
+    return fail(c, LOWDIFF_E_INVALID, "replay: bad argument");
+  if (!n_steps) return LOWDIFF_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // per-step scalars to the device (tail of the replay scratch is not reused: own buffer)
+  float* scal_dev = nullptr;
+  CK(cudaMallocAsync((void**)&scal_dev, (size_t)n_steps * 12, s));
+  CK(cudaMemcpyAsync(scal_dev, scalars, (size_t)n_steps * 12, cudaMemcpyHostToDevice, s));
+  const float consts[5] = {c->cfg.adam.beta1, c->cfg.adam.one_minus_beta1, c->cfg.adam.beta2,
+                           c->cfg.adam.one_minus_beta2, c->cfg.adam.eps};
+  cudaError_t e = ld::launch_replay(c, optim, c->cfg.mean != 0, consts, world, n_steps, diffs, scal_dev, p, m, v, s);
+  cudaFreeAsync(scal_dev, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "launch_replay");
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_chain_scan(const lowdiff_config* cfg, int64_t target, int64_t* full_iter, int64_t* last_iter) {
+  if (validate_cfg(cfg) || !cfg->ckpt_dir) return LOWDIFF_E_INVALID;
+  Chain ch;
+  std::string err;
+  lowdiff_status st = scan_chain(*cfg, target, &ch, &err);
+  if (st) return st;
+  if (full_iter) *full_iter = ch.F;
+  if (last_iter) *last_iter = ch.last;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_recover(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int64_t* recovered,
+                               void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!c->cfg.ckpt_dir) return fail(c, LOWDIFF_E_INVALID, "recover: no ckpt_dir");
+  if (!p) return fail(c, LOWDIFF_E_INVALID, "recover: NULL p");
+  if ((st = lowdiff_sync(c))) return st;     // our own pending files first
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Chain ch;
+  std::string err;
+  if ((st = scan_chain(c->cfg, target, &ch, &err))) return fail(c, st, err);
+  const uint32_t world = (uint32_t)c->cfg.world;
+  const uint64_t psi = (uint64_t)c->psi, K = (uint64_t)c->K;
+  // 1. full checkpoint shards -> p, m, v
+  uint32_t optim = 0;
+  float consts[5] = {0, 0, 0, 0, 0};
+  uint16_t flags = 0;
+  for (uint32_t r = 0; r < world; ++r) {
+    std::vector<uint8_t> buf;
+    if (!read_all(ch.full_paths[r], buf)) return fail(c, LOWDIFF_E_IO, "cannot read " + ch.full_paths[r]);
+    const uint64_t sb = psi * r / world, se = psi * (r + 1) / world, S = se - sb;
+    if (buf.size() != 100 + 12 * S || std::memcmp(buf.data(), "LDF1", 4) != 0 ||
+        lowdiff_crc32c(buf.data(), buf.size() - 4) != rd<uint32_t>(buf.data() + buf.size() - 4) ||
+        rd<uint32_t>(buf.data() + 8) != r || rd<uint32_t>(buf.data() + 12) != world ||
+        (int64_t)rd<uint64_t>(buf.data() + 16) != ch.F || rd<uint64_t>(buf.data() + 24) != psi ||
+        rd<uint64_t>(buf.data() + 32) != sb || rd<uint64_t>(buf.data() + 40) != se)
+      return fail(c, LOWDIFF_E_CORRUPT, "corrupt full checkpoint " + ch.full_paths[r]);
+    optim = rd<uint32_t>(buf.data() + 48);
+    flags = rd<uint16_t>(buf.data() + 6);
+    std::memcpy(consts, buf.data() + 64, 20);
+    const float* body = reinterpret_cast<const float*>(buf.data() + 96);
+    CK(cudaMemcpy(p + sb, body, S * 4, cudaMemcpyHostToDevice));
+    if (m) CK(cudaMemcpy(m + sb, body + S, S * 4, cudaMemcpyHostToDevice));
+    if (v) CK(cudaMemcpy(v + sb, body + 2 * S, S * 4, cudaMemcpyHostToDevice));
+  }
+  if (optim == LOWDIFF_ADAM && (!m || !v)) return fail(c, LOWDIFF_E_INVALID, "recover: Adam needs m and v");
+  const int64_t n = ch.last - ch.F;
+  // 2. stream the differentials through the fused replay in chunks of steps that fit HBM
+  const size_t step_bytes = (size_t)world * 8 * K;
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const size_t per_step = step_bytes + ld::replay_scratch_bytes(c->psi, (int)world, 1);
+  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)(free_b / 2 / std::max<size_t>(1, per_step))));
+  uint32_t* d_diffs = nullptr;
+  if (n > 0) CK(cudaMalloc(&d_diffs, (size_t)chunk * step_bytes));
+  std::map<std::string, std::vector<uint8_t>> cache;   // verified batch files in use
+  lowdiff_status result = LOWDIFF_OK;
+  std::vector<lowdiff_step_scalars> scal;
+  for (int64_t t0 = ch.F + 1; t0 <= ch.last && result == LOWDIFF_OK; t0 += chunk) {
+    const int64_t t1 = std::min<int64_t>(ch.last, t0 + chunk - 1);
+    scal.assign((size_t)(t1 - t0 + 1), {0, 0, 0});
+    for (int64_t t = t0; t <= t1 && result == LOWDIFF_OK; ++t) {
+      for (uint32_t r = 0; r < world; ++r) {
+        const auto& w = ch.where[r][t];
+        auto itc = cache.find(w.first);
+        if (itc == cache.end()) {
+          // drop files no longer needed by this rank (iterations are visited in order)
+          for (auto jt = cache.begin(); jt != cache.end();) {
+            bool used = false;
+            for (uint32_t q = 0; q < world && !used; ++q) {
+              auto f = ch.where[q].find(t);
+              used = f != ch.where[q].end() && f->second.first == jt->first;
+            }
+            jt = used ? std::next(jt) : cache.erase(jt);
+          }
+          std::vector<uint8_t> buf;
+          if (!read_all(w.first, buf)) { result = fail(c, LOWDIFF_E_IO, "cannot read " + w.first); break; }
+          const uint32_t nit = buf.size() >= 100 ? rd<uint32_t>(buf.data() + 24) : 0;
+          const size_t want = 100 + 16 * (size_t)c->cfg.n_layers + (size_t)nit * (32 + 8 * K);
+          if (buf.size() != want || std::memcmp(buf.data(), "LDB1", 4) != 0 ||
+              lowdiff_crc32c(buf.data(), buf.size() - 4) != rd<uint32_t>(buf.data() + buf.size() - 4) ||
+              rd<uint32_t>(buf.data() + 8) != r || rd<uint32_t>(buf.data() + 12) != world ||
+              rd<uint32_t>(buf.data() + 28) != (uint32_t)c->cfg.n_layers || rd<uint64_t>(buf.data() + 32) != psi ||
+              rd<uint64_t>(buf.data() + 40) != K || rd<uint32_t>(buf.data() + 48) != c->cfg.density_ppm ||
+              rd<uint32_t>(buf.data() + 52) != optim) {
+            result = fail(c, LOWDIFF_E_CORRUPT, "corrupt batch file " + w.first);
+            break;
+          }
+          itc = cache.emplace(w.first, std::move(buf)).first;
+        }
+        const uint8_t* blk = itc->second.data() + 96 + 16 * (size_t)c->cfg.n_layers + (size_t)w.second * (32 + 8 * K);
+        if ((int64_t)rd<uint64_t>(blk) != t) { result = fail(c, LOWDIFF_E_CORRUPT, "block iteration mismatch"); break; }
+        lowdiff_step_scalars sc;
+        std::memcpy(&sc, blk + 8, 12);
+        if (r == 0) scal[t - t0] = sc;
+        else if (std::memcmp(&sc, &scal[t - t0], 12) != 0) {
+          result = fail(c, LOWDIFF_E_CORRUPT, "ranks disagree on the scalars of iteration " + std::to_string(t));
+          break;
+        }
+        cudaError_t e = cudaMemcpy(d_diffs + ((size_t)(t - t0) * world + r) * 2 * K, blk + 32, 8 * K,
+                                   cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { result = cuda_fail(c, e, "H2D differential"); break; }
+      }
+    }
+    if (result) break;
+    // per-step scalars to the device, then one fused replay launch for the chunk of steps
+    float* scal_dev = nullptr;
+    cudaError_t e2 = cudaMalloc((void**)&scal_dev, scal.size() * 12);
+    if (e2 == cudaSuccess) e2 = cudaMemcpy(scal_dev, scal.data(), scal.size() * 12, cudaMemcpyHostToDevice);
+    if (e2 == cudaSuccess)
+      e2 = ld::launch_replay(c, (int)optim, (flags & 2) != 0, consts, (int)world, t1 - t0 + 1, d_diffs, scal_dev, p, m,
+                             v, s);
+    if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(s);
+    if (scal_dev) cudaFree(scal_dev);
+    if (e2 != cudaSuccess) result = cuda_fail(c, e2, "replay");
+  }
+  if (d_diffs) cudaFree(d_diffs);
+  if (result) return result;
+  CK(cudaStreamSynchronize(s));
+  if (recovered) *recovered = ch.last;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx* c, int64_t iteration, int32_t first_layer, int32_t n_layers,
+                                      const float* grad_bucket, void* producer) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!grad_bucket || first_layer < 0 || n_layers < 1 || first_layer + n_layers > c->cfg.n_layers || iteration < 0)
+    return fail(c, LOWDIFF_E_INVALID, "snapshot_layer: bad argument");
+  const int buf = (int)(iteration & 1);
+  if (!c->snap_host[buf]) {
+    CK(cudaHostAlloc((void**)&c->snap_host[buf], (size_t)c->psi * 4, cudaHostAllocDefault));
+  }
+  if (c->snap_iter[buf] != iteration) {
+    CK(cudaEventSynchronize(c->snap_done[buf]));   // iteration - 2 finished with this buffer
+    c->snap_iter[buf] = iteration;
+    c->snap_seen[buf].assign(c->cfg.n_layers, 0);
+  }
+  for (int l = first_layer; l < first_layer + n_layers; ++l) c->snap_seen[buf][l] = 1;
+  cudaStream_t p = static_cast<cudaStream_t>(producer);
+  CK(cudaEventRecord(c->ev_tmp, p));
+  CK(cudaStreamWaitEvent(c->side, c->ev_tmp, 0));
+  const uint64_t lo = c->off[first_layer], hi = c->off[first_layer + n_layers];
+  int h;
+  ld::prof_begin(c, "snapshot_d2h", c->side, &h);
+  CK(cudaMemcpyAsync(c->snap_host[buf] + lo, grad_bucket, (hi - lo) * 4, cudaMemcpyDeviceToHost, c->side));
+  ld::prof_end(c, h, c->side);
+  CK(cudaEventRecord(c->snap_done[buf], c->side));
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_snapshot_wait(lowdiff_ctx* c, int64_t iteration, const float** host_grad) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  const int buf = (int)(iteration & 1);
+  if (iteration < 0 || c->snap_iter[buf] != iteration) return fail(c, LOWDIFF_E_STATE, "snapshot_wait: unknown iteration");
+  for (uint8_t x : c->snap_seen[buf])
+    if (!x) return fail(c, LOWDIFF_E_STATE, "snapshot_wait: some layer of the iteration was not snapshotted");
+  CK(cudaEventSynchronize(c->snap_done[buf]));
+  if (host_grad) *host_grad = c->snap_host[buf];
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_get_stats(const lowdiff_ctx* c, lowdiff_stats* out) {
+  if (!c || !out) return LOWDIFF_E_INVALID;
+  out->files_written = c->files_written;
+  out->bytes_written = c->bytes_written;
+  out->ring_stall_ns = c->stall_ns;
+  out->writer_busy_ns = c->writer_ns;
+  uint32_t cnt[4] = {0, 0, 0, 0};
+  if (cudaMemcpy(cnt, c->plan.counters, 12, cudaMemcpyDeviceToHost) == cudaSuccess) {
+    out->spec_hits = cnt[1];
+    out->spec_misses = cnt[2];
+  } else {
+    out->spec_hits = out->spec_misses = -1;
+  }
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_prof_enable(lowdiff_ctx* c, int32_t enable) {
+  if (!c) return LOWDIFF_E_INVALID;
+  cudaDeviceSynchronize();
+  for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  c->prof_recs.clear();
+  c->prof = enable != 0;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_prof_read(lowdiff_ctx* c, const char* name, double* total_ms, int64_t* launches) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  double ms = 0;
+  int64_t n = 0;
+  for (auto& r : c->prof_recs) {
+    if (name && name[0] && std::strcmp(name, r.name) != 0) continue;
+    CK(cudaEventSynchronize(r.b));
+    float x = 0;
+    CK(cudaEventElapsedTime(&x, r.a, r.b));
+    ms += x;
+    ++n;
+  }
+  if (total_ms) *total_ms = ms;
+  if (launches) *launches = n;
+  return LOWDIFF_OK;
+}
+
+int64_t lowdiff_kernel_launches(const lowdiff_ctx* c) { return c ? c->launches.load() : 0; }
+
+const char* lowdiff_last_error(const lowdiff_ctx* c) { return c ? c->last_error.c_str() : "null context"; }
+
+// ---- host-only serialisers used by multi-rank host tests
+lowdiff_status lowdiff_write_batch_host(const lowdiff_config* cfg, int64_t first_iter, int32_t n_iters,
+                                        const lowdiff_step_scalars* scalars, const uint32_t* blocks) {
+  if (validate_cfg(cfg) || !cfg->ckpt_dir || n_iters < 1 || !scalars || !blocks) return LOWDIFF_E_INVALID;
+  std::vector<int64_t> numel(cfg->numel, cfg->numel + cfg->n_layers);
+  int64_t psi = 0, K = 0;
+  for (int l = 0; l < cfg->n_layers; ++l) { psi += numel[l]; K += (int64_t)k_rule((uint64_t)numel[l], cfg->density_ppm); }
+  std::vector<uint8_t> pre;
+  ld::build_prefix(*cfg, numel, psi, K, pre);
+  const uint64_t first = (uint64_t)first_iter;
+  const uint32_t n = (uint32_t)n_iters;
+  std::memcpy(pre.data() + 16, &first, 8);
+  std::memcpy(pre.data() + 24, &n, 4);
+  std::vector<uint8_t> body((size_t)n * (32 + 8 * K), 0);
+  for (uint32_t i = 0; i < n; ++i) {
+    uint8_t* b = body.data() + (size_t)i * (32 + 8 * K);
+    const uint64_t it = first + i;
+    std::memcpy(b, &it, 8);
+    std::memcpy(b + 8, &scalars[i], 12);
+    std::memcpy(b + 32, blocks + (size_t)i * 2 * K, 8 * K);
+  }
+  uint32_t crc = ld::crc32c_update(0xFFFFFFFFu, pre.data(), pre.size());
+  crc = ld::crc32c_update(crc, body.data(), body.size()) ^ 0xFFFFFFFFu;
+  ::mkdir(cfg->ckpt_dir, 0755);
+  std::string err;
+  return ld::write_file_atomic(ld::batch_name(cfg->ckpt_dir, cfg->rank, first_iter),
+                               {{pre.data(), pre.size()}, {body.data(), body.size()}, {&crc, 4}}, cfg->fsync != 0, &err);
+}
+
+lowdiff_status lowdiff_write_full_host(const lowdiff_config* cfg, int64_t iteration, const float* p, const float* m,
+                                       const float* v) {
+  if (validate_cfg(cfg) || !cfg->ckpt_dir || !p || iteration < 0) return LOWDIFF_E_INVALID;
+  uint64_t psi = 0;
+  for (int l = 0; l < cfg->n_layers; ++l) psi += (uint64_t)cfg->numel[l];
+  const uint64_t sb = psi * cfg->rank / cfg->world, se = psi * (cfg->rank + 1) / cfg->world, S = se - sb;
+  std::vector<uint8_t> buf(96 + 12 * S, 0);
+  std::memcpy(buf.data(), "LDF1", 4);
+  const uint16_t ver = 1, flags = (uint16_t)((cfg->error_feedback ? 1 : 0) | (cfg->mean ? 2 : 0));
+  const uint32_t rk = (uint32_t)cfg->rank, wd = (uint32_t)cfg->world, opt = (uint32_t)cfg->optim;
+  const uint64_t itu = (uint64_t)iteration;
+  std::memcpy(buf.data() + 4, &ver, 2);
+  std::memcpy(buf.data() + 6, &flags, 2);
+  std::memcpy(buf.data() + 8, &rk, 4);
+  std::memcpy(buf.data() + 12, &wd, 4);
+  std::memcpy(buf.data() + 16, &itu, 8);
+  std::memcpy(buf.data() + 24, &psi, 8);
+  std::memcpy(buf.data() + 32, &sb, 8);
+  std::memcpy(buf.data() + 40, &se, 8);
+  std::memcpy(buf.data() + 48, &opt, 4);
+  std::memcpy(buf.data() + 64, &cfg->adam, 20);
+  const float* src[3] = {p, m, v};
+  for (int a = 0; a < 3; ++a)
+    if (src[a]) std::memcpy(buf.data() + 96 + a * S * 4, src[a] + sb, S * 4);
+  uint32_t crc = lowdiff_crc32c(buf.data(), buf.size());
+  ::mkdir(cfg->ckpt_dir, 0755);
+  std::string err;
+  return ld::write_file_atomic(ld::full_name(cfg->ckpt_dir, cfg->rank, iteration),
+                               {{buf.data(), buf.size()}, {&crc, 4}}, cfg->fsync != 0, &err);
+}
+
+}  // extern "C"

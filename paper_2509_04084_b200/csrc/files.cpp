@@ -1,0 +1,159 @@
+// Checkpoint file formats, CRC-32C and atomic writes (host side of lowdiff_batch_persist /
+// lowdiff_full_ckpt / lowdiff_recover).
+//
+// .ldb (batched differential checkpoint C^B; "groups the buffered
+// differential checkpoints ... writes it to storage in a single I/O operation"):
+//   header 64 B | hyper 32 B | layer table 16 B x L | n_iters x (32 B block header + 8K) | CRC32C
+// .ldf (full checkpoint C^F, this rank's shard of p, m, v, 3*Psi PAPER.md:150):
+//   header 64 B | hyper 32 B | p, m, v f32[shard] | CRC32C
+// Written as <name>.tmp then rename() so a crash never exposes a partial file.
+// Exact byte layout: DESIGN.md "File formats".
+#include <fcntl.h>
+#include <nmmintrin.h>
+#include <sys/stat.h>
+#include <sys/uio.h>
+#include <unistd.h>
+
+#include <cerrno>
+#include <cstdio>
+#include <cstring>
+
+#include "internal.h"
+
+namespace ld {
+
+uint32_t crc32c_update(uint32_t crc, const void* data, size_t len) {
+  // hardware CRC32 (SSE4.2 crc32 instruction implements the Castagnoli polynomial)
+  const uint8_t* p = static_cast<const uint8_t*>(data);
+  uint64_t c = crc;
+  while (len && (reinterpret_cast<uintptr_t>(p) & 7)) { c = _mm_crc32_u8((uint32_t)c, *p++); --len; }
+  while (len >= 8) {
+    uint64_t w;
+    std::memcpy(&w, p, 8);
+    c = _mm_crc32_u64(c, w);
+    p += 8;
+    len -= 8;
+  }
+  while (len) { c = _mm_crc32_u8((uint32_t)c, *p++); --len; }
+  return (uint32_t)c;
+}
+
+static std::string pad(int64_t v, int w) {
+  char buf[32];
+  std::snprintf(buf, sizeof buf, "%0*lld", w, (long long)v);
+  return buf;
+}
+
+std::string batch_name(const std::string& dir, int rank, int64_t first) {
+  return dir + "/ld_diff_r" + pad(rank, 3) + "_" + pad(first, 12) + ".ldb";
+}
+
+std::string full_name(const std::string& dir, int rank, int64_t it) {
+  return dir + "/ld_full_r" + pad(rank, 3) + "_" + pad(it, 12) + ".ldf";
+}
+
+namespace {
+struct W {
+  std::vector<uint8_t>& b;
+  void u16(uint16_t v) { raw(&v, 2); }
+  void u32(uint32_t v) { raw(&v, 4); }
+  void u64(uint64_t v) { raw(&v, 8); }
+  void f32(float v) { raw(&v, 4); }
+  void raw(const void* p, size_t n) {   // x86-64 is little-endian: native order == file order
+    const uint8_t* q = static_cast<const uint8_t*>(p);
+    b.insert(b.end(), q, q + n);
+  }
+};
+}  // namespace
+
+// header + hyper + layer table; n_iters (offset 24) and first_iter (offset 16) patched per file
+void build_prefix(const lowdiff_config& cfg, const std::vector<int64_t>& numel, int64_t psi, int64_t K,
+                  std::vector<uint8_t>& out) {
+  out.clear();
+  W w{out};
+  w.raw("LDB1", 4);
+  w.u16(1);
+  w.u16((uint16_t)((cfg.error_feedback ? 1 : 0) | (cfg.mean ? 2 : 0)));
+  w.u32((uint32_t)cfg.rank);
+  w.u32((uint32_t)cfg.world);
+  w.u64(0);                        // first_iter (patched)
+  w.u32(0);                        // n_iters (patched)
+  w.u32((uint32_t)cfg.n_layers);
+  w.u64((uint64_t)psi);
+  w.u64((uint64_t)K);
+  w.u32(cfg.density_ppm);
+  w.u32((uint32_t)cfg.optim);
+  w.u64(0);
+  const float h[5] = {cfg.adam.beta1, cfg.adam.one_minus_beta1, cfg.adam.beta2, cfg.adam.one_minus_beta2,
+                      cfg.adam.eps};
+  for (float x : h) w.f32(x);
+  w.u32(0); w.u32(0); w.u32(0);
+  for (int l = 0; l < cfg.n_layers; ++l) {
+    uint64_t n = (uint64_t)numel[l];
+    uint64_t k = n * cfg.density_ppm / 1000000ull;
+    if (k > n) k = n;
+    if (k < 1) k = 1;
+    w.u64(n);
+    w.u32((uint32_t)k);
+    w.u32(0);
+  }
+}
+
+lowdiff_status write_file_atomic(const std::string& path, const std::vector<std::pair<const void*, size_t>>& parts,
+                                 bool do_fsync, std::string* err) {
+  const std::string tmp = path + ".tmp";
+  int fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
+  if (fd < 0) {
+    *err = "open " + tmp + ": " + std::strerror(errno);
+    return LOWDIFF_E_IO;
+  }
+  // one writev per <= 1024 segments / 1 GiB; restart on short writes
+  std::vector<iovec> iov;
+  for (auto& p : parts) {
+    const uint8_t* q = static_cast<const uint8_t*>(p.first);
+    size_t n = p.second;
+    while (n) {
+      size_t c = n > (1u << 30) ? (1u << 30) : n;
+      iov.push_back({const_cast<uint8_t*>(q), c});
+      q += c;
+      n -= c;
+    }
+  }
+  size_t i = 0;
+  while (i < iov.size()) {
+    int cnt = (int)std::min<size_t>(iov.size() - i, 1024);
+    ssize_t wr = ::writev(fd, &iov[i], cnt);
+    if (wr < 0) {
+      if (errno == EINTR) continue;
+      *err = "writev " + tmp + ": " + std::strerror(errno);
+      ::close(fd);
+      ::unlink(tmp.c_str());
+      return LOWDIFF_E_IO;
+    }
+    size_t left = (size_t)wr;
+    while (left && i < iov.size()) {
+      if (left >= iov[i].iov_len) { left -= iov[i].iov_len; ++i; }
+      else {
+        iov[i].iov_base = static_cast<uint8_t*>(iov[i].iov_base) + left;
+        iov[i].iov_len -= left;
+        left = 0;
+      }
+    }
+  }
+  if (do_fsync && ::fsync(fd) != 0) {
+    *err = "fsync " + tmp + ": " + std::strerror(errno);
+    ::close(fd);
+    return LOWDIFF_E_IO;
+  }
+  if (::close(fd) != 0) {
+    *err = "close " + tmp + ": " + std::strerror(errno);
+    return LOWDIFF_E_IO;
+  }
+  if (::rename(tmp.c_str(), path.c_str()) != 0) {
+    *err = "rename " + tmp + ": " + std::strerror(errno);
+    return LOWDIFF_E_IO;
+  }
+  return LOWDIFF_OK;
+}
+
+}  // namespace ld

@@ -1,0 +1,174 @@
+// Internal declarations of liblowdiff (B200 / sm_100a).  Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/lowdiff.h"
+
+namespace ld {
+
+// ---------------------------------------------------------------- compress plan
+// Layers with n <= kSmallMax are selected by one CTA entirely in shared memory.
+// Larger layers are cut into chunks of kChunk elements whose boundaries are
+// 4-element aligned in the flat buffer (so every 16-byte slot lies in one chunk).
+constexpr int kChunk = 16384;          // elements per chunk (64 KB of fp32)
+constexpr int kScanThreads = 512;      // threads per chunk CTA: 8 float4 slots each
+constexpr int kSmallMax = 16384;       // small-layer bound (64 KB smem for acc)
+constexpr int kSmallThreads = 512;
+constexpr int kMergeTile = 8192;       // merge tile (elements per CTA)
+constexpr int kReplayTile = 2048;      // replay tile (elements per CTA)
+constexpr int kReplayThreads = 256;
+constexpr uint32_t kNoThreshold = 0xFFFFFFFFu;
+
+// per-large-layer selection state (device)
+struct LayerSel {
+  uint32_t prefix;   // key bits fixed by the digits done so far
+  uint32_t kleft;    // entries still to take among those matching prefix
+  uint32_t total;    // candidate count
+  uint32_t refill;   // 1: speculative band too narrow, whole layer became candidates
+};
+
+struct DevPlan {
+  // layers
+  int32_t n_layers;
+  int32_t n_large, n_small;
+  const uint64_t* layer_off;     // [L+1]
+  const uint32_t* layer_k;       // [L]
+  const uint64_t* layer_koff;    // [L]
+  const int32_t* small_layers;   // [n_small] layer ids
+  const int32_t* large_layers;   // [n_large] layer ids
+  const int32_t* large_chunk0;   // [n_large+1] first chunk of each large layer
+  // chunks (large layers only)
+  int32_t n_chunks;
+  const int32_t* chunk_slot;     // [n_chunks] index into large_layers
+  const uint64_t* chunk_base;    // [n_chunks] first element (4-aligned) of the chunk's slot grid
+  const uint64_t* chunk_lo;      // [n_chunks] first element that belongs to the chunk
+  const uint64_t* chunk_hi;      // [n_chunks] one past the last element
+  // scratch
+  uint32_t* cand_idx;            // [n_chunks * kChunk] candidate global indices, index-ordered
+  uint32_t* cand_val;            // [n_chunks * kChunk] candidate acc bits
+  uint32_t* chunk_count;         // [n_chunks]
+  uint32_t* chunk_gt;            // [n_chunks]
+  uint32_t* chunk_eq;            // [n_chunks]
+  uint32_t* chunk_out;           // [n_chunks] output offset inside the layer
+  uint32_t* chunk_take;          // [n_chunks] ties taken from this chunk
+  uint32_t* hist;                // [n_large * (2048 + 2048 + 512)]
+  LayerSel* sel;                 // [n_large]
+  uint32_t* thr;                 // [n_large] speculative threshold key (persistent across calls)
+  uint32_t* refill_list;         // [n_chunks] chunk ids to rescan
+  uint32_t* counters;            // [0] refill chunk count, [1] spec hits, [2] spec misses
+  uint32_t* err;                 // [0] non-finite flag, [1] first bad layer
+};
+
+// ---------------------------------------------------------------- context
+struct ProfRec { const char* name; cudaEvent_t a, b; };
+
+struct Slot {
+  uint8_t* host;        // 32-byte block header + 8K payload
+  uint32_t* err_host;   // device error flags copied next to the payload
+  cudaEvent_t done;
+  int64_t iteration;
+};
+
+}  // namespace ld
+
+struct lowdiff_ctx {
+  // configuration
+  lowdiff_config cfg;
+  std::vector<int64_t> numel;
+  std::string ckpt_dir;
+  int64_t psi = 0, K = 0;
+  std::vector<uint64_t> off, koff;
+  std::vector<uint32_t> k;
+  int device = 0;
+  // device plan + buffers
+  ld::DevPlan plan{};
+  std::vector<void*> dev_allocs;
+  // streams / events
+  cudaStream_t side = nullptr;       // D2H copies
+  cudaEvent_t ev_tmp = nullptr;
+  cudaEvent_t last_d2h = nullptr;    // WAR guard for the send buffer
+  const void* last_d2h_src = nullptr;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  // status
+  lowdiff_status poisoned = LOWDIFF_OK;
+  lowdiff_status deferred = LOWDIFF_OK;
+  std::string last_error;
+  std::mutex err_mu;
+  // persistence ring + writer
+  int R = 0, b = 1;
+  size_t slot_bytes = 0;
+  uint8_t* ring = nullptr;            // pinned
+  uint32_t* err_pinned = nullptr;     // pinned [R*2]
+  std::vector<ld::Slot> slots;
+  std::deque<int> free_slots;
+  std::deque<int> queued;             // FIFO to the writer
+  std::mutex mu;
+  std::condition_variable cv_free, cv_work, cv_idle;
+  bool stop = false, flush_req = false;
+  int writer_busy = 0;
+  std::thread writer;
+  int64_t next_iter = -1;
+  std::vector<uint8_t> prefix;        // header + hyper + layer table (n_iters patched per file)
+  // stats
+  std::atomic<int64_t> files_written{0}, bytes_written{0}, stall_ns{0}, writer_ns{0};
+  int64_t spec_hits = 0, spec_misses = 0;
+  // full checkpoint staging
+  float* full_host = nullptr;         // pinned 3 * shard
+  size_t full_cap = 0;
+  cudaEvent_t full_done = nullptr;
+  bool full_pending = false;
+  int64_t full_iter = -1;
+  std::thread full_writer;
+  // LowDiff+ snapshot
+  float* snap_host[2] = {nullptr, nullptr};
+  int64_t snap_iter[2] = {-1, -1};
+  std::vector<uint8_t> snap_seen[2];
+  cudaEvent_t snap_done[2] = {nullptr, nullptr};
+  // profiling
+  bool prof = false;
+  std::vector<ld::ProfRec> prof_recs;
+  std::vector<cudaEvent_t> prof_pool;
+  std::atomic<int64_t> launches{0};
+  // replay scratch
+  void* replay_scratch = nullptr;
+  size_t replay_scratch_bytes = 0;
+  void* merge_scratch = nullptr;
+  size_t merge_scratch_bytes = 0;
+};
+
+namespace ld {
+// kernels.cu
+cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send,
+                            cudaStream_t s);
+cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, float* dense,
+                         cudaStream_t s);
+cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* consts5, int world,
+                          int64_t n_steps, const uint32_t* diffs, const float* scal_dev, float* p,
+                          float* m, float* v, cudaStream_t s);
+size_t merge_scratch_bytes(int64_t psi, int world, int64_t n_blocks);
+size_t replay_scratch_bytes(int64_t psi, int world, int64_t n_steps);
+
+// profiling helpers (api.cpp)
+void prof_begin(lowdiff_ctx* c, const char* name, cudaStream_t s, int* handle);
+void prof_end(lowdiff_ctx* c, int handle, cudaStream_t s);
+
+// files.cpp
+uint32_t crc32c_update(uint32_t crc, const void* data, size_t len);
+std::string batch_name(const std::string& dir, int rank, int64_t first);
+std::string full_name(const std::string& dir, int rank, int64_t it);
+void build_prefix(const lowdiff_config& cfg, const std::vector<int64_t>& numel, int64_t psi,
+                  int64_t K, std::vector<uint8_t>& out);
+lowdiff_status write_file_atomic(const std::string& path, const std::vector<std::pair<const void*, size_t>>& parts,
+                                 bool do_fsync, std::string* err);
+}  // namespace ld

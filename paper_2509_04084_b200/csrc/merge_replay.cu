@@ -1,0 +1,246 @@
+// Merge (decompress) and fused multi-step replay on sm_100a.
+//
+// merge  -- Alg. 1 line 7 "Comp^-1" after the allgather "Sync":
+//           G[j] = ((+0 + v_0[j]) + v_1[j] + ... + v_{N-1}[j]) / N, rank order, IEEE divide
+//           (R-8).  Tile-gather: every CTA owns a tile of the dense output, sums the
+//           entries that fall in it rank by rank in shared memory (indices are unique within a
+//           rank, so a rank's adds never collide) and writes the tile once with 128-bit stores.
+//           No atomics -> bit-deterministic for any N.  The per-(block, tile) entry ranges come
+//           from one linear pass over the (globally ascending) index lists.
+// replay -- Alg. 1 recovery loop, Eq. 1 update, dense Adam
+//           (R-10) or SGD (R-12), fused over steps: every CTA keeps its tile of (p, m, v) in
+//           registers, rebuilds G_t for the tile in shared memory exactly as the merge does,
+//           applies the update with block t's stored scalars, and writes the tile once at the
+//           end.  Per element this is the sequential recurrence, in order -- bit-identical to
+//           applying the steps one by one (the paper's log-n pairwise merge, is not
+//           exact for Adam; R-16).
+// All float operations are explicit round-to-nearest intrinsics (no FMA contraction, no
+// fast-math, denormals preserved; R-20/R-21).
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace ld {
+namespace {
+
+// start[b][t] = lower_bound(idx_b, t * tile) for t = 0..n_tiles (idx_b ascending, K entries)
+__global__ void tile_start_kernel(const uint32_t* __restrict__ blocks, int64_t n_blocks, uint64_t stride,
+                                  uint64_t K, uint32_t tile, int64_t n_tiles, uint32_t* __restrict__ start) {
+  const uint64_t per = K + 1;
+  const uint64_t total = (uint64_t)n_blocks * per;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = x / per, e = x % per;
+    const uint32_t* idx = blocks + b * stride;
+    const int64_t t_lo = e == 0 ? 0 : (int64_t)(idx[e - 1] / tile) + 1;
+    const int64_t t_hi = e == K ? n_tiles : (int64_t)(idx[e] / tile);
+    uint32_t* st = start + b * (uint64_t)(n_tiles + 1);
+    for (int64_t t = t_lo; t <= t_hi; ++t) st[t] = (uint32_t)e;
+  }
+}
+
+template <bool MEAN>
+__global__ void __launch_bounds__(256)
+merge_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const uint32_t* __restrict__ start,
+             int64_t n_tiles, uint64_t psi, float* __restrict__ dense) {
+  __shared__ float acc[kMergeTile];
+  const int64_t t = blockIdx.x;
+  const uint64_t j0 = (uint64_t)t * kMergeTile;
+  const int len = (int)min((uint64_t)kMergeTile, psi - j0);
+  float4* acc4 = reinterpret_cast<float4*>(acc);
+  for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) acc4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  for (int r = 0; r < world; ++r) {
+    const uint32_t* idx = gathered + (uint64_t)r * 2 * K;
+    const uint32_t* val = idx + K;
+    const uint32_t* st = start + (uint64_t)r * (n_tiles + 1) + t;
+    const uint32_t a = st[0], b = st[1];
+    for (uint32_t e = a + threadIdx.x; e < b; e += blockDim.x) {
+      const uint32_t j = idx[e] - (uint32_t)j0;
+      acc[j] = __fadd_rn(acc[j], __uint_as_float(val[e]));
+    }
+    __syncthreads();
+  }
+  const float n = (float)world;
+  if (len == kMergeTile) {
+    float4* out = reinterpret_cast<float4*>(dense + j0);
+    for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) {
+      float4 v = acc4[q];
+      if (MEAN) v = make_float4(__fdiv_rn(v.x, n), __fdiv_rn(v.y, n), __fdiv_rn(v.z, n), __fdiv_rn(v.w, n));
+      out[q] = v;
+    }
+  } else {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) dense[j0 + i] = MEAN ? __fdiv_rn(acc[i], n) : acc[i];
+  }
+}
+
+struct AdamK { float b1, c1, b2, c2, eps; };
+
+// Fused n-step replay.  Thread owns elements j0 + 4*(tid + 256*i) + q, i in {0,1}, q in 0..3.
+template <int OPT, bool MEAN>
+__global__ void __launch_bounds__(kReplayThreads)
+replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
+              const uint32_t* __restrict__ start, int64_t n_tiles, const float* __restrict__ scal,
+              AdamK ak, uint64_t psi, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v) {
+  __shared__ float G[kReplayTile];
+  const int64_t t = blockIdx.x;
+  const uint64_t j0 = (uint64_t)t * kReplayTile;
+  const int len = (int)min((uint64_t)kReplayTile, psi - j0);
+  const bool full = len == kReplayTile;
+  const int tid = threadIdx.x;
+  float P[8], M[8], V[8];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int o = 4 * (tid + kReplayThreads * i) + q;
+      const bool in = o < len;
+      P[4 * i + q] = in ? p[j0 + o] : 0.f;
+      M[4 * i + q] = (OPT == LOWDIFF_ADAM && in) ? m[j0 + o] : 0.f;
+      V[4 * i + q] = (OPT == LOWDIFF_ADAM && in) ? v[j0 + o] : 0.f;
+    }
+  }
+  (void)full;
+  const float n = (float)world;
+  const uint64_t tstride = (uint64_t)(n_tiles + 1);
+#pragma unroll 1
+  for (int64_t s = 0; s < n_steps; ++s) {
+    float4* G4 = reinterpret_cast<float4*>(G);
+    G4[tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+    G4[tid + kReplayThreads] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    const uint32_t* blk = diffs + (uint64_t)s * world * 2 * K;
+    const uint32_t* st = start + (uint64_t)s * world * tstride + t;
+    for (int r = 0; r < world; ++r) {
+      const uint32_t* idx = blk + (uint64_t)r * 2 * K;
+      const uint32_t* val = idx + K;
+      const uint32_t a = __ldg(st + r * tstride), b = __ldg(st + r * tstride + 1);
+      for (uint32_t e = a + tid; e < b; e += kReplayThreads) {
+        const uint32_t j = __ldg(idx + e) - (uint32_t)j0;
+        G[j] = __fadd_rn(G[j], __uint_as_float(__ldg(val + e)));
+      }
+      __syncthreads();
+    }
+    const float lr = __ldg(scal + 3 * s), r1 = __ldg(scal + 3 * s + 1), r2 = __ldg(scal + 3 * s + 2);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float4 gv = G4[tid + kReplayThreads * i];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float g = q == 0 ? gv.x : q == 1 ? gv.y : q == 2 ? gv.z : gv.w;
+        if (MEAN) g = __fdiv_rn(g, n);
+        const int x = 4 * i + q;
+        if (OPT == LOWDIFF_ADAM) {
+          // m = b1*m + c1*g ; v = b2*v + c2*(g*g) ; mh = m*r1 ; vh = v*r2
+          // d = sqrt(vh) + eps ; u = mh / d ; p = p - lr*u          (R-11)
+          M[x] = __fadd_rn(__fmul_rn(ak.b1, M[x]), __fmul_rn(ak.c1, g));
+          V[x] = __fadd_rn(__fmul_rn(ak.b2, V[x]), __fmul_rn(ak.c2, __fmul_rn(g, g)));
+          const float mh = __fmul_rn(M[x], r1);
+          const float vh = __fmul_rn(V[x], r2);
+          const float d = __fadd_rn(__fsqrt_rn(vh), ak.eps);
+          const float u = __fdiv_rn(mh, d);
+          P[x] = __fsub_rn(P[x], __fmul_rn(lr, u));
+        } else {
+          P[x] = __fsub_rn(P[x], __fmul_rn(lr, g));
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int o = 4 * (tid + kReplayThreads * i) + q;
+      if (o < len) {
+        p[j0 + o] = P[4 * i + q];
+        if (OPT == LOWDIFF_ADAM) { m[j0 + o] = M[4 * i + q]; v[j0 + o] = V[4 * i + q]; }
+      }
+    }
+  }
+}
+
+int num_sms2() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+}  // namespace
+
+size_t merge_scratch_bytes(int64_t psi, int world, int64_t n_blocks) {
+  (void)world;
+  const int64_t n_tiles = (psi + kMergeTile - 1) / kMergeTile;
+  return (size_t)n_blocks * (n_tiles + 1) * sizeof(uint32_t);
+}
+
+size_t replay_scratch_bytes(int64_t psi, int world, int64_t n_steps) {
+  const int64_t n_tiles = (psi + kReplayTile - 1) / kReplayTile;
+  return (size_t)n_steps * world * (n_tiles + 1) * sizeof(uint32_t) + (size_t)n_steps * 3 * sizeof(float) + 256;
+}
+
+cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, float* dense, cudaStream_t s) {
+  const int64_t psi = c->psi;
+  const uint64_t K = (uint64_t)c->K;
+  const int64_t n_tiles = (psi + kMergeTile - 1) / kMergeTile;
+  const size_t need = merge_scratch_bytes(psi, world, world);
+  if (c->merge_scratch_bytes < need) {
+    if (c->merge_scratch) cudaFree(c->merge_scratch);
+    c->merge_scratch = nullptr;
+    c->merge_scratch_bytes = 0;
+    cudaError_t e = cudaMalloc(&c->merge_scratch, need);
+    if (e != cudaSuccess) return e;
+    c->merge_scratch_bytes = need;
+  }
+  uint32_t* start = static_cast<uint32_t*>(c->merge_scratch);
+  const int sms = num_sms2();
+  int h;
+  prof_begin(c, "merge", s, &h);
+  tile_start_kernel<<<sms * 8, 256, 0, s>>>(gathered, world, 2 * K, K, kMergeTile, n_tiles, start);
+  if (c->cfg.mean)
+    merge_kernel<true><<<(unsigned)n_tiles, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense);
+  else
+    merge_kernel<false><<<(unsigned)n_tiles, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense);
+  prof_end(c, h, s);
+  c->launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* consts5, int world, int64_t n_steps,
+                          const uint32_t* diffs, const float* scal_dev, float* p, float* m, float* v,
+                          cudaStream_t s) {
+  const int64_t psi = c->psi;
+  const uint64_t K = (uint64_t)c->K;
+  const int64_t n_tiles = (psi + kReplayTile - 1) / kReplayTile;
+  const size_t tbytes = (size_t)n_steps * world * (n_tiles + 1) * sizeof(uint32_t);
+  if (c->replay_scratch_bytes < tbytes) {
+    if (c->replay_scratch) cudaFree(c->replay_scratch);
+    c->replay_scratch = nullptr;
+    c->replay_scratch_bytes = 0;
+    cudaError_t e = cudaMalloc(&c->replay_scratch, tbytes);
+    if (e != cudaSuccess) return e;
+    c->replay_scratch_bytes = tbytes;
+  }
+  uint32_t* start = static_cast<uint32_t*>(c->replay_scratch);
+  const int sms = num_sms2();
+  AdamK ak{consts5[0], consts5[1], consts5[2], consts5[3], consts5[4]};
+  int h;
+  prof_begin(c, "replay_index", s, &h);
+  tile_start_kernel<<<sms * 8, 256, 0, s>>>(diffs, n_steps * world, 2 * K, K, kReplayTile, n_tiles, start);
+  prof_end(c, h, s);
+  prof_begin(c, "replay", s, &h);
+  const unsigned grid = (unsigned)n_tiles;
+  if (optim == LOWDIFF_ADAM) {
+    if (mean) replay_kernel<LOWDIFF_ADAM, true><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, (uint64_t)psi, p, m, v);
+    else replay_kernel<LOWDIFF_ADAM, false><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, (uint64_t)psi, p, m, v);
+  } else {
+    if (mean) replay_kernel<LOWDIFF_SGD, true><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, (uint64_t)psi, p, m, v);
+    else replay_kernel<LOWDIFF_SGD, false><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, (uint64_t)psi, p, m, v);
+  }
+  prof_end(c, h, s);
+  c->launches += 2;
+  return cudaGetLastError();
+}
+
+}  // namespace ld

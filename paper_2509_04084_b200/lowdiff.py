@@ -1,0 +1,311 @@
+"""Thin Python binding of liblowdiff (include/lowdiff.h) -- argument marshalling only.
+
+Every step of the LowDiff hot path runs in the CUDA library; this module only turns
+torch tensors into device pointers, streams into cudaStream_t handles, and status codes into
+exceptions.  There is no fallback: if ``_lib/liblowdiff.so`` is missing the import fails.
+Function names follow the C ABI (``lowdiff_<name>`` -> ``Context.<name>``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "liblowdiff.so")
+
+OK, E_INVALID, E_DIM, E_NUMERIC, E_CUDA, E_NCCL, E_IO, E_CORRUPT, E_GAP, E_STATE = range(10)
+SGD, ADAM = 0, 1
+STATUS_NAMES = ["OK", "E_INVALID", "E_DIM", "E_NUMERIC", "E_CUDA", "E_NCCL", "E_IO", "E_CORRUPT",
+                "E_GAP", "E_STATE"]
+
+
+class LowDiffError(RuntimeError):
+    def __init__(self, fn: str, code: int, msg: str = ""):
+        name = STATUS_NAMES[code] if 0 <= code < len(STATUS_NAMES) else str(code)
+        super().__init__(f"lowdiff_{fn} -> {name}" + (f": {msg}" if msg else ""))
+        self.code = code
+
+
+class StepScalars(C.Structure):
+    _fields_ = [("lr", C.c_float), ("bc1_inv", C.c_float), ("bc2_inv", C.c_float)]
+
+
+class AdamConsts(C.Structure):
+    _fields_ = [("beta1", C.c_float), ("one_minus_beta1", C.c_float), ("beta2", C.c_float),
+                ("one_minus_beta2", C.c_float), ("eps", C.c_float)]
+
+
+class Config(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("numel", C.POINTER(C.c_int64)), ("density_ppm", C.c_uint32),
+                ("error_feedback", C.c_int32), ("mean", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
+                ("nccl_unique_id", C.c_void_p), ("device", C.c_int32), ("ckpt_dir", C.c_char_p),
+                ("batch_size", C.c_int32), ("ring_slots", C.c_int32), ("write_files", C.c_int32),
+                ("fsync", C.c_int32), ("optim", C.c_int32), ("adam", AdamConsts)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("files_written", C.c_int64), ("bytes_written", C.c_int64), ("ring_stall_ns", C.c_int64),
+                ("writer_busy_ns", C.c_int64), ("spec_hits", C.c_int64), ("spec_misses", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        P, S = C.c_void_p, C.c_int
+        sig = {
+            "create": ([C.POINTER(Config), C.POINTER(C.c_void_p)], S),
+            "destroy": ([P], S),
+            "query": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], S),
+            "layer_k": ([P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], S),
+            "compress": ([P, P, P, P, P], S),
+            "exchange": ([P, P, P, P, P], S),
+            "merge": ([P, C.c_int32, P, P, P], S),
+            "batch_persist": ([P, C.c_int64, C.POINTER(StepScalars), P, P], S),
+            "full_ckpt": ([P, C.c_int64, P, P, P, P], S),
+            "recover": ([P, C.c_int64, P, P, P, C.POINTER(C.c_int64), P], S),
+            "replay": ([P, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P], S),
+            "snapshot_layer": ([P, C.c_int64, C.c_int32, C.c_int32, P, P], S),
+            "snapshot_wait": ([P, C.c_int64, C.POINTER(C.c_void_p)], S),
+            "sync": ([P], S),
+            "get_stats": ([P, C.POINTER(Stats)], S),
+            "prof_enable": ([P, C.c_int32], S),
+            "prof_read": ([P, C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)], S),
+            "kernel_launches": ([P], C.c_int64),
+            "last_error": ([P], C.c_char_p),
+            "nccl_unique_id": ([P], S),
+            "derive_step_scalars": ([C.c_int64, C.c_double, C.c_double, C.c_double, C.POINTER(StepScalars)], S),
+            "derive_adam_consts": ([C.c_double, C.c_double, C.c_double, C.POINTER(AdamConsts)], S),
+            "crc32c": ([P, C.c_size_t], C.c_uint32),
+            "chain_scan": ([C.POINTER(Config), C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], S),
+            "write_batch_host": ([C.POINTER(Config), C.c_int64, C.c_int32, C.POINTER(StepScalars), P], S),
+            "write_full_host": ([C.POINTER(Config), C.c_int64, P, P, P], S),
+            "abi_version": ([], C.c_int32),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, "lowdiff_" + name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "exchange", "merge", "batch_persist",
+            "full_ckpt", "recover", "replay", "snapshot_layer", "snapshot_wait", "sync", "get_stats",
+            "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
+            "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host",
+            "write_full_host", "abi_version"]
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        assert t.is_contiguous(), "tensors must be contiguous"
+        return C.c_void_p(t.data_ptr())
+    return C.c_void_p(int(t))
+
+
+def _stream(s):
+    if s is None:
+        s = torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream if hasattr(s, "cuda_stream") else int(s))
+
+
+def derive_step_scalars(t: int, lr: float, beta1: float = 0.9, beta2: float = 0.999) -> StepScalars:
+    out = StepScalars()
+    _check("derive_step_scalars", lib().lowdiff_derive_step_scalars(t, lr, beta1, beta2, C.byref(out)))
+    return out
+
+
+def derive_adam_consts(beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8) -> AdamConsts:
+    out = AdamConsts()
+    _check("derive_adam_consts", lib().lowdiff_derive_adam_consts(beta1, beta2, eps, C.byref(out)))
+    return out
+
+
+def crc32c(data: bytes) -> int:
+    buf = C.create_string_buffer(data, len(data))
+    return int(lib().lowdiff_crc32c(buf, len(data)))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check("nccl_unique_id", lib().lowdiff_nccl_unique_id(buf))
+    return buf.raw
+
+
+def _check(fn, code, ctx=None):
+    if code != OK:
+        msg = ""
+        if ctx is not None:
+            m = lib().lowdiff_last_error(ctx)
+            msg = m.decode() if m else ""
+        raise LowDiffError(fn, code, msg)
+
+
+@dataclass
+class Options:
+    density_ppm: int = 10000
+    error_feedback: bool = True
+    mean: bool = True
+    rank: int = 0
+    world: int = 1
+    nccl_id: bytes | None = None
+    device: int = 0
+    ckpt_dir: str | None = None
+    batch_size: int = 1
+    ring_slots: int = 0
+    write_files: bool = True
+    fsync: bool = False
+    optim: int = ADAM
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+
+def make_config(sizes, o: Options):
+    numel = (C.c_int64 * len(sizes))(*[int(n) for n in sizes])
+    idbuf = C.create_string_buffer(o.nccl_id, 128) if o.nccl_id is not None else None
+    cfg = Config(len(sizes), numel, o.density_ppm, int(o.error_feedback), int(o.mean), o.rank, o.world,
+                 C.cast(idbuf, C.c_void_p) if idbuf is not None else None, o.device,
+                 o.ckpt_dir.encode() if o.ckpt_dir else None, o.batch_size, o.ring_slots, int(o.write_files),
+                 int(o.fsync), o.optim, derive_adam_consts(o.beta1, o.beta2, o.eps))
+    cfg._keep = (numel, idbuf)   # keep the buffers alive with the struct
+    return cfg
+
+
+class Context:
+    """One lowdiff_ctx (one per process and GPU)."""
+
+    def __init__(self, sizes, opts: Options | None = None, **kw):
+        o = opts or Options(**kw)
+        self.opts = o
+        self.sizes = [int(n) for n in sizes]
+        self._cfg = make_config(self.sizes, o)
+        h = C.c_void_p()
+        _check("create", lib().lowdiff_create(C.byref(self._cfg), C.byref(h)))
+        self._h = h
+        psi, K = C.c_int64(), C.c_int64()
+        _check("query", lib().lowdiff_query(h, C.byref(psi), C.byref(K)), h)
+        self.psi, self.K = psi.value, K.value
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            h, self._h = self._h, None
+            _check("destroy", lib().lowdiff_destroy(h))
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _c(self, fn, code):
+        _check(fn, code, self._h)
+
+    # -- the five calls
+    def compress(self, grad, residual, send, stream=None):
+        self._c("compress", lib().lowdiff_compress(self._h, _ptr(grad), _ptr(residual), _ptr(send), _stream(stream)))
+
+    def exchange(self, send, gathered, dense_out, stream=None):
+        self._c("exchange", lib().lowdiff_exchange(self._h, _ptr(send), _ptr(gathered), _ptr(dense_out),
+                                                   _stream(stream)))
+
+    def merge(self, world, gathered, dense_out, stream=None):
+        self._c("merge", lib().lowdiff_merge(self._h, world, _ptr(gathered), _ptr(dense_out), _stream(stream)))
+
+    def batch_persist(self, iteration, scalars: StepScalars, send, stream=None):
+        self._c("batch_persist", lib().lowdiff_batch_persist(self._h, iteration, C.byref(scalars), _ptr(send),
+                                                             _stream(stream)))
+
+    def full_ckpt(self, iteration, p, m=None, v=None, stream=None):
+        self._c("full_ckpt", lib().lowdiff_full_ckpt(self._h, iteration, _ptr(p), _ptr(m), _ptr(v), _stream(stream)))
+
+    def recover(self, p, m=None, v=None, target=-1, stream=None) -> int:
+        rec = C.c_int64(-1)
+        self._c("recover", lib().lowdiff_recover(self._h, target, _ptr(p), _ptr(m), _ptr(v), C.byref(rec),
+                                                 _stream(stream)))
+        return rec.value
+
+    def replay(self, optim, world, n_steps, diffs, scalars, p, m=None, v=None, stream=None):
+        arr = (StepScalars * max(1, n_steps))(*scalars)
+        self._c("replay", lib().lowdiff_replay(self._h, optim, world, n_steps, _ptr(diffs), arr, _ptr(p), _ptr(m),
+                                               _ptr(v), _stream(stream)))
+        self._keep_scalars = arr
+
+    def snapshot_layer(self, iteration, first_layer, n_layers, grad_bucket, stream=None):
+        self._c("snapshot_layer", lib().lowdiff_snapshot_layer(self._h, iteration, first_layer, n_layers,
+                                                               _ptr(grad_bucket), _stream(stream)))
+
+    def snapshot_wait(self, iteration):
+        """Returns a CPU float32 tensor viewing the pinned snapshot buffer (valid until iteration + 2)."""
+        p = C.c_void_p()
+        self._c("snapshot_wait", lib().lowdiff_snapshot_wait(self._h, iteration, C.byref(p)))
+        arr = (C.c_float * self.psi).from_address(p.value)
+        return torch.frombuffer(arr, dtype=torch.float32)
+
+    def sync(self):
+        self._c("sync", lib().lowdiff_sync(self._h))
+
+    # -- introspection
+    def layer_k(self, layer):
+        k, koff = C.c_int64(), C.c_int64()
+        self._c("layer_k", lib().lowdiff_layer_k(self._h, layer, C.byref(k), C.byref(koff)))
+        return k.value, koff.value
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._c("get_stats", lib().lowdiff_get_stats(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in Stats._fields_}
+
+    def prof_enable(self, on=True):
+        self._c("prof_enable", lib().lowdiff_prof_enable(self._h, int(on)))
+
+    def prof_read(self, name=""):
+        ms, n = C.c_double(), C.c_int64()
+        self._c("prof_read", lib().lowdiff_prof_read(self._h, name.encode(), C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def kernel_launches(self) -> int:
+        return int(lib().lowdiff_kernel_launches(self._h))
+
+
+def chain_scan(sizes, opts: Options, target=-1):
+    cfg = make_config(sizes, opts)
+    f, l = C.c_int64(), C.c_int64()
+    _check("chain_scan", lib().lowdiff_chain_scan(C.byref(cfg), target, C.byref(f), C.byref(l)))
+    return f.value, l.value
+
+
+def write_batch_host(sizes, opts: Options, first_iter, scalars, blocks):
+    """blocks: numpy/torch uint32 array [n_iters, 2K] on the host."""
+    import numpy as np
+    cfg = make_config(sizes, opts)
+    b = np.ascontiguousarray(np.asarray(blocks, dtype=np.uint32))
+    arr = (StepScalars * len(scalars))(*scalars)
+    _check("write_batch_host", lib().lowdiff_write_batch_host(C.byref(cfg), first_iter, len(scalars), arr,
+                                                              b.ctypes.data_as(C.c_void_p)))
+
+
+def write_full_host(sizes, opts: Options, iteration, p, m=None, v=None):
+    import numpy as np
+    cfg = make_config(sizes, opts)
+    arrs = [None if a is None else np.ascontiguousarray(np.asarray(a, dtype=np.float32)) for a in (p, m, v)]
+    ptrs = [None if a is None else a.ctypes.data_as(C.c_void_p) for a in arrs]
+    _check("write_full_host", lib().lowdiff_write_full_host(C.byref(cfg), iteration, *ptrs))

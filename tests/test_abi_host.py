@@ -1,0 +1,183 @@
+"""CPU-only checks of the product library (no GPU): it loads, exports every symbol that
+include/lowdiff.h declares, and its host-side logic (scalar derivation, CRC-32C, file
+serialisers, chain scan) agrees with the oracle and with the stated rules."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2509_04084_b200 as ld
+from paper_2509_04084_b200 import lowdiff as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "lowdiff.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lowdiff_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = B.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == {"lowdiff_" + n for n in B.EXPORTED}
+    assert L.lowdiff_abi_version() == 1
+
+
+def test_library_is_sm100a_and_links_nccl():
+    so = B.LIB_PATH
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    deps = subprocess.run(["ldd", so], capture_output=True, text=True).stdout
+    assert "libnccl.so.2" in deps
+
+
+def test_scalars_and_consts_match_oracle(ref):
+    for t in (1, 2, 7, 100, 5000):
+        for lr in (1e-3, 0.1, 3e-4):
+            s = ld.derive_step_scalars(t, lr)
+            o = ref.step_scalars(t, lr)
+            assert np.array_equal(np.array([s.lr, s.bc1_inv, s.bc2_inv], np.float32), o)
+    c = ld.derive_adam_consts()
+    assert np.array_equal(np.array([c.beta1, c.one_minus_beta1, c.beta2, c.one_minus_beta2, c.eps], np.float32),
+                          ref.adam_consts())
+
+
+def test_crc32c_matches_oracle(ref):
+    rng = np.random.default_rng(0)
+    for n in (0, 1, 7, 8, 9, 63, 1000, 4097):
+        data = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        assert ld.crc32c(data) == ref.crc32c(data)
+
+
+SIZES = [1000, 10, 3000, 7, 20000]
+
+
+def _opts(tmp, **kw):
+    o = ld.Options(density_ppm=20000, ckpt_dir=str(tmp), **kw)
+    return o
+
+
+def test_host_batch_writer_is_byte_identical_to_oracle(ref, tmp_path):
+    for world, rank in ((1, 0), (4, 3)):
+        o = _opts(tmp_path, world=world, rank=rank, nccl_id=b"\0" * 128 if world > 1 else None)
+        K = sum(ref.k_table(SIZES, o.density_ppm))
+        rng = np.random.default_rng(world)
+        blocks = rng.integers(0, 2**32, (3, 2 * K), dtype=np.uint64).astype(np.uint32)
+        scal = [ld.derive_step_scalars(t, 1e-3) for t in (11, 12, 13)]
+        ld.write_batch_host(SIZES, o, 11, scal, blocks)
+        got = open(os.path.join(tmp_path, ref.batch_name(rank, 11)), "rb").read()
+        want = ref.batch_serialize(rank, world, 11, SIZES, o.density_ppm, ref.ADAM, ref.FLAG_EF | ref.FLAG_MEAN,
+                                   ref.adam_consts(), np.stack([ref.step_scalars(t, 1e-3) for t in (11, 12, 13)]),
+                                   blocks)
+        assert got == want
+
+
+def test_host_full_writer_is_byte_identical_to_oracle(ref, tmp_path):
+    psi = sum(SIZES)
+    rng = np.random.default_rng(9)
+    p, m, v = (rng.standard_normal(psi).astype(np.float32) for _ in range(3))
+    for world in (1, 3):
+        for rank in range(world):
+            o = _opts(tmp_path, world=world, rank=rank, nccl_id=b"\0" * 128 if world > 1 else None)
+            ld.write_full_host(SIZES, o, 5, p, m, v)
+            got = open(os.path.join(tmp_path, ref.full_name(rank, 5)), "rb").read()
+            assert got == ref.full_serialize(rank, world, 5, ref.ADAM, 3, ref.adam_consts(), p, m, v)
+    o = _opts(tmp_path, optim=ld.SGD)
+    ld.write_full_host(SIZES, o, 6, p)
+    assert open(os.path.join(tmp_path, ref.full_name(0, 6)), "rb").read() == \
+        ref.full_serialize(0, 1, 6, ref.SGD, 3, ref.adam_consts(), p)
+
+
+def test_chain_scan_rules(ref, tmp_path):
+    o = _opts(tmp_path)
+    K = sum(ref.k_table(SIZES, o.density_ppm))
+    psi = sum(SIZES)
+    z = np.zeros(psi, np.float32)
+    blk = lambda n: np.zeros((n, 2 * K), np.uint32)
+    sc = lambda a, n: [ld.derive_step_scalars(t, 1e-3) for t in range(a, a + n)]
+    with pytest.raises(ld.LowDiffError) as e:
+        ld.chain_scan(SIZES, o)
+    assert e.value.code == B.E_GAP                      # no full checkpoint at all
+    ld.write_full_host(SIZES, o, 100, z, z, z)
+    assert ld.chain_scan(SIZES, o) == (100, 100)        # Full@100 only
+    ld.write_batch_host(SIZES, o, 101, sc(101, 20), blk(20))
+    ld.write_batch_host(SIZES, o, 121, sc(121, 17), blk(17))
+    assert ld.chain_scan(SIZES, o) == (100, 137)        # Full@100 + 101..137
+    assert ld.chain_scan(SIZES, o, 120) == (100, 120)
+    ld.write_batch_host(SIZES, o, 139, sc(139, 2), blk(2))
+    assert ld.chain_scan(SIZES, o) == (100, 137)        # 138 missing: the chain stops
+    with pytest.raises(ld.LowDiffError) as e:
+        ld.chain_scan(SIZES, o, 140)
+    assert e.value.code == B.E_GAP
+    ld.write_full_host(SIZES, o, 130, z, z, z)
+    assert ld.chain_scan(SIZES, o) == (130, 137)
+    assert ld.chain_scan(SIZES, o, 129) == (100, 129)
+
+
+def _gloo_worker(rank, world, port, tmp, q):
+    import torch.distributed as dist
+    import paper_2509_04084_b200 as ld2
+    import oracle as ref2
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        import torch
+        # rank 0 makes the NCCL unique id and broadcasts it (the bootstrap lowdiff_create expects)
+        idt = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            idt = torch.frombuffer(bytearray(ld2.nccl_unique_id()), dtype=torch.uint8).clone()
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.tolist())
+        o = ld2.Options(density_ppm=20000, ckpt_dir=tmp, world=world, rank=rank, nccl_id=nid)
+        K = sum(ref2.k_table(SIZES, o.density_ppm))
+        psi = sum(SIZES)
+        rng = np.random.default_rng(0)   # same on every rank: the replicated state
+        p = rng.standard_normal(psi).astype(np.float32)
+        ld2.write_full_host(SIZES, o, 0, p, p * 0, p * 0)
+        blocks = np.random.default_rng(100 + rank).integers(0, 2**32, (4, 2 * K), dtype=np.uint64).astype(np.uint32)
+        ld2.write_batch_host(SIZES, o, 1, [ld2.derive_step_scalars(t, 1e-3) for t in range(1, 5)], blocks)
+        dist.barrier()
+        full, last = ld2.chain_scan(SIZES, o)
+        dist.barrier()
+        if rank == 1:
+            os.remove(os.path.join(tmp, ref2.batch_name(0, 1)))
+        dist.barrier()
+        try:
+            ld2.chain_scan(SIZES, o, 2)
+            gap = None
+        except ld2.LowDiffError as e:
+            gap = e.code
+        q.put((rank, full, last, gap, len(set(nid)) > 1))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, "error", repr(e), None, None))
+
+
+def test_two_rank_gloo_sharded_files_and_chain(tmp_path):
+    """World-size-2 host path: NCCL-id bootstrap over torch.distributed (gloo), each rank writes its
+    own shard and its own differential blocks, the chain is complete only with every rank's files."""
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, str(tmp_path), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, full, last, gap, idok in res:
+        assert full == 0 and last == 4, res
+        assert gap == B.E_GAP and idok
+    files = sorted(os.listdir(tmp_path))
+    assert "ld_full_r000_000000000000.ldf" in files and "ld_full_r001_000000000000.ldf" in files
