@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""LowDiff hot-path benchmark (BASELINE.json metric: "compress+exchange+persist GB/s per iteration;
+recovery replay params/s").
+
+One step = one iteration of the per-iteration chain on every rank: lowdiff_compress (per-layer top-k
+with error feedback) -> lowdiff_exchange (NCCL allgather + merge into the dense gradient) ->
+lowdiff_batch_persist (D2H of the rank's own block into the pinned ring), on synthetic gradients
+shaped like GPT-2 XL (BJ:10; 1,557,611,200 params, 580 tensors) at 1% density.  The timed region
+ends when the last block has landed in host memory (lowdiff_wait_persist).  value = dense fp32
+gradient bytes consumed per second by all ranks (4 * Psi * N / t_step).  Recovery replay (M2) is
+timed in the same run and reported under "recovery".
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from inputs import gradient, table  # noqa: E402
+
+METRIC = "compress+exchange+persist GB/s per iteration"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "note": "fallback (B200_PROFILING.md)"}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        d["note"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    except OSError:
+        return dict(PEAKS_FALLBACK)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.t.join(timeout=2)
+        sm, smax, reasons, power = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+def init_dist(gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    if world != gpus:
+        print(f"warning: --gpus {gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    return rank, world, local
+
+
+def allmax(x, world):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# --------------------------------------------------------------------------- oracle (CPU) legs
+def oracle_sample(sizes_all, ppm, budget_s):
+    """Time the oracle (as it stands, 1 thread) on a bounded sample of the workload: consecutive
+    layers of the table starting after the embeddings, grown until ~budget_s of CPU work."""
+    import oracle as ref
+    ref.build()
+    # calibrate on ~2M parameters
+    start = 2
+    cal = []
+    n = 0
+    i = start
+    while n < 2_000_000 and i < len(sizes_all):
+        cal.append(sizes_all[i])
+        n += sizes_all[i]
+        i += 1
+    t_cal = _oracle_chain(ref, cal, ppm)[0]
+    per_param = t_cal / sum(cal)
+    target = max(sum(cal), int(budget_s / max(per_param, 1e-12)))
+    sample, n, i = [], 0, start
+    while i < len(sizes_all) and n + sizes_all[i] <= target:
+        sample.append(sizes_all[i])
+        n += sizes_all[i]
+        i += 1
+    if not sample:
+        sample = cal
+    t, K = _oracle_chain(ref, sample, ppm)
+    return t, sample, (start, start + len(sample))
+
+
+def _oracle_chain(ref, sizes, ppm):
+    psi = sum(sizes)
+    g = gradient(sizes, 0, 0, dist="D1", device="cpu").numpy()
+    r = np.zeros(psi, np.float32)
+    t0 = time.perf_counter()
+    send, r = ref.compress(sizes, ppm, g, r, ef=True)
+    K = send.size // 2
+    ref.exchange(send, 1, K, psi)
+    ref.batch_serialize(0, 1, 1, sizes, ppm, ref.ADAM, 3, ref.adam_consts(), ref.step_scalars(1, 1e-3)[None],
+                        send[None])
+    return time.perf_counter() - t0, K
+
+
+def run_reference(args):
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sizes = table(args.workload)
+    per_step_budget = max(0.5, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
+    import oracle as ref
+    ref.build()
+    _, sample, (a, b) = oracle_sample(sizes, args.ppm, per_step_budget)
+    psi_s = sum(sample)
+    for _ in range(args.warmup):
+        _oracle_chain(ref, sample, args.ppm)
+    times = [_oracle_chain(ref, sample, args.ppm)[0] for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    value = 4 * psi_s / t / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.workload}@{args.ppm}ppm", "parallelism": f"dp{args.gpus}"},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.workload} layers [{a},{b}) = {psi_s} params per step "
+                                       "(compress + exchange + batch serialize, 1 rank)"},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import paper_2509_04084_b200 as ld
+
+    rank, world, local = init_dist(args.gpus)
+    dev = torch.device("cuda", local)
+    peaks = load_peaks()
+    B_HBM = peaks["hbm_gbs"] * 1e9
+    sizes = table(args.workload)
+    psi = sum(sizes)
+    nid = None
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(ld.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        nid = bytes(t.cpu().tolist())
+    tmp = tempfile.mkdtemp(prefix="lowdiff_bench_")
+    ctx = ld.Context(sizes, density_ppm=args.ppm, rank=rank, world=world, nccl_id=nid, device=local,
+                     ckpt_dir=tmp, batch_size=4, ring_slots=8, write_files=False, optim=ld.ADAM)
+    K = ctx.K
+    grads = [gradient(sizes, rank, i, dist="D4", alpha=0.5, model=args.workload, device=dev) for i in range(2)]
+    r = torch.zeros(psi, device=dev)
+    dense = torch.empty(psi, device=dev)
+    send = torch.empty(2 * K, dtype=torch.int32, device=dev)
+    gathered = torch.empty(world * 2 * K, dtype=torch.int32, device=dev) if world > 1 else None
+    scal = [ld.derive_step_scalars(t, 1e-3) for t in range(1, args.warmup + args.steps + 2)]
+    it = [0]
+
+    def step():
+        t = it[0]
+        ctx.compress(grads[t % 2], r, send)
+        ctx.exchange(send, gathered, dense)
+        ctx.batch_persist(t + 1, scal[t], send)
+        it[0] += 1
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.sync()
+    ctx.prof_enable(True)
+    l0 = ctx.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = Clocks(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    ctx.wait_persist()
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier(world)
+    ms = allmax(e0.elapsed_time(e1), world)
+    launches = ctx.kernel_launches() - l0
+    kern = {}
+    for name in ("small_layer", "scan", "select", "emit", "merge", "allgather", "d2h"):
+        tot, n = ctx.prof_read(name)
+        if n:
+            kern[name] = {"ms_per_launch": tot / n, "launches": n, "share_of_step": tot / args.steps / (ms / args.steps)}
+    ctx.prof_enable(False)
+    ctx.sync()
+    st = ctx.stats()
+    ms_step = ms / args.steps
+    value = world * 4 * psi / (ms_step / 1e3) / 1e9
+
+    # roofline of the dominant kernel: the scan (EF add + residual write + candidate compaction)
+    psi_large = sum(n for n in sizes if n > 16384)
+    scan_bytes = 12 * psi_large
+    scan_ms = kern.get("scan", {}).get("ms_per_launch", float("nan"))
+    achieved = scan_bytes / (scan_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(f"scan@{args.workload}")
+    except (OSError, ValueError):
+        pass
+    roofline = {"kernel": "scan_kernel (lowdiff_compress pass A)", "bound": "hbm", "achieved": achieved,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "algorithmic_bytes_per_launch": scan_bytes, "peak_source": peaks["note"]}
+
+    # BJ:5 gate: T_floor / t_chain; PCIe D2H bandwidth measured here
+    host = torch.empty(2 * K, dtype=torch.int32, pin_memory=True)
+    torch.cuda.synchronize()
+    ta = time.perf_counter()
+    for _ in range(3):
+        host.copy_(send, non_blocking=True)
+    torch.cuda.synchronize()
+    b_pcie = 3 * 8 * K / (time.perf_counter() - ta)
+    t_c = (12 * psi + 8 * K) / B_HBM
+    t_ag = (world - 1) * 8 * K / 770e9
+    t_m = (4 * psi + 8 * world * K) / B_HBM
+    t_d2h = (8 * K + 32) / b_pcie
+    t_floor = t_c + max(t_ag + t_m, t_d2h)
+    gate = {"t_floor_ms": t_floor * 1e3, "t_chain_ms": ms_step, "frac": t_floor / (ms_step / 1e3),
+            "pcie_d2h_gbs_measured": b_pcie / 1e9, "nvlink_gbs": 770.0}
+
+    # e2e: the same chain through the C ABI with the gradient in pinned HOST memory
+    e2e = None
+    if not args.no_e2e:
+        hg = torch.empty(psi, dtype=torch.float32, pin_memory=True)
+        hg.copy_(grads[0].cpu())
+        hout = torch.empty(2 * K, dtype=torch.int32, pin_memory=True)
+        gdev = grads[1]
+        n_e2e = max(1, min(args.steps, 3))
+        for _ in range(1):
+            gdev.copy_(hg, non_blocking=True)
+            step()
+        torch.cuda.synchronize()
+        barrier(world)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(n_e2e):
+            gdev.copy_(hg, non_blocking=True)
+            t = it[0]
+            ctx.compress(gdev, r, send)
+            ctx.exchange(send, gathered, dense)
+            ctx.batch_persist(t + 1, scal[min(t, len(scal) - 1)], send)
+            it[0] += 1
+            hout.copy_(send, non_blocking=True)
+        ctx.wait_persist()
+        f1.record()
+        torch.cuda.synchronize()
+        ems = allmax(f0.elapsed_time(f1), world) / n_e2e
+        e2e = {"value": world * 4 * psi / (ems / 1e3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 4 * psi,
+               "d2h_bytes_per_step": 8 * K, "ms_per_step": ems, "steps": n_e2e}
+        del hg, hout
+    ctx.sync()
+
+    # recovery replay (M2): n steps of gathered blocks resident in HBM, fused Adam replay
+    recovery = None
+    if not args.no_recovery:
+        del dense
+        step_bytes = world * 8 * K
+        free, _ = torch.cuda.mem_get_info()
+        n_rep = int(max(1, min(args.replay_steps, (free - 3 * 4 * psi - 2 * 2**30) * 0.8 // (step_bytes * 1.1))))
+        diffs = torch.empty((n_rep, world * 2 * K), dtype=torch.int32, device=dev)
+        dn = torch.empty(psi, device=dev)
+        for t in range(n_rep):
+            if world > 1:
+                ctx.compress(grads[t % 2], r, send)
+                ctx.exchange(send, diffs[t], dn)
+            else:
+                ctx.compress(grads[t % 2], r, diffs[t])
+        del dn
+        torch.cuda.synchronize()
+        p = torch.randn(psi, device=dev) * 0.02
+        m = torch.zeros(psi, device=dev)
+        v = torch.zeros(psi, device=dev)
+        rscal = [ld.derive_step_scalars(t, 1e-3) for t in range(1, n_rep + 1)]
+        ctx.replay(ld.ADAM, world, min(2, n_rep), diffs, rscal[:2], p, m, v)   # warm-up
+        torch.cuda.synchronize()
+        ctx.prof_enable(True)
+        barrier(world)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        ctx.replay(ld.ADAM, world, n_rep, diffs, rscal, p, m, v)
+        g1.record()
+        torch.cuda.synchronize()
+        rms = allmax(g0.elapsed_time(g1), world)
+        rk_ms, _ = ctx.prof_read("replay")
+        ri_ms, _ = ctx.prof_read("replay_index")
+        ctx.prof_enable(False)
+        t_rep = rms / 1e3
+        unfused = n_rep * (24 * psi + 8 * world * K)
+        fused = 24 * psi + n_rep * 8 * world * K
+        alu_peak = 148 * 128 * (peaks.get("sm_max_mhz", 1965.0) * 1e6)   # fp32 lane-instr/s
+        recovery = {"metric": "recovery replay params/s", "value": world * n_rep * psi / t_rep,
+                    "unit": "param-steps/s", "optimizer": "adam", "steps": n_rep, "ranks_per_step": world,
+                    "ms": rms, "replay_kernel_ms": rk_ms, "index_kernel_ms": ri_ms,
+                    "effective_unfused_gbs": unfused / t_rep / 1e9,
+                    "frac_of_hbm_unfused_model": unfused / t_rep / B_HBM,
+                    "fused_algorithmic_gbs": fused / t_rep / 1e9,
+                    "alu_lane_instr_per_param_step_at_peak": alu_peak * t_rep / (n_rep * psi)}
+        del diffs, p, m, v
+
+    # writer throughput (files, CRC-32C, rename) on this box's storage, reported separately
+    writer = None
+    if not args.no_writer and rank == 0:
+        wdir = tempfile.mkdtemp(prefix="lowdiff_w_")
+        wctx = ld.Context(sizes, density_ppm=args.ppm, ckpt_dir=wdir, batch_size=2, ring_slots=4, write_files=True)
+        t0 = time.perf_counter()
+        for t in range(1, 5):
+            wctx.batch_persist(t, scal[t], send)
+        wctx.sync()
+        dt = time.perf_counter() - t0
+        ws = wctx.stats()
+        writer = {"files": ws["files_written"], "bytes": ws["bytes_written"], "seconds": dt,
+                  "gbs": ws["bytes_written"] / dt / 1e9, "dir": "tempfile.mkdtemp()"}
+        wctx.close()
+        subprocess.run(["rm", "-rf", wdir])
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        t_o, sample, (a, b) = oracle_sample(sizes, args.ppm, args.cpu_budget)
+        cpu = {"value": 4 * sum(sample) / t_o / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": f"{args.workload} layers [{a},{b}) = {sum(sample)} params, one iteration of compress "
+                         f"+ exchange + batch serialize on 1 thread ({t_o:.1f} s)"}
+
+    ctx.close()
+    subprocess.run(["rm", "-rf", tmp])
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.workload}@{args.ppm}ppm", "psi": psi, "layers": len(sizes),
+                       "k_total": K, "density_ppm": args.ppm, "batch_size": 4, "parallelism": f"dp{world}",
+                       "inputs": "D4 row-sparse Gaussian, alpha=0.5 rank correlation; 2 gradient buffers of "
+                                 f"{4 * psi / 1e9:.2f} GB alternate (> L2, no flush needed)",
+                       "persist": "D2H of the rank's block into the pinned ring inside the timed region; "
+                                  "file writing measured separately (writer)"},
+            "roofline": roofline, "gate_bj5": gate, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk, "recovery": recovery, "writer": writer,
+            "spec": {"hits": st["spec_hits"], "misses": st["spec_misses"]}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="gpt2_xl", choices=["gpt2_xl", "bert_large", "resnet50", "mlp"])
+    ap.add_argument("--ppm", type=int, default=10000)
+    ap.add_argument("--replay-steps", type=int, default=100)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-recovery", action="store_true")
+    ap.add_argument("--no-writer", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

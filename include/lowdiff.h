@@ -135,6 +135,10 @@ lowdiff_status lowdiff_batch_persist(lowdiff_ctx *ctx, int64_t iteration,
                                      const lowdiff_step_scalars *scalars, const uint32_t *send,
                                      void *producer);
 
+/* Make `stream` wait (device-side, no host block) until every D2H copy issued so far by
+ *    lowdiff_batch_persist / lowdiff_full_ckpt / lowdiff_snapshot_layer has landed in host memory. */
+lowdiff_status lowdiff_wait_persist(lowdiff_ctx *ctx, void *stream);
+
 /* 4. Full checkpoint (Alg. 1 line 15): this rank's shard
  *    [floor(rank*Psi/world), floor((rank+1)*Psi/world)) of p, m, v (m, v may be NULL ->
  *    zeros), copied D2H on a side stream after an event on `producer`; `producer` then

@@ -448,6 +448,7 @@ lowdiff_status lowdiff_create(const lowdiff_config* cfg, lowdiff_ctx** out) {
   if ((st = build_plan(c))) return bail(st);
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_tmp, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_side_all, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->last_d2h, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->full_done, cudaEventDisableTiming) != cudaSuccess)
     return bail(LOWDIFF_E_CUDA);
@@ -526,7 +527,7 @@ lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
   for (auto* p : c->dev_allocs) cudaFree(p);
   if (c->replay_scratch) cudaFree(c->replay_scratch);
   if (c->merge_scratch) cudaFree(c->merge_scratch);
-  for (auto e : {c->ev_tmp, c->last_d2h, c->full_done, c->snap_done[0], c->snap_done[1]}) if (e) cudaEventDestroy(e);
+  for (auto e : {c->ev_tmp, c->ev_side_all, c->last_d2h, c->full_done, c->snap_done[0], c->snap_done[1]}) if (e) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
   delete c;
   return st;
@@ -633,6 +634,14 @@ lowdiff_status lowdiff_batch_persist(lowdiff_ctx* c, int64_t iteration, const lo
     c->queued.push_back(slot);
     c->cv_work.notify_all();
   }
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_wait_persist(lowdiff_ctx* c, void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  CK(cudaEventRecord(c->ev_side_all, c->side));
+  CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), c->ev_side_all, 0));
   return LOWDIFF_OK;
 }
 

@@ -96,6 +96,7 @@ struct lowdiff_ctx {
   // streams / events
   cudaStream_t side = nullptr;       // D2H copies
   cudaEvent_t ev_tmp = nullptr;
+  cudaEvent_t ev_side_all = nullptr; // lowdiff_wait_persist
   cudaEvent_t last_d2h = nullptr;    // WAR guard for the send buffer
   const void* last_d2h_src = nullptr;
   // NCCL

@@ -71,6 +71,7 @@ def lib():
             "merge": ([P, C.c_int32, P, P, P], S),
             "batch_persist": ([P, C.c_int64, C.POINTER(StepScalars), P, P], S),
             "full_ckpt": ([P, C.c_int64, P, P, P, P], S),
+            "wait_persist": ([P, P], S),
             "recover": ([P, C.c_int64, P, P, P, C.POINTER(C.c_int64), P], S),
             "replay": ([P, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P], S),
             "snapshot_layer": ([P, C.c_int64, C.c_int32, C.c_int32, P, P], S),
@@ -99,7 +100,7 @@ def lib():
 
 
 EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "exchange", "merge", "batch_persist",
-            "full_ckpt", "recover", "replay", "snapshot_layer", "snapshot_wait", "sync", "get_stats",
+            "full_ckpt", "wait_persist", "recover", "replay", "snapshot_layer", "snapshot_wait", "sync", "get_stats",
             "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
             "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host",
             "write_full_host", "abi_version"]
@@ -233,6 +234,9 @@ class Context:
     def batch_persist(self, iteration, scalars: StepScalars, send, stream=None):
         self._c("batch_persist", lib().lowdiff_batch_persist(self._h, iteration, C.byref(scalars), _ptr(send),
                                                              _stream(stream)))
+
+    def wait_persist(self, stream=None):
+        self._c("wait_persist", lib().lowdiff_wait_persist(self._h, _stream(stream)))
 
     def full_ckpt(self, iteration, p, m=None, v=None, stream=None):
         self._c("full_ckpt", lib().lowdiff_full_ckpt(self._h, iteration, _ptr(p), _ptr(m), _ptr(v), _stream(stream)))
