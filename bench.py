@@ -226,8 +226,9 @@ def run_ours(args):
     def step():
         t = it[0]
         ctx.compress(grads[t % 2], r, send)
-        ctx.exchange(send, gathered, dense)
+        # the rank's own block is final after compress: its D2H (side stream) overlaps the exchange
         ctx.batch_persist(t + 1, scal[t], send)
+        ctx.exchange(send, gathered, dense)
         it[0] += 1
 
     for _ in range(args.warmup):
@@ -312,8 +313,8 @@ def run_ours(args):
             gdev.copy_(hg, non_blocking=True)
             t = it[0]
             ctx.compress(gdev, r, send)
-            ctx.exchange(send, gathered, dense)
             ctx.batch_persist(t + 1, scal[min(t, len(scal) - 1)], send)
+            ctx.exchange(send, gathered, dense)
             it[0] += 1
             hout.copy_(send, non_blocking=True)
         ctx.wait_persist()

@@ -559,7 +559,7 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   if (e != cudaSuccess) return e;
   const int sms = num_sms();
   const int warp_blocks = (P.n_large * 32 + 255) / 256;
-  const int pgrid = sms * 4;
+  const int pgrid = (P.n_chunks + 7) / 8;   // one warp per chunk: latency hidden by parallelism
 
   prof_begin(c, "scan", s, &h);
   if (ef) scan_kernel<true><<<P.n_chunks, kScanThreads, 0, s>>>(P, grad, residual);

@@ -39,7 +39,22 @@ __global__ void tile_start_kernel(const uint32_t* __restrict__ blocks, int64_t n
   }
 }
 
-template <bool MEAN>
+// G = S / N.  DIV = 0: no division (sum mode, or N = 1 where x / 1 == x bit for bit);
+// DIV = 1: N is a power of two, so x / N == x * 2^-log2(N) exactly (both are the correctly rounded
+// value of the same real number, subnormals included); DIV = 2: IEEE division.
+template <int DIV>
+__device__ __forceinline__ float mean_of(float s, float n, float inv) {
+  if (DIV == 0) return s;
+  if (DIV == 1) return __fmul_rn(s, inv);
+  return __fdiv_rn(s, n);
+}
+
+int div_mode(bool mean, int world) {
+  if (!mean || world == 1) return 0;
+  return (world & (world - 1)) == 0 ? 1 : 2;
+}
+
+template <int DIV>
 __global__ void __launch_bounds__(256)
 merge_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const uint32_t* __restrict__ start,
              int64_t n_tiles, uint64_t psi, float* __restrict__ dense) {
@@ -61,23 +76,26 @@ merge_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const
     }
     __syncthreads();
   }
-  const float n = (float)world;
+  const float n = (float)world, inv = 1.0f / (float)world;
   if (len == kMergeTile) {
     float4* out = reinterpret_cast<float4*>(dense + j0);
     for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) {
       float4 v = acc4[q];
-      if (MEAN) v = make_float4(__fdiv_rn(v.x, n), __fdiv_rn(v.y, n), __fdiv_rn(v.z, n), __fdiv_rn(v.w, n));
+      v = make_float4(mean_of<DIV>(v.x, n, inv), mean_of<DIV>(v.y, n, inv), mean_of<DIV>(v.z, n, inv),
+                      mean_of<DIV>(v.w, n, inv));
       out[q] = v;
     }
   } else {
-    for (int i = threadIdx.x; i < len; i += blockDim.x) dense[j0 + i] = MEAN ? __fdiv_rn(acc[i], n) : acc[i];
+    for (int i = threadIdx.x; i < len; i += blockDim.x) dense[j0 + i] = mean_of<DIV>(acc[i], n, inv);
   }
 }
 
 struct AdamK { float b1, c1, b2, c2, eps; };
 
 // Fused n-step replay.  Thread owns elements j0 + 4*(tid + 256*i) + q, i in {0,1}, q in 0..3.
-template <int OPT, bool MEAN>
+constexpr int kReplayMaxWorld = 8;
+
+template <int OPT, int DIV>
 __global__ void __launch_bounds__(kReplayThreads)
 replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
               const uint32_t* __restrict__ start, int64_t n_tiles, const float* __restrict__ scal,
@@ -101,34 +119,73 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
     }
   }
   (void)full;
-  const float n = (float)world;
+  const float n = (float)world, inv = 1.0f / (float)world;
   const uint64_t tstride = (uint64_t)(n_tiles + 1);
+  // entry ranges of step s for every rank, double-buffered in shared memory: the loads for step
+  // s+1 are issued by threads tid < world at the start of step s and land during its compute
+  __shared__ uint32_t s_a[2][kReplayMaxWorld], s_b[2][kReplayMaxWorld];
+  if (tid < world && tid < kReplayMaxWorld) {
+    s_a[0][tid] = __ldg(start + (uint64_t)tid * tstride + t);
+    s_b[0][tid] = __ldg(start + (uint64_t)tid * tstride + t + 1);
+  }
+  float4* G4 = reinterpret_cast<float4*>(G);
 #pragma unroll 1
   for (int64_t s = 0; s < n_steps; ++s) {
-    float4* G4 = reinterpret_cast<float4*>(G);
+    const int cur = (int)(s & 1);
+    uint32_t na = 0, nb = 0;
+    if (tid < world && tid < kReplayMaxWorld && s + 1 < n_steps) {
+      const uint32_t* st1 = start + ((uint64_t)(s + 1) * world + tid) * tstride + t;
+      na = __ldg(st1);
+      nb = __ldg(st1 + 1);
+    }
+    const float lr = __ldg(scal + 3 * s), r1 = __ldg(scal + 3 * s + 1), r2 = __ldg(scal + 3 * s + 2);
     G4[tid] = make_float4(0.f, 0.f, 0.f, 0.f);
     G4[tid + kReplayThreads] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     const uint32_t* blk = diffs + (uint64_t)s * world * 2 * K;
-    const uint32_t* st = start + (uint64_t)s * world * tstride + t;
-    for (int r = 0; r < world; ++r) {
+    // first round of every rank's entries loaded up front (independent loads in flight),
+    // then added rank by rank: the rank-order sum of DESIGN.md R-8
+    uint32_t pj[kReplayMaxWorld], pv[kReplayMaxWorld];
+#pragma unroll
+    for (int r = 0; r < kReplayMaxWorld; ++r) {
+      pj[r] = 0xFFFFFFFFu;
+      if (r < world) {
+        const uint32_t e = s_a[cur][r] + tid;
+        if (e < s_b[cur][r]) {
+          const uint32_t* idx = blk + (uint64_t)r * 2 * K;
+          pj[r] = __ldg(idx + e) - (uint32_t)j0;
+          pv[r] = __ldg(idx + K + e);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kReplayMaxWorld; ++r) {
+      if (r < world) {
+        if (pj[r] != 0xFFFFFFFFu) G[pj[r]] = __fadd_rn(G[pj[r]], __uint_as_float(pv[r]));
+        const uint32_t* idx = blk + (uint64_t)r * 2 * K;
+        for (uint32_t e = s_a[cur][r] + tid + kReplayThreads; e < s_b[cur][r]; e += kReplayThreads) {
+          const uint32_t j = __ldg(idx + e) - (uint32_t)j0;
+          G[j] = __fadd_rn(G[j], __uint_as_float(__ldg(idx + K + e)));
+        }
+        __syncthreads();
+      }
+    }
+    for (int r = kReplayMaxWorld; r < world; ++r) {   // ranks beyond the register window
+      const uint32_t* st = start + ((uint64_t)s * world + r) * tstride + t;
       const uint32_t* idx = blk + (uint64_t)r * 2 * K;
-      const uint32_t* val = idx + K;
-      const uint32_t a = __ldg(st + r * tstride), b = __ldg(st + r * tstride + 1);
+      const uint32_t a = __ldg(st), b = __ldg(st + 1);
       for (uint32_t e = a + tid; e < b; e += kReplayThreads) {
         const uint32_t j = __ldg(idx + e) - (uint32_t)j0;
-        G[j] = __fadd_rn(G[j], __uint_as_float(__ldg(val + e)));
+        G[j] = __fadd_rn(G[j], __uint_as_float(__ldg(idx + K + e)));
       }
       __syncthreads();
     }
-    const float lr = __ldg(scal + 3 * s), r1 = __ldg(scal + 3 * s + 1), r2 = __ldg(scal + 3 * s + 2);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const float4 gv = G4[tid + kReplayThreads * i];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        float g = q == 0 ? gv.x : q == 1 ? gv.y : q == 2 ? gv.z : gv.w;
-        if (MEAN) g = __fdiv_rn(g, n);
+        const float g = mean_of<DIV>(q == 0 ? gv.x : q == 1 ? gv.y : q == 2 ? gv.z : gv.w, n, inv);
         const int x = 4 * i + q;
         if (OPT == LOWDIFF_ADAM) {
           // m = b1*m + c1*g ; v = b2*v + c2*(g*g) ; mh = m*r1 ; vh = v*r2
@@ -137,14 +194,18 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
           V[x] = __fadd_rn(__fmul_rn(ak.b2, V[x]), __fmul_rn(ak.c2, __fmul_rn(g, g)));
           const float mh = __fmul_rn(M[x], r1);
           const float vh = __fmul_rn(V[x], r2);
-          const float d = __fadd_rn(__fsqrt_rn(vh), ak.eps);
-          const float u = __fdiv_rn(mh, d);
+          // sqrt(+-0) = +-0 and +-0 / d = +-0 (d > 0) are IEEE-exact; testing for them keeps the
+          // untouched elements (v == 0, m == 0) off the library's special-case slow path
+          const float sq = vh == 0.f ? vh : __fsqrt_rn(vh);
+          const float d = __fadd_rn(sq, ak.eps);
+          const float u = mh == 0.f ? mh : __fdiv_rn(mh, d);
           P[x] = __fsub_rn(P[x], __fmul_rn(lr, u));
         } else {
           P[x] = __fsub_rn(P[x], __fmul_rn(lr, g));
         }
       }
     }
+    if (tid < world && tid < kReplayMaxWorld) { s_a[cur ^ 1][tid] = na; s_b[cur ^ 1][tid] = nb; }
     __syncthreads();
   }
 #pragma unroll
@@ -198,10 +259,12 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
   int h;
   prof_begin(c, "merge", s, &h);
   tile_start_kernel<<<sms * 8, 256, 0, s>>>(gathered, world, 2 * K, K, kMergeTile, n_tiles, start);
-  if (c->cfg.mean)
-    merge_kernel<true><<<(unsigned)n_tiles, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense);
-  else
-    merge_kernel<false><<<(unsigned)n_tiles, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense);
+  const unsigned grid = (unsigned)n_tiles;
+  switch (div_mode(c->cfg.mean != 0, world)) {
+    case 0: merge_kernel<0><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
+    case 1: merge_kernel<1><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
+    default: merge_kernel<2><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
+  }
   prof_end(c, h, s);
   c->launches += 2;
   return cudaGetLastError();
@@ -231,13 +294,16 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
   prof_end(c, h, s);
   prof_begin(c, "replay", s, &h);
   const unsigned grid = (unsigned)n_tiles;
+  const int dm = div_mode(mean, world);
+#define LD_REPLAY(OPT, DIV) \
+  replay_kernel<OPT, DIV><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, \
+                                                          (uint64_t)psi, p, m, v)
   if (optim == LOWDIFF_ADAM) {
-    if (mean) replay_kernel<LOWDIFF_ADAM, true><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, (uint64_t)psi, p, m, v);
-    else replay_kernel<LOWDIFF_ADAM, false><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, (uint64_t)psi, p, m, v);
+    if (dm == 0) LD_REPLAY(LOWDIFF_ADAM, 0); else if (dm == 1) LD_REPLAY(LOWDIFF_ADAM, 1); else LD_REPLAY(LOWDIFF_ADAM, 2);
   } else {
-    if (mean) replay_kernel<LOWDIFF_SGD, true><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, (uint64_t)psi, p, m, v);
-    else replay_kernel<LOWDIFF_SGD, false><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, (uint64_t)psi, p, m, v);
+    if (dm == 0) LD_REPLAY(LOWDIFF_SGD, 0); else if (dm == 1) LD_REPLAY(LOWDIFF_SGD, 1); else LD_REPLAY(LOWDIFF_SGD, 2);
   }
+#undef LD_REPLAY
   prof_end(c, h, s);
   c->launches += 2;
   return cudaGetLastError();
