@@ -195,7 +195,6 @@ void release(lowdiff_ctx* c, std::vector<int>& batch) {
 
 void writer_loop(lowdiff_ctx* c) {
   std::vector<int> batch;
-  uint32_t err_seen = 0;
   cudaSetDevice(c->device);
   for (;;) {
     int slot = -1;
@@ -221,8 +220,8 @@ void writer_loop(lowdiff_ctx* c) {
       if (e != cudaSuccess) {
         set_deferred(c, LOWDIFF_E_CUDA, std::string("D2H of a differential: ") + cudaGetErrorString(e));
         drop = true;
-      } else if (S.err_host[0] != err_seen) {
-        err_seen = S.err_host[0];
+      } else if (S.err_host[0] > c->err_seen.load()) {
+        c->err_seen = S.err_host[0];   // device counter of non-finite events (never reset)
         char msg[160];
         std::snprintf(msg, sizeof msg, "non-finite accumulated gradient before iteration %lld (first layer %u)",
                       (long long)S.iteration, S.err_host[1]);
@@ -494,9 +493,9 @@ lowdiff_status lowdiff_sync(lowdiff_ctx* c) {
   CK(cudaMemcpy(err, c->plan.err, 8, cudaMemcpyDeviceToHost));
   lowdiff_status d = take_deferred(c);
   if (d) return d;
-  if (err[0] != 0) {
-    // counter semantics: reset after reporting so the next sync reports only new events
-    CK(cudaMemset(c->plan.err, 0, 4));
+  if (err[0] > c->err_seen.load()) {
+    // the device keeps a monotone counter of non-finite events; report only new ones
+    c->err_seen = err[0];
     return fail(c, LOWDIFF_E_NUMERIC, "non-finite accumulated gradient (first layer " + std::to_string(err[1]) + ")");
   }
   return LOWDIFF_OK;
@@ -554,7 +553,8 @@ lowdiff_status lowdiff_compress(lowdiff_ctx* c, const float* grad, float* residu
   if (!aligned16(grad) || !aligned16(send) || (residual && !aligned16(residual)))
     return fail(c, LOWDIFF_E_INVALID, "compress: buffers must be 16-byte aligned");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (c->last_d2h_src == send) CK(cudaStreamWaitEvent(s, c->last_d2h, 0));   // WAR on the send block
+  for (auto& ps : c->d2h_src)   // WAR: a persist of this buffer may still be copying it out
+    if (ps.first == send) CK(cudaStreamWaitEvent(s, c->slots[ps.second].done, 0));
   CK(ld::launch_compress(c, grad, c->cfg.error_feedback ? residual : nullptr, send, s));
   return LOWDIFF_OK;
 }
@@ -627,8 +627,17 @@ lowdiff_status lowdiff_batch_persist(lowdiff_ctx* c, int64_t iteration, const lo
   ld::prof_end(c, hnd, c->side);
   CK(cudaMemcpyAsync(S.err_host, c->plan.err, 8, cudaMemcpyDeviceToHost, c->side));
   CK(cudaEventRecord(S.done, c->side));
-  CK(cudaEventRecord(c->last_d2h, c->side));
-  c->last_d2h_src = send;
+  // remember the latest slot copying `send` (its event orders after every earlier copy: one side stream)
+  bool found = false;
+  for (auto& ps : c->d2h_src)
+    if (ps.first == send) { ps.second = slot; found = true; }
+  if (!found) {
+    if (c->d2h_src.size() >= 64) {   // many distinct send buffers: drain instead of tracking them all
+      CK(cudaStreamSynchronize(c->side));
+      c->d2h_src.clear();
+    }
+    c->d2h_src.push_back({send, slot});
+  }
   {
     std::lock_guard<std::mutex> g(c->mu);
     c->queued.push_back(slot);

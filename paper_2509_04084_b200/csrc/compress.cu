@@ -24,6 +24,8 @@
 //   HBM traffic in the steady state: 12 B/param (+ ~0.13 B/param of candidates) + 8 B/entry.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace ld {
@@ -142,7 +144,7 @@ small_layer_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r
     bad |= (u & 0x7F800000u) == 0x7F800000u;
     acc[i] = u;
   }
-  if (bad) { atomicOr(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)li); }
+  if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)li); }
   if (tid == 0) { s_prefix = 0; s_kleft = k; }
 
   const int shifts[3] = {20, 9, 0};
@@ -284,7 +286,7 @@ __device__ __forceinline__ void scan_chunk(const DevPlan& P, int ch, const float
     for (int q = 0; q < 4; ++q) tot += __popc(__ballot_sync(0xFFFFFFFFu, (f >> q) & 1u));
     if (lane == 0) sh_tot[j * (kScanThreads / 32) + warp] = tot;
   }
-  if (bad) { atomicOr(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
+  if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
   __syncthreads();
   // exclusive scan of the 8 x 16 segment counts in (j, warp) order: one warp, 4 per lane
   if (warp == 0) {
@@ -328,6 +330,210 @@ __device__ __forceinline__ void scan_chunk(const DevPlan& P, int ch, const float
   uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
   for (int b = tid; b < kH0; b += kScanThreads)
     if (sh_hist[b]) atomicAdd(&hrow[b], sh_hist[b]);
+}
+
+// ---------------------------------------------------------------- large layers: TMA-pipelined scan
+// Persistent CTAs (2 per SM) stream their chunks through a 3-stage shared-memory ring filled by
+// 1-D bulk tensor copies (cp.async.bulk, completion on an mbarrier with expect_tx), so the next
+// sub-tiles are already in flight while the current one is added, stored and compacted.
+constexpr int kSub = 4096;                  // elements per sub-tile (16 KB per operand)
+constexpr int kStages = 3;
+constexpr int kSlotsPerThread = kSub / 4 / kScanThreads;   // 2 float4 slots per thread per sub-tile
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "LD_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LD_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(0x12F0000000000000ull)  // evict_first
+      : "memory");
+}
+
+struct SubTile {
+  int ch;          // chunk id (-1: none)
+  int sub;         // sub-tile within the chunk
+};
+
+__device__ __forceinline__ bool next_sub(const DevPlan& P, SubTile& s) {
+  // advance (ch, sub) over this CTA's chunks: ch = blockIdx.x + i * gridDim.x
+  const uint64_t span = P.chunk_hi[s.ch] - P.chunk_base[s.ch];
+  if ((uint64_t)(s.sub + 1) * kSub < span) { ++s.sub; return true; }
+  s.ch += gridDim.x;
+  s.sub = 0;
+  return s.ch < P.n_chunks;
+}
+
+// issue the bulk copies of one sub-tile into stage st (thread 0 only)
+template <bool EF>
+__device__ __forceinline__ void issue_sub(const DevPlan& P, const SubTile& s, int st, float* sg, float* sr,
+                                          uint64_t* full, const float* g, const float* r, uint64_t psi) {
+  const uint64_t sb = P.chunk_base[s.ch] + (uint64_t)s.sub * kSub;
+  const uint64_t se = min(sb + kSub, P.chunk_hi[s.ch]);
+  uint64_t ve = (se + 3) & ~3ull;           // whole float4 slots ...
+  if (ve > psi) ve = psi & ~3ull;           // ... that lie inside the caller's buffer
+  const uint32_t bytes = ve > sb ? (uint32_t)((ve - sb) * 4) : 0u;
+  mbar_arrive_expect_tx(&full[st], bytes * (EF ? 2u : 1u));
+  if (bytes) {
+    bulk_g2s(sg + st * kSub, g + sb, bytes, &full[st]);
+    if (EF) bulk_g2s(sr + st * kSub, r + sb, bytes, &full[st]);
+  }
+}
+
+template <bool EF>
+__global__ void __launch_bounds__(kScanThreads, 2)
+scan_tma_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, uint64_t psi) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  float* sg = reinterpret_cast<float*>(dsm);                 // [kStages][kSub]
+  float* sr = sg + kStages * kSub;                           // [kStages][kSub] (EF)
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ uint32_t sh_hist[kH0];
+  __shared__ uint32_t sh_tot[2 * (kScanThreads / 32) + 1];
+  __shared__ uint32_t s_run;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if ((int)blockIdx.x >= P.n_chunks) return;
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int b = tid; b < kH0; b += kScanThreads) sh_hist[b] = 0;
+  if (tid == 0) s_run = 0;
+  __syncthreads();
+  SubTile prod{(int)blockIdx.x, 0};
+  bool prod_ok = true;
+  if (tid == 0) {
+    for (int st = 0; st < kStages && prod_ok; ++st) {
+      issue_sub<EF>(P, prod, st, sg, sr, full, g, r, psi);
+      prod_ok = next_sub(P, prod);
+    }
+  }
+  SubTile cur{(int)blockIdx.x, 0};
+  int stage = 0;
+  uint32_t phase = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  for (;;) {
+    bool bad = false;
+    const int ch = cur.ch;
+    const int slot = P.chunk_slot[ch];
+    const uint64_t lo = P.chunk_lo[ch], hi = P.chunk_hi[ch];
+    const uint64_t sb = P.chunk_base[ch] + (uint64_t)cur.sub * kSub;
+    const uint32_t thr = P.thr[slot];
+    mbar_wait(&full[stage], phase);
+    const float* tg = sg + stage * kSub;
+    const float* tr = sr + stage * kSub;
+    float4 a[kSlotsPerThread];
+    uint32_t f[kSlotsPerThread];
+#pragma unroll
+    for (int j = 0; j < kSlotsPerThread; ++j) {
+      const int q = j * kScanThreads + tid;
+      const uint64_t e0 = sb + 4ull * q;
+      uint32_t vm = 0;
+      if (e0 >= lo && e0 + 4 <= hi) vm = 0xF;
+      else if (e0 + 4 > lo && e0 < hi)
+        for (int k = 0; k < 4; ++k) vm |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (vm) {
+        if (e0 + 4 <= psi) {
+          const float4 gv = reinterpret_cast<const float4*>(tg)[q];
+          if (EF) {
+            const float4 rv = reinterpret_cast<const float4*>(tr)[q];
+            x = make_float4(__fadd_rn(rv.x, gv.x), __fadd_rn(rv.y, gv.y), __fadd_rn(rv.z, gv.z), __fadd_rn(rv.w, gv.w));
+          } else {
+            x = gv;
+          }
+        } else {   // the last partial float4 of the buffer was not bulk-copied
+          for (int k = 0; k < 4; ++k)
+            if ((vm >> k) & 1u) f4set(x, k, EF ? __fadd_rn(r[e0 + k], g[e0 + k]) : g[e0 + k]);
+        }
+        if (EF) {
+          if (vm == 0xF) st_stream(r + e0, x);
+          else
+            for (int k = 0; k < 4; ++k)
+              if ((vm >> k) & 1u) r[e0 + k] = f4get(x, k);
+        }
+      }
+      uint32_t fl = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t key = key_of(f4get(x, k));
+        const bool v = (vm >> k) & 1u;
+        bad |= v && key >= 0x7F800000u;
+        if (v && key >= thr) { fl |= 1u << k; atomicAdd(&sh_hist[key >> 20], 1u); }
+      }
+      f[j] = fl;
+      a[j] = x;
+      uint32_t tot = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tot += __popc(__ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u));
+      if (lane == 0) sh_tot[j * (kScanThreads / 32) + warp] = tot;
+    }
+    if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
+    __syncthreads();   // sh_tot complete; every thread is done reading this stage
+    if (tid == 0 && prod_ok) {   // refill the stage just consumed
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_sub<EF>(P, prod, stage, sg, sr, full, g, r, psi);
+      prod_ok = next_sub(P, prod);
+    }
+    if (warp == 0) {
+      const int nseg = kSlotsPerThread * (kScanThreads / 32);   // 32 segments: one per lane
+      uint32_t v = lane < nseg ? sh_tot[lane] : 0u, inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const uint32_t base = s_run;
+      if (lane < nseg) sh_tot[lane] = base + inc - v;
+      if (lane == 31) sh_tot[nseg] = base + inc;
+    }
+    __syncthreads();
+    uint32_t* cidx = P.cand_idx + (uint64_t)ch * kChunk;
+    uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
+#pragma unroll
+    for (int j = 0; j < kSlotsPerThread; ++j) {
+      const uint32_t fl = f[j];
+      uint32_t pos = sh_tot[j * (kScanThreads / 32) + warp];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) pos += __popc(__ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u) & lt);
+      if (fl) {
+        const uint64_t e0 = sb + 4ull * (j * kScanThreads + tid);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if ((fl >> k) & 1u) { cidx[pos] = (uint32_t)(e0 + k); cval[pos] = __float_as_uint(f4get(a[j], k)); ++pos; }
+      }
+    }
+    if (tid == 0) s_run = sh_tot[kSlotsPerThread * (kScanThreads / 32)];
+    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+    const bool last_sub = (uint64_t)(cur.sub + 1) * kSub >= hi - P.chunk_base[ch];
+    if (last_sub) {
+      __syncthreads();   // s_run final, histogram complete
+      if (tid == 0) P.chunk_count[ch] = s_run;
+      uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
+      for (int b = tid; b < kH0; b += kScanThreads) {
+        const uint32_t h = sh_hist[b];
+        if (h) { atomicAdd(&hrow[b], h); sh_hist[b] = 0; }
+      }
+      if (tid == 0) s_run = 0;
+    }
+    __syncthreads();
+    if (!next_sub(P, cur)) break;
+  }
 }
 
 template <bool EF>
@@ -561,10 +767,21 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   const int warp_blocks = (P.n_large * 32 + 255) / 256;
   const int pgrid = (P.n_chunks + 7) / 8;   // one warp per chunk: latency hidden by parallelism
 
-  prof_begin(c, "scan", s, &h);
-  if (ef) scan_kernel<true><<<P.n_chunks, kScanThreads, 0, s>>>(P, grad, residual);
-  else scan_kernel<false><<<P.n_chunks, kScanThreads, 0, s>>>(P, grad, residual);
-  prof_end(c, h, s);
+  {
+    static bool tma_attr[2] = {false, false};
+    const size_t smem = (size_t)kStages * kSub * sizeof(float) * (ef ? 2 : 1);
+    if (!tma_attr[ef]) {
+      e = ef ? cudaFuncSetAttribute(scan_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+             : cudaFuncSetAttribute(scan_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      tma_attr[ef] = true;
+    }
+    const int grid = std::min(P.n_chunks, sms * 2);
+    prof_begin(c, "scan", s, &h);
+    if (ef) scan_tma_kernel<true><<<grid, kScanThreads, smem, s>>>(P, grad, residual, (uint64_t)c->psi);
+    else scan_tma_kernel<false><<<grid, kScanThreads, smem, s>>>(P, grad, residual, (uint64_t)c->psi);
+    prof_end(c, h, s);
+  }
   prof_begin(c, "select", s, &h);
   find_kernel<<<warp_blocks, 256, 0, s>>>(P, 0);
   if (ef) rescan_kernel<true><<<sms * 2, kScanThreads, 0, s>>>(P, grad, residual);

@@ -97,8 +97,9 @@ struct lowdiff_ctx {
   cudaStream_t side = nullptr;       // D2H copies
   cudaEvent_t ev_tmp = nullptr;
   cudaEvent_t ev_side_all = nullptr; // lowdiff_wait_persist
-  cudaEvent_t last_d2h = nullptr;    // WAR guard for the send buffer
-  const void* last_d2h_src = nullptr;
+  cudaEvent_t last_d2h = nullptr;    // unused (kept for ABI-stable layout of the struct)
+  std::vector<std::pair<const void*, int>> d2h_src;   // send buffer -> ring slot of its latest D2H (WAR)
+  std::atomic<uint32_t> err_seen{0};  // non-finite events already reported
   // NCCL
   ncclComm_t comm = nullptr;
   // status
