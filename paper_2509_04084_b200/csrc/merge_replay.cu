@@ -121,43 +121,50 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
   (void)full;
   const float n = (float)world, inv = 1.0f / (float)world;
   const uint64_t tstride = (uint64_t)(n_tiles + 1);
-  // entry ranges of step s for every rank, double-buffered in shared memory: the loads for step
-  // s+1 are issued by threads tid < world at the start of step s and land during its compute
+  // Software pipeline over steps (everything that step s+1 needs from HBM is in flight while step
+  // s computes): rng[x & 1] in shared memory holds the entry ranges of step x for every rank; the
+  // first 256 entries of every rank for step s sit in registers (pj, pv), loaded during step s-1.
   __shared__ uint32_t s_a[2][kReplayMaxWorld], s_b[2][kReplayMaxWorld];
-  if (tid < world && tid < kReplayMaxWorld) {
+  const bool ranger = tid < world && tid < kReplayMaxWorld;
+  if (ranger) {
     s_a[0][tid] = __ldg(start + (uint64_t)tid * tstride + t);
     s_b[0][tid] = __ldg(start + (uint64_t)tid * tstride + t + 1);
-  }
-  float4* G4 = reinterpret_cast<float4*>(G);
-#pragma unroll 1
-  for (int64_t s = 0; s < n_steps; ++s) {
-    const int cur = (int)(s & 1);
-    uint32_t na = 0, nb = 0;
-    if (tid < world && tid < kReplayMaxWorld && s + 1 < n_steps) {
-      const uint32_t* st1 = start + ((uint64_t)(s + 1) * world + tid) * tstride + t;
-      na = __ldg(st1);
-      nb = __ldg(st1 + 1);
+    if (n_steps > 1) {
+      const uint32_t* st1 = start + ((uint64_t)world + tid) * tstride + t;
+      s_a[1][tid] = __ldg(st1);
+      s_b[1][tid] = __ldg(st1 + 1);
     }
-    const float lr = __ldg(scal + 3 * s), r1 = __ldg(scal + 3 * s + 1), r2 = __ldg(scal + 3 * s + 2);
-    G4[tid] = make_float4(0.f, 0.f, 0.f, 0.f);
-    G4[tid + kReplayThreads] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncthreads();
-    const uint32_t* blk = diffs + (uint64_t)s * world * 2 * K;
-    // first round of every rank's entries loaded up front (independent loads in flight),
-    // then added rank by rank: the rank-order sum of DESIGN.md R-8
-    uint32_t pj[kReplayMaxWorld], pv[kReplayMaxWorld];
+  }
+  __syncthreads();
+  uint32_t pj[kReplayMaxWorld], pv[kReplayMaxWorld];
+  auto load_entries = [&](int64_t x) {   // first round of step x's entries of every rank
+    const uint32_t* blk = diffs + (uint64_t)x * world * 2 * K;
+    const int b = (int)(x & 1);
 #pragma unroll
     for (int r = 0; r < kReplayMaxWorld; ++r) {
       pj[r] = 0xFFFFFFFFu;
+      pv[r] = 0u;
       if (r < world) {
-        const uint32_t e = s_a[cur][r] + tid;
-        if (e < s_b[cur][r]) {
+        const uint32_t e = s_a[b][r] + tid;
+        if (e < s_b[b][r]) {
           const uint32_t* idx = blk + (uint64_t)r * 2 * K;
           pj[r] = __ldg(idx + e) - (uint32_t)j0;
           pv[r] = __ldg(idx + K + e);
         }
       }
     }
+  };
+  load_entries(0);
+  float lr = __ldg(scal), r1 = __ldg(scal + 1), r2 = __ldg(scal + 2);
+  float4* G4 = reinterpret_cast<float4*>(G);
+#pragma unroll 1
+  for (int64_t s = 0; s < n_steps; ++s) {
+    const int cur = (int)(s & 1);
+    G4[tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+    G4[tid + kReplayThreads] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    const uint32_t* blk = diffs + (uint64_t)s * world * 2 * K;
+    // rank by rank from +0: the rank-order sum of DESIGN.md R-8
 #pragma unroll
     for (int r = 0; r < kReplayMaxWorld; ++r) {
       if (r < world) {
@@ -180,6 +187,20 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       }
       __syncthreads();
     }
+    // prefetch for the next steps while this one computes
+    const float slr = lr, sr1 = r1, sr2 = r2;
+    uint32_t na = 0, nb = 0;
+    if (s + 1 < n_steps) {
+      load_entries(s + 1);
+      lr = __ldg(scal + 3 * (s + 1));
+      r1 = __ldg(scal + 3 * (s + 1) + 1);
+      r2 = __ldg(scal + 3 * (s + 1) + 2);
+    }
+    if (ranger && s + 2 < n_steps) {
+      const uint32_t* st2 = start + ((uint64_t)(s + 2) * world + tid) * tstride + t;
+      na = __ldg(st2);
+      nb = __ldg(st2 + 1);
+    }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const float4 gv = G4[tid + kReplayThreads * i];
@@ -192,20 +213,20 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
           // d = sqrt(vh) + eps ; u = mh / d ; p = p - lr*u          (R-11)
           M[x] = __fadd_rn(__fmul_rn(ak.b1, M[x]), __fmul_rn(ak.c1, g));
           V[x] = __fadd_rn(__fmul_rn(ak.b2, V[x]), __fmul_rn(ak.c2, __fmul_rn(g, g)));
-          const float mh = __fmul_rn(M[x], r1);
-          const float vh = __fmul_rn(V[x], r2);
+          const float mh = __fmul_rn(M[x], sr1);
+          const float vh = __fmul_rn(V[x], sr2);
           // sqrt(+-0) = +-0 and +-0 / d = +-0 (d > 0) are IEEE-exact; testing for them keeps the
           // untouched elements (v == 0, m == 0) off the library's special-case slow path
           const float sq = vh == 0.f ? vh : __fsqrt_rn(vh);
           const float d = __fadd_rn(sq, ak.eps);
           const float u = mh == 0.f ? mh : __fdiv_rn(mh, d);
-          P[x] = __fsub_rn(P[x], __fmul_rn(lr, u));
+          P[x] = __fsub_rn(P[x], __fmul_rn(slr, u));
         } else {
-          P[x] = __fsub_rn(P[x], __fmul_rn(lr, g));
+          P[x] = __fsub_rn(P[x], __fmul_rn(slr, g));
         }
       }
     }
-    if (tid < world && tid < kReplayMaxWorld) { s_a[cur ^ 1][tid] = na; s_b[cur ^ 1][tid] = nb; }
+    if (ranger) { s_a[cur][tid] = na; s_b[cur][tid] = nb; }   // ranges of step s+2
     __syncthreads();
   }
 #pragma unroll
