@@ -600,6 +600,25 @@ __global__ void find_kernel(DevPlan P, int mode) {
     const uint32_t* h = hrow + (mode == 2 ? kH0 : kH0 + kH1);
     uint32_t bin, above;
     warp_find_bin(h, nb, S.kleft, &bin, &above);
+    if (mode == 2) {
+      // Speculative band for the next call: the key with C = 1.5 k_l candidate keys at or above it
+      // (digit-0 resolution, refined with the digit-1 histogram when C falls in T's digit-0 bin).
+      // Only a prediction -- the next call checks #candidates >= k_l and refills otherwise.
+      const uint32_t C = k + max(k / 2, 32u);
+      uint32_t nt = P.thr[slot];
+      if (S.total >= C) {
+        uint32_t b0, a0;
+        warp_find_bin(hrow, kH0, C, &b0, &a0);
+        if (b0 == S.prefix) {
+          uint32_t b1, a1;
+          warp_find_bin(h, nb, C - a0, &b1, &a1);
+          nt = (b0 << 20) | (b1 << 9);
+        } else {
+          nt = b0 << 20;
+        }
+      }
+      if (lane == 0) S.next_thr = nt;
+    }
     if (lane == 0) { S.prefix = (S.prefix << (mode == 2 ? 11 : 9)) | bin; S.kleft -= above; }
   }
 }
@@ -677,9 +696,8 @@ __global__ void __launch_bounds__(256) layer_scan_kernel(DevPlan P) {
     if (c < c1) { P.chunk_out[c] = ob; P.chunk_take[c] = take; }
   }
   if (threadIdx.x == 0) {
-    // speculative band for the next call: key >= bits(0.98 * |T|)
-    const float t = __uint_as_float(T);
-    const uint32_t nt = __float_as_uint(__fmul_rn(t, 0.98f)) & 0x7FFFFFFFu;
+    // speculative band for the next call, never above this call's T
+    const uint32_t nt = P.sel[slot].next_thr;
     P.thr[slot] = nt <= T ? nt : T;
   }
 }

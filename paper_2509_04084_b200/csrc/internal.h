@@ -35,6 +35,8 @@ struct LayerSel {
   uint32_t kleft;    // entries still to take among those matching prefix
   uint32_t total;    // candidate count
   uint32_t refill;   // 1: speculative band too narrow, whole layer became candidates
+  uint32_t next_thr; // speculative band for the next call (key with ~1.5 k_l keys above it)
+  uint32_t pad[3];
 };
 
 struct DevPlan {
@@ -158,6 +160,7 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
 cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* consts5, int world,
                           int64_t n_steps, const uint32_t* diffs, const float* scal_dev, float* p,
                           float* m, float* v, cudaStream_t s);
+cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches, uint64_t* first);
 size_t merge_scratch_bytes(int64_t psi, int world, int64_t n_blocks);
 size_t replay_scratch_bytes(int64_t psi, int world, int64_t n_steps);
 

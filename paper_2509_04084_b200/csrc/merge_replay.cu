@@ -18,6 +18,7 @@
 // fast-math, denormals preserved; R-20/R-21).
 #include <cuda_runtime.h>
 
+#include "ieee_fast.cuh"
 #include "internal.h"
 
 namespace ld {
@@ -96,7 +97,7 @@ struct AdamK { float b1, c1, b2, c2, eps; };
 constexpr int kReplayMaxWorld = 8;
 
 template <int OPT, int DIV>
-__global__ void __launch_bounds__(kReplayThreads)
+__global__ void __launch_bounds__(kReplayThreads, 3)
 replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
               const uint32_t* __restrict__ start, int64_t n_tiles, const float* __restrict__ scal,
               AdamK ak, uint64_t psi, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v) {
@@ -215,11 +216,10 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
           V[x] = __fadd_rn(__fmul_rn(ak.b2, V[x]), __fmul_rn(ak.c2, __fmul_rn(g, g)));
           const float mh = __fmul_rn(M[x], sr1);
           const float vh = __fmul_rn(V[x], sr2);
-          // sqrt(+-0) = +-0 and +-0 / d = +-0 (d > 0) are IEEE-exact; testing for them keeps the
-          // untouched elements (v == 0, m == 0) off the library's special-case slow path
-          const float sq = vh == 0.f ? vh : __fsqrt_rn(vh);
-          const float d = __fadd_rn(sq, ak.eps);
-          const float u = mh == 0.f ? mh : __fdiv_rn(mh, d);
+          // branch-free correctly rounded sqrt / divide (ieee_fast.cuh): bit-identical to
+          // __fsqrt_rn / __fdiv_rn without the per-lane divergence of their slow-path guards
+          const float d = __fadd_rn(sqrt_rn_nb(vh), ak.eps);
+          const float u = div_rn_nb(mh, d);
           P[x] = __fsub_rn(P[x], __fmul_rn(slr, u));
         } else {
           P[x] = __fsub_rn(P[x], __fmul_rn(slr, g));

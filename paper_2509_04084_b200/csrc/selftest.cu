@@ -1,0 +1,94 @@
+// lowdiff_selftest: device-side proofs for the branch-free IEEE helpers of ieee_fast.cuh.
+//   which = 0: sqrt_rn_nb vs __fsqrt_rn over every non-negative float and -0 (2^31 + 1 inputs)
+//   which = 1: div_rn_nb vs __fdiv_rn on n pseudo-random operand pairs: raw 32-bit patterns
+//              (NaN, Inf, denormals, zeros included) and pairs drawn from the replay's domain
+//              (m*r1 over sqrt(v*r2)+eps), plus exhaustive sweeps of the window edges
+#include <cuda_runtime.h>
+
+#include "ieee_fast.cuh"
+#include "internal.h"
+
+namespace ld {
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void sqrt_check_kernel(unsigned long long* bad, unsigned long long* first) {
+  const uint64_t total = (1ull << 31) + 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = i == (1ull << 31) ? 0x80000000u : (uint32_t)i;
+    const float x = __uint_as_float(u);
+    const uint32_t a = __float_as_uint(sqrt_rn_nb(x)), b = __float_as_uint(__fsqrt_rn(x));
+    if (a != b) {
+      atomicAdd(bad, 1ull);
+      atomicMin(first, (unsigned long long)u);
+    }
+  }
+}
+
+__global__ void div_check_kernel(uint64_t n, uint64_t seed, unsigned long long* bad, unsigned long long* first) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = mix64(seed ^ mix64(i));
+    const uint64_t h2 = mix64(h);
+    uint32_t ua, ub;
+    switch (i & 3) {
+      case 0:   // raw bit patterns
+        ua = (uint32_t)h;
+        ub = (uint32_t)(h >> 32);
+        break;
+      case 1: {  // the replay's domain: mh ~ 1e-30..1e3 (either sign), d = sqrt(vh) + eps >= 1e-8
+        const float mag = exp2f(-100.f + 110.f * (float)(h & 0xFFFFFF) / 16777216.f);
+        const float mh = ((h >> 24) & 1) ? -mag : mag;
+        const float vh = exp2f(-80.f + 90.f * (float)((h >> 32) & 0xFFFFFF) / 16777216.f);
+        ua = __float_as_uint(mh);
+        ub = __float_as_uint(__fadd_rn(__fsqrt_rn(vh), 1e-8f));
+        break;
+      }
+      case 2: {  // exponents swept across the fast-window edges, random mantissas
+        const uint32_t ea = 40 + (uint32_t)(h % 180), eb = 40 + (uint32_t)((h >> 16) % 180);
+        ua = ((uint32_t)(h2 >> 63) << 31) | (ea << 23) | ((uint32_t)h2 & 0x7FFFFF);
+        ub = ((uint32_t)(h2 >> 62 & 1) << 31) | (eb << 23) | ((uint32_t)(h2 >> 23) & 0x7FFFFF);
+        break;
+      }
+      default: {  // near-ties: mantissas with few bits set, zeros, denormals
+        ua = (uint32_t)h & 0xFF8000FFu;
+        ub = ((uint32_t)(h >> 32) & 0xFFF00001u) | 0x00800000u;
+        if ((h2 & 15) == 0) ua &= 0x80000000u;
+        if ((h2 & 240) == 0) ub &= 0x807FFFFFu;
+        break;
+      }
+    }
+    const float a = __uint_as_float(ua), b = __uint_as_float(ub);
+    const uint32_t x = __float_as_uint(div_rn_nb(a, b)), y = __float_as_uint(__fdiv_rn(a, b));
+    if (x != y && !((x & 0x7FFFFFFFu) > 0x7F800000u && (y & 0x7FFFFFFFu) > 0x7F800000u)) {
+      atomicAdd(bad, 1ull);
+      atomicMin(first, (unsigned long long)i);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches, uint64_t* first) {
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 16);
+  if (e != cudaSuccess) return e;
+  unsigned long long init[2] = {0ull, ~0ull};
+  cudaMemcpy(d, init, 16, cudaMemcpyHostToDevice);
+  if (which == 0) sqrt_check_kernel<<<148 * 16, 256>>>(d, d + 1);
+  else div_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
+  e = cudaDeviceSynchronize();
+  unsigned long long h[2] = {0, 0};
+  if (e == cudaSuccess) e = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  *mismatches = h[0];
+  *first = h[1];
+  return e;
+}
+
+}  // namespace ld

@@ -90,6 +90,7 @@ def lib():
             "write_batch_host": ([C.POINTER(Config), C.c_int64, C.c_int32, C.POINTER(StepScalars), P], S),
             "write_full_host": ([C.POINTER(Config), C.c_int64, P, P, P], S),
             "abi_version": ([], C.c_int32),
+            "selftest": ([C.c_int32, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], S),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, "lowdiff_" + name)
@@ -103,7 +104,14 @@ EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "exchange", "me
             "full_ckpt", "wait_persist", "recover", "replay", "snapshot_layer", "snapshot_wait", "sync", "get_stats",
             "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
             "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host",
-            "write_full_host", "abi_version"]
+            "write_full_host", "abi_version", "selftest"]
+
+
+def selftest(which: int, n: int = 0, seed: int = 0):
+    """(mismatches, first_bad) of the device IEEE helpers vs the CUDA intrinsics (needs a GPU)."""
+    bad, first = C.c_uint64(), C.c_uint64()
+    _check("selftest", lib().lowdiff_selftest(which, n, seed, C.byref(bad), C.byref(first)))
+    return bad.value, first.value
 
 
 def _ptr(t):
