@@ -138,6 +138,7 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   void* p;
   if ((st = dalloc(c, nc * ld::kChunk * 4, &p))) return st; P.cand_idx = (uint32_t*)p;
   if ((st = dalloc(c, nc * ld::kChunk * 4, &p))) return st; P.cand_val = (uint32_t*)p;
+  if ((st = dalloc(c, nc * ld::kSegsPerChunk * sizeof(uint16_t), &p))) return st; P.seg_count = (uint16_t*)p;
   if ((st = dalloc(c, nc * 4 * 6, &p))) return st;
   P.chunk_count = (uint32_t*)p; P.chunk_gt = P.chunk_count + nc; P.chunk_eq = P.chunk_gt + nc;
   P.chunk_out = P.chunk_eq + nc; P.chunk_take = P.chunk_out + nc; P.refill_list = P.chunk_take + nc;

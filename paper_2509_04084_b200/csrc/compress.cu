@@ -5,23 +5,29 @@
 //   acc = residual + grad; select per layer the k_l largest keys bits(acc) & 0x7FFFFFFF,
 //   ties to the lower index; emit index-ascending; residual' = acc with the selection zeroed.
 //
-// How (DESIGN.md "Compress kernels"):
+// How (DESIGN.md §4.1):
 //   small layers (n <= 16384): one CTA per layer, acc staged in shared memory, 3-digit MSB
 //     radix select (11/11/9 key bits) with shared-memory histograms, ordered emit by block scan.
-//   large layers: 16384-element chunks, one 512-thread CTA each.
-//     scan:    128-bit streaming loads of grad and residual, EF add, residual' = acc
-//              (128-bit stores), and an ORDER-PRESERVING compaction of the candidates
-//              key >= tau_l (tau_l = 0.98 x the layer's previous k-th key) into the chunk's
-//              slot of a candidate buffer, with the first radix digit histogrammed on the fly.
+//   large layers: 16384-element chunks, each cut into four 4096-element sub-tiles and 64
+//     "segments" of 256 elements (one per compute warp per sub-tile).
+//     scan:    warp-specialised persistent kernel.  A producer warp streams grad and residual
+//              sub-tiles into a 3-stage shared-memory ring with 1-D bulk copies
+//              (cp.async.bulk + mbarrier expect_tx); 16 compute warps add them (EF), store
+//              residual' = acc with 128-bit stores, and compact the candidates key >= tau_l of
+//              their segment in index order with warp ballots -- no block-wide barrier on the
+//              hot path (segments are independent; their counts go to a table).  tau_l is the
+//              speculative band predicted by the previous call; the first radix digit of the
+//              candidates is histogrammed in shared memory on the fly.
 //     plan:    per layer, if #candidates >= k_l the exact top-k lies inside the candidates
-//              (speculation hit); else the layer is "refilled": every element becomes a
-//              candidate (rescan).  Exactness never depends on the prediction.
-//     digits:  two more radix digits over the (small) candidate lists -> exact k-th key T
-//              and the number of ties at T to take.
-//     count/scan/emit: per-chunk counts of key > T and key == T, per-layer exclusive scans,
-//              then a warp per chunk writes its selected entries at their final position
-//              (index order is chunk order, then in-chunk order) and zeroes residual'.
-//   HBM traffic in the steady state: 12 B/param (+ ~0.13 B/param of candidates) + 8 B/entry.
+//              (speculation hit); otherwise the layer is "refilled": the same scan kernel
+//              re-reads acc with tau = 0, so every element becomes a candidate.  Exactness
+//              never depends on the prediction.
+//     digits:  two more radix digits over the (small) candidate lists -> exact k-th key T and
+//              the number of ties at T to take (lowest indices first).
+//     count / layer scan / emit: per-chunk counts of key > T and key == T, per-layer exclusive
+//              scans, then a warp per chunk writes its selected entries at their final position
+//              (index order = chunk, segment, in-segment order) and zeroes residual' there.
+//   HBM traffic in the steady state: 12 B/param (+ ~0.2 B/param of candidates) + 8 B/entry.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,18 +40,13 @@ namespace {
 constexpr int kH0 = 2048, kH1 = 2048, kH2 = 512;   // digit sizes: key bits [30:20] [19:9] [8:0]
 constexpr int kHistRow = kH0 + kH1 + kH2;
 
-__device__ __forceinline__ float4 ld_stream(const float* p) {
-  float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ float4 ld_rw(const float* p) {
-  float4 v;
-  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-  return v;
-}
+constexpr int kSub = 4096;                          // elements per sub-tile (16 KB per operand)
+constexpr int kWsWarps = 16;                        // compute warps of the scan kernel
+constexpr int kWsThreads = (kWsWarps + 1) * 32;     // + one producer warp
+constexpr int kStages = 3;                          // shared-memory ring depth
+static_assert(kSub / kWsWarps == kSeg, "one segment per compute warp per sub-tile");
+static_assert(kChunk / kSeg == kSegsPerChunk, "segment table shape");
+
 __device__ __forceinline__ void st_stream(float* p, float4 v) {
   asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
                :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
@@ -57,6 +58,39 @@ __device__ __forceinline__ void f4set(float4& v, int q, float x) {
   if (q == 0) v.x = x; else if (q == 1) v.y = x; else if (q == 2) v.z = x; else v.w = x;
 }
 __device__ __forceinline__ uint32_t key_of(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "LD_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LD_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared, completion counted on an mbarrier; L2 evict_first (streamed once)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(0x12F0000000000000ull)
+      : "memory");
+}
+__device__ __forceinline__ void compute_bar() {   // named barrier over the 16 compute warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(kWsWarps * 32) : "memory");
+}
 
 // Warp-cooperative search of the radix bin that holds the kleft-th largest key among the
 // entries counted in h[0..nb) (bins ordered by key).  Returns the bin and the number of
@@ -118,6 +152,37 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* sh32, 
   *total = sh32[32];
   __syncthreads();
   return r;
+}
+
+// ---------------------------------------------------------------- segment tables
+// The candidates of chunk ch live in 64 segments of 256 slots; segment s holds its cnt[s]
+// candidates, index-ascending, at cand[(ch*64 + s)*256 ...].  A warp loads the 64 counts,
+// scans them into so[0..64] (so[64] = chunk total) and addresses candidate c of the chunk as
+// segment s = max{s : so[s] <= c}, slot c - so[s].
+__device__ __forceinline__ uint32_t warp_load_segs(const DevPlan& P, int ch, uint32_t* so) {
+  const int lane = threadIdx.x & 31;
+  const uint16_t* cnt = P.seg_count + (uint64_t)ch * kSegsPerChunk;
+  const uint32_t c0 = cnt[lane], c1 = cnt[32 + lane];
+  uint32_t i0 = c0, i1 = c1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y0 = __shfl_up_sync(0xFFFFFFFFu, i0, o), y1 = __shfl_up_sync(0xFFFFFFFFu, i1, o);
+    if (lane >= o) { i0 += y0; i1 += y1; }
+  }
+  const uint32_t t0 = __shfl_sync(0xFFFFFFFFu, i0, 31);
+  so[lane] = i0 - c0;
+  so[32 + lane] = t0 + i1 - c1;
+  const uint32_t total = t0 + __shfl_sync(0xFFFFFFFFu, i1, 31);
+  if (lane == 0) so[64] = total;
+  __syncwarp();
+  return total;
+}
+__device__ __forceinline__ uint64_t seg_addr(int ch, const uint32_t* so, uint32_t c) {
+  int s = 0;
+#pragma unroll
+  for (int step = 32; step; step >>= 1)
+    if (so[s + step] <= c) s += step;
+  return ((uint64_t)ch * kSegsPerChunk + s) * kSeg + (c - so[s]);
 }
 
 // ---------------------------------------------------------------- small layers
@@ -204,362 +269,183 @@ small_layer_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r
   }
 }
 
-// ---------------------------------------------------------------- large layers: scan
+// ---------------------------------------------------------------- large layers: warp-specialised scan
+// REFILL = false: all chunks, acc = r + g, residual' = acc stored, candidates key >= thr[layer].
+// REFILL = true : the chunks in refill_list (count in counters[0]); acc re-read (r when EF, else g),
+//                 nothing stored but the candidates, thr = 0 (every element is a candidate).
 template <bool EF, bool REFILL>
-__device__ __forceinline__ void scan_chunk(const DevPlan& P, int ch, const float* __restrict__ g,
-                                           float* __restrict__ r, uint32_t* sh_hist, uint32_t* sh_tot) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int slot = P.chunk_slot[ch];
-  const uint64_t base = P.chunk_base[ch], lo = P.chunk_lo[ch], hi = P.chunk_hi[ch];
-  const uint32_t thr = REFILL ? 0u : P.thr[slot];
-  for (int b = tid; b < kH0; b += kScanThreads) sh_hist[b] = 0;
-
-  float4 a[8];
-  uint32_t vmask = 0;   // bit 4j+q: element q of slot j belongs to the chunk
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint64_t e0 = base + 4ull * (uint64_t)(j * kScanThreads + tid);
-    a[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e0 >= lo && e0 + 4 <= hi) {
-      vmask |= 0xFu << (4 * j);
-      if (REFILL) {
-        a[j] = EF ? ld_rw(r + e0) : ld_stream(g + e0);
-      } else {
-        const float4 gv = ld_stream(g + e0);
-        if (EF) {
-          const float4 rv = ld_rw(r + e0);
-          a[j] = make_float4(__fadd_rn(rv.x, gv.x), __fadd_rn(rv.y, gv.y), __fadd_rn(rv.z, gv.z),
-                             __fadd_rn(rv.w, gv.w));
-        } else {
-          a[j] = gv;
-        }
-      }
-    } else if (e0 + 4 > lo && e0 < hi) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint64_t e = e0 + q;
-        if (e >= lo && e < hi) {
-          vmask |= 1u << (4 * j + q);
-          float x;
-          if (REFILL) x = EF ? r[e] : g[e];
-          else x = EF ? __fadd_rn(r[e], g[e]) : g[e];
-          f4set(a[j], q, x);
-        }
-      }
-    }
-  }
-  if (EF && !REFILL) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint64_t e0 = base + 4ull * (uint64_t)(j * kScanThreads + tid);
-      const uint32_t vj = (vmask >> (4 * j)) & 0xFu;
-      if (vj == 0xF) {
-        st_stream(r + e0, a[j]);
-      } else if (vj) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (vj & (1u << q)) r[e0 + q] = f4get(a[j], q);
-      }
-    }
-  }
-  __syncthreads();   // histogram zeroed
-
-  // candidate flags, digit-0 histogram, per-(j, warp) counts
-  uint32_t fmask = 0;   // bit 4j+q: candidate
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint32_t f = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t key = key_of(f4get(a[j], q));
-      const bool v = (vmask >> (4 * j + q)) & 1u;
-      bad |= v && key >= 0x7F800000u;
-      if (v && key >= thr) {
-        f |= 1u << q;
-        atomicAdd(&sh_hist[key >> 20], 1u);
-      }
-    }
-    fmask |= f << (4 * j);
-    uint32_t tot = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) tot += __popc(__ballot_sync(0xFFFFFFFFu, (f >> q) & 1u));
-    if (lane == 0) sh_tot[j * (kScanThreads / 32) + warp] = tot;
-  }
-  if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
-  __syncthreads();
-  // exclusive scan of the 8 x 16 segment counts in (j, warp) order: one warp, 4 per lane
-  if (warp == 0) {
-    uint32_t v[4], s = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) { v[q] = sh_tot[lane * 4 + q]; s += v[q]; }
-    uint32_t inc = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    uint32_t run = inc - s;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) { sh_tot[lane * 4 + q] = run; run += v[q]; }
-    if (lane == 31) sh_tot[128] = inc;
-  }
-  __syncthreads();
-  const unsigned lt = (1u << lane) - 1u;
-  uint32_t* cidx = P.cand_idx + (uint64_t)ch * kChunk;
-  uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t f = (fmask >> (4 * j)) & 0xFu;
-    uint32_t pos = sh_tot[j * (kScanThreads / 32) + warp];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) pos += __popc(__ballot_sync(0xFFFFFFFFu, (f >> q) & 1u) & lt);
-    if (f) {
-      const uint64_t e0 = base + 4ull * (uint64_t)(j * kScanThreads + tid);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if ((f >> q) & 1u) {
-          cidx[pos] = (uint32_t)(e0 + q);
-          cval[pos] = __float_as_uint(f4get(a[j], q));
-          ++pos;
-        }
-      }
-    }
-  }
-  if (tid == 0) P.chunk_count[ch] = sh_tot[128];
-  uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
-  for (int b = tid; b < kH0; b += kScanThreads)
-    if (sh_hist[b]) atomicAdd(&hrow[b], sh_hist[b]);
-}
-
-// ---------------------------------------------------------------- large layers: TMA-pipelined scan
-// Persistent CTAs (2 per SM) stream their chunks through a 3-stage shared-memory ring filled by
-// 1-D bulk tensor copies (cp.async.bulk, completion on an mbarrier with expect_tx), so the next
-// sub-tiles are already in flight while the current one is added, stored and compacted.
-constexpr int kSub = 4096;                  // elements per sub-tile (16 KB per operand)
-constexpr int kStages = 3;
-constexpr int kSlotsPerThread = kSub / 4 / kScanThreads;   // 2 float4 slots per thread per sub-tile
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "LD_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra LD_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(0x12F0000000000000ull)  // evict_first
-      : "memory");
-}
-
-struct SubTile {
-  int ch;          // chunk id (-1: none)
-  int sub;         // sub-tile within the chunk
-};
-
-__device__ __forceinline__ bool next_sub(const DevPlan& P, SubTile& s) {
-  // advance (ch, sub) over this CTA's chunks: ch = blockIdx.x + i * gridDim.x
-  const uint64_t span = P.chunk_hi[s.ch] - P.chunk_base[s.ch];
-  if ((uint64_t)(s.sub + 1) * kSub < span) { ++s.sub; return true; }
-  s.ch += gridDim.x;
-  s.sub = 0;
-  return s.ch < P.n_chunks;
-}
-
-// issue the bulk copies of one sub-tile into stage st (thread 0 only)
-template <bool EF>
-__device__ __forceinline__ void issue_sub(const DevPlan& P, const SubTile& s, int st, float* sg, float* sr,
-                                          uint64_t* full, const float* g, const float* r, uint64_t psi) {
-  const uint64_t sb = P.chunk_base[s.ch] + (uint64_t)s.sub * kSub;
-  const uint64_t se = min(sb + kSub, P.chunk_hi[s.ch]);
-  uint64_t ve = (se + 3) & ~3ull;           // whole float4 slots ...
-  if (ve > psi) ve = psi & ~3ull;           // ... that lie inside the caller's buffer
-  const uint32_t bytes = ve > sb ? (uint32_t)((ve - sb) * 4) : 0u;
-  mbar_arrive_expect_tx(&full[st], bytes * (EF ? 2u : 1u));
-  if (bytes) {
-    bulk_g2s(sg + st * kSub, g + sb, bytes, &full[st]);
-    if (EF) bulk_g2s(sr + st * kSub, r + sb, bytes, &full[st]);
-  }
-}
-
-template <bool EF>
-__global__ void __launch_bounds__(kScanThreads, 2)
-scan_tma_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, uint64_t psi) {
+__global__ void __launch_bounds__(kWsThreads, 2)
+scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, uint64_t psi) {
+  constexpr bool TWO = EF && !REFILL;             // grad and residual both streamed
   extern __shared__ __align__(128) uint8_t dsm[];
-  float* sg = reinterpret_cast<float*>(dsm);                 // [kStages][kSub]
-  float* sr = sg + kStages * kSub;                           // [kStages][kSub] (EF)
-  __shared__ __align__(8) uint64_t full[kStages];
+  float* sA = reinterpret_cast<float*>(dsm);      // [kStages][kSub]  grad (or acc when REFILL)
+  float* sB = sA + kStages * kSub;                // [kStages][kSub]  residual (TWO only)
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t sh_hist[kH0];
-  __shared__ uint32_t sh_tot[2 * (kScanThreads / 32) + 1];
-  __shared__ uint32_t s_run;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if ((int)blockIdx.x >= P.n_chunks) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t n_work = REFILL ? P.counters[0] : (uint32_t)P.n_chunks;
+  if (blockIdx.x >= n_work) return;
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], kWsWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int b = tid; b < kH0; b += kScanThreads) sh_hist[b] = 0;
-  if (tid == 0) s_run = 0;
+  for (int b = tid; b < kH0; b += kWsThreads) sh_hist[b] = 0;
   __syncthreads();
-  SubTile prod{(int)blockIdx.x, 0};
-  bool prod_ok = true;
-  if (tid == 0) {
-    for (int st = 0; st < kStages && prod_ok; ++st) {
-      issue_sub<EF>(P, prod, st, sg, sr, full, g, r, psi);
-      prod_ok = next_sub(P, prod);
-    }
-  }
-  SubTile cur{(int)blockIdx.x, 0};
-  int stage = 0;
-  uint32_t phase = 0;
-  const unsigned lt = (1u << lane) - 1u;
-  for (;;) {
-    bool bad = false;
-    const int ch = cur.ch;
-    const int slot = P.chunk_slot[ch];
-    const uint64_t lo = P.chunk_lo[ch], hi = P.chunk_hi[ch];
-    const uint64_t sb = P.chunk_base[ch] + (uint64_t)cur.sub * kSub;
-    const uint32_t thr = P.thr[slot];
-    mbar_wait(&full[stage], phase);
-    const float* tg = sg + stage * kSub;
-    const float* tr = sr + stage * kSub;
-    float4 a[kSlotsPerThread];
-    uint32_t f[kSlotsPerThread];
-#pragma unroll
-    for (int j = 0; j < kSlotsPerThread; ++j) {
-      const int q = j * kScanThreads + tid;
-      const uint64_t e0 = sb + 4ull * q;
-      uint32_t vm = 0;
-      if (e0 >= lo && e0 + 4 <= hi) vm = 0xF;
-      else if (e0 + 4 > lo && e0 < hi)
-        for (int k = 0; k < 4; ++k) vm |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
-      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (vm) {
-        if (e0 + 4 <= psi) {
-          const float4 gv = reinterpret_cast<const float4*>(tg)[q];
-          if (EF) {
-            const float4 rv = reinterpret_cast<const float4*>(tr)[q];
-            x = make_float4(__fadd_rn(rv.x, gv.x), __fadd_rn(rv.y, gv.y), __fadd_rn(rv.z, gv.z), __fadd_rn(rv.w, gv.w));
-          } else {
-            x = gv;
+  const float* srcA = REFILL ? (EF ? r : g) : g;
+
+  if (warp == kWsWarps) {   // ------------------------------------------------ producer warp
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (uint32_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int ch = REFILL ? (int)P.refill_list[w] : (int)w;
+        const uint64_t hi = P.chunk_hi[ch];
+        for (uint64_t sb = P.chunk_base[ch]; sb < hi; sb += kSub, ++it) {
+          const int st = (int)(it % kStages);
+          mbar_wait(&empty[st], ((it / kStages) & 1u) ^ 1u);
+          uint64_t ve = (min(sb + kSub, hi) + 3) & ~3ull;   // whole float4 slots ...
+          if (ve > psi) ve = psi & ~3ull;                     // ... inside the caller's buffer
+          const uint32_t bytes = ve > sb ? (uint32_t)((ve - sb) * 4) : 0u;
+          mbar_arrive_expect_tx(&full[st], bytes * (TWO ? 2u : 1u));
+          if (bytes) {
+            bulk_g2s(sA + st * kSub, srcA + sb, bytes, &full[st]);
+            if (TWO) bulk_g2s(sB + st * kSub, r + sb, bytes, &full[st]);
           }
-        } else {   // the last partial float4 of the buffer was not bulk-copied
-          for (int k = 0; k < 4; ++k)
-            if ((vm >> k) & 1u) f4set(x, k, EF ? __fadd_rn(r[e0 + k], g[e0 + k]) : g[e0 + k]);
         }
-        if (EF) {
-          if (vm == 0xF) st_stream(r + e0, x);
-          else
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------------- compute warps
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t it = 0;
+  int cur_slot = -1;
+  uint32_t thr = 0;
+  for (uint32_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const int ch = REFILL ? (int)P.refill_list[w] : (int)w;
+    const int slot = P.chunk_slot[ch];
+    if (slot != cur_slot) {   // flush the digit-0 histogram of the previous layer
+      if (cur_slot >= 0) {
+        compute_bar();
+        uint32_t* hrow = P.hist + (uint64_t)cur_slot * kHistRow;
+        for (int b = tid; b < kH0; b += kWsWarps * 32) {
+          const uint32_t h = sh_hist[b];
+          if (h) { atomicAdd(&hrow[b], h); sh_hist[b] = 0; }
+        }
+        compute_bar();
+      }
+      cur_slot = slot;
+      thr = REFILL ? 0u : P.thr[slot];
+    }
+    const uint64_t lo = P.chunk_lo[ch], hi = P.chunk_hi[ch];
+    uint16_t* segc = P.seg_count + (uint64_t)ch * kSegsPerChunk;
+    int sub = 0;
+    for (uint64_t sb = P.chunk_base[ch]; sb < hi; sb += kSub, ++it, ++sub) {
+      const int st = (int)(it % kStages);
+      mbar_wait(&full[st], (it / kStages) & 1u);
+      const float4* tA = reinterpret_cast<const float4*>(sA + st * kSub);
+      const float4* tB = reinterpret_cast<const float4*>(sB + st * kSub);
+      float4 a[2];
+      uint32_t f[2];
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int q = warp * (kSeg / 4) + j * 32 + lane;   // float4 slot inside the sub-tile
+        const uint64_t e0 = sb + 4ull * q;
+        uint32_t vm = 0;
+        if (e0 >= lo && e0 + 4 <= hi) vm = 0xF;
+        else if (e0 + 4 > lo && e0 < hi)
+          for (int k = 0; k < 4; ++k) vm |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (vm) {
+          if (e0 + 4 <= psi) {
+            const float4 av = tA[q];
+            if (TWO) {
+              const float4 rv = tB[q];
+              x = make_float4(__fadd_rn(rv.x, av.x), __fadd_rn(rv.y, av.y), __fadd_rn(rv.z, av.z),
+                              __fadd_rn(rv.w, av.w));
+            } else {
+              x = av;
+            }
+          } else {   // the buffer's last partial float4 was not bulk-copied
             for (int k = 0; k < 4; ++k)
-              if ((vm >> k) & 1u) r[e0 + k] = f4get(x, k);
+              if ((vm >> k) & 1u) {
+                float y;
+                if (REFILL) y = EF ? r[e0 + k] : g[e0 + k];
+                else y = EF ? __fadd_rn(r[e0 + k], g[e0 + k]) : g[e0 + k];
+                f4set(x, k, y);
+              }
+          }
+          if (TWO) {
+            if (vm == 0xF) st_stream(r + e0, x);
+            else
+              for (int k = 0; k < 4; ++k)
+                if ((vm >> k) & 1u) r[e0 + k] = f4get(x, k);
+          }
         }
+        uint32_t fl = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t key = key_of(f4get(x, k));
+          const bool v = (vm >> k) & 1u;
+          bad |= v && key >= 0x7F800000u;
+          if (v && key >= thr) { fl |= 1u << k; atomicAdd(&sh_hist[key >> 20], 1u); }
+        }
+        f[j] = fl;
+        a[j] = x;
       }
-      uint32_t fl = 0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done with the stage
+      if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
+      // ordered compaction of the warp's segment: elements in (j, lane, k) order = index order
+      const int seg = sub * kWsWarps + warp;
+      uint32_t* cidx = P.cand_idx + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
+      uint32_t* cval = P.cand_val + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
+      uint32_t run = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t key = key_of(f4get(x, k));
-        const bool v = (vm >> k) & 1u;
-        bad |= v && key >= 0x7F800000u;
-        if (v && key >= thr) { fl |= 1u << k; atomicAdd(&sh_hist[key >> 20], 1u); }
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t fl = f[j];
+        unsigned bm[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bm[k] = __ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u);
+        uint32_t pos = run;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pos += __popc(bm[k] & lt);
+        if (fl) {
+          const uint64_t e0 = sb + 4ull * (warp * (kSeg / 4) + j * 32 + lane);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if ((fl >> k) & 1u) { cidx[pos] = (uint32_t)(e0 + k); cval[pos] = __float_as_uint(f4get(a[j], k)); ++pos; }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) run += __popc(bm[k]);
       }
-      f[j] = fl;
-      a[j] = x;
-      uint32_t tot = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) tot += __popc(__ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u));
-      if (lane == 0) sh_tot[j * (kScanThreads / 32) + warp] = tot;
+      if (lane == 0) segc[seg] = (uint16_t)run;
     }
-    if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
-    __syncthreads();   // sh_tot complete; every thread is done reading this stage
-    if (tid == 0 && prod_ok) {   // refill the stage just consumed
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_sub<EF>(P, prod, stage, sg, sr, full, g, r, psi);
-      prod_ok = next_sub(P, prod);
-    }
-    if (warp == 0) {
-      const int nseg = kSlotsPerThread * (kScanThreads / 32);   // 32 segments: one per lane
-      uint32_t v = lane < nseg ? sh_tot[lane] : 0u, inc = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      const uint32_t base = s_run;
-      if (lane < nseg) sh_tot[lane] = base + inc - v;
-      if (lane == 31) sh_tot[nseg] = base + inc;
-    }
-    __syncthreads();
-    uint32_t* cidx = P.cand_idx + (uint64_t)ch * kChunk;
-    uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
-#pragma unroll
-    for (int j = 0; j < kSlotsPerThread; ++j) {
-      const uint32_t fl = f[j];
-      uint32_t pos = sh_tot[j * (kScanThreads / 32) + warp];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) pos += __popc(__ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u) & lt);
-      if (fl) {
-        const uint64_t e0 = sb + 4ull * (j * kScanThreads + tid);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if ((fl >> k) & 1u) { cidx[pos] = (uint32_t)(e0 + k); cval[pos] = __float_as_uint(f4get(a[j], k)); ++pos; }
-      }
-    }
-    if (tid == 0) s_run = sh_tot[kSlotsPerThread * (kScanThreads / 32)];
-    if (++stage == kStages) { stage = 0; phase ^= 1u; }
-    const bool last_sub = (uint64_t)(cur.sub + 1) * kSub >= hi - P.chunk_base[ch];
-    if (last_sub) {
-      __syncthreads();   // s_run final, histogram complete
-      if (tid == 0) P.chunk_count[ch] = s_run;
-      uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
-      for (int b = tid; b < kH0; b += kScanThreads) {
-        const uint32_t h = sh_hist[b];
-        if (h) { atomicAdd(&hrow[b], h); sh_hist[b] = 0; }
-      }
-      if (tid == 0) s_run = 0;
-    }
-    __syncthreads();
-    if (!next_sub(P, cur)) break;
+    if (lane == 0)
+      for (int s2 = sub; s2 < kSegsPerChunk / kWsWarps; ++s2) segc[s2 * kWsWarps + warp] = 0;
+  }
+  if (cur_slot >= 0) {
+    compute_bar();
+    uint32_t* hrow = P.hist + (uint64_t)cur_slot * kHistRow;
+    for (int b = tid; b < kH0; b += kWsWarps * 32)
+      if (sh_hist[b]) atomicAdd(&hrow[b], sh_hist[b]);
   }
 }
 
-template <bool EF>
-__global__ void __launch_bounds__(kScanThreads, 2)
-scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
-  __shared__ uint32_t sh_hist[kH0];
-  __shared__ uint32_t sh_tot[8 * (kScanThreads / 32) + 1];
-  scan_chunk<EF, false>(P, blockIdx.x, g, r, sh_hist, sh_tot);
-}
-
-template <bool EF>
-__global__ void __launch_bounds__(kScanThreads, 2)
-rescan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
-  __shared__ uint32_t sh_hist[kH0];
-  __shared__ uint32_t sh_tot[8 * (kScanThreads / 32) + 1];
-  const uint32_t n = P.counters[0];
-  for (uint32_t w = blockIdx.x; w < n; w += gridDim.x) {
-    scan_chunk<EF, true>(P, (int)P.refill_list[w], g, r, sh_hist, sh_tot);
-    __syncthreads();
-  }
+// per chunk: candidate total (sum of its 64 segment counts); warp per chunk
+__global__ void chunk_total_kernel(DevPlan P) {
+  __shared__ uint32_t so_all[8][kSegsPerChunk + 1];
+  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ch >= P.n_chunks) return;
+  const uint32_t tot = warp_load_segs(P, ch, so_all[threadIdx.x >> 5]);
+  if ((threadIdx.x & 31) == 0) P.chunk_count[ch] = tot;
 }
 
 // ---------------------------------------------------------------- per-layer plan / digit search
 // mode 0: after scan -- decide hit/refill, find digit 0 for hits, queue refills
 // mode 1: after rescan -- find digit 0 for refilled layers
-// mode 2/3: find digit 1/2 for every large layer
+// mode 2/3: find digit 1/2 for every large layer (mode 2 also predicts the next band)
 __global__ void find_kernel(DevPlan P, int mode) {
   const int slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -625,55 +511,52 @@ __global__ void find_kernel(DevPlan P, int mode) {
 
 // digit d (1 or 2) histogram over candidates matching the prefix: warp per chunk
 __global__ void digit_kernel(DevPlan P, int d) {
+  __shared__ uint32_t so_all[8][kSegsPerChunk + 1];
   const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ch >= P.n_chunks) return;
+  uint32_t* so = so_all[threadIdx.x >> 5];
   const int shift = d == 1 ? 9 : 0;
   const int hs = d == 1 ? 20 : 9;
   const uint32_t mask = d == 1 ? 0x7FFu : 0x1FFu;
-  const int hoff = d == 1 ? kH0 : kH0 + kH1;
-  for (int ch = gw; ch < P.n_chunks; ch += nwarps) {
-    const int slot = P.chunk_slot[ch];
-    const uint32_t pre = P.sel[slot].prefix;
-    const uint32_t cnt = P.chunk_count[ch];
-    const uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
-    uint32_t* h = P.hist + (uint64_t)slot * kHistRow + hoff;
-    for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const uint32_t key = i < cnt ? cval[i] & 0x7FFFFFFFu : 0u;
-      const bool m = i < cnt && (key >> hs) == pre;
-      const unsigned act = __ballot_sync(0xFFFFFFFFu, m);
-      if (m) {
-        const uint32_t bin = (key >> shift) & mask;
-        const unsigned peers = __match_any_sync(act, bin);
-        if (lane == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
-      }
+  const int slot = P.chunk_slot[ch];
+  const uint32_t pre = P.sel[slot].prefix;
+  uint32_t* h = P.hist + (uint64_t)slot * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
+  const uint32_t cnt = warp_load_segs(P, ch, so);
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t key = i < cnt ? P.cand_val[seg_addr(ch, so, i)] & 0x7FFFFFFFu : 0u;
+    const bool m = i < cnt && (key >> hs) == pre;
+    const unsigned act = __ballot_sync(0xFFFFFFFFu, m);
+    if (m) {
+      const uint32_t bin = (key >> shift) & mask;
+      const unsigned peers = __match_any_sync(act, bin);
+      if (lane == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
     }
   }
 }
 
 // per chunk: #(key > T) and #(key == T)
 __global__ void count_kernel(DevPlan P) {
+  __shared__ uint32_t so_all[8][kSegsPerChunk + 1];
   const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int ch = gw; ch < P.n_chunks; ch += nwarps) {
-    const uint32_t T = P.sel[P.chunk_slot[ch]].prefix;
-    const uint32_t cnt = P.chunk_count[ch];
-    const uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
-    uint32_t gt = 0, eq = 0;
-    for (uint32_t i = lane; i < cnt; i += 32) {
-      const uint32_t key = cval[i] & 0x7FFFFFFFu;
-      gt += key > T;
-      eq += key == T;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      gt += __shfl_xor_sync(0xFFFFFFFFu, gt, o);
-      eq += __shfl_xor_sync(0xFFFFFFFFu, eq, o);
-    }
-    if (lane == 0) { P.chunk_gt[ch] = gt; P.chunk_eq[ch] = eq; }
+  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ch >= P.n_chunks) return;
+  uint32_t* so = so_all[threadIdx.x >> 5];
+  const uint32_t T = P.sel[P.chunk_slot[ch]].prefix;
+  const uint32_t cnt = warp_load_segs(P, ch, so);
+  uint32_t gt = 0, eq = 0;
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const uint32_t key = P.cand_val[seg_addr(ch, so, i)] & 0x7FFFFFFFu;
+    gt += key > T;
+    eq += key == T;
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    gt += __shfl_xor_sync(0xFFFFFFFFu, gt, o);
+    eq += __shfl_xor_sync(0xFFFFFFFFu, eq, o);
+  }
+  if (lane == 0) { P.chunk_gt[ch] = gt; P.chunk_eq[ch] = eq; }
 }
 
 // per large layer (one CTA): exclusive scans over its chunks; next speculative threshold
@@ -696,7 +579,7 @@ __global__ void __launch_bounds__(256) layer_scan_kernel(DevPlan P) {
     if (c < c1) { P.chunk_out[c] = ob; P.chunk_take[c] = take; }
   }
   if (threadIdx.x == 0) {
-    // speculative band for the next call (DESIGN.md "speculation"), never above this call's T
+    // speculative band for the next call (DESIGN.md §4.1), never above this call's T
     const uint32_t nt = P.sel[slot].next_thr;
     P.thr[slot] = nt <= T ? nt : T;
   }
@@ -705,38 +588,37 @@ __global__ void __launch_bounds__(256) layer_scan_kernel(DevPlan P) {
 // warp per chunk: ordered emit of the selected candidates, residual' zeroing
 template <bool EF>
 __global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K, float* __restrict__ r) {
+  __shared__ uint32_t so_all[8][kSegsPerChunk + 1];
   const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ch >= P.n_chunks) return;
+  uint32_t* so = so_all[threadIdx.x >> 5];
   const unsigned lt = (1u << lane) - 1u;
-  for (int ch = gw; ch < P.n_chunks; ch += nwarps) {
-    const int slot = P.chunk_slot[ch];
-    const uint32_t T = P.sel[slot].prefix;
-    const uint32_t take = P.chunk_take[ch];
-    const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + P.chunk_out[ch];
-    const uint32_t cnt = P.chunk_count[ch];
-    const uint32_t* cidx = P.cand_idx + (uint64_t)ch * kChunk;
-    const uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
-    uint32_t eq_run = 0, out_run = 0;
-    for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const bool v = i < cnt;
-      const uint32_t val = v ? cval[i] : 0u;
-      const uint32_t key = val & 0x7FFFFFFFu;
-      const bool is_eq = v && key == T;
-      const unsigned eqm = __ballot_sync(0xFFFFFFFFu, is_eq);
-      const bool sel = v && (key > T || (is_eq && eq_run + __popc(eqm & lt) < take));
-      const unsigned sm = __ballot_sync(0xFFFFFFFFu, sel);
-      if (sel) {
-        const uint32_t idx = cidx[i];
-        const uint64_t o = dst0 + out_run + __popc(sm & lt);
-        send[o] = idx;
-        send[K + o] = val;
-        if (EF) r[idx] = 0.0f;
-      }
-      eq_run += __popc(eqm);
-      out_run += __popc(sm);
+  const int slot = P.chunk_slot[ch];
+  const uint32_t T = P.sel[slot].prefix;
+  const uint32_t take = P.chunk_take[ch];
+  const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + P.chunk_out[ch];
+  const uint32_t cnt = warp_load_segs(P, ch, so);
+  uint32_t eq_run = 0, out_run = 0;
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const bool v = i < cnt;
+    const uint64_t a = v ? seg_addr(ch, so, i) : 0;
+    const uint32_t val = v ? P.cand_val[a] : 0u;
+    const uint32_t idx = v ? P.cand_idx[a] : 0u;
+    const uint32_t key = val & 0x7FFFFFFFu;
+    const bool is_eq = v && key == T;
+    const unsigned eqm = __ballot_sync(0xFFFFFFFFu, is_eq);
+    const bool sel = v && (key > T || (is_eq && eq_run + __popc(eqm & lt) < take));
+    const unsigned sm = __ballot_sync(0xFFFFFFFFu, sel);
+    if (sel) {
+      const uint64_t o = dst0 + out_run + __popc(sm & lt);
+      send[o] = idx;
+      send[K + o] = val;
+      if (EF) r[idx] = 0.0f;
     }
+    eq_run += __popc(eqm);
+    out_run += __popc(sm);
   }
 }
 
@@ -749,6 +631,19 @@ int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+template <bool EF, bool REFILL>
+cudaError_t launch_scan(const DevPlan& P, int grid, const float* g, float* r, uint64_t psi, cudaStream_t s) {
+  static bool attr = false;
+  const size_t smem = (size_t)kStages * kSub * sizeof(float) * 2;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(scan_kernel<EF, REFILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  scan_kernel<EF, REFILL><<<grid, kWsThreads, smem, s>>>(P, g, r, psi);
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -782,41 +677,34 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   e = cudaMemsetAsync(P.counters, 0, 4 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const int sms = num_sms();
-  const int warp_blocks = (P.n_large * 32 + 255) / 256;
-  const int pgrid = (P.n_chunks + 7) / 8;   // one warp per chunk: latency hidden by parallelism
+  const int layer_blocks = (P.n_large * 32 + 255) / 256;     // warp per large layer
+  const int chunk_blocks = (P.n_chunks + 7) / 8;              // warp per chunk
+  const int scan_grid = std::min(P.n_chunks, sms * 2);        // persistent: 2 CTAs per SM
 
-  {
-    static bool tma_attr[2] = {false, false};
-    const size_t smem = (size_t)kStages * kSub * sizeof(float) * (ef ? 2 : 1);
-    if (!tma_attr[ef]) {
-      e = ef ? cudaFuncSetAttribute(scan_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-             : cudaFuncSetAttribute(scan_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      tma_attr[ef] = true;
-    }
-    const int grid = std::min(P.n_chunks, sms * 2);
-    prof_begin(c, "scan", s, &h);
-    if (ef) scan_tma_kernel<true><<<grid, kScanThreads, smem, s>>>(P, grad, residual, (uint64_t)c->psi);
-    else scan_tma_kernel<false><<<grid, kScanThreads, smem, s>>>(P, grad, residual, (uint64_t)c->psi);
-    prof_end(c, h, s);
-  }
+  prof_begin(c, "scan", s, &h);
+  e = ef ? launch_scan<true, false>(P, scan_grid, grad, residual, (uint64_t)c->psi, s)
+         : launch_scan<false, false>(P, scan_grid, grad, residual, (uint64_t)c->psi, s);
+  if (e != cudaSuccess) return e;
+  prof_end(c, h, s);
   prof_begin(c, "select", s, &h);
-  find_kernel<<<warp_blocks, 256, 0, s>>>(P, 0);
-  if (ef) rescan_kernel<true><<<sms * 2, kScanThreads, 0, s>>>(P, grad, residual);
-  else rescan_kernel<false><<<sms * 2, kScanThreads, 0, s>>>(P, grad, residual);
-  find_kernel<<<warp_blocks, 256, 0, s>>>(P, 1);
-  digit_kernel<<<pgrid, 256, 0, s>>>(P, 1);
-  find_kernel<<<warp_blocks, 256, 0, s>>>(P, 2);
-  digit_kernel<<<pgrid, 256, 0, s>>>(P, 2);
-  find_kernel<<<warp_blocks, 256, 0, s>>>(P, 3);
-  count_kernel<<<pgrid, 256, 0, s>>>(P);
+  chunk_total_kernel<<<chunk_blocks, 256, 0, s>>>(P);
+  find_kernel<<<layer_blocks, 256, 0, s>>>(P, 0);
+  e = ef ? launch_scan<true, true>(P, sms * 2, grad, residual, (uint64_t)c->psi, s)
+         : launch_scan<false, true>(P, sms * 2, grad, residual, (uint64_t)c->psi, s);
+  if (e != cudaSuccess) return e;
+  find_kernel<<<layer_blocks, 256, 0, s>>>(P, 1);
+  digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
+  find_kernel<<<layer_blocks, 256, 0, s>>>(P, 2);
+  digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 2);
+  find_kernel<<<layer_blocks, 256, 0, s>>>(P, 3);
+  count_kernel<<<chunk_blocks, 256, 0, s>>>(P);
   layer_scan_kernel<<<P.n_large, 256, 0, s>>>(P);
   prof_end(c, h, s);
   prof_begin(c, "emit", s, &h);
-  if (ef) emit_kernel<true><<<pgrid, 256, 0, s>>>(P, send, (uint64_t)c->K, residual);
-  else emit_kernel<false><<<pgrid, 256, 0, s>>>(P, send, (uint64_t)c->K, residual);
+  if (ef) emit_kernel<true><<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K, residual);
+  else emit_kernel<false><<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K, residual);
   prof_end(c, h, s);
-  c->launches += 11;
+  c->launches += 12;
   return cudaGetLastError();
 }
 

@@ -97,7 +97,7 @@ struct AdamK { float b1, c1, b2, c2, eps; };
 constexpr int kReplayMaxWorld = 8;
 
 template <int OPT, int DIV>
-__global__ void __launch_bounds__(kReplayThreads, 3)
+__global__ void __launch_bounds__(kReplayThreads, 2)
 replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
               const uint32_t* __restrict__ start, int64_t n_tiles, const float* __restrict__ scal,
               AdamK ak, uint64_t psi, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v) {
@@ -202,29 +202,51 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       na = __ldg(st2);
       nb = __ldg(st2 + 1);
     }
+    float gx[8];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const float4 gv = G4[tid + kReplayThreads * i];
+      gx[4 * i + 0] = mean_of<DIV>(gv.x, n, inv);
+      gx[4 * i + 1] = mean_of<DIV>(gv.y, n, inv);
+      gx[4 * i + 2] = mean_of<DIV>(gv.z, n, inv);
+      gx[4 * i + 3] = mean_of<DIV>(gv.w, n, inv);
+    }
+    if (OPT == LOWDIFF_ADAM) {
+      // m = b1*m + c1*g ; v = b2*v + c2*(g*g) ; mh = m*r1 ; vh = v*r2
+      // d = sqrt(vh) + eps ; u = mh / d ; p = p - lr*u          (R-11)
+      // The 8 elements are computed as independent straight-line chains (ILP); the correctly
+      // rounded sqrt / divide take the exact fast sequence (ieee_fast.cuh) for every lane and a
+      // warp-rare fix-up pass redoes out-of-window operands with the intrinsics.
+      float mh[8], vh[8], d[8], u[8];
+      uint32_t slow = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float g = mean_of<DIV>(q == 0 ? gv.x : q == 1 ? gv.y : q == 2 ? gv.z : gv.w, n, inv);
-        const int x = 4 * i + q;
-        if (OPT == LOWDIFF_ADAM) {
-          // m = b1*m + c1*g ; v = b2*v + c2*(g*g) ; mh = m*r1 ; vh = v*r2
-          // d = sqrt(vh) + eps ; u = mh / d ; p = p - lr*u          (R-11)
-          M[x] = __fadd_rn(__fmul_rn(ak.b1, M[x]), __fmul_rn(ak.c1, g));
-          V[x] = __fadd_rn(__fmul_rn(ak.b2, V[x]), __fmul_rn(ak.c2, __fmul_rn(g, g)));
-          const float mh = __fmul_rn(M[x], sr1);
-          const float vh = __fmul_rn(V[x], sr2);
-          // branch-free correctly rounded sqrt / divide (ieee_fast.cuh): bit-identical to
-          // __fsqrt_rn / __fdiv_rn without the per-lane divergence of their slow-path guards
-          const float d = __fadd_rn(sqrt_rn_nb(vh), ak.eps);
-          const float u = div_rn_nb(mh, d);
-          P[x] = __fsub_rn(P[x], __fmul_rn(slr, u));
-        } else {
-          P[x] = __fsub_rn(P[x], __fmul_rn(slr, g));
+      for (int x = 0; x < 8; ++x) {
+        M[x] = __fadd_rn(__fmul_rn(ak.b1, M[x]), __fmul_rn(ak.c1, gx[x]));
+        V[x] = __fadd_rn(__fmul_rn(ak.b2, V[x]), __fmul_rn(ak.c2, __fmul_rn(gx[x], gx[x])));
+        mh[x] = __fmul_rn(M[x], sr1);
+        vh[x] = __fmul_rn(V[x], sr2);
+        bool sl;
+        d[x] = __fadd_rn(sqrt_rn_fast(vh[x], &sl), ak.eps);
+        slow |= (uint32_t)sl << x;
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        bool sl;
+        u[x] = div_rn_fast(mh[x], d[x], &sl);
+        slow |= (uint32_t)sl << (8 + x);
+      }
+      if (slow) {   // static indices keep mh/vh/d/u in registers
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          if ((slow >> x) & 1u) d[x] = __fadd_rn(__fsqrt_rn(vh[x]), ak.eps);
+          if ((slow >> x) & 0x101u) u[x] = __fdiv_rn(mh[x], d[x]);
         }
       }
+#pragma unroll
+      for (int x = 0; x < 8; ++x) P[x] = __fsub_rn(P[x], __fmul_rn(slr, u[x]));
+    } else {
+#pragma unroll
+      for (int x = 0; x < 8; ++x) P[x] = __fsub_rn(P[x], __fmul_rn(slr, gx[x]));
     }
     if (ranger) { s_a[cur][tid] = na; s_b[cur][tid] = nb; }   // ranges of step s+2
     __syncthreads();
