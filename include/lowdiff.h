@@ -189,6 +189,7 @@ typedef struct {
   int64_t ring_stall_ns;       /* host time lowdiff_batch_persist spent blocked on a full ring */
   int64_t writer_busy_ns;      /* writer thread time spent building + writing files            */
   int64_t spec_hits, spec_misses;   /* large layers selected from the speculative band / refilled */
+  int64_t spec_candidates;          /* candidates the band admitted in those hit layers (last call) */
 } lowdiff_stats;
 lowdiff_status lowdiff_get_stats(const lowdiff_ctx *ctx, lowdiff_stats *out);
 

@@ -144,6 +144,7 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   P.chunk_out = P.chunk_eq + nc; P.chunk_take = P.chunk_out + nc; P.refill_list = P.chunk_take + nc;
   if ((st = dalloc(c, nl * (2048 + 2048 + 512) * 4, &p))) return st; P.hist = (uint32_t*)p;
   if ((st = dalloc(c, nl * sizeof(ld::LayerSel), &p))) return st; P.sel = (ld::LayerSel*)p;
+  CK(cudaMemset(P.sel, 0, nl * sizeof(ld::LayerSel)));   // band = 0: not yet adapted
   if ((st = dalloc(c, nl * 4, &p))) return st; P.thr = (uint32_t*)p;
   CK(cudaMemset(P.thr, 0xFF, nl * 4));   // no speculative band before the first call
   if ((st = dalloc(c, 8 * 4, &p))) return st; P.counters = (uint32_t*)p;
@@ -913,11 +914,12 @@ lowdiff_status lowdiff_get_stats(const lowdiff_ctx* c, lowdiff_stats* out) {
   out->ring_stall_ns = c->stall_ns;
   out->writer_busy_ns = c->writer_ns;
   uint32_t cnt[4] = {0, 0, 0, 0};
-  if (cudaMemcpy(cnt, c->plan.counters, 12, cudaMemcpyDeviceToHost) == cudaSuccess) {
+  if (cudaMemcpy(cnt, c->plan.counters, 16, cudaMemcpyDeviceToHost) == cudaSuccess) {
     out->spec_hits = cnt[1];
     out->spec_misses = cnt[2];
+    out->spec_candidates = cnt[3];
   } else {
-    out->spec_hits = out->spec_misses = -1;
+    out->spec_hits = out->spec_misses = out->spec_candidates = -1;
   }
   return LOWDIFF_OK;
 }

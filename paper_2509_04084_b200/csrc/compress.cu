@@ -463,7 +463,16 @@ __global__ void find_kernel(DevPlan P, int mode) {
     if (tot >= k) {
       uint32_t bin, above;
       warp_find_bin(hrow, kH0, k, &bin, &above);
-      if (lane == 0) { S.prefix = bin; S.kleft = k - above; S.total = tot; S.refill = 0; atomicAdd(&P.counters[1], 1u); }
+      if (lane == 0) {
+        S.prefix = bin; S.kleft = k - above; S.total = tot; S.refill = 0;
+        // adapt the band: the previous call chose it to admit `band` x k keys of ITS distribution;
+        // under error feedback the accumulated values drift upward between calls, so the band
+        // admitted tot / k x k now.  Aim the next band at 1.5 k_l admitted.
+        const float b = S.band > 0.f ? S.band : 1.5f;
+        S.band = fminf(4.f, fmaxf(1.02f, b * 1.5f * (float)k / (float)tot));
+        atomicAdd(&P.counters[1], 1u);
+        atomicAdd(&P.counters[3], tot);
+      }
     } else {
       for (int b = lane; b < kH0; b += 32) hrow[b] = 0;
       uint32_t base = 0;
@@ -471,6 +480,7 @@ __global__ void find_kernel(DevPlan P, int mode) {
         base = atomicAdd(&P.counters[0], (uint32_t)(c1 - c0));
         S.refill = 1;
         S.total = (uint32_t)(P.layer_off[li + 1] - P.layer_off[li]);
+        S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : 1.5f;   // missed: widen
         atomicAdd(&P.counters[2], 1u);
       }
       base = __shfl_sync(0xFFFFFFFFu, base, 0);
@@ -487,10 +497,11 @@ __global__ void find_kernel(DevPlan P, int mode) {
     uint32_t bin, above;
     warp_find_bin(h, nb, S.kleft, &bin, &above);
     if (mode == 2) {
-      // Speculative band for the next call: the key with C = 1.5 k_l candidate keys at or above it
-      // (digit-0 resolution, refined with the digit-1 histogram when C falls in T's digit-0 bin).
-      // Only a prediction -- the next call checks #candidates >= k_l and refills otherwise.
-      const uint32_t C = k + max(k / 2, 32u);
+      // Speculative band for the next call: the key with C = band x k_l candidate keys at or above
+      // it (digit-0 resolution, refined with the digit-1 histogram when C falls in T's digit-0
+      // bin).  Only a prediction -- the next call checks #candidates >= k_l and refills otherwise.
+      const float band = S.band > 0.f ? S.band : 1.5f;
+      const uint32_t C = max(k + 32u, (uint32_t)fminf((float)k * band, 4.0e9f));
       uint32_t nt = P.thr[slot];
       if (S.total >= C) {
         uint32_t b0, a0;

@@ -37,8 +37,9 @@ struct LayerSel {
   uint32_t kleft;    // entries still to take among those matching prefix
   uint32_t total;    // candidate count
   uint32_t refill;   // 1: speculative band too narrow, whole layer became candidates
-  uint32_t next_thr; // speculative band for the next call (key with ~1.5 k_l keys above it)
-  uint32_t pad[3];
+  uint32_t next_thr; // speculative band for the next call
+  float band;        // band width as a multiple of k_l in this call's distribution (adaptive; 0 = unset)
+  uint32_t pad[2];
 };
 
 struct DevPlan {

@@ -48,7 +48,8 @@ class Config(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("files_written", C.c_int64), ("bytes_written", C.c_int64), ("ring_stall_ns", C.c_int64),
-                ("writer_busy_ns", C.c_int64), ("spec_hits", C.c_int64), ("spec_misses", C.c_int64)]
+                ("writer_busy_ns", C.c_int64), ("spec_hits", C.c_int64), ("spec_misses", C.c_int64),
+                ("spec_candidates", C.c_int64)]
 
 
 _lib = None
