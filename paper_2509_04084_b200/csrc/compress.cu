@@ -8,26 +8,25 @@
 // How:
 //   small layers (n <= 16384): one CTA per layer, acc staged in shared memory, 3-digit MSB
 //     radix select (11/11/9 key bits) with shared-memory histograms, ordered emit by block scan.
-//   large layers: 16384-element chunks, each cut into four 4096-element sub-tiles and 64
-//     "segments" of 256 elements (one per compute warp per sub-tile).
-//     scan:    warp-specialised persistent kernel.  A producer warp streams grad and residual
-//              sub-tiles into a 3-stage shared-memory ring with 1-D bulk copies
-//              (cp.async.bulk + mbarrier expect_tx); 16 compute warps add them (EF), store
-//              residual' = acc with 128-bit stores, and compact the candidates key >= tau_l of
-//              their segment in index order with warp ballots -- no block-wide barrier on the
-//              hot path (segments are independent; their counts go to a table).  tau_l is the
-//              speculative band predicted by the previous call; the first radix digit of the
-//              candidates is histogrammed in shared memory on the fly.
+//   large layers: 16384-element chunks = 64 segments of 256 elements.
+//     scan:    a full-grid streaming kernel (one warp per segment, 2 x 128-bit loads of grad and
+//              of residual per lane, 128-bit store of residual' = acc): the pattern measured at
+//              ~7.1 TB/s for 2 reads + 1 write on this GPU (tools/stream_probe.cu).  Each warp
+//              compacts its segment's candidates key >= tau_l in index order with ballots; no
+//              shared memory, no barriers.  tau_l is the speculative band predicted by the
+//              previous call.
+//     prep:    warp per chunk: compacts the 64 segment lists in place into one index-ordered
+//              chunk list, counts it, and histograms the first radix digit (key bits [30:20]).
 //     plan:    per layer, if #candidates >= k_l the exact top-k lies inside the candidates
-//              (speculation hit); otherwise the layer is "refilled": the same scan kernel
-//              re-reads acc with tau = 0, so every element becomes a candidate.  Exactness
-//              never depends on the prediction.
-//     digits:  two more radix digits over the (small) candidate lists -> exact k-th key T and
-//              the number of ties at T to take (lowest indices first).
+//              (speculation hit); otherwise the layer is "refilled": the scan re-reads acc with
+//              tau = 0 so every element becomes a candidate.  Exactness never depends on the
+//              prediction.
+//     digits:  two more radix digits over the candidate lists -> exact k-th key T and the number
+//              of ties at T to take (lowest indices first).
 //     count / layer scan / emit: per-chunk counts of key > T and key == T, per-layer exclusive
 //              scans, then a warp per chunk writes its selected entries at their final position
-//              (index order = chunk, segment, in-segment order) and zeroes residual' there.
-//   HBM traffic in the steady state: 12 B/param (+ ~0.2 B/param of candidates) + 8 B/entry.
+//              and zeroes residual' there.
+//   HBM traffic in the steady state: 12 B/param + ~16 B per candidate (~1.5-2.5 k) + 8 B/entry.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,18 +38,10 @@ namespace {
 
 constexpr int kH0 = 2048, kH1 = 2048, kH2 = 512;   // digit sizes: key bits [30:20] [19:9] [8:0]
 constexpr int kHistRow = kH0 + kH1 + kH2;
+constexpr int kScanWarps = 4;                       // segments per scan CTA
+constexpr int kPiecesPerChunk = kSegsPerChunk / kScanWarps;   // 16 scan CTAs per chunk
+constexpr int kUnroll = 4;                          // candidate rounds in flight per warp
 
-constexpr int kSub = 4096;                          // elements per sub-tile (16 KB per operand)
-constexpr int kWsWarps = 16;                        // compute warps of the scan kernel
-constexpr int kWsThreads = (kWsWarps + 1) * 32;     // + one producer warp
-constexpr int kStages = 3;                          // shared-memory ring depth
-static_assert(kSub / kWsWarps == kSeg, "one segment per compute warp per sub-tile");
-static_assert(kChunk / kSeg == kSegsPerChunk, "segment table shape");
-
-__device__ __forceinline__ void st_stream(float* p, float4 v) {
-  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
-               :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
-}
 __device__ __forceinline__ float f4get(const float4& v, int q) {
   return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
 }
@@ -58,39 +49,6 @@ __device__ __forceinline__ void f4set(float4& v, int q, float x) {
   if (q == 0) v.x = x; else if (q == 1) v.y = x; else if (q == 2) v.z = x; else v.w = x;
 }
 __device__ __forceinline__ uint32_t key_of(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "LD_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra LD_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// 1-D bulk copy global -> shared, completion counted on an mbarrier; L2 evict_first (streamed once)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(0x12F0000000000000ull)
-      : "memory");
-}
-__device__ __forceinline__ void compute_bar() {   // named barrier over the 16 compute warps only
-  asm volatile("bar.sync 1, %0;" ::"n"(kWsWarps * 32) : "memory");
-}
 
 // Warp-cooperative search of the radix bin that holds the kleft-th largest key among the
 // entries counted in h[0..nb) (bins ordered by key).  Returns the bin and the number of
@@ -154,35 +112,13 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* sh32, 
   return r;
 }
 
-// ---------------------------------------------------------------- segment tables
-// The candidates of chunk ch live in 64 segments of 256 slots; segment s holds its cnt[s]
-// candidates, index-ascending, at cand[(ch*64 + s)*256 ...].  A warp loads the 64 counts,
-// scans them into so[0..64] (so[64] = chunk total) and addresses candidate c of the chunk as
-// segment s = max{s : so[s] <= c}, slot c - so[s].
-__device__ __forceinline__ uint32_t warp_load_segs(const DevPlan& P, int ch, uint32_t* so) {
-  const int lane = threadIdx.x & 31;
-  const uint16_t* cnt = P.seg_count + (uint64_t)ch * kSegsPerChunk;
-  const uint32_t c0 = cnt[lane], c1 = cnt[32 + lane];
-  uint32_t i0 = c0, i1 = c1;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y0 = __shfl_up_sync(0xFFFFFFFFu, i0, o), y1 = __shfl_up_sync(0xFFFFFFFFu, i1, o);
-    if (lane >= o) { i0 += y0; i1 += y1; }
+// warp-aggregated histogram increment: lanes with m set add 1 to h[bin]
+__device__ __forceinline__ void warp_hist_add(uint32_t* h, bool m, uint32_t bin) {
+  const unsigned act = __ballot_sync(0xFFFFFFFFu, m);
+  if (m) {
+    const unsigned peers = __match_any_sync(act, bin);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
   }
-  const uint32_t t0 = __shfl_sync(0xFFFFFFFFu, i0, 31);
-  so[lane] = i0 - c0;
-  so[32 + lane] = t0 + i1 - c1;
-  const uint32_t total = t0 + __shfl_sync(0xFFFFFFFFu, i1, 31);
-  if (lane == 0) so[64] = total;
-  __syncwarp();
-  return total;
-}
-__device__ __forceinline__ uint64_t seg_addr(int ch, const uint32_t* so, uint32_t c) {
-  int s = 0;
-#pragma unroll
-  for (int step = 32; step; step >>= 1)
-    if (so[s + step] <= c) s += step;
-  return ((uint64_t)ch * kSegsPerChunk + s) * kSeg + (c - so[s]);
 }
 
 // ---------------------------------------------------------------- small layers
@@ -269,177 +205,160 @@ small_layer_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r
   }
 }
 
-// ---------------------------------------------------------------- large layers: warp-specialised scan
-// REFILL = false: all chunks, acc = r + g, residual' = acc stored, candidates key >= thr[layer].
-// REFILL = true : the chunks in refill_list (count in counters[0]); acc re-read (r when EF, else g),
-//                 nothing stored but the candidates, thr = 0 (every element is a candidate).
+// ---------------------------------------------------------------- large layers: streaming scan
+// One warp per 256-element segment, 4 warps (a 1024-element piece) per CTA.
+// REFILL = false: grid = 16 pieces x all chunks; acc = r + g; residual' = acc stored;
+//                 candidates key >= thr[layer].
+// REFILL = true : persistent grid over 16 pieces x the chunks in refill_list (count in
+//                 counters[0]); acc re-read (r when EF, else g); thr = 0.
 template <bool EF, bool REFILL>
-__global__ void __launch_bounds__(kWsThreads, 2)
+__global__ void __launch_bounds__(kScanWarps * 32)
 scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, uint64_t psi) {
-  constexpr bool TWO = EF && !REFILL;             // grad and residual both streamed
-  extern __shared__ __align__(128) uint8_t dsm[];
-  float* sA = reinterpret_cast<float*>(dsm);      // [kStages][kSub]  grad (or acc when REFILL)
-  float* sB = sA + kStages * kSub;                // [kStages][kSub]  residual (TWO only)
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  __shared__ uint32_t sh_hist[kH0];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t n_work = REFILL ? P.counters[0] : (uint32_t)P.n_chunks;
-  if (blockIdx.x >= n_work) return;
-  if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], kWsWarps); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int b = tid; b < kH0; b += kWsThreads) sh_hist[b] = 0;
-  __syncthreads();
-  const float* srcA = REFILL ? (EF ? r : g) : g;
-
-  if (warp == kWsWarps) {   // ------------------------------------------------ producer warp
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (uint32_t w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const int ch = REFILL ? (int)P.refill_list[w] : (int)w;
-        const uint64_t hi = P.chunk_hi[ch];
-        for (uint64_t sb = P.chunk_base[ch]; sb < hi; sb += kSub, ++it) {
-          const int st = (int)(it % kStages);
-          mbar_wait(&empty[st], ((it / kStages) & 1u) ^ 1u);
-          uint64_t ve = (min(sb + kSub, hi) + 3) & ~3ull;   // whole float4 slots ...
-          if (ve > psi) ve = psi & ~3ull;                     // ... inside the caller's buffer
-          const uint32_t bytes = ve > sb ? (uint32_t)((ve - sb) * 4) : 0u;
-          mbar_arrive_expect_tx(&full[st], bytes * (TWO ? 2u : 1u));
-          if (bytes) {
-            bulk_g2s(sA + st * kSub, srcA + sb, bytes, &full[st]);
-            if (TWO) bulk_g2s(sB + st * kSub, r + sb, bytes, &full[st]);
-          }
-        }
-      }
-    }
-    return;
-  }
-
-  // ---------------------------------------------------------------------- compute warps
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  uint32_t it = 0;
-  int cur_slot = -1;
-  uint32_t thr = 0;
-  for (uint32_t w = blockIdx.x; w < n_work; w += gridDim.x) {
-    const int ch = REFILL ? (int)P.refill_list[w] : (int)w;
-    const int slot = P.chunk_slot[ch];
-    if (slot != cur_slot) {   // flush the digit-0 histogram of the previous layer
-      if (cur_slot >= 0) {
-        compute_bar();
-        uint32_t* hrow = P.hist + (uint64_t)cur_slot * kHistRow;
-        for (int b = tid; b < kH0; b += kWsWarps * 32) {
-          const uint32_t h = sh_hist[b];
-          if (h) { atomicAdd(&hrow[b], h); sh_hist[b] = 0; }
-        }
-        compute_bar();
-      }
-      cur_slot = slot;
-      thr = REFILL ? 0u : P.thr[slot];
-    }
+  const uint64_t n_items = REFILL ? (uint64_t)P.counters[0] * kPiecesPerChunk
+                                  : (uint64_t)P.n_chunks * kPiecesPerChunk;
+  for (uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const int ch = REFILL ? (int)P.refill_list[w / kPiecesPerChunk] : (int)(w / kPiecesPerChunk);
+    const int seg = (int)(w % kPiecesPerChunk) * kScanWarps + warp;
+    const uint64_t sbase = P.chunk_base[ch] + (uint64_t)seg * kSeg;
     const uint64_t lo = P.chunk_lo[ch], hi = P.chunk_hi[ch];
-    uint16_t* segc = P.seg_count + (uint64_t)ch * kSegsPerChunk;
-    int sub = 0;
-    for (uint64_t sb = P.chunk_base[ch]; sb < hi; sb += kSub, ++it, ++sub) {
-      const int st = (int)(it % kStages);
-      mbar_wait(&full[st], (it / kStages) & 1u);
-      const float4* tA = reinterpret_cast<const float4*>(sA + st * kSub);
-      const float4* tB = reinterpret_cast<const float4*>(sB + st * kSub);
-      float4 a[2];
-      uint32_t f[2];
-      bool bad = false;
+    const int slot = P.chunk_slot[ch];
+    const uint32_t thr = REFILL ? 0u : P.thr[slot];
+    float4 a[2];
+    uint32_t vm[2];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int q = warp * (kSeg / 4) + j * 32 + lane;   // float4 slot inside the sub-tile
-        const uint64_t e0 = sb + 4ull * q;
-        uint32_t vm = 0;
-        if (e0 >= lo && e0 + 4 <= hi) vm = 0xF;
-        else if (e0 + 4 > lo && e0 < hi)
-          for (int k = 0; k < 4; ++k) vm |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
-        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (vm) {
-          if (e0 + 4 <= psi) {
-            const float4 av = tA[q];
-            if (TWO) {
-              const float4 rv = tB[q];
-              x = make_float4(__fadd_rn(rv.x, av.x), __fadd_rn(rv.y, av.y), __fadd_rn(rv.z, av.z),
-                              __fadd_rn(rv.w, av.w));
-            } else {
-              x = av;
-            }
-          } else {   // the buffer's last partial float4 was not bulk-copied
-            for (int k = 0; k < 4; ++k)
-              if ((vm >> k) & 1u) {
-                float y;
-                if (REFILL) y = EF ? r[e0 + k] : g[e0 + k];
-                else y = EF ? __fadd_rn(r[e0 + k], g[e0 + k]) : g[e0 + k];
-                f4set(x, k, y);
-              }
-          }
-          if (TWO) {
-            if (vm == 0xF) st_stream(r + e0, x);
-            else
-              for (int k = 0; k < 4; ++k)
-                if ((vm >> k) & 1u) r[e0 + k] = f4get(x, k);
-          }
-        }
-        uint32_t fl = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t key = key_of(f4get(x, k));
-          const bool v = (vm >> k) & 1u;
-          bad |= v && key >= 0x7F800000u;
-          if (v && key >= thr) { fl |= 1u << k; atomicAdd(&sh_hist[key >> 20], 1u); }
-        }
-        f[j] = fl;
-        a[j] = x;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done with the stage
-      if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
-      // ordered compaction of the warp's segment: elements in (j, lane, k) order = index order
-      const int seg = sub * kWsWarps + warp;
-      uint32_t* cidx = P.cand_idx + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
-      uint32_t* cval = P.cand_val + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
-      uint32_t run = 0;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const uint32_t fl = f[j];
-        unsigned bm[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) bm[k] = __ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u);
-        uint32_t pos = run;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) pos += __popc(bm[k] & lt);
-        if (fl) {
-          const uint64_t e0 = sb + 4ull * (warp * (kSeg / 4) + j * 32 + lane);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if ((fl >> k) & 1u) { cidx[pos] = (uint32_t)(e0 + k); cval[pos] = __float_as_uint(f4get(a[j], k)); ++pos; }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) run += __popc(bm[k]);
-      }
-      if (lane == 0) segc[seg] = (uint16_t)run;
+    for (int j = 0; j < 2; ++j) {
+      const uint64_t e0 = sbase + 4ull * (j * 32 + lane);
+      vm[j] = 0;
+      if (e0 >= lo && e0 + 4 <= hi) vm[j] = 0xF;
+      else if (e0 + 4 > lo && e0 < hi)
+        for (int k = 0; k < 4; ++k) vm[j] |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
     }
-    if (lane == 0)
-      for (int s2 = sub; s2 < kSegsPerChunk / kWsWarps; ++s2) segc[s2 * kWsWarps + warp] = 0;
-  }
-  if (cur_slot >= 0) {
-    compute_bar();
-    uint32_t* hrow = P.hist + (uint64_t)cur_slot * kHistRow;
-    for (int b = tid; b < kH0; b += kWsWarps * 32)
-      if (sh_hist[b]) atomicAdd(&hrow[b], sh_hist[b]);
+    // loads first (4 x 128-bit in flight per lane), then the adds
+    float4 gv[2], rv[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint64_t e0 = sbase + 4ull * (j * 32 + lane);
+      if (vm[j] == 0xF) {
+        if (REFILL) {
+          gv[j] = *reinterpret_cast<const float4*>((EF ? r : g) + e0);
+        } else {
+          gv[j] = __ldcs(reinterpret_cast<const float4*>(g + e0));
+          if (EF) rv[j] = __ldcs(reinterpret_cast<const float4*>(r + e0));
+        }
+      }
+    }
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint64_t e0 = sbase + 4ull * (j * 32 + lane);
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (vm[j] == 0xF) {
+        if (!REFILL && EF) x = make_float4(__fadd_rn(rv[j].x, gv[j].x), __fadd_rn(rv[j].y, gv[j].y),
+                                           __fadd_rn(rv[j].z, gv[j].z), __fadd_rn(rv[j].w, gv[j].w));
+        else x = gv[j];
+        if (!REFILL && EF) __stcs(reinterpret_cast<float4*>(r + e0), x);
+      } else if (vm[j]) {   // ragged edge of a layer: scalar
+        for (int k = 0; k < 4; ++k)
+          if ((vm[j] >> k) & 1u) {
+            float y;
+            if (REFILL) y = EF ? r[e0 + k] : g[e0 + k];
+            else y = EF ? __fadd_rn(r[e0 + k], g[e0 + k]) : g[e0 + k];
+            f4set(x, k, y);
+            if (!REFILL && EF) r[e0 + k] = y;
+          }
+      }
+      a[j] = x;
+    }
+    // flags + ordered compaction of this warp's segment: (j, lane, k) order == index order
+    uint32_t* cidx = P.cand_idx + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
+    uint32_t* cval = P.cand_val + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
+    uint32_t run = 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      uint32_t fl = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t key = key_of(f4get(a[j], k));
+        const bool v = (vm[j] >> k) & 1u;
+        bad |= v && key >= 0x7F800000u;
+        fl |= (v && key >= thr) ? 1u << k : 0u;
+      }
+      unsigned bm[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) bm[k] = __ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u);
+      uint32_t pos = run;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) pos += __popc(bm[k] & lt);
+      if (fl) {
+        const uint64_t e0 = sbase + 4ull * (j * 32 + lane);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if ((fl >> k) & 1u) { cidx[pos] = (uint32_t)(e0 + k); cval[pos] = __float_as_uint(f4get(a[j], k)); ++pos; }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) run += __popc(bm[k]);
+    }
+    if (lane == 0) P.seg_count[(uint64_t)ch * kSegsPerChunk + seg] = (uint16_t)run;
+    if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
+    if (!REFILL) break;
   }
 }
 
-// per chunk: candidate total (sum of its 64 segment counts); warp per chunk
-__global__ void chunk_total_kernel(DevPlan P) {
+// ---------------------------------------------------------------- chunk prep (warp per chunk)
+// Compact the 64 segment lists of a chunk in place into one index-ordered list at the chunk's
+// base (a candidate never moves up, and every lane loads before it stores, so no unread source is
+// overwritten), store the chunk total, and histogram the first radix digit.
+// only_refill: process just the chunks of refilled layers (after the rescan).
+__global__ void chunk_prep_kernel(DevPlan P, int only_refill) {
   __shared__ uint32_t so_all[8][kSegsPerChunk + 1];
+  const int lane = threadIdx.x & 31;
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ch >= P.n_chunks) return;
-  const uint32_t tot = warp_load_segs(P, ch, so_all[threadIdx.x >> 5]);
-  if ((threadIdx.x & 31) == 0) P.chunk_count[ch] = tot;
+  const int slot = P.chunk_slot[ch];
+  if (only_refill && !P.sel[slot].refill) return;
+  uint32_t* so = so_all[threadIdx.x >> 5];
+  const uint16_t* cnt = P.seg_count + (uint64_t)ch * kSegsPerChunk;
+  const uint32_t c0 = cnt[lane], c1 = cnt[32 + lane];
+  uint32_t i0 = c0, i1 = c1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y0 = __shfl_up_sync(0xFFFFFFFFu, i0, o), y1 = __shfl_up_sync(0xFFFFFFFFu, i1, o);
+    if (lane >= o) { i0 += y0; i1 += y1; }
+  }
+  const uint32_t t0 = __shfl_sync(0xFFFFFFFFu, i0, 31);
+  so[lane] = i0 - c0;
+  so[32 + lane] = t0 + i1 - c1;
+  const uint32_t total = t0 + __shfl_sync(0xFFFFFFFFu, i1, 31);
+  if (lane == 0) { so[64] = total; P.chunk_count[ch] = total; }
+  __syncwarp();
+  uint32_t* cidx = P.cand_idx + (uint64_t)ch * kChunk;
+  uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
+  uint32_t* h0 = P.hist + (uint64_t)slot * kHistRow;
+  for (uint32_t base = 0; base < total; base += 32 * kUnroll) {
+    uint32_t vi[kUnroll], vv[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t c = base + u * 32 + lane;
+      vi[u] = vv[u] = 0;
+      if (c < total) {
+        int s = 0;
+#pragma unroll
+        for (int step = 32; step; step >>= 1)
+          if (so[s + step] <= c) s += step;
+        const uint32_t src = (uint32_t)s * kSeg + (c - so[s]);
+        vi[u] = cidx[src];
+        vv[u] = cval[src];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t c = base + u * 32 + lane;
+      if (c < total) { cidx[c] = vi[u]; cval[c] = vv[u]; }
+      warp_hist_add(h0, c < total, (vv[u] & 0x7FFFFFFFu) >> 20);
+    }
+  }
 }
 
 // ---------------------------------------------------------------- per-layer plan / digit search
@@ -522,45 +441,49 @@ __global__ void find_kernel(DevPlan P, int mode) {
 
 // digit d (1 or 2) histogram over candidates matching the prefix: warp per chunk
 __global__ void digit_kernel(DevPlan P, int d) {
-  __shared__ uint32_t so_all[8][kSegsPerChunk + 1];
   const int lane = threadIdx.x & 31;
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ch >= P.n_chunks) return;
-  uint32_t* so = so_all[threadIdx.x >> 5];
   const int shift = d == 1 ? 9 : 0;
   const int hs = d == 1 ? 20 : 9;
   const uint32_t mask = d == 1 ? 0x7FFu : 0x1FFu;
   const int slot = P.chunk_slot[ch];
   const uint32_t pre = P.sel[slot].prefix;
   uint32_t* h = P.hist + (uint64_t)slot * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
-  const uint32_t cnt = warp_load_segs(P, ch, so);
-  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
-    const uint32_t i = i0 + lane;
-    const uint32_t key = i < cnt ? P.cand_val[seg_addr(ch, so, i)] & 0x7FFFFFFFu : 0u;
-    const bool m = i < cnt && (key >> hs) == pre;
-    const unsigned act = __ballot_sync(0xFFFFFFFFu, m);
-    if (m) {
-      const uint32_t bin = (key >> shift) & mask;
-      const unsigned peers = __match_any_sync(act, bin);
-      if (lane == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+  const uint32_t cnt = P.chunk_count[ch];
+  const uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
+  for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
+    uint32_t key[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t i = base + u * 32 + lane;
+      key[u] = i < cnt ? cval[i] & 0x7FFFFFFFu : 0xFFFFFFFFu;
     }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      warp_hist_add(h, key[u] != 0xFFFFFFFFu && (key[u] >> hs) == pre, (key[u] >> shift) & mask);
   }
 }
 
 // per chunk: #(key > T) and #(key == T)
 __global__ void count_kernel(DevPlan P) {
-  __shared__ uint32_t so_all[8][kSegsPerChunk + 1];
   const int lane = threadIdx.x & 31;
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ch >= P.n_chunks) return;
-  uint32_t* so = so_all[threadIdx.x >> 5];
   const uint32_t T = P.sel[P.chunk_slot[ch]].prefix;
-  const uint32_t cnt = warp_load_segs(P, ch, so);
+  const uint32_t cnt = P.chunk_count[ch];
+  const uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
   uint32_t gt = 0, eq = 0;
-  for (uint32_t i = lane; i < cnt; i += 32) {
-    const uint32_t key = P.cand_val[seg_addr(ch, so, i)] & 0x7FFFFFFFu;
-    gt += key > T;
-    eq += key == T;
+  for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t i = base + u * 32 + lane;
+      if (i < cnt) {
+        const uint32_t key = cval[i] & 0x7FFFFFFFu;
+        gt += key > T;
+        eq += key == T;
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -599,37 +522,43 @@ __global__ void __launch_bounds__(256) layer_scan_kernel(DevPlan P) {
 // warp per chunk: ordered emit of the selected candidates, residual' zeroing
 template <bool EF>
 __global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K, float* __restrict__ r) {
-  __shared__ uint32_t so_all[8][kSegsPerChunk + 1];
   const int lane = threadIdx.x & 31;
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ch >= P.n_chunks) return;
-  uint32_t* so = so_all[threadIdx.x >> 5];
   const unsigned lt = (1u << lane) - 1u;
   const int slot = P.chunk_slot[ch];
   const uint32_t T = P.sel[slot].prefix;
   const uint32_t take = P.chunk_take[ch];
   const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + P.chunk_out[ch];
-  const uint32_t cnt = warp_load_segs(P, ch, so);
+  const uint32_t cnt = P.chunk_count[ch];
+  const uint32_t* cidx = P.cand_idx + (uint64_t)ch * kChunk;
+  const uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
   uint32_t eq_run = 0, out_run = 0;
-  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
-    const uint32_t i = i0 + lane;
-    const bool v = i < cnt;
-    const uint64_t a = v ? seg_addr(ch, so, i) : 0;
-    const uint32_t val = v ? P.cand_val[a] : 0u;
-    const uint32_t idx = v ? P.cand_idx[a] : 0u;
-    const uint32_t key = val & 0x7FFFFFFFu;
-    const bool is_eq = v && key == T;
-    const unsigned eqm = __ballot_sync(0xFFFFFFFFu, is_eq);
-    const bool sel = v && (key > T || (is_eq && eq_run + __popc(eqm & lt) < take));
-    const unsigned sm = __ballot_sync(0xFFFFFFFFu, sel);
-    if (sel) {
-      const uint64_t o = dst0 + out_run + __popc(sm & lt);
-      send[o] = idx;
-      send[K + o] = val;
-      if (EF) r[idx] = 0.0f;
+  for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
+    uint32_t vv[kUnroll], vi[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t i = base + u * 32 + lane;
+      vv[u] = i < cnt ? cval[i] : 0u;
+      vi[u] = i < cnt ? cidx[i] : 0u;
     }
-    eq_run += __popc(eqm);
-    out_run += __popc(sm);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const bool v = base + u * 32 + lane < cnt;
+      const uint32_t key = vv[u] & 0x7FFFFFFFu;
+      const bool is_eq = v && key == T;
+      const unsigned eqm = __ballot_sync(0xFFFFFFFFu, is_eq);
+      const bool sel = v && (key > T || (is_eq && eq_run + __popc(eqm & lt) < take));
+      const unsigned sm = __ballot_sync(0xFFFFFFFFu, sel);
+      if (sel) {
+        const uint64_t o = dst0 + out_run + __popc(sm & lt);
+        send[o] = vi[u];
+        send[K + o] = vv[u];
+        if (EF) r[vi[u]] = 0.0f;
+      }
+      eq_run += __popc(eqm);
+      out_run += __popc(sm);
+    }
   }
 }
 
@@ -642,19 +571,6 @@ int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
-}
-
-template <bool EF, bool REFILL>
-cudaError_t launch_scan(const DevPlan& P, int grid, const float* g, float* r, uint64_t psi, cudaStream_t s) {
-  static bool attr = false;
-  const size_t smem = (size_t)kStages * kSub * sizeof(float) * 2;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(scan_kernel<EF, REFILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  scan_kernel<EF, REFILL><<<grid, kWsThreads, smem, s>>>(P, g, r, psi);
-  return cudaSuccess;
 }
 
 }  // namespace
@@ -690,19 +606,20 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   const int sms = num_sms();
   const int layer_blocks = (P.n_large * 32 + 255) / 256;     // warp per large layer
   const int chunk_blocks = (P.n_chunks + 7) / 8;              // warp per chunk
-  const int scan_grid = std::min(P.n_chunks, sms * 2);        // persistent: 2 CTAs per SM
+  const unsigned scan_grid = (unsigned)P.n_chunks * kPiecesPerChunk;   // full grid: no tail loop
+  const int uK = kScanWarps * 32;
+  const uint64_t psi = (uint64_t)c->psi;
 
   prof_begin(c, "scan", s, &h);
-  e = ef ? launch_scan<true, false>(P, scan_grid, grad, residual, (uint64_t)c->psi, s)
-         : launch_scan<false, false>(P, scan_grid, grad, residual, (uint64_t)c->psi, s);
-  if (e != cudaSuccess) return e;
+  if (ef) scan_kernel<true, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, psi);
+  else scan_kernel<false, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, psi);
   prof_end(c, h, s);
   prof_begin(c, "select", s, &h);
-  chunk_total_kernel<<<chunk_blocks, 256, 0, s>>>(P);
+  chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 0);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 0);
-  e = ef ? launch_scan<true, true>(P, sms * 2, grad, residual, (uint64_t)c->psi, s)
-         : launch_scan<false, true>(P, sms * 2, grad, residual, (uint64_t)c->psi, s);
-  if (e != cudaSuccess) return e;
+  if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, psi);
+  else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, psi);
+  chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 1);
   digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 2);
@@ -715,7 +632,7 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   if (ef) emit_kernel<true><<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K, residual);
   else emit_kernel<false><<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K, residual);
   prof_end(c, h, s);
-  c->launches += 12;
+  c->launches += 14;
   return cudaGetLastError();
 }
 
