@@ -136,9 +136,8 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   P.chunk_slot = d_cslot; P.chunk_base = d_cb; P.chunk_lo = d_clo; P.chunk_hi = d_chi;
   const size_t nc = (size_t)std::max(1, P.n_chunks), nl = (size_t)std::max(1, P.n_large);
   void* p;
-  if ((st = dalloc(c, nc * ld::kChunk * 4, &p))) return st; P.cand_idx = (uint32_t*)p;
-  if ((st = dalloc(c, nc * ld::kChunk * 4, &p))) return st; P.cand_val = (uint32_t*)p;
-  if ((st = dalloc(c, nc * ld::kSegsPerChunk * sizeof(uint16_t), &p))) return st; P.seg_count = (uint16_t*)p;
+  if ((st = dalloc(c, nc * ld::kChunk * sizeof(uint64_t), &p))) return st; P.cand = (uint64_t*)p;
+  if ((st = dalloc(c, nc * ld::kSegsPerChunk * sizeof(uint32_t), &p))) return st; P.seg_count = (uint32_t*)p;
   if ((st = dalloc(c, nc * 4 * 6, &p))) return st;
   P.chunk_count = (uint32_t*)p; P.chunk_gt = P.chunk_count + nc; P.chunk_eq = P.chunk_gt + nc;
   P.chunk_out = P.chunk_eq + nc; P.chunk_take = P.chunk_out + nc; P.refill_list = P.chunk_take + nc;

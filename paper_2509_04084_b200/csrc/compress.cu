@@ -8,14 +8,14 @@
 // How:
 //   small layers (n <= 16384): one CTA per layer, acc staged in shared memory, 3-digit MSB
 //     radix select (11/11/9 key bits) with shared-memory histograms, ordered emit by block scan.
-//   large layers: 16384-element chunks = 64 segments of 256 elements.
-//     scan:    a full-grid streaming kernel (one warp per segment, 2 x 128-bit loads of grad and
-//              of residual per lane, 128-bit store of residual' = acc): the pattern measured at
+//   large layers: 16384-element chunks = 16 segments of 1024 elements.
+//     scan:    a full-grid streaming kernel (one warp per segment, rounds of 2 x 128-bit loads of grad
+//              and of residual per lane, 128-bit stores of residual' = acc): the pattern measured at
 //              ~7.1 TB/s for 2 reads + 1 write on this GPU (tools/stream_probe.cu).  Each warp
 //              compacts its segment's candidates key >= tau_l in index order with ballots; no
 //              shared memory, no barriers.  tau_l is the speculative band predicted by the
 //              previous call.
-//     prep:    warp per chunk: compacts the 64 segment lists in place into one index-ordered
+//     prep:    warp per chunk: compacts the 16 segment lists in place into one index-ordered
 //              chunk list, counts it, and histograms the first radix digit (key bits [30:20]).
 //     plan:    per layer, if #candidates >= k_l the exact top-k lies inside the candidates
 //              (speculation hit); otherwise the layer is "refilled": the scan re-reads acc with
@@ -206,14 +206,16 @@ small_layer_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r
 }
 
 // ---------------------------------------------------------------- large layers: streaming scan
-// One warp per 256-element segment, 4 warps (a 1024-element piece) per CTA.
-// REFILL = false: grid = 16 pieces x all chunks; acc = r + g; residual' = acc stored;
+// One warp per 1024-element segment (4 rounds of 2 float4 per lane), 4 warps per CTA.
+// REFILL = false: grid = 4 pieces x all chunks; acc = r + g; residual' = acc stored;
 //                 candidates key >= thr[layer].
-// REFILL = true : persistent grid over 16 pieces x the chunks in refill_list (count in
+// REFILL = true : persistent grid over 4 pieces x the chunks in refill_list (count in
 //                 counters[0]); acc re-read (r when EF, else g); thr = 0.
+// Candidates are 64-bit (acc bits << 32 | global index) so a segment's run is one contiguous,
+// mostly full-sector write.
 template <bool EF, bool REFILL>
 __global__ void __launch_bounds__(kScanWarps * 32)
-scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, uint64_t psi) {
+scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const uint64_t n_items = REFILL ? (uint64_t)P.counters[0] * kPiecesPerChunk
@@ -225,142 +227,148 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, uint6
     const uint64_t lo = P.chunk_lo[ch], hi = P.chunk_hi[ch];
     const int slot = P.chunk_slot[ch];
     const uint32_t thr = REFILL ? 0u : P.thr[slot];
-    float4 a[2];
-    uint32_t vm[2];
+    uint64_t* cd = P.cand + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
+    uint32_t run = 0;
+    bool bad = false;
+#pragma unroll 1
+    for (int rd = 0; rd < kSeg / 256; ++rd) {   // 4 rounds x (2 float4 x 32 lanes)
+      float4 a[2], gv[2], rv[2];
+      uint32_t vm[2];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const uint64_t e0 = sbase + 4ull * (j * 32 + lane);
-      vm[j] = 0;
-      if (e0 >= lo && e0 + 4 <= hi) vm[j] = 0xF;
-      else if (e0 + 4 > lo && e0 < hi)
-        for (int k = 0; k < 4; ++k) vm[j] |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
-    }
-    // loads first (4 x 128-bit in flight per lane), then the adds
-    float4 gv[2], rv[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const uint64_t e0 = sbase + 4ull * (j * 32 + lane);
-      if (vm[j] == 0xF) {
-        if (REFILL) {
-          gv[j] = *reinterpret_cast<const float4*>((EF ? r : g) + e0);
-        } else {
-          gv[j] = __ldcs(reinterpret_cast<const float4*>(g + e0));
-          if (EF) rv[j] = __ldcs(reinterpret_cast<const float4*>(r + e0));
+      for (int j = 0; j < 2; ++j) {
+        const uint64_t e0 = sbase + 4ull * ((rd * 2 + j) * 32 + lane);
+        vm[j] = 0;
+        if (e0 >= lo && e0 + 4 <= hi) vm[j] = 0xF;
+        else if (e0 + 4 > lo && e0 < hi)
+          for (int k = 0; k < 4; ++k) vm[j] |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
+        if (vm[j] == 0xF) {   // loads first: 4 x 128-bit in flight per lane
+          if (REFILL) {
+            gv[j] = *reinterpret_cast<const float4*>((EF ? r : g) + e0);
+          } else {
+            gv[j] = __ldcs(reinterpret_cast<const float4*>(g + e0));
+            if (EF) rv[j] = __ldcs(reinterpret_cast<const float4*>(r + e0));
+          }
         }
       }
-    }
-    bool bad = false;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const uint64_t e0 = sbase + 4ull * (j * 32 + lane);
-      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (vm[j] == 0xF) {
-        if (!REFILL && EF) x = make_float4(__fadd_rn(rv[j].x, gv[j].x), __fadd_rn(rv[j].y, gv[j].y),
-                                           __fadd_rn(rv[j].z, gv[j].z), __fadd_rn(rv[j].w, gv[j].w));
-        else x = gv[j];
-        if (!REFILL && EF) __stcs(reinterpret_cast<float4*>(r + e0), x);
-      } else if (vm[j]) {   // ragged edge of a layer: scalar
-        for (int k = 0; k < 4; ++k)
-          if ((vm[j] >> k) & 1u) {
-            float y;
-            if (REFILL) y = EF ? r[e0 + k] : g[e0 + k];
-            else y = EF ? __fadd_rn(r[e0 + k], g[e0 + k]) : g[e0 + k];
-            f4set(x, k, y);
-            if (!REFILL && EF) r[e0 + k] = y;
-          }
+      for (int j = 0; j < 2; ++j) {
+        const uint64_t e0 = sbase + 4ull * ((rd * 2 + j) * 32 + lane);
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (vm[j] == 0xF) {
+          if (!REFILL && EF) x = make_float4(__fadd_rn(rv[j].x, gv[j].x), __fadd_rn(rv[j].y, gv[j].y),
+                                             __fadd_rn(rv[j].z, gv[j].z), __fadd_rn(rv[j].w, gv[j].w));
+          else x = gv[j];
+          if (!REFILL && EF) __stcs(reinterpret_cast<float4*>(r + e0), x);
+        } else if (vm[j]) {   // ragged edge of a layer: scalar
+          for (int k = 0; k < 4; ++k)
+            if ((vm[j] >> k) & 1u) {
+              float y;
+              if (REFILL) y = EF ? r[e0 + k] : g[e0 + k];
+              else y = EF ? __fadd_rn(r[e0 + k], g[e0 + k]) : g[e0 + k];
+              f4set(x, k, y);
+              if (!REFILL && EF) r[e0 + k] = y;
+            }
+        }
+        a[j] = x;
       }
-      a[j] = x;
-    }
-    // flags + ordered compaction of this warp's segment: (j, lane, k) order == index order
-    uint32_t* cidx = P.cand_idx + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
-    uint32_t* cval = P.cand_val + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
-    uint32_t run = 0;
+      // flags + ordered compaction: (round, j, lane, k) order == index order
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      uint32_t fl = 0;
+      for (int j = 0; j < 2; ++j) {
+        uint32_t fl = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t key = key_of(f4get(a[j], k));
-        const bool v = (vm[j] >> k) & 1u;
-        bad |= v && key >= 0x7F800000u;
-        fl |= (v && key >= thr) ? 1u << k : 0u;
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t key = key_of(f4get(a[j], k));
+          const bool v = (vm[j] >> k) & 1u;
+          bad |= v && key >= 0x7F800000u;
+          fl |= (v && key >= thr) ? 1u << k : 0u;
+        }
+        unsigned bm[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bm[k] = __ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u);
+        uint32_t pos = run;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pos += __popc(bm[k] & lt);
+        if (fl) {
+          const uint32_t e0 = (uint32_t)(sbase + 4ull * ((rd * 2 + j) * 32 + lane));
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if ((fl >> k) & 1u) cd[pos++] = ((uint64_t)__float_as_uint(f4get(a[j], k)) << 32) | (e0 + k);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) run += __popc(bm[k]);
       }
-      unsigned bm[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) bm[k] = __ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u);
-      uint32_t pos = run;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) pos += __popc(bm[k] & lt);
-      if (fl) {
-        const uint64_t e0 = sbase + 4ull * (j * 32 + lane);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if ((fl >> k) & 1u) { cidx[pos] = (uint32_t)(e0 + k); cval[pos] = __float_as_uint(f4get(a[j], k)); ++pos; }
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) run += __popc(bm[k]);
     }
-    if (lane == 0) P.seg_count[(uint64_t)ch * kSegsPerChunk + seg] = (uint16_t)run;
+    if (lane == 0) P.seg_count[(uint64_t)ch * kSegsPerChunk + seg] = run;
     if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
     if (!REFILL) break;
   }
 }
 
 // ---------------------------------------------------------------- chunk prep (warp per chunk)
-// Compact the 64 segment lists of a chunk in place into one index-ordered list at the chunk's
-// base (a candidate never moves up, and every lane loads before it stores, so no unread source is
-// overwritten), store the chunk total, and histogram the first radix digit.
+// Compact the 16 segment lists of a chunk in place into one index-ordered list at the chunk's
+// base (a candidate never moves up, and each round loads before it stores, so no unread source is
+// overwritten), store the chunk total, and histogram the first radix digit -- in shared memory
+// when all chunks of the CTA belong to one layer (chunk slots are monotone), else directly.
 // only_refill: process just the chunks of refilled layers (after the rescan).
-__global__ void chunk_prep_kernel(DevPlan P, int only_refill) {
-  __shared__ uint32_t so_all[8][kSegsPerChunk + 1];
+__global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_refill) {
+  __shared__ uint32_t sh[kH0];
   const int lane = threadIdx.x & 31;
-  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (ch >= P.n_chunks) return;
-  const int slot = P.chunk_slot[ch];
-  if (only_refill && !P.sel[slot].refill) return;
-  uint32_t* so = so_all[threadIdx.x >> 5];
-  const uint16_t* cnt = P.seg_count + (uint64_t)ch * kSegsPerChunk;
-  const uint32_t c0 = cnt[lane], c1 = cnt[32 + lane];
-  uint32_t i0 = c0, i1 = c1;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y0 = __shfl_up_sync(0xFFFFFFFFu, i0, o), y1 = __shfl_up_sync(0xFFFFFFFFu, i1, o);
-    if (lane >= o) { i0 += y0; i1 += y1; }
+  const int c_first = blockIdx.x * 8;
+  const int c_last = min(P.n_chunks, c_first + 8) - 1;
+  const int ch = c_first + (threadIdx.x >> 5);
+  const bool uniform = P.chunk_slot[c_first] == P.chunk_slot[c_last];
+  if (uniform) {
+    for (int b = threadIdx.x; b < kH0; b += 256) sh[b] = 0;
+    __syncthreads();
   }
-  const uint32_t t0 = __shfl_sync(0xFFFFFFFFu, i0, 31);
-  so[lane] = i0 - c0;
-  so[32 + lane] = t0 + i1 - c1;
-  const uint32_t total = t0 + __shfl_sync(0xFFFFFFFFu, i1, 31);
-  if (lane == 0) { so[64] = total; P.chunk_count[ch] = total; }
-  __syncwarp();
-  uint32_t* cidx = P.cand_idx + (uint64_t)ch * kChunk;
-  uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
-  uint32_t* h0 = P.hist + (uint64_t)slot * kHistRow;
-  for (uint32_t base = 0; base < total; base += 32 * kUnroll) {
-    uint32_t vi[kUnroll], vv[kUnroll];
+  const int slot = ch <= c_last ? P.chunk_slot[ch] : P.chunk_slot[c_last];
+  const bool active = ch <= c_last && (!only_refill || P.sel[slot].refill);
+  if (active) {
+    const uint32_t c = lane < kSegsPerChunk ? P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] : 0u;
+    uint32_t inc = c;
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint32_t c = base + u * 32 + lane;
-      vi[u] = vv[u] = 0;
-      if (c < total) {
-        int s = 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const uint32_t so = inc - c;                                  // lanes 0..15: segment offsets
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    if (lane == 0) P.chunk_count[ch] = total;
+    uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
+    uint32_t* h0 = uniform ? sh : P.hist + (uint64_t)slot * kHistRow;
+    for (uint32_t base = 0; base < total; base += 32 * kUnroll) {
+      uint64_t v[kUnroll];
 #pragma unroll
-        for (int step = 32; step; step >>= 1)
-          if (so[s + step] <= c) s += step;
-        const uint32_t src = (uint32_t)s * kSeg + (c - so[s]);
-        vi[u] = cidx[src];
-        vv[u] = cval[src];
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t cc = base + u * 32 + lane;
+        int s = 0;   // segment of candidate cc: max{s : so[s] <= cc}, by shuffles over lanes 0..15
+#pragma unroll
+        for (int step = 8; step; step >>= 1) {
+          const uint32_t t = __shfl_sync(0xFFFFFFFFu, so, s + step);
+          if (t <= cc) s += step;
+        }
+        const uint32_t sos = __shfl_sync(0xFFFFFFFFu, so, s);
+        v[u] = cc < total ? cd[(uint32_t)s * kSeg + (cc - sos)] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t cc = base + u * 32 + lane;
+        if (cc < total) cd[cc] = v[u];
+        const uint32_t bin = (uint32_t)(v[u] >> 52) & 0x7FFu;   // key bits [30:20]
+        if (uniform) { if (cc < total) atomicAdd(&h0[bin], 1u); }
+        else warp_hist_add(h0, cc < total, bin);
       }
     }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint32_t c = base + u * 32 + lane;
-      if (c < total) { cidx[c] = vi[u]; cval[c] = vv[u]; }
-      warp_hist_add(h0, c < total, (vv[u] & 0x7FFFFFFFu) >> 20);
+  }
+  if (uniform) {
+    __syncthreads();
+    if (!only_refill || P.sel[P.chunk_slot[c_first]].refill) {
+      uint32_t* hrow = P.hist + (uint64_t)P.chunk_slot[c_first] * kHistRow;
+      for (int b = threadIdx.x; b < kH0; b += 256)
+        if (sh[b]) atomicAdd(&hrow[b], sh[b]);
     }
   }
 }
-
 // ---------------------------------------------------------------- per-layer plan / digit search
 // mode 0: after scan -- decide hit/refill, find digit 0 for hits, queue refills
 // mode 1: after rescan -- find digit 0 for refilled layers
@@ -439,29 +447,50 @@ __global__ void find_kernel(DevPlan P, int mode) {
   }
 }
 
-// digit d (1 or 2) histogram over candidates matching the prefix: warp per chunk
-__global__ void digit_kernel(DevPlan P, int d) {
+// digit d (1 or 2) histogram over candidates matching the prefix: warp per chunk, 8 chunks per
+// CTA aggregated in shared memory when they belong to one layer
+__global__ void __launch_bounds__(256) digit_kernel(DevPlan P, int d) {
+  __shared__ uint32_t sh[kH1];
   const int lane = threadIdx.x & 31;
-  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (ch >= P.n_chunks) return;
+  const int c_first = blockIdx.x * 8;
+  const int c_last = min(P.n_chunks, c_first + 8) - 1;
+  const int ch = c_first + (threadIdx.x >> 5);
+  const bool uniform = P.chunk_slot[c_first] == P.chunk_slot[c_last];
+  const int nb = d == 1 ? kH1 : kH2;
+  if (uniform) {
+    for (int b = threadIdx.x; b < nb; b += 256) sh[b] = 0;
+    __syncthreads();
+  }
   const int shift = d == 1 ? 9 : 0;
   const int hs = d == 1 ? 20 : 9;
   const uint32_t mask = d == 1 ? 0x7FFu : 0x1FFu;
-  const int slot = P.chunk_slot[ch];
-  const uint32_t pre = P.sel[slot].prefix;
-  uint32_t* h = P.hist + (uint64_t)slot * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
-  const uint32_t cnt = P.chunk_count[ch];
-  const uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
-  for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
-    uint32_t key[kUnroll];
+  if (ch <= c_last) {
+    const int slot = P.chunk_slot[ch];
+    const uint32_t pre = P.sel[slot].prefix;
+    uint32_t* h = uniform ? sh : P.hist + (uint64_t)slot * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
+    const uint32_t cnt = P.chunk_count[ch];
+    const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
+    for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
+      uint32_t key[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint32_t i = base + u * 32 + lane;
-      key[u] = i < cnt ? cval[i] & 0x7FFFFFFFu : 0xFFFFFFFFu;
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t i = base + u * 32 + lane;
+        key[u] = i < cnt ? (uint32_t)(cd[i] >> 32) & 0x7FFFFFFFu : 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const bool m = key[u] != 0xFFFFFFFFu && (key[u] >> hs) == pre;
+        const uint32_t bin = (key[u] >> shift) & mask;
+        if (uniform) { if (m) atomicAdd(&h[bin], 1u); }
+        else warp_hist_add(h, m, bin);
+      }
     }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-      warp_hist_add(h, key[u] != 0xFFFFFFFFu && (key[u] >> hs) == pre, (key[u] >> shift) & mask);
+  }
+  if (uniform) {
+    __syncthreads();
+    uint32_t* hg = P.hist + (uint64_t)P.chunk_slot[c_first] * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
+    for (int b = threadIdx.x; b < nb; b += 256)
+      if (sh[b]) atomicAdd(&hg[b], sh[b]);
   }
 }
 
@@ -472,14 +501,14 @@ __global__ void count_kernel(DevPlan P) {
   if (ch >= P.n_chunks) return;
   const uint32_t T = P.sel[P.chunk_slot[ch]].prefix;
   const uint32_t cnt = P.chunk_count[ch];
-  const uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
+  const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
   uint32_t gt = 0, eq = 0;
   for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint32_t i = base + u * 32 + lane;
       if (i < cnt) {
-        const uint32_t key = cval[i] & 0x7FFFFFFFu;
+        const uint32_t key = (uint32_t)(cd[i] >> 32) & 0x7FFFFFFFu;
         gt += key > T;
         eq += key == T;
       }
@@ -492,7 +521,6 @@ __global__ void count_kernel(DevPlan P) {
   }
   if (lane == 0) { P.chunk_gt[ch] = gt; P.chunk_eq[ch] = eq; }
 }
-
 // per large layer (one CTA): exclusive scans over its chunks; next speculative threshold
 __global__ void __launch_bounds__(256) layer_scan_kernel(DevPlan P) {
   __shared__ uint32_t sh32[33];
@@ -531,37 +559,35 @@ __global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K, 
   const uint32_t take = P.chunk_take[ch];
   const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + P.chunk_out[ch];
   const uint32_t cnt = P.chunk_count[ch];
-  const uint32_t* cidx = P.cand_idx + (uint64_t)ch * kChunk;
-  const uint32_t* cval = P.cand_val + (uint64_t)ch * kChunk;
+  const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
   uint32_t eq_run = 0, out_run = 0;
   for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
-    uint32_t vv[kUnroll], vi[kUnroll];
+    uint64_t v[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint32_t i = base + u * 32 + lane;
-      vv[u] = i < cnt ? cval[i] : 0u;
-      vi[u] = i < cnt ? cidx[i] : 0u;
+      v[u] = i < cnt ? cd[i] : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const bool v = base + u * 32 + lane < cnt;
-      const uint32_t key = vv[u] & 0x7FFFFFFFu;
-      const bool is_eq = v && key == T;
+      const bool ok = base + u * 32 + lane < cnt;
+      const uint32_t val = (uint32_t)(v[u] >> 32), idx = (uint32_t)v[u];
+      const uint32_t key = val & 0x7FFFFFFFu;
+      const bool is_eq = ok && key == T;
       const unsigned eqm = __ballot_sync(0xFFFFFFFFu, is_eq);
-      const bool sel = v && (key > T || (is_eq && eq_run + __popc(eqm & lt) < take));
+      const bool sel = ok && (key > T || (is_eq && eq_run + __popc(eqm & lt) < take));
       const unsigned sm = __ballot_sync(0xFFFFFFFFu, sel);
       if (sel) {
         const uint64_t o = dst0 + out_run + __popc(sm & lt);
-        send[o] = vi[u];
-        send[K + o] = vv[u];
-        if (EF) r[vi[u]] = 0.0f;
+        send[o] = idx;
+        send[K + o] = val;
+        if (EF) r[idx] = 0.0f;
       }
       eq_run += __popc(eqm);
       out_run += __popc(sm);
     }
   }
 }
-
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -608,17 +634,16 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   const int chunk_blocks = (P.n_chunks + 7) / 8;              // warp per chunk
   const unsigned scan_grid = (unsigned)P.n_chunks * kPiecesPerChunk;   // full grid: no tail loop
   const int uK = kScanWarps * 32;
-  const uint64_t psi = (uint64_t)c->psi;
 
   prof_begin(c, "scan", s, &h);
-  if (ef) scan_kernel<true, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, psi);
-  else scan_kernel<false, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, psi);
+  if (ef) scan_kernel<true, false><<<scan_grid, uK, 0, s>>>(P, grad, residual);
+  else scan_kernel<false, false><<<scan_grid, uK, 0, s>>>(P, grad, residual);
   prof_end(c, h, s);
   prof_begin(c, "select", s, &h);
   chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 0);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 0);
-  if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, psi);
-  else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, psi);
+  if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual);
+  else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual);
   chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 1);
   digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);

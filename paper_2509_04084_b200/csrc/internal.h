@@ -21,8 +21,8 @@ namespace ld {
 // Larger layers are cut into chunks of kChunk elements whose boundaries are
 // 4-element aligned in the flat buffer (so every 16-byte slot lies in one chunk).
 constexpr int kChunk = 16384;          // elements per chunk (64 KB of fp32)
-constexpr int kSeg = 256;              // candidate segment: one compute warp's share of a sub-tile
-constexpr int kSegsPerChunk = kChunk / kSeg;   // 64
+constexpr int kSeg = 1024;             // candidate segment: the elements one scan warp streams
+constexpr int kSegsPerChunk = kChunk / kSeg;   // 16
 constexpr int kScanThreads = 512;      // threads per chunk CTA: 8 float4 slots each
 constexpr int kSmallMax = 16384;       // small-layer bound (64 KB smem for acc)
 constexpr int kSmallThreads = 512;
@@ -59,9 +59,9 @@ struct DevPlan {
   const uint64_t* chunk_lo;      // [n_chunks] first element that belongs to the chunk
   const uint64_t* chunk_hi;      // [n_chunks] one past the last element
   // scratch
-  uint32_t* cand_idx;            // [n_chunks * 64 segments * 256] candidate global indices
-  uint32_t* cand_val;            // [n_chunks * 64 segments * 256] candidate acc bits
-  uint16_t* seg_count;           // [n_chunks * 64] candidates per segment (index-ordered inside)
+  uint64_t* cand;                // [n_chunks * kChunk] candidates (acc bits << 32 | global index):
+                                 //   written per segment by the scan, compacted per chunk by prep
+  uint32_t* seg_count;           // [n_chunks * 16] candidates per segment (index-ordered inside)
   uint32_t* chunk_count;         // [n_chunks]
   uint32_t* chunk_gt;            // [n_chunks]
   uint32_t* chunk_eq;            // [n_chunks]
