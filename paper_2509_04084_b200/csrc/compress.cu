@@ -39,7 +39,8 @@ namespace {
 constexpr int kH0 = 2048, kH1 = 2048, kH2 = 512;   // digit sizes: key bits [30:20] [19:9] [8:0]
 constexpr int kHistRow = kH0 + kH1 + kH2;
 constexpr int kScanWarps = 4;                       // segments per scan CTA
-constexpr int kPiecesPerChunk = kSegsPerChunk / kScanWarps;   // 16 scan CTAs per chunk
+constexpr int kPiecesPerChunk = kSegsPerChunk / kScanWarps;   // 4 scan CTAs per chunk
+constexpr int kJ = 1;                               // float4 per lane per scan round
 constexpr int kUnroll = 4;                          // candidate rounds in flight per warp
 
 __device__ __forceinline__ float f4get(const float4& v, int q) {
@@ -214,66 +215,70 @@ small_layer_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r
 // Candidates are 64-bit (acc bits << 32 | global index) so a segment's run is one contiguous,
 // mostly full-sector write.
 template <bool EF, bool REFILL>
-__global__ void __launch_bounds__(kScanWarps * 32)
+__global__ void __launch_bounds__(kScanWarps * 32, 16)
 scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const uint64_t n_items = REFILL ? (uint64_t)P.counters[0] * kPiecesPerChunk
-                                  : (uint64_t)P.n_chunks * kPiecesPerChunk;
-  for (uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+  const uint32_t n_items = REFILL ? P.counters[0] * kPiecesPerChunk : (uint32_t)P.n_chunks * kPiecesPerChunk;
+  for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x) {
     const int ch = REFILL ? (int)P.refill_list[w / kPiecesPerChunk] : (int)(w / kPiecesPerChunk);
     const int seg = (int)(w % kPiecesPerChunk) * kScanWarps + warp;
-    const uint64_t sbase = P.chunk_base[ch] + (uint64_t)seg * kSeg;
-    const uint64_t lo = P.chunk_lo[ch], hi = P.chunk_hi[ch];
+    // chunk-local 32-bit offsets keep the register footprint (and so the occupancy that hides HBM
+    // latency) at the level of a plain streaming kernel
+    const uint64_t cbase = P.chunk_base[ch];
+    const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
     const int slot = P.chunk_slot[ch];
     const uint32_t thr = REFILL ? 0u : P.thr[slot];
+    const float* gc = g + cbase;
+    float* rc = r + cbase;
     uint64_t* cd = P.cand + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
+    const uint32_t sb = (uint32_t)seg * kSeg;
     uint32_t run = 0;
     bool bad = false;
 #pragma unroll 1
-    for (int rd = 0; rd < kSeg / 256; ++rd) {   // 4 rounds x (2 float4 x 32 lanes)
-      float4 a[2], gv[2], rv[2];
-      uint32_t vm[2];
+    for (int rd = 0; rd < kSeg / (128 * kJ); ++rd) {   // rounds of kJ float4 x 32 lanes
+      float4 a[kJ], gv[kJ], rv[kJ];
+      uint32_t vm[kJ];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const uint64_t e0 = sbase + 4ull * ((rd * 2 + j) * 32 + lane);
+      for (int j = 0; j < kJ; ++j) {
+        const uint32_t e0 = sb + 4u * ((rd * kJ + j) * 32 + lane);
         vm[j] = 0;
         if (e0 >= lo && e0 + 4 <= hi) vm[j] = 0xF;
         else if (e0 + 4 > lo && e0 < hi)
           for (int k = 0; k < 4; ++k) vm[j] |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
         if (vm[j] == 0xF) {   // loads first: 4 x 128-bit in flight per lane
           if (REFILL) {
-            gv[j] = *reinterpret_cast<const float4*>((EF ? r : g) + e0);
+            gv[j] = *reinterpret_cast<const float4*>((EF ? rc : gc) + e0);
           } else {
-            gv[j] = __ldcs(reinterpret_cast<const float4*>(g + e0));
-            if (EF) rv[j] = __ldcs(reinterpret_cast<const float4*>(r + e0));
+            gv[j] = __ldcs(reinterpret_cast<const float4*>(gc + e0));
+            if (EF) rv[j] = __ldcs(reinterpret_cast<const float4*>(rc + e0));
           }
         }
       }
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const uint64_t e0 = sbase + 4ull * ((rd * 2 + j) * 32 + lane);
+      for (int j = 0; j < kJ; ++j) {
+        const uint32_t e0 = sb + 4u * ((rd * kJ + j) * 32 + lane);
         float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
         if (vm[j] == 0xF) {
           if (!REFILL && EF) x = make_float4(__fadd_rn(rv[j].x, gv[j].x), __fadd_rn(rv[j].y, gv[j].y),
                                              __fadd_rn(rv[j].z, gv[j].z), __fadd_rn(rv[j].w, gv[j].w));
           else x = gv[j];
-          if (!REFILL && EF) __stcs(reinterpret_cast<float4*>(r + e0), x);
+          if (!REFILL && EF) __stcs(reinterpret_cast<float4*>(rc + e0), x);
         } else if (vm[j]) {   // ragged edge of a layer: scalar
           for (int k = 0; k < 4; ++k)
             if ((vm[j] >> k) & 1u) {
               float y;
-              if (REFILL) y = EF ? r[e0 + k] : g[e0 + k];
-              else y = EF ? __fadd_rn(r[e0 + k], g[e0 + k]) : g[e0 + k];
+              if (REFILL) y = EF ? rc[e0 + k] : gc[e0 + k];
+              else y = EF ? __fadd_rn(rc[e0 + k], gc[e0 + k]) : gc[e0 + k];
               f4set(x, k, y);
-              if (!REFILL && EF) r[e0 + k] = y;
+              if (!REFILL && EF) rc[e0 + k] = y;
             }
         }
         a[j] = x;
       }
       // flags + ordered compaction: (round, j, lane, k) order == index order
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < kJ; ++j) {
         uint32_t fl = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -289,7 +294,7 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) pos += __popc(bm[k] & lt);
         if (fl) {
-          const uint32_t e0 = (uint32_t)(sbase + 4ull * ((rd * 2 + j) * 32 + lane));
+          const uint32_t e0 = (uint32_t)cbase + sb + 4u * ((rd * kJ + j) * 32 + lane);   // global index (Psi < 2^32)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if ((fl >> k) & 1u) cd[pos++] = ((uint64_t)__float_as_uint(f4get(a[j], k)) << 32) | (e0 + k);
