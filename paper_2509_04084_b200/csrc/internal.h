@@ -26,8 +26,10 @@ constexpr int kSegsPerChunk = kChunk / kSeg;   // 16
 constexpr int kScanThreads = 512;      // threads per chunk CTA: 8 float4 slots each
 constexpr int kSmallMax = 16384;       // small-layer bound (64 KB smem for acc)
 constexpr int kSmallThreads = 512;
-constexpr int kMergeTile = 8192;       // merge tile (elements per CTA)
-constexpr int kReplayTile = 2048;      // replay tile (elements per CTA)
+constexpr int kMergeTileShift = 13;
+constexpr int kMergeTile = 1 << kMergeTileShift;     // merge tile (elements per CTA)
+constexpr int kReplayTileShift = 11;
+constexpr int kReplayTile = 1 << kReplayTileShift;   // replay tile (elements per CTA)
 constexpr int kReplayThreads = 256;
 constexpr uint32_t kNoThreshold = 0xFFFFFFFFu;
 

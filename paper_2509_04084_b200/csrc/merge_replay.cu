@@ -24,19 +24,18 @@
 namespace ld {
 namespace {
 
-// start[b][t] = lower_bound(idx_b, t * tile) for t = 0..n_tiles (idx_b ascending, K entries)
+// start[b][t] = lower_bound(idx_b, t * 2^tile_shift) for t = 0..n_tiles (idx_b ascending, K entries).
+// Entry e owns the tiles (tile(idx[e-1]), tile(idx[e])]; grid.y walks the blocks (no 64-bit division).
 __global__ void tile_start_kernel(const uint32_t* __restrict__ blocks, int64_t n_blocks, uint64_t stride,
-                                  uint64_t K, uint32_t tile, int64_t n_tiles, uint32_t* __restrict__ start) {
-  const uint64_t per = K + 1;
-  const uint64_t total = (uint64_t)n_blocks * per;
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
-       x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = x / per, e = x % per;
-    const uint32_t* idx = blocks + b * stride;
-    const int64_t t_lo = e == 0 ? 0 : (int64_t)(idx[e - 1] / tile) + 1;
-    const int64_t t_hi = e == K ? n_tiles : (int64_t)(idx[e] / tile);
-    uint32_t* st = start + b * (uint64_t)(n_tiles + 1);
-    for (int64_t t = t_lo; t <= t_hi; ++t) st[t] = (uint32_t)e;
+                                  uint32_t K, int tile_shift, uint32_t n_tiles, uint32_t* __restrict__ start) {
+  for (int64_t b = blockIdx.y; b < n_blocks; b += gridDim.y) {
+    const uint32_t* idx = blocks + (uint64_t)b * stride;
+    uint32_t* st = start + (uint64_t)b * (n_tiles + 1);
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e <= K; e += gridDim.x * blockDim.x) {
+      const uint32_t t_lo = e == 0 ? 0u : (__ldg(idx + e - 1) >> tile_shift) + 1;
+      const uint32_t t_hi = e == K ? n_tiles : (__ldg(idx + e) >> tile_shift);
+      for (uint32_t t = t_lo; t <= t_hi; ++t) st[t] = e;
+    }
   }
 }
 
@@ -94,10 +93,9 @@ merge_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const
 struct AdamK { float b1, c1, b2, c2, eps; };
 
 // Fused n-step replay.  Thread owns elements j0 + 4*(tid + 256*i) + q, i in {0,1}, q in 0..3.
-constexpr int kReplayMaxWorld = 8;
-
-template <int OPT, int DIV>
-__global__ void __launch_bounds__(kReplayThreads, 2)
+// MAXW >= min(world, 8): ranks whose first-round entries are prefetched in registers.
+template <int OPT, int DIV, int MAXW>
+__global__ void __launch_bounds__(kReplayThreads, MAXW >= 8 ? 3 : 4)
 replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
               const uint32_t* __restrict__ start, int64_t n_tiles, const float* __restrict__ scal,
               AdamK ak, uint64_t psi, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v) {
@@ -105,7 +103,6 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
   const int64_t t = blockIdx.x;
   const uint64_t j0 = (uint64_t)t * kReplayTile;
   const int len = (int)min((uint64_t)kReplayTile, psi - j0);
-  const bool full = len == kReplayTile;
   const int tid = threadIdx.x;
   float P[8], M[8], V[8];
 #pragma unroll
@@ -119,14 +116,13 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       V[4 * i + q] = (OPT == LOWDIFF_ADAM && in) ? v[j0 + o] : 0.f;
     }
   }
-  (void)full;
   const float n = (float)world, inv = 1.0f / (float)world;
   const uint64_t tstride = (uint64_t)(n_tiles + 1);
   // Software pipeline over steps (everything that step s+1 needs from HBM is in flight while step
-  // s computes): rng[x & 1] in shared memory holds the entry ranges of step x for every rank; the
-  // first 256 entries of every rank for step s sit in registers (pj, pv), loaded during step s-1.
-  __shared__ uint32_t s_a[2][kReplayMaxWorld], s_b[2][kReplayMaxWorld];
-  const bool ranger = tid < world && tid < kReplayMaxWorld;
+  // s computes): s_a/s_b[x & 1] in shared memory hold the entry ranges of step x for every rank;
+  // the first 256 entries of every rank for step s sit in registers (pj, pv), loaded during s-1.
+  __shared__ uint32_t s_a[2][MAXW], s_b[2][MAXW];
+  const bool ranger = tid < world && tid < MAXW;
   if (ranger) {
     s_a[0][tid] = __ldg(start + (uint64_t)tid * tstride + t);
     s_b[0][tid] = __ldg(start + (uint64_t)tid * tstride + t + 1);
@@ -137,12 +133,12 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
     }
   }
   __syncthreads();
-  uint32_t pj[kReplayMaxWorld], pv[kReplayMaxWorld];
+  uint32_t pj[MAXW], pv[MAXW];
   auto load_entries = [&](int64_t x) {   // first round of step x's entries of every rank
     const uint32_t* blk = diffs + (uint64_t)x * world * 2 * K;
     const int b = (int)(x & 1);
 #pragma unroll
-    for (int r = 0; r < kReplayMaxWorld; ++r) {
+    for (int r = 0; r < MAXW; ++r) {
       pj[r] = 0xFFFFFFFFu;
       pv[r] = 0u;
       if (r < world) {
@@ -167,7 +163,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
     const uint32_t* blk = diffs + (uint64_t)s * world * 2 * K;
     // rank by rank from +0: the rank-order sum of DESIGN.md R-8
 #pragma unroll
-    for (int r = 0; r < kReplayMaxWorld; ++r) {
+    for (int r = 0; r < MAXW; ++r) {
       if (r < world) {
         if (pj[r] != 0xFFFFFFFFu) G[pj[r]] = __fadd_rn(G[pj[r]], __uint_as_float(pv[r]));
         const uint32_t* idx = blk + (uint64_t)r * 2 * K;
@@ -178,7 +174,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
         __syncthreads();
       }
     }
-    for (int r = kReplayMaxWorld; r < world; ++r) {   // ranks beyond the register window
+    for (int r = MAXW; r < world; ++r) {   // ranks beyond the register window
       const uint32_t* st = start + ((uint64_t)s * world + r) * tstride + t;
       const uint32_t* idx = blk + (uint64_t)r * 2 * K;
       const uint32_t a = __ldg(st), b = __ldg(st + 1);
@@ -202,51 +198,48 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       na = __ldg(st2);
       nb = __ldg(st2 + 1);
     }
-    float gx[8];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 2; ++i) {   // two halves of 4 independent element chains (ILP 4)
       const float4 gv = G4[tid + kReplayThreads * i];
-      gx[4 * i + 0] = mean_of<DIV>(gv.x, n, inv);
-      gx[4 * i + 1] = mean_of<DIV>(gv.y, n, inv);
-      gx[4 * i + 2] = mean_of<DIV>(gv.z, n, inv);
-      gx[4 * i + 3] = mean_of<DIV>(gv.w, n, inv);
-    }
-    if (OPT == LOWDIFF_ADAM) {
-      // m = b1*m + c1*g ; v = b2*v + c2*(g*g) ; mh = m*r1 ; vh = v*r2
-      // d = sqrt(vh) + eps ; u = mh / d ; p = p - lr*u          (R-11)
-      // The 8 elements are computed as independent straight-line chains (ILP); the correctly
-      // rounded sqrt / divide take the exact fast sequence (ieee_fast.cuh) for every lane and a
-      // warp-rare fix-up pass redoes out-of-window operands with the intrinsics.
-      float mh[8], vh[8], d[8], u[8];
-      uint32_t slow = 0;
+      float gx[4] = {mean_of<DIV>(gv.x, n, inv), mean_of<DIV>(gv.y, n, inv), mean_of<DIV>(gv.z, n, inv),
+                     mean_of<DIV>(gv.w, n, inv)};
+      if (OPT == LOWDIFF_ADAM) {
+        // m = b1*m + c1*g ; v = b2*v + c2*(g*g) ; mh = m*r1 ; vh = v*r2
+        // d = sqrt(vh) + eps ; u = mh / d ; p = p - lr*u          (R-11)
+        // Correctly rounded sqrt / divide take the exact fast sequence (ieee_fast.cuh) for every
+        // lane; a warp-rare fix-up redoes out-of-window operands with the intrinsics.
+        float mh[4], vh[4], d[4], u[4];
+        uint32_t slow = 0;
 #pragma unroll
-      for (int x = 0; x < 8; ++x) {
-        M[x] = __fadd_rn(__fmul_rn(ak.b1, M[x]), __fmul_rn(ak.c1, gx[x]));
-        V[x] = __fadd_rn(__fmul_rn(ak.b2, V[x]), __fmul_rn(ak.c2, __fmul_rn(gx[x], gx[x])));
-        mh[x] = __fmul_rn(M[x], sr1);
-        vh[x] = __fmul_rn(V[x], sr2);
-        bool sl;
-        d[x] = __fadd_rn(sqrt_rn_fast(vh[x], &sl), ak.eps);
-        slow |= (uint32_t)sl << x;
-      }
-#pragma unroll
-      for (int x = 0; x < 8; ++x) {
-        bool sl;
-        u[x] = div_rn_fast(mh[x], d[x], &sl);
-        slow |= (uint32_t)sl << (8 + x);
-      }
-      if (slow) {   // static indices keep mh/vh/d/u in registers
-#pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          if ((slow >> x) & 1u) d[x] = __fadd_rn(__fsqrt_rn(vh[x]), ak.eps);
-          if ((slow >> x) & 0x101u) u[x] = __fdiv_rn(mh[x], d[x]);
+        for (int q = 0; q < 4; ++q) {
+          const int x = 4 * i + q;
+          M[x] = __fadd_rn(__fmul_rn(ak.b1, M[x]), __fmul_rn(ak.c1, gx[q]));
+          V[x] = __fadd_rn(__fmul_rn(ak.b2, V[x]), __fmul_rn(ak.c2, __fmul_rn(gx[q], gx[q])));
+          mh[q] = __fmul_rn(M[x], sr1);
+          vh[q] = __fmul_rn(V[x], sr2);
+          bool sl;
+          d[q] = __fadd_rn(sqrt_rn_fast(vh[q], &sl), ak.eps);
+          slow |= (uint32_t)sl << q;
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          bool sl;
+          u[q] = div_rn_fast(mh[q], d[q], &sl);
+          slow |= (uint32_t)sl << (4 + q);
+        }
+        if (slow) {   // static indices keep mh/vh/d/u in registers
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if ((slow >> q) & 1u) d[q] = __fadd_rn(__fsqrt_rn(vh[q]), ak.eps);
+            if ((slow >> q) & 0x11u) u[q] = __fdiv_rn(mh[q], d[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) P[4 * i + q] = __fsub_rn(P[4 * i + q], __fmul_rn(slr, u[q]));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) P[4 * i + q] = __fsub_rn(P[4 * i + q], __fmul_rn(slr, gx[q]));
       }
-#pragma unroll
-      for (int x = 0; x < 8; ++x) P[x] = __fsub_rn(P[x], __fmul_rn(slr, u[x]));
-    } else {
-#pragma unroll
-      for (int x = 0; x < 8; ++x) P[x] = __fsub_rn(P[x], __fmul_rn(slr, gx[x]));
     }
     if (ranger) { s_a[cur][tid] = na; s_b[cur][tid] = nb; }   // ranges of step s+2
     __syncthreads();
@@ -301,7 +294,11 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
   const int sms = num_sms2();
   int h;
   prof_begin(c, "merge", s, &h);
-  tile_start_kernel<<<sms * 8, 256, 0, s>>>(gathered, world, 2 * K, K, kMergeTile, n_tiles, start);
+  {
+    const unsigned gx = (unsigned)std::min<uint64_t>((K + 256) / 256, (uint64_t)sms * 16);
+    tile_start_kernel<<<dim3(gx, (unsigned)world), 256, 0, s>>>(gathered, world, 2 * K, (uint32_t)K,
+                                                                 kMergeTileShift, (uint32_t)n_tiles, start);
+  }
   const unsigned grid = (unsigned)n_tiles;
   switch (div_mode(c->cfg.mean != 0, world)) {
     case 0: merge_kernel<0><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
@@ -333,19 +330,33 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
   AdamK ak{consts5[0], consts5[1], consts5[2], consts5[3], consts5[4]};
   int h;
   prof_begin(c, "replay_index", s, &h);
-  tile_start_kernel<<<sms * 8, 256, 0, s>>>(diffs, n_steps * world, 2 * K, K, kReplayTile, n_tiles, start);
+  {
+    const int64_t nb = n_steps * world;
+    const unsigned gy = (unsigned)std::min<int64_t>(nb, 65535);
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((K + 256) / 256, (int64_t)sms * 16 / gy + 1));
+    tile_start_kernel<<<dim3(gx, gy), 256, 0, s>>>(diffs, nb, 2 * K, (uint32_t)K, kReplayTileShift,
+                                                   (uint32_t)n_tiles, start);
+  }
   prof_end(c, h, s);
   prof_begin(c, "replay", s, &h);
   const unsigned grid = (unsigned)n_tiles;
   const int dm = div_mode(mean, world);
-#define LD_REPLAY(OPT, DIV) \
-  replay_kernel<OPT, DIV><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, \
-                                                          (uint64_t)psi, p, m, v)
+#define LD_REPLAY(OPT, DIV, W) \
+  replay_kernel<OPT, DIV, W><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, \
+                                                             ak, (uint64_t)psi, p, m, v)
+#define LD_REPLAY_W(OPT, DIV)                                  \
+  do {                                                         \
+    if (world == 1) LD_REPLAY(OPT, DIV, 1);                    \
+    else if (world == 2) LD_REPLAY(OPT, DIV, 2);               \
+    else if (world <= 4) LD_REPLAY(OPT, DIV, 4);               \
+    else LD_REPLAY(OPT, DIV, 8);                               \
+  } while (0)
   if (optim == LOWDIFF_ADAM) {
-    if (dm == 0) LD_REPLAY(LOWDIFF_ADAM, 0); else if (dm == 1) LD_REPLAY(LOWDIFF_ADAM, 1); else LD_REPLAY(LOWDIFF_ADAM, 2);
+    if (dm == 0) LD_REPLAY_W(LOWDIFF_ADAM, 0); else if (dm == 1) LD_REPLAY_W(LOWDIFF_ADAM, 1); else LD_REPLAY_W(LOWDIFF_ADAM, 2);
   } else {
-    if (dm == 0) LD_REPLAY(LOWDIFF_SGD, 0); else if (dm == 1) LD_REPLAY(LOWDIFF_SGD, 1); else LD_REPLAY(LOWDIFF_SGD, 2);
+    if (dm == 0) LD_REPLAY_W(LOWDIFF_SGD, 0); else if (dm == 1) LD_REPLAY_W(LOWDIFF_SGD, 1); else LD_REPLAY_W(LOWDIFF_SGD, 2);
   }
+#undef LD_REPLAY_W
 #undef LD_REPLAY
   prof_end(c, h, s);
   c->launches += 2;
