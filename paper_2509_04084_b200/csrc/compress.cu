@@ -60,7 +60,16 @@ __device__ __forceinline__ void warp_find_bin(const uint32_t* h, int nb, uint32_
   const int w = nb / 32;
   const int top = nb - lane * w;                 // lane 0 owns the highest bins
   uint32_t s = 0;
-  for (int b = top - 1; b >= top - w; --b) s += h[b];
+  if (w == 64) {   // the 2048-bin digits: 64 independent loads in flight per lane
+    uint32_t part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int b = 0; b < 64; ++b) part[b & 7] += h[top - 1 - b];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += part[q];
+  } else {
+#pragma unroll 16
+    for (int b = top - 1; b >= top - w; --b) s += h[b];
+  }
   uint32_t inc = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -389,6 +398,7 @@ __global__ void find_kernel(DevPlan P, int mode) {
   if (mode == 0) {
     const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
     uint32_t tot = 0;
+#pragma unroll 8
     for (int c = c0 + lane; c < c1; c += 32) tot += P.chunk_count[c];
 #pragma unroll
     for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
@@ -527,13 +537,13 @@ __global__ void count_kernel(DevPlan P) {
   if (lane == 0) { P.chunk_gt[ch] = gt; P.chunk_eq[ch] = eq; }
 }
 // per large layer (one CTA): exclusive scans over its chunks; next speculative threshold
-__global__ void __launch_bounds__(256) layer_scan_kernel(DevPlan P) {
+__global__ void __launch_bounds__(1024) layer_scan_kernel(DevPlan P) {
   __shared__ uint32_t sh32[33];
   const int slot = blockIdx.x;
   const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
   const uint32_t T = P.sel[slot].prefix, need = P.sel[slot].kleft;
   uint32_t eq_carry = 0, out_carry = 0;
-  for (int cb = c0; cb < c1; cb += 256) {
+  for (int cb = c0; cb < c1; cb += blockDim.x) {
     const int c = cb + threadIdx.x;
     const uint32_t eq = c < c1 ? P.chunk_eq[c] : 0, gt = c < c1 ? P.chunk_gt[c] : 0;
     uint32_t tot;
@@ -586,13 +596,21 @@ __global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K, 
         const uint64_t o = dst0 + out_run + __popc(sm & lt);
         send[o] = idx;
         send[K + o] = val;
-        if (EF) r[idx] = 0.0f;
       }
       eq_run += __popc(eqm);
       out_run += __popc(sm);
     }
   }
 }
+// residual'[idx] = +0.0f for every emitted index (small layers' entries are already zero there);
+// 4 indices per thread, consecutive threads -> ascending addresses
+__global__ void zero_selected_kernel(const uint32_t* __restrict__ send, uint32_t K, float* __restrict__ r) {
+  const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (i0 + q < K) r[__ldg(send + i0 + q)] = 0.0f;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -656,11 +674,16 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 2);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 3);
   count_kernel<<<chunk_blocks, 256, 0, s>>>(P);
-  layer_scan_kernel<<<P.n_large, 256, 0, s>>>(P);
+  layer_scan_kernel<<<P.n_large, 1024, 0, s>>>(P);
   prof_end(c, h, s);
   prof_begin(c, "emit", s, &h);
   if (ef) emit_kernel<true><<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K, residual);
   else emit_kernel<false><<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K, residual);
+  if (ef) {   // residual' = 0 at the selection: walk the (ascending) send indices, stores in address order
+    const uint32_t K = (uint32_t)c->K;
+    zero_selected_kernel<<<(K + 1023) / 1024, 256, 0, s>>>(send, K, residual);
+    c->launches += 1;
+  }
   prof_end(c, h, s);
   c->launches += 14;
   return cudaGetLastError();
