@@ -102,6 +102,11 @@ lowdiff_status lowdiff_layer_k(const lowdiff_ctx *ctx, int32_t layer, int64_t *k
  *      LOWER index; write them index-ascending into `send` at koff_l:
  *      send = idx u32[K] (global flat index) || val f32-bits u32[K];
  *      residual' = acc with the selected entries set to +0.0f.
+ *    For layers larger than 16384 elements the +0.0f at the selected positions are DEFERRED:
+ *    the residual buffer keeps acc there and the next lowdiff_compress on the same buffer
+ *    zeroes them on the fly (the selection is {key > T_l} U {key == T_l, index < cut_l}, kept in
+ *    the context), saving a scattered write pass.  Call lowdiff_residual_materialize before
+ *    reading or modifying the buffer outside lowdiff_compress.
  *    grad: device f32[Psi] (read).  residual: device f32[Psi] (read/write; ignored and may
  *    be NULL when error_feedback = 0).  send: device u32[2K] (written).
  *    A non-finite acc sets a device flag; the next persist/sync returns LOWDIFF_E_NUMERIC.
@@ -109,6 +114,11 @@ lowdiff_status lowdiff_layer_k(const lowdiff_ctx *ctx, int32_t layer, int64_t *k
  *    waits for that copy (write-after-read). */
 lowdiff_status lowdiff_compress(lowdiff_ctx *ctx, const float *grad, float *residual,
                                 uint32_t *send, void *stream);
+
+/* Write the deferred +0.0f of the last lowdiff_compress into `residual` (device f32[Psi]), so
+ *    that it equals residual' exactly; afterwards the buffer may be read or changed freely.
+ *    A no-op when nothing is pending.  Asynchronous on `stream`. */
+lowdiff_status lowdiff_residual_materialize(lowdiff_ctx *ctx, float *residual, void *stream);
 
 /* 2. Exchange (Alg. 1 lines 5 and 7): ncclAllGather of the fixed-size
  *    blocks (rank r's block lands at gathered + r*2K), then the merge

@@ -145,6 +145,8 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   if ((st = dalloc(c, nl * sizeof(ld::LayerSel), &p))) return st; P.sel = (ld::LayerSel*)p;
   CK(cudaMemset(P.sel, 0, nl * sizeof(ld::LayerSel)));   // band = 0: not yet adapted
   if ((st = dalloc(c, nl * 4, &p))) return st; P.thr = (uint32_t*)p;
+  if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_T = (uint32_t*)p;
+  if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_cut = (uint32_t*)p;
   CK(cudaMemset(P.thr, 0xFF, nl * 4));   // no speculative band before the first call
   if ((st = dalloc(c, 8 * 4, &p))) return st; P.counters = (uint32_t*)p;
   if ((st = dalloc(c, 4 * 4, &p))) return st; P.err = (uint32_t*)p;
@@ -562,6 +564,14 @@ lowdiff_status lowdiff_compress(lowdiff_ctx* c, const float* grad, float* residu
   for (auto& ps : c->d2h_src)   // WAR: a persist of this buffer may still be copying it out
     if (ps.first == send) CK(cudaStreamWaitEvent(s, c->slots[ps.second].done, 0));
   CK(ld::launch_compress(c, grad, c->cfg.error_feedback ? residual : nullptr, send, s));
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_residual_materialize(lowdiff_ctx* c, float* residual, void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!residual || !aligned16(residual)) return fail(c, LOWDIFF_E_INVALID, "residual_materialize: bad buffer");
+  CK(ld::launch_materialize(c, residual, static_cast<cudaStream_t>(stream)));
   return LOWDIFF_OK;
 }
 

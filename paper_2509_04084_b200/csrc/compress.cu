@@ -223,9 +223,17 @@ small_layer_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r
 //                 counters[0]); acc re-read (r when EF, else g); thr = 0.
 // Candidates are 64-bit (acc bits << 32 | global index) so a segment's run is one contiguous,
 // mostly full-sector write.
+// Lazy residual zeroing: the previous call left residual' = acc at its selection; an element was
+// selected iff key > T_prev or (key == T_prev and index < cut_prev), so the scan zeroes it here
+// (exactly the +0.0f the eager residual' would hold) instead of a scattered zeroing pass.
+__device__ __forceinline__ float lazy_zero(float rv, uint32_t gidx, uint32_t T, uint32_t cut) {
+  const uint32_t key = key_of(rv);
+  return (key > T || (key == T && gidx < cut)) ? 0.0f : rv;
+}
+
 template <bool EF, bool REFILL>
 __global__ void __launch_bounds__(kScanWarps * 32, 16)
-scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
+scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int lazy) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t n_items = REFILL ? P.counters[0] * kPiecesPerChunk : (uint32_t)P.n_chunks * kPiecesPerChunk;
@@ -238,6 +246,9 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
     const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
     const int slot = P.chunk_slot[ch];
     const uint32_t thr = REFILL ? 0u : P.thr[slot];
+    const bool lz = !REFILL && EF && lazy;
+    const uint32_t lT = lz ? P.sel_T[slot] : 0xFFFFFFFFu, lcut = lz ? P.sel_cut[slot] : 0u;
+    const uint32_t gbase = (uint32_t)cbase;   // Psi < 2^32
     const float* gc = g + cbase;
     float* rc = r + cbase;
     uint64_t* cd = P.cand + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
@@ -269,16 +280,22 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
         const uint32_t e0 = sb + 4u * ((rd * kJ + j) * 32 + lane);
         float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
         if (vm[j] == 0xF) {
-          if (!REFILL && EF) x = make_float4(__fadd_rn(rv[j].x, gv[j].x), __fadd_rn(rv[j].y, gv[j].y),
-                                             __fadd_rn(rv[j].z, gv[j].z), __fadd_rn(rv[j].w, gv[j].w));
-          else x = gv[j];
+          if (!REFILL && EF) {
+            const uint32_t gi = gbase + e0;
+            x = make_float4(__fadd_rn(lazy_zero(rv[j].x, gi, lT, lcut), gv[j].x),
+                            __fadd_rn(lazy_zero(rv[j].y, gi + 1, lT, lcut), gv[j].y),
+                            __fadd_rn(lazy_zero(rv[j].z, gi + 2, lT, lcut), gv[j].z),
+                            __fadd_rn(lazy_zero(rv[j].w, gi + 3, lT, lcut), gv[j].w));
+          } else {
+            x = gv[j];
+          }
           if (!REFILL && EF) __stcs(reinterpret_cast<float4*>(rc + e0), x);
         } else if (vm[j]) {   // ragged edge of a layer: scalar
           for (int k = 0; k < 4; ++k)
             if ((vm[j] >> k) & 1u) {
               float y;
               if (REFILL) y = EF ? rc[e0 + k] : gc[e0 + k];
-              else y = EF ? __fadd_rn(rc[e0 + k], gc[e0 + k]) : gc[e0 + k];
+              else y = EF ? __fadd_rn(lazy_zero(rc[e0 + k], gbase + e0 + k, lT, lcut), gc[e0 + k]) : gc[e0 + k];
               f4set(x, k, y);
               if (!REFILL && EF) rc[e0 + k] = y;
             }
@@ -553,18 +570,23 @@ __global__ void __launch_bounds__(1024) layer_scan_kernel(DevPlan P) {
     const uint32_t o = gt + take;
     const uint32_t ob = out_carry + block_excl_scan(o, sh32, &tot);
     out_carry += tot;
-    if (c < c1) { P.chunk_out[c] = ob; P.chunk_take[c] = take; }
+    if (c < c1) {
+      P.chunk_out[c] = ob;
+      P.chunk_take[c] = take;
+      P.chunk_eq[c] = (take > 0 && eb + take == need) ? 1u : 0u;   // holds the layer's last taken tie
+    }
   }
   if (threadIdx.x == 0) {
+    P.sel_T[slot] = T;
     // speculative band for the next call, never above this call's T
     const uint32_t nt = P.sel[slot].next_thr;
     P.thr[slot] = nt <= T ? nt : T;
   }
 }
 
-// warp per chunk: ordered emit of the selected candidates, residual' zeroing
-template <bool EF>
-__global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K, float* __restrict__ r) {
+// warp per chunk: ordered emit of the selected candidates; the chunk holding the layer's last
+// taken tie records its index + 1 (sel_cut) for the lazy residual zeroing
+__global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K) {
   const int lane = threadIdx.x & 31;
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ch >= P.n_chunks) return;
@@ -572,6 +594,7 @@ __global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K, 
   const int slot = P.chunk_slot[ch];
   const uint32_t T = P.sel[slot].prefix;
   const uint32_t take = P.chunk_take[ch];
+  const bool last_tie_chunk = P.chunk_eq[ch] != 0u;
   const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + P.chunk_out[ch];
   const uint32_t cnt = P.chunk_count[ch];
   const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
@@ -597,18 +620,32 @@ __global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K, 
         send[o] = idx;
         send[K + o] = val;
       }
+      if (last_tie_chunk && is_eq && eq_run + __popc(eqm & lt) == take - 1) P.sel_cut[slot] = idx + 1;
       eq_run += __popc(eqm);
       out_run += __popc(sm);
     }
   }
 }
-// residual'[idx] = +0.0f for every emitted index (small layers' entries are already zero there);
-// 4 indices per thread, consecutive threads -> ascending addresses
-__global__ void zero_selected_kernel(const uint32_t* __restrict__ send, uint32_t K, float* __restrict__ r) {
-  const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (i0 + q < K) r[__ldg(send + i0 + q)] = 0.0f;
+
+// residual' = 0 at the last selection of the large layers (lowdiff_residual_materialize): a
+// streaming pass applying the lazy rule; small layers are always zeroed eagerly
+__global__ void materialize_kernel(DevPlan P, float* __restrict__ r) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t w = blockIdx.x;
+  const int ch = (int)(w / kPiecesPerChunk);
+  if (ch >= P.n_chunks) return;
+  const int seg = (int)(w % kPiecesPerChunk) * kScanWarps + warp;
+  const uint64_t cbase = P.chunk_base[ch];
+  const uint64_t lo = P.chunk_lo[ch], hi = P.chunk_hi[ch];
+  const int slot = P.chunk_slot[ch];
+  const uint32_t T = P.sel_T[slot], cut = P.sel_cut[slot];
+  for (int i = lane; i < kSeg; i += 32) {
+    const uint64_t e = cbase + (uint64_t)seg * kSeg + i;
+    if (e >= lo && e < hi) {
+      const uint32_t key = key_of(r[e]);
+      if (key > T || (key == T && (uint32_t)e < cut)) r[e] = 0.0f;   // selected last call -> +0
+    }
+  }
 }
 
 int num_sms() {
@@ -658,15 +695,17 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   const unsigned scan_grid = (unsigned)P.n_chunks * kPiecesPerChunk;   // full grid: no tail loop
   const int uK = kScanWarps * 32;
 
+  // lazy residual zeroing applies only to the residual buffer whose selection is pending
+  const int lazy = (ef && c->lazy_residual == residual) ? 1 : 0;
   prof_begin(c, "scan", s, &h);
-  if (ef) scan_kernel<true, false><<<scan_grid, uK, 0, s>>>(P, grad, residual);
-  else scan_kernel<false, false><<<scan_grid, uK, 0, s>>>(P, grad, residual);
+  if (ef) scan_kernel<true, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, lazy);
+  else scan_kernel<false, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, 0);
   prof_end(c, h, s);
   prof_begin(c, "select", s, &h);
   chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 0);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 0);
-  if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual);
-  else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual);
+  if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, 0);
+  else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, 0);
   chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 1);
   digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
@@ -677,15 +716,19 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   layer_scan_kernel<<<P.n_large, 1024, 0, s>>>(P);
   prof_end(c, h, s);
   prof_begin(c, "emit", s, &h);
-  if (ef) emit_kernel<true><<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K, residual);
-  else emit_kernel<false><<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K, residual);
-  if (ef) {   // residual' = 0 at the selection: walk the (ascending) send indices, stores in address order
-    const uint32_t K = (uint32_t)c->K;
-    zero_selected_kernel<<<(K + 1023) / 1024, 256, 0, s>>>(send, K, residual);
-    c->launches += 1;
-  }
+  emit_kernel<<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K);
   prof_end(c, h, s);
+  c->lazy_residual = ef ? residual : nullptr;   // this call's large-layer selection is now pending
   c->launches += 14;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_materialize(lowdiff_ctx* c, float* residual, cudaStream_t s) {
+  DevPlan& P = c->plan;
+  if (!P.n_large || c->lazy_residual == nullptr) return cudaSuccess;
+  materialize_kernel<<<(unsigned)P.n_chunks * kPiecesPerChunk, kScanWarps * 32, 0, s>>>(P, residual);
+  c->launches += 1;
+  if (residual == c->lazy_residual) c->lazy_residual = nullptr;   // zeros are in place now
   return cudaGetLastError();
 }
 

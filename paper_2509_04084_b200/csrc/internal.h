@@ -72,6 +72,10 @@ struct DevPlan {
   uint32_t* hist;                // [n_large * (2048 + 2048 + 512)]
   LayerSel* sel;                 // [n_large]
   uint32_t* thr;                 // [n_large] speculative threshold key (persistent across calls)
+  // lazy residual zeroing: the previous call's selection of a large layer is
+  // {key(r) > sel_T} U {key(r) == sel_T and index < sel_cut}; the next scan zeroes it on the fly
+  uint32_t* sel_T;               // [n_large] previous call's exact k-th key
+  uint32_t* sel_cut;             // [n_large] one past the global index of the last tie it took
   uint32_t* refill_list;         // [n_chunks] chunk ids to rescan
   uint32_t* counters;            // [0] refill chunk count, [1] spec hits, [2] spec misses
   uint32_t* err;                 // [0] non-finite flag, [1] first bad layer
@@ -108,6 +112,7 @@ struct lowdiff_ctx {
   cudaEvent_t last_d2h = nullptr;    // unused (kept for ABI-stable layout of the struct)
   std::vector<std::pair<const void*, int>> d2h_src;   // send buffer -> ring slot of its latest D2H (WAR)
   std::atomic<uint32_t> err_seen{0};  // non-finite events already reported
+  const float* lazy_residual = nullptr;   // residual whose last selection is not yet zeroed (large layers)
   // NCCL
   ncclComm_t comm = nullptr;
   // status
@@ -161,6 +166,7 @@ namespace ld {
 // kernels.cu
 cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send,
                             cudaStream_t s);
+cudaError_t launch_materialize(lowdiff_ctx* c, float* residual, cudaStream_t s);
 cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, float* dense,
                          cudaStream_t s);
 cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* consts5, int world,

@@ -68,6 +68,7 @@ def lib():
             "query": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], S),
             "layer_k": ([P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], S),
             "compress": ([P, P, P, P, P], S),
+            "residual_materialize": ([P, P, P], S),
             "exchange": ([P, P, P, P, P], S),
             "merge": ([P, C.c_int32, P, P, P], S),
             "batch_persist": ([P, C.c_int64, C.POINTER(StepScalars), P, P], S),
@@ -101,7 +102,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "exchange", "merge", "batch_persist",
+EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_materialize", "exchange", "merge", "batch_persist",
             "full_ckpt", "wait_persist", "recover", "replay", "snapshot_layer", "snapshot_wait", "sync", "get_stats",
             "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
             "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host",
@@ -232,6 +233,9 @@ class Context:
     # -- the five calls
     def compress(self, grad, residual, send, stream=None):
         self._c("compress", lib().lowdiff_compress(self._h, _ptr(grad), _ptr(residual), _ptr(send), _stream(stream)))
+
+    def residual_materialize(self, residual, stream=None):
+        self._c("residual_materialize", lib().lowdiff_residual_materialize(self._h, _ptr(residual), _stream(stream)))
 
     def exchange(self, send, gathered, dense_out, stream=None):
         self._c("exchange", lib().lowdiff_exchange(self._h, _ptr(send), _ptr(gathered), _ptr(dense_out),
