@@ -90,6 +90,27 @@ merge_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const
   }
 }
 
+// world == 1: G = (+0 + v) at the block's indices, +0 elsewhere.  The tile is zero-filled with
+// 128-bit stores straight to global memory, then (after a CTA barrier orders the writes) the tile's
+// entries are stored over it while those lines are still in L2 -- no shared-memory accumulator.
+__global__ void __launch_bounds__(256)
+merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __restrict__ start,
+              int64_t n_tiles, uint64_t psi, float* __restrict__ dense) {
+  const int64_t t = blockIdx.x;
+  const uint64_t j0 = (uint64_t)t * kMergeTile;
+  const int len = (int)min((uint64_t)kMergeTile, psi - j0);
+  if (len == kMergeTile) {
+    float4* out = reinterpret_cast<float4*>(dense + j0);
+    for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  } else {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) dense[j0 + i] = 0.f;
+  }
+  __syncthreads();
+  const uint32_t a = __ldg(start + t), b = __ldg(start + t + 1);
+  for (uint32_t e = a + threadIdx.x; e < b; e += blockDim.x)
+    dense[__ldg(send + e)] = __fadd_rn(0.f, __uint_as_float(__ldg(send + K + e)));
+}
+
 struct AdamK { float b1, c1, b2, c2, eps; };
 
 // Fused n-step replay.  Thread owns elements j0 + 4*(tid + 256*i) + q, i in {0,1}, q in 0..3.
@@ -300,6 +321,12 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
                                                                  kMergeTileShift, (uint32_t)n_tiles, start);
   }
   const unsigned grid = (unsigned)n_tiles;
+  if (world == 1) {
+    merge1_kernel<<<grid, 256, 0, s>>>(gathered, K, start, n_tiles, (uint64_t)psi, dense);
+    prof_end(c, h, s);
+    c->launches += 2;
+    return cudaGetLastError();
+  }
   switch (div_mode(c->cfg.mean != 0, world)) {
     case 0: merge_kernel<0><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
     case 1: merge_kernel<1><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
