@@ -16,7 +16,8 @@
  *  - Every call returns lowdiff_status; none throws, aborts or exits.  A CUDA or NCCL
  *    failure poisons the context: every later call returns the same code.
  *  - Device pointers are plain CUDA device addresses (e.g. torch tensor data_ptr()),
- *    contiguous, 16-byte aligned (else LOWDIFF_E_INVALID).  The CALLER owns every
+ *    contiguous; fp32 arrays of Psi elements 16-byte aligned, u32 send/gathered blocks 4-byte
+ *    aligned (else LOWDIFF_E_INVALID).  The CALLER owns every
  *    device buffer; the library never frees or reallocates caller memory.
  *  - `stream` arguments are cudaStream_t handles passed as void*.  Calls that take a
  *    stream enqueue work on it and return without a host synchronisation unless

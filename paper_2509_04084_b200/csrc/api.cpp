@@ -558,7 +558,8 @@ lowdiff_status lowdiff_compress(lowdiff_ctx* c, const float* grad, float* residu
   lowdiff_status st = entry(c);
   if (st) return st;
   if (!grad || !send || (c->cfg.error_feedback && !residual)) return fail(c, LOWDIFF_E_INVALID, "compress: NULL buffer");
-  if (!aligned16(grad) || !aligned16(send) || (residual && !aligned16(residual)))
+  // grad/residual are streamed with 128-bit accesses; the send block only needs 4-byte alignment
+  if (!aligned16(grad) || (reinterpret_cast<uintptr_t>(send) & 3u) || (residual && !aligned16(residual)))
     return fail(c, LOWDIFF_E_INVALID, "compress: buffers must be 16-byte aligned");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (auto& ps : c->d2h_src)   // WAR: a persist of this buffer may still be copying it out
@@ -579,7 +580,8 @@ lowdiff_status lowdiff_merge(lowdiff_ctx* c, int32_t world, const uint32_t* gath
   lowdiff_status st = entry(c);
   if (st) return st;
   if (world < 1 || !gathered || !dense_out) return fail(c, LOWDIFF_E_INVALID, "merge: bad argument");
-  if (!aligned16(gathered) || !aligned16(dense_out)) return fail(c, LOWDIFF_E_INVALID, "merge: buffers must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(gathered) & 3u) || !aligned16(dense_out))
+    return fail(c, LOWDIFF_E_INVALID, "merge: gathered must be 4-byte and dense_out 16-byte aligned");
   CK(ld::launch_merge(c, world, gathered, dense_out, static_cast<cudaStream_t>(stream)));
   return LOWDIFF_OK;
 }
