@@ -241,7 +241,8 @@ lowdiff_status lowdiff_write_full_host(const lowdiff_config *cfg, int64_t iterat
 int32_t lowdiff_abi_version(void);
 /* Device self-test of the branch-free IEEE sqrt/division used by the replay kernel against
  * __fsqrt_rn/__fdiv_rn (which = 0: all 2^31+1 non-negative floats; which = 1: n pseudo-random
- * operand pairs from `seed`).  Needs a GPU (current device); synchronous. */
+ * operand pairs from `seed`; which = 2: Adam's fused u = mh / (sqrt(vh) + eps) on n random
+ * triples).  Needs a GPU (current device); synchronous. */
 lowdiff_status lowdiff_selftest(int32_t which, uint64_t n, uint64_t seed, uint64_t *mismatches,
                                 uint64_t *first_bad);
 

@@ -146,6 +146,7 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   CK(cudaMemset(P.sel, 0, nl * sizeof(ld::LayerSel)));   // band = 0: not yet adapted
   if ((st = dalloc(c, nl * 4, &p))) return st; P.thr = (uint32_t*)p;
   if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_T = (uint32_t*)p;
+  if ((st = dalloc(c, nl * 4, &p))) return st; P.layer_total = (uint32_t*)p;
   if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_cut = (uint32_t*)p;
   CK(cudaMemset(P.thr, 0xFF, nl * 4));   // no speculative band before the first call
   if ((st = dalloc(c, 8 * 4, &p))) return st; P.counters = (uint32_t*)p;
@@ -367,7 +368,15 @@ void prof_begin(lowdiff_ctx* c, const char* name, cudaStream_t s, int* handle) {
   *handle = -1;
   if (!c->prof) return;
   ProfRec r{name, nullptr, nullptr};
-  if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
+  // events come from a pool that survives prof_enable: recording stays cheap inside a timed loop
+  const size_t need = 2 * (c->prof_recs.size() + 1);
+  while (c->prof_pool.size() < need) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    c->prof_pool.push_back(e);
+  }
+  r.a = c->prof_pool[need - 2];
+  r.b = c->prof_pool[need - 1];
   cudaEventRecord(r.a, s);
   c->prof_recs.push_back(r);
   *handle = (int)c->prof_recs.size() - 1;
@@ -383,7 +392,7 @@ extern "C" {
 int32_t lowdiff_abi_version(void) { return 1; }
 
 lowdiff_status lowdiff_selftest(int32_t which, uint64_t n, uint64_t seed, uint64_t* mismatches, uint64_t* first_bad) {
-  if (!mismatches || !first_bad || (which != 0 && which != 1)) return LOWDIFF_E_INVALID;
+  if (!mismatches || !first_bad || which < 0 || which > 2) return LOWDIFF_E_INVALID;
   return ld::run_selftest(which, n, seed, mismatches, first_bad) == cudaSuccess ? LOWDIFF_OK : LOWDIFF_E_CUDA;
 }
 
@@ -526,7 +535,7 @@ lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
   if (c->side) cudaStreamSynchronize(c->side);
   if (c->comm) ncclCommDestroy(c->comm);
   for (auto& s : c->slots) if (s.done) cudaEventDestroy(s.done);
-  for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : c->prof_pool) cudaEventDestroy(e);
   if (c->ring) cudaFreeHost(c->ring);
   if (c->err_pinned) cudaFreeHost(c->err_pinned);
   if (c->full_host) cudaFreeHost(c->full_host);
@@ -938,8 +947,7 @@ lowdiff_status lowdiff_get_stats(const lowdiff_ctx* c, lowdiff_stats* out) {
 lowdiff_status lowdiff_prof_enable(lowdiff_ctx* c, int32_t enable) {
   if (!c) return LOWDIFF_E_INVALID;
   cudaDeviceSynchronize();
-  for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
-  c->prof_recs.clear();
+  c->prof_recs.clear();   // the events stay in prof_pool for reuse
   c->prof = enable != 0;
   return LOWDIFF_OK;
 }

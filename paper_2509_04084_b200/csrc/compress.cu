@@ -131,6 +131,32 @@ __device__ __forceinline__ void warp_hist_add(uint32_t* h, bool m, uint32_t bin)
   }
 }
 
+// Segment table of chunk ch, warp-wide: lanes 0..15 end up holding the exclusive candidate offset
+// `so` of segment `lane`; returns the chunk's candidate total.  A chunk's candidates in index order
+// are segment 0's list, then segment 1's, ... (each list index-ordered by the scan).
+__device__ __forceinline__ uint32_t warp_segs(const DevPlan& P, int ch, uint32_t* so) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t c = lane < kSegsPerChunk ? P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] : 0u;
+  uint32_t inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  *so = inc - c;
+  return __shfl_sync(0xFFFFFFFFu, inc, 31);
+}
+// slot (within the chunk's 16384) of the chunk's c-th candidate: 4-step shuffle search; all lanes
+__device__ __forceinline__ uint32_t seg_slot(uint32_t so, uint32_t c) {
+  int s = 0;
+#pragma unroll
+  for (int step = kSegsPerChunk / 2; step; step >>= 1) {
+    const uint32_t t = __shfl_sync(0xFFFFFFFFu, so, s + step);
+    if (t <= c) s += step;
+  }
+  return (uint32_t)s * kSeg + (c - __shfl_sync(0xFFFFFFFFu, so, s));
+}
+
 // ---------------------------------------------------------------- small layers
 template <bool EF>
 __global__ void __launch_bounds__(kSmallThreads)
@@ -330,6 +356,16 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
       }
     }
     if (lane == 0) P.seg_count[(uint64_t)ch * kSegsPerChunk + seg] = run;
+    // digit-0 histogram and layer total of the candidates just written (L2-resident re-read;
+    // warp-aggregated global reductions keep the streaming loop itself lean)
+    __syncwarp();
+    uint32_t* h0 = P.hist + (uint64_t)slot * kHistRow;
+    for (uint32_t i0 = 0; i0 < run; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const bool m = i < run;
+      warp_hist_add(h0, m, m ? (uint32_t)(cd[i] >> 52) & 0x7FFu : 0u);
+    }
+    if (lane == 0 && run) atomicAdd(&P.layer_total[slot], run);
     if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
     if (!REFILL) break;
   }
@@ -414,11 +450,7 @@ __global__ void find_kernel(DevPlan P, int mode) {
   uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
   if (mode == 0) {
     const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
-    uint32_t tot = 0;
-#pragma unroll 8
-    for (int c = c0 + lane; c < c1; c += 32) tot += P.chunk_count[c];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+    const uint32_t tot = P.layer_total[slot];   // accumulated by the scan
     if (tot >= k) {
       uint32_t bin, above;
       warp_find_bin(hrow, kH0, k, &bin, &above);
@@ -500,14 +532,16 @@ __global__ void __launch_bounds__(256) digit_kernel(DevPlan P, int d) {
     const int slot = P.chunk_slot[ch];
     const uint32_t pre = P.sel[slot].prefix;
     uint32_t* h = uniform ? sh : P.hist + (uint64_t)slot * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
-    const uint32_t cnt = P.chunk_count[ch];
+    uint32_t so;
+    const uint32_t cnt = warp_segs(P, ch, &so);
     const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
     for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
       uint32_t key[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const uint32_t i = base + u * 32 + lane;
-        key[u] = i < cnt ? (uint32_t)(cd[i] >> 32) & 0x7FFFFFFFu : 0xFFFFFFFFu;
+        const uint32_t sl = seg_slot(so, i);
+        key[u] = i < cnt ? (uint32_t)(cd[sl] >> 32) & 0x7FFFFFFFu : 0xFFFFFFFFu;
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
@@ -532,15 +566,18 @@ __global__ void count_kernel(DevPlan P) {
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ch >= P.n_chunks) return;
   const uint32_t T = P.sel[P.chunk_slot[ch]].prefix;
-  const uint32_t cnt = P.chunk_count[ch];
+  uint32_t so;
+  const uint32_t cnt = warp_segs(P, ch, &so);
+  P.chunk_count[ch] = cnt;   // (same value from every lane) for emit
   const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
   uint32_t gt = 0, eq = 0;
   for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint32_t i = base + u * 32 + lane;
+      const uint32_t sl = seg_slot(so, i);
       if (i < cnt) {
-        const uint32_t key = (uint32_t)(cd[i] >> 32) & 0x7FFFFFFFu;
+        const uint32_t key = (uint32_t)(cd[sl] >> 32) & 0x7FFFFFFFu;
         gt += key > T;
         eq += key == T;
       }
@@ -596,7 +633,8 @@ __global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K) 
   const uint32_t take = P.chunk_take[ch];
   const bool last_tie_chunk = P.chunk_eq[ch] != 0u;
   const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + P.chunk_out[ch];
-  const uint32_t cnt = P.chunk_count[ch];
+  uint32_t so;
+  const uint32_t cnt = warp_segs(P, ch, &so);
   const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
   uint32_t eq_run = 0, out_run = 0;
   for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
@@ -604,7 +642,8 @@ __global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K) 
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint32_t i = base + u * 32 + lane;
-      v[u] = i < cnt ? cd[i] : 0ull;
+      const uint32_t sl = seg_slot(so, i);
+      v[u] = i < cnt ? cd[sl] : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -687,6 +726,8 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   if (!P.n_large) return cudaGetLastError();
   e = cudaMemsetAsync(P.hist, 0, compress_hist_bytes(P.n_large), s);
   if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(P.layer_total, 0, (size_t)P.n_large * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(P.counters, 0, 4 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const int sms = num_sms();
@@ -702,11 +743,9 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   else scan_kernel<false, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, 0);
   prof_end(c, h, s);
   prof_begin(c, "select", s, &h);
-  chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 0);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 0);
   if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, 0);
   else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, 0);
-  chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 1);
   digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 2);

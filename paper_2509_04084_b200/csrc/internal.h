@@ -24,7 +24,8 @@ constexpr int kChunk = 16384;          // elements per chunk (64 KB of fp32)
 constexpr int kSeg = 1024;             // candidate segment: the elements one scan warp streams
 constexpr int kSegsPerChunk = kChunk / kSeg;   // 16
 constexpr int kScanThreads = 512;      // threads per chunk CTA: 8 float4 slots each
-constexpr int kSmallMax = 16384;       // small-layer bound (64 KB smem for acc)
+constexpr int kSmallMax = 4096;        // small-layer bound: one CTA selects it in shared memory
+                                       // (larger layers go through the parallel chunk path)
 constexpr int kSmallThreads = 512;
 constexpr int kMergeTileShift = 13;
 constexpr int kMergeTile = 1 << kMergeTileShift;     // merge tile (elements per CTA)
@@ -65,6 +66,7 @@ struct DevPlan {
                                  //   written per segment by the scan, compacted per chunk by prep
   uint32_t* seg_count;           // [n_chunks * 16] candidates per segment (index-ordered inside)
   uint32_t* chunk_count;         // [n_chunks]
+  uint32_t* layer_total;         // [n_large] candidates admitted per large layer (this call)
   uint32_t* chunk_gt;            // [n_chunks]
   uint32_t* chunk_eq;            // [n_chunks]
   uint32_t* chunk_out;           // [n_chunks] output offset inside the layer

@@ -138,6 +138,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
     }
   }
   const float n = (float)world, inv = 1.0f / (float)world;
+  const bool eps_ok = ak.eps >= 0x1p-60f && ak.eps <= 0x1p59f;   // adam_u_fast's precondition
   const uint64_t tstride = (uint64_t)(n_tiles + 1);
   // Software pipeline over steps (everything that step s+1 needs from HBM is in flight while step
   // s computes): s_a/s_b[x & 1] in shared memory hold the entry ranges of step x for every rank;
@@ -229,8 +230,8 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
         // d = sqrt(vh) + eps ; u = mh / d ; p = p - lr*u          (R-11)
         // Correctly rounded sqrt / divide take the exact fast sequence (ieee_fast.cuh) for every
         // lane; a warp-rare fix-up redoes out-of-window operands with the intrinsics.
-        float mh[4], vh[4], d[4], u[4];
-        uint32_t slow = 0;
+        float mh[4], vh[4], u[4];
+        bool slow = !eps_ok;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int x = 4 * i + q;
@@ -239,21 +240,12 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
           mh[q] = __fmul_rn(M[x], sr1);
           vh[q] = __fmul_rn(V[x], sr2);
           bool sl;
-          d[q] = __fadd_rn(sqrt_rn_fast(vh[q], &sl), ak.eps);
-          slow |= (uint32_t)sl << q;
+          u[q] = adam_u_fast(mh[q], vh[q], ak.eps, &sl);
+          slow |= sl;
         }
+        if (slow) {   // rare: redo the whole group exactly with the intrinsics
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          bool sl;
-          u[q] = div_rn_fast(mh[q], d[q], &sl);
-          slow |= (uint32_t)sl << (4 + q);
-        }
-        if (slow) {   // static indices keep mh/vh/d/u in registers
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if ((slow >> q) & 1u) d[q] = __fadd_rn(__fsqrt_rn(vh[q]), ak.eps);
-            if ((slow >> q) & 0x11u) u[q] = __fdiv_rn(mh[q], d[q]);
-          }
+          for (int q = 0; q < 4; ++q) u[q] = __fdiv_rn(mh[q], __fadd_rn(__fsqrt_rn(vh[q]), ak.eps));
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) P[4 * i + q] = __fsub_rn(P[4 * i + q], __fmul_rn(slr, u[q]));

@@ -72,6 +72,35 @@ __global__ void div_check_kernel(uint64_t n, uint64_t seed, unsigned long long* 
   }
 }
 
+// which = 2: adam_u_fast(mh, vh, eps) + the exact fallback vs __fdiv_rn(mh, __fsqrt_rn(vh) + eps)
+__global__ void adam_check_kernel(uint64_t n, uint64_t seed, unsigned long long* bad, unsigned long long* first) {
+  const float eps_set[4] = {1e-8f, 1e-6f, 0x1p-60f, 1.0f};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = mix64(seed ^ mix64(i)), h2 = mix64(h);
+    const float eps = eps_set[h2 & 3];
+    uint32_t ua, uv;
+    if ((i & 1) == 0) {   // raw bit patterns (vh forced non-negative, as Adam's v*r2 is)
+      ua = (uint32_t)h;
+      uv = (uint32_t)(h >> 32) & 0x7FFFFFFFu;
+    } else {              // Adam's domain, zeros and window edges
+      const float mag = exp2f(-140.f + 270.f * (float)(h & 0xFFFFFF) / 16777216.f);
+      ua = __float_as_uint(((h >> 24) & 1) ? -mag : mag);
+      uv = __float_as_uint(exp2f(-140.f + 270.f * (float)((h >> 32) & 0xFFFFFF) / 16777216.f));
+      if ((h2 & 0x30) == 0) ua &= 0x80000000u;
+      if ((h2 & 0xC0) == 0) uv = 0;
+    }
+    const float mh = __uint_as_float(ua), vh = __uint_as_float(uv);
+    bool sl;
+    float u = adam_u_fast(mh, vh, eps, &sl);
+    if (sl) u = __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), eps));
+    const uint32_t x = __float_as_uint(u), y = __float_as_uint(__fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), eps)));
+    if (x != y && !((x & 0x7FFFFFFFu) > 0x7F800000u && (y & 0x7FFFFFFFu) > 0x7F800000u)) {
+      atomicAdd(bad, 1ull);
+      atomicMin(first, (unsigned long long)i);
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches, uint64_t* first) {
@@ -81,7 +110,8 @@ cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatc
   unsigned long long init[2] = {0ull, ~0ull};
   cudaMemcpy(d, init, 16, cudaMemcpyHostToDevice);
   if (which == 0) sqrt_check_kernel<<<148 * 16, 256>>>(d, d + 1);
-  else div_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
+  else if (which == 1) div_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
+  else adam_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
   e = cudaDeviceSynchronize();
   unsigned long long h[2] = {0, 0};
   if (e == cudaSuccess) e = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
