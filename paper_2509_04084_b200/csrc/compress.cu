@@ -356,28 +356,17 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
       }
     }
     if (lane == 0) P.seg_count[(uint64_t)ch * kSegsPerChunk + seg] = run;
-    // digit-0 histogram and layer total of the candidates just written (L2-resident re-read;
-    // warp-aggregated global reductions keep the streaming loop itself lean)
-    __syncwarp();
-    uint32_t* h0 = P.hist + (uint64_t)slot * kHistRow;
-    for (uint32_t i0 = 0; i0 < run; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const bool m = i < run;
-      warp_hist_add(h0, m, m ? (uint32_t)(cd[i] >> 52) & 0x7FFu : 0u);
-    }
-    if (lane == 0 && run) atomicAdd(&P.layer_total[slot], run);
     if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
     if (!REFILL) break;
   }
 }
 
-// ---------------------------------------------------------------- chunk prep (warp per chunk)
-// Compact the 16 segment lists of a chunk in place into one index-ordered list at the chunk's
-// base (a candidate never moves up, and each round loads before it stores, so no unread source is
-// overwritten), store the chunk total, and histogram the first radix digit -- in shared memory
-// when all chunks of the CTA belong to one layer (chunk slots are monotone), else directly.
-// only_refill: process just the chunks of refilled layers (after the rescan).
-__global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_refill) {
+// ---------------------------------------------------------------- digit-0 histogram (warp per chunk)
+// Reads the chunk's candidates in place (segment-addressed, no compaction), histograms the first
+// radix digit -- in shared memory when all 8 chunks of the CTA belong to one layer (chunk slots
+// are monotone), else with warp-aggregated global reductions -- and adds the chunk total to the
+// layer total.  only_refill: just the chunks of refilled layers (after the rescan).
+__global__ void __launch_bounds__(256) hist0_kernel(DevPlan P, int only_refill) {
   __shared__ uint32_t sh[kH0];
   const int lane = threadIdx.x & 31;
   const int c_first = blockIdx.x * 8;
@@ -391,39 +380,23 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_ref
   const int slot = ch <= c_last ? P.chunk_slot[ch] : P.chunk_slot[c_last];
   const bool active = ch <= c_last && (!only_refill || P.sel[slot].refill);
   if (active) {
-    const uint32_t c = lane < kSegsPerChunk ? P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] : 0u;
-    uint32_t inc = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    const uint32_t so = inc - c;                                  // lanes 0..15: segment offsets
-    const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, 31);
-    if (lane == 0) P.chunk_count[ch] = total;
-    uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
+    uint32_t so;
+    const uint32_t total = warp_segs(P, ch, &so);
+    if (lane == 0 && total && !only_refill) atomicAdd(&P.layer_total[slot], total);
+    const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
     uint32_t* h0 = uniform ? sh : P.hist + (uint64_t)slot * kHistRow;
     for (uint32_t base = 0; base < total; base += 32 * kUnroll) {
-      uint64_t v[kUnroll];
+      uint32_t bin[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const uint32_t cc = base + u * 32 + lane;
-        int s = 0;   // segment of candidate cc: max{s : so[s] <= cc}, by shuffles over lanes 0..15
-#pragma unroll
-        for (int step = 8; step; step >>= 1) {
-          const uint32_t t = __shfl_sync(0xFFFFFFFFu, so, s + step);
-          if (t <= cc) s += step;
-        }
-        const uint32_t sos = __shfl_sync(0xFFFFFFFFu, so, s);
-        v[u] = cc < total ? cd[(uint32_t)s * kSeg + (cc - sos)] : 0ull;
+        const uint32_t sl = seg_slot(so, cc);
+        bin[u] = cc < total ? (uint32_t)(cd[sl] >> 52) & 0x7FFu : 0xFFFFFFFFu;   // key bits [30:20]
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
-        const uint32_t cc = base + u * 32 + lane;
-        if (cc < total) cd[cc] = v[u];
-        const uint32_t bin = (uint32_t)(v[u] >> 52) & 0x7FFu;   // key bits [30:20]
-        if (uniform) { if (cc < total) atomicAdd(&h0[bin], 1u); }
-        else warp_hist_add(h0, cc < total, bin);
+        if (uniform) { if (bin[u] != 0xFFFFFFFFu) atomicAdd(&h0[bin[u]], 1u); }
+        else warp_hist_add(h0, bin[u] != 0xFFFFFFFFu, bin[u] & 0x7FFu);
       }
     }
   }
@@ -743,9 +716,11 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   else scan_kernel<false, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, 0);
   prof_end(c, h, s);
   prof_begin(c, "select", s, &h);
+  hist0_kernel<<<chunk_blocks, 256, 0, s>>>(P, 0);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 0);
   if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, 0);
   else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, 0);
+  hist0_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 1);
   digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 2);
