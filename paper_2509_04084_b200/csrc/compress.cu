@@ -131,32 +131,6 @@ __device__ __forceinline__ void warp_hist_add(uint32_t* h, bool m, uint32_t bin)
   }
 }
 
-// Segment table of chunk ch, warp-wide: lanes 0..15 end up holding the exclusive candidate offset
-// `so` of segment `lane`; returns the chunk's candidate total.  A chunk's candidates in index order
-// are segment 0's list, then segment 1's, ... (each list index-ordered by the scan).
-__device__ __forceinline__ uint32_t warp_segs(const DevPlan& P, int ch, uint32_t* so) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t c = lane < kSegsPerChunk ? P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] : 0u;
-  uint32_t inc = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  *so = inc - c;
-  return __shfl_sync(0xFFFFFFFFu, inc, 31);
-}
-// slot (within the chunk's 16384) of the chunk's c-th candidate: 4-step shuffle search; all lanes
-__device__ __forceinline__ uint32_t seg_slot(uint32_t so, uint32_t c) {
-  int s = 0;
-#pragma unroll
-  for (int step = kSegsPerChunk / 2; step; step >>= 1) {
-    const uint32_t t = __shfl_sync(0xFFFFFFFFu, so, s + step);
-    if (t <= c) s += step;
-  }
-  return (uint32_t)s * kSeg + (c - __shfl_sync(0xFFFFFFFFu, so, s));
-}
-
 // ---------------------------------------------------------------- small layers
 template <bool EF>
 __global__ void __launch_bounds__(kSmallThreads)
@@ -361,12 +335,13 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
   }
 }
 
-// ---------------------------------------------------------------- digit-0 histogram (warp per chunk)
-// Reads the chunk's candidates in place (segment-addressed, no compaction), histograms the first
-// radix digit -- in shared memory when all 8 chunks of the CTA belong to one layer (chunk slots
-// are monotone), else with warp-aggregated global reductions -- and adds the chunk total to the
-// layer total.  only_refill: just the chunks of refilled layers (after the rescan).
-__global__ void __launch_bounds__(256) hist0_kernel(DevPlan P, int only_refill) {
+// ---------------------------------------------------------------- chunk prep (warp per chunk)
+// Compact the 16 segment lists of a chunk in place into one index-ordered list at the chunk's
+// base (a candidate never moves up, and each round loads before it stores, so no unread source is
+// overwritten), store the chunk total, and histogram the first radix digit -- in shared memory
+// when all chunks of the CTA belong to one layer (chunk slots are monotone), else directly.
+// only_refill: process just the chunks of refilled layers (after the rescan).
+__global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_refill) {
   __shared__ uint32_t sh[kH0];
   const int lane = threadIdx.x & 31;
   const int c_first = blockIdx.x * 8;
@@ -380,23 +355,39 @@ __global__ void __launch_bounds__(256) hist0_kernel(DevPlan P, int only_refill) 
   const int slot = ch <= c_last ? P.chunk_slot[ch] : P.chunk_slot[c_last];
   const bool active = ch <= c_last && (!only_refill || P.sel[slot].refill);
   if (active) {
-    uint32_t so;
-    const uint32_t total = warp_segs(P, ch, &so);
-    if (lane == 0 && total && !only_refill) atomicAdd(&P.layer_total[slot], total);
-    const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
+    const uint32_t c = lane < kSegsPerChunk ? P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] : 0u;
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const uint32_t so = inc - c;                                  // lanes 0..15: segment offsets
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    if (lane == 0) P.chunk_count[ch] = total;
+    uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
     uint32_t* h0 = uniform ? sh : P.hist + (uint64_t)slot * kHistRow;
     for (uint32_t base = 0; base < total; base += 32 * kUnroll) {
-      uint32_t bin[kUnroll];
+      uint64_t v[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const uint32_t cc = base + u * 32 + lane;
-        const uint32_t sl = seg_slot(so, cc);
-        bin[u] = cc < total ? (uint32_t)(cd[sl] >> 52) & 0x7FFu : 0xFFFFFFFFu;   // key bits [30:20]
+        int s = 0;   // segment of candidate cc: max{s : so[s] <= cc}, by shuffles over lanes 0..15
+#pragma unroll
+        for (int step = 8; step; step >>= 1) {
+          const uint32_t t = __shfl_sync(0xFFFFFFFFu, so, s + step);
+          if (t <= cc) s += step;
+        }
+        const uint32_t sos = __shfl_sync(0xFFFFFFFFu, so, s);
+        v[u] = cc < total ? cd[(uint32_t)s * kSeg + (cc - sos)] : 0ull;
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
-        if (uniform) { if (bin[u] != 0xFFFFFFFFu) atomicAdd(&h0[bin[u]], 1u); }
-        else warp_hist_add(h0, bin[u] != 0xFFFFFFFFu, bin[u] & 0x7FFu);
+        const uint32_t cc = base + u * 32 + lane;
+        if (cc < total) cd[cc] = v[u];
+        const uint32_t bin = (uint32_t)(v[u] >> 52) & 0x7FFu;   // key bits [30:20]
+        if (uniform) { if (cc < total) atomicAdd(&h0[bin], 1u); }
+        else warp_hist_add(h0, cc < total, bin);
       }
     }
   }
@@ -423,7 +414,11 @@ __global__ void find_kernel(DevPlan P, int mode) {
   uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
   if (mode == 0) {
     const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
-    const uint32_t tot = P.layer_total[slot];   // accumulated by the scan
+    uint32_t tot = 0;
+#pragma unroll 8
+    for (int c = c0 + lane; c < c1; c += 32) tot += P.chunk_count[c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
     if (tot >= k) {
       uint32_t bin, above;
       warp_find_bin(hrow, kH0, k, &bin, &above);
@@ -431,9 +426,10 @@ __global__ void find_kernel(DevPlan P, int mode) {
         S.prefix = bin; S.kleft = k - above; S.total = tot; S.refill = 0;
         // adapt the band: the previous call chose it to admit `band` x k keys of ITS distribution;
         // under error feedback the accumulated values drift upward between calls, so the band
-        // admitted tot / k x k now.  Aim the next band at 1.5 k_l admitted.
+        // admitted tot / k x k now.  Aim the next band at 1.5 k_l admitted; the band may sit above
+        // this call's T (band < 1) when the drift alone admits more than that.
         const float b = S.band > 0.f ? S.band : 1.5f;
-        S.band = fminf(4.f, fmaxf(1.02f, b * 1.5f * (float)k / (float)tot));
+        S.band = fminf(4.f, fmaxf(0.25f, b * 1.5f * (float)k / (float)tot));
         atomicAdd(&P.counters[1], 1u);
         atomicAdd(&P.counters[3], tot);
       }
@@ -444,7 +440,7 @@ __global__ void find_kernel(DevPlan P, int mode) {
         base = atomicAdd(&P.counters[0], (uint32_t)(c1 - c0));
         S.refill = 1;
         S.total = (uint32_t)(P.layer_off[li + 1] - P.layer_off[li]);
-        S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : 1.5f;   // missed: widen
+        S.band = S.band > 0.f ? fminf(4.f, fmaxf(1.5f, S.band * 2.f)) : 1.5f;   // missed: widen
         atomicAdd(&P.counters[2], 1u);
       }
       base = __shfl_sync(0xFFFFFFFFu, base, 0);
@@ -465,7 +461,7 @@ __global__ void find_kernel(DevPlan P, int mode) {
       // it (digit-0 resolution, refined with the digit-1 histogram when C falls in T's digit-0
       // bin).  Only a prediction -- the next call checks #candidates >= k_l and refills otherwise.
       const float band = S.band > 0.f ? S.band : 1.5f;
-      const uint32_t C = max(k + 32u, (uint32_t)fminf((float)k * band, 4.0e9f));
+      const uint32_t C = max(1u, (uint32_t)fminf((float)k * band, 4.0e9f));
       uint32_t nt = P.thr[slot];
       if (S.total >= C) {
         uint32_t b0, a0;
@@ -505,16 +501,14 @@ __global__ void __launch_bounds__(256) digit_kernel(DevPlan P, int d) {
     const int slot = P.chunk_slot[ch];
     const uint32_t pre = P.sel[slot].prefix;
     uint32_t* h = uniform ? sh : P.hist + (uint64_t)slot * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
-    uint32_t so;
-    const uint32_t cnt = warp_segs(P, ch, &so);
+    const uint32_t cnt = P.chunk_count[ch];
     const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
     for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
       uint32_t key[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const uint32_t i = base + u * 32 + lane;
-        const uint32_t sl = seg_slot(so, i);
-        key[u] = i < cnt ? (uint32_t)(cd[sl] >> 32) & 0x7FFFFFFFu : 0xFFFFFFFFu;
+        key[u] = i < cnt ? (uint32_t)(cd[i] >> 32) & 0x7FFFFFFFu : 0xFFFFFFFFu;
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
@@ -539,18 +533,15 @@ __global__ void count_kernel(DevPlan P) {
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ch >= P.n_chunks) return;
   const uint32_t T = P.sel[P.chunk_slot[ch]].prefix;
-  uint32_t so;
-  const uint32_t cnt = warp_segs(P, ch, &so);
-  P.chunk_count[ch] = cnt;   // (same value from every lane) for emit
+  const uint32_t cnt = P.chunk_count[ch];
   const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
   uint32_t gt = 0, eq = 0;
   for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint32_t i = base + u * 32 + lane;
-      const uint32_t sl = seg_slot(so, i);
       if (i < cnt) {
-        const uint32_t key = (uint32_t)(cd[sl] >> 32) & 0x7FFFFFFFu;
+        const uint32_t key = (uint32_t)(cd[i] >> 32) & 0x7FFFFFFFu;
         gt += key > T;
         eq += key == T;
       }
@@ -588,9 +579,8 @@ __global__ void __launch_bounds__(1024) layer_scan_kernel(DevPlan P) {
   }
   if (threadIdx.x == 0) {
     P.sel_T[slot] = T;
-    // speculative band for the next call, never above this call's T
-    const uint32_t nt = P.sel[slot].next_thr;
-    P.thr[slot] = nt <= T ? nt : T;
+    // speculative band for the next call; it may exceed this call's T
+    P.thr[slot] = P.sel[slot].next_thr;
   }
 }
 
@@ -606,8 +596,7 @@ __global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K) 
   const uint32_t take = P.chunk_take[ch];
   const bool last_tie_chunk = P.chunk_eq[ch] != 0u;
   const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + P.chunk_out[ch];
-  uint32_t so;
-  const uint32_t cnt = warp_segs(P, ch, &so);
+  const uint32_t cnt = P.chunk_count[ch];
   const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
   uint32_t eq_run = 0, out_run = 0;
   for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
@@ -615,8 +604,7 @@ __global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K) 
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint32_t i = base + u * 32 + lane;
-      const uint32_t sl = seg_slot(so, i);
-      v[u] = i < cnt ? cd[sl] : 0ull;
+      v[u] = i < cnt ? cd[i] : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -699,8 +687,6 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   if (!P.n_large) return cudaGetLastError();
   e = cudaMemsetAsync(P.hist, 0, compress_hist_bytes(P.n_large), s);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(P.layer_total, 0, (size_t)P.n_large * sizeof(uint32_t), s);
-  if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(P.counters, 0, 4 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const int sms = num_sms();
@@ -716,11 +702,11 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   else scan_kernel<false, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, 0);
   prof_end(c, h, s);
   prof_begin(c, "select", s, &h);
-  hist0_kernel<<<chunk_blocks, 256, 0, s>>>(P, 0);
+  chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 0);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 0);
   if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, 0);
   else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, 0);
-  hist0_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
+  chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 1);
   digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 2);
