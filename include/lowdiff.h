@@ -238,6 +238,20 @@ lowdiff_status lowdiff_write_batch_host(const lowdiff_config *cfg, int64_t first
 /* Serialise this rank's full-checkpoint shard from host arrays of length Psi (host only). */
 lowdiff_status lowdiff_write_full_host(const lowdiff_config *cfg, int64_t iteration, const float *p,
                                        const float *m, const float *v);
+/* ---- checkpointing configuration (§4.3, Eq. 3-5; module PAPER.md:454-455)
+ * System parameters of the wasted-time model, all times in ONE unit (R-25 uses
+ * iterations): N GPUs, M mean time between failures, W write bandwidth (bytes per time unit),
+ * S full-checkpoint bytes, T total run time, R_F time to load a full checkpoint, R_D time to
+ * merge one differential. */
+typedef struct { double N, M, W, S, T, R_F, R_D; } lowdiff_sys_params;
+/* Eq. 3: T_wasted(f, b) for f full checkpoints per time unit and b differentials per batch. */
+lowdiff_status lowdiff_wasted_time(const lowdiff_sys_params *p, double f, double b, double *out);
+/* Eq. 5: the stationary point f* = cbrt(R_D W^2/(4 S^2 M^2)), b* = cbrt(2 S R_D M / W). */
+lowdiff_status lowdiff_optimal_config(const lowdiff_sys_params *p, double *f_star, double *b_star);
+/* One stepwise adaptation of the integer configuration (full-checkpoint interval *fcf in time
+ * units, batch size *batch) toward the rounded optimum, applied only if it lowers Eq. 3. */
+lowdiff_status lowdiff_config_step(const lowdiff_sys_params *p, int64_t *fcf, int32_t *batch);
+
 int32_t lowdiff_abi_version(void);
 /* Device self-test of the branch-free IEEE sqrt/division used by the replay kernel against
  * __fsqrt_rn/__fdiv_rn (which = 0: all 2^31+1 non-negative floats; which = 1: n pseudo-random

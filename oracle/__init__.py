@@ -58,6 +58,10 @@ def lib():
                                                  C.c_uint32, P, P, P, P, P, C.c_uint64]
         L.lowdiff_ref_recover.argtypes = [C.c_char_p, C.c_uint32, C.c_int, P, C.c_uint32, C.c_int64,
                                           P, P, P, P]
+        L.lowdiff_ref_wasted_time.restype = C.c_double
+        L.lowdiff_ref_wasted_time.argtypes = [C.c_double] * 9
+        L.lowdiff_ref_optimal_config.restype = None
+        L.lowdiff_ref_optimal_config.argtypes = [C.c_double] * 4 + [C.POINTER(C.c_double)] * 2
         _lib = L
     return _lib
 
@@ -199,3 +203,15 @@ def recover(directory, world, sizes, ppm, target=-1, with_moments=True):
     _check("recover", lib().lowdiff_ref_recover(str(directory).encode(), world, len(sizes), _p(numel), ppm,
                                                 target, _p(p), _p(m), _p(v), _p(rec)))
     return p, m, v, int(rec[0])
+
+
+def wasted_time(N, M, W, S, T, R_F, R_D, f, b):
+    """Eq. 3, term by term (see oracle/lowdiff_ref.cpp)."""
+    return float(lib().lowdiff_ref_wasted_time(N, M, W, S, T, R_F, R_D, f, b))
+
+
+def optimal_config(M, W, S, R_D):
+    """Eq. 5 (PAPER.md:345-348)."""
+    f, b = C.c_double(), C.c_double()
+    lib().lowdiff_ref_optimal_config(M, W, S, R_D, C.byref(f), C.byref(b))
+    return f.value, b.value

@@ -453,4 +453,34 @@ int lowdiff_ref_recover(const char* dir, uint32_t world, int n_layers, const int
   return OK;
 }
 
+// --------------------------------------------------------------------------
+// Checkpointing configuration, §4.3 "Configuration Modeling", written
+// term by term from the itemised list PAPER.md:322-330 (one time unit throughout, R-25):
+//   failures            = T / M
+//   full-ckpt write     = S / W
+//   full checkpoints    = f x T
+//   lost work           = N x T/M x b/2
+//   merges on average   = 1/2 (1/f x 1/b - 1)
+//   recovery time       = N x T/M x (R_F + R_D x merges)
+//   steady-state cost   = N x S/W x f x T
+//   T_wasted            = recovery time + lost work + steady-state cost        (Eq. 3)
+// and the optimum stated by Eq. 5.
+// --------------------------------------------------------------------------
+double lowdiff_ref_wasted_time(double N, double M, double W, double S, double T, double R_F, double R_D,
+                               double f, double b) {
+  const double failures = T / M;
+  const double full_ckpt_write = S / W;
+  const double full_ckpts = f * T;
+  const double lost_work = N * failures * (b / 2.0);
+  const double merges = 0.5 * (1.0 / f * 1.0 / b - 1.0);
+  const double recovery = N * failures * (R_F + R_D * merges);
+  const double steady = N * full_ckpt_write * full_ckpts;
+  return recovery + lost_work + steady;
+}
+
+void lowdiff_ref_optimal_config(double M, double W, double S, double R_D, double* f_star, double* b_star) {
+  *f_star = std::cbrt(R_D * W * W / (4.0 * S * S * M * M));
+  *b_star = std::cbrt(2.0 * S * R_D * M / W);
+}
+
 }  // extern "C"

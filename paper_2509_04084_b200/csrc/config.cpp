@@ -1,0 +1,62 @@
+// Checkpointing configuration (NEXT-4): the wasted-time model and its optimum, §4.3
+// "Optimizing Checkpointing Configuration" and the optimal configuration
+// module.  Host arithmetic only, in double.  All time quantities share one
+// unit (R-25 reads the model in iterations: f = full checkpoints per iteration, so the
+// full-checkpoint interval FCF = 1/f iterations; b = differentials per batched write).
+#include <cmath>
+
+#include "../../include/lowdiff.h"
+
+namespace {
+bool valid(const lowdiff_sys_params* p) {
+  return p && p->N > 0 && p->M > 0 && p->W > 0 && p->S > 0 && p->T > 0 && p->R_F >= 0 && p->R_D > 0;
+}
+}  // namespace
+
+extern "C" {
+
+// Eq. 3:
+//   T_wasted = (N T / M) (b/2 + R_F + R_D/2 (1/(f b) - 1)) + N T S f / W
+lowdiff_status lowdiff_wasted_time(const lowdiff_sys_params* p, double f, double b, double* out) {
+  if (!valid(p) || !out || f <= 0 || b <= 0) return LOWDIFF_E_INVALID;
+  const double failures = p->N * p->T / p->M;                      // N x (T / M)
+  const double recovery = b / 2.0 + p->R_F + p->R_D / 2.0 * (1.0 / (f * b) - 1.0);
+  const double steady = p->N * p->T * p->S * f / p->W;              // N x (S / W) x f T
+  *out = failures * recovery + steady;
+  return LOWDIFF_OK;
+}
+
+// Eq. 5, from the first-order conditions of Eq. 4:
+//   f* = cbrt(R_D W^2 / (4 S^2 M^2)),   b* = cbrt(2 S R_D M / W)
+lowdiff_status lowdiff_optimal_config(const lowdiff_sys_params* p, double* f_star, double* b_star) {
+  if (!valid(p) || !f_star || !b_star) return LOWDIFF_E_INVALID;
+  *f_star = std::cbrt(p->R_D * p->W * p->W / (4.0 * p->S * p->S * p->M * p->M));
+  *b_star = std::cbrt(2.0 * p->S * p->R_D * p->M / p->W);
+  return LOWDIFF_OK;
+}
+
+// Stepwise runtime adaptation: move the integer configuration (full-checkpoint
+// interval in iterations, batch size) one step toward the rounded Eq. 5 optimum for the current
+// parameter estimates -- one iteration of FCF change per 10% of distance (at least 1), one batch
+// step -- but only while the step lowers Eq. 3.
+lowdiff_status lowdiff_config_step(const lowdiff_sys_params* p, int64_t* fcf, int32_t* batch) {
+  if (!valid(p) || !fcf || !batch || *fcf < 1 || *batch < 1) return LOWDIFF_E_INVALID;
+  double fs, bs;
+  lowdiff_optimal_config(p, &fs, &bs);
+  const int64_t fcf_t = std::llround(std::fmax(1.0, 1.0 / fs));
+  const int32_t b_t = (int32_t)std::lround(std::fmax(1.0, bs));
+  int64_t nf = *fcf;
+  if (nf != fcf_t) {
+    const int64_t d = fcf_t - nf, mag = d > 0 ? d : -d;
+    const int64_t stp = mag / 10 > 0 ? mag / 10 : 1;
+    nf += d > 0 ? stp : -stp;
+  }
+  int32_t nb = *batch + (b_t > *batch ? 1 : (b_t < *batch ? -1 : 0));
+  double cur, nxt;
+  lowdiff_wasted_time(p, 1.0 / (double)*fcf, (double)*batch, &cur);
+  lowdiff_wasted_time(p, 1.0 / (double)nf, (double)nb, &nxt);
+  if (nxt <= cur) { *fcf = nf; *batch = nb; }
+  return LOWDIFF_OK;
+}
+
+}  // extern "C"

@@ -46,6 +46,10 @@ class Config(C.Structure):
                 ("fsync", C.c_int32), ("optim", C.c_int32), ("adam", AdamConsts)]
 
 
+class SysParams(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("N", "M", "W", "S", "T", "R_F", "R_D")]
+
+
 class Stats(C.Structure):
     _fields_ = [("files_written", C.c_int64), ("bytes_written", C.c_int64), ("ring_stall_ns", C.c_int64),
                 ("writer_busy_ns", C.c_int64), ("spec_hits", C.c_int64), ("spec_misses", C.c_int64),
@@ -93,6 +97,9 @@ def lib():
             "write_full_host": ([C.POINTER(Config), C.c_int64, P, P, P], S),
             "abi_version": ([], C.c_int32),
             "selftest": ([C.c_int32, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], S),
+            "wasted_time": ([C.POINTER(SysParams), C.c_double, C.c_double, C.POINTER(C.c_double)], S),
+            "optimal_config": ([C.POINTER(SysParams), C.POINTER(C.c_double), C.POINTER(C.c_double)], S),
+            "config_step": ([C.POINTER(SysParams), C.POINTER(C.c_int64), C.POINTER(C.c_int32)], S),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, "lowdiff_" + name)
@@ -106,7 +113,28 @@ EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_mater
             "full_ckpt", "wait_persist", "recover", "replay", "snapshot_layer", "snapshot_wait", "sync", "get_stats",
             "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
             "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host",
-            "write_full_host", "abi_version", "selftest"]
+            "write_full_host", "abi_version", "selftest", "wasted_time", "optimal_config", "config_step"]
+
+
+def wasted_time(params: dict, f: float, b: float) -> float:
+    """Eq. 3 of the paper; params keys N, M, W, S, T, R_F, R_D."""
+    out = C.c_double()
+    _check("wasted_time", lib().lowdiff_wasted_time(C.byref(SysParams(**params)), f, b, C.byref(out)))
+    return out.value
+
+
+def optimal_config(params: dict):
+    """Eq. 5 (PAPER.md:345-348): (f*, b*)."""
+    f, b = C.c_double(), C.c_double()
+    _check("optimal_config", lib().lowdiff_optimal_config(C.byref(SysParams(**params)), C.byref(f), C.byref(b)))
+    return f.value, b.value
+
+
+def config_step(params: dict, fcf: int, batch: int):
+    """One stepwise adaptation of (full-checkpoint interval, batch size)."""
+    f, b = C.c_int64(fcf), C.c_int32(batch)
+    _check("config_step", lib().lowdiff_config_step(C.byref(SysParams(**params)), C.byref(f), C.byref(b)))
+    return f.value, b.value
 
 
 def selftest(which: int, n: int = 0, seed: int = 0):

@@ -1,0 +1,89 @@
+"""NEXT-4: checkpointing configuration (§4.3, Eq. 3-5; module PAPER.md:454-455).
+
+Pins: the oracle's Eq. 3 is written term by term from the itemised model; its
+Eq. 5 optimum is checked against a brute-force grid minimisation of Eq. 3 and against the
+first-order conditions (Eq. 4) by finite differences; the qualitative shape of Table 1 (the
+optimal batch size grows with the full-checkpoint interval) is checked on the model.  The product
+(C ABI) must agree with the oracle."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_2509_04084_b200 as ld
+from paper_2509_04084_b200 import lowdiff as B
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+# a GPT-2-S-like setting in iteration units: 1.4 GB full checkpoint, 2 GB/s SSD at 0.3 s/iteration,
+# 8 GPUs, MTBF 2 h at 0.3 s/iteration, 1e5 iterations, R_F = 5 iterations, R_D = 0.2 iterations
+CASES = [
+    dict(N=8, M=24000, W=0.6e9, S=1.4e9, T=1e5, R_F=5.0, R_D=0.2),
+    dict(N=64, M=1800, W=2e9, S=8.7e9, T=5e4, R_F=20.0, R_D=1.0),
+    dict(N=1, M=1e6, W=5e8, S=3e8, T=1e6, R_F=1.0, R_D=0.05),
+]
+
+
+def ref_args(p):
+    return (p["N"], p["M"], p["W"], p["S"], p["T"], p["R_F"], p["R_D"])
+
+
+@pytest.mark.parametrize("p", CASES)
+def test_oracle_closed_form_is_grid_minimum(ref, p):
+    f_star, b_star = ref.optimal_config(p["M"], p["W"], p["S"], p["R_D"])
+    fs = f_star * np.exp(np.linspace(-1.5, 1.5, 301))
+    bs = b_star * np.exp(np.linspace(-1.5, 1.5, 301))
+    grid = np.array([[ref.wasted_time(*ref_args(p), f, b) for b in bs] for f in fs])
+    i, j = np.unravel_index(np.argmin(grid), grid.shape)
+    assert abs(math.log(fs[i] / f_star)) <= 0.011 and abs(math.log(bs[j] / b_star)) <= 0.011
+    # Eq. 4: both partial derivatives vanish at the optimum (central differences)
+    h = 1e-6
+    tw = lambda f, b: ref.wasted_time(*ref_args(p), f, b)
+    df = (tw(f_star * (1 + h), b_star) - tw(f_star * (1 - h), b_star)) / (2 * h * f_star)
+    db = (tw(f_star, b_star * (1 + h)) - tw(f_star, b_star * (1 - h))) / (2 * h * b_star)
+    scale = tw(f_star, b_star)
+    assert abs(df * f_star) < 1e-5 * scale and abs(db * b_star) < 1e-5 * scale
+
+
+def test_table1_shape(ref):
+    """Table 1: the best BS per row is non-decreasing in FCF.  The model gives
+    b_opt(f) = sqrt(R_D / f) for a fixed f, which grows with the interval 1/f."""
+    rows = [ln for ln in open(os.path.join(GOLD, "table1_fcf_bs.txt")) if ln.strip() and not ln.startswith("#")]
+    paper_best = []
+    for ln in rows:
+        fcf, vals = ln.split("|")
+        paper_best.append((int(fcf), 1 + int(np.argmin([float(x) for x in vals.split()]))))
+    assert [b for _, b in paper_best] == sorted(b for _, b in paper_best) == [2, 2, 3, 3]
+    p = dict(N=8, M=24000, W=0.6e9, S=1.4e9, T=1e5, R_F=5.0, R_D=0.1)
+    model_best = []
+    for fcf, _ in paper_best:
+        vals = [ref.wasted_time(*ref_args(p), 1.0 / fcf, b) for b in range(1, 7)]
+        model_best.append(1 + int(np.argmin(vals)))
+    assert model_best == sorted(model_best) and model_best[0] < model_best[-1]
+
+
+@pytest.mark.parametrize("p", CASES)
+def test_product_matches_oracle(ref, p):
+    f, b = ld.lowdiff.optimal_config(p)
+    rf, rb = ref.optimal_config(p["M"], p["W"], p["S"], p["R_D"])
+    assert f == rf and b == rb
+    for ff in (f, 2 * f, 0.5 * f):
+        for bb in (1.0, b, 3.0):
+            assert math.isclose(B.wasted_time(p, ff, bb), ref.wasted_time(*ref_args(p), ff, bb), rel_tol=1e-12)
+
+
+@pytest.mark.parametrize("p", CASES)
+def test_stepwise_adaptation_converges_and_never_worsens(ref, p):
+    f_star, b_star = ref.optimal_config(p["M"], p["W"], p["S"], p["R_D"])
+    fcf, batch = 1, 1
+    prev = ref.wasted_time(*ref_args(p), 1.0 / fcf, batch)
+    for _ in range(200):
+        fcf, batch = B.config_step(p, fcf, batch)
+        cur = ref.wasted_time(*ref_args(p), 1.0 / fcf, batch)
+        assert cur <= prev * (1 + 1e-12)
+        prev = cur
+    assert abs(fcf - round(1.0 / f_star)) <= max(1, 0.1 * round(1.0 / f_star))
+    assert abs(batch - round(b_star)) <= 1
+    with pytest.raises(ld.LowDiffError):
+        B.config_step(dict(p, M=0.0), 10, 2)
