@@ -182,7 +182,8 @@ lowdiff_status lowdiff_replay(lowdiff_ctx *ctx, int32_t optim, int32_t world, in
  *    after the caller's gradient sync of layers [first_layer, first_layer+n_layers)
  *    (contiguous in the flat gradient; grad_bucket points at layer first_layer), copy
  *    them D2H on a side stream into the pinned buffer of `iteration` (double-buffered:
- *    iterations t and t+1 may be in flight). */
+ *    iterations t and t+1 may be in flight).  grad_bucket must not be rewritten before the
+ *    copy has read it: lowdiff_wait_persist(ctx, s) orders stream s after it. */
 lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx *ctx, int64_t iteration, int32_t first_layer,
                                       int32_t n_layers, const float *grad_bucket, void *producer);
 
@@ -190,6 +191,48 @@ lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx *ctx, int64_t iteration, int32
  *    f32[Psi] valid until iteration + 2 is first snapshotted.  LOWDIFF_E_STATE if some
  *    layer of that iteration was never submitted. */
 lowdiff_status lowdiff_snapshot_wait(lowdiff_ctx *ctx, int64_t iteration, const float **host_grad);
+
+/* ---- LowDiff+ CPU replica (Sec. 5.2; Alg. 2 l.11-13) ----
+ * A host-resident copy of this rank's shard [floor(rank*Psi/world), floor((rank+1)*Psi/world))
+ * of (p, m, v), advanced on a worker thread by the snapshotted synced gradients with the host
+ * optimizer (bitwise equal to the device replay), persisted as a regular .ldf shard, and
+ * restored to the GPU after a software failure.
+ *
+ * replica_init: (re)start the replica from the device state (p, m, v; m, v may be NULL -> zeros)
+ *    after `iteration` optimizer steps; the D2H copy is ordered after `producer`'s prior work and
+ *    `producer` waits for it (write-after-read).  threads = host threads of the optimizer (>= 1).
+ *    Pinned host memory: 12 * shard bytes.  Pending work of a previous replica is drained first. */
+lowdiff_status lowdiff_replica_init(lowdiff_ctx *ctx, int64_t iteration, const float *p, const float *m,
+                                    const float *v, int32_t threads, void *producer);
+/* replica_step: queue M^C_t = M^C_{t-1} + Opt(G_t) for t = `iteration` = (replica iteration after
+ *    the queued steps) + 1, G_t = the gradient snapshotted for `iteration` (every layer must have
+ *    been submitted with lowdiff_snapshot_layer: else LOWDIFF_E_STATE), scalars = that step's
+ *    scalars.  Returns at once; while the step is pending, lowdiff_snapshot_layer for
+ *    iteration + 2 blocks (the snapshot buffer is still being read; counted in replica_stall_ns). */
+lowdiff_status lowdiff_replica_step(lowdiff_ctx *ctx, int64_t iteration, const lowdiff_step_scalars *scalars);
+/* replica_persist: queue a persist of the replica as it stands after the queued steps, as
+ *    ld_full_r{rank}_{iteration}.ldf (same format and sharding as lowdiff_full_ckpt, so
+ *    lowdiff_recover uses it as a full checkpoint).  The worker copies the shard to a staging
+ *    buffer and a writer thread writes it while the replica keeps advancing. */
+lowdiff_status lowdiff_replica_persist(lowdiff_ctx *ctx);
+/* replica_wait: drain the queue (and the persist writer); *iteration = replica iteration.
+ *    *p, *m, *v (any may be NULL) = host pointers to the shard (valid until the next call that
+ *    queues work or destroys the context); *shard_begin / *shard_end = the shard range. */
+lowdiff_status lowdiff_replica_wait(lowdiff_ctx *ctx, int64_t *iteration, const float **p, const float **m,
+                                    const float **v, int64_t *shard_begin, int64_t *shard_end);
+/* replica_restore: drain, then copy the replica into device p, m, v (f32[Psi]; m, v may be NULL
+ *    for SGD): this rank's shard H2D, the other shards by an NCCL broadcast from their owners
+ *    (world > 1: every rank must call it; needs an NCCL context).  Synchronous on `stream`;
+ *    *iteration = the restored iteration. */
+lowdiff_status lowdiff_replica_restore(lowdiff_ctx *ctx, float *p, float *m, float *v, int64_t *iteration,
+                                       void *stream);
+/* Host optimizer used by the replica (no context; element-wise over n, split over `threads`
+ *    host threads): Adam in the op order of DESIGN.md R-11 / SGD p -= lr * G, IEEE single
+ *    precision, no contraction.  Arrays are host memory, p/m/v updated in place. */
+lowdiff_status lowdiff_host_adam_step(int64_t n, const float *G, const lowdiff_adam_consts *consts,
+                                      const lowdiff_step_scalars *scalars, float *p, float *m, float *v,
+                                      int32_t threads);
+lowdiff_status lowdiff_host_sgd_step(int64_t n, const float *G, float lr, float *p, int32_t threads);
 
 /* Drain D2H copies and the writer (flushing a final partial batch) and
  * surface deferred errors. */
@@ -201,6 +244,8 @@ typedef struct {
   int64_t writer_busy_ns;      /* writer thread time spent building + writing files            */
   int64_t spec_hits, spec_misses;   /* large layers selected from the speculative band / refilled */
   int64_t spec_candidates;          /* candidates the band admitted in those hit layers (last call) */
+  int64_t replica_busy_ns;          /* replica worker time spent in the host optimizer            */
+  int64_t replica_stall_ns;         /* host time lowdiff_snapshot_layer waited for the replica    */
 } lowdiff_stats;
 lowdiff_status lowdiff_get_stats(const lowdiff_ctx *ctx, lowdiff_stats *out);
 

@@ -64,6 +64,37 @@ void set_deferred(lowdiff_ctx* c, lowdiff_status st, const std::string& msg) {
   if (st == LOWDIFF_E_CUDA) c->poisoned = st;
 }
 
+// 96-byte .ldf header: shard [sb, se) of p | m | v after `iteration` steps
+std::vector<uint8_t> ldf_header(const lowdiff_config& cfg, int64_t iteration, uint64_t psi, uint64_t sb, uint64_t se) {
+  std::vector<uint8_t> hdr(96, 0);
+  std::memcpy(hdr.data(), "LDF1", 4);
+  const uint16_t ver = 1, flags = (uint16_t)((cfg.error_feedback ? 1 : 0) | (cfg.mean ? 2 : 0));
+  const uint32_t rk = (uint32_t)cfg.rank, wd = (uint32_t)cfg.world, opt = (uint32_t)cfg.optim;
+  const uint64_t itu = (uint64_t)iteration;
+  std::memcpy(hdr.data() + 4, &ver, 2);
+  std::memcpy(hdr.data() + 6, &flags, 2);
+  std::memcpy(hdr.data() + 8, &rk, 4);
+  std::memcpy(hdr.data() + 12, &wd, 4);
+  std::memcpy(hdr.data() + 16, &itu, 8);
+  std::memcpy(hdr.data() + 24, &psi, 8);
+  std::memcpy(hdr.data() + 32, &sb, 8);
+  std::memcpy(hdr.data() + 40, &se, 8);
+  std::memcpy(hdr.data() + 48, &opt, 4);
+  std::memcpy(hdr.data() + 64, &cfg.adam, 20);
+  return hdr;
+}
+
+// write header + body (3 * S floats) + CRC-32C atomically
+lowdiff_status write_ldf(const lowdiff_config& cfg, const std::string& dir, int64_t iteration, uint64_t psi,
+                         uint64_t sb, uint64_t se, const float* body, std::string* err) {
+  const std::vector<uint8_t> hdr = ldf_header(cfg, iteration, psi, sb, se);
+  const size_t bytes = 3 * (se - sb) * 4;
+  uint32_t crc = ld::crc32c_update(0xFFFFFFFFu, hdr.data(), hdr.size());
+  crc = ld::crc32c_update(crc, body, bytes) ^ 0xFFFFFFFFu;
+  return ld::write_file_atomic(ld::full_name(dir, cfg.rank, iteration), {{hdr.data(), hdr.size()}, {body, bytes}, {&crc, 4}},
+                               cfg.fsync != 0, err);
+}
+
 uint64_t k_rule(uint64_t n, uint32_t ppm) {   // DESIGN.md R-3
   uint64_t k = n * ppm / 1000000ull;
   return std::max<uint64_t>(1, std::min(k, n));
@@ -518,6 +549,9 @@ lowdiff_status lowdiff_sync(lowdiff_ctx* c) {
   return LOWDIFF_OK;
 }
 
+static void replica_drain(lowdiff_ctx* c);
+static void replica_shutdown(lowdiff_ctx* c);
+
 lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
   if (!c) return LOWDIFF_OK;
   lowdiff_status st = LOWDIFF_OK;
@@ -531,8 +565,12 @@ lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
     c->writer.join();
   }
   if (c->full_writer.joinable()) c->full_writer.join();
+  replica_drain(c);
+  replica_shutdown(c);
   cudaSetDevice(c->device);
   if (c->side) cudaStreamSynchronize(c->side);
+  if (c->rep_host) cudaFreeHost(c->rep_host);
+  if (c->rep_init_done) cudaEventDestroy(c->rep_init_done);
   if (c->comm) ncclCommDestroy(c->comm);
   for (auto& s : c->slots) if (s.done) cudaEventDestroy(s.done);
   for (auto e : c->prof_pool) cudaEventDestroy(e);
@@ -714,27 +752,8 @@ lowdiff_status lowdiff_full_ckpt(lowdiff_ctx* c, int64_t iteration, const float*
     cudaError_t e = cudaEventSynchronize(c->full_done);
     if (e != cudaSuccess) { set_deferred(c, LOWDIFF_E_CUDA, cudaGetErrorString(e)); return; }
     const int64_t t0 = now_ns();
-    std::vector<uint8_t> hdr(96, 0);
-    std::memcpy(hdr.data(), "LDF1", 4);
-    const uint16_t ver = 1, flags = (uint16_t)((c->cfg.error_feedback ? 1 : 0) | (c->cfg.mean ? 2 : 0));
-    std::memcpy(hdr.data() + 4, &ver, 2);
-    std::memcpy(hdr.data() + 6, &flags, 2);
-    const uint32_t rk = (uint32_t)c->cfg.rank, wd = (uint32_t)c->cfg.world, opt = (uint32_t)c->cfg.optim;
-    const uint64_t itu = (uint64_t)iteration, psi = (uint64_t)c->psi;
-    std::memcpy(hdr.data() + 8, &rk, 4);
-    std::memcpy(hdr.data() + 12, &wd, 4);
-    std::memcpy(hdr.data() + 16, &itu, 8);
-    std::memcpy(hdr.data() + 24, &psi, 8);
-    std::memcpy(hdr.data() + 32, &sb, 8);
-    std::memcpy(hdr.data() + 40, &se, 8);
-    std::memcpy(hdr.data() + 48, &opt, 4);
-    std::memcpy(hdr.data() + 64, &c->cfg.adam, 20);
-    uint32_t crc = ld::crc32c_update(0xFFFFFFFFu, hdr.data(), hdr.size());
-    crc = ld::crc32c_update(crc, c->full_host, 3 * S * 4) ^ 0xFFFFFFFFu;
     std::string err;
-    lowdiff_status s2 = ld::write_file_atomic(ld::full_name(c->ckpt_dir, c->cfg.rank, iteration),
-                                              {{hdr.data(), hdr.size()}, {c->full_host, 3 * S * 4}, {&crc, 4}},
-                                              c->cfg.fsync != 0, &err);
+    lowdiff_status s2 = write_ldf(c->cfg, c->ckpt_dir, iteration, (uint64_t)c->psi, sb, se, c->full_host, &err);
     if (s2) set_deferred(c, s2, err);
     else { c->files_written += 1; c->bytes_written += (int64_t)(100 + 12 * S); }
     c->writer_ns += now_ns() - t0;
@@ -898,6 +917,14 @@ lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx* c, int64_t iteration, int32_t
     CK(cudaHostAlloc((void**)&c->snap_host[buf], (size_t)c->psi * 4, cudaHostAllocDefault));
   }
   if (c->snap_iter[buf] != iteration) {
+    const int64_t old = c->snap_iter[buf];
+    if (c->rep_active && old >= 0 && old <= c->rep_tail) {
+      // the replica worker still has to read iteration `old` from this buffer
+      const int64_t t0 = now_ns();
+      std::unique_lock<std::mutex> lk(c->rep_mu);
+      c->rep_done_cv.wait(lk, [&] { return c->rep_iter.load() >= old; });
+      c->rep_stall_ns += now_ns() - t0;
+    }
     CK(cudaEventSynchronize(c->snap_done[buf]));   // iteration - 2 finished with this buffer
     c->snap_iter[buf] = iteration;
     c->snap_seen[buf].assign(c->cfg.n_layers, 0);
@@ -927,6 +954,210 @@ lowdiff_status lowdiff_snapshot_wait(lowdiff_ctx* c, int64_t iteration, const fl
   return LOWDIFF_OK;
 }
 
+// ---------------------------------------------------------------- LowDiff+ CPU replica (NEXT-3)
+// Worker: applies queued snapshot gradients to the host shard in order (ld::host_adam/host_sgd,
+// replica.cpp), and hands persist requests to a writer thread through a staging copy.
+static void replica_loop(lowdiff_ctx* c) {
+  cudaSetDevice(c->device);
+  const uint64_t S = c->rep_se - c->rep_sb;
+  for (;;) {
+    ld::RepJob j;
+    {
+      std::unique_lock<std::mutex> lk(c->rep_mu);
+      c->rep_cv.wait(lk, [&] { return c->rep_stop || !c->rep_q.empty(); });
+      if (c->rep_q.empty()) return;
+      j = c->rep_q.front();
+      c->rep_q.pop_front();
+      c->rep_busy = 1;
+    }
+    cudaError_t e = cudaSuccess;
+    if (j.kind == 0) {
+      e = cudaEventSynchronize(c->rep_init_done);
+    } else if (j.kind == 1) {
+      const int buf = (int)(j.iteration & 1);
+      e = cudaEventSynchronize(c->snap_done[buf]);
+      if (e == cudaSuccess) {
+        const int64_t t0 = now_ns();
+        const float* G = c->snap_host[buf] + c->rep_sb;
+        if (c->cfg.optim == LOWDIFF_ADAM)
+          ld::host_adam((int64_t)S, G, c->cfg.adam, j.sc, c->rep_host, c->rep_host + S, c->rep_host + 2 * S,
+                        c->rep_threads);
+        else
+          ld::host_sgd((int64_t)S, G, j.sc.lr, c->rep_host, c->rep_threads);
+        c->rep_ns += now_ns() - t0;
+      }
+    } else if (c->cfg.ckpt_dir && c->cfg.write_files) {
+      if (c->rep_writer.joinable()) c->rep_writer.join();
+      c->rep_stage.assign(c->rep_host, c->rep_host + 3 * S);
+      const int64_t it = j.iteration;
+      c->rep_writer = std::thread([c, it]() {
+        const int64_t t0 = now_ns();
+        std::string err;
+        lowdiff_status s2 = write_ldf(c->cfg, c->ckpt_dir, it, (uint64_t)c->psi, c->rep_sb, c->rep_se,
+                                      c->rep_stage.data(), &err);
+        if (s2) set_deferred(c, s2, err);
+        else { c->files_written += 1; c->bytes_written += (int64_t)(100 + 12 * (c->rep_se - c->rep_sb)); }
+        c->writer_ns += now_ns() - t0;
+      });
+    }
+    if (e != cudaSuccess) set_deferred(c, LOWDIFF_E_CUDA, std::string("replica: ") + cudaGetErrorString(e));
+    {
+      std::lock_guard<std::mutex> g(c->rep_mu);
+      if (j.kind != 2) c->rep_iter = j.iteration;
+      c->rep_busy = 0;
+    }
+    c->rep_done_cv.notify_all();
+  }
+}
+
+// drain the queue and the persist writer (worker stays alive)
+static void replica_drain(lowdiff_ctx* c) {
+  if (!c->rep_active) return;
+  {
+    std::unique_lock<std::mutex> lk(c->rep_mu);
+    c->rep_done_cv.wait(lk, [&] { return c->rep_q.empty() && !c->rep_busy; });
+  }
+  // the writer is only joined by the worker or here; the worker is idle now
+  if (c->rep_writer.joinable()) c->rep_writer.join();
+}
+
+static void replica_shutdown(lowdiff_ctx* c) {
+  if (c->rep_thread.joinable()) {
+    {
+      std::lock_guard<std::mutex> g(c->rep_mu);
+      c->rep_stop = true;
+    }
+    c->rep_cv.notify_all();
+    c->rep_thread.join();
+  }
+  if (c->rep_writer.joinable()) c->rep_writer.join();
+  c->rep_stop = false;
+  c->rep_active = false;
+}
+
+static void replica_push(lowdiff_ctx* c, const ld::RepJob& j) {
+  {
+    std::lock_guard<std::mutex> g(c->rep_mu);
+    c->rep_q.push_back(j);
+  }
+  c->rep_cv.notify_one();
+}
+
+lowdiff_status lowdiff_replica_init(lowdiff_ctx* c, int64_t iteration, const float* p, const float* m, const float* v,
+                                    int32_t threads, void* producer) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!p || iteration < 0 || threads < 1) return fail(c, LOWDIFF_E_INVALID, "replica_init: bad argument");
+  if (c->cfg.optim == LOWDIFF_ADAM && (!m || !v)) return fail(c, LOWDIFF_E_INVALID, "replica_init: Adam needs m and v");
+  replica_drain(c);
+  replica_shutdown(c);
+  const uint64_t sb = (uint64_t)c->psi * c->cfg.rank / c->cfg.world;
+  const uint64_t se = (uint64_t)c->psi * (c->cfg.rank + 1) / c->cfg.world;
+  const uint64_t S = se - sb;
+  if (!c->rep_host || c->rep_se - c->rep_sb != S) {
+    if (c->rep_host) cudaFreeHost(c->rep_host);
+    c->rep_host = nullptr;
+    CK(cudaHostAlloc((void**)&c->rep_host, std::max<size_t>(1, 3 * S) * 4, cudaHostAllocDefault));
+  }
+  if (!c->rep_init_done) CK(cudaEventCreateWithFlags(&c->rep_init_done, cudaEventDisableTiming));
+  c->rep_sb = sb;
+  c->rep_se = se;
+  c->rep_threads = threads;
+  cudaStream_t pr = static_cast<cudaStream_t>(producer);
+  CK(cudaEventRecord(c->ev_tmp, pr));
+  CK(cudaStreamWaitEvent(c->side, c->ev_tmp, 0));
+  const float* src[3] = {p, m, v};
+  for (int a = 0; a < 3; ++a) {
+    if (src[a]) CK(cudaMemcpyAsync(c->rep_host + a * S, src[a] + sb, S * 4, cudaMemcpyDeviceToHost, c->side));
+    else std::memset(c->rep_host + a * S, 0, S * 4);
+  }
+  CK(cudaEventRecord(c->rep_init_done, c->side));
+  CK(cudaStreamWaitEvent(pr, c->rep_init_done, 0));
+  c->rep_iter = -1;
+  c->rep_tail = iteration;
+  c->rep_active = true;
+  c->rep_thread = std::thread(replica_loop, c);
+  replica_push(c, {0, iteration, {0.f, 0.f, 0.f}});
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_replica_step(lowdiff_ctx* c, int64_t iteration, const lowdiff_step_scalars* scalars) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if ((st = take_deferred(c))) return st;
+  if (!c->rep_active) return fail(c, LOWDIFF_E_STATE, "replica_step: no replica (call lowdiff_replica_init)");
+  if (!scalars) return fail(c, LOWDIFF_E_INVALID, "replica_step: NULL scalars");
+  if (iteration != c->rep_tail + 1)
+    return fail(c, LOWDIFF_E_STATE, "replica_step: expected iteration " + std::to_string(c->rep_tail + 1));
+  const int buf = (int)(iteration & 1);
+  if (c->snap_iter[buf] != iteration) return fail(c, LOWDIFF_E_STATE, "replica_step: iteration was not snapshotted");
+  for (uint8_t x : c->snap_seen[buf])
+    if (!x) return fail(c, LOWDIFF_E_STATE, "replica_step: some layer of the iteration was not snapshotted");
+  c->rep_tail = iteration;
+  replica_push(c, {1, iteration, *scalars});
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_replica_persist(lowdiff_ctx* c) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if ((st = take_deferred(c))) return st;
+  if (!c->rep_active) return fail(c, LOWDIFF_E_STATE, "replica_persist: no replica");
+  if (!c->cfg.ckpt_dir) return fail(c, LOWDIFF_E_INVALID, "replica_persist: no ckpt_dir");
+  replica_push(c, {2, c->rep_tail, {0.f, 0.f, 0.f}});
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_replica_wait(lowdiff_ctx* c, int64_t* iteration, const float** p, const float** m,
+                                    const float** v, int64_t* shard_begin, int64_t* shard_end) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!c->rep_active) return fail(c, LOWDIFF_E_STATE, "replica_wait: no replica");
+  replica_drain(c);
+  if ((st = take_deferred(c))) return st;
+  const uint64_t S = c->rep_se - c->rep_sb;
+  if (iteration) *iteration = c->rep_iter.load();
+  if (p) *p = c->rep_host;
+  if (m) *m = c->rep_host + S;
+  if (v) *v = c->rep_host + 2 * S;
+  if (shard_begin) *shard_begin = (int64_t)c->rep_sb;
+  if (shard_end) *shard_end = (int64_t)c->rep_se;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_replica_restore(lowdiff_ctx* c, float* p, float* m, float* v, int64_t* iteration, void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!c->rep_active) return fail(c, LOWDIFF_E_STATE, "replica_restore: no replica");
+  if (!p || (c->cfg.optim == LOWDIFF_ADAM && (!m || !v))) return fail(c, LOWDIFF_E_INVALID, "replica_restore: bad argument");
+  if (c->cfg.world > 1 && !c->comm) return fail(c, LOWDIFF_E_STATE, "replica_restore: world > 1 needs an NCCL context");
+  replica_drain(c);
+  if ((st = take_deferred(c))) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t S = c->rep_se - c->rep_sb;
+  float* dst[3] = {p, m, v};
+  for (int a = 0; a < 3; ++a)
+    if (dst[a] && S) CK(cudaMemcpyAsync(dst[a] + c->rep_sb, c->rep_host + a * S, S * 4, cudaMemcpyHostToDevice, s));
+  if (c->cfg.world > 1) {
+    // every other shard from its owner (uneven shard sizes: one broadcast per owner)
+    ncclResult_t r = ncclGroupStart();
+    const uint64_t psi = (uint64_t)c->psi, W = (uint64_t)c->cfg.world;
+    for (int a = 0; a < 3 && r == ncclSuccess; ++a) {
+      if (!dst[a]) continue;
+      for (uint64_t q = 0; q < W && r == ncclSuccess; ++q) {
+        const uint64_t qb = psi * q / W, qe = psi * (q + 1) / W;
+        r = ncclBroadcast(dst[a] + qb, dst[a] + qb, qe - qb, ncclFloat, (int)q, c->comm, s);
+      }
+    }
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess) return fail(c, LOWDIFF_E_NCCL, std::string("replica_restore: ") + ncclGetErrorString(r));
+  }
+  CK(cudaStreamSynchronize(s));
+  if (iteration) *iteration = c->rep_iter.load();
+  return LOWDIFF_OK;
+}
+
 lowdiff_status lowdiff_get_stats(const lowdiff_ctx* c, lowdiff_stats* out) {
   if (!c || !out) return LOWDIFF_E_INVALID;
   out->files_written = c->files_written;
@@ -941,6 +1172,8 @@ lowdiff_status lowdiff_get_stats(const lowdiff_ctx* c, lowdiff_stats* out) {
   } else {
     out->spec_hits = out->spec_misses = out->spec_candidates = -1;
   }
+  out->replica_busy_ns = c->rep_ns;
+  out->replica_stall_ns = c->rep_stall_ns;
   return LOWDIFF_OK;
 }
 
@@ -1009,29 +1242,13 @@ lowdiff_status lowdiff_write_full_host(const lowdiff_config* cfg, int64_t iterat
   uint64_t psi = 0;
   for (int l = 0; l < cfg->n_layers; ++l) psi += (uint64_t)cfg->numel[l];
   const uint64_t sb = psi * cfg->rank / cfg->world, se = psi * (cfg->rank + 1) / cfg->world, S = se - sb;
-  std::vector<uint8_t> buf(96 + 12 * S, 0);
-  std::memcpy(buf.data(), "LDF1", 4);
-  const uint16_t ver = 1, flags = (uint16_t)((cfg->error_feedback ? 1 : 0) | (cfg->mean ? 2 : 0));
-  const uint32_t rk = (uint32_t)cfg->rank, wd = (uint32_t)cfg->world, opt = (uint32_t)cfg->optim;
-  const uint64_t itu = (uint64_t)iteration;
-  std::memcpy(buf.data() + 4, &ver, 2);
-  std::memcpy(buf.data() + 6, &flags, 2);
-  std::memcpy(buf.data() + 8, &rk, 4);
-  std::memcpy(buf.data() + 12, &wd, 4);
-  std::memcpy(buf.data() + 16, &itu, 8);
-  std::memcpy(buf.data() + 24, &psi, 8);
-  std::memcpy(buf.data() + 32, &sb, 8);
-  std::memcpy(buf.data() + 40, &se, 8);
-  std::memcpy(buf.data() + 48, &opt, 4);
-  std::memcpy(buf.data() + 64, &cfg->adam, 20);
+  std::vector<float> body(3 * S, 0.f);
   const float* src[3] = {p, m, v};
   for (int a = 0; a < 3; ++a)
-    if (src[a]) std::memcpy(buf.data() + 96 + a * S * 4, src[a] + sb, S * 4);
-  uint32_t crc = lowdiff_crc32c(buf.data(), buf.size());
+    if (src[a]) std::memcpy(body.data() + a * S, src[a] + sb, S * 4);
   ::mkdir(cfg->ckpt_dir, 0755);
   std::string err;
-  return ld::write_file_atomic(ld::full_name(cfg->ckpt_dir, cfg->rank, iteration),
-                               {{buf.data(), buf.size()}, {&crc, 4}}, cfg->fsync != 0, &err);
+  return write_ldf(*cfg, cfg->ckpt_dir, iteration, psi, sb, se, body.data(), &err);
 }
 
 }  // extern "C"

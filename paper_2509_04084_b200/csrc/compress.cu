@@ -426,10 +426,9 @@ __global__ void find_kernel(DevPlan P, int mode) {
         S.prefix = bin; S.kleft = k - above; S.total = tot; S.refill = 0;
         // adapt the band: the previous call chose it to admit `band` x k keys of ITS distribution;
         // under error feedback the accumulated values drift upward between calls, so the band
-        // admitted tot / k x k now.  Aim the next band at 1.5 k_l admitted; the band may sit above
-        // this call's T (band < 1) when the drift alone admits more than that.
+        // admitted tot / k x k now.  Aim the next band at 1.5 k_l admitted.
         const float b = S.band > 0.f ? S.band : 1.5f;
-        S.band = fminf(4.f, fmaxf(0.25f, b * 1.5f * (float)k / (float)tot));
+        S.band = fminf(4.f, fmaxf(1.02f, b * 1.5f * (float)k / (float)tot));
         atomicAdd(&P.counters[1], 1u);
         atomicAdd(&P.counters[3], tot);
       }
@@ -440,7 +439,7 @@ __global__ void find_kernel(DevPlan P, int mode) {
         base = atomicAdd(&P.counters[0], (uint32_t)(c1 - c0));
         S.refill = 1;
         S.total = (uint32_t)(P.layer_off[li + 1] - P.layer_off[li]);
-        S.band = S.band > 0.f ? fminf(4.f, fmaxf(1.5f, S.band * 2.f)) : 1.5f;   // missed: widen
+        S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : 1.5f;   // missed: widen
         atomicAdd(&P.counters[2], 1u);
       }
       base = __shfl_sync(0xFFFFFFFFu, base, 0);
@@ -461,7 +460,7 @@ __global__ void find_kernel(DevPlan P, int mode) {
       // it (digit-0 resolution, refined with the digit-1 histogram when C falls in T's digit-0
       // bin).  Only a prediction -- the next call checks #candidates >= k_l and refills otherwise.
       const float band = S.band > 0.f ? S.band : 1.5f;
-      const uint32_t C = max(1u, (uint32_t)fminf((float)k * band, 4.0e9f));
+      const uint32_t C = max(k + 32u, (uint32_t)fminf((float)k * band, 4.0e9f));
       uint32_t nt = P.thr[slot];
       if (S.total >= C) {
         uint32_t b0, a0;
@@ -579,8 +578,9 @@ __global__ void __launch_bounds__(1024) layer_scan_kernel(DevPlan P) {
   }
   if (threadIdx.x == 0) {
     P.sel_T[slot] = T;
-    // speculative band for the next call; it may exceed this call's T
-    P.thr[slot] = P.sel[slot].next_thr;
+    // speculative band for the next call, never above this call's T
+    const uint32_t nt = P.sel[slot].next_thr;
+    P.thr[slot] = nt <= T ? nt : T;
   }
 }
 

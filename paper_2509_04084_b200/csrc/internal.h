@@ -93,6 +93,15 @@ struct Slot {
   int64_t iteration;
 };
 
+// work item of the LowDiff+ replica worker: 0 = initial copy landed, 1 = apply the snapshotted
+// gradient of `iteration`, 2 = persist the replica as it stands after the preceding items
+struct RepJob { int kind; int64_t iteration; lowdiff_step_scalars sc; };
+
+// replica.cpp: host optimizer steps over [0, n) split over `threads` (bitwise = the device replay)
+void host_adam(int64_t n, const float* G, const lowdiff_adam_consts& a, const lowdiff_step_scalars& s, float* p,
+               float* m, float* v, int threads);
+void host_sgd(int64_t n, const float* G, float lr, float* p, int threads);
+
 }  // namespace ld
 
 struct lowdiff_ctx {
@@ -152,6 +161,22 @@ struct lowdiff_ctx {
   int64_t snap_iter[2] = {-1, -1};
   std::vector<uint8_t> snap_seen[2];
   cudaEvent_t snap_done[2] = {nullptr, nullptr};
+  // LowDiff+ CPU replica of this rank's shard [rep_sb, rep_se) (replica.cpp, api.cpp)
+  bool rep_active = false;
+  uint64_t rep_sb = 0, rep_se = 0;
+  float* rep_host = nullptr;          // pinned 3 * shard: p | m | v
+  int rep_threads = 1;
+  std::atomic<int64_t> rep_iter{-1};  // optimizer steps applied to the replica (worker-visible)
+  int64_t rep_tail = -1;              // iteration the replica reaches once the queue drains
+  std::deque<ld::RepJob> rep_q;
+  std::mutex rep_mu;
+  std::condition_variable rep_cv, rep_done_cv;
+  bool rep_stop = false;
+  int rep_busy = 0;
+  std::thread rep_thread, rep_writer;
+  std::vector<float> rep_stage;       // persisted copy (the worker keeps updating the replica)
+  cudaEvent_t rep_init_done = nullptr;
+  std::atomic<int64_t> rep_ns{0}, rep_stall_ns{0};
   // profiling
   bool prof = false;
   std::vector<ld::ProfRec> prof_recs;

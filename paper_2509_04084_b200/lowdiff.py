@@ -53,7 +53,7 @@ class SysParams(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("files_written", C.c_int64), ("bytes_written", C.c_int64), ("ring_stall_ns", C.c_int64),
                 ("writer_busy_ns", C.c_int64), ("spec_hits", C.c_int64), ("spec_misses", C.c_int64),
-                ("spec_candidates", C.c_int64)]
+                ("spec_candidates", C.c_int64), ("replica_busy_ns", C.c_int64), ("replica_stall_ns", C.c_int64)]
 
 
 _lib = None
@@ -82,6 +82,14 @@ def lib():
             "replay": ([P, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P], S),
             "snapshot_layer": ([P, C.c_int64, C.c_int32, C.c_int32, P, P], S),
             "snapshot_wait": ([P, C.c_int64, C.POINTER(C.c_void_p)], S),
+            "replica_init": ([P, C.c_int64, P, P, P, C.c_int32, P], S),
+            "replica_step": ([P, C.c_int64, C.POINTER(StepScalars)], S),
+            "replica_persist": ([P], S),
+            "replica_wait": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                              C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64)], S),
+            "replica_restore": ([P, P, P, P, C.POINTER(C.c_int64), P], S),
+            "host_adam_step": ([C.c_int64, P, C.POINTER(AdamConsts), C.POINTER(StepScalars), P, P, P, C.c_int32], S),
+            "host_sgd_step": ([C.c_int64, P, C.c_float, P, C.c_int32], S),
             "sync": ([P], S),
             "get_stats": ([P, C.POINTER(Stats)], S),
             "prof_enable": ([P, C.c_int32], S),
@@ -110,7 +118,9 @@ def lib():
 
 
 EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_materialize", "exchange", "merge", "batch_persist",
-            "full_ckpt", "wait_persist", "recover", "replay", "snapshot_layer", "snapshot_wait", "sync", "get_stats",
+            "full_ckpt", "wait_persist", "recover", "replay", "snapshot_layer", "snapshot_wait", "replica_init",
+            "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
+            "sync", "get_stats",
             "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
             "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host",
             "write_full_host", "abi_version", "selftest", "wasted_time", "optimal_config", "config_step"]
@@ -305,6 +315,36 @@ class Context:
         arr = (C.c_float * self.psi).from_address(p.value)
         return torch.frombuffer(arr, dtype=torch.float32)
 
+    # -- LowDiff+ CPU replica (Alg. 2 l.11-13)
+    def replica_init(self, iteration, p, m=None, v=None, threads=None, stream=None):
+        threads = threads or max(1, min(32, (os.cpu_count() or 1)))
+        self._c("replica_init", lib().lowdiff_replica_init(self._h, iteration, _ptr(p), _ptr(m), _ptr(v), threads,
+                                                           _stream(stream)))
+
+    def replica_step(self, iteration, scalars: StepScalars):
+        self._c("replica_step", lib().lowdiff_replica_step(self._h, iteration, C.byref(scalars)))
+
+    def replica_persist(self):
+        self._c("replica_persist", lib().lowdiff_replica_persist(self._h))
+
+    def replica_wait(self):
+        """Drains the replica; returns (iteration, p, m, v, shard_begin, shard_end), p/m/v CPU float32
+        tensors viewing the pinned replica shard (valid until more replica work is queued)."""
+        it, sb, se = C.c_int64(), C.c_int64(), C.c_int64()
+        ptr = [C.c_void_p() for _ in range(3)]
+        self._c("replica_wait", lib().lowdiff_replica_wait(self._h, C.byref(it), *[C.byref(x) for x in ptr],
+                                                           C.byref(sb), C.byref(se)))
+        n = se.value - sb.value
+        views = [torch.frombuffer((C.c_float * max(1, n)).from_address(x.value), dtype=torch.float32)[:n]
+                 for x in ptr]
+        return (it.value, *views, sb.value, se.value)
+
+    def replica_restore(self, p, m=None, v=None, stream=None) -> int:
+        it = C.c_int64()
+        self._c("replica_restore", lib().lowdiff_replica_restore(self._h, _ptr(p), _ptr(m), _ptr(v), C.byref(it),
+                                                                 _stream(stream)))
+        return it.value
+
     def sync(self):
         self._c("sync", lib().lowdiff_sync(self._h))
 
@@ -346,6 +386,27 @@ def write_batch_host(sizes, opts: Options, first_iter, scalars, blocks):
     arr = (StepScalars * len(scalars))(*scalars)
     _check("write_batch_host", lib().lowdiff_write_batch_host(C.byref(cfg), first_iter, len(scalars), arr,
                                                               b.ctypes.data_as(C.c_void_p)))
+
+
+def host_adam_step(G, consts: AdamConsts, scalars: StepScalars, p, m, v, threads=1):
+    """The replica's host Adam on numpy float32 arrays (p, m, v updated in place)."""
+    import numpy as np
+    for a in (p, m, v):
+        assert a.dtype == np.float32 and a.flags.c_contiguous
+    g = np.ascontiguousarray(G, dtype=np.float32)
+    assert g.size == p.size == m.size == v.size
+    _check("host_adam_step", lib().lowdiff_host_adam_step(p.size, g.ctypes.data_as(C.c_void_p), C.byref(consts),
+                                                          C.byref(scalars), *[a.ctypes.data_as(C.c_void_p)
+                                                                              for a in (p, m, v)], threads))
+
+
+def host_sgd_step(G, lr, p, threads=1):
+    import numpy as np
+    assert p.dtype == np.float32 and p.flags.c_contiguous
+    g = np.ascontiguousarray(G, dtype=np.float32)
+    assert g.size == p.size
+    _check("host_sgd_step", lib().lowdiff_host_sgd_step(p.size, g.ctypes.data_as(C.c_void_p), lr,
+                                                        p.ctypes.data_as(C.c_void_p), threads))
 
 
 def write_full_host(sizes, opts: Options, iteration, p, m=None, v=None):
