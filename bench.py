@@ -392,6 +392,37 @@ def run_ours(args):
         wctx.close()
         subprocess.run(["rm", "-rf", wdir])
 
+    # LowDiff+ CPU replica: host Adam over one rank's shard of an 8-GPU job,
+    # fed by the snapshot of the synced gradient (only the shard crosses PCIe); reported separately
+    replica = None
+    if not args.no_replica and rank == 0:
+        rw = 8
+        rctx = ld.Context(sizes, density_ppm=args.ppm, world=rw, rank=0)
+        S = psi // rw
+        rp = torch.randn(S, device=dev)
+        rm = torch.zeros(S, device=dev)
+        rv = torch.zeros(S, device=dev)
+        threads = max(1, min(32, os.cpu_count() or 1))
+        rctx.replica_init(0, rp, rm, rv, threads=threads)
+        n_r = 4
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for t in range(1, n_r + 1):
+            rctx.snapshot_layer(t, 0, len(sizes), grads[t % 2])
+            rctx.wait_persist()
+            rctx.replica_step(t, scal[t])
+        rctx.replica_wait()
+        dt = time.perf_counter() - t0
+        rs = rctx.stats()
+        busy = rs["replica_busy_ns"] / 1e9 / n_r
+        replica = {"shard_params": S, "of_world": rw, "threads": threads, "steps": n_r,
+                   "host_adam_ms_per_step": busy * 1e3, "pipeline_ms_per_step": dt / n_r * 1e3,
+                   "host_param_steps_per_s": S / busy if busy > 0 else None,
+                   "host_algorithmic_gbs": 28 * S / busy / 1e9 if busy > 0 else None,
+                   "bytes_model": "28 B/param-step: G read 4 + p, m, v read+write 24 (host DRAM)"}
+        rctx.close()
+        del rp, rm, rv
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         t_o, sample, (a, b) = oracle_sample(sizes, args.ppm, args.cpu_budget)
@@ -414,6 +445,7 @@ def run_ours(args):
                                   "file writing measured separately (writer)"},
             "roofline": roofline, "gate_bj5": gate, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "recovery": recovery, "writer": writer,
+            "replica": replica,
             "spec": {"hits": st["spec_hits"], "misses": st["spec_misses"]}}
     print(json.dumps(line), flush=True)
 
@@ -432,6 +464,7 @@ def main():
     ap.add_argument("--no-recovery", action="store_true")
     ap.add_argument("--no-writer", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-replica", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

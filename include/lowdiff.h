@@ -9,8 +9,9 @@
  *   lowdiff_batch_persist  reuse queue -> pinned ring -> batched file Alg. 1 l.6,12-14
  *   lowdiff_full_ckpt      sharded full checkpoint C^F               Alg. 1 l.15
  *   lowdiff_recover        chain scan + fused replay onto C^F        Alg. 1 l.16-24 PAPER.md:248-259
- * plus the LowDiff+ layer-wise dense snapshot (Alg. 2 l.19) and a
- * device-resident replay entry point used by recover and by the benchmark.
+ * plus the LowDiff+ layer-wise dense snapshot (Alg. 2 l.19), the LowDiff+ CPU
+ * replica (Sec. 5.2), the checkpointing-configuration model (Eq. 3-5,
+ * PAPER.md:318-350) and a device-resident replay entry point used by recover and the benchmark.
  *
  * Conventions (all calls):
  *  - Every call returns lowdiff_status; none throws, aborts or exits.  A CUDA or NCCL
@@ -103,7 +104,7 @@ lowdiff_status lowdiff_layer_k(const lowdiff_ctx *ctx, int32_t layer, int64_t *k
  *      LOWER index; write them index-ascending into `send` at koff_l:
  *      send = idx u32[K] (global flat index) || val f32-bits u32[K];
  *      residual' = acc with the selected entries set to +0.0f.
- *    For layers larger than 16384 elements the +0.0f at the selected positions are DEFERRED:
+ *    For layers larger than 4096 elements the +0.0f at the selected positions are DEFERRED:
  *    the residual buffer keeps acc there and the next lowdiff_compress on the same buffer
  *    zeroes them on the fly (the selection is {key > T_l} U {key == T_l, index < cut_l}, kept in
  *    the context), saving a scattered write pass.  Call lowdiff_residual_materialize before
@@ -183,7 +184,9 @@ lowdiff_status lowdiff_replay(lowdiff_ctx *ctx, int32_t optim, int32_t world, in
  *    (contiguous in the flat gradient; grad_bucket points at layer first_layer), copy
  *    them D2H on a side stream into the pinned buffer of `iteration` (double-buffered:
  *    iterations t and t+1 may be in flight).  grad_bucket must not be rewritten before the
- *    copy has read it: lowdiff_wait_persist(ctx, s) orders stream s after it. */
+ *    copy has read it: lowdiff_wait_persist(ctx, s) orders stream s after it.  While a CPU
+ *    replica is active (lowdiff_replica_init) only the replica's shard of the bucket is copied;
+ *    the rest of the host buffer is then not updated. */
 lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx *ctx, int64_t iteration, int32_t first_layer,
                                       int32_t n_layers, const float *grad_bucket, void *producer);
 
@@ -284,7 +287,7 @@ lowdiff_status lowdiff_write_batch_host(const lowdiff_config *cfg, int64_t first
 lowdiff_status lowdiff_write_full_host(const lowdiff_config *cfg, int64_t iteration, const float *p,
                                        const float *m, const float *v);
 /* ---- checkpointing configuration (§4.3, Eq. 3-5; module PAPER.md:454-455)
- * System parameters of the wasted-time model, all times in ONE unit (R-25 uses
+ * System parameters of the wasted-time model, all times in ONE unit (R-27 uses
  * iterations): N GPUs, M mean time between failures, W write bandwidth (bytes per time unit),
  * S full-checkpoint bytes, T total run time, R_F time to load a full checkpoint, R_D time to
  * merge one differential. */

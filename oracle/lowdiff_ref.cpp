@@ -455,7 +455,7 @@ int lowdiff_ref_recover(const char* dir, uint32_t world, int n_layers, const int
 
 // --------------------------------------------------------------------------
 // Checkpointing configuration, §4.3 "Configuration Modeling", written
-// term by term from the itemised list PAPER.md:322-330 (one time unit throughout, R-25):
+// term by term from the itemised list PAPER.md:322-330 (one time unit throughout, R-27):
 //   failures            = T / M
 //   full-ckpt write     = S / W
 //   full checkpoints    = f x T

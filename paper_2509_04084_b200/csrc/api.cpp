@@ -934,9 +934,13 @@ lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx* c, int64_t iteration, int32_t
   CK(cudaEventRecord(c->ev_tmp, p));
   CK(cudaStreamWaitEvent(c->side, c->ev_tmp, 0));
   const uint64_t lo = c->off[first_layer], hi = c->off[first_layer + n_layers];
+  // with an active replica only its shard of the bucket crosses PCIe (the rest is not read)
+  const uint64_t a = c->rep_active ? std::max(lo, c->rep_sb) : lo;
+  const uint64_t z = c->rep_active ? std::min(hi, c->rep_se) : hi;
   int h;
   ld::prof_begin(c, "snapshot_d2h", c->side, &h);
-  CK(cudaMemcpyAsync(c->snap_host[buf] + lo, grad_bucket, (hi - lo) * 4, cudaMemcpyDeviceToHost, c->side));
+  if (a < z)
+    CK(cudaMemcpyAsync(c->snap_host[buf] + a, grad_bucket + (a - lo), (z - a) * 4, cudaMemcpyDeviceToHost, c->side));
   ld::prof_end(c, h, c->side);
   CK(cudaEventRecord(c->snap_done[buf], c->side));
   return LOWDIFF_OK;

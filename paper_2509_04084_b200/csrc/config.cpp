@@ -1,7 +1,7 @@
 // Checkpointing configuration (NEXT-4): the wasted-time model and its optimum, §4.3
 // "Optimizing Checkpointing Configuration" and the optimal configuration
 // module.  Host arithmetic only, in double.  All time quantities share one
-// unit (R-25 reads the model in iterations: f = full checkpoints per iteration, so the
+// unit (R-27 reads the model in iterations: f = full checkpoints per iteration, so the
 // full-checkpoint interval FCF = 1/f iterations; b = differentials per batched write).
 #include <cmath>
 
