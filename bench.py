@@ -329,6 +329,28 @@ def run_ours(args):
         del hg, hout
     ctx.sync()
 
+    # full checkpoint (a7): the producer waits only for the D2D stage of the rank's 12 Psi / N shard;
+    # the D2H from the stage follows on the side stream (p, m, v stand-ins: the gradient buffers)
+    fullck = None
+    if not args.no_full:
+        fs = (psi * (rank + 1) // world) - (psi * rank // world)
+        ctx.full_ckpt(0, grads[0], grads[1], grads[0])   # warm-up: allocates the stage and pinned host
+        ctx.wait_persist()
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        barrier(world)
+        e0.record()
+        ctx.full_ckpt(1, grads[0], grads[1], grads[0])
+        e1.record()
+        ctx.wait_persist()
+        e2.record()
+        torch.cuda.synchronize()
+        stall = allmax(e0.elapsed_time(e1), world)
+        done = allmax(e0.elapsed_time(e2), world)
+        fullck = {"shard_bytes": 12 * fs, "producer_stall_ms": stall, "d2h_done_ms": done,
+                  "stall_gbs": 12 * fs / (stall / 1e3) / 1e9, "d2h_gbs": 12 * fs / (done / 1e3) / 1e9,
+                  "note": "producer waits for the D2D stage only (DESIGN.md 4.4); the D2H runs behind it"}
+
     # recovery replay (M2): n steps of gathered blocks resident in HBM, fused Adam replay
     recovery = None
     if not args.no_recovery:
@@ -346,17 +368,19 @@ def run_ours(args):
                 ctx.compress(grads[t % 2], r, diffs[t])
         del dn
         torch.cuda.synchronize()
-        p = torch.randn(psi, device=dev) * 0.02
-        m = torch.zeros(psi, device=dev)
-        v = torch.zeros(psi, device=dev)
+        # sharded recovery (NEXT-2): every rank replays only its parameter range
+        lo, hi = psi * rank // world, psi * (rank + 1) // world
+        p = torch.randn(hi - lo, device=dev) * 0.02
+        m = torch.zeros(hi - lo, device=dev)
+        v = torch.zeros(hi - lo, device=dev)
         rscal = [ld.derive_step_scalars(t, 1e-3) for t in range(1, n_rep + 1)]
-        ctx.replay(ld.ADAM, world, n_rep, diffs, rscal, p, m, v)   # warm-up (also sizes the index scratch)
+        ctx.replay_range(ld.ADAM, world, n_rep, diffs, rscal, lo, hi, p, m, v)   # warm-up (sizes the scratch)
         torch.cuda.synchronize()
         ctx.prof_enable(True)
         barrier(world)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record()
-        ctx.replay(ld.ADAM, world, n_rep, diffs, rscal, p, m, v)
+        ctx.replay_range(ld.ADAM, world, n_rep, diffs, rscal, lo, hi, p, m, v)
         g1.record()
         torch.cuda.synchronize()
         rms = allmax(g0.elapsed_time(g1), world)
@@ -364,16 +388,18 @@ def run_ours(args):
         ri_ms, _ = ctx.prof_read("replay_index")
         ctx.prof_enable(False)
         t_rep = rms / 1e3
-        unfused = n_rep * (24 * psi + 8 * world * K)
-        fused = 24 * psi + n_rep * 8 * world * K
+        S = hi - lo
+        unfused = n_rep * (24 * S + 8 * world * K)
+        fused = 24 * S + n_rep * 8 * world * K
         alu_peak = 148 * 128 * (peaks.get("sm_max_mhz", 1965.0) * 1e6)   # fp32 lane-instr/s
-        recovery = {"metric": "recovery replay params/s", "value": world * n_rep * psi / t_rep,
+        recovery = {"metric": "recovery replay params/s", "value": n_rep * psi / t_rep,
                     "unit": "param-steps/s", "optimizer": "adam", "steps": n_rep, "ranks_per_step": world,
+                    "sharded": f"each of {world} rank(s) replays its 1/{world} of Psi (lowdiff_replay_range)",
                     "ms": rms, "replay_kernel_ms": rk_ms, "index_kernel_ms": ri_ms,
-                    "effective_unfused_gbs": unfused / t_rep / 1e9,
+                    "effective_unfused_gbs_per_rank": unfused / t_rep / 1e9,
                     "frac_of_hbm_unfused_model": unfused / t_rep / B_HBM,
-                    "fused_algorithmic_gbs": fused / t_rep / 1e9,
-                    "alu_lane_instr_per_param_step_at_peak": alu_peak * t_rep / (n_rep * psi)}
+                    "fused_algorithmic_gbs_per_rank": fused / t_rep / 1e9,
+                    "alu_lane_instr_per_param_step_at_peak": alu_peak * t_rep / (n_rep * S)}
         del diffs, p, m, v
 
     # writer throughput (files, CRC-32C, rename) on this box's storage, reported separately
@@ -404,19 +430,27 @@ def run_ours(args):
         rv = torch.zeros(S, device=dev)
         threads = max(1, min(32, os.cpu_count() or 1))
         rctx.replica_init(0, rp, rm, rv, threads=threads)
-        n_r = 4
+        n_w, n_r = 2, 4
+        for t in range(1, n_w + 1):   # warm-up: pins both snapshot buffers
+            rctx.snapshot_layer(t, 0, len(sizes), grads[t % 2])
+            rctx.wait_persist()
+            rctx.replica_step(t, scal[t])
+        rctx.replica_wait()
+        busy0 = rctx.stats()["replica_busy_ns"]
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for t in range(1, n_r + 1):
+        for t in range(n_w + 1, n_w + n_r + 1):
             rctx.snapshot_layer(t, 0, len(sizes), grads[t % 2])
             rctx.wait_persist()
             rctx.replica_step(t, scal[t])
         rctx.replica_wait()
         dt = time.perf_counter() - t0
         rs = rctx.stats()
-        busy = rs["replica_busy_ns"] / 1e9 / n_r
+        busy = (rs["replica_busy_ns"] - busy0) / 1e9 / n_r
         replica = {"shard_params": S, "of_world": rw, "threads": threads, "steps": n_r,
                    "host_adam_ms_per_step": busy * 1e3, "pipeline_ms_per_step": dt / n_r * 1e3,
+                   "stall_ms_total": rs["replica_stall_ns"] / 1e6,
+                   "snapshot_bytes_per_step": 4 * S,
                    "host_param_steps_per_s": S / busy if busy > 0 else None,
                    "host_algorithmic_gbs": 28 * S / busy / 1e9 if busy > 0 else None,
                    "bytes_model": "28 B/param-step: G read 4 + p, m, v read+write 24 (host DRAM)"}
@@ -444,7 +478,7 @@ def run_ours(args):
                        "persist": "D2H of the rank's block into the pinned ring inside the timed region; "
                                   "file writing measured separately (writer)"},
             "roofline": roofline, "gate_bj5": gate, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": clk, "recovery": recovery, "writer": writer,
+            "gpu_launches": launches, "clocks": clk, "recovery": recovery, "writer": writer, "full_ckpt": fullck,
             "replica": replica,
             "spec": {"hits": st["spec_hits"], "misses": st["spec_misses"]}}
     print(json.dumps(line), flush=True)
@@ -465,6 +499,7 @@ def main():
     ap.add_argument("--no-writer", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-replica", action="store_true")
+    ap.add_argument("--no-full", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -136,6 +136,16 @@ lowdiff_status lowdiff_exchange(lowdiff_ctx *ctx, const uint32_t *send, uint32_t
 lowdiff_status lowdiff_merge(lowdiff_ctx *ctx, int32_t world, const uint32_t *gathered,
                              float *dense_out, void *stream);
 
+/* Exchange + optimizer step without a dense gradient (Alg. 1 lines 5, 7, 8,
+ *    PAPER.md:231-237): the allgather of lowdiff_exchange, then p, m, v <- Opt(G, scalars) with
+ *    G the merge of the gathered blocks computed tile by tile in shared memory and never written
+ *    to HBM (the fused replay kernel with n = 1; optimizer = cfg.optim).  Bitwise equal to
+ *    lowdiff_exchange followed by the R-11 Adam / R-12 SGD step on dense_out.  p, m, v: device
+ *    f32[Psi] (m, v unused for SGD); gathered as in lowdiff_exchange.  Asynchronous. */
+lowdiff_status lowdiff_exchange_update(lowdiff_ctx *ctx, const uint32_t *send, uint32_t *gathered,
+                                       const lowdiff_step_scalars *scalars, float *p, float *m, float *v,
+                                       void *stream);
+
 /* 3. Batch persist (Alg. 1 line 6 Q.put, lines 12-14; Steps 1-3).
  *    Records an event on `producer`; a library side stream waits on it and copies this
  *    rank's own send block (8K bytes) into a pinned-host ring slot.  The writer thread
@@ -153,9 +163,12 @@ lowdiff_status lowdiff_wait_persist(lowdiff_ctx *ctx, void *stream);
 
 /* 4. Full checkpoint (Alg. 1 line 15): this rank's shard
  *    [floor(rank*Psi/world), floor((rank+1)*Psi/world)) of p, m, v (m, v may be NULL ->
- *    zeros), copied D2H on a side stream after an event on `producer`; `producer` then
- *    waits (device-side) for the copy, so the caller's next update cannot overwrite the
- *    snapshot (write-after-read).  Persisted asynchronously as .ldf.
+ *    zeros), copied on a side stream after an event on `producer`: first D2D into a library-
+ *    owned device stage (12 * shard bytes of HBM, allocated at the first call), and `producer`
+ *    waits (device-side) only for that copy, so the caller's next update cannot overwrite the
+ *    snapshot (write-after-read) yet is not held behind PCIe; then D2H from the
+ *    stage.  If the stage cannot be allocated the shard is copied D2H directly and `producer`
+ *    waits for that.  Persisted asynchronously as .ldf.
  *    `iteration` = optimizer steps applied to (p, m, v). */
 lowdiff_status lowdiff_full_ckpt(lowdiff_ctx *ctx, int64_t iteration, const float *p,
                                  const float *m, const float *v, void *producer);
@@ -178,6 +191,25 @@ lowdiff_status lowdiff_recover(lowdiff_ctx *ctx, int64_t target, float *p, float
 lowdiff_status lowdiff_replay(lowdiff_ctx *ctx, int32_t optim, int32_t world, int64_t n_steps,
                               const uint32_t *diffs, const lowdiff_step_scalars *scalars,
                               float *p, float *m, float *v, void *stream);
+
+/* Sharded recovery (NEXT-2; the per-element replay of R-16 split by parameter range).
+ * replay_range: lowdiff_replay restricted to elements [begin, end) of Psi; p, m, v are device
+ *    f32[end - begin] holding exactly that range (p[0] = element begin).  The result equals the
+ *    same elements of a full lowdiff_replay bit for bit.
+ * recover_sharded: lowdiff_recover for this rank's shard [floor(rank*Psi/world),
+ *    floor((rank+1)*Psi/world)) only: reads only this rank's .ldf shard, uploads only the entries
+ *    of each differential block that fall in the shard (the indices ascend, so they are one
+ *    contiguous run per block), and replays only the shard into p, m, v (device f32[Psi];
+ *    elements outside the shard are not touched).  gather != 0 (world > 1, NCCL context needed):
+ *    then fills the other shards from their owners by NCCL broadcasts, so every rank ends with
+ *    the full state.  Chain selection (F, last) is exactly that of lowdiff_recover (all ranks
+ *    agree).  Synchronous. */
+lowdiff_status lowdiff_replay_range(lowdiff_ctx *ctx, int32_t optim, int32_t world, int64_t n_steps,
+                                    const uint32_t *diffs, const lowdiff_step_scalars *scalars,
+                                    int64_t begin, int64_t end, float *p, float *m, float *v,
+                                    void *stream);
+lowdiff_status lowdiff_recover_sharded(lowdiff_ctx *ctx, int64_t target, float *p, float *m, float *v,
+                                       int32_t gather, int64_t *recovered, void *stream);
 
 /* LowDiff+ layer-wise snapshot (Sec. 5.1; Alg. 2 l.19):
  *    after the caller's gradient sync of layers [first_layer, first_layer+n_layers)

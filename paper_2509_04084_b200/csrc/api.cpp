@@ -497,7 +497,8 @@ lowdiff_status lowdiff_create(const lowdiff_config* cfg, lowdiff_ctx** out) {
       cudaEventCreateWithFlags(&c->ev_tmp, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_side_all, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->last_d2h, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->full_done, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&c->full_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->full_staged, cudaEventDisableTiming) != cudaSuccess)
     return bail(LOWDIFF_E_CUDA);
   for (int i = 0; i < 2; ++i)
     if (cudaEventCreateWithFlags(&c->snap_done[i], cudaEventDisableTiming) != cudaSuccess) return bail(LOWDIFF_E_CUDA);
@@ -581,7 +582,9 @@ lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
   for (auto* p : c->dev_allocs) cudaFree(p);
   if (c->replay_scratch) cudaFree(c->replay_scratch);
   if (c->merge_scratch) cudaFree(c->merge_scratch);
-  for (auto e : {c->ev_tmp, c->ev_side_all, c->last_d2h, c->full_done, c->snap_done[0], c->snap_done[1]}) if (e) cudaEventDestroy(e);
+  if (c->full_stage) cudaFree(c->full_stage);
+  for (auto e : {c->ev_tmp, c->ev_side_all, c->last_d2h, c->full_done, c->full_staged, c->snap_done[0], c->snap_done[1]})
+    if (e) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
   delete c;
   return st;
@@ -651,6 +654,30 @@ lowdiff_status lowdiff_exchange(lowdiff_ctx* c, const uint32_t* send, uint32_t* 
   }
   if (gathered && gathered != send) CK(cudaMemcpyAsync(gathered, send, blk * 4, cudaMemcpyDeviceToDevice, s));
   return lowdiff_merge(c, 1, send, dense_out, stream);
+}
+
+// SURVEY NEXT-1 (second half): the live optimizer step straight from the gathered blocks -- the
+// fused replay with n = 1 -- so the dense G is never materialised in HBM (24 B/param + 8 N K instead
+// of 4 B/param for the merge plus 28 B/param for a dense Adam step).
+lowdiff_status lowdiff_exchange_update(lowdiff_ctx* c, const uint32_t* send, uint32_t* gathered,
+                                       const lowdiff_step_scalars* scalars, float* p, float* m, float* v,
+                                       void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!send || !scalars || (c->cfg.world > 1 && !gathered)) return fail(c, LOWDIFF_E_INVALID, "exchange_update: NULL buffer");
+  const size_t blk = 2 * (size_t)c->K;
+  const uint32_t* blocks = send;
+  if (c->cfg.world > 1) {
+    if (!c->comm) return fail(c, LOWDIFF_E_STATE, "exchange_update: context was created without an NCCL id");
+    int h;
+    ld::prof_begin(c, "allgather", s, &h);
+    ncclResult_t r = ncclAllGather(send, gathered, blk, ncclUint32, c->comm, s);
+    ld::prof_end(c, h, s);
+    if (r != ncclSuccess) return fail(c, LOWDIFF_E_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    blocks = gathered;
+  }
+  return lowdiff_replay(c, c->cfg.optim, c->cfg.world, 1, blocks, scalars, p, m, v, stream);
 }
 
 lowdiff_status lowdiff_batch_persist(lowdiff_ctx* c, int64_t iteration, const lowdiff_step_scalars* scalars,
@@ -740,12 +767,37 @@ lowdiff_status lowdiff_full_ckpt(lowdiff_ctx* c, int64_t iteration, const float*
   CK(cudaEventRecord(c->ev_tmp, pr));
   CK(cudaStreamWaitEvent(c->side, c->ev_tmp, 0));
   const float* src[3] = {p, m, v};
-  for (int a = 0; a < 3; ++a) {
-    if (src[a]) CK(cudaMemcpyAsync(c->full_host + a * S, src[a] + sb, S * 4, cudaMemcpyDeviceToHost, c->side));
-    else std::memset(c->full_host + a * S, 0, S * 4);
+  // D2D stage: the producer's next update waits only for an HBM->HBM copy of the
+  // shard (12 S bytes at HBM speed) instead of the PCIe transfer; the D2H then runs from the stage.
+  // Without the device memory for the stage, the snapshot goes straight D2H.
+  if (c->full_stage_cap < 3 * S) {
+    if (c->full_stage) cudaFree(c->full_stage);
+    c->full_stage = nullptr;
+    c->full_stage_cap = 0;
+    if (cudaMalloc((void**)&c->full_stage, std::max<size_t>(1, 3 * S) * 4) == cudaSuccess) c->full_stage_cap = 3 * S;
+    else { c->full_stage = nullptr; cudaGetLastError(); }
   }
-  CK(cudaEventRecord(c->full_done, c->side));
-  CK(cudaStreamWaitEvent(pr, c->full_done, 0));   // the next update waits for the snapshot (WAR)
+  int h;
+  ld::prof_begin(c, "full_snapshot", c->side, &h);
+  if (c->full_stage) {
+    for (int a = 0; a < 3; ++a) {
+      if (src[a]) CK(cudaMemcpyAsync(c->full_stage + a * S, src[a] + sb, S * 4, cudaMemcpyDeviceToDevice, c->side));
+      else CK(cudaMemsetAsync(c->full_stage + a * S, 0, S * 4, c->side));
+    }
+    CK(cudaEventRecord(c->full_staged, c->side));
+    CK(cudaStreamWaitEvent(pr, c->full_staged, 0));   // the next update waits for the stage (WAR)
+    ld::prof_end(c, h, c->side);
+    CK(cudaMemcpyAsync(c->full_host, c->full_stage, 3 * S * 4, cudaMemcpyDeviceToHost, c->side));
+    CK(cudaEventRecord(c->full_done, c->side));
+  } else {
+    for (int a = 0; a < 3; ++a) {
+      if (src[a]) CK(cudaMemcpyAsync(c->full_host + a * S, src[a] + sb, S * 4, cudaMemcpyDeviceToHost, c->side));
+      else std::memset(c->full_host + a * S, 0, S * 4);
+    }
+    CK(cudaEventRecord(c->full_done, c->side));
+    CK(cudaStreamWaitEvent(pr, c->full_done, 0));   // the next update waits for the snapshot (WAR)
+    ld::prof_end(c, h, c->side);
+  }
   if (!c->cfg.ckpt_dir || !c->cfg.write_files) return LOWDIFF_OK;
   c->full_writer = std::thread([c, iteration, sb, se, S]() {
     cudaSetDevice(c->device);
@@ -761,14 +813,17 @@ lowdiff_status lowdiff_full_ckpt(lowdiff_ctx* c, int64_t iteration, const float*
   return LOWDIFF_OK;
 }
 
-lowdiff_status lowdiff_replay(lowdiff_ctx* c, int32_t optim, int32_t world, int64_t n_steps, const uint32_t* diffs,
-                              const lowdiff_step_scalars* scalars, float* p, float* m, float* v, void* stream) {
+lowdiff_status lowdiff_replay_range(lowdiff_ctx* c, int32_t optim, int32_t world, int64_t n_steps,
+                                    const uint32_t* diffs, const lowdiff_step_scalars* scalars, int64_t begin,
+                                    int64_t end, float* p, float* m, float* v, void* stream) {
   lowdiff_status st = entry(c);
   if (st) return st;
+  if (begin >= 0 && begin == end && end <= c->psi && n_steps >= 0) return LOWDIFF_OK;   // empty range
   if (world < 1 || n_steps < 0 || (n_steps && (!diffs || !scalars)) || !p ||
-      (optim == LOWDIFF_ADAM && (!m || !v)) || (optim != LOWDIFF_ADAM && optim != LOWDIFF_SGD))
+      (optim == LOWDIFF_ADAM && (!m || !v)) || (optim != LOWDIFF_ADAM && optim != LOWDIFF_SGD) || begin < 0 ||
+      end > c->psi || begin > end)
     return fail(c, LOWDIFF_E_INVALID, "replay: bad argument");
-  if (!n_steps) return LOWDIFF_OK;
+  if (!n_steps || begin == end) return LOWDIFF_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // per-step scalars to the device (tail of the replay scratch is not reused: own buffer)
   float* scal_dev = nullptr;
@@ -776,10 +831,17 @@ lowdiff_status lowdiff_replay(lowdiff_ctx* c, int32_t optim, int32_t world, int6
   CK(cudaMemcpyAsync(scal_dev, scalars, (size_t)n_steps * 12, cudaMemcpyHostToDevice, s));
   const float consts[5] = {c->cfg.adam.beta1, c->cfg.adam.one_minus_beta1, c->cfg.adam.beta2,
                            c->cfg.adam.one_minus_beta2, c->cfg.adam.eps};
-  cudaError_t e = ld::launch_replay(c, optim, c->cfg.mean != 0, consts, world, n_steps, diffs, scal_dev, p, m, v, s);
+  cudaError_t e = ld::launch_replay(c, optim, c->cfg.mean != 0, consts, world, n_steps, diffs, scal_dev,
+                                    (uint64_t)begin, (uint64_t)end, nullptr, p, m, v, s);
   cudaFreeAsync(scal_dev, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "launch_replay");
   return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_replay(lowdiff_ctx* c, int32_t optim, int32_t world, int64_t n_steps, const uint32_t* diffs,
+                              const lowdiff_step_scalars* scalars, float* p, float* m, float* v, void* stream) {
+  if (!c) return LOWDIFF_E_INVALID;
+  return lowdiff_replay_range(c, optim, world, n_steps, diffs, scalars, 0, c->psi, p, m, v, stream);
 }
 
 lowdiff_status lowdiff_chain_scan(const lowdiff_config* cfg, int64_t target, int64_t* full_iter, int64_t* last_iter) {
@@ -793,8 +855,29 @@ lowdiff_status lowdiff_chain_scan(const lowdiff_config* cfg, int64_t target, int
   return LOWDIFF_OK;
 }
 
-lowdiff_status lowdiff_recover(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int64_t* recovered,
-                               void* stream) {
+// Every rank's shard [floor(q Psi / N), floor((q+1) Psi / N)) of each non-NULL dst array, broadcast
+// from its owner q (uneven shard sizes: one broadcast per owner, grouped).
+static lowdiff_status bcast_shards(lowdiff_ctx* c, float* dst[3], cudaStream_t s) {
+  ncclResult_t r = ncclGroupStart();
+  const uint64_t psi = (uint64_t)c->psi, W = (uint64_t)c->cfg.world;
+  for (int a = 0; a < 3 && r == ncclSuccess; ++a) {
+    if (!dst[a]) continue;
+    for (uint64_t q = 0; q < W && r == ncclSuccess; ++q) {
+      const uint64_t qb = psi * q / W, qe = psi * (q + 1) / W;
+      r = ncclBroadcast(dst[a] + qb, dst[a] + qb, qe - qb, ncclFloat, (int)q, c->comm, s);
+    }
+  }
+  ncclResult_t r2 = ncclGroupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) return fail(c, LOWDIFF_E_NCCL, std::string("shard broadcast: ") + ncclGetErrorString(r));
+  return LOWDIFF_OK;
+}
+
+// Recovery of elements [lo, hi): lo = 0, hi = Psi loads every full shard and replays everything;
+// the sharded form (NEXT-2) loads only this rank's .ldf shard and replays only its element range,
+// uploading only the entries of each differential block that fall in it.
+static lowdiff_status recover_impl(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int64_t* recovered,
+                                   void* stream, bool sharded) {
   lowdiff_status st = entry(c);
   if (st) return st;
   if (!c->cfg.ckpt_dir) return fail(c, LOWDIFF_E_INVALID, "recover: no ckpt_dir");
@@ -806,11 +889,13 @@ lowdiff_status lowdiff_recover(lowdiff_ctx* c, int64_t target, float* p, float* 
   if ((st = scan_chain(c->cfg, target, &ch, &err))) return fail(c, st, err);
   const uint32_t world = (uint32_t)c->cfg.world;
   const uint64_t psi = (uint64_t)c->psi, K = (uint64_t)c->K;
+  const uint64_t lo = sharded ? psi * (uint64_t)c->cfg.rank / world : 0;
+  const uint64_t hi = sharded ? psi * ((uint64_t)c->cfg.rank + 1) / world : psi;
   // 1. full checkpoint shards -> p, m, v
   uint32_t optim = 0;
   float consts[5] = {0, 0, 0, 0, 0};
   uint16_t flags = 0;
-  for (uint32_t r = 0; r < world; ++r) {
+  for (uint32_t r = sharded ? (uint32_t)c->cfg.rank : 0; r < (sharded ? (uint32_t)c->cfg.rank + 1 : world); ++r) {
     std::vector<uint8_t> buf;
     if (!read_all(ch.full_paths[r], buf)) return fail(c, LOWDIFF_E_IO, "cannot read " + ch.full_paths[r]);
     const uint64_t sb = psi * r / world, se = psi * (r + 1) / world, S = se - sb;
@@ -837,13 +922,17 @@ lowdiff_status lowdiff_recover(lowdiff_ctx* c, int64_t target, float* p, float* 
   const size_t per_step = step_bytes + ld::replay_scratch_bytes(c->psi, (int)world, 1);
   int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)(free_b / 2 / std::max<size_t>(1, per_step))));
   uint32_t* d_diffs = nullptr;
+  uint32_t* d_ranges = nullptr;
+  std::vector<uint32_t> ranges;
   if (n > 0) CK(cudaMalloc(&d_diffs, (size_t)chunk * step_bytes));
+  if (n > 0 && sharded) CK(cudaMalloc(&d_ranges, (size_t)chunk * world * 8));
   std::map<std::string, std::vector<uint8_t>> cache;   // verified batch files in use
   lowdiff_status result = LOWDIFF_OK;
   std::vector<lowdiff_step_scalars> scal;
   for (int64_t t0 = ch.F + 1; t0 <= ch.last && result == LOWDIFF_OK; t0 += chunk) {
     const int64_t t1 = std::min<int64_t>(ch.last, t0 + chunk - 1);
     scal.assign((size_t)(t1 - t0 + 1), {0, 0, 0});
+    ranges.assign((size_t)(t1 - t0 + 1) * world * 2, 0);
     for (int64_t t = t0; t <= t1 && result == LOWDIFF_OK; ++t) {
       for (uint32_t r = 0; r < world; ++r) {
         const auto& w = ch.where[r][t];
@@ -882,8 +971,23 @@ lowdiff_status lowdiff_recover(lowdiff_ctx* c, int64_t target, float* p, float* 
           result = fail(c, LOWDIFF_E_CORRUPT, "ranks disagree on the scalars of iteration " + std::to_string(t));
           break;
         }
-        cudaError_t e = cudaMemcpy(d_diffs + ((size_t)(t - t0) * world + r) * 2 * K, blk + 32, 8 * K,
-                                   cudaMemcpyHostToDevice);
+        uint32_t* dst = d_diffs + ((size_t)(t - t0) * world + r) * 2 * K;
+        cudaError_t e;
+        if (!sharded) {
+          e = cudaMemcpy(dst, blk + 32, 8 * K, cudaMemcpyHostToDevice);
+        } else {
+          // the block's indices ascend: its entries inside [lo, hi) are one contiguous run [a, b)
+          // (Psi < 2^32, so lo and hi fit the u32 index type)
+          const uint32_t* idx = reinterpret_cast<const uint32_t*>(blk + 32);
+          const uint32_t a = (uint32_t)(std::lower_bound(idx, idx + K, (uint32_t)lo) - idx);
+          const uint32_t b = (uint32_t)(std::lower_bound(idx, idx + K, (uint32_t)hi) - idx);
+          ranges[((size_t)(t - t0) * world + r) * 2] = a;
+          ranges[((size_t)(t - t0) * world + r) * 2 + 1] = b;
+          e = cudaSuccess;
+          if (b > a) e = cudaMemcpy(dst + a, idx + a, (size_t)(b - a) * 4, cudaMemcpyHostToDevice);
+          if (e == cudaSuccess && b > a)
+            e = cudaMemcpy(dst + K + a, idx + K + a, (size_t)(b - a) * 4, cudaMemcpyHostToDevice);
+        }
         if (e != cudaSuccess) { result = cuda_fail(c, e, "H2D differential"); break; }
       }
     }
@@ -892,17 +996,36 @@ lowdiff_status lowdiff_recover(lowdiff_ctx* c, int64_t target, float* p, float* 
     float* scal_dev = nullptr;
     cudaError_t e2 = cudaMalloc((void**)&scal_dev, scal.size() * 12);
     if (e2 == cudaSuccess) e2 = cudaMemcpy(scal_dev, scal.data(), scal.size() * 12, cudaMemcpyHostToDevice);
+    if (e2 == cudaSuccess && sharded)
+      e2 = cudaMemcpy(d_ranges, ranges.data(), ranges.size() * 4, cudaMemcpyHostToDevice);
     if (e2 == cudaSuccess)
-      e2 = ld::launch_replay(c, (int)optim, (flags & 2) != 0, consts, (int)world, t1 - t0 + 1, d_diffs, scal_dev, p, m,
-                             v, s);
+      e2 = ld::launch_replay(c, (int)optim, (flags & 2) != 0, consts, (int)world, t1 - t0 + 1, d_diffs, scal_dev, lo,
+                             hi, sharded ? d_ranges : nullptr, p + lo, m ? m + lo : nullptr, v ? v + lo : nullptr, s);
     if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(s);
     if (scal_dev) cudaFree(scal_dev);
     if (e2 != cudaSuccess) result = cuda_fail(c, e2, "replay");
   }
   if (d_diffs) cudaFree(d_diffs);
+  if (d_ranges) cudaFree(d_ranges);
   if (result) return result;
   CK(cudaStreamSynchronize(s));
   if (recovered) *recovered = ch.last;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_recover(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int64_t* recovered,
+                               void* stream) {
+  return recover_impl(c, target, p, m, v, recovered, stream, false);
+}
+
+lowdiff_status lowdiff_recover_sharded(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int32_t gather,
+                                       int64_t* recovered, void* stream) {
+  lowdiff_status st = recover_impl(c, target, p, m, v, recovered, stream, true);
+  if (st || !gather || c->cfg.world == 1) return st;
+  if (!c->comm) return fail(c, LOWDIFF_E_STATE, "recover_sharded: gather needs an NCCL context");
+  float* dst[3] = {p, m, v};
+  if ((st = bcast_shards(c, dst, static_cast<cudaStream_t>(stream)))) return st;
+  CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return LOWDIFF_OK;
 }
 
@@ -1142,21 +1265,7 @@ lowdiff_status lowdiff_replica_restore(lowdiff_ctx* c, float* p, float* m, float
   float* dst[3] = {p, m, v};
   for (int a = 0; a < 3; ++a)
     if (dst[a] && S) CK(cudaMemcpyAsync(dst[a] + c->rep_sb, c->rep_host + a * S, S * 4, cudaMemcpyHostToDevice, s));
-  if (c->cfg.world > 1) {
-    // every other shard from its owner (uneven shard sizes: one broadcast per owner)
-    ncclResult_t r = ncclGroupStart();
-    const uint64_t psi = (uint64_t)c->psi, W = (uint64_t)c->cfg.world;
-    for (int a = 0; a < 3 && r == ncclSuccess; ++a) {
-      if (!dst[a]) continue;
-      for (uint64_t q = 0; q < W && r == ncclSuccess; ++q) {
-        const uint64_t qb = psi * q / W, qe = psi * (q + 1) / W;
-        r = ncclBroadcast(dst[a] + qb, dst[a] + qb, qe - qb, ncclFloat, (int)q, c->comm, s);
-      }
-    }
-    ncclResult_t r2 = ncclGroupEnd();
-    if (r == ncclSuccess) r = r2;
-    if (r != ncclSuccess) return fail(c, LOWDIFF_E_NCCL, std::string("replica_restore: ") + ncclGetErrorString(r));
-  }
+  if (c->cfg.world > 1 && (st = bcast_shards(c, dst, s))) return st;
   CK(cudaStreamSynchronize(s));
   if (iteration) *iteration = c->rep_iter.load();
   return LOWDIFF_OK;

@@ -153,6 +153,9 @@ struct lowdiff_ctx {
   float* full_host = nullptr;         // pinned 3 * shard
   size_t full_cap = 0;
   cudaEvent_t full_done = nullptr;
+  float* full_stage = nullptr;        // device 3 * shard: D2D stage so the producer waits for HBM only
+  size_t full_stage_cap = 0;
+  cudaEvent_t full_staged = nullptr;
   bool full_pending = false;
   int64_t full_iter = -1;
   std::thread full_writer;
@@ -196,9 +199,11 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
 cudaError_t launch_materialize(lowdiff_ctx* c, float* residual, cudaStream_t s);
 cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, float* dense,
                          cudaStream_t s);
+// replays elements [lo, hi); p, m, v point at element lo.  ranges: NULL (every entry of every block
+// is valid) or device u32[2 * n_steps * world] = the valid entry range of each block.
 cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* consts5, int world,
-                          int64_t n_steps, const uint32_t* diffs, const float* scal_dev, float* p,
-                          float* m, float* v, cudaStream_t s);
+                          int64_t n_steps, const uint32_t* diffs, const float* scal_dev, uint64_t lo,
+                          uint64_t hi, const uint32_t* ranges, float* p, float* m, float* v, cudaStream_t s);
 cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches, uint64_t* first);
 size_t merge_scratch_bytes(int64_t psi, int world, int64_t n_blocks);
 size_t replay_scratch_bytes(int64_t psi, int world, int64_t n_steps);

@@ -24,17 +24,26 @@
 namespace ld {
 namespace {
 
-// start[b][t] = lower_bound(idx_b, t * 2^tile_shift) for t = 0..n_tiles (idx_b ascending, K entries).
+// start[b][t - T0] = lower_bound(idx_b, t * 2^tile_shift) for t = T0..T1 (idx_b ascending).
 // Entry e owns the tiles (tile(idx[e-1]), tile(idx[e])]; grid.y walks the blocks (no 64-bit division).
+// ranges (optional, u32[2 * n_blocks]): only entries [a_b, b_b) of block b are valid (the rest of
+// the block was not uploaded); the tiles before the first valid entry get a_b, those after the last
+// get b_b.  Entries outside the range lie outside the element range being replayed.
 __global__ void tile_start_kernel(const uint32_t* __restrict__ blocks, int64_t n_blocks, uint64_t stride,
-                                  uint32_t K, int tile_shift, uint32_t n_tiles, uint32_t* __restrict__ start) {
+                                  uint32_t K, int tile_shift, uint32_t T0, uint32_t T1,
+                                  const uint32_t* __restrict__ ranges, uint32_t* __restrict__ start) {
+  const uint32_t W = T1 - T0 + 1;
   for (int64_t b = blockIdx.y; b < n_blocks; b += gridDim.y) {
     const uint32_t* idx = blocks + (uint64_t)b * stride;
-    uint32_t* st = start + (uint64_t)b * (n_tiles + 1);
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e <= K; e += gridDim.x * blockDim.x) {
-      const uint32_t t_lo = e == 0 ? 0u : (__ldg(idx + e - 1) >> tile_shift) + 1;
-      const uint32_t t_hi = e == K ? n_tiles : (__ldg(idx + e) >> tile_shift);
-      for (uint32_t t = t_lo; t <= t_hi; ++t) st[t] = e;
+    uint32_t* st = start + (uint64_t)b * W;
+    const uint32_t ea = ranges ? __ldg(ranges + 2 * b) : 0u;
+    const uint32_t eb = ranges ? __ldg(ranges + 2 * b + 1) : K;
+    for (uint32_t e = ea + blockIdx.x * blockDim.x + threadIdx.x; e <= eb; e += gridDim.x * blockDim.x) {
+      uint32_t t_lo = e == ea ? T0 : (__ldg(idx + e - 1) >> tile_shift) + 1;
+      uint32_t t_hi = e == eb ? T1 : (__ldg(idx + e) >> tile_shift);
+      t_lo = max(t_lo, T0);
+      t_hi = min(t_hi, T1);
+      for (uint32_t t = t_lo; t <= t_hi; ++t) st[t - T0] = e;
     }
   }
 }
@@ -119,37 +128,39 @@ template <int OPT, int DIV, int MAXW>
 __global__ void __launch_bounds__(kReplayThreads, MAXW >= 8 ? 3 : 4)
 replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
               const uint32_t* __restrict__ start, int64_t n_tiles, const float* __restrict__ scal,
-              AdamK ak, uint64_t psi, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v) {
+              AdamK ak, uint64_t lo, uint64_t hi, int64_t tile0, float* __restrict__ p, float* __restrict__ m,
+              float* __restrict__ v) {
+  // elements [lo, hi) are replayed; p, m, v hold exactly that range (p[0] is element lo)
   __shared__ float G[kReplayTile];
-  const int64_t t = blockIdx.x;
+  const int64_t t = tile0 + blockIdx.x;
   const uint64_t j0 = (uint64_t)t * kReplayTile;
-  const int len = (int)min((uint64_t)kReplayTile, psi - j0);
   const int tid = threadIdx.x;
   float P[8], M[8], V[8];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int o = 4 * (tid + kReplayThreads * i) + q;
-      const bool in = o < len;
-      P[4 * i + q] = in ? p[j0 + o] : 0.f;
-      M[4 * i + q] = (OPT == LOWDIFF_ADAM && in) ? m[j0 + o] : 0.f;
-      V[4 * i + q] = (OPT == LOWDIFF_ADAM && in) ? v[j0 + o] : 0.f;
+      const uint64_t j = j0 + 4 * (tid + kReplayThreads * i) + q;
+      const bool in = j >= lo && j < hi;
+      P[4 * i + q] = in ? p[j - lo] : 0.f;
+      M[4 * i + q] = (OPT == LOWDIFF_ADAM && in) ? m[j - lo] : 0.f;
+      V[4 * i + q] = (OPT == LOWDIFF_ADAM && in) ? v[j - lo] : 0.f;
     }
   }
   const float n = (float)world, inv = 1.0f / (float)world;
   const bool eps_ok = ak.eps >= 0x1p-60f && ak.eps <= 0x1p59f;   // adam_u_fast's precondition
-  const uint64_t tstride = (uint64_t)(n_tiles + 1);
+  const uint64_t tstride = (uint64_t)(n_tiles + 1);   // n_tiles = tiles in the window
+  const int64_t tl = blockIdx.x;                       // tile relative to the window
   // Software pipeline over steps (everything that step s+1 needs from HBM is in flight while step
   // s computes): s_a/s_b[x & 1] in shared memory hold the entry ranges of step x for every rank;
   // the first 256 entries of every rank for step s sit in registers (pj, pv), loaded during s-1.
   __shared__ uint32_t s_a[2][MAXW], s_b[2][MAXW];
   const bool ranger = tid < world && tid < MAXW;
   if (ranger) {
-    s_a[0][tid] = __ldg(start + (uint64_t)tid * tstride + t);
-    s_b[0][tid] = __ldg(start + (uint64_t)tid * tstride + t + 1);
+    s_a[0][tid] = __ldg(start + (uint64_t)tid * tstride + tl);
+    s_b[0][tid] = __ldg(start + (uint64_t)tid * tstride + tl + 1);
     if (n_steps > 1) {
-      const uint32_t* st1 = start + ((uint64_t)world + tid) * tstride + t;
+      const uint32_t* st1 = start + ((uint64_t)world + tid) * tstride + tl;
       s_a[1][tid] = __ldg(st1);
       s_b[1][tid] = __ldg(st1 + 1);
     }
@@ -197,7 +208,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       }
     }
     for (int r = MAXW; r < world; ++r) {   // ranks beyond the register window
-      const uint32_t* st = start + ((uint64_t)s * world + r) * tstride + t;
+      const uint32_t* st = start + ((uint64_t)s * world + r) * tstride + tl;
       const uint32_t* idx = blk + (uint64_t)r * 2 * K;
       const uint32_t a = __ldg(st), b = __ldg(st + 1);
       for (uint32_t e = a + tid; e < b; e += kReplayThreads) {
@@ -216,7 +227,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       r2 = __ldg(scal + 3 * (s + 1) + 2);
     }
     if (ranger && s + 2 < n_steps) {
-      const uint32_t* st2 = start + ((uint64_t)(s + 2) * world + tid) * tstride + t;
+      const uint32_t* st2 = start + ((uint64_t)(s + 2) * world + tid) * tstride + tl;
       na = __ldg(st2);
       nb = __ldg(st2 + 1);
     }
@@ -261,10 +272,10 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
   for (int i = 0; i < 2; ++i) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int o = 4 * (tid + kReplayThreads * i) + q;
-      if (o < len) {
-        p[j0 + o] = P[4 * i + q];
-        if (OPT == LOWDIFF_ADAM) { m[j0 + o] = M[4 * i + q]; v[j0 + o] = V[4 * i + q]; }
+      const uint64_t j = j0 + 4 * (tid + kReplayThreads * i) + q;
+      if (j >= lo && j < hi) {
+        p[j - lo] = P[4 * i + q];
+        if (OPT == LOWDIFF_ADAM) { m[j - lo] = M[4 * i + q]; v[j - lo] = V[4 * i + q]; }
       }
     }
   }
@@ -310,7 +321,8 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
   {
     const unsigned gx = (unsigned)std::min<uint64_t>((K + 256) / 256, (uint64_t)sms * 16);
     tile_start_kernel<<<dim3(gx, (unsigned)world), 256, 0, s>>>(gathered, world, 2 * K, (uint32_t)K,
-                                                                 kMergeTileShift, (uint32_t)n_tiles, start);
+                                                                 kMergeTileShift, 0u, (uint32_t)n_tiles, nullptr,
+                                                                 start);
   }
   const unsigned grid = (unsigned)n_tiles;
   if (world == 1) {
@@ -330,11 +342,13 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
 }
 
 cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* consts5, int world, int64_t n_steps,
-                          const uint32_t* diffs, const float* scal_dev, float* p, float* m, float* v,
-                          cudaStream_t s) {
-  const int64_t psi = c->psi;
+                          const uint32_t* diffs, const float* scal_dev, uint64_t lo, uint64_t hi,
+                          const uint32_t* ranges, float* p, float* m, float* v, cudaStream_t s) {
+  if (lo >= hi) return cudaSuccess;
   const uint64_t K = (uint64_t)c->K;
-  const int64_t n_tiles = (psi + kReplayTile - 1) / kReplayTile;
+  // the window of tiles that hold [lo, hi): tile0 .. tile0 + n_tiles - 1 (start table: n_tiles + 1)
+  const int64_t tile0 = (int64_t)(lo >> kReplayTileShift);
+  const int64_t n_tiles = (int64_t)((hi - 1) >> kReplayTileShift) - tile0 + 1;
   const size_t tbytes = (size_t)n_steps * world * (n_tiles + 1) * sizeof(uint32_t);
   if (c->replay_scratch_bytes < tbytes) {
     if (c->replay_scratch) cudaFree(c->replay_scratch);
@@ -353,8 +367,8 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
     const int64_t nb = n_steps * world;
     const unsigned gy = (unsigned)std::min<int64_t>(nb, 65535);
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((K + 256) / 256, (int64_t)sms * 16 / gy + 1));
-    tile_start_kernel<<<dim3(gx, gy), 256, 0, s>>>(diffs, nb, 2 * K, (uint32_t)K, kReplayTileShift,
-                                                   (uint32_t)n_tiles, start);
+    tile_start_kernel<<<dim3(gx, gy), 256, 0, s>>>(diffs, nb, 2 * K, (uint32_t)K, kReplayTileShift, (uint32_t)tile0,
+                                                   (uint32_t)(tile0 + n_tiles), ranges, start);
   }
   prof_end(c, h, s);
   prof_begin(c, "replay", s, &h);
@@ -362,7 +376,7 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
   const int dm = div_mode(mean, world);
 #define LD_REPLAY(OPT, DIV, W) \
   replay_kernel<OPT, DIV, W><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, \
-                                                             ak, (uint64_t)psi, p, m, v)
+                                                             ak, lo, hi, tile0, p, m, v)
 #define LD_REPLAY_W(OPT, DIV)                                  \
   do {                                                         \
     if (world == 1) LD_REPLAY(OPT, DIV, 1);                    \

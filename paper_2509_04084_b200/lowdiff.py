@@ -75,11 +75,14 @@ def lib():
             "residual_materialize": ([P, P, P], S),
             "exchange": ([P, P, P, P, P], S),
             "merge": ([P, C.c_int32, P, P, P], S),
+            "exchange_update": ([P, P, P, C.POINTER(StepScalars), P, P, P, P], S),
             "batch_persist": ([P, C.c_int64, C.POINTER(StepScalars), P, P], S),
             "full_ckpt": ([P, C.c_int64, P, P, P, P], S),
             "wait_persist": ([P, P], S),
             "recover": ([P, C.c_int64, P, P, P, C.POINTER(C.c_int64), P], S),
             "replay": ([P, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P], S),
+            "replay_range": ([P, C.c_int32, C.c_int32, C.c_int64, P, P, C.c_int64, C.c_int64, P, P, P, P], S),
+            "recover_sharded": ([P, C.c_int64, P, P, P, C.c_int32, C.POINTER(C.c_int64), P], S),
             "snapshot_layer": ([P, C.c_int64, C.c_int32, C.c_int32, P, P], S),
             "snapshot_wait": ([P, C.c_int64, C.POINTER(C.c_void_p)], S),
             "replica_init": ([P, C.c_int64, P, P, P, C.c_int32, P], S),
@@ -117,8 +120,8 @@ def lib():
     return _lib
 
 
-EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_materialize", "exchange", "merge", "batch_persist",
-            "full_ckpt", "wait_persist", "recover", "replay", "snapshot_layer", "snapshot_wait", "replica_init",
+EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_materialize", "exchange", "merge", "exchange_update", "batch_persist",
+            "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "replica_init",
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
             "sync", "get_stats",
             "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
@@ -282,6 +285,10 @@ class Context:
     def merge(self, world, gathered, dense_out, stream=None):
         self._c("merge", lib().lowdiff_merge(self._h, world, _ptr(gathered), _ptr(dense_out), _stream(stream)))
 
+    def exchange_update(self, send, gathered, scalars: StepScalars, p, m=None, v=None, stream=None):
+        self._c("exchange_update", lib().lowdiff_exchange_update(self._h, _ptr(send), _ptr(gathered), C.byref(scalars),
+                                                                 _ptr(p), _ptr(m), _ptr(v), _stream(stream)))
+
     def batch_persist(self, iteration, scalars: StepScalars, send, stream=None):
         self._c("batch_persist", lib().lowdiff_batch_persist(self._h, iteration, C.byref(scalars), _ptr(send),
                                                              _stream(stream)))
@@ -303,6 +310,19 @@ class Context:
         self._c("replay", lib().lowdiff_replay(self._h, optim, world, n_steps, _ptr(diffs), arr, _ptr(p), _ptr(m),
                                                _ptr(v), _stream(stream)))
         self._keep_scalars = arr
+
+    def replay_range(self, optim, world, n_steps, diffs, scalars, begin, end, p, m=None, v=None, stream=None):
+        """p, m, v: device float32 tensors of end - begin elements (the range only)."""
+        arr = (StepScalars * max(1, n_steps))(*scalars)
+        self._c("replay_range", lib().lowdiff_replay_range(self._h, optim, world, n_steps, _ptr(diffs), arr, begin, end,
+                                                           _ptr(p), _ptr(m), _ptr(v), _stream(stream)))
+        self._keep_scalars = arr
+
+    def recover_sharded(self, p, m=None, v=None, target=-1, gather=True, stream=None) -> int:
+        it = C.c_int64()
+        self._c("recover_sharded", lib().lowdiff_recover_sharded(self._h, target, _ptr(p), _ptr(m), _ptr(v),
+                                                                 int(bool(gather)), C.byref(it), _stream(stream)))
+        return it.value
 
     def snapshot_layer(self, iteration, first_layer, n_layers, grad_bucket, stream=None):
         self._c("snapshot_layer", lib().lowdiff_snapshot_layer(self._h, iteration, first_layer, n_layers,
