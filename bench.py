@@ -269,7 +269,7 @@ def run_ours(args):
     value = world * 4 * psi / (ms_step / 1e3) / 1e9
 
     # roofline of the dominant kernel: the scan (EF add + residual write + candidate compaction)
-    psi_large = sum(n for n in sizes if n > 16384)
+    psi_large = sum(n for n in sizes if n > 4096)   # layers above kSmallMax go through the scan
     scan_bytes = 12 * psi_large
     scan_ms = kern.get("scan", {}).get("ms_per_launch", float("nan"))
     achieved = scan_bytes / (scan_ms / 1e3) / 1e9
@@ -282,6 +282,34 @@ def run_ours(args):
     roofline = {"kernel": "scan_kernel (lowdiff_compress pass A)", "bound": "hbm", "achieved": achieved,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                 "algorithmic_bytes_per_launch": scan_bytes, "peak_source": peaks["note"]}
+
+    # live optimizer step from the gathered blocks (NEXT-1 second half): exchange_update never
+    # materialises G; compared with exchange (merge) + a dense Adam step in the algorithmic-byte model
+    update = None
+    if not args.no_update:
+        p = torch.randn(psi, device=dev) * 0.02
+        m = torch.zeros(psi, device=dev)
+        v = torch.zeros(psi, device=dev)
+        sd = sends[0]
+        for t in range(2):
+            ctx.exchange_update(sd, gathered, scal[t], p, m, v)
+        torch.cuda.synchronize()
+        n_u = 5
+        u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        u0.record()
+        for t in range(n_u):
+            ctx.exchange_update(sd, gathered, scal[t + 2], p, m, v)
+        u1.record()
+        torch.cuda.synchronize()
+        ums = allmax(u0.elapsed_time(u1), world) / n_u
+        fused_b = 24 * psi + 8 * world * K
+        unfused_b = (4 * psi + 8 * world * K) + 28 * psi
+        update = {"ms_per_step": ums, "algorithmic_bytes": fused_b, "gbs": fused_b / (ums / 1e3) / 1e9,
+                  "frac_of_hbm": fused_b / (ums / 1e3) / B_HBM,
+                  "unfused_model_bytes": unfused_b, "unfused_floor_ms": unfused_b / B_HBM * 1e3,
+                  "note": "allgather + fused merge/Adam (replay kernel, n=1); p, m, v fp32 in HBM"}
+        del p, m, v
 
     # BJ:5 gate: T_floor / t_chain; PCIe D2H bandwidth measured here
     host = torch.empty(2 * K, dtype=torch.int32, pin_memory=True)
@@ -478,7 +506,7 @@ def run_ours(args):
                        "persist": "D2H of the rank's block into the pinned ring inside the timed region; "
                                   "file writing measured separately (writer)"},
             "roofline": roofline, "gate_bj5": gate, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": clk, "recovery": recovery, "writer": writer, "full_ckpt": fullck,
+            "gpu_launches": launches, "clocks": clk, "recovery": recovery, "writer": writer, "full_ckpt": fullck, "update": update,
             "replica": replica,
             "spec": {"hits": st["spec_hits"], "misses": st["spec_misses"]}}
     print(json.dumps(line), flush=True)
@@ -500,6 +528,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-replica", action="store_true")
     ap.add_argument("--no-full", action="store_true")
+    ap.add_argument("--no-update", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -136,6 +136,31 @@ lowdiff_status lowdiff_exchange(lowdiff_ctx *ctx, const uint32_t *send, uint32_t
 lowdiff_status lowdiff_merge(lowdiff_ctx *ctx, int32_t world, const uint32_t *gathered,
                              float *dense_out, void *stream);
 
+/* ---- Peer-memory exchange: allgather fused into the merge over NVLink ----
+ * Each rank's send blocks live in library-owned device "slots" that the other ranks map (CUDA
+ * IPC); lowdiff_exchange_peer's merge kernel reads every rank's entries of its output tile
+ * straight from the owner's HBM, so no gathered buffer is written or re-read locally.
+ * Same arithmetic as lowdiff_exchange (bitwise equal).  Protocol (all ranks in lockstep):
+ *   1. lowdiff_peer_alloc(ctx, n, slots, flags, handles): n in 1..4 slots of u32[2K] (+ a tile
+ *      table) and a flag buffer (*flags, may be NULL); handles (may be NULL) = (n + 1) x 64-byte cudaIpcMemHandle_t (slots,
+ *      then flags) to share with the other ranks (e.g. torch.distributed.all_gather_object).
+ *   2. lowdiff_ipc_open(ctx, handle, &ptr) for every peer handle (mappings are closed by
+ *      lowdiff_destroy), then lowdiff_peer_set(ctx, ptrs): ptrs = world x (n + 1) device
+ *      pointers in rank order (rank q: its n slots, then its flags; own entries = own buffers).
+ *      Ranks that share one device (tests) pass each other's pointers directly.
+ *   3. every iteration: lowdiff_compress(ctx, g, r, slots[i], s) -- it first waits (device-side)
+ *      until every rank has read the previous block of slot i, and afterwards publishes the new
+ *      block with its per-slot epoch -- then lowdiff_exchange_peer(ctx, i, dense_out, s), which
+ *      waits (device-side) for every rank's block of this epoch, merges, and tells every owner
+ *      it is done.  Alternate slots so that one rank's compress overlaps the peers' reads.
+ *   Every device-side wait is bounded (20 s): a protocol misuse (a rank that never compresses or
+ *   exchanges) then surfaces as LOWDIFF_E_STATE from lowdiff_sync rather than a hang. */
+lowdiff_status lowdiff_peer_alloc(lowdiff_ctx *ctx, int32_t n_slots, uint32_t **slots_out, void **flags_out,
+                                  void *handles_out);
+lowdiff_status lowdiff_ipc_open(lowdiff_ctx *ctx, const void *handle64, void **ptr);
+lowdiff_status lowdiff_peer_set(lowdiff_ctx *ctx, const void *const *ptrs);
+lowdiff_status lowdiff_exchange_peer(lowdiff_ctx *ctx, int32_t slot, float *dense_out, void *stream);
+
 /* Exchange + optimizer step without a dense gradient (Alg. 1 lines 5, 7, 8,
  *    PAPER.md:231-237): the allgather of lowdiff_exchange, then p, m, v <- Opt(G, scalars) with
  *    G the merge of the gathered blocks computed tile by tile in shared memory and never written

@@ -542,6 +542,14 @@ lowdiff_status lowdiff_sync(lowdiff_ctx* c) {
   CK(cudaMemcpy(err, c->plan.err, 8, cudaMemcpyDeviceToHost));
   lowdiff_status d = take_deferred(c);
   if (d) return d;
+  if (c->peer_flags) {
+    unsigned long long pe = 0;
+    CK(cudaMemcpy(&pe, c->peer_flags + ld::peer_err_word(c->peer_slots), 8, cudaMemcpyDeviceToHost));
+    if (pe) {
+      CK(cudaMemset(c->peer_flags + ld::peer_err_word(c->peer_slots), 0, 8));
+      return fail(c, LOWDIFF_E_STATE, "peer exchange: a wait for another rank timed out (protocol misuse)");
+    }
+  }
   if (err[0] > c->err_seen.load()) {
     // the device keeps a monotone counter of non-finite events; report only new ones
     c->err_seen = err[0];
@@ -583,6 +591,9 @@ lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
   if (c->replay_scratch) cudaFree(c->replay_scratch);
   if (c->merge_scratch) cudaFree(c->merge_scratch);
   if (c->full_stage) cudaFree(c->full_stage);
+  for (void* q : c->peer_opened) cudaIpcCloseMemHandle(q);
+  for (uint32_t* q : c->peer_own) cudaFree(q);
+  if (c->peer_flags) cudaFree(c->peer_flags);
   for (auto e : {c->ev_tmp, c->ev_side_all, c->last_d2h, c->full_done, c->full_staged, c->snap_done[0], c->snap_done[1]})
     if (e) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
@@ -614,7 +625,105 @@ lowdiff_status lowdiff_compress(lowdiff_ctx* c, const float* grad, float* residu
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (auto& ps : c->d2h_src)   // WAR: a persist of this buffer may still be copying it out
     if (ps.first == send) CK(cudaStreamWaitEvent(s, c->slots[ps.second].done, 0));
+  int pslot = -1;                // a peer-exchange slot (NEXT-1)?
+  for (int i = 0; i < c->peer_slots; ++i)
+    if (c->peer_own[i] == send) pslot = i;
+  if (pslot >= 0 && c->peer_set && c->peer_epoch[pslot] > 0)   // WAR: every rank has read the old block
+    CK(ld::launch_peer_wait_done(c->peer_flags, c->peer_slots, pslot, c->cfg.world, c->peer_epoch[pslot], s));
   CK(ld::launch_compress(c, grad, c->cfg.error_feedback ? residual : nullptr, send, s));
+  if (pslot >= 0) {              // publish: the block's merge tile starts, then its ready flag
+    CK(ld::launch_tile_start(send, (uint64_t)c->K, c->psi, send + 2 * c->K, s));
+    c->peer_epoch[pslot] += 1;
+    CK(ld::launch_peer_ready(c->peer_flags, pslot, c->peer_epoch[pslot], s));
+    c->launches += 2;
+  }
+  return LOWDIFF_OK;
+}
+
+// ---------------------------------------------------------------- peer-memory exchange (NEXT-1)
+lowdiff_status lowdiff_peer_alloc(lowdiff_ctx* c, int32_t n_slots, uint32_t** slots_out, void** flags_out,
+                                  void* handles_out) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (n_slots < 1 || n_slots > 4 || !slots_out || c->cfg.world > ld::kPeerMaxWorld)
+    return fail(c, LOWDIFF_E_INVALID, "peer_alloc: bad argument (1..4 slots, world <= 8)");
+  if (c->peer_slots) return fail(c, LOWDIFF_E_STATE, "peer_alloc: already allocated");
+  const int64_t n_tiles = (c->psi + ld::kMergeTile - 1) / ld::kMergeTile;
+  for (int i = 0; i < n_slots; ++i) {
+    void* b = nullptr;
+    CK(cudaMalloc(&b, (2 * (size_t)c->K + (size_t)n_tiles + 1) * 4));
+    c->peer_own.push_back(static_cast<uint32_t*>(b));
+  }
+  const size_t fbytes = (size_t)(ld::peer_err_word(n_slots) + 1) * 8;
+  CK(cudaMalloc((void**)&c->peer_flags, fbytes));
+  CK(cudaMemset(c->peer_flags, 0, fbytes));
+  c->peer_slots = n_slots;
+  c->peer_epoch.assign(n_slots, 0);
+  uint8_t* h = static_cast<uint8_t*>(handles_out);
+  for (int i = 0; i < n_slots; ++i) {
+    slots_out[i] = c->peer_own[i];
+    if (h) CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(h + 64 * i), c->peer_own[i]));
+  }
+  if (h) CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(h + 64 * n_slots), c->peer_flags));
+  if (flags_out) *flags_out = c->peer_flags;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_ipc_open(lowdiff_ctx* c, const void* handle64, void** ptr) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!handle64 || !ptr) return fail(c, LOWDIFF_E_INVALID, "ipc_open: NULL argument");
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle64, sizeof hd);
+  CK(cudaIpcOpenMemHandle(ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+  c->peer_opened.push_back(*ptr);
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_peer_set(lowdiff_ctx* c, const void* const* ptrs) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!c->peer_slots || !ptrs) return fail(c, LOWDIFF_E_STATE, "peer_set: call lowdiff_peer_alloc first");
+  const int n = c->peer_slots, W = c->cfg.world;
+  for (int q = 0; q < W; ++q)
+    for (int i = 0; i <= n; ++i)
+      if (!ptrs[q * (n + 1) + i]) return fail(c, LOWDIFF_E_INVALID, "peer_set: NULL pointer");
+  for (int i = 0; i < n; ++i)
+    if (ptrs[c->cfg.rank * (n + 1) + i] != c->peer_own[i])
+      return fail(c, LOWDIFF_E_INVALID, "peer_set: own entries must be this context's slots");
+  if (ptrs[c->cfg.rank * (n + 1) + n] != c->peer_flags)
+    return fail(c, LOWDIFF_E_INVALID, "peer_set: own flag entry must be this context's flags");
+  c->peer_ptrs.assign(ptrs, ptrs + (size_t)W * (n + 1));
+  c->peer_set = true;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_exchange_peer(lowdiff_ctx* c, int32_t slot, float* dense_out, void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!c->peer_set) return fail(c, LOWDIFF_E_STATE, "exchange_peer: call lowdiff_peer_set first");
+  if (slot < 0 || slot >= c->peer_slots || !dense_out || !aligned16(dense_out))
+    return fail(c, LOWDIFF_E_INVALID, "exchange_peer: bad argument");
+  if (!c->peer_epoch[slot]) return fail(c, LOWDIFF_E_STATE, "exchange_peer: nothing was compressed into the slot");
+  const int n = c->peer_slots;
+  ld::PeerTable T{};
+  T.world = c->cfg.world;
+  T.self = c->cfg.rank;
+  T.slot = slot;
+  T.n_slots = n;
+  T.epoch = c->peer_epoch[slot];
+  for (int q = 0; q < T.world; ++q) {
+    T.send[q] = static_cast<const uint32_t*>(c->peer_ptrs[q * (n + 1) + slot]);
+    T.start[q] = T.send[q] + 2 * c->K;
+    T.flags[q] = const_cast<unsigned long long*>(static_cast<const unsigned long long*>(c->peer_ptrs[q * (n + 1) + n]));
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int h;
+  ld::prof_begin(c, "peer_merge", s, &h);
+  cudaError_t e = ld::launch_peer_merge(T, (uint64_t)c->K, c->psi, c->cfg.mean != 0, dense_out, s);
+  ld::prof_end(c, h, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "peer_merge");
+  c->launches += 2;
   return LOWDIFF_OK;
 }
 
@@ -772,6 +881,9 @@ lowdiff_status lowdiff_full_ckpt(lowdiff_ctx* c, int64_t iteration, const float*
   // Without the device memory for the stage, the snapshot goes straight D2H.
   if (c->full_stage_cap < 3 * S) {
     if (c->full_stage) cudaFree(c->full_stage);
+  for (void* q : c->peer_opened) cudaIpcCloseMemHandle(q);
+  for (uint32_t* q : c->peer_own) cudaFree(q);
+  if (c->peer_flags) cudaFree(c->peer_flags);
     c->full_stage = nullptr;
     c->full_stage_cap = 0;
     if (cudaMalloc((void**)&c->full_stage, std::max<size_t>(1, 3 * S) * 4) == cudaSuccess) c->full_stage_cap = 3 * S;

@@ -97,6 +97,24 @@ struct Slot {
 // gradient of `iteration`, 2 = persist the replica as it stands after the preceding items
 struct RepJob { int kind; int64_t iteration; lowdiff_step_scalars sc; };
 
+// peer-memory exchange (peer.cu): flag words per rank = ready[n_slots] | done[n_slots][kPeerMaxWorld]
+// | error counter
+constexpr int kPeerMaxWorld = 8;
+__host__ __device__ constexpr int peer_err_word(int n_slots) { return n_slots + n_slots * kPeerMaxWorld; }
+struct PeerTable {
+  int world, self, slot, n_slots;
+  unsigned long long epoch;
+  const uint32_t* send[kPeerMaxWorld];     // rank q's send block in `slot` (u32[2K])
+  const uint32_t* start[kPeerMaxWorld];    // rank q's merge tile-start table for that block
+  unsigned long long* flags[kPeerMaxWorld];
+};
+cudaError_t launch_peer_ready(unsigned long long* own_flags, int slot, unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_peer_wait_done(unsigned long long* own_flags, int n_slots, int slot, int world,
+                                  unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_peer_merge(const PeerTable& T, uint64_t K, int64_t psi, bool mean, float* dense, cudaStream_t s);
+// merge_replay.cu: the merge's tile-start table of one block (n_tiles + 1 entries)
+cudaError_t launch_tile_start(const uint32_t* block, uint64_t K, int64_t psi, uint32_t* start, cudaStream_t s);
+
 // replica.cpp: host optimizer steps over [0, n) split over `threads` (bitwise = the device replay)
 void host_adam(int64_t n, const float* G, const lowdiff_adam_consts& a, const lowdiff_step_scalars& s, float* p,
                float* m, float* v, int threads);
@@ -164,6 +182,14 @@ struct lowdiff_ctx {
   int64_t snap_iter[2] = {-1, -1};
   std::vector<uint8_t> snap_seen[2];
   cudaEvent_t snap_done[2] = {nullptr, nullptr};
+  // peer-memory exchange (NEXT-1; peer.cu): own slots = send u32[2K] | merge tile starts
+  int peer_slots = 0;
+  std::vector<uint32_t*> peer_own;
+  unsigned long long* peer_flags = nullptr;
+  std::vector<const void*> peer_ptrs;             // world x (n_slots + 1): slot buffers..., flags
+  bool peer_set = false;
+  std::vector<unsigned long long> peer_epoch;     // per slot: epoch of the block now in it
+  std::vector<void*> peer_opened;                 // IPC mappings opened through this context
   // LowDiff+ CPU replica of this rank's shard [rep_sb, rep_se) (replica.cpp, api.cpp)
   bool rep_active = false;
   uint64_t rep_sb = 0, rep_se = 0;

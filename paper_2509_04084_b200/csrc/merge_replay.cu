@@ -301,6 +301,14 @@ size_t replay_scratch_bytes(int64_t psi, int world, int64_t n_steps) {
   return (size_t)n_steps * world * (n_tiles + 1) * sizeof(uint32_t) + (size_t)n_steps * 3 * sizeof(float) + 256;
 }
 
+cudaError_t launch_tile_start(const uint32_t* block, uint64_t K, int64_t psi, uint32_t* start, cudaStream_t s) {
+  const int64_t n_tiles = (psi + kMergeTile - 1) / kMergeTile;
+  const unsigned gx = (unsigned)std::min<uint64_t>((K + 256) / 256, (uint64_t)num_sms2() * 16);
+  tile_start_kernel<<<dim3(gx, 1), 256, 0, s>>>(block, 1, 2 * K, (uint32_t)K, kMergeTileShift, 0u, (uint32_t)n_tiles,
+                                                 nullptr, start);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, float* dense, cudaStream_t s) {
   const int64_t psi = c->psi;
   const uint64_t K = (uint64_t)c->K;

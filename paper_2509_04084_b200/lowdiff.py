@@ -76,6 +76,10 @@ def lib():
             "exchange": ([P, P, P, P, P], S),
             "merge": ([P, C.c_int32, P, P, P], S),
             "exchange_update": ([P, P, P, C.POINTER(StepScalars), P, P, P, P], S),
+            "peer_alloc": ([P, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), P], S),
+            "ipc_open": ([P, P, C.POINTER(C.c_void_p)], S),
+            "peer_set": ([P, C.POINTER(C.c_void_p)], S),
+            "exchange_peer": ([P, C.c_int32, P, P], S),
             "batch_persist": ([P, C.c_int64, C.POINTER(StepScalars), P, P], S),
             "full_ckpt": ([P, C.c_int64, P, P, P, P], S),
             "wait_persist": ([P, P], S),
@@ -120,7 +124,8 @@ def lib():
     return _lib
 
 
-EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_materialize", "exchange", "merge", "exchange_update", "batch_persist",
+EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_materialize", "exchange", "merge", "exchange_update", "peer_alloc", "ipc_open",
+            "peer_set", "exchange_peer", "batch_persist",
             "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "replica_init",
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
             "sync", "get_stats",
@@ -164,6 +169,14 @@ def _ptr(t):
         assert t.is_contiguous(), "tensors must be contiguous"
         return C.c_void_p(t.data_ptr())
     return C.c_void_p(int(t))
+
+
+def _device_view(addr, n):
+    """An int32 CUDA tensor of n elements viewing library-owned device memory at addr (not owned)."""
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (addr, False), "version": 3,
+                                    "strides": None}
+    return torch.as_tensor(_Arr(), device="cuda")
 
 
 def _stream(s):
@@ -288,6 +301,48 @@ class Context:
     def exchange_update(self, send, gathered, scalars: StepScalars, p, m=None, v=None, stream=None):
         self._c("exchange_update", lib().lowdiff_exchange_update(self._h, _ptr(send), _ptr(gathered), C.byref(scalars),
                                                                  _ptr(p), _ptr(m), _ptr(v), _stream(stream)))
+
+    # -- peer-memory exchange (NEXT-1)
+    def peer_alloc(self, n_slots=2, handles=True):
+        """Allocates the library's send slots; returns (slot tensors u32[2K] as int32 views, handle bytes)."""
+        ptrs = (C.c_void_p * n_slots)()
+        hbuf = C.create_string_buffer(64 * (n_slots + 1)) if handles else None
+        flags = C.c_void_p()
+        self._c("peer_alloc", lib().lowdiff_peer_alloc(self._h, n_slots, ptrs, C.byref(flags), hbuf))
+        self.peer_n = n_slots
+        self.peer_ptrs = [int(p) for p in ptrs]
+        self.peer_flags_ptr = int(flags.value)
+        return [_device_view(p, 2 * self.K) for p in self.peer_ptrs], (hbuf.raw if handles else None)
+
+    def ipc_open(self, handle: bytes) -> int:
+        out = C.c_void_p()
+        self._c("ipc_open", lib().lowdiff_ipc_open(self._h, C.create_string_buffer(handle, 64), C.byref(out)))
+        return out.value
+
+    def peer_set(self, table):
+        """table: world x (n_slots + 1) device addresses (rank order; each rank's slots then flags)."""
+        flat = [int(x) for row in table for x in row]
+        arr = (C.c_void_p * len(flat))(*flat)
+        self._c("peer_set", lib().lowdiff_peer_set(self._h, arr))
+
+    def peer_setup(self, n_slots=2, group=None):
+        """Multi-process setup over torch.distributed: allocate, share IPC handles, map the peers'."""
+        import torch.distributed as dist
+        slots, h = self.peer_alloc(n_slots, handles=True)
+        world, rank = self.opts.world, self.opts.rank
+        allh = [None] * world
+        dist.all_gather_object(allh, h, group=group)
+        table = []
+        for q in range(world):
+            if q == rank:
+                table.append(self.peer_ptrs + [self.peer_flags_ptr])
+            else:
+                table.append([self.ipc_open(allh[q][64 * i:64 * (i + 1)]) for i in range(n_slots + 1)])
+        self.peer_set(table)
+        return slots
+
+    def exchange_peer(self, slot, dense_out, stream=None):
+        self._c("exchange_peer", lib().lowdiff_exchange_peer(self._h, slot, _ptr(dense_out), _stream(stream)))
 
     def batch_persist(self, iteration, scalars: StepScalars, send, stream=None):
         self._c("batch_persist", lib().lowdiff_batch_persist(self._h, iteration, C.byref(scalars), _ptr(send),
