@@ -220,7 +220,16 @@ def run_ours(args):
     dense = torch.empty(psi, device=dev)
     # double-buffered send blocks: the D2H of iteration t's block overlaps the
     # compress of t+1; the library makes a compress wait only for the D2H of the buffer it overwrites
-    sends = [torch.empty(2 * K, dtype=torch.int32, device=dev) for _ in range(2)]
+    if args.exchange == "peer":
+        # NEXT-1: the send slots are library-owned and mapped by every peer (CUDA IPC); the merge
+        # reads the peers' blocks directly (no gathered buffer)
+        if world > 1:
+            sends = ctx.peer_setup(2)
+        else:
+            sends, _ = ctx.peer_alloc(2, handles=False)
+            ctx.peer_set([ctx.peer_ptrs + [ctx.peer_flags_ptr]])
+    else:
+        sends = [torch.empty(2 * K, dtype=torch.int32, device=dev) for _ in range(2)]
     send = sends[0]
     gathered = torch.empty(world * 2 * K, dtype=torch.int32, device=dev) if world > 1 else None
     scal = [ld.derive_step_scalars(t, 1e-3) for t in range(1, args.warmup + args.steps + 8)]
@@ -232,7 +241,10 @@ def run_ours(args):
         ctx.compress(grads[t % 2] if g is None else g, r, sd)
         # the rank's own block is final after compress: its D2H (side stream) overlaps the exchange
         ctx.batch_persist(t + 1, scal[t], sd)
-        ctx.exchange(sd, gathered, dense)
+        if args.exchange == "peer":
+            ctx.exchange_peer(t % 2, dense)
+        else:
+            ctx.exchange(sd, gathered, dense)
         it[0] += 1
         return sd
 
@@ -258,7 +270,7 @@ def run_ours(args):
     ms = allmax(e0.elapsed_time(e1), world)
     launches = ctx.kernel_launches() - l0
     kern = {}
-    for name in ("small_layer", "scan", "select", "emit", "merge", "allgather", "d2h"):
+    for name in ("small_layer", "scan", "select", "emit", "merge", "peer_merge", "allgather", "d2h"):
         tot, n = ctx.prof_read(name)
         if n:
             kern[name] = {"ms_per_launch": tot / n, "launches": n, "share_of_step": tot / args.steps / (ms / args.steps)}
@@ -308,7 +320,7 @@ def run_ours(args):
         update = {"ms_per_step": ums, "algorithmic_bytes": fused_b, "gbs": fused_b / (ums / 1e3) / 1e9,
                   "frac_of_hbm": fused_b / (ums / 1e3) / B_HBM,
                   "unfused_model_bytes": unfused_b, "unfused_floor_ms": unfused_b / B_HBM * 1e3,
-                  "note": "allgather + fused merge/Adam (replay kernel, n=1); p, m, v fp32 in HBM"}
+                  "note": "allgather + update_kernel (tile merge in smem + streaming Adam); p, m, v fp32 in HBM"}
         del p, m, v
 
     # BJ:5 gate: T_floor / t_chain; PCIe D2H bandwidth measured here
@@ -388,10 +400,11 @@ def run_ours(args):
         n_rep = int(max(1, min(args.replay_steps, (free - 3 * 4 * psi - 2 * 2**30) * 0.8 // (step_bytes * 1.1))))
         diffs = torch.empty((n_rep, world * 2 * K), dtype=torch.int32, device=dev)
         dn = torch.empty(psi, device=dev)
+        rsend = torch.empty(2 * K, dtype=torch.int32, device=dev)   # not a peer slot
         for t in range(n_rep):
             if world > 1:
-                ctx.compress(grads[t % 2], r, send)
-                ctx.exchange(send, diffs[t], dn)
+                ctx.compress(grads[t % 2], r, rsend)
+                ctx.exchange(rsend, diffs[t], dn)
             else:
                 ctx.compress(grads[t % 2], r, diffs[t])
         del dn
@@ -500,7 +513,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.workload}@{args.ppm}ppm", "psi": psi, "layers": len(sizes),
-                       "k_total": K, "density_ppm": args.ppm, "batch_size": 4, "parallelism": f"dp{world}",
+                       "k_total": K, "density_ppm": args.ppm, "batch_size": 4, "parallelism": f"dp{world}", "exchange": args.exchange,
                        "inputs": "D4 row-sparse Gaussian, alpha=0.5 rank correlation; 2 gradient buffers of "
                                  f"{4 * psi / 1e9:.2f} GB alternate (> L2, no flush needed)",
                        "persist": "D2H of the rank's block into the pinned ring inside the timed region; "
@@ -529,6 +542,8 @@ def main():
     ap.add_argument("--no-replica", action="store_true")
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-update", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="nccl: ncclAllGather + merge; peer: merge reading the peers' slots (NEXT-1)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -786,7 +786,12 @@ lowdiff_status lowdiff_exchange_update(lowdiff_ctx* c, const uint32_t* send, uin
     if (r != ncclSuccess) return fail(c, LOWDIFF_E_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
     blocks = gathered;
   }
-  return lowdiff_replay(c, c->cfg.optim, c->cfg.world, 1, blocks, scalars, p, m, v, stream);
+  if (!p || (c->cfg.optim == LOWDIFF_ADAM && (!m || !v)) || !aligned16(p) || (m && !aligned16(m)) ||
+      (v && !aligned16(v)))
+    return fail(c, LOWDIFF_E_INVALID, "exchange_update: p, m, v must be 16-byte aligned device arrays");
+  cudaError_t e = ld::launch_update(c, c->cfg.world, blocks, *scalars, p, m, v, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "launch_update");
+  return LOWDIFF_OK;
 }
 
 lowdiff_status lowdiff_batch_persist(lowdiff_ctx* c, int64_t iteration, const lowdiff_step_scalars* scalars,

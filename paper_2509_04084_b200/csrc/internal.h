@@ -230,6 +230,8 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
 cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* consts5, int world,
                           int64_t n_steps, const uint32_t* diffs, const float* scal_dev, uint64_t lo,
                           uint64_t hi, const uint32_t* ranges, float* p, float* m, float* v, cudaStream_t s);
+cudaError_t launch_update(lowdiff_ctx* c, int world, const uint32_t* gathered, const lowdiff_step_scalars& sc,
+                          float* p, float* m, float* v, cudaStream_t s);
 cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches, uint64_t* first);
 size_t merge_scratch_bytes(int64_t psi, int world, int64_t n_blocks);
 size_t replay_scratch_bytes(int64_t psi, int world, int64_t n_steps);

@@ -281,6 +281,78 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
   }
 }
 
+// Live optimizer step from the gathered blocks (lowdiff_exchange_update): the merge's
+// tile gather into shared memory, then one streaming pass over the tile's p, m, v with 128-bit
+// loads/stores, the R-11 Adam / R-12 SGD on each element (same operations and order as the replay
+// kernel, so the same bits), two float4 groups in flight per thread.  G never reaches HBM:
+// 24 B/param (Adam) + 8 N B/entry instead of merge 4 B/param + dense step 28 B/param.
+template <int OPT, int DIV>
+__global__ void __launch_bounds__(256)
+update_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const uint32_t* __restrict__ start,
+              int64_t n_tiles, uint64_t psi, AdamK ak, float lr, float r1, float r2, float* __restrict__ p,
+              float* __restrict__ m, float* __restrict__ v) {
+  __shared__ float acc[kMergeTile];
+  const int64_t t = blockIdx.x;
+  const uint64_t j0 = (uint64_t)t * kMergeTile;
+  const int len = (int)min((uint64_t)kMergeTile, psi - j0);
+  float4* acc4 = reinterpret_cast<float4*>(acc);
+  for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) acc4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  for (int r = 0; r < world; ++r) {
+    const uint32_t* idx = gathered + (uint64_t)r * 2 * K;
+    const uint32_t* val = idx + K;
+    const uint32_t* st = start + (uint64_t)r * (n_tiles + 1) + t;
+    const uint32_t a = st[0], b = st[1];
+    for (uint32_t e = a + threadIdx.x; e < b; e += blockDim.x) {
+      const uint32_t j = idx[e] - (uint32_t)j0;
+      acc[j] = __fadd_rn(acc[j], __uint_as_float(val[e]));
+    }
+    __syncthreads();
+  }
+  const float n = (float)world, inv = 1.0f / (float)world;
+  const bool eps_ok = ak.eps >= 0x1p-60f && ak.eps <= 0x1p59f;
+  auto step1 = [&](float g, float& P, float& M, float& V) {
+    if (OPT == LOWDIFF_ADAM) {
+      M = __fadd_rn(__fmul_rn(ak.b1, M), __fmul_rn(ak.c1, g));
+      V = __fadd_rn(__fmul_rn(ak.b2, V), __fmul_rn(ak.c2, __fmul_rn(g, g)));
+      const float mh = __fmul_rn(M, r1), vh = __fmul_rn(V, r2);
+      bool sl;
+      float u = adam_u_fast(mh, vh, ak.eps, &sl);
+      if (sl || !eps_ok) u = __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), ak.eps));
+      P = __fsub_rn(P, __fmul_rn(lr, u));
+    } else {
+      P = __fsub_rn(P, __fmul_rn(lr, g));
+    }
+  };
+  if (len == kMergeTile) {
+    float4* p4 = reinterpret_cast<float4*>(p + j0);
+    float4* m4 = reinterpret_cast<float4*>(m + j0);
+    float4* v4 = reinterpret_cast<float4*>(v + j0);
+#pragma unroll 2
+    for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) {
+      float4 P = __ldcs(p4 + q), M, V;
+      if (OPT == LOWDIFF_ADAM) { M = __ldcs(m4 + q); V = __ldcs(v4 + q); }
+      const float4 gv = acc4[q];
+      const float g[4] = {mean_of<DIV>(gv.x, n, inv), mean_of<DIV>(gv.y, n, inv), mean_of<DIV>(gv.z, n, inv),
+                          mean_of<DIV>(gv.w, n, inv)};
+      step1(g[0], P.x, M.x, V.x);
+      step1(g[1], P.y, M.y, V.y);
+      step1(g[2], P.z, M.z, V.z);
+      step1(g[3], P.w, M.w, V.w);
+      __stcs(p4 + q, P);
+      if (OPT == LOWDIFF_ADAM) { __stcs(m4 + q, M); __stcs(v4 + q, V); }
+    }
+  } else {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      float P = p[j0 + i], M = 0.f, V = 0.f;
+      if (OPT == LOWDIFF_ADAM) { M = m[j0 + i]; V = v[j0 + i]; }
+      step1(mean_of<DIV>(acc[i], n, inv), P, M, V);
+      p[j0 + i] = P;
+      if (OPT == LOWDIFF_ADAM) { m[j0 + i] = M; v[j0 + i] = V; }
+    }
+  }
+}
+
 int num_sms2() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -344,6 +416,47 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
     case 1: merge_kernel<1><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
     default: merge_kernel<2><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
   }
+  prof_end(c, h, s);
+  c->launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(lowdiff_ctx* c, int world, const uint32_t* gathered, const lowdiff_step_scalars& sc,
+                          float* p, float* m, float* v, cudaStream_t s) {
+  const int64_t psi = c->psi;
+  const uint64_t K = (uint64_t)c->K;
+  const int64_t n_tiles = (psi + kMergeTile - 1) / kMergeTile;
+  const size_t need = merge_scratch_bytes(psi, world, world);
+  if (c->merge_scratch_bytes < need) {
+    if (c->merge_scratch) cudaFree(c->merge_scratch);
+    c->merge_scratch = nullptr;
+    c->merge_scratch_bytes = 0;
+    cudaError_t e = cudaMalloc(&c->merge_scratch, need);
+    if (e != cudaSuccess) return e;
+    c->merge_scratch_bytes = need;
+  }
+  uint32_t* start = static_cast<uint32_t*>(c->merge_scratch);
+  int h;
+  prof_begin(c, "update", s, &h);
+  {
+    const unsigned gx = (unsigned)std::min<uint64_t>((K + 256) / 256, (uint64_t)num_sms2() * 16);
+    tile_start_kernel<<<dim3(gx, (unsigned)world), 256, 0, s>>>(gathered, world, 2 * K, (uint32_t)K,
+                                                                 kMergeTileShift, 0u, (uint32_t)n_tiles, nullptr,
+                                                                 start);
+  }
+  const AdamK ak{c->cfg.adam.beta1, c->cfg.adam.one_minus_beta1, c->cfg.adam.beta2, c->cfg.adam.one_minus_beta2,
+                 c->cfg.adam.eps};
+  const unsigned grid = (unsigned)n_tiles;
+  const int dm = div_mode(c->cfg.mean != 0, world);
+#define LD_UPD(OPT, DIV) \
+  update_kernel<OPT, DIV><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, ak, sc.lr, \
+                                               sc.bc1_inv, sc.bc2_inv, p, m, v)
+  if (c->cfg.optim == LOWDIFF_ADAM) {
+    if (dm == 0) LD_UPD(LOWDIFF_ADAM, 0); else if (dm == 1) LD_UPD(LOWDIFF_ADAM, 1); else LD_UPD(LOWDIFF_ADAM, 2);
+  } else {
+    if (dm == 0) LD_UPD(LOWDIFF_SGD, 0); else if (dm == 1) LD_UPD(LOWDIFF_SGD, 1); else LD_UPD(LOWDIFF_SGD, 2);
+  }
+#undef LD_UPD
   prof_end(c, h, s);
   c->launches += 2;
   return cudaGetLastError();
