@@ -356,6 +356,19 @@ lowdiff_status lowdiff_optimal_config(const lowdiff_sys_params *p, double *f_sta
 /* One stepwise adaptation of the integer configuration (full-checkpoint interval *fcf in time
  * units, batch size *batch) toward the rounded optimum, applied only if it lowers Eq. 3. */
 lowdiff_status lowdiff_config_step(const lowdiff_sys_params *p, int64_t *fcf, int32_t *batch);
+/* Failure-injection simulator: failures of the N GPUs as a Poisson process of rate
+ * N / M over the productive time [0, T) (inter-arrival -log(1 - u) M / N; u from splitmix64 over a
+ * counter starting at `seed`), each "software" with probability sw_fraction.
+ * Hardware failure at t: x = t mod (1/f); lost work x mod b; recovery R_F + R_D floor(x / b).
+ * Software failure (LowDiff+ replica restore): recovery R_S, no lost work.
+ * steady = N (S / W) floor(f T); wasted = lost + recovery + steady (the ledger of Eq. 3, whose
+ * expectation it equals when 1/f is a multiple of b); effective_ratio = T / (T + wasted). */
+typedef struct {
+  int64_t failures, hw_failures;
+  double lost_work, recovery, steady, wasted, effective_ratio;
+} lowdiff_sim_report;
+lowdiff_status lowdiff_simulate_failures(const lowdiff_sys_params *p, double f, double b, double sw_fraction,
+                                         double R_S, uint64_t seed, lowdiff_sim_report *out);
 
 int32_t lowdiff_abi_version(void);
 /* Device self-test of the branch-free IEEE sqrt/division used by the replay kernel against

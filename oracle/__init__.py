@@ -62,6 +62,8 @@ def lib():
         L.lowdiff_ref_wasted_time.argtypes = [C.c_double] * 9
         L.lowdiff_ref_optimal_config.restype = None
         L.lowdiff_ref_optimal_config.argtypes = [C.c_double] * 4 + [C.POINTER(C.c_double)] * 2
+        L.lowdiff_ref_simulate.restype = None
+        L.lowdiff_ref_simulate.argtypes = [C.c_double] * 11 + [C.c_uint64, P, P]
         _lib = L
     return _lib
 
@@ -215,3 +217,11 @@ def optimal_config(M, W, S, R_D):
     f, b = C.c_double(), C.c_double()
     lib().lowdiff_ref_optimal_config(M, W, S, R_D, C.byref(f), C.byref(b))
     return f.value, b.value
+
+
+def simulate(N, M, W, S, T, R_F, R_D, f, b, sw_fraction=0.0, R_S=0.0, seed=0):
+    """Failure-injection simulator: (failures, hw_failures, lost, recovery, steady, wasted)."""
+    counts = np.zeros(2, np.int64)
+    ledger = np.zeros(4, np.float64)
+    lib().lowdiff_ref_simulate(N, M, W, S, T, R_F, R_D, f, b, sw_fraction, R_S, seed, _p(counts), _p(ledger))
+    return int(counts[0]), int(counts[1]), *[float(x) for x in ledger]

@@ -483,4 +483,66 @@ void lowdiff_ref_optimal_config(double M, double W, double S, double R_D, double
   *b_star = std::cbrt(2.0 * S * R_D * M / W);
 }
 
+// --------------------------------------------------------------------------
+// Failure-injection simulator (SPEC.md failure-sim module), written as a trace
+// followed by a ledger so each step can be read against Eq. 3's itemised model:
+//   trace: failures of the N GPUs form a Poisson process of rate N / M over the productive time
+//          [0, T) (exponential inter-arrival times of mean M / N, inverse-CDF -log(1 - u)); each
+//          failure is "software" with probability sw_fraction.  u comes from splitmix64 over a
+//          counter (u_i = top 53 bits of splitmix64(seed + (i+1) * 0x9E3779B97F4A7C15) / 2^53),
+//          draws in the order: inter-arrival, kind, inter-arrival, kind, ...
+//   ledger per hardware failure at time t: x = t mod (1/f) (time since the last full checkpoint),
+//          lost work = x mod b (since the last persisted batch), merges = floor(x / b) persisted
+//          batches to replay, recovery = R_F + R_D x merges.
+//   ledger per software failure (LowDiff+): recovery = R_S (replica restore), no
+//          lost work (the replica is current).
+//   steady = N x S/W x floor(f T) full checkpoints; wasted = lost + recovery + steady.
+// --------------------------------------------------------------------------
+static uint64_t ref_splitmix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static double ref_uniform(uint64_t seed, uint64_t i) {
+  return (double)(ref_splitmix64(seed + (i + 1) * 0x9E3779B97F4A7C15ull) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+void lowdiff_ref_simulate(double N, double M, double W, double S, double T, double R_F, double R_D, double f,
+                          double b, double sw_fraction, double R_S, uint64_t seed, int64_t* counts /*[2]*/,
+                          double* ledger /*[4]: lost, recovery, steady, wasted*/) {
+  // 1. the failure trace
+  std::vector<double> times;
+  std::vector<int> software;
+  uint64_t draw = 0;
+  double t = 0.0;
+  for (;;) {
+    const double u = ref_uniform(seed, draw++);
+    t = t + (-std::log1p(-u)) * (M / N);
+    const double k = ref_uniform(seed, draw++);
+    if (t >= T) break;
+    times.push_back(t);
+    software.push_back(k < sw_fraction ? 1 : 0);
+  }
+  // 2. the ledger
+  double lost = 0.0, recovery = 0.0;
+  int64_t hw = 0;
+  for (size_t i = 0; i < times.size(); ++i) {
+    if (software[i]) {
+      recovery = recovery + R_S;
+      continue;
+    }
+    ++hw;
+    const double x = std::fmod(times[i], 1.0 / f);
+    lost = lost + std::fmod(x, b);
+    recovery = recovery + (R_F + R_D * std::floor(x / b));
+  }
+  const double steady = N * (S / W) * std::floor(f * T);
+  counts[0] = (int64_t)times.size();
+  counts[1] = hw;
+  ledger[0] = lost;
+  ledger[1] = recovery;
+  ledger[2] = steady;
+  ledger[3] = lost + recovery + steady;
+}
+
 }  // extern "C"

@@ -59,4 +59,52 @@ lowdiff_status lowdiff_config_step(const lowdiff_sys_params* p, int64_t* fcf, in
   return LOWDIFF_OK;
 }
 
+// Failure-injection simulator: one pass over a Poisson failure process of rate N / M
+// (the N GPUs, each with mean time between failures M) over the productive time [0, T), charging
+// every failure with the wasted time Alg. 1's recovery implies for the configuration (f, b):
+// hardware -> lost work since the last persisted batch + R_F + R_D per persisted batch since the
+// last full checkpoint; software (LowDiff+) -> R_S for restoring the CPU replica.
+// Random numbers: splitmix64 over a counter, inter-arrival then kind per event.
+namespace {
+struct SplitMix {
+  uint64_t seed, i = 0;
+  double next() {
+    uint64_t z = seed + (++i) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * 0x1p-53;
+  }
+};
+}  // namespace
+
+lowdiff_status lowdiff_simulate_failures(const lowdiff_sys_params* p, double f, double b, double sw_fraction,
+                                         double R_S, uint64_t seed, lowdiff_sim_report* out) {
+  if (!valid(p) || !out || !(f > 0) || !(b > 0) || !(sw_fraction >= 0 && sw_fraction <= 1) || !(R_S >= 0))
+    return LOWDIFF_E_INVALID;
+  SplitMix rng{seed};
+  const double mean_gap = p->M / p->N, interval = 1.0 / f;
+  lowdiff_sim_report r{};
+  double now = 0.0;
+  for (;;) {
+    now += -std::log1p(-rng.next()) * mean_gap;
+    const bool sw = rng.next() < sw_fraction;
+    if (now >= p->T) break;
+    r.failures += 1;
+    if (sw) {
+      r.recovery += R_S;
+    } else {
+      r.hw_failures += 1;
+      const double since_full = std::fmod(now, interval);
+      r.lost_work += std::fmod(since_full, b);
+      r.recovery += p->R_F + p->R_D * std::floor(since_full / b);
+    }
+  }
+  r.steady = p->N * (p->S / p->W) * std::floor(f * p->T);
+  r.wasted = r.lost_work + r.recovery + r.steady;
+  r.effective_ratio = p->T / (p->T + r.wasted);
+  *out = r;
+  return LOWDIFF_OK;
+}
+
 }  // extern "C"

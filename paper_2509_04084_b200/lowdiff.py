@@ -50,6 +50,12 @@ class SysParams(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("N", "M", "W", "S", "T", "R_F", "R_D")]
 
 
+class SimReport(C.Structure):
+    _fields_ = [("failures", C.c_int64), ("hw_failures", C.c_int64), ("lost_work", C.c_double),
+                ("recovery", C.c_double), ("steady", C.c_double), ("wasted", C.c_double),
+                ("effective_ratio", C.c_double)]
+
+
 class Stats(C.Structure):
     _fields_ = [("files_written", C.c_int64), ("bytes_written", C.c_int64), ("ring_stall_ns", C.c_int64),
                 ("writer_busy_ns", C.c_int64), ("spec_hits", C.c_int64), ("spec_misses", C.c_int64),
@@ -115,6 +121,8 @@ def lib():
             "wasted_time": ([C.POINTER(SysParams), C.c_double, C.c_double, C.POINTER(C.c_double)], S),
             "optimal_config": ([C.POINTER(SysParams), C.POINTER(C.c_double), C.POINTER(C.c_double)], S),
             "config_step": ([C.POINTER(SysParams), C.POINTER(C.c_int64), C.POINTER(C.c_int32)], S),
+            "simulate_failures": ([C.POINTER(SysParams), C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                   C.POINTER(SimReport)], S),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, "lowdiff_" + name)
@@ -131,7 +139,8 @@ EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_mater
             "sync", "get_stats",
             "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
             "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host",
-            "write_full_host", "abi_version", "selftest", "wasted_time", "optimal_config", "config_step"]
+            "write_full_host", "abi_version", "selftest", "wasted_time", "optimal_config", "config_step",
+            "simulate_failures"]
 
 
 def wasted_time(params: dict, f: float, b: float) -> float:
@@ -153,6 +162,15 @@ def config_step(params: dict, fcf: int, batch: int):
     f, b = C.c_int64(fcf), C.c_int32(batch)
     _check("config_step", lib().lowdiff_config_step(C.byref(SysParams(**params)), C.byref(f), C.byref(b)))
     return f.value, b.value
+
+
+def simulate_failures(params: dict, f: float, b: float, sw_fraction: float = 0.0, R_S: float = 0.0,
+                      seed: int = 0) -> dict:
+    """Failure-injection simulator: the wasted-time ledger of one failure trace."""
+    out = SimReport()
+    _check("simulate_failures", lib().lowdiff_simulate_failures(C.byref(SysParams(**params)), f, b, sw_fraction, R_S,
+                                                                seed, C.byref(out)))
+    return {k: getattr(out, k) for k, _ in SimReport._fields_}
 
 
 def selftest(which: int, n: int = 0, seed: int = 0):

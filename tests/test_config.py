@@ -87,3 +87,57 @@ def test_stepwise_adaptation_converges_and_never_worsens(ref, p):
     assert abs(batch - round(b_star)) <= 1
     with pytest.raises(ld.LowDiffError):
         B.config_step(dict(p, M=0.0), 10, 2)
+
+
+# ---------------------------------------------------------------- failure-injection simulator
+SIM = dict(N=8, M=2000.0, W=0.6e9, S=1.4e9, T=2e5, R_F=5.0, R_D=0.2)
+
+
+def test_sim_trace_is_poisson_and_deterministic(ref):
+    """The trace has N T / M failures in expectation (Poisson: within 4 sigma), is a pure function
+    of the seed, and the kind draw follows sw_fraction."""
+    a = ref.simulate(*ref_args(SIM), 1 / 200.0, 4.0, 0.0, 0.0, seed=11)
+    assert a == ref.simulate(*ref_args(SIM), 1 / 200.0, 4.0, 0.0, 0.0, seed=11)
+    assert a != ref.simulate(*ref_args(SIM), 1 / 200.0, 4.0, 0.0, 0.0, seed=12)
+    lam = SIM["N"] * SIM["T"] / SIM["M"]
+    assert abs(a[0] - lam) < 4 * math.sqrt(lam)
+    assert a[1] == a[0]                                     # sw_fraction 0: all hardware
+    s1 = ref.simulate(*ref_args(SIM), 1 / 200.0, 4.0, 1.0, 3.0, seed=11)
+    assert s1[0] == a[0] and s1[1] == 0                     # same arrival draws, all software
+    assert s1[2] == 0.0 and s1[3] == 3.0 * s1[0]            # software: R_S each, no lost work
+    h = ref.simulate(*ref_args(SIM), 1 / 200.0, 4.0, 0.5, 3.0, seed=11)
+    assert abs(h[1] - 0.5 * h[0]) < 4 * math.sqrt(0.25 * h[0])
+
+
+def test_sim_ledger_and_no_failure_limit(ref):
+    n, hw, lost, rec, steady, wasted = ref.simulate(*ref_args(SIM), 1 / 250.0, 5.0, 0.2, 1.0, seed=3)
+    assert wasted == lost + rec + steady
+    assert steady == SIM["N"] * (SIM["S"] / SIM["W"]) * math.floor(SIM["T"] / 250.0)
+    assert 0 <= lost <= 5.0 * hw
+    quiet = dict(SIM, M=1e30)
+    assert ref.simulate(*ref_args(quiet), 1 / 250.0, 5.0, seed=3)[:4] == (0, 0, 0.0, 0.0)
+
+
+@pytest.mark.parametrize("fcf,b", [(200, 4), (300, 10), (60, 1)])
+def test_sim_mean_matches_eq3(ref, fcf, b):
+    """Over 300 seeds the mean simulated wasted time equals Eq. 3's prediction within 3 standard
+    errors (1/f a multiple of b, where Eq. 3's b/2 and (1/(fb) - 1)/2 are exact expectations).
+    This pins the recovery terms of the oracle's Eq. 3 by simulation of Alg. 1's recovery."""
+    f = 1.0 / fcf
+    xs = np.array([ref.simulate(*ref_args(SIM), f, float(b), seed=s)[5] for s in range(300)])
+    pred = ref.wasted_time(*ref_args(SIM), f, float(b))
+    se = xs.std(ddof=1) / math.sqrt(xs.size)
+    assert abs(xs.mean() - pred) < 3 * se + 1e-9 * pred, (xs.mean(), pred, se)
+
+
+def test_sim_product_matches_oracle(ref):
+    for seed in (0, 1, 99):
+        for swf in (0.0, 0.3):
+            want = ref.simulate(*ref_args(SIM), 1 / 180.0, 3.0, swf, 2.5, seed=seed)
+            got = B.simulate_failures(SIM, 1 / 180.0, 3.0, swf, 2.5, seed)
+            assert (got["failures"], got["hw_failures"]) == want[:2]
+            for k, w in zip(("lost_work", "recovery", "steady", "wasted"), want[2:]):
+                assert math.isclose(got[k], w, rel_tol=1e-12, abs_tol=1e-12), (k, got[k], w)
+            assert got["effective_ratio"] == SIM["T"] / (SIM["T"] + got["wasted"])
+    with pytest.raises(ld.LowDiffError):
+        B.simulate_failures(SIM, 0.0, 3.0)
