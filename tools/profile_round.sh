@@ -1,0 +1,19 @@
+#!/bin/bash
+# One profiling pass on a GPU box (run under gpurun from the repo root); outputs in gpurun_out/.
+# Not part of the product.  1) the bench line, 2) the ncu launch list of a short bench command,
+# 3) ncu --set full of the top kernels (one launch each, steady state).
+set -u
+OUT=gpurun_out
+mkdir -p $OUT
+python bench.py --steps 20 --warmup 8 > $OUT/p_bench.json 2> $OUT/p_bench.err
+tail -2 $OUT/p_bench.err
+SHORT="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-writer --no-replica --no-full --replay-steps 10"
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active \
+    --clock-control none -c 600 --csv --log-file $OUT/launches.csv $SHORT > $OUT/p_launches.out 2>&1
+tail -2 $OUT/p_launches.out
+for ks in scan_kernel:4 merge1_kernel:4 update_kernel:4 replay_kernel:1 emit_kernel:4; do
+  k=${ks%%:*}; skip=${ks##*:}
+  ncu --set full --clock-control none --import-source on -k regex:^$k -s $skip -c 1 -o $OUT/prof_$k $SHORT \
+      > $OUT/p_$k.out 2>&1
+  tail -1 $OUT/p_$k.out
+done
