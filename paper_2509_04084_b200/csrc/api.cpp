@@ -169,9 +169,10 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   void* p;
   if ((st = dalloc(c, nc * ld::kChunk * sizeof(uint64_t), &p))) return st; P.cand = (uint64_t*)p;
   if ((st = dalloc(c, nc * ld::kSegsPerChunk * sizeof(uint32_t), &p))) return st; P.seg_count = (uint32_t*)p;
-  if ((st = dalloc(c, nc * 4 * 6, &p))) return st;
+  if ((st = dalloc(c, nc * 4 * 7, &p))) return st;
   P.chunk_count = (uint32_t*)p; P.chunk_gt = P.chunk_count + nc; P.chunk_eq = P.chunk_gt + nc;
   P.chunk_out = P.chunk_eq + nc; P.chunk_take = P.chunk_out + nc; P.refill_list = P.chunk_take + nc;
+  P.refill_list2 = P.refill_list + nc;
   if ((st = dalloc(c, nl * (2048 + 2048 + 512) * 4, &p))) return st; P.hist = (uint32_t*)p;
   if ((st = dalloc(c, nl * sizeof(ld::LayerSel), &p))) return st; P.sel = (ld::LayerSel*)p;
   CK(cudaMemset(P.sel, 0, nl * sizeof(ld::LayerSel)));   // band = 0: not yet adapted
@@ -179,7 +180,10 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_T = (uint32_t*)p;
   if ((st = dalloc(c, nl * 4, &p))) return st; P.layer_total = (uint32_t*)p;
   if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_cut = (uint32_t*)p;
+  if ((st = dalloc(c, nl * 4, &p))) return st; P.thr_safe = (uint32_t*)p;
   CK(cudaMemset(P.thr, 0xFF, nl * 4));   // no speculative band before the first call
+  CK(cudaMemset(P.thr_safe, 0xFF, nl * 4));
+  CK(cudaMemset(P.sel_T, 0xFF, nl * 4));  // no previous k-th key (no drift estimate yet)
   if ((st = dalloc(c, 8 * 4, &p))) return st; P.counters = (uint32_t*)p;
   if ((st = dalloc(c, 4 * 4, &p))) return st; P.err = (uint32_t*)p;
   CK(cudaMemset(P.err, 0, 16));

@@ -219,7 +219,9 @@ small_layer_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r
 // One warp per 1024-element segment (4 rounds of 2 float4 per lane), 4 warps per CTA.
 // REFILL = false: grid = 4 pieces x all chunks; acc = r + g; residual' = acc stored;
 //                 candidates key >= thr[layer].
-// REFILL = true : persistent grid over 4 pieces x the chunks in refill_list (count in
+// REFILL = true : (`lazy` then carries the refill level: 1 -> refill_list / counters[0] at the
+//                 layer's safe threshold thr_safe, 2 -> refill_list2 / counters[4] at 0)
+//                 persistent grid over 4 pieces x the chunks in refill_list (count in
 //                 counters[0]); acc re-read (r when EF, else g); thr = 0.
 // Candidates are 64-bit (acc bits << 32 | global index) so a segment's run is one contiguous,
 // mostly full-sector write.
@@ -244,16 +246,19 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   uint64_t* sbuf = sbuf_all[warp];
-  const uint32_t n_items = REFILL ? P.counters[0] * kPiecesPerChunk : (uint32_t)P.n_chunks * kPiecesPerChunk;
+  // refill level (REFILL only): 1 = rescan at the layer's safe threshold, 2 = rescan at 0
+  const uint32_t* rlist = lazy == 2 ? P.refill_list2 : P.refill_list;
+  const uint32_t n_items = REFILL ? P.counters[lazy == 2 ? 4 : 0] * kPiecesPerChunk
+                                  : (uint32_t)P.n_chunks * kPiecesPerChunk;
   for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-    const int ch = REFILL ? (int)P.refill_list[w / kPiecesPerChunk] : (int)(w / kPiecesPerChunk);
+    const int ch = REFILL ? (int)rlist[w / kPiecesPerChunk] : (int)(w / kPiecesPerChunk);
     const int seg = (int)(w % kPiecesPerChunk) * kScanWarps + warp;
     // chunk-local 32-bit offsets keep the register footprint (and so the occupancy that hides HBM
     // latency) at the level of a plain streaming kernel
     const uint64_t cbase = P.chunk_base[ch];
     const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
     const int slot = P.chunk_slot[ch];
-    const uint32_t thr = REFILL ? 0u : P.thr[slot];
+    const uint32_t thr = REFILL ? (lazy == 2 ? 0u : P.thr_safe[slot]) : P.thr[slot];
     const bool lz = !REFILL && EF && lazy;
     const uint32_t lT = lz ? P.sel_T[slot] : 0xFFFFFFFFu, lcut = lz ? P.sel_cut[slot] : 0u;
     const uint32_t gbase = (uint32_t)cbase;   // Psi < 2^32
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_ref
     __syncthreads();
   }
   const int slot = ch <= c_last ? P.chunk_slot[ch] : P.chunk_slot[c_last];
-  const bool active = ch <= c_last && (!only_refill || P.sel[slot].refill);
+  const bool active = ch <= c_last && (!only_refill || P.sel[slot].refill == (uint32_t)only_refill);
   if (active) {
     const uint32_t c = lane < kSegsPerChunk ? P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] : 0u;
     uint32_t inc = c;
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_ref
   }
   if (uniform) {
     __syncthreads();
-    if (!only_refill || P.sel[P.chunk_slot[c_first]].refill) {
+    if (!only_refill || P.sel[P.chunk_slot[c_first]].refill == (uint32_t)only_refill) {
       uint32_t* hrow = P.hist + (uint64_t)P.chunk_slot[c_first] * kHistRow;
       for (int b = threadIdx.x; b < kH0; b += 256)
         if (sh[b]) atomicAdd(&hrow[b], sh[b]);
@@ -428,9 +433,30 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_ref
   }
 }
 // ---------------------------------------------------------------- per-layer plan / digit search
-// mode 0: after scan -- decide hit/refill, find digit 0 for hits, queue refills
-// mode 1: after rescan -- find digit 0 for refilled layers
+// mode 0: after scan -- decide hit/refill, find digit 0 for hits, queue level-1 (or level-2) refills
+// mode 1: after the level-1 rescan -- hit: digit 0; still short: queue a level-2 refill
+// mode 4: after the level-2 rescan -- digit 0 for those layers (every element is a candidate)
 // mode 2/3: find digit 1/2 for every large layer (mode 2 also predicts the next band)
+__device__ __forceinline__ uint32_t layer_candidates(const DevPlan& P, int c0, int c1, int lane) {
+  uint32_t tot = 0;
+#pragma unroll 8
+  for (int c = c0 + lane; c < c1; c += 32) tot += P.chunk_count[c];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+  return tot;
+}
+
+// queue every chunk of the layer for a rescan at `level` (zeroes the layer's digit-0 histogram)
+__device__ void queue_refill(const DevPlan& P, int slot, int level, int c0, int c1, int lane) {
+  uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
+  for (int b = lane; b < kH0; b += 32) hrow[b] = 0;
+  uint32_t base = 0;
+  if (lane == 0) base = atomicAdd(&P.counters[level == 2 ? 4 : 0], (uint32_t)(c1 - c0));
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  uint32_t* list = level == 2 ? P.refill_list2 : P.refill_list;
+  for (int c = c0 + lane; c < c1; c += 32) list[base + (c - c0)] = (uint32_t)c;
+}
+
 __global__ void find_kernel(DevPlan P, int mode) {
   const int slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -439,13 +465,9 @@ __global__ void find_kernel(DevPlan P, int mode) {
   const uint32_t k = P.layer_k[li];
   LayerSel& S = P.sel[slot];
   uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
+  const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
   if (mode == 0) {
-    const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
-    uint32_t tot = 0;
-#pragma unroll 8
-    for (int c = c0 + lane; c < c1; c += 32) tot += P.chunk_count[c];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+    const uint32_t tot = layer_candidates(P, c0, c1, lane);
     if (tot >= k) {
       uint32_t bin, above;
       warp_find_bin(hrow, kH0, k, &bin, &above);
@@ -456,24 +478,39 @@ __global__ void find_kernel(DevPlan P, int mode) {
         // admitted tot / k x k now.  Aim the next band at 1.5 k_l admitted.
         const float b = S.band > 0.f ? S.band : 1.5f;
         S.band = fminf(4.f, fmaxf(1.02f, b * 1.5f * (float)k / (float)tot));
+        S.alpha = fminf(0.5f, S.alpha + 0.05f);   // drift share of the threshold: recover slowly
         atomicAdd(&P.counters[1], 1u);
         atomicAdd(&P.counters[3], tot);
       }
     } else {
-      for (int b = lane; b < kH0; b += 32) hrow[b] = 0;
-      uint32_t base = 0;
+      // missed.  Level 1 rescans at the safe threshold (this distribution's band, without the
+      // drift share) when that is lower than the one that missed; otherwise straight to level 2.
+      const int level = P.thr_safe[slot] < P.thr[slot] ? 1 : 2;
+      queue_refill(P, slot, level, c0, c1, lane);
       if (lane == 0) {
-        base = atomicAdd(&P.counters[0], (uint32_t)(c1 - c0));
-        S.refill = 1;
+        S.refill = (uint32_t)level;
         S.total = (uint32_t)(P.layer_off[li + 1] - P.layer_off[li]);
-        S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : 1.5f;   // missed: widen
+        S.alpha *= 0.5f;                          // the drift prediction overshot
+        if (level == 2) S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : 1.5f;   // widen
         atomicAdd(&P.counters[2], 1u);
       }
-      base = __shfl_sync(0xFFFFFFFFu, base, 0);
-      for (int c = c0 + lane; c < c1; c += 32) P.refill_list[base + (c - c0)] = (uint32_t)c;
     }
   } else if (mode == 1) {
-    if (!S.refill) return;
+    if (S.refill != 1) return;
+    const uint32_t tot = layer_candidates(P, c0, c1, lane);
+    if (tot >= k) {
+      uint32_t bin, above;
+      warp_find_bin(hrow, kH0, k, &bin, &above);
+      if (lane == 0) { S.prefix = bin; S.kleft = k - above; S.total = tot; }
+    } else {
+      queue_refill(P, slot, 2, c0, c1, lane);
+      if (lane == 0) {
+        S.refill = 2;
+        S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : 1.5f;
+      }
+    }
+  } else if (mode == 4) {
+    if (S.refill != 2) return;
     uint32_t bin, above;
     warp_find_bin(hrow, kH0, k, &bin, &above);
     if (lane == 0) { S.prefix = bin; S.kleft = k - above; }
@@ -500,7 +537,17 @@ __global__ void find_kernel(DevPlan P, int mode) {
           nt = b0 << 20;
         }
       }
-      if (lane == 0) S.next_thr = nt;
+      // drift share: under error feedback the k-th key moved from T_{t-1} (sel_T, still the previous
+      // call's) to T_t (>= the digit-1 prefix); lead the next band by alpha x that drift.
+      const uint32_t t_lo = ((S.prefix << 11) | bin) << 9;
+      const uint32_t t_prev = P.sel_T[slot];
+      uint32_t na = nt;
+      if (t_prev != 0xFFFFFFFFu && t_lo > t_prev && nt != 0xFFFFFFFFu) {
+        const float a = fmaxf(0.f, fminf(0.5f, S.alpha));
+        na = nt + (uint32_t)(a * (float)(t_lo - t_prev));
+        na = min(na, 0x7F800000u);
+      }
+      if (lane == 0) { S.next_thr = na; S.next_safe = nt; }
     }
     if (lane == 0) { S.prefix = (S.prefix << (mode == 2 ? 11 : 9)) | bin; S.kleft -= above; }
   }
@@ -605,9 +652,12 @@ __global__ void __launch_bounds__(1024) layer_scan_kernel(DevPlan P) {
   }
   if (threadIdx.x == 0) {
     P.sel_T[slot] = T;
-    // speculative band for the next call, never above this call's T
-    const uint32_t nt = P.sel[slot].next_thr;
-    P.thr[slot] = nt <= T ? nt : T;
+    // speculative band for the next call: the drift-led threshold (may exceed T)
+    // and the safe one (never above this call's T) that a level-1 refill falls back to
+    const uint32_t ns = P.sel[slot].next_safe;
+    const uint32_t sf = ns <= T ? ns : T;
+    P.thr_safe[slot] = sf;
+    P.thr[slot] = max(sf, P.sel[slot].next_thr);
   }
 }
 
@@ -714,7 +764,7 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   if (!P.n_large) return cudaGetLastError();
   e = cudaMemsetAsync(P.hist, 0, compress_hist_bytes(P.n_large), s);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(P.counters, 0, 4 * sizeof(uint32_t), s);
+  e = cudaMemsetAsync(P.counters, 0, 8 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const int sms = num_sms();
   const int layer_blocks = (P.n_large * 32 + 255) / 256;     // warp per large layer
@@ -731,10 +781,12 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   prof_begin(c, "select", s, &h);
   chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 0);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 0);
-  if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, 0);
-  else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, 0);
-  chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
-  find_kernel<<<layer_blocks, 256, 0, s>>>(P, 1);
+  for (int level = 1; level <= 2; ++level) {   // refills (empty grids in the steady state)
+    if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, level);
+    else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, level);
+    chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, level);
+    find_kernel<<<layer_blocks, 256, 0, s>>>(P, level == 1 ? 1 : 4);
+  }
   digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 2);
   digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 2);
@@ -746,7 +798,7 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   emit_kernel<<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K);
   prof_end(c, h, s);
   c->lazy_residual = ef ? residual : nullptr;   // this call's large-layer selection is now pending
-  c->launches += 14;
+  c->launches += 17;
   return cudaGetLastError();
 }
 

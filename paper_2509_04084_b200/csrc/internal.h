@@ -40,9 +40,10 @@ struct LayerSel {
   uint32_t kleft;    // entries still to take among those matching prefix
   uint32_t total;    // candidate count
   uint32_t refill;   // 1: speculative band too narrow, whole layer became candidates
-  uint32_t next_thr; // speculative band for the next call
+  uint32_t next_thr; // speculative band for the next call (drift-led)
   float band;        // band width as a multiple of k_l in this call's distribution (adaptive; 0 = unset)
-  uint32_t pad[2];
+  uint32_t next_safe;// the same band without the drift lead (level-1 refill threshold)
+  float alpha;       // share of the last drift of T the next band leads by (adaptive)
 };
 
 struct DevPlan {
@@ -78,8 +79,11 @@ struct DevPlan {
   // {key(r) > sel_T} U {key(r) == sel_T and index < sel_cut}; the next scan zeroes it on the fly
   uint32_t* sel_T;               // [n_large] previous call's exact k-th key
   uint32_t* sel_cut;             // [n_large] one past the global index of the last tie it took
-  uint32_t* refill_list;         // [n_chunks] chunk ids to rescan
-  uint32_t* counters;            // [0] refill chunk count, [1] spec hits, [2] spec misses
+  uint32_t* refill_list;         // [n_chunks] chunk ids to rescan at the safe threshold (level 1)
+  uint32_t* refill_list2;        // [n_chunks] chunk ids to rescan at 0 (level 2)
+  uint32_t* thr_safe;            // [n_large] the band without the drift lead
+  uint32_t* counters;            // [0] level-1 refill chunks, [1] spec hits, [2] spec misses,
+                                 // [3] candidates of hit layers, [4] level-2 refill chunks
   uint32_t* err;                 // [0] non-finite flag, [1] first bad layer
 };
 
