@@ -374,7 +374,8 @@ int32_t lowdiff_abi_version(void);
 /* Device self-test of the branch-free IEEE sqrt/division used by the replay kernel against
  * __fsqrt_rn/__fdiv_rn (which = 0: all 2^31+1 non-negative floats; which = 1: n pseudo-random
  * operand pairs from `seed`; which = 2: Adam's fused u = mh / (sqrt(vh) + eps) on n random
- * triples).  Needs a GPU (current device); synchronous. */
+ * triples; which = 3: the paired (f32x2) Adam step of the replay / update kernels on n random
+ * element pairs against the scalar R-11 sequence).  Needs a GPU (current device); synchronous. */
 lowdiff_status lowdiff_selftest(int32_t which, uint64_t n, uint64_t seed, uint64_t *mismatches,
                                 uint64_t *first_bad);
 

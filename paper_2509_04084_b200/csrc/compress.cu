@@ -375,6 +375,7 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
 // only_refill: process just the chunks of refilled layers (after the rescan).
 __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_refill) {
   __shared__ uint32_t sh[kH0];
+  if (only_refill && P.counters[only_refill == 2 ? 4 : 0] == 0) return;   // no refill at this level
   const int lane = threadIdx.x & 31;
   const int c_first = blockIdx.x * 8;
   const int c_last = min(P.n_chunks, c_first + 8) - 1;

@@ -135,18 +135,29 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
   const int64_t t = tile0 + blockIdx.x;
   const uint64_t j0 = (uint64_t)t * kReplayTile;
   const int tid = threadIdx.x;
-  float P[8], M[8], V[8];
+  // state in element pairs (f32x2: FADD2/FMUL2/FFMA2 do both halves in one instruction, each
+  // rounded exactly like the scalar operation): pair x = 2 i + h holds elements 2h, 2h+1 of the
+  // thread's float4 slot i
+  f32x2 P2[4], M2[4], V2[4];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t j = j0 + 4 * (tid + kReplayThreads * i) + q;
-      const bool in = j >= lo && j < hi;
-      P[4 * i + q] = in ? p[j - lo] : 0.f;
-      M[4 * i + q] = (OPT == LOWDIFF_ADAM && in) ? m[j - lo] : 0.f;
-      V[4 * i + q] = (OPT == LOWDIFF_ADAM && in) ? v[j - lo] : 0.f;
+    for (int h = 0; h < 2; ++h) {
+      float pe[2], me[2], ve[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const uint64_t j = j0 + 4 * (tid + kReplayThreads * i) + 2 * h + e;
+        const bool in = j >= lo && j < hi;
+        pe[e] = in ? p[j - lo] : 0.f;
+        me[e] = (OPT == LOWDIFF_ADAM && in) ? m[j - lo] : 0.f;
+        ve[e] = (OPT == LOWDIFF_ADAM && in) ? v[j - lo] : 0.f;
+      }
+      P2[2 * i + h] = pk2(pe[0], pe[1]);
+      M2[2 * i + h] = pk2(me[0], me[1]);
+      V2[2 * i + h] = pk2(ve[0], ve[1]);
     }
   }
+  const AdamK2 k2 = make_adamk2(ak.b1, ak.c1, ak.b2, ak.c2, ak.eps);
   const float n = (float)world, inv = 1.0f / (float)world;
   const bool eps_ok = ak.eps >= 0x1p-60f && ak.eps <= 0x1p59f;   // adam_u_fast's precondition
   const uint64_t tstride = (uint64_t)(n_tiles + 1);   // n_tiles = tiles in the window
@@ -231,38 +242,32 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       na = __ldg(st2);
       nb = __ldg(st2 + 1);
     }
+    const f32x2 LR = pk2(slr, slr), R1 = pk2(sr1, sr1), R2 = pk2(sr2, sr2);
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {   // two halves of 4 independent element chains (ILP 4)
+    for (int i = 0; i < 2; ++i) {   // two float4 slots = 4 independent element pairs (ILP)
       const float4 gv = G4[tid + kReplayThreads * i];
-      float gx[4] = {mean_of<DIV>(gv.x, n, inv), mean_of<DIV>(gv.y, n, inv), mean_of<DIV>(gv.z, n, inv),
-                     mean_of<DIV>(gv.w, n, inv)};
+      const f32x2 g01 = pk2(mean_of<DIV>(gv.x, n, inv), mean_of<DIV>(gv.y, n, inv));
+      const f32x2 g23 = pk2(mean_of<DIV>(gv.z, n, inv), mean_of<DIV>(gv.w, n, inv));
       if (OPT == LOWDIFF_ADAM) {
         // m = b1*m + c1*g ; v = b2*v + c2*(g*g) ; mh = m*r1 ; vh = v*r2
         // d = sqrt(vh) + eps ; u = mh / d ; p = p - lr*u          (R-11)
         // Correctly rounded sqrt / divide take the exact fast sequence (ieee_fast.cuh) for every
         // lane; a warp-rare fix-up redoes out-of-window operands with the intrinsics.
-        float mh[4], vh[4], u[4];
-        bool slow = !eps_ok;
+        f32x2 mh[2], vh[2], u[2];
+        bool s0, s1;
+        u[0] = adam2_u(M2[2 * i], V2[2 * i], g01, k2, R1, R2, &mh[0], &vh[0], &s0);
+        u[1] = adam2_u(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2, &mh[1], &vh[1], &s1);
+        if (s0 || s1 || !eps_ok) {   // rare: redo the group exactly with the intrinsics
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int x = 4 * i + q;
-          M[x] = __fadd_rn(__fmul_rn(ak.b1, M[x]), __fmul_rn(ak.c1, gx[q]));
-          V[x] = __fadd_rn(__fmul_rn(ak.b2, V[x]), __fmul_rn(ak.c2, __fmul_rn(gx[q], gx[q])));
-          mh[q] = __fmul_rn(M[x], sr1);
-          vh[q] = __fmul_rn(V[x], sr2);
-          bool sl;
-          u[q] = adam_u_fast(mh[q], vh[q], ak.eps, &sl);
-          slow |= sl;
+          for (int h = 0; h < 2; ++h)
+            u[h] = pk2(__fdiv_rn(lo2(mh[h]), __fadd_rn(__fsqrt_rn(lo2(vh[h])), ak.eps)),
+                       __fdiv_rn(hi2(mh[h]), __fadd_rn(__fsqrt_rn(hi2(vh[h])), ak.eps)));
         }
-        if (slow) {   // rare: redo the whole group exactly with the intrinsics
-#pragma unroll
-          for (int q = 0; q < 4; ++q) u[q] = __fdiv_rn(mh[q], __fadd_rn(__fsqrt_rn(vh[q]), ak.eps));
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) P[4 * i + q] = __fsub_rn(P[4 * i + q], __fmul_rn(slr, u[q]));
+        P2[2 * i] = sub_prod2(P2[2 * i], LR, u[0]);
+        P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, u[1]);
       } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) P[4 * i + q] = __fsub_rn(P[4 * i + q], __fmul_rn(slr, gx[q]));
+        P2[2 * i] = sub_prod2(P2[2 * i], LR, g01);
+        P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, g23);
       }
     }
     if (ranger) { s_a[cur][tid] = na; s_b[cur][tid] = nb; }   // ranges of step s+2
@@ -273,9 +278,13 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t j = j0 + 4 * (tid + kReplayThreads * i) + q;
+      const int x = 2 * i + (q >> 1);
       if (j >= lo && j < hi) {
-        p[j - lo] = P[4 * i + q];
-        if (OPT == LOWDIFF_ADAM) { m[j - lo] = M[4 * i + q]; v[j - lo] = V[4 * i + q]; }
+        p[j - lo] = (q & 1) ? hi2(P2[x]) : lo2(P2[x]);
+        if (OPT == LOWDIFF_ADAM) {
+          m[j - lo] = (q & 1) ? hi2(M2[x]) : lo2(M2[x]);
+          v[j - lo] = (q & 1) ? hi2(V2[x]) : lo2(V2[x]);
+        }
       }
     }
   }

@@ -101,6 +101,59 @@ __global__ void adam_check_kernel(uint64_t n, uint64_t seed, unsigned long long*
   }
 }
 
+// which = 3: the paired Adam step (adam2_u + the exact fallback, then p - lr*u) on random states vs
+// the scalar R-11 sequence written with the CUDA intrinsics
+__global__ void adam2_check_kernel(uint64_t n, uint64_t seed, unsigned long long* bad, unsigned long long* first) {
+  const float eps_set[4] = {1e-8f, 1e-6f, 0x1p-60f, 1.0f};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    float p[2], m[2], v[2], g[2];
+    uint64_t h = mix64(seed ^ mix64(i));
+    const float eps = eps_set[h & 3];
+    const float b1 = 0.9f, c1 = 0.1f, b2 = 0.999f, c2 = 0.001f;
+    const float lr = exp2f(-20.f + 19.f * (float)((h >> 8) & 0xFFFF) / 65536.f);
+    const float r1 = 1.f + 9.f * (float)((h >> 24) & 0xFFFF) / 65536.f;
+    const float r2 = 1.f + 999.f * (float)((h >> 40) & 0xFFFF) / 65536.f;
+    for (int e = 0; e < 2; ++e) {
+      h = mix64(h);
+      const float mag = exp2f(-150.f + 200.f * (float)(h & 0xFFFFFF) / 16777216.f);
+      g[e] = ((h >> 24) & 1) ? -mag : mag;
+      if (((h >> 25) & 7) == 0) g[e] = ((h >> 28) & 1) ? -0.0f : 0.0f;
+      h = mix64(h);
+      p[e] = __uint_as_float((uint32_t)h & 0xBFFFFFFFu);   // finite, any sign
+      const float mm = exp2f(-150.f + 160.f * (float)((h >> 32) & 0xFFFFFF) / 16777216.f);
+      m[e] = ((h >> 56) & 1) ? -mm : mm;
+      if (((h >> 57) & 7) == 0) m[e] = 0.0f;
+      h = mix64(h);
+      v[e] = exp2f(-150.f + 160.f * (float)(h & 0xFFFFFF) / 16777216.f);
+      if (((h >> 24) & 7) == 0) v[e] = 0.0f;
+    }
+    const AdamK2 k2 = make_adamk2(b1, c1, b2, c2, eps);
+    f32x2 P = pk2(p[0], p[1]), M = pk2(m[0], m[1]), V = pk2(v[0], v[1]), mh, vh;
+    bool sl;
+    f32x2 u = adam2_u(M, V, pk2(g[0], g[1]), k2, pk2(r1, r1), pk2(r2, r2), &mh, &vh, &sl);
+    if (sl)
+      u = pk2(__fdiv_rn(lo2(mh), __fadd_rn(__fsqrt_rn(lo2(vh)), eps)),
+              __fdiv_rn(hi2(mh), __fadd_rn(__fsqrt_rn(hi2(vh)), eps)));
+    P = sub_prod2(P, pk2(lr, lr), u);
+    const float got[6] = {lo2(P), hi2(P), lo2(M), hi2(M), lo2(V), hi2(V)};
+    for (int e = 0; e < 2; ++e) {
+      const float me = __fadd_rn(__fmul_rn(b1, m[e]), __fmul_rn(c1, g[e]));
+      const float ve = __fadd_rn(__fmul_rn(b2, v[e]), __fmul_rn(c2, __fmul_rn(g[e], g[e])));
+      const float ue = __fdiv_rn(__fmul_rn(me, r1), __fadd_rn(__fsqrt_rn(__fmul_rn(ve, r2)), eps));
+      const float pe = __fsub_rn(p[e], __fmul_rn(lr, ue));
+      const float want[3] = {pe, me, ve};
+      const float have[3] = {got[e], got[2 + e], got[4 + e]};
+      for (int q = 0; q < 3; ++q) {
+        const uint32_t x = __float_as_uint(have[q]), y = __float_as_uint(want[q]);
+        if (x != y && !((x & 0x7FFFFFFFu) > 0x7F800000u && (y & 0x7FFFFFFFu) > 0x7F800000u)) {
+          atomicAdd(bad, 1ull);
+          atomicMin(first, (unsigned long long)i);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches, uint64_t* first) {
@@ -111,7 +164,8 @@ cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatc
   cudaMemcpy(d, init, 16, cudaMemcpyHostToDevice);
   if (which == 0) sqrt_check_kernel<<<148 * 16, 256>>>(d, d + 1);
   else if (which == 1) div_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
-  else adam_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
+  else if (which == 2) adam_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
+  else adam2_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
   e = cudaDeviceSynchronize();
   unsigned long long h[2] = {0, 0};
   if (e == cudaSuccess) e = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
