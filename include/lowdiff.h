@@ -252,6 +252,18 @@ lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx *ctx, int64_t iteration, int32
  *    layer of that iteration was never submitted. */
 lowdiff_status lowdiff_snapshot_wait(lowdiff_ctx *ctx, int64_t iteration, const float **host_grad);
 
+/* Snapshot bucket plan (no context, host only): cut the layer table into runs of contiguous
+ *    layers of at least min_bytes of fp32 gradient each, in BACKWARD order (the order a
+ *    backward pass finalises them: the last layer first; PAPER.md:366-369 snapshots layer by
+ *    layer as gradients become ready, and SURVEY §8(a) a9 asks for >= 4 MB runs so the many
+ *    6.4 KB LayerNorm/bias tensors are never copied one by one).  Bucket i covers layers
+ *    [first[i], first[i] + count[i]); first[0] + count[0] == n_layers, first[n-1] == 0.  The
+ *    last bucket formed (the one holding layer 0) absorbs any remainder below min_bytes.
+ *    cap = capacity of first/count; *n_buckets = buckets written.  E_INVALID on bad arguments
+ *    (n_layers < 1, a numel < 1, min_bytes < 0), E_DIM if cap is too small. */
+lowdiff_status lowdiff_bucket_plan(int32_t n_layers, const int64_t *numel, int64_t min_bytes,
+                                   int32_t *first, int32_t *count, int32_t cap, int32_t *n_buckets);
+
 /* ---- LowDiff+ CPU replica (Sec. 5.2; Alg. 2 l.11-13) ----
  * A host-resident copy of this rank's shard [floor(rank*Psi/world), floor((rank+1)*Psi/world))
  * of (p, m, v), advanced on a worker thread by the snapshotted synced gradients with the host

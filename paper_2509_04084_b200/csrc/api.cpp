@@ -1190,6 +1190,31 @@ lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx* c, int64_t iteration, int32_t
   return LOWDIFF_OK;
 }
 
+// Backward-order buckets of >= min_bytes contiguous layers (LowDiff+ snapshot granularity).
+lowdiff_status lowdiff_bucket_plan(int32_t n_layers, const int64_t* numel, int64_t min_bytes, int32_t* first,
+                                   int32_t* count, int32_t cap, int32_t* n_buckets) {
+  if (n_layers < 1 || !numel || min_bytes < 0 || !first || !count || !n_buckets || cap < 0) return LOWDIFF_E_INVALID;
+  for (int32_t l = 0; l < n_layers; ++l)
+    if (numel[l] < 1) return LOWDIFF_E_INVALID;
+  int32_t n = 0, hi = n_layers;   // the bucket being formed ends (exclusive) at layer hi
+  int64_t bytes = 0;
+  for (int32_t l = n_layers - 1; l >= 0; --l) {
+    bytes += 4 * numel[l];
+    if (bytes >= min_bytes && l > 0) {
+      if (n == cap) return LOWDIFF_E_DIM;
+      first[n] = l, count[n] = hi - l, ++n;
+      hi = l, bytes = 0;
+    }
+  }
+  // the bucket holding layer 0 takes whatever is left (possibly below min_bytes)
+  if (bytes > 0 || n == 0) {
+    if (n == cap) return LOWDIFF_E_DIM;
+    first[n] = 0, count[n] = hi, ++n;
+  }
+  *n_buckets = n;
+  return LOWDIFF_OK;
+}
+
 lowdiff_status lowdiff_snapshot_wait(lowdiff_ctx* c, int64_t iteration, const float** host_grad) {
   lowdiff_status st = entry(c);
   if (st) return st;

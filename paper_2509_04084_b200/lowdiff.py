@@ -95,6 +95,7 @@ def lib():
             "recover_sharded": ([P, C.c_int64, P, P, P, C.c_int32, C.POINTER(C.c_int64), P], S),
             "snapshot_layer": ([P, C.c_int64, C.c_int32, C.c_int32, P, P], S),
             "snapshot_wait": ([P, C.c_int64, C.POINTER(C.c_void_p)], S),
+            "bucket_plan": ([C.c_int32, P, C.c_int64, P, P, C.c_int32, C.POINTER(C.c_int32)], S),
             "replica_init": ([P, C.c_int64, P, P, P, C.c_int32, P], S),
             "replica_step": ([P, C.c_int64, C.POINTER(StepScalars)], S),
             "replica_persist": ([P], S),
@@ -134,7 +135,7 @@ def lib():
 
 EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_materialize", "exchange", "merge", "exchange_update", "peer_alloc", "ipc_open",
             "peer_set", "exchange_peer", "batch_persist",
-            "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "replica_init",
+            "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "bucket_plan", "replica_init",
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
             "sync", "get_stats",
             "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
@@ -479,6 +480,15 @@ def write_batch_host(sizes, opts: Options, first_iter, scalars, blocks):
     arr = (StepScalars * len(scalars))(*scalars)
     _check("write_batch_host", lib().lowdiff_write_batch_host(C.byref(cfg), first_iter, len(scalars), arr,
                                                               b.ctypes.data_as(C.c_void_p)))
+
+
+def bucket_plan(sizes, min_bytes=4 << 20):
+    """LowDiff+ snapshot buckets in backward order: [(first_layer, n_layers), ...]."""
+    n = len(sizes)
+    numel = (C.c_int64 * n)(*sizes)
+    first, count, nb = (C.c_int32 * n)(), (C.c_int32 * n)(), C.c_int32()
+    _check("bucket_plan", lib().lowdiff_bucket_plan(n, numel, min_bytes, first, count, n, C.byref(nb)))
+    return [(first[i], count[i]) for i in range(nb.value)]
 
 
 def host_adam_step(G, consts: AdamConsts, scalars: StepScalars, p, m, v, threads=1):

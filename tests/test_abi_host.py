@@ -181,3 +181,41 @@ def test_two_rank_gloo_sharded_files_and_chain(tmp_path):
         assert gap == B.E_GAP and idok
     files = sorted(os.listdir(tmp_path))
     assert "ld_full_r000_000000000000.ldf" in files and "ld_full_r001_000000000000.ldf" in files
+
+
+@pytest.mark.parametrize("model", ["gpt2_xl", "bert_large", "resnet50", "mlp"])
+@pytest.mark.parametrize("min_mb", [0, 1, 4, 64])
+def test_bucket_plan_covers_backward_order_minimal_runs(model, min_mb):
+    """LowDiff+ buckets: contiguous runs in backward order that tile the whole
+    layer table; every bucket but the one holding layer 0 reaches min_bytes and is minimal (dropping
+    its lowest layer falls below min_bytes), so the 6.4 KB LayerNorm/bias tensors never travel alone
+    once min_bytes exceeds them."""
+    from inputs import table
+    sizes = table(model)
+    mb = min_mb << 20
+    plan = ld.bucket_plan(sizes, mb)
+    assert plan[0][0] + plan[0][1] == len(sizes) and plan[-1][0] == 0
+    for (f0, c0), (f1, c1) in zip(plan, plan[1:]):
+        assert f1 + c1 == f0                                  # contiguous, descending
+    for f, c in plan:
+        assert c >= 1
+        b = 4 * sum(sizes[f:f + c])
+        if f > 0:
+            assert b >= mb and (c == 1 or 4 * sum(sizes[f + 1:f + c]) < mb)
+    if mb == 0:
+        assert plan == [(l, 1) for l in range(len(sizes) - 1, -1, -1)]
+    if mb >= 4 << 20 and model == "gpt2_xl":
+        assert all(c > 1 or sizes[f] * 4 >= mb for f, c in plan[:-1])
+
+
+def test_bucket_plan_errors():
+    import ctypes as C
+    L = B.lib()
+    first, count, nb = (C.c_int32 * 4)(), (C.c_int32 * 4)(), C.c_int32()
+    sizes = (C.c_int64 * 3)(10, 0, 5)
+    assert L.lowdiff_bucket_plan(3, sizes, 16, first, count, 4, C.byref(nb)) == 1       # numel < 1
+    sizes = (C.c_int64 * 3)(10, 10, 5)
+    assert L.lowdiff_bucket_plan(3, sizes, 0, first, count, 2, C.byref(nb)) == 2        # cap too small
+    assert L.lowdiff_bucket_plan(3, sizes, 0, first, count, 3, C.byref(nb)) == 0 and nb.value == 3
+    assert L.lowdiff_bucket_plan(3, sizes, 10**9, first, count, 1, C.byref(nb)) == 0
+    assert nb.value == 1 and (first[0], count[0]) == (0, 3)
