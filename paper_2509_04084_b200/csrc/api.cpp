@@ -179,6 +179,7 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   if ((st = dalloc(c, nl * 4, &p))) return st; P.thr = (uint32_t*)p;
   if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_T = (uint32_t*)p;
   if ((st = dalloc(c, nl * 4, &p))) return st; P.layer_total = (uint32_t*)p;
+  CK(cudaMemset(P.layer_total, 0, nl * 4));   // then kept zero between calls by layer_scan_kernel
   if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_cut = (uint32_t*)p;
   if ((st = dalloc(c, nl * 4, &p))) return st; P.thr_safe = (uint32_t*)p;
   CK(cudaMemset(P.thr, 0xFF, nl * 4));   // no speculative band before the first call
@@ -498,6 +499,9 @@ lowdiff_status lowdiff_create(const lowdiff_config* cfg, lowdiff_ctx** out) {
   if ((st = entry(c))) return bail(st);
   if ((st = build_plan(c))) return bail(st);
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_tmp, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_side_all, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->last_d2h, cudaEventDisableTiming) != cudaSuccess ||
@@ -601,6 +605,9 @@ lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
   for (auto e : {c->ev_tmp, c->ev_side_all, c->last_d2h, c->full_done, c->full_staged, c->snap_done[0], c->snap_done[1]})
     if (e) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->aux) cudaStreamDestroy(c->aux);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
   return st;
 }

@@ -60,12 +60,16 @@ __device__ __forceinline__ void warp_find_bin(const uint32_t* h, int nb, uint32_
   const int w = nb / 32;
   const int top = nb - lane * w;                 // lane 0 owns the highest bins
   uint32_t s = 0;
-  if (w == 64) {   // the 2048-bin digits: 64 independent loads in flight per lane
-    uint32_t part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (w == 64 || w == 16) {   // the 2048- and 512-bin digits: all of the lane's 128-bit loads in
+                              // flight at once (h is 16-byte aligned, top - w a multiple of 16)
+    const uint4* h4 = reinterpret_cast<const uint4*>(h + top - w);
+    uint4 q[16];
 #pragma unroll
-    for (int b = 0; b < 64; ++b) part[b & 7] += h[top - 1 - b];
+    for (int i = 0; i < 16; ++i)
+      if (i < w / 4) q[i] = h4[i];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) s += part[q];
+    for (int i = 0; i < 16; ++i)
+      if (i < w / 4) s += (q[i].x + q[i].y) + (q[i].z + q[i].w);
   } else {
 #pragma unroll 16
     for (int b = top - 1; b >= top - w; --b) s += h[b];
@@ -80,18 +84,44 @@ __device__ __forceinline__ void warp_find_bin(const uint32_t* h, int nb, uint32_
   const bool mine = exc < kleft && kleft <= inc;
   const unsigned who = __ballot_sync(0xFFFFFFFFu, mine);
   const int src = who ? __ffs(who) - 1 : 31;
-  uint32_t bin = 0, above = 0;
-  if (lane == src) {
-    uint32_t run = exc;
-    bin = (uint32_t)(top - w);
-    for (int b = top - 1; b >= top - w; --b) {
-      if (run + h[b] >= kleft) { bin = (uint32_t)b; break; }
-      run += h[b];
-    }
-    above = run;
+  // second level, warp-parallel: the w bins of lane src (w = 64 or <= 32), highest first, spread
+  // over the lanes (2 or 1 per lane), prefix-summed with shuffles -- two dependent loads instead of
+  // one lane walking up to 64 bins serially (that walk was ~37 us of a ResNet-50 call)
+  const int stop = __shfl_sync(0xFFFFFFFFu, top, src);
+  const uint32_t base = __shfl_sync(0xFFFFFFFFu, exc, src);
+  const uint32_t need = kleft - base;   // >= 1 when src holds the bin
+  const int per = w > 32 ? w / 32 : 1;  // bins per lane (w is 64 or a power of two <= 32)
+  const int b_hi = stop - 1 - lane * per;
+  uint32_t c0 = 0, c1 = 0;
+  if (lane * per < w) {
+    c0 = h[b_hi];
+    if (per == 2) c1 = h[b_hi - 1];
   }
-  *bin_out = __shfl_sync(0xFFFFFFFFu, bin, src);
-  *above_out = __shfl_sync(0xFFFFFFFFu, above, src);
+  const uint32_t s2 = c0 + c1;
+  uint32_t inc2 = s2;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc2, o);
+    if (lane >= o) inc2 += y;
+  }
+  const uint32_t exc2 = inc2 - s2;
+  const bool hit = lane * per < w && exc2 < need && need <= inc2;
+  const unsigned who2 = __ballot_sync(0xFFFFFFFFu, hit);
+  uint32_t bin, above;
+  if (who2) {
+    const int src2 = __ffs(who2) - 1;
+    // in lane src2: the higher bin b_hi first, then b_hi - 1
+    const bool first = exc2 + c0 >= need;
+    bin = first ? (uint32_t)b_hi : (uint32_t)(b_hi - 1);
+    above = base + exc2 + (first ? 0u : c0);
+    bin = __shfl_sync(0xFFFFFFFFu, bin, src2);
+    above = __shfl_sync(0xFFFFFFFFu, above, src2);
+  } else {   // kleft exceeds the total (never on a consistent histogram): lowest bin, all counted
+    bin = (uint32_t)(stop - w);
+    above = base + __shfl_sync(0xFFFFFFFFu, inc2, 31);
+  }
+  *bin_out = bin;
+  *above_out = above;
 }
 
 // Block-wide exclusive scan of one value per thread (blockDim.x multiple of 32, <= 1024).
@@ -375,6 +405,7 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
 // only_refill: process just the chunks of refilled layers (after the rescan).
 __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_refill) {
   __shared__ uint32_t sh[kH0];
+  __shared__ uint32_t s_tot;
   if (only_refill && P.counters[only_refill == 2 ? 4 : 0] == 0) return;   // no refill at this level
   const int lane = threadIdx.x & 31;
   const int c_first = blockIdx.x * 8;
@@ -383,6 +414,7 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_ref
   const bool uniform = P.chunk_slot[c_first] == P.chunk_slot[c_last];
   if (uniform) {
     for (int b = threadIdx.x; b < kH0; b += 256) sh[b] = 0;
+    if (threadIdx.x == 0) s_tot = 0;
     __syncthreads();
   }
   const int slot = ch <= c_last ? P.chunk_slot[ch] : P.chunk_slot[c_last];
@@ -397,7 +429,11 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_ref
     }
     const uint32_t so = inc - c;                                  // lanes 0..15: segment offsets
     const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, 31);
-    if (lane == 0) P.chunk_count[ch] = total;
+    if (lane == 0) {
+      P.chunk_count[ch] = total;
+      if (uniform) atomicAdd(&s_tot, total);
+      else atomicAdd(&P.layer_total[slot], total);   // per-layer candidate count (find mode 0/1)
+    }
     uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
     uint32_t* h0 = uniform ? sh : P.hist + (uint64_t)slot * kHistRow;
     for (uint32_t base = 0; base < total; base += 32 * kUnroll) {
@@ -430,6 +466,7 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_ref
       uint32_t* hrow = P.hist + (uint64_t)P.chunk_slot[c_first] * kHistRow;
       for (int b = threadIdx.x; b < kH0; b += 256)
         if (sh[b]) atomicAdd(&hrow[b], sh[b]);
+      if (threadIdx.x == 0 && s_tot) atomicAdd(&P.layer_total[P.chunk_slot[c_first]], s_tot);
     }
   }
 }
@@ -438,19 +475,17 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_ref
 // mode 1: after the level-1 rescan -- hit: digit 0; still short: queue a level-2 refill
 // mode 4: after the level-2 rescan -- digit 0 for those layers (every element is a candidate)
 // mode 2/3: find digit 1/2 for every large layer (mode 2 also predicts the next band)
-__device__ __forceinline__ uint32_t layer_candidates(const DevPlan& P, int c0, int c1, int lane) {
-  uint32_t tot = 0;
-#pragma unroll 8
-  for (int c = c0 + lane; c < c1; c += 32) tot += P.chunk_count[c];
-#pragma unroll
-  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
-  return tot;
+// candidates admitted for the layer this call: summed by chunk_prep (one load instead of a walk
+// over up to ~5000 chunk counts per layer)
+__device__ __forceinline__ uint32_t layer_candidates(const DevPlan& P, int slot) {
+  return *reinterpret_cast<volatile const uint32_t*>(P.layer_total + slot);
 }
 
 // queue every chunk of the layer for a rescan at `level` (zeroes the layer's digit-0 histogram)
 __device__ void queue_refill(const DevPlan& P, int slot, int level, int c0, int c1, int lane) {
   uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
   for (int b = lane; b < kH0; b += 32) hrow[b] = 0;
+  if (lane == 0) P.layer_total[slot] = 0;   // the rescan's chunk_prep recounts every chunk
   uint32_t base = 0;
   if (lane == 0) base = atomicAdd(&P.counters[level == 2 ? 4 : 0], (uint32_t)(c1 - c0));
   base = __shfl_sync(0xFFFFFFFFu, base, 0);
@@ -458,7 +493,7 @@ __device__ void queue_refill(const DevPlan& P, int slot, int level, int c0, int 
   for (int c = c0 + lane; c < c1; c += 32) list[base + (c - c0)] = (uint32_t)c;
 }
 
-__global__ void find_kernel(DevPlan P, int mode) {
+__global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
   const int slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (slot >= P.n_large) return;
@@ -468,7 +503,7 @@ __global__ void find_kernel(DevPlan P, int mode) {
   uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
   const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
   if (mode == 0) {
-    const uint32_t tot = layer_candidates(P, c0, c1, lane);
+    const uint32_t tot = layer_candidates(P, slot);
     if (tot >= k) {
       uint32_t bin, above;
       warp_find_bin(hrow, kH0, k, &bin, &above);
@@ -498,7 +533,7 @@ __global__ void find_kernel(DevPlan P, int mode) {
     }
   } else if (mode == 1) {
     if (S.refill != 1) return;
-    const uint32_t tot = layer_candidates(P, c0, c1, lane);
+    const uint32_t tot = layer_candidates(P, slot);
     if (tot >= k) {
       uint32_t bin, above;
       warp_find_bin(hrow, kH0, k, &bin, &above);
@@ -652,6 +687,7 @@ __global__ void __launch_bounds__(1024) layer_scan_kernel(DevPlan P) {
     }
   }
   if (threadIdx.x == 0) {
+    P.layer_total[slot] = 0;   // zero for the next call's chunk_prep
     P.sel_T[slot] = T;
     // speculative band for the next call: the drift-led threshold (may exceed T)
     // and the safe one (never above this call's T) that a level-1 refill falls back to
@@ -756,11 +792,20 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
       if (e != cudaSuccess) return e;
       attr_set[ef] = true;
     }
-    prof_begin(c, "small_layer", s, &h);
-    if (ef) small_layer_kernel<true><<<P.n_small, kSmallThreads, smem, s>>>(P, grad, residual, send, (uint64_t)c->K);
-    else small_layer_kernel<false><<<P.n_small, kSmallThreads, smem, s>>>(P, grad, residual, send, (uint64_t)c->K);
-    prof_end(c, h, s);
+    // the small layers touch disjoint elements and send entries from the large-layer path, so
+    // they run on a forked stream, concurrently with the scan, and join before the call returns
+    const bool fork = P.n_large && c->aux;
+    cudaStream_t ss = fork ? c->aux : s;
+    if (fork) {
+      if ((e = cudaEventRecord(c->ev_fork, s)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(c->aux, c->ev_fork, 0)) != cudaSuccess) return e;
+    }
+    prof_begin(c, "small_layer", ss, &h);
+    if (ef) small_layer_kernel<true><<<P.n_small, kSmallThreads, smem, ss>>>(P, grad, residual, send, (uint64_t)c->K);
+    else small_layer_kernel<false><<<P.n_small, kSmallThreads, smem, ss>>>(P, grad, residual, send, (uint64_t)c->K);
+    prof_end(c, h, ss);
     c->launches += 1;
+    if (fork && (e = cudaEventRecord(c->ev_join, c->aux)) != cudaSuccess) return e;
   }
   if (!P.n_large) return cudaGetLastError();
   e = cudaMemsetAsync(P.hist, 0, compress_hist_bytes(P.n_large), s);
@@ -798,6 +843,7 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   prof_begin(c, "emit", s, &h);
   emit_kernel<<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K);
   prof_end(c, h, s);
+  if (P.n_small && c->aux && (e = cudaStreamWaitEvent(s, c->ev_join, 0)) != cudaSuccess) return e;   // join
   c->lazy_residual = ef ? residual : nullptr;   // this call's large-layer selection is now pending
   c->launches += 17;
   return cudaGetLastError();

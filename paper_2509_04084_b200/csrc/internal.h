@@ -140,6 +140,8 @@ struct lowdiff_ctx {
   std::vector<void*> dev_allocs;
   // streams / events
   cudaStream_t side = nullptr;       // D2H copies
+  cudaStream_t aux = nullptr;        // small-layer compress, forked from the caller's stream
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_tmp = nullptr;
   cudaEvent_t ev_side_all = nullptr; // lowdiff_wait_persist
   cudaEvent_t last_d2h = nullptr;    // unused (kept for ABI-stable layout of the struct)
