@@ -58,6 +58,14 @@ def lib():
                                                  C.c_uint32, P, P, P, P, P, C.c_uint64]
         L.lowdiff_ref_recover.argtypes = [C.c_char_p, C.c_uint32, C.c_int, P, C.c_uint32, C.c_int64,
                                           P, P, P, P]
+        L.lowdiff_ref_union_compact.argtypes = [C.c_int, C.c_uint64, C.c_uint64, P, C.c_int, C.c_uint64,
+                                                C.c_uint64, P, P, C.c_uint64, P]
+        L.lowdiff_ref_union_bytes.restype = C.c_int64
+        L.lowdiff_ref_union_bytes.argtypes = [C.c_int, C.c_int, P]
+        L.lowdiff_ref_union_serialize.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int, P,
+                                                  C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P, C.c_uint64]
+        L.lowdiff_ref_recover_union.argtypes = [C.c_char_p, C.c_uint32, C.c_int, P, C.c_uint32, C.c_int64,
+                                                P, P, P, P]
         L.lowdiff_ref_wasted_time.restype = C.c_double
         L.lowdiff_ref_wasted_time.argtypes = [C.c_double] * 9
         L.lowdiff_ref_optimal_config.restype = None
@@ -204,6 +212,60 @@ def recover(directory, world, sizes, ppm, target=-1, with_moments=True):
     rec = np.zeros(1, np.int64)
     _check("recover", lib().lowdiff_ref_recover(str(directory).encode(), world, len(sizes), _p(numel), ppm,
                                                 target, _p(p), _p(m), _p(v), _p(rec)))
+    return p, m, v, int(rec[0])
+
+
+def union_compact(gathered, world, K, psi, lo=0, hi=None, mean=True):
+    """Union-compacted differential C^U_t of [lo, hi): (idx u32[U], val u32[U]) -- see lowdiff_ref.cpp."""
+    hi = psi if hi is None else hi
+    ga = _c(gathered, np.uint32)
+    assert ga.size == world * 2 * K
+    cap = min(world * K, hi - lo)
+    idx = np.zeros(max(cap, 1), np.uint32)
+    val = np.zeros(max(cap, 1), np.uint32)
+    cnt = np.zeros(1, np.uint64)
+    _check("union_compact", lib().lowdiff_ref_union_compact(world, K, psi, _p(ga), int(bool(mean)), lo, hi,
+                                                            _p(idx), _p(val), cap, _p(cnt)))
+    n = int(cnt[0])
+    return idx[:n].copy(), val[:n].copy()
+
+
+def union_bytes(n_layers, counts):
+    c = _c(counts, np.uint64)
+    return int(lib().lowdiff_ref_union_bytes(n_layers, c.size, _p(c)))
+
+
+def union_serialize(rank, world, first_iter, sizes, ppm, optim, flags, consts, scalars, unions) -> bytes:
+    """unions: list of (idx, val) per iteration (this rank's shard)."""
+    numel = _c(sizes, np.int64)
+    sc = _c(scalars, np.float32).reshape(-1, 3)
+    n = sc.shape[0]
+    assert len(unions) == n
+    counts = np.array([len(u[0]) for u in unions], np.uint64)
+    ent = np.concatenate([np.concatenate([_c(i, np.uint32), _c(v, np.uint32)]) for i, v in unions]
+                         + [np.zeros(0, np.uint32)])
+    cap = union_bytes(len(sizes), counts)
+    out = np.zeros(cap, np.uint8)
+    _check("union_serialize", lib().lowdiff_ref_union_serialize(
+        rank, world, first_iter, n, len(sizes), _p(numel), ppm, optim, flags, _p(_c(consts, np.float32)),
+        _p(sc), _p(counts), _p(ent if ent.size else np.zeros(1, np.uint32)), _p(out), cap))
+    return out.tobytes()
+
+
+def union_name(rank, first):
+    return f"ld_union_r{rank:03d}_{first:012d}.ldu"
+
+
+def recover_union(directory, world, sizes, ppm, target=-1, with_moments=True):
+    """Recovery from .ldf + .ldu files: (p, m, v, recovered_iteration)."""
+    numel = _c(sizes, np.int64)
+    psi = int(numel.sum())
+    p = np.zeros(psi, np.float32)
+    m = np.zeros(psi, np.float32) if with_moments else None
+    v = np.zeros(psi, np.float32) if with_moments else None
+    rec = np.zeros(1, np.int64)
+    _check("recover_union", lib().lowdiff_ref_recover_union(str(directory).encode(), world, len(sizes), _p(numel),
+                                                            ppm, target, _p(p), _p(m), _p(v), _p(rec)))
     return p, m, v, int(rec[0])
 
 

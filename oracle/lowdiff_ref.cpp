@@ -13,6 +13,9 @@
 //   optimizer  -- Eq. 1 M_{t+1} = M_t + Adam(G_t), Adam
 //                 moments; SGD (north_star; not in the paper)
 //   recover    -- Alg. 1 recovery process, Eq. 2
+//   union      -- union-compacted differential C^U_t: the synchronised G~_t
+//                 (Alg. 1 lines 5-6) kept as a dictionary
+//                 (PAPER.md:452), its .ldu file and recovery from it (R-29)
 //
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
 // load this library.  It shares no code, header, table or constant generator
@@ -447,6 +450,213 @@ int lowdiff_ref_recover(const char* dir, uint32_t world, int n_layers, const int
     if (st) return st;
     if (optim == 1) st = lowdiff_ref_adam_step(psi, G.data(), consts, scal, p, m, v);
     else st = lowdiff_ref_sgd_step(psi, G.data(), scal[0], p);
+    if (st) return st;
+  }
+  *recovered = last;
+  return OK;
+}
+
+// --------------------------------------------------------------------------
+// Union-compacted differential C^U_t (R-29).  After
+// Sync (Alg. 1 line 5) the checkpointing process receives the
+// synchronised compressed gradient G~_t (Q.put, line 6) and may
+// keep it as a dictionary ("dictionary accumulation"):
+//   U_t = { j : j is an index of some rank's block of iteration t }
+//   C^U_t = [(j, G_t[j]) for j in U_t, ascending],  G_t = Comp^-1(G~_t)
+// written here exactly in that order: (1) the dense G_t of the exchange above,
+// (2) a membership flag per index from every rank's index list, (3) the
+// members inside [lo, hi) in ascending order with their G_t value.  Rank r
+// stores the members in its parameter shard [floor(r Psi/N), floor((r+1) Psi/N)).
+// --------------------------------------------------------------------------
+int lowdiff_ref_union_compact(int world, uint64_t K, uint64_t psi, const uint32_t* gathered, int mean,
+                              uint64_t lo, uint64_t hi, uint32_t* out_idx, uint32_t* out_val, uint64_t cap,
+                              uint64_t* count) {
+  if (!fp_env_ok()) return E_FPENV;
+  if (world < 1 || !gathered || !count || lo > hi || hi > psi) return E_INVALID;
+  std::vector<float> G(psi);
+  int st = lowdiff_ref_exchange(world, K, psi, gathered, mean, G.data());   // (1)
+  if (st) return st;
+  std::vector<char> member(psi, 0);                                         // (2)
+  for (int r = 0; r < world; ++r)
+    for (uint64_t e = 0; e < K; ++e) member[gathered[(uint64_t)r * 2 * K + e]] = 1;
+  uint64_t n = 0;                                                           // (3)
+  for (uint64_t j = lo; j < hi; ++j) {
+    if (!member[j]) continue;
+    if (n < cap) {
+      out_idx[n] = (uint32_t)j;
+      out_val[n] = float_bits(G[j]);
+    }
+    ++n;
+  }
+  *count = n;
+  return n <= cap ? OK : E_DIM;
+}
+
+// .ldu file: b consecutive union-compacted differentials of rank r's shard
+//   header 80 B: "LDU1" | u16 version=1 | u16 flags (bit0 EF, bit1 mean) | u32 rank |
+//     u32 world | u64 first_iter (16) | u32 n_iters | u32 n_layers | u64 Psi (32) | u64 K |
+//     u32 ppm (48) | u32 optim | u64 shard_begin (56) | u64 shard_end (64) | u64 0 (72)
+//   hyper 32 B | layer table L x {u64 numel, u32 k, u32 0} |
+//   n_iters x ({u64 iteration, f32 lr, f32 bc1_inv, f32 bc2_inv, u32 count, u64 0} +
+//              idx u32[count] + val u32[count]) | u32 CRC-32C of all preceding bytes
+int64_t lowdiff_ref_union_bytes(int n_layers, int n_iters, const uint64_t* counts) {
+  int64_t b = 80 + 32 + 16 * (int64_t)n_layers + 4;
+  for (int i = 0; i < n_iters; ++i) b += 32 + 8 * (int64_t)counts[i];
+  return b;
+}
+
+int lowdiff_ref_union_serialize(uint32_t rank, uint32_t world, uint64_t first_iter, uint32_t n_iters,
+                                int n_layers, const int64_t* numel, uint32_t ppm, uint32_t optim,
+                                uint32_t flags, const float* consts5, const float* scalars /* n x 3 */,
+                                const uint64_t* counts /* n */, const uint32_t* entries /* per iteration:
+                                idx[count] then val[count], concatenated */, uint8_t* out, uint64_t cap) {
+  uint64_t psi = 0, K = 0;
+  for (int l = 0; l < n_layers; ++l) { psi += (uint64_t)numel[l]; K += k_of((uint64_t)numel[l], ppm); }
+  std::vector<uint8_t> b;
+  b.push_back('L'); b.push_back('D'); b.push_back('U'); b.push_back('1');
+  put_u16(b, 1); put_u16(b, (uint16_t)flags);
+  put_u32(b, rank); put_u32(b, world);
+  put_u64(b, first_iter);
+  put_u32(b, n_iters); put_u32(b, (uint32_t)n_layers);
+  put_u64(b, psi); put_u64(b, K);
+  put_u32(b, ppm); put_u32(b, optim);
+  put_u64(b, psi * rank / world);
+  put_u64(b, psi * (rank + 1) / world);
+  put_u64(b, 0);
+  for (int i = 0; i < 5; ++i) put_f32(b, consts5[i]);
+  for (int i = 0; i < 3; ++i) put_u32(b, 0);
+  for (int l = 0; l < n_layers; ++l) {
+    put_u64(b, (uint64_t)numel[l]);
+    put_u32(b, (uint32_t)k_of((uint64_t)numel[l], ppm));
+    put_u32(b, 0);
+  }
+  const uint32_t* q = entries;
+  for (uint32_t it = 0; it < n_iters; ++it) {
+    put_u64(b, first_iter + it);
+    for (int i = 0; i < 3; ++i) put_f32(b, scalars[3 * it + i]);
+    put_u32(b, (uint32_t)counts[it]);
+    put_u64(b, 0);
+    for (uint64_t e = 0; e < 2 * counts[it]; ++e) put_u32(b, q[e]);
+    q += 2 * counts[it];
+  }
+  put_u32(b, crc32c_bitwise(b.data(), b.size()));
+  if (b.size() > cap) return E_INVALID;
+  std::memcpy(out, b.data(), b.size());
+  return OK;
+}
+
+// Recovery from union-compacted differentials (Alg. 1 recovery, with C^U_t in
+// place of the gathered blocks): the same chain rules as lowdiff_ref_recover (.ldf shards of the
+// latest complete full F <= target; for t = F+1..target every rank's .ldu must hold iteration t,
+// later files winning), then per iteration G_t[j] = the stored value for every stored j (the ranks'
+// shards are disjoint), +0.0f elsewhere, and the optimizer step with the block's scalars.
+int lowdiff_ref_recover_union(const char* dir, uint32_t world, int n_layers, const int64_t* numel,
+                              uint32_t ppm, int64_t target, float* p, float* m, float* v,
+                              int64_t* recovered) {
+  if (!fp_env_ok()) return E_FPENV;
+  uint64_t psi = 0, K = 0;
+  for (int l = 0; l < n_layers; ++l) { psi += (uint64_t)numel[l]; K += k_of((uint64_t)numel[l], ppm); }
+  std::map<int64_t, std::map<uint32_t, std::string>> fulls;
+  std::vector<std::map<int64_t, std::string>> diffs(world);
+  DIR* d = opendir(dir);
+  if (!d) return E_IO;
+  while (struct dirent* de = readdir(d)) {
+    std::string name = de->d_name;
+    unsigned r = 0; unsigned long long it = 0; char tail[16] = {0};
+    if (name.size() == 29 && std::sscanf(name.c_str(), "ld_full_r%3u_%12llu.%3s", &r, &it, tail) == 3 &&
+        std::string(tail) == "ldf" && r < world)
+      fulls[(int64_t)it][r] = std::string(dir) + "/" + name;
+    if (name.size() == 30 && std::sscanf(name.c_str(), "ld_union_r%3u_%12llu.%3s", &r, &it, tail) == 3 &&
+        std::string(tail) == "ldu" && r < world)
+      diffs[r][(int64_t)it] = std::string(dir) + "/" + name;
+  }
+  closedir(d);
+  int64_t F = -1;
+  for (auto it = fulls.rbegin(); it != fulls.rend(); ++it) {
+    if (target >= 0 && it->first > target) continue;
+    if (it->second.size() == world) { F = it->first; break; }
+  }
+  if (F < 0) return E_GAP;
+  uint32_t optim = 0;
+  for (uint32_t r = 0; r < world; ++r) {
+    std::vector<uint8_t> buf;
+    if (!read_file(fulls[F][r], buf)) return E_IO;
+    const uint64_t sb = psi * r / world, se = psi * (r + 1) / world, S = se - sb;
+    if (buf.size() != 64 + 32 + 12 * S + 4) return E_CORRUPT;
+    if (std::memcmp(buf.data(), "LDF1", 4) != 0) return E_CORRUPT;
+    if (crc32c_bitwise(buf.data(), buf.size() - 4) != get_u32(buf.data() + buf.size() - 4)) return E_CORRUPT;
+    if (get_u32(buf.data() + 8) != r || get_u32(buf.data() + 12) != world ||
+        (int64_t)get_u64(buf.data() + 16) != F || get_u64(buf.data() + 24) != psi ||
+        get_u64(buf.data() + 32) != sb || get_u64(buf.data() + 40) != se)
+      return E_CORRUPT;
+    optim = get_u32(buf.data() + 48);
+    const uint8_t* q = buf.data() + 96;
+    for (uint64_t j = 0; j < S; ++j) p[sb + j] = get_f32(q + 4 * j);
+    for (uint64_t j = 0; j < S; ++j) if (m) m[sb + j] = get_f32(q + 4 * (S + j));
+    for (uint64_t j = 0; j < S; ++j) if (v) v[sb + j] = get_f32(q + 4 * (2 * S + j));
+  }
+  // which file (and byte offset) holds iteration t of rank r; every used file is verified
+  std::vector<std::map<int64_t, std::pair<std::string, uint64_t>>> where(world);
+  std::map<std::string, std::vector<uint8_t>> loaded;
+  for (uint32_t r = 0; r < world; ++r) {
+    for (auto& fe : diffs[r]) {   // ascending first_iter: later files override earlier ones
+      std::vector<uint8_t> buf;
+      if (!read_file(fe.second, buf) || buf.size() < 116) return E_CORRUPT;
+      if (std::memcmp(buf.data(), "LDU1", 4) != 0) return E_CORRUPT;
+      if (crc32c_bitwise(buf.data(), buf.size() - 4) != get_u32(buf.data() + buf.size() - 4)) return E_CORRUPT;
+      if (get_u32(buf.data() + 8) != r || get_u32(buf.data() + 12) != world ||
+          get_u32(buf.data() + 28) != (uint32_t)n_layers || get_u64(buf.data() + 32) != psi ||
+          get_u64(buf.data() + 40) != K || get_u32(buf.data() + 48) != ppm || get_u32(buf.data() + 52) != optim ||
+          get_u64(buf.data() + 56) != psi * r / world || get_u64(buf.data() + 64) != psi * (r + 1) / world)
+        return E_CORRUPT;
+      const uint32_t n_iters = get_u32(buf.data() + 24);
+      uint64_t off = 112 + 16 * (uint64_t)n_layers;
+      for (uint32_t i = 0; i < n_iters; ++i) {
+        if (off + 32 > buf.size() - 4) return E_CORRUPT;
+        const uint64_t cnt = get_u32(buf.data() + off + 20);
+        if ((int64_t)get_u64(buf.data() + off) != fe.first + i) return E_CORRUPT;
+        where[r][fe.first + i] = {fe.second, off};
+        off += 32 + 8 * cnt;
+      }
+      if (off != buf.size() - 4) return E_CORRUPT;
+      loaded[fe.second] = std::move(buf);
+    }
+  }
+  int64_t last = F;
+  while (true) {
+    const int64_t t = last + 1;
+    if (target >= 0 && t > target) break;
+    bool all = true;
+    for (uint32_t r = 0; r < world; ++r) all = all && where[r].count(t);
+    if (!all) break;
+    last = t;
+  }
+  if (target >= 0 && last < target) return E_GAP;
+  std::vector<float> G(psi);
+  for (int64_t t = F + 1; t <= last; ++t) {
+    float scal[3] = {0, 0, 0};
+    float consts[5] = {0, 0, 0, 0, 0};
+    std::fill(G.begin(), G.end(), 0.0f);
+    for (uint32_t r = 0; r < world; ++r) {
+      const std::vector<uint8_t>& buf = loaded[where[r][t].first];
+      const uint8_t* blk = buf.data() + where[r][t].second;
+      float s3[3] = {get_f32(blk + 8), get_f32(blk + 12), get_f32(blk + 16)};
+      if (r == 0) {
+        std::memcpy(scal, s3, sizeof scal);
+        for (int i = 0; i < 5; ++i) consts[i] = get_f32(buf.data() + 80 + 4 * i);
+      } else if (std::memcmp(scal, s3, sizeof scal) != 0) {
+        return E_CORRUPT;
+      }
+      const uint64_t cnt = get_u32(blk + 20);
+      const uint64_t sb = psi * r / world, se = psi * (r + 1) / world;
+      for (uint64_t e = 0; e < cnt; ++e) {
+        const uint32_t j = get_u32(blk + 32 + 4 * e);
+        if (j < sb || j >= se) return E_CORRUPT;
+        G[j] = get_f32(blk + 32 + 4 * (cnt + e));
+      }
+    }
+    int st = optim == 1 ? lowdiff_ref_adam_step(psi, G.data(), consts, scal, p, m, v)
+                        : lowdiff_ref_sgd_step(psi, G.data(), scal[0], p);
     if (st) return st;
   }
   *recovered = last;
