@@ -498,6 +498,46 @@ def run_ours(args):
         rctx.close()
         del rp, rm, rv
 
+    # union-compacted differentials (NEXT-4): the union of 8 ranks' blocks (8 simulated ranks with
+    # rank-correlated gradients, D4 with alpha = 0.5) compacted over rank 0's shard and over all of Psi
+    union = None
+    if not args.no_union and rank == 0:
+        NU = 8
+        uctx = ld.Context(sizes, density_ppm=args.ppm, world=NU, rank=0, device=local)
+        g8 = torch.empty(NU * 2 * K, dtype=torch.int32, device=dev)
+        rz = torch.zeros(psi, device=dev)
+        for q in range(NU):
+            gq = gradient(sizes, q, 0, dist="D4", alpha=0.5, model=args.workload, device=dev)
+            rz.zero_()
+            uctx.compress(gq, rz, g8[q * 2 * K:(q + 1) * 2 * K])
+            del gq
+        del rz
+        res_u = {}
+        for name, (lo, hi) in (("shard0", (0, psi // NU)), ("all", (0, psi))):
+            cap = min(NU * K, hi - lo)
+            out = torch.empty(2 * cap, dtype=torch.int32, device=dev)
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            uctx.union_compact(NU, g8, lo, hi, out, cap, cnt)
+            torch.cuda.synchronize()
+            u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            u0.record()
+            for _ in range(5):
+                uctx.union_compact(NU, g8, lo, hi, out, cap, cnt)
+            u1.record()
+            torch.cuda.synchronize()
+            ums = u0.elapsed_time(u1) / 5
+            n_u = int(cnt.item())
+            share = NU * K * (hi - lo) / psi          # gathered entries falling in the range (expected)
+            alg = 2 * 8 * share + 8 * n_u             # entries read twice (count, emit) + union written
+            res_u[name] = {"range": [lo, hi], "entries": n_u, "ms": ums,
+                           "bytes_union": 8 * n_u, "bytes_gathered_share": int(8 * share),
+                           "ratio_to_gathered": n_u / share, "algorithmic_gbs": alg / (ums / 1e3) / 1e9}
+            del out, cnt
+        uctx.close()
+        del g8
+        union = {"ranks": NU, "inputs": "D4, alpha = 0.5 rank correlation, one iteration per rank", **res_u,
+                 "note": "union = indices of any rank's block with the merged value (R-29); persisted per shard"}
+
     # M3: LowDiff+ layer-wise dense snapshot.  A proxy backward pass (not our
     # code: torch copies, HBM-bound, duration proportional to each bucket's size) finalises the
     # gradient bucket by bucket in backward order; after each bucket lowdiff_snapshot_layer queues
@@ -578,7 +618,7 @@ def run_ours(args):
                                   "file writing measured separately (writer)"},
             "roofline": roofline, "gate_bj5": gate, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "recovery": recovery, "writer": writer, "full_ckpt": fullck, "update": update,
-            "replica": replica, "snapshot": snapshot,
+            "replica": replica, "snapshot": snapshot, "union": union,
             "spec": {"hits": st["spec_hits"], "misses": st["spec_misses"]}}
     print(json.dumps(line), flush=True)
 
@@ -601,6 +641,7 @@ def main():
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-update", action="store_true")
     ap.add_argument("--no-snapshot", action="store_true")
+    ap.add_argument("--no-union", action="store_true")
     ap.add_argument("--snapshot-reps", type=int, default=20,
                     help="proxy backward: HBM passes over each bucket (20 ~ 38 ms for GPT-2 XL, about the backward "
                          "of 8K tokens at ~1.2 PFLOP/s)")

@@ -236,6 +236,45 @@ lowdiff_status lowdiff_replay_range(lowdiff_ctx *ctx, int32_t optim, int32_t wor
 lowdiff_status lowdiff_recover_sharded(lowdiff_ctx *ctx, int64_t target, float *p, float *m, float *v,
                                        int32_t gather, int64_t *recovered, void *stream);
 
+/* ---- Union-compacted differentials (R-29) ----
+ * C^U_t = the synchronised compressed gradient G~_t of Alg. 1 line 5, put in the
+ * reusing queue after Sync (line 6), kept as an index -> value dictionary
+ * ("dictionary accumulation"): every index j that appears in some rank's block of the
+ * iteration, ascending, with the merged value G_t[j] exactly as lowdiff_exchange writes it (rank-
+ * order sum from +0, then / N when the context's mean flag is set).  Smaller than the N fixed-K
+ * blocks whenever the ranks' supports overlap; replays to the same state bit for bit.
+ *
+ * union_compact: the members in [begin, end) of the union of the `world` blocks in `gathered`
+ *    (device u32[world * 2K], rank r's block at r * 2K, each index-ascending) ->
+ *    out = idx u32[cap] | val u32[cap] (device, entries [0, *count_dev) valid, ascending),
+ *    *count_dev = device u64.  cap must be >= min(world * K, end - begin) (the worst case; else
+ *    E_INVALID), so the result always fits.  Enqueued on `stream`, no host synchronisation.
+ *    E_DIM if [begin, end) is not inside [0, Psi). */
+lowdiff_status lowdiff_union_compact(lowdiff_ctx *ctx, int32_t world, const uint32_t *gathered, int64_t begin,
+                                     int64_t end, uint32_t *out, int64_t cap, uint64_t *count_dev, void *stream);
+/* union_persist: compact this rank's shard [floor(rank*Psi/world), floor((rank+1)*Psi/world)) of
+ *    the gathered blocks of `iteration` (as union_compact with world = the context's) into a
+ *    library-owned device buffer on `producer`, then a writer thread copies exactly the union out
+ *    (a count read first) and writes batches of batch_size iterations as
+ *    <ckpt_dir>/ld_union_r{rank:03}_{first:012}.ldu (layout: DESIGN.md §3; *.tmp then rename;
+ *    no files without a ckpt_dir).  `gathered` may be reused once `producer` has passed this call.
+ *    Two buffers alternate: the call blocks on the host only while the buffer of iteration - 2 is
+ *    still being copied out.  `iteration` must be the previous call's + 1 (else E_STATE).  A non-
+ *    finite accumulated gradient before the iteration stops the chain (E_NUMERIC deferred to the
+ *    next call / lowdiff_sync).  lowdiff_sync flushes the final partial batch. */
+lowdiff_status lowdiff_union_persist(lowdiff_ctx *ctx, int64_t iteration, const lowdiff_step_scalars *scalars,
+                                     const uint32_t *gathered, void *producer);
+/* recover_union: Alg. 1 recovery from full checkpoints and .ldu files with the
+ *    chain rules of lowdiff_recover (latest complete Full F <= target; every needed rank's .ldu
+ *    must hold each of F+1..target, later files winning; E_GAP / E_CORRUPT / E_IO as there).
+ *    sharded = 0: every shard and every rank's union files, all of p, m, v (f32[Psi]) restored;
+ *    sharded = 1: only this rank's .ldf shard and .ldu files, only its element range of p, m, v
+ *    written (the arrays are still indexed by global element).  The replay is the fused kernel
+ *    of lowdiff_replay; the result is bitwise the state lowdiff_recover reaches from the .ldb
+ *    chain of the same run.  Synchronous on `stream`. */
+lowdiff_status lowdiff_recover_union(lowdiff_ctx *ctx, int64_t target, float *p, float *m, float *v, int32_t sharded,
+                                     int64_t *recovered, void *stream);
+
 /* LowDiff+ layer-wise snapshot (Sec. 5.1; Alg. 2 l.19):
  *    after the caller's gradient sync of layers [first_layer, first_layer+n_layers)
  *    (contiguous in the flat gradient; grad_bucket points at layer first_layer), copy
@@ -318,6 +357,9 @@ typedef struct {
   int64_t spec_candidates;          /* candidates the band admitted in those hit layers (last call) */
   int64_t replica_busy_ns;          /* replica worker time spent in the host optimizer            */
   int64_t replica_stall_ns;         /* host time lowdiff_snapshot_layer waited for the replica    */
+  int64_t union_files_written;      /* .ldu files written (lowdiff_union_persist)                 */
+  int64_t union_bytes_written;
+  int64_t union_entries;            /* union entries persisted (sum over iterations)              */
 } lowdiff_stats;
 lowdiff_status lowdiff_get_stats(const lowdiff_ctx *ctx, lowdiff_stats *out);
 

@@ -100,6 +100,7 @@ struct Slot {
 // work item of the LowDiff+ replica worker: 0 = initial copy landed, 1 = apply the snapshotted
 // gradient of `iteration`, 2 = persist the replica as it stands after the preceding items
 struct RepJob { int kind; int64_t iteration; lowdiff_step_scalars sc; };
+struct UJob { int64_t iteration; lowdiff_step_scalars sc; int buf; };
 
 // peer-memory exchange (peer.cu): flag words per rank = ready[n_slots] | done[n_slots][kPeerMaxWorld]
 // | error counter
@@ -222,6 +223,27 @@ struct lowdiff_ctx {
   size_t replay_scratch_bytes = 0;
   void* merge_scratch = nullptr;
   size_t merge_scratch_bytes = 0;
+  void* union_scratch = nullptr;
+  size_t union_scratch_bytes = 0;
+  // union-compacted persistence (NEXT-4): two library-owned device buffers idx | val of u_cap
+  // entries each (this rank's shard), their counts, a writer thread that copies exactly the
+  // count out and writes .ldu batches
+  uint32_t* u_buf[2] = {nullptr, nullptr};
+  unsigned long long* u_cnt_dev = nullptr;      // [2]
+  unsigned long long* u_cnt_host = nullptr;     // pinned [2]
+  cudaEvent_t u_ready[2] = {nullptr, nullptr};
+  bool u_inuse[2] = {false, false};
+  uint64_t u_cap = 0;
+  int64_t u_next_iter = -1;
+  uint32_t u_err_seen = 0;
+  std::deque<ld::UJob> u_q;
+  std::mutex u_mu;
+  std::condition_variable u_cv, u_cv_free, u_cv_idle;
+  bool u_stop = false, u_flush = false;
+  int u_busy = 0;
+  std::thread u_writer;
+  cudaStream_t u_stream = nullptr;
+  std::atomic<int64_t> u_files{0}, u_bytes{0}, u_entries{0};
 };
 
 namespace ld {
@@ -233,9 +255,18 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
                          cudaStream_t s);
 // replays elements [lo, hi); p, m, v point at element lo.  ranges: NULL (every entry of every block
 // is valid) or device u32[2 * n_steps * world] = the valid entry range of each block.
+// k_stride: blocks are u32[2 * k_stride] (idx | val); 0 = the context's K (fixed-K blocks)
 cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* consts5, int world,
                           int64_t n_steps, const uint32_t* diffs, const float* scal_dev, uint64_t lo,
-                          uint64_t hi, const uint32_t* ranges, float* p, float* m, float* v, cudaStream_t s);
+                          uint64_t hi, const uint32_t* ranges, float* p, float* m, float* v, cudaStream_t s,
+                          uint64_t k_stride = 0);
+// start[b * (T1 - T0 + 1) + t - T0] = first entry of block b (stride 2K, indices ascending) in tile t
+cudaError_t launch_tile_window(const uint32_t* blocks, int n_blocks, uint64_t K, int shift, uint32_t T0, uint32_t T1,
+                               uint32_t* start, cudaStream_t s);
+// union.cu: union-compacted differential of [lo, hi): out = idx u32[cap] | val u32[cap]
+cudaError_t launch_union(lowdiff_ctx* c, int world, bool mean, const uint32_t* gathered, uint64_t lo, uint64_t hi,
+                         uint32_t* out, uint64_t cap, unsigned long long* count_dev, cudaStream_t s);
+size_t union_scratch_bytes(int world, uint64_t lo, uint64_t hi);
 cudaError_t launch_update(lowdiff_ctx* c, int world, const uint32_t* gathered, const lowdiff_step_scalars& sc,
                           float* p, float* m, float* v, cudaStream_t s);
 cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches, uint64_t* first);

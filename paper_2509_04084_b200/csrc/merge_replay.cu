@@ -390,6 +390,14 @@ cudaError_t launch_tile_start(const uint32_t* block, uint64_t K, int64_t psi, ui
   return cudaGetLastError();
 }
 
+cudaError_t launch_tile_window(const uint32_t* blocks, int n_blocks, uint64_t K, int shift, uint32_t T0, uint32_t T1,
+                               uint32_t* start, cudaStream_t s) {
+  const unsigned gx = (unsigned)std::min<uint64_t>((K + 256) / 256, (uint64_t)num_sms2() * 16);
+  tile_start_kernel<<<dim3(gx, (unsigned)n_blocks), 256, 0, s>>>(blocks, n_blocks, 2 * K, (uint32_t)K, shift, T0, T1,
+                                                                  nullptr, start);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, float* dense, cudaStream_t s) {
   const int64_t psi = c->psi;
   const uint64_t K = (uint64_t)c->K;
@@ -473,9 +481,9 @@ cudaError_t launch_update(lowdiff_ctx* c, int world, const uint32_t* gathered, c
 
 cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* consts5, int world, int64_t n_steps,
                           const uint32_t* diffs, const float* scal_dev, uint64_t lo, uint64_t hi,
-                          const uint32_t* ranges, float* p, float* m, float* v, cudaStream_t s) {
+                          const uint32_t* ranges, float* p, float* m, float* v, cudaStream_t s, uint64_t k_stride) {
   if (lo >= hi) return cudaSuccess;
-  const uint64_t K = (uint64_t)c->K;
+  const uint64_t K = k_stride ? k_stride : (uint64_t)c->K;
   // the window of tiles that hold [lo, hi): tile0 .. tile0 + n_tiles - 1 (start table: n_tiles + 1)
   const int64_t tile0 = (int64_t)(lo >> kReplayTileShift);
   const int64_t n_tiles = (int64_t)((hi - 1) >> kReplayTileShift) - tile0 + 1;

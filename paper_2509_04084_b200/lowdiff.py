@@ -59,7 +59,8 @@ class SimReport(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("files_written", C.c_int64), ("bytes_written", C.c_int64), ("ring_stall_ns", C.c_int64),
                 ("writer_busy_ns", C.c_int64), ("spec_hits", C.c_int64), ("spec_misses", C.c_int64),
-                ("spec_candidates", C.c_int64), ("replica_busy_ns", C.c_int64), ("replica_stall_ns", C.c_int64)]
+                ("spec_candidates", C.c_int64), ("replica_busy_ns", C.c_int64), ("replica_stall_ns", C.c_int64),
+                ("union_files_written", C.c_int64), ("union_bytes_written", C.c_int64), ("union_entries", C.c_int64)]
 
 
 _lib = None
@@ -96,6 +97,9 @@ def lib():
             "snapshot_layer": ([P, C.c_int64, C.c_int32, C.c_int32, P, P], S),
             "snapshot_wait": ([P, C.c_int64, C.POINTER(C.c_void_p)], S),
             "bucket_plan": ([C.c_int32, P, C.c_int64, P, P, C.c_int32, C.POINTER(C.c_int32)], S),
+            "union_compact": ([P, C.c_int32, P, C.c_int64, C.c_int64, P, C.c_int64, P, P], S),
+            "union_persist": ([P, C.c_int64, C.POINTER(StepScalars), P, P], S),
+            "recover_union": ([P, C.c_int64, P, P, P, C.c_int32, C.POINTER(C.c_int64), P], S),
             "replica_init": ([P, C.c_int64, P, P, P, C.c_int32, P], S),
             "replica_step": ([P, C.c_int64, C.POINTER(StepScalars)], S),
             "replica_persist": ([P], S),
@@ -135,7 +139,8 @@ def lib():
 
 EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_materialize", "exchange", "merge", "exchange_update", "peer_alloc", "ipc_open",
             "peer_set", "exchange_peer", "batch_persist",
-            "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "bucket_plan", "replica_init",
+            "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "bucket_plan", "union_compact", "union_persist", "recover_union",
+            "replica_init",
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
             "sync", "get_stats",
             "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
@@ -397,6 +402,21 @@ class Context:
         self._c("recover_sharded", lib().lowdiff_recover_sharded(self._h, target, _ptr(p), _ptr(m), _ptr(v),
                                                                  int(bool(gather)), C.byref(it), _stream(stream)))
         return it.value
+
+    def union_compact(self, world, gathered, begin, end, out, cap, count_dev, stream=None):
+        """C^U_t of [begin, end) into out = idx u32[cap] | val u32[cap]; count in count_dev (u64)."""
+        self._c("union_compact", lib().lowdiff_union_compact(self._h, world, _ptr(gathered), begin, end, _ptr(out),
+                                                             cap, _ptr(count_dev), _stream(stream)))
+
+    def union_persist(self, iteration, scalars: StepScalars, gathered, stream=None):
+        self._c("union_persist", lib().lowdiff_union_persist(self._h, iteration, C.byref(scalars), _ptr(gathered),
+                                                             _stream(stream)))
+
+    def recover_union(self, p, m=None, v=None, target=-1, sharded=False, stream=None) -> int:
+        rec = C.c_int64()
+        self._c("recover_union", lib().lowdiff_recover_union(self._h, target, _ptr(p), _ptr(m), _ptr(v),
+                                                             int(bool(sharded)), C.byref(rec), _stream(stream)))
+        return rec.value
 
     def snapshot_layer(self, iteration, first_layer, n_layers, grad_bucket, stream=None):
         self._c("snapshot_layer", lib().lowdiff_snapshot_layer(self._h, iteration, first_layer, n_layers,
