@@ -120,7 +120,7 @@ merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __r
     dense[__ldg(send + e)] = __fadd_rn(0.f, __uint_as_float(__ldg(send + K + e)));
 }
 
-struct AdamK { float b1, c1, b2, c2, eps; };
+struct AdamK { float b1, c1, b2, c2, eps, nz; };   // nz = -0.0f (ieee_fast.cuh: opaque -0 addend)
 
 // Fused n-step replay.  Thread owns elements j0 + 4*(tid + 256*i) + q, i in {0,1}, q in 0..3.
 // MAXW >= min(world, 8): ranks whose first-round entries are prefetched in registers.
@@ -157,7 +157,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       V2[2 * i + h] = pk2(ve[0], ve[1]);
     }
   }
-  const AdamK2 k2 = make_adamk2(ak.b1, ak.c1, ak.b2, ak.c2, ak.eps);
+  const AdamK2 k2 = make_adamk2(ak.b1, ak.c1, ak.b2, ak.c2, ak.eps, ak.nz);
   const float n = (float)world, inv = 1.0f / (float)world;
   const bool eps_ok = ak.eps >= 0x1p-60f && ak.eps <= 0x1p59f;   // adam_u_fast's precondition
   const uint64_t tstride = (uint64_t)(n_tiles + 1);   // n_tiles = tiles in the window
@@ -257,17 +257,17 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
         bool s0, s1;
         u[0] = adam2_u(M2[2 * i], V2[2 * i], g01, k2, R1, R2, &mh[0], &vh[0], &s0);
         u[1] = adam2_u(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2, &mh[1], &vh[1], &s1);
-        if (s0 || s1 || !eps_ok) {   // rare: redo the group exactly with the intrinsics
+        if (s0 | s1 | !eps_ok) {   // rare: redo the group exactly with the intrinsics
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             u[h] = pk2(__fdiv_rn(lo2(mh[h]), __fadd_rn(__fsqrt_rn(lo2(vh[h])), ak.eps)),
                        __fdiv_rn(hi2(mh[h]), __fadd_rn(__fsqrt_rn(hi2(vh[h])), ak.eps)));
         }
-        P2[2 * i] = sub_prod2(P2[2 * i], LR, u[0]);
-        P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, u[1]);
+        P2[2 * i] = sub_prod2(P2[2 * i], LR, u[0], k2.nz);
+        P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, u[1], k2.nz);
       } else {
-        P2[2 * i] = sub_prod2(P2[2 * i], LR, g01);
-        P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, g23);
+        P2[2 * i] = sub_prod2(P2[2 * i], LR, g01, k2.nz);
+        P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, g23, k2.nz);
       }
     }
     if (ranger) { s_a[cur][tid] = na; s_b[cur][tid] = nb; }   // ranges of step s+2
@@ -462,7 +462,7 @@ cudaError_t launch_update(lowdiff_ctx* c, int world, const uint32_t* gathered, c
                                                                  start);
   }
   const AdamK ak{c->cfg.adam.beta1, c->cfg.adam.one_minus_beta1, c->cfg.adam.beta2, c->cfg.adam.one_minus_beta2,
-                 c->cfg.adam.eps};
+                 c->cfg.adam.eps, -0.0f};
   const unsigned grid = (unsigned)n_tiles;
   const int dm = div_mode(c->cfg.mean != 0, world);
 #define LD_UPD(OPT, DIV) \
@@ -498,7 +498,7 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
   }
   uint32_t* start = static_cast<uint32_t*>(c->replay_scratch);
   const int sms = num_sms2();
-  AdamK ak{consts5[0], consts5[1], consts5[2], consts5[3], consts5[4]};
+  AdamK ak{consts5[0], consts5[1], consts5[2], consts5[3], consts5[4], -0.0f};
   int h;
   prof_begin(c, "replay_index", s, &h);
   {

@@ -103,7 +103,8 @@ __global__ void adam_check_kernel(uint64_t n, uint64_t seed, unsigned long long*
 
 // which = 3: the paired Adam step (adam2_u + the exact fallback, then p - lr*u) on random states vs
 // the scalar R-11 sequence written with the CUDA intrinsics
-__global__ void adam2_check_kernel(uint64_t n, uint64_t seed, unsigned long long* bad, unsigned long long* first) {
+__global__ void adam2_check_kernel(uint64_t n, uint64_t seed, float neg0, unsigned long long* bad,
+                                   unsigned long long* first) {
   const float eps_set[4] = {1e-8f, 1e-6f, 0x1p-60f, 1.0f};
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     float p[2], m[2], v[2], g[2];
@@ -127,14 +128,14 @@ __global__ void adam2_check_kernel(uint64_t n, uint64_t seed, unsigned long long
       v[e] = exp2f(-150.f + 160.f * (float)(h & 0xFFFFFF) / 16777216.f);
       if (((h >> 24) & 7) == 0) v[e] = 0.0f;
     }
-    const AdamK2 k2 = make_adamk2(b1, c1, b2, c2, eps);
+    const AdamK2 k2 = make_adamk2(b1, c1, b2, c2, eps, neg0);
     f32x2 P = pk2(p[0], p[1]), M = pk2(m[0], m[1]), V = pk2(v[0], v[1]), mh, vh;
     bool sl;
     f32x2 u = adam2_u(M, V, pk2(g[0], g[1]), k2, pk2(r1, r1), pk2(r2, r2), &mh, &vh, &sl);
     if (sl)
       u = pk2(__fdiv_rn(lo2(mh), __fadd_rn(__fsqrt_rn(lo2(vh)), eps)),
               __fdiv_rn(hi2(mh), __fadd_rn(__fsqrt_rn(hi2(vh)), eps)));
-    P = sub_prod2(P, pk2(lr, lr), u);
+    P = sub_prod2(P, pk2(lr, lr), u, k2.nz);
     const float got[6] = {lo2(P), hi2(P), lo2(M), hi2(M), lo2(V), hi2(V)};
     for (int e = 0; e < 2; ++e) {
       const float me = __fadd_rn(__fmul_rn(b1, m[e]), __fmul_rn(c1, g[e]));
@@ -165,7 +166,7 @@ cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatc
   if (which == 0) sqrt_check_kernel<<<148 * 16, 256>>>(d, d + 1);
   else if (which == 1) div_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
   else if (which == 2) adam_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
-  else adam2_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
+  else adam2_check_kernel<<<148 * 16, 256>>>(n, seed, -0.0f, d, d + 1);
   e = cudaDeviceSynchronize();
   unsigned long long h[2] = {0, 0};
   if (e == cudaSuccess) e = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
