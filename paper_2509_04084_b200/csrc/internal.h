@@ -31,7 +31,11 @@ constexpr int kMergeTileShift = 13;
 constexpr int kMergeTile = 1 << kMergeTileShift;     // merge tile (elements per CTA)
 constexpr int kReplayTileShift = 11;
 constexpr int kReplayTile = 1 << kReplayTileShift;   // replay tile (elements per CTA)
-constexpr int kReplayThreads = 256;
+#ifndef LD_REPLAY_THREADS
+#define LD_REPLAY_THREADS 128   // x 4 float4 slots = 16 elements per thread (measured best, B200)
+#endif
+constexpr int kReplayThreads = LD_REPLAY_THREADS;
+constexpr int kReplaySlots = kReplayTile / (4 * kReplayThreads);   // float4 slots per thread
 constexpr uint32_t kNoThreshold = 0xFFFFFFFFu;
 
 // per-large-layer selection state (device)

@@ -120,12 +120,19 @@ merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __r
     dense[__ldg(send + e)] = __fadd_rn(0.f, __uint_as_float(__ldg(send + K + e)));
 }
 
+#ifndef LD_REPLAY_MINB
+#define LD_REPLAY_MINB 8   // resident CTAs per SM the replay is compiled for (128 threads: 64 registers)
+#endif
+
 struct AdamK { float b1, c1, b2, c2, eps, nz; };   // nz = -0.0f (ieee_fast.cuh: opaque -0 addend)
 
-// Fused n-step replay.  Thread owns elements j0 + 4*(tid + 256*i) + q, i in {0,1}, q in 0..3.
+// Fused n-step replay.  Thread owns elements j0 + 4*(tid + kReplayThreads*i) + q, i < kReplaySlots,
+// q in 0..3 (128 threads x 4 slots: the per-step fixed work -- zeroing G, barriers, the entry
+// loops -- is amortised over 16 elements per thread; measured 249 -> 214 ms for 100 GPT-2 XL steps
+// against 256 threads x 2 slots, and 357 ms for 512 x 1).
 // MAXW >= min(world, 8): ranks whose first-round entries are prefetched in registers.
 template <int OPT, int DIV, int MAXW>
-__global__ void __launch_bounds__(kReplayThreads, MAXW >= 8 ? 3 : 4)
+__global__ void __launch_bounds__(kReplayThreads, MAXW >= 8 ? LD_REPLAY_MINB * 3 / 4 : LD_REPLAY_MINB)
 replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
               const uint32_t* __restrict__ start, int64_t n_tiles, const float* __restrict__ scal,
               AdamK ak, uint64_t lo, uint64_t hi, int64_t tile0, float* __restrict__ p, float* __restrict__ m,
@@ -138,9 +145,9 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
   // state in element pairs (f32x2: FADD2/FMUL2/FFMA2 do both halves in one instruction, each
   // rounded exactly like the scalar operation): pair x = 2 i + h holds elements 2h, 2h+1 of the
   // thread's float4 slot i
-  f32x2 P2[4], M2[4], V2[4];
+  f32x2 P2[2 * kReplaySlots], M2[2 * kReplaySlots], V2[2 * kReplaySlots];
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kReplaySlots; ++i) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float pe[2], me[2], ve[2];
@@ -164,7 +171,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
   const int64_t tl = blockIdx.x;                       // tile relative to the window
   // Software pipeline over steps (everything that step s+1 needs from HBM is in flight while step
   // s computes): s_a/s_b[x & 1] in shared memory hold the entry ranges of step x for every rank;
-  // the first 256 entries of every rank for step s sit in registers (pj, pv), loaded during s-1.
+  // the first kReplayThreads entries of every rank for step s sit in registers (pj, pv), loaded during s-1.
   __shared__ uint32_t s_a[2][MAXW], s_b[2][MAXW];
   const bool ranger = tid < world && tid < MAXW;
   if (ranger) {
@@ -201,8 +208,8 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
 #pragma unroll 1
   for (int64_t s = 0; s < n_steps; ++s) {
     const int cur = (int)(s & 1);
-    G4[tid] = make_float4(0.f, 0.f, 0.f, 0.f);
-    G4[tid + kReplayThreads] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < kReplaySlots; ++i) G4[tid + kReplayThreads * i] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     const uint32_t* blk = diffs + (uint64_t)s * world * 2 * K;
     // rank by rank from +0: the rank-order sum of DESIGN.md R-8
@@ -244,7 +251,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
     }
     const f32x2 LR = pk2(slr, slr), R1 = pk2(sr1, sr1), R2 = pk2(sr2, sr2);
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {   // two float4 slots = 4 independent element pairs (ILP)
+    for (int i = 0; i < kReplaySlots; ++i) {   // float4 slots: 2 independent element pairs each
       const float4 gv = G4[tid + kReplayThreads * i];
       const f32x2 g01 = pk2(mean_of<DIV>(gv.x, n, inv), mean_of<DIV>(gv.y, n, inv));
       const f32x2 g23 = pk2(mean_of<DIV>(gv.z, n, inv), mean_of<DIV>(gv.w, n, inv));
@@ -274,7 +281,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kReplaySlots; ++i) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t j = j0 + 4 * (tid + kReplayThreads * i) + q;

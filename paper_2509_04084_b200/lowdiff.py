@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "liblowdiff.so")
+LIB_PATH = os.environ.get("LOWDIFF_LIB") or os.path.join(_HERE, "_lib", "liblowdiff.so")   # env: tuning builds
 
 OK, E_INVALID, E_DIM, E_NUMERIC, E_CUDA, E_NCCL, E_IO, E_CORRUPT, E_GAP, E_STATE = range(10)
 SGD, ADAM = 0, 1
