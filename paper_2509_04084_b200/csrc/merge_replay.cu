@@ -126,11 +126,16 @@ merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __r
 
 struct AdamK { float b1, c1, b2, c2, eps, nz; };   // nz = -0.0f (ieee_fast.cuh: opaque -0 addend)
 
-// Fused n-step replay.  Thread owns elements j0 + 4*(tid + kReplayThreads*i) + q, i < kReplaySlots,
-// q in 0..3 (128 threads x 4 slots: the per-step fixed work -- zeroing G, barriers, the entry
-// loops -- is amortised over 16 elements per thread; measured 249 -> 214 ms for 100 GPT-2 XL steps
-// against 256 threads x 2 slots, and 357 ms for 512 x 1).
+// Fused n-step replay.  Each warp owns a contiguous kWarpSpan-element region of the CTA's tile and
+// lane l the elements j0 + wb + 4*(l + 32*i) + q (i < kReplaySlots, q < 4): the per-step G_t of the
+// region is built in the warp's own slice of shared memory, so a step needs only __syncwarp --
+// no CTA barrier (barrier stalls were 17% of the 256-thread version's samples).  128 threads x 4
+// slots: the per-step fixed work (zeroing, entry loops) is amortised over 16 elements per thread
+// (measured 249 -> 214 ms for 100 GPT-2 XL steps against 256 x 2, 357 ms for 512 x 1).
 // MAXW >= min(world, 8): ranks whose first-round entries are prefetched in registers.
+constexpr int kWarpSpan = kReplayTile / (kReplayThreads / 32);
+static_assert(kWarpSpan == 128 * kReplaySlots, "one float4 per lane per slot");
+
 template <int OPT, int DIV, int MAXW>
 __global__ void __launch_bounds__(kReplayThreads, MAXW >= 8 ? LD_REPLAY_MINB * 3 / 4 : LD_REPLAY_MINB)
 replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
@@ -138,13 +143,16 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
               AdamK ak, uint64_t lo, uint64_t hi, int64_t tile0, float* __restrict__ p, float* __restrict__ m,
               float* __restrict__ v) {
   // elements [lo, hi) are replayed; p, m, v hold exactly that range (p[0] is element lo)
-  __shared__ float G[kReplayTile];
+  __shared__ __align__(16) float G[kReplayTile];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t t = tile0 + blockIdx.x;
   const uint64_t j0 = (uint64_t)t * kReplayTile;
-  const int tid = threadIdx.x;
+  const uint32_t wb = (uint32_t)warp * kWarpSpan;           // the warp's region: [j0 + wb, j0 + wb + span)
+  const uint32_t jw = (uint32_t)j0 + wb;                    // Psi < 2^32
+  float* Gw = G + wb;
+  float4* G4w = reinterpret_cast<float4*>(Gw);
   // state in element pairs (f32x2: FADD2/FMUL2/FFMA2 do both halves in one instruction, each
-  // rounded exactly like the scalar operation): pair x = 2 i + h holds elements 2h, 2h+1 of the
-  // thread's float4 slot i
+  // rounded exactly like the scalar operation): pair x = 2 i + h holds elements 2h, 2h+1 of slot i
   f32x2 P2[2 * kReplaySlots], M2[2 * kReplaySlots], V2[2 * kReplaySlots];
 #pragma unroll
   for (int i = 0; i < kReplaySlots; ++i) {
@@ -153,7 +161,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       float pe[2], me[2], ve[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const uint64_t j = j0 + 4 * (tid + kReplayThreads * i) + 2 * h + e;
+        const uint64_t j = (uint64_t)jw + 4 * (lane + 32 * i) + 2 * h + e;
         const bool in = j >= lo && j < hi;
         pe[e] = in ? p[j - lo] : 0.f;
         me[e] = (OPT == LOWDIFF_ADAM && in) ? m[j - lo] : 0.f;
@@ -169,90 +177,96 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
   const bool eps_ok = ak.eps >= 0x1p-60f && ak.eps <= 0x1p59f;   // adam_u_fast's precondition
   const uint64_t tstride = (uint64_t)(n_tiles + 1);   // n_tiles = tiles in the window
   const int64_t tl = blockIdx.x;                       // tile relative to the window
-  // Software pipeline over steps (everything that step s+1 needs from HBM is in flight while step
-  // s computes): s_a/s_b[x & 1] in shared memory hold the entry ranges of step x for every rank;
-  // the first kReplayThreads entries of every rank for step s sit in registers (pj, pv), loaded during s-1.
-  __shared__ uint32_t s_a[2][MAXW], s_b[2][MAXW];
-  const bool ranger = tid < world && tid < MAXW;
-  if (ranger) {
-    s_a[0][tid] = __ldg(start + (uint64_t)tid * tstride + tl);
-    s_b[0][tid] = __ldg(start + (uint64_t)tid * tstride + tl + 1);
+  // Software pipeline over steps: lane r (< 32) holds rank r's entry range of this tile for the
+  // current step (ra_c, rb_c) and the next (ra_n, rb_n); the ranges of step s+2 and the first
+  // round of step s+1's entries (pj, pv: entry a_r + lane of every rank < MAXW) are loaded while
+  // step s computes.
+  const int wr = world < 32 ? world : 32;
+  uint32_t ra_c = 0, rb_c = 0, ra_n = 0, rb_n = 0;
+  if (lane < wr) {
+    ra_c = __ldg(start + (uint64_t)lane * tstride + tl);
+    rb_c = __ldg(start + (uint64_t)lane * tstride + tl + 1);
     if (n_steps > 1) {
-      const uint32_t* st1 = start + ((uint64_t)world + tid) * tstride + tl;
-      s_a[1][tid] = __ldg(st1);
-      s_b[1][tid] = __ldg(st1 + 1);
+      const uint32_t* st1 = start + ((uint64_t)world + lane) * tstride + tl;
+      ra_n = __ldg(st1);
+      rb_n = __ldg(st1 + 1);
     }
   }
-  __syncthreads();
   uint32_t pj[MAXW], pv[MAXW];
-  auto load_entries = [&](int64_t x) {   // first round of step x's entries of every rank
+  auto load_entries = [&](int64_t x, uint32_t ra, uint32_t rb) {   // first round of step x
     const uint32_t* blk = diffs + (uint64_t)x * world * 2 * K;
-    const int b = (int)(x & 1);
 #pragma unroll
     for (int r = 0; r < MAXW; ++r) {
       pj[r] = 0xFFFFFFFFu;
       pv[r] = 0u;
       if (r < world) {
-        const uint32_t e = s_a[b][r] + tid;
-        if (e < s_b[b][r]) {
+        const uint32_t e = __shfl_sync(0xFFFFFFFFu, ra, r) + lane;
+        const uint32_t eb = __shfl_sync(0xFFFFFFFFu, rb, r);
+        if (e < eb) {
           const uint32_t* idx = blk + (uint64_t)r * 2 * K;
-          pj[r] = __ldg(idx + e) - (uint32_t)j0;
+          pj[r] = __ldg(idx + e) - jw;   // >= kWarpSpan (wrapped) when outside the warp's region
           pv[r] = __ldg(idx + K + e);
         }
       }
     }
   };
-  load_entries(0);
+  load_entries(0, ra_c, rb_c);
   float lr = __ldg(scal), r1 = __ldg(scal + 1), r2 = __ldg(scal + 2);
-  float4* G4 = reinterpret_cast<float4*>(G);
 #pragma unroll 1
   for (int64_t s = 0; s < n_steps; ++s) {
-    const int cur = (int)(s & 1);
 #pragma unroll
-    for (int i = 0; i < kReplaySlots; ++i) G4[tid + kReplayThreads * i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncthreads();
+    for (int i = 0; i < kReplaySlots; ++i) G4w[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
     const uint32_t* blk = diffs + (uint64_t)s * world * 2 * K;
-    // rank by rank from +0: the rank-order sum of DESIGN.md R-8
+    // rank by rank from +0: the rank-order sum of DESIGN.md R-8 (indices unique within a rank)
 #pragma unroll
     for (int r = 0; r < MAXW; ++r) {
       if (r < world) {
-        if (pj[r] != 0xFFFFFFFFu) G[pj[r]] = __fadd_rn(G[pj[r]], __uint_as_float(pv[r]));
+        if (pj[r] < (uint32_t)kWarpSpan) Gw[pj[r]] = __fadd_rn(Gw[pj[r]], __uint_as_float(pv[r]));
+        const uint32_t a = __shfl_sync(0xFFFFFFFFu, ra_c, r), b = __shfl_sync(0xFFFFFFFFu, rb_c, r);
         const uint32_t* idx = blk + (uint64_t)r * 2 * K;
-        for (uint32_t e = s_a[cur][r] + tid + kReplayThreads; e < s_b[cur][r]; e += kReplayThreads) {
-          const uint32_t j = __ldg(idx + e) - (uint32_t)j0;
-          G[j] = __fadd_rn(G[j], __uint_as_float(__ldg(idx + K + e)));
+        for (uint32_t e = a + 32 + lane; e < b; e += 32) {
+          const uint32_t jl = __ldg(idx + e) - jw;
+          if (jl < (uint32_t)kWarpSpan) Gw[jl] = __fadd_rn(Gw[jl], __uint_as_float(__ldg(idx + K + e)));
         }
-        __syncthreads();
+        __syncwarp();
       }
     }
     for (int r = MAXW; r < world; ++r) {   // ranks beyond the register window
-      const uint32_t* st = start + ((uint64_t)s * world + r) * tstride + tl;
-      const uint32_t* idx = blk + (uint64_t)r * 2 * K;
-      const uint32_t a = __ldg(st), b = __ldg(st + 1);
-      for (uint32_t e = a + tid; e < b; e += kReplayThreads) {
-        const uint32_t j = __ldg(idx + e) - (uint32_t)j0;
-        G[j] = __fadd_rn(G[j], __uint_as_float(__ldg(idx + K + e)));
+      uint32_t a, b;
+      if (r < 32) {
+        a = __shfl_sync(0xFFFFFFFFu, ra_c, r);
+        b = __shfl_sync(0xFFFFFFFFu, rb_c, r);
+      } else {
+        const uint32_t* st = start + ((uint64_t)s * world + r) * tstride + tl;
+        a = __ldg(st);
+        b = __ldg(st + 1);
       }
-      __syncthreads();
+      const uint32_t* idx = blk + (uint64_t)r * 2 * K;
+      for (uint32_t e = a + lane; e < b; e += 32) {
+        const uint32_t jl = __ldg(idx + e) - jw;
+        if (jl < (uint32_t)kWarpSpan) Gw[jl] = __fadd_rn(Gw[jl], __uint_as_float(__ldg(idx + K + e)));
+      }
+      __syncwarp();
     }
     // prefetch for the next steps while this one computes
     const float slr = lr, sr1 = r1, sr2 = r2;
     uint32_t na = 0, nb = 0;
     if (s + 1 < n_steps) {
-      load_entries(s + 1);
+      load_entries(s + 1, ra_n, rb_n);
       lr = __ldg(scal + 3 * (s + 1));
       r1 = __ldg(scal + 3 * (s + 1) + 1);
       r2 = __ldg(scal + 3 * (s + 1) + 2);
     }
-    if (ranger && s + 2 < n_steps) {
-      const uint32_t* st2 = start + ((uint64_t)(s + 2) * world + tid) * tstride + tl;
+    if (lane < wr && s + 2 < n_steps) {
+      const uint32_t* st2 = start + ((uint64_t)(s + 2) * world + lane) * tstride + tl;
       na = __ldg(st2);
       nb = __ldg(st2 + 1);
     }
     const f32x2 LR = pk2(slr, slr), R1 = pk2(sr1, sr1), R2 = pk2(sr2, sr2);
 #pragma unroll
     for (int i = 0; i < kReplaySlots; ++i) {   // float4 slots: 2 independent element pairs each
-      const float4 gv = G4[tid + kReplayThreads * i];
+      const float4 gv = G4w[lane + 32 * i];
       const f32x2 g01 = pk2(mean_of<DIV>(gv.x, n, inv), mean_of<DIV>(gv.y, n, inv));
       const f32x2 g23 = pk2(mean_of<DIV>(gv.z, n, inv), mean_of<DIV>(gv.w, n, inv));
       if (OPT == LOWDIFF_ADAM) {
@@ -260,15 +274,17 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
         // d = sqrt(vh) + eps ; u = mh / d ; p = p - lr*u          (R-11)
         // Correctly rounded sqrt / divide take the exact fast sequence (ieee_fast.cuh) for every
         // lane; a warp-rare fix-up redoes out-of-window operands with the intrinsics.
-        f32x2 mh[2], vh[2], u[2];
+        f32x2 u[2];
         bool s0, s1;
-        u[0] = adam2_u(M2[2 * i], V2[2 * i], g01, k2, R1, R2, &mh[0], &vh[0], &s0);
-        u[1] = adam2_u(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2, &mh[1], &vh[1], &s1);
+        u[0] = adam2_u(M2[2 * i], V2[2 * i], g01, k2, R1, R2, &s0);
+        u[1] = adam2_u(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2, &s1);
         if (s0 | s1 | !eps_ok) {   // rare: redo the group exactly with the intrinsics
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            u[h] = pk2(__fdiv_rn(lo2(mh[h]), __fadd_rn(__fsqrt_rn(lo2(vh[h])), ak.eps)),
-                       __fdiv_rn(hi2(mh[h]), __fadd_rn(__fsqrt_rn(hi2(vh[h])), ak.eps)));
+          for (int h = 0; h < 2; ++h) {
+            const f32x2 mh = mul2(M2[2 * i + h], R1), vh = mul2(V2[2 * i + h], R2);
+            u[h] = pk2(__fdiv_rn(lo2(mh), __fadd_rn(__fsqrt_rn(lo2(vh)), ak.eps)),
+                       __fdiv_rn(hi2(mh), __fadd_rn(__fsqrt_rn(hi2(vh)), ak.eps)));
+          }
         }
         P2[2 * i] = sub_prod2(P2[2 * i], LR, u[0], k2.nz);
         P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, u[1], k2.nz);
@@ -277,14 +293,17 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
         P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, g23, k2.nz);
       }
     }
-    if (ranger) { s_a[cur][tid] = na; s_b[cur][tid] = nb; }   // ranges of step s+2
-    __syncthreads();
+    ra_c = ra_n;
+    rb_c = rb_n;
+    ra_n = na;
+    rb_n = nb;
+    __syncwarp();   // every lane has read this step's G before the next step zeroes and adds
   }
 #pragma unroll
   for (int i = 0; i < kReplaySlots; ++i) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint64_t j = j0 + 4 * (tid + kReplayThreads * i) + q;
+      const uint64_t j = (uint64_t)jw + 4 * (lane + 32 * i) + q;
       const int x = 2 * i + (q >> 1);
       if (j >= lo && j < hi) {
         p[j - lo] = (q & 1) ? hi2(P2[x]) : lo2(P2[x]);

@@ -129,9 +129,10 @@ __global__ void adam2_check_kernel(uint64_t n, uint64_t seed, float neg0, unsign
       if (((h >> 24) & 7) == 0) v[e] = 0.0f;
     }
     const AdamK2 k2 = make_adamk2(b1, c1, b2, c2, eps, neg0);
-    f32x2 P = pk2(p[0], p[1]), M = pk2(m[0], m[1]), V = pk2(v[0], v[1]), mh, vh;
+    f32x2 P = pk2(p[0], p[1]), M = pk2(m[0], m[1]), V = pk2(v[0], v[1]);
     bool sl;
-    f32x2 u = adam2_u(M, V, pk2(g[0], g[1]), k2, pk2(r1, r1), pk2(r2, r2), &mh, &vh, &sl);
+    f32x2 u = adam2_u(M, V, pk2(g[0], g[1]), k2, pk2(r1, r1), pk2(r2, r2), &sl);
+    const f32x2 mh = mul2(M, pk2(r1, r1)), vh = mul2(V, pk2(r2, r2));
     if (sl)
       u = pk2(__fdiv_rn(lo2(mh), __fadd_rn(__fsqrt_rn(lo2(vh)), eps)),
               __fdiv_rn(hi2(mh), __fadd_rn(__fsqrt_rn(hi2(vh)), eps)));
