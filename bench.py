@@ -58,7 +58,7 @@ class Clocks:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -441,6 +441,20 @@ def run_ours(args):
                     "frac_of_hbm_unfused_model": unfused / t_rep / B_HBM,
                     "fused_algorithmic_gbs_per_rank": fused / t_rep / 1e9,
                     "alu_lane_instr_per_param_step_at_peak": alu_peak * t_rep / (n_rep * S)}
+        # SGD replay of the same blocks (SURVEY §8(d) M2, C4 SGD row): HBM model n (8 S + 8 N K)
+        ctx.replay_range(ld.SGD, world, n_rep, diffs, rscal, lo, hi, p)   # warm-up
+        torch.cuda.synchronize()
+        barrier(world)
+        g0.record()
+        ctx.replay_range(ld.SGD, world, n_rep, diffs, rscal, lo, hi, p)
+        g1.record()
+        torch.cuda.synchronize()
+        sms_ = allmax(g0.elapsed_time(g1), world)
+        unf_sgd = n_rep * (8 * S + 8 * world * K)
+        recovery["sgd"] = {"value": n_rep * psi / (sms_ / 1e3), "unit": "param-steps/s", "steps": n_rep, "ms": sms_,
+                           "effective_unfused_gbs_per_rank": unf_sgd / (sms_ / 1e3) / 1e9,
+                           "frac_of_hbm_unfused_model": unf_sgd / (sms_ / 1e3) / B_HBM,
+                           "fused_algorithmic_gbs_per_rank": (8 * S + n_rep * 8 * world * K) / (sms_ / 1e3) / 1e9}
         del diffs, p, m, v
 
     # writer throughput (files, CRC-32C, rename) on this box's storage, reported separately

@@ -123,7 +123,7 @@ def _oracle_live(ref, sizes, ppm, world, T, lr, seed):
     return states, gath, scals
 
 
-@pytest.mark.parametrize("world,b", [(1, 2), (2, 3), (3, 4)])
+@pytest.mark.parametrize("world,b", [(1, 2), (2, 3), (3, 4), (8, 2)])
 def test_union_persist_files_and_recover(ref, tmp_path, world, b):
     sizes, ppm, T, lr = [30000, 1600, 50000, 7], 10000, 7, 1e-2
     psi = sum(sizes)
