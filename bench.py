@@ -232,7 +232,7 @@ def run_ours(args):
         sends = [torch.empty(2 * K, dtype=torch.int32, device=dev) for _ in range(2)]
     send = sends[0]
     gathered = torch.empty(world * 2 * K, dtype=torch.int32, device=dev) if world > 1 else None
-    scal = [ld.derive_step_scalars(t, 1e-3) for t in range(1, args.warmup + args.steps + 8)]
+    scal = [ld.derive_step_scalars(t, 1e-3) for t in range(1, args.warmup + 2 * args.steps + 40)]
     it = [0]
 
     def step(g=None):
@@ -248,11 +248,12 @@ def run_ours(args):
         it[0] += 1
         return sd
 
+    if not args.no_graphs:
+        ctx.set_graphs(True)          # compress + merge replayed as captured CUDA graphs
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     ctx.sync()
-    ctx.prof_enable(True)
     l0 = ctx.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = Clocks(local)
@@ -269,11 +270,19 @@ def run_ours(args):
     barrier(world)
     ms = allmax(e0.elapsed_time(e1), world)
     launches = ctx.kernel_launches() - l0
+    # per-kernel breakdown: a separate pass of the same steps with CUDA events recorded on the
+    # launching streams (profiling replaces the graphs by plain launches; not the timed region)
+    n_prof = max(3, min(args.steps, 10))
+    ctx.prof_enable(True)
+    for _ in range(n_prof):
+        step()
+    ctx.wait_persist()
+    torch.cuda.synchronize()
     kern = {}
     for name in ("small_layer", "scan", "select", "emit", "merge", "peer_merge", "allgather", "d2h"):
         tot, n = ctx.prof_read(name)
         if n:
-            kern[name] = {"ms_per_launch": tot / n, "launches": n, "share_of_step": tot / args.steps / (ms / args.steps)}
+            kern[name] = {"ms_per_launch": tot / n, "launches": n, "share_of_step": tot / n_prof / (ms / args.steps)}
     ctx.prof_enable(False)
     ctx.sync()
     st = ctx.stats()
@@ -393,6 +402,7 @@ def run_ours(args):
 
     # recovery replay (M2): n steps of gathered blocks resident in HBM, fused Adam replay
     recovery = None
+    ctx.set_graphs(False)   # the recovery leg compresses into 100 different blocks: plain launches
     if not args.no_recovery:
         del dense
         step_bytes = world * 8 * K
@@ -626,6 +636,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.workload}@{args.ppm}ppm", "psi": psi, "layers": len(sizes),
                        "k_total": K, "density_ppm": args.ppm, "batch_size": 4, "parallelism": f"dp{world}", "exchange": args.exchange,
+                       "cuda_graphs": not args.no_graphs,
                        "inputs": "D4 row-sparse Gaussian, alpha=0.5 rank correlation; 2 gradient buffers of "
                                  f"{4 * psi / 1e9:.2f} GB alternate (> L2, no flush needed)",
                        "persist": "D2H of the rank's block into the pinned ring inside the timed region; "
@@ -656,6 +667,7 @@ def main():
     ap.add_argument("--no-update", action="store_true")
     ap.add_argument("--no-snapshot", action="store_true")
     ap.add_argument("--no-union", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="plain launches instead of captured CUDA graphs")
     ap.add_argument("--snapshot-reps", type=int, default=20,
                     help="proxy backward: HBM passes over each bucket (20 ~ 38 ms for GPT-2 XL, about the backward "
                          "of 8K tokens at ~1.2 PFLOP/s)")

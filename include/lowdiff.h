@@ -370,6 +370,14 @@ lowdiff_status lowdiff_prof_enable(lowdiff_ctx *ctx, int32_t enable);
 lowdiff_status lowdiff_prof_read(lowdiff_ctx *ctx, const char *name, double *total_ms,
                                  int64_t *launches);
 
+/* CUDA graphs (enable != 0): lowdiff_compress and the merge of lowdiff_exchange / lowdiff_merge
+ *    capture their kernel sequence into a CUDA graph per (call, buffer addresses, deferred-zero
+ *    state) on first use and replay it afterwards -- the same kernels with the same arguments, so
+ *    the same bits, with fewer launch gaps (what bounds small models).  Up to 8 graphs are cached;
+ *    a graph is rebuilt when a library scratch buffer it uses is reallocated.  Ignored while
+ *    profiling is enabled (lowdiff_prof_enable).  Off by default. */
+lowdiff_status lowdiff_set_graphs(lowdiff_ctx *ctx, int32_t enable);
+
 /* Number of kernels this library launched on behalf of ctx since creation. */
 int64_t lowdiff_kernel_launches(const lowdiff_ctx *ctx);
 

@@ -424,6 +424,56 @@ void prof_end(lowdiff_ctx* c, int handle, cudaStream_t s) {
 }
 }  // namespace ld
 
+// ---------------------------------------------------------------- CUDA graphs
+// Launch-latency-bound configurations (small models: ~20 dependent kernels of a few us each) replay
+// a captured graph of a call's kernels instead of launching them one by one.  A graph is keyed by
+// the call kind, its buffer addresses and the host-side state its launch sequence depends on, and
+// is rebuilt when a scratch buffer it baked in is reallocated (scratch_gen).  At most 8 are kept.
+template <class F>
+static lowdiff_status run_graphed(lowdiff_ctx* c, int kind, const void* a, const void* b, const void* d, int flag,
+                                  cudaStream_t s, F&& body) {
+  for (auto& g : c->graphs) {
+    if (g.kind == kind && g.a == a && g.b == b && g.c == d && g.flag == flag && g.gen == c->scratch_gen) {
+      g.last_use = ++c->graph_tick;
+      CK(cudaGraphLaunch(g.exec, s));
+      c->launches += g.launches;
+      return LOWDIFF_OK;
+    }
+  }
+  if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  const int64_t l0 = c->launches;
+  CK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+  cudaError_t e = body(c->cap_stream);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(c->cap_stream, &graph);
+  const int64_t n = c->launches - l0;
+  c->launches = l0;
+  if (e == cudaSuccess) e = e2;
+  cudaGraphExec_t exec = nullptr;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(c, e, "graph capture");
+  // drop graphs of stale scratch, then the least recently used beyond 8
+  for (size_t i = 0; i < c->graphs.size();) {
+    if (c->graphs[i].gen != c->scratch_gen) {
+      cudaGraphExecDestroy(c->graphs[i].exec);
+      c->graphs.erase(c->graphs.begin() + (long)i);
+    } else {
+      ++i;
+    }
+  }
+  if (c->graphs.size() >= 8) {
+    auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                [](const ld::GraphEntry& x, const ld::GraphEntry& y) { return x.last_use < y.last_use; });
+    cudaGraphExecDestroy(lru->exec);
+    c->graphs.erase(lru);
+  }
+  c->graphs.push_back(ld::GraphEntry{kind, a, b, d, flag, c->scratch_gen, exec, n, ++c->graph_tick});
+  CK(cudaGraphLaunch(exec, s));
+  c->launches += n;
+  return LOWDIFF_OK;
+}
+
 extern "C" {
 
 int32_t lowdiff_abi_version(void) { return 1; }
@@ -611,6 +661,8 @@ lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
   if (c->peer_flags) cudaFree(c->peer_flags);
   for (auto e : {c->ev_tmp, c->ev_side_all, c->last_d2h, c->full_done, c->full_staged, c->snap_done[0], c->snap_done[1]})
     if (e) cudaEventDestroy(e);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -633,6 +685,13 @@ lowdiff_status lowdiff_layer_k(const lowdiff_ctx* c, int32_t layer, int64_t* k, 
   return LOWDIFF_OK;
 }
 
+lowdiff_status lowdiff_set_graphs(lowdiff_ctx* c, int32_t enable) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  c->use_graphs = enable != 0;
+  return LOWDIFF_OK;
+}
+
 lowdiff_status lowdiff_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send, void* stream) {
   lowdiff_status st = entry(c);
   if (st) return st;
@@ -648,7 +707,18 @@ lowdiff_status lowdiff_compress(lowdiff_ctx* c, const float* grad, float* residu
     if (c->peer_own[i] == send) pslot = i;
   if (pslot >= 0 && c->peer_set && c->peer_epoch[pslot] > 0)   // WAR: every rank has read the old block
     CK(ld::launch_peer_wait_done(c->peer_flags, c->peer_slots, pslot, c->cfg.world, c->peer_epoch[pslot], s));
-  CK(ld::launch_compress(c, grad, c->cfg.error_feedback ? residual : nullptr, send, s));
+  float* res = c->cfg.error_feedback ? residual : nullptr;
+  if (c->use_graphs && !c->prof) {
+    const int lazy = (res && c->lazy_residual == res) ? 1 : 0;   // the only host state the sequence reads
+    // (measured: the refill levels as conditional IF nodes set by a flag kernel were slower than
+    // replaying their empty grids -- ResNet-50 174 -> 188 us per step -- so the graph is a plain capture)
+    if ((st = run_graphed(c, 0, grad, res, send, lazy, s,
+                          [&](cudaStream_t cs) { return ld::launch_compress(c, grad, res, send, cs); })))
+      return st;
+    c->lazy_residual = res;   // what launch_compress records for a replayed call too
+  } else {
+    CK(ld::launch_compress(c, grad, res, send, s));
+  }
   if (pslot >= 0) {              // publish: the block's merge tile starts, then its ready flag
     CK(ld::launch_tile_start(send, (uint64_t)c->K, c->psi, send + 2 * c->K, s));
     c->peer_epoch[pslot] += 1;
@@ -759,7 +829,15 @@ lowdiff_status lowdiff_merge(lowdiff_ctx* c, int32_t world, const uint32_t* gath
   if (world < 1 || !gathered || !dense_out) return fail(c, LOWDIFF_E_INVALID, "merge: bad argument");
   if ((reinterpret_cast<uintptr_t>(gathered) & 3u) || !aligned16(dense_out))
     return fail(c, LOWDIFF_E_INVALID, "merge: gathered must be 4-byte and dense_out 16-byte aligned");
-  CK(ld::launch_merge(c, world, gathered, dense_out, static_cast<cudaStream_t>(stream)));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->use_graphs && !c->prof) {
+    // size the scratch outside the capture (its pointer is baked into the graph)
+    if (c->merge_scratch_bytes < ld::merge_scratch_bytes(c->psi, world, world)) CK(ld::launch_merge(c, world, gathered, dense_out, s));
+    else return run_graphed(c, 1, gathered, dense_out, nullptr, world, s,
+                            [&](cudaStream_t cs) { return ld::launch_merge(c, world, gathered, dense_out, cs); });
+    return LOWDIFF_OK;
+  }
+  CK(ld::launch_merge(c, world, gathered, dense_out, s));
   return LOWDIFF_OK;
 }
 

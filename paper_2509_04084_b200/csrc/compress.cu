@@ -777,12 +777,16 @@ int num_sms() {
 
 size_t compress_hist_bytes(int n_large) { return (size_t)n_large * kHistRow * sizeof(uint32_t); }
 
-cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send,
-                            cudaStream_t s) {
+// lowdiff_compress in phases: head (small layers forked, scan, chunk prep, plan), refill levels 1
+// and 2 (empty grids unless the plan queued a refill), tail (digits, counts, emit, join).
+// launch_compress runs them in order (the CUDA-graph form captures the same sequence).
+cudaError_t compress_head(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send, cudaStream_t s,
+                          int* sel_h) {
   DevPlan& P = c->plan;
   const bool ef = c->cfg.error_feedback != 0;
   int h;
   cudaError_t e;
+  *sel_h = -1;
   if (P.n_small) {
     static bool attr_set[2] = {false, false};
     const size_t smem = (size_t)(kSmallMax + 2048) * sizeof(uint32_t);
@@ -793,7 +797,7 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
       attr_set[ef] = true;
     }
     // the small layers touch disjoint elements and send entries from the large-layer path, so
-    // they run on a forked stream, concurrently with the scan, and join before the call returns
+    // they run on a forked stream, concurrently with the scan, and join in the tail
     const bool fork = P.n_large && c->aux;
     cudaStream_t ss = fork ? c->aux : s;
     if (fork) {
@@ -812,41 +816,71 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(P.counters, 0, 8 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
-  const int sms = num_sms();
   const int layer_blocks = (P.n_large * 32 + 255) / 256;     // warp per large layer
   const int chunk_blocks = (P.n_chunks + 7) / 8;              // warp per chunk
   const unsigned scan_grid = (unsigned)P.n_chunks * kPiecesPerChunk;   // full grid: no tail loop
   const int uK = kScanWarps * 32;
-
   // lazy residual zeroing applies only to the residual buffer whose selection is pending
   const int lazy = (ef && c->lazy_residual == residual) ? 1 : 0;
   prof_begin(c, "scan", s, &h);
   if (ef) scan_kernel<true, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, lazy);
   else scan_kernel<false, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, 0);
   prof_end(c, h, s);
-  prof_begin(c, "select", s, &h);
+  prof_begin(c, "select", s, sel_h);
   chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 0);
   find_kernel<<<layer_blocks, 256, 0, s>>>(P, 0);
-  for (int level = 1; level <= 2; ++level) {   // refills (empty grids in the steady state)
-    if (ef) scan_kernel<true, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, level);
-    else scan_kernel<false, true><<<sms * 16, uK, 0, s>>>(P, grad, residual, level);
-    chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, level);
-    find_kernel<<<layer_blocks, 256, 0, s>>>(P, level == 1 ? 1 : 4);
-  }
-  digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
-  find_kernel<<<layer_blocks, 256, 0, s>>>(P, 2);
-  digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 2);
-  find_kernel<<<layer_blocks, 256, 0, s>>>(P, 3);
-  count_kernel<<<chunk_blocks, 256, 0, s>>>(P);
-  layer_scan_kernel<<<P.n_large, 1024, 0, s>>>(P);
-  prof_end(c, h, s);
-  prof_begin(c, "emit", s, &h);
-  emit_kernel<<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K);
-  prof_end(c, h, s);
-  if (P.n_small && c->aux && (e = cudaStreamWaitEvent(s, c->ev_join, 0)) != cudaSuccess) return e;   // join
-  c->lazy_residual = ef ? residual : nullptr;   // this call's large-layer selection is now pending
-  c->launches += 17;
+  c->launches += 3;
   return cudaGetLastError();
+}
+
+cudaError_t compress_refill(lowdiff_ctx* c, const float* grad, float* residual, int level, cudaStream_t s) {
+  DevPlan& P = c->plan;
+  if (!P.n_large) return cudaSuccess;
+  const bool ef = c->cfg.error_feedback != 0;
+  const int layer_blocks = (P.n_large * 32 + 255) / 256;
+  const int chunk_blocks = (P.n_chunks + 7) / 8;
+  const int uK = kScanWarps * 32;
+  if (ef) scan_kernel<true, true><<<num_sms() * 16, uK, 0, s>>>(P, grad, residual, level);
+  else scan_kernel<false, true><<<num_sms() * 16, uK, 0, s>>>(P, grad, residual, level);
+  chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, level);
+  find_kernel<<<layer_blocks, 256, 0, s>>>(P, level == 1 ? 1 : 4);
+  c->launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t compress_tail(lowdiff_ctx* c, float* residual, uint32_t* send, cudaStream_t s, int sel_h) {
+  DevPlan& P = c->plan;
+  const bool ef = c->cfg.error_feedback != 0;
+  cudaError_t e;
+  if (P.n_large) {
+    const int layer_blocks = (P.n_large * 32 + 255) / 256;
+    const int chunk_blocks = (P.n_chunks + 7) / 8;
+    digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
+    find_kernel<<<layer_blocks, 256, 0, s>>>(P, 2);
+    digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 2);
+    find_kernel<<<layer_blocks, 256, 0, s>>>(P, 3);
+    count_kernel<<<chunk_blocks, 256, 0, s>>>(P);
+    layer_scan_kernel<<<P.n_large, 1024, 0, s>>>(P);
+    prof_end(c, sel_h, s);
+    int h;
+    prof_begin(c, "emit", s, &h);
+    emit_kernel<<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K);
+    prof_end(c, h, s);
+    if (P.n_small && c->aux && (e = cudaStreamWaitEvent(s, c->ev_join, 0)) != cudaSuccess) return e;   // join
+    c->launches += 7;
+  }
+  c->lazy_residual = ef ? residual : nullptr;   // this call's large-layer selection is now pending
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send,
+                            cudaStream_t s) {
+  int sel_h;
+  cudaError_t e = compress_head(c, grad, residual, send, s, &sel_h);
+  if (e == cudaSuccess) e = compress_refill(c, grad, residual, 1, s);
+  if (e == cudaSuccess) e = compress_refill(c, grad, residual, 2, s);
+  if (e == cudaSuccess) e = compress_tail(c, residual, send, s, sel_h);
+  return e;
 }
 
 cudaError_t launch_materialize(lowdiff_ctx* c, float* residual, cudaStream_t s) {

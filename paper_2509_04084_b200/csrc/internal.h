@@ -105,6 +105,11 @@ struct Slot {
 // gradient of `iteration`, 2 = persist the replica as it stands after the preceding items
 struct RepJob { int kind; int64_t iteration; lowdiff_step_scalars sc; };
 struct UJob { int64_t iteration; lowdiff_step_scalars sc; int buf; };
+// a captured CUDA graph of one call's kernels, keyed by the call kind and its buffers
+struct GraphEntry {
+  int kind; const void *a, *b, *c; int flag; uint64_t gen;
+  cudaGraphExec_t exec; int64_t launches; uint64_t last_use;
+};
 
 // peer-memory exchange (peer.cu): flag words per rank = ready[n_slots] | done[n_slots][kPeerMaxWorld]
 // | error counter
@@ -229,6 +234,12 @@ struct lowdiff_ctx {
   size_t merge_scratch_bytes = 0;
   void* union_scratch = nullptr;
   size_t union_scratch_bytes = 0;
+  uint64_t scratch_gen = 0;          // bumped when a scratch buffer a graph may bake in is reallocated
+  // CUDA graphs of lowdiff_compress / merge (lowdiff_set_graphs)
+  bool use_graphs = false;
+  cudaStream_t cap_stream = nullptr;
+  std::vector<ld::GraphEntry> graphs;
+  uint64_t graph_tick = 0;
   // union-compacted persistence (NEXT-4): two library-owned device buffers idx | val of u_cap
   // entries each (this rank's shard), their counts, a writer thread that copies exactly the
   // count out and writes .ldu batches
@@ -255,6 +266,11 @@ namespace ld {
 cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send,
                             cudaStream_t s);
 cudaError_t launch_materialize(lowdiff_ctx* c, float* residual, cudaStream_t s);
+// the phases of launch_compress (compress.cu)
+cudaError_t compress_head(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send, cudaStream_t s,
+                          int* sel_h);
+cudaError_t compress_refill(lowdiff_ctx* c, const float* grad, float* residual, int level, cudaStream_t s);
+cudaError_t compress_tail(lowdiff_ctx* c, float* residual, uint32_t* send, cudaStream_t s, int sel_h);
 cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, float* dense,
                          cudaStream_t s);
 // replays elements [lo, hi); p, m, v point at element lo.  ranges: NULL (every entry of every block

@@ -432,6 +432,7 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
   if (c->merge_scratch_bytes < need) {
     if (c->merge_scratch) cudaFree(c->merge_scratch);
     c->merge_scratch = nullptr;
+    c->scratch_gen += 1;   // captured graphs that baked in the old buffer are rebuilt
     c->merge_scratch_bytes = 0;
     cudaError_t e = cudaMalloc(&c->merge_scratch, need);
     if (e != cudaSuccess) return e;
@@ -473,6 +474,7 @@ cudaError_t launch_update(lowdiff_ctx* c, int world, const uint32_t* gathered, c
   if (c->merge_scratch_bytes < need) {
     if (c->merge_scratch) cudaFree(c->merge_scratch);
     c->merge_scratch = nullptr;
+    c->scratch_gen += 1;   // captured graphs that baked in the old buffer are rebuilt
     c->merge_scratch_bytes = 0;
     cudaError_t e = cudaMalloc(&c->merge_scratch, need);
     if (e != cudaSuccess) return e;

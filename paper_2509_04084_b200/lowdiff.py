@@ -113,6 +113,7 @@ def lib():
             "prof_enable": ([P, C.c_int32], S),
             "prof_read": ([P, C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)], S),
             "kernel_launches": ([P], C.c_int64),
+            "set_graphs": ([P, C.c_int32], S),
             "last_error": ([P], C.c_char_p),
             "nccl_unique_id": ([P], S),
             "derive_step_scalars": ([C.c_int64, C.c_double, C.c_double, C.c_double, C.POINTER(StepScalars)], S),
@@ -143,7 +144,7 @@ EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_mater
             "replica_init",
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
             "sync", "get_stats",
-            "prof_enable", "prof_read", "kernel_launches", "last_error", "nccl_unique_id",
+            "prof_enable", "prof_read", "kernel_launches", "set_graphs", "last_error", "nccl_unique_id",
             "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host",
             "write_full_host", "abi_version", "selftest", "wasted_time", "optimal_config", "config_step",
             "simulate_failures"]
@@ -472,6 +473,10 @@ class Context:
         s = Stats()
         self._c("get_stats", lib().lowdiff_get_stats(self._h, C.byref(s)))
         return {f: getattr(s, f) for f, _ in Stats._fields_}
+
+    def set_graphs(self, on=True):
+        """Replay compress / merge as captured CUDA graphs (fewer launch gaps for small models)."""
+        self._c("set_graphs", lib().lowdiff_set_graphs(self._h, int(bool(on))))
 
     def prof_enable(self, on=True):
         self._c("prof_enable", lib().lowdiff_prof_enable(self._h, int(on)))
