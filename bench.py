@@ -124,6 +124,17 @@ def barrier(world):
         dist.barrier()
 
 
+def workload_config(args, sizes, K, world):
+    """The `config` object both arms print (same workload keys)."""
+    psi = sum(sizes)
+    return {"workload": f"{args.workload}@{args.ppm}ppm", "psi": psi, "layers": len(sizes), "k_total": K,
+            "density_ppm": args.ppm, "batch_size": 4, "parallelism": f"dp{world}",
+            "inputs": "D4 row-sparse Gaussian, alpha=0.5 rank correlation; 2 gradient buffers of "
+                      f"{4 * psi / 1e9:.2f} GB alternate (> L2, no flush needed)",
+            "persist": "D2H of the rank's block into the pinned ring inside the timed region; "
+                       "file writing measured separately (writer)"}
+
+
 # --------------------------------------------------------------------------- oracle (CPU) legs
 def oracle_sample(sizes_all, ppm, budget_s):
     """Time the oracle (as it stands, 1 thread) on a bounded sample of the workload: consecutive
@@ -185,7 +196,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.workload}@{args.ppm}ppm", "parallelism": f"dp{args.gpus}"},
+            "config": workload_config(args, sizes, sum(ref.k_table(sizes, args.ppm)), args.gpus),
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": f"{args.workload} layers [{a},{b}) = {psi_s} params per step "
                                        "(compress + exchange + batch serialize, 1 rank)"},
@@ -261,12 +272,18 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks.start()
     e0.record()
-    for _ in range(args.steps):
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
         step()
+        marks[i].record()   # per-step spread (compute stream; the last block's D2H ends the region)
     ctx.wait_persist()
     e1.record()
     torch.cuda.synchronize()
     clk = clocks.stop()
+    per = [e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, args.steps)]
+    per.sort()
+    spread = {"p10": per[len(per) // 10], "p50": per[len(per) // 2], "p90": per[(9 * len(per)) // 10],
+              "note": "compute-stream time per step (event after each step); value uses the whole region"}
     barrier(world)
     ms = allmax(e0.elapsed_time(e1), world)
     launches = ctx.kernel_launches() - l0
@@ -634,14 +651,9 @@ def run_ours(args):
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.workload}@{args.ppm}ppm", "psi": psi, "layers": len(sizes),
-                       "k_total": K, "density_ppm": args.ppm, "batch_size": 4, "parallelism": f"dp{world}", "exchange": args.exchange,
-                       "cuda_graphs": not args.no_graphs,
-                       "inputs": "D4 row-sparse Gaussian, alpha=0.5 rank correlation; 2 gradient buffers of "
-                                 f"{4 * psi / 1e9:.2f} GB alternate (> L2, no flush needed)",
-                       "persist": "D2H of the rank's block into the pinned ring inside the timed region; "
-                                  "file writing measured separately (writer)"},
-            "roofline": roofline, "gate_bj5": gate, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
+            "config": {**workload_config(args, sizes, K, world), "exchange": args.exchange,
+                       "cuda_graphs": not args.no_graphs},
+            "roofline": roofline, "gate_bj5": gate, "kernels": kern, "per_step_ms": spread, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "recovery": recovery, "writer": writer, "full_ckpt": fullck, "update": update,
             "replica": replica, "snapshot": snapshot, "union": union,
             "spec": {"hits": st["spec_hits"], "misses": st["spec_misses"]}}
