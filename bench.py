@@ -569,7 +569,7 @@ def run_ours(args):
             ums = u0.elapsed_time(u1) / 5
             n_u = int(cnt.item())
             share = NU * K * (hi - lo) / psi          # gathered entries falling in the range (expected)
-            alg = 2 * 8 * share + 8 * n_u             # entries read twice (count, emit) + union written
+            alg = 8 * share + 8 * n_u                 # gathered entries in range read once + union written
             res_u[name] = {"range": [lo, hi], "entries": n_u, "ms": ums,
                            "bytes_union": 8 * n_u, "bytes_gathered_share": int(8 * share),
                            "ratio_to_gathered": n_u / share, "algorithmic_gbs": alg / (ums / 1e3) / 1e9}

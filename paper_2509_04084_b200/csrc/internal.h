@@ -280,9 +280,10 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
                           int64_t n_steps, const uint32_t* diffs, const float* scal_dev, uint64_t lo,
                           uint64_t hi, const uint32_t* ranges, float* p, float* m, float* v, cudaStream_t s,
                           uint64_t k_stride = 0);
-// start[b * (T1 - T0 + 1) + t - T0] = first entry of block b (stride 2K, indices ascending) in tile t
+// start[b * (T1 - T0 + 1) + t - T0] = first entry of block b (stride 2K, indices ascending) in tile t;
+// ranges: device scratch u32[2 * n_blocks] (the window's entry range of each block)
 cudaError_t launch_tile_window(const uint32_t* blocks, int n_blocks, uint64_t K, int shift, uint32_t T0, uint32_t T1,
-                               uint32_t* start, cudaStream_t s);
+                               uint32_t* start, uint32_t* ranges, cudaStream_t s);
 // union.cu: union-compacted differential of [lo, hi): out = idx u32[cap] | val u32[cap]
 cudaError_t launch_union(lowdiff_ctx* c, int world, bool mean, const uint32_t* gathered, uint64_t lo, uint64_t hi,
                          uint32_t* out, uint64_t cap, unsigned long long* count_dev, cudaStream_t s);

@@ -416,11 +416,54 @@ cudaError_t launch_tile_start(const uint32_t* block, uint64_t K, int64_t psi, ui
   return cudaGetLastError();
 }
 
+namespace {
+// warp-cooperative lower_bound over an ascending u32 array: 32 probes per round
+__device__ uint32_t warp_lower_bound(const uint32_t* __restrict__ a, uint32_t n, uint32_t key) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = n;   // the answer lies in [lo, hi]
+  while (hi - lo > 32) {
+    const uint32_t span = hi - lo;
+    const uint32_t p = lo + (uint32_t)(((uint64_t)span * (uint32_t)(lane + 1)) / 33u);
+    const bool below = __ldg(a + p) < key;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, below);
+    const int c = __popc(m);   // probes below the key (a prefix of the lanes: a is ascending)
+    const uint32_t nlo = c ? __shfl_sync(0xFFFFFFFFu, p, c - 1) + 1 : lo;
+    const uint32_t nhi = c < 32 ? __shfl_sync(0xFFFFFFFFu, p, c < 32 ? c : 31) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  const uint32_t p = lo + (uint32_t)lane;
+  const bool below = p < hi && __ldg(a + p) < key;
+  return lo + (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, below));
+}
+
+// ranges[2b], ranges[2b+1] = the entries of block b inside tiles [T0, T1) (warp per block)
+__global__ void window_range_kernel(const uint32_t* __restrict__ blocks, int n_blocks, uint64_t stride, uint32_t K,
+                                    int shift, uint32_t T0, uint32_t T1, uint32_t* __restrict__ ranges) {
+  const int b = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (b >= n_blocks) return;
+  const uint32_t* idx = blocks + (uint64_t)b * stride;
+  const uint64_t jlo = (uint64_t)T0 << shift, jhi = (uint64_t)T1 << shift;
+  const uint32_t ea = warp_lower_bound(idx, K, jlo > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)jlo);
+  const uint32_t eb = jhi > 0xFFFFFFFFull ? K : warp_lower_bound(idx, K, (uint32_t)jhi);
+  if ((threadIdx.x & 31) == 0) {
+    ranges[2 * b] = ea;
+    ranges[2 * b + 1] = eb;
+  }
+}
+}  // namespace
+
+// the start table of tiles T0..T1 reading only the entries that fall in them (a window-range search
+// first: a shard's table no longer streams every rank's whole index list)
 cudaError_t launch_tile_window(const uint32_t* blocks, int n_blocks, uint64_t K, int shift, uint32_t T0, uint32_t T1,
-                               uint32_t* start, cudaStream_t s) {
-  const unsigned gx = (unsigned)std::min<uint64_t>((K + 256) / 256, (uint64_t)num_sms2() * 16);
+                               uint32_t* start, uint32_t* ranges, cudaStream_t s) {
+  window_range_kernel<<<(n_blocks * 32 + 127) / 128, 128, 0, s>>>(blocks, n_blocks, 2 * K, (uint32_t)K, shift, T0, T1,
+                                                                   ranges);
+  // entries in the window: ~ K (T1 - T0) / (all tiles) per block; size the grid for the window
+  const uint64_t per = std::max<uint64_t>(1, K);
+  const unsigned gx = (unsigned)std::min<uint64_t>((per + 256) / 256, (uint64_t)num_sms2() * 16);
   tile_start_kernel<<<dim3(gx, (unsigned)n_blocks), 256, 0, s>>>(blocks, n_blocks, 2 * K, (uint32_t)K, shift, T0, T1,
-                                                                  nullptr, start);
+                                                                  ranges, start);
   return cudaGetLastError();
 }
 

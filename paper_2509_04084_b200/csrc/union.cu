@@ -8,13 +8,12 @@
 // the dense gradient (same rank order, same division).  When the ranks' supports overlap the union
 // is smaller than the N fixed-K blocks (0.47 N K at rank correlation 0.9).
 //
-// How: the merge's 8192-element tile grid.  Pass 1 (one CTA per tile in the window): a 8192-bit
-// membership bitmap in shared memory from every rank's entries of the tile (binary-searched start
-// table, as in the merge), popcount inside [lo, hi) -> tile count.  Pass 2 (one CTA): exclusive scan
-// of the tile counts -> output offsets and the total.  Pass 3 (one CTA per tile): the bitmap again
-// plus the rank-order sum in a shared-memory accumulator, a block scan of the per-word popcounts,
-// and every thread writes the members of its 32-element word in index order.
-// HBM: the gathered entries of the window twice (2 x 8 B per entry) + 8 B per union entry.
+// How: the merge's 8192-element tile grid, one CTA per tile of the window, one pass: a 8192-bit
+// membership bitmap and the rank-order sums in shared memory (binary-searched tile-start table, as
+// in the merge), the tile's count inside [lo, hi), its output offset by a decoupled look-back over
+// the preceding tiles, and every thread writes the members of its 32-element word in index order.
+// (A three-kernel version -- count, scan, emit -- read the entries twice: 0.61 ms per GPT-2 XL shard
+// at 8 ranks.)  HBM: 8 B per gathered entry in the window + 8 B per union entry.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,6 +25,7 @@ namespace {
 
 constexpr int kUT = kMergeTile;               // elements per tile
 constexpr int kUWords = kUT / 32;             // bitmap words per tile (= threads per CTA)
+constexpr int kUGroup = 8;                    // ranks whose first entries are loaded together
 static_assert(kUWords == 256, "one bitmap word per thread");
 
 // G = S / N, as the merge (merge_replay.cu): DIV 0 none, 1 power of two (exact scaling), 2 IEEE
@@ -72,106 +72,107 @@ __device__ __forceinline__ uint32_t block_scan256(uint32_t x, uint32_t* sh, uint
   return r;
 }
 
-// membership bitmap of tile t (relative window tile tl) from every rank's entries
-__device__ __forceinline__ void build_bitmap(const uint32_t* __restrict__ gathered, int world, uint64_t K,
-                                             const uint32_t* __restrict__ start, int64_t nt, int64_t tl,
-                                             uint32_t j0, uint32_t* bm) {
-  for (int r = 0; r < world; ++r) {
-    const uint32_t* idx = gathered + (uint64_t)r * 2 * K;
-    const uint32_t* st = start + (uint64_t)r * (nt + 1) + tl;
-    const uint32_t a = __ldg(st), b = __ldg(st + 1);
-    for (uint32_t e = a + threadIdx.x; e < b; e += blockDim.x) {
-      const uint32_t j = __ldg(idx + e) - j0;
-      atomicOr(&bm[j >> 5], 1u << (j & 31));
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256)
-union_count_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const uint32_t* __restrict__ start,
-                   int64_t nt, int64_t t0, uint64_t lo, uint64_t hi, uint32_t* __restrict__ tile_cnt) {
-  __shared__ uint32_t bm[kUWords];
-  __shared__ uint32_t sh[9];
-  const int64_t tl = blockIdx.x;
-  const uint64_t j0 = (uint64_t)(t0 + tl) * kUT;
-  bm[threadIdx.x] = 0u;
-  __syncthreads();
-  build_bitmap(gathered, world, K, start, nt, tl, (uint32_t)j0, bm);
-  __syncthreads();
-  const uint32_t c = __popc(bm[threadIdx.x] & word_mask(j0 + 32u * threadIdx.x, lo, hi));
-  uint32_t tot;
-  block_scan256(c, sh, &tot);
-  if (threadIdx.x == 0) tile_cnt[tl] = tot;
-}
-
-// exclusive scan of nt tile counts by one 1024-thread CTA (thread q owns a contiguous run)
-__global__ void __launch_bounds__(1024)
-union_scan_kernel(const uint32_t* __restrict__ cnt, int64_t nt, uint32_t* __restrict__ off,
-                  unsigned long long* __restrict__ total) {
-  __shared__ uint32_t sh[33];
-  const int64_t per = (nt + 1023) / 1024;
-  const int64_t a0 = (int64_t)threadIdx.x * per, a = a0 < nt ? a0 : nt, b = a + per < nt ? a + per : nt;
-  uint32_t s = 0;
-  for (int64_t i = a; i < b; ++i) s += cnt[i];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t inc = s;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  if (lane == 31) sh[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    const uint32_t v = sh[lane];
-    uint32_t vi = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, vi, o);
-      if (lane >= o) vi += y;
-    }
-    sh[lane] = vi - v;
-    if (lane == 31) sh[32] = vi;
-  }
-  __syncthreads();
-  uint32_t run = sh[wid] + inc - s;
-  for (int64_t i = a; i < b; ++i) {
-    off[i] = run;
-    run += cnt[i];
-  }
-  if (threadIdx.x == 0) *total = sh[32];
-}
+// Single pass (one CTA per tile): membership bitmap and rank-order sums built together -- an
+// element's first rank writes +0 + v, later ranks add (the bitmap says whether the element was
+// already touched; indices are unique within a rank, ranks are separated by barriers), so the
+// 32 KB accumulator needs no zeroing -- then the tile's count, its output offset by a decoupled
+// look-back over the preceding tiles' published counts (warp 0 reads 32 predecessors at a time),
+// and the ordered emit.  One read of the entries, one launch.
 
 template <int DIV>
 __global__ void __launch_bounds__(256)
-union_emit_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const uint32_t* __restrict__ start,
-                  int64_t nt, int64_t t0, uint64_t lo, uint64_t hi, const uint32_t* __restrict__ off, uint64_t cap,
-                  uint32_t* __restrict__ out) {
+union_tile_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const uint32_t* __restrict__ start,
+                  int64_t nt, int64_t t0, uint64_t lo, uint64_t hi, unsigned long long* __restrict__ tile_state,
+                  uint64_t cap, uint32_t* __restrict__ out, unsigned long long* __restrict__ count) {
   __shared__ float acc[kUT];
   __shared__ uint32_t bm[kUWords];
   __shared__ uint32_t sh[9];
+  __shared__ unsigned long long s_excl;
+  const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kValMask = (1ull << 62) - 1;
   const int64_t tl = blockIdx.x;
   const uint64_t j0 = (uint64_t)(t0 + tl) * kUT;
-  float4* acc4 = reinterpret_cast<float4*>(acc);
-  for (int q = threadIdx.x; q < kUT / 4; q += blockDim.x) acc4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int lane = threadIdx.x & 31;
+  __shared__ uint32_t s_a[kUGroup], s_b[kUGroup];
   bm[threadIdx.x] = 0u;
-  __syncthreads();
-  // rank by rank from +0 (the merge's order; indices are unique within a rank)
-  for (int r = 0; r < world; ++r) {
-    const uint32_t* idx = gathered + (uint64_t)r * 2 * K;
-    const uint32_t* val = idx + K;
-    const uint32_t* st = start + (uint64_t)r * (nt + 1) + tl;
-    const uint32_t a = __ldg(st), b = __ldg(st + 1);
-    for (uint32_t e = a + threadIdx.x; e < b; e += blockDim.x) {
-      const uint32_t j = __ldg(idx + e) - (uint32_t)j0;
-      acc[j] = __fadd_rn(acc[j], __uint_as_float(__ldg(val + e)));
-      atomicOr(&bm[j >> 5], 1u << (j & 31));
+  auto add = [&](uint32_t j, float v) {
+    const uint32_t bit = 1u << (j & 31);
+    const bool seen = (bm[j >> 5] & bit) != 0u;   // set by an earlier rank (barrier-ordered)
+    acc[j] = __fadd_rn(seen ? acc[j] : 0.0f, v);
+    if (!seen) atomicOr(&bm[j >> 5], bit);
+  };
+  // ranks in groups of kUGroup: their tile ranges in one round trip, the first round of every rank's
+  // entries in registers in a second, then the rank-ordered adds out of registers
+  for (int r0 = 0; r0 < world; r0 += kUGroup) {
+    const int ng = world - r0 < kUGroup ? world - r0 : kUGroup;
+    if ((int)threadIdx.x < ng) {
+      const uint32_t* st = start + (uint64_t)(r0 + threadIdx.x) * (nt + 1) + tl;
+      s_a[threadIdx.x] = __ldg(st);
+      s_b[threadIdx.x] = __ldg(st + 1);
     }
     __syncthreads();
+    uint32_t pj[kUGroup], pv[kUGroup];
+#pragma unroll
+    for (int g = 0; g < kUGroup; ++g) {
+      pj[g] = 0xFFFFFFFFu;
+      pv[g] = 0u;
+      if (g < ng) {
+        const uint32_t e = s_a[g] + threadIdx.x;
+        if (e < s_b[g]) {
+          const uint32_t* idx = gathered + (uint64_t)(r0 + g) * 2 * K;
+          pj[g] = __ldg(idx + e) - (uint32_t)j0;
+          pv[g] = __ldg(idx + K + e);
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < kUGroup; ++g) {
+      if (g < ng) {
+        if (pj[g] != 0xFFFFFFFFu) add(pj[g], __uint_as_float(pv[g]));
+        const uint32_t* idx = gathered + (uint64_t)(r0 + g) * 2 * K;
+        for (uint32_t e = s_a[g] + blockDim.x + threadIdx.x; e < s_b[g]; e += blockDim.x)
+          add(__ldg(idx + e) - (uint32_t)j0, __uint_as_float(__ldg(idx + K + e)));
+        __syncthreads();
+      }
+    }
   }
   uint32_t word = bm[threadIdx.x] & word_mask(j0 + 32u * threadIdx.x, lo, hi);
   uint32_t tot;
-  uint64_t pos = (uint64_t)off[tl] + block_scan256(__popc(word), sh, &tot);
+  const uint32_t pre = block_scan256(__popc(word), sh, &tot);
+  if (threadIdx.x < 32) {
+    unsigned long long excl = 0;
+    if (tl == 0) {
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(tile_state, kInc | tot);
+      }
+    } else {
+      if (lane == 0) atomicExch(tile_state + tl, kAgg | tot);
+      int64_t p = tl - 1;
+      for (;;) {
+        const int64_t q = p - lane;   // lane 0: the nearest predecessor
+        unsigned long long w = q >= 0 ? *reinterpret_cast<volatile unsigned long long*>(tile_state + q) : kInc;
+        if (__any_sync(0xFFFFFFFFu, (w >> 62) == 0ull)) continue;   // a predecessor has not published yet
+        const unsigned inc = __ballot_sync(0xFFFFFFFFu, (w >> 62) == 2ull);
+        const int stop = inc ? __ffs(inc) - 1 : 31;                 // nearest inclusive prefix
+        unsigned long long v = lane <= stop ? (w & kValMask) : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        excl += v;
+        if (inc) break;
+        p -= 32;
+      }
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(tile_state + tl, kInc | (excl + tot));
+      }
+    }
+    if (lane == 0) {
+      s_excl = excl;
+      if (tl == nt - 1) *count = excl + tot;
+    }
+  }
+  __syncthreads();
+  uint64_t pos = s_excl + pre;
   const float n = (float)world, inv = 1.0f / (float)world;
   while (word) {
     const int bit = __ffs(word) - 1;
@@ -190,7 +191,8 @@ union_emit_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, 
 size_t union_scratch_bytes(int world, uint64_t lo, uint64_t hi) {
   if (hi <= lo) return 0;
   const int64_t t0 = (int64_t)(lo / kUT), nt = (int64_t)((hi - 1) / kUT) - t0 + 1;
-  return ((size_t)world * (nt + 1) + 2 * (size_t)nt) * sizeof(uint32_t);
+  const size_t starts = ((size_t)world * (nt + 1) + 2 * (size_t)world + 1) / 2 * 2;   // + ranges; 8-B aligned
+  return starts * sizeof(uint32_t) + (size_t)nt * sizeof(unsigned long long);
 }
 
 cudaError_t launch_union(lowdiff_ctx* c, int world, bool mean, const uint32_t* gathered, uint64_t lo, uint64_t hi,
@@ -208,20 +210,22 @@ cudaError_t launch_union(lowdiff_ctx* c, int world, bool mean, const uint32_t* g
     c->union_scratch_bytes = need;
   }
   uint32_t* start = static_cast<uint32_t*>(c->union_scratch);
-  uint32_t* cnt = start + (size_t)world * (nt + 1);
-  uint32_t* off = cnt + nt;
+  const size_t starts = ((size_t)world * (nt + 1) + 2 * (size_t)world + 1) / 2 * 2;
+  uint32_t* ranges = start + (size_t)world * (nt + 1);
+  unsigned long long* tile_state = reinterpret_cast<unsigned long long*>(start + starts);
   int h;
   prof_begin(c, "union", s, &h);
-  cudaError_t e = launch_tile_window(gathered, world, K, kMergeTileShift, (uint32_t)t0, (uint32_t)(t0 + nt), start, s);
+  cudaError_t e = launch_tile_window(gathered, world, K, kMergeTileShift, (uint32_t)t0, (uint32_t)(t0 + nt), start,
+                                     ranges, s);
   if (e != cudaSuccess) return e;
-  union_count_kernel<<<(unsigned)nt, kUWords, 0, s>>>(gathered, world, K, start, nt, t0, lo, hi, cnt);
-  union_scan_kernel<<<1, 1024, 0, s>>>(cnt, nt, off, count_dev);
+  e = cudaMemsetAsync(tile_state, 0, (size_t)nt * sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
   const int dm = !mean || world == 1 ? 0 : ((world & (world - 1)) == 0 ? 1 : 2);
-  if (dm == 0) union_emit_kernel<0><<<(unsigned)nt, kUWords, 0, s>>>(gathered, world, K, start, nt, t0, lo, hi, off, cap, out);
-  else if (dm == 1) union_emit_kernel<1><<<(unsigned)nt, kUWords, 0, s>>>(gathered, world, K, start, nt, t0, lo, hi, off, cap, out);
-  else union_emit_kernel<2><<<(unsigned)nt, kUWords, 0, s>>>(gathered, world, K, start, nt, t0, lo, hi, off, cap, out);
+  if (dm == 0) union_tile_kernel<0><<<(unsigned)nt, kUWords, 0, s>>>(gathered, world, K, start, nt, t0, lo, hi, tile_state, cap, out, count_dev);
+  else if (dm == 1) union_tile_kernel<1><<<(unsigned)nt, kUWords, 0, s>>>(gathered, world, K, start, nt, t0, lo, hi, tile_state, cap, out, count_dev);
+  else union_tile_kernel<2><<<(unsigned)nt, kUWords, 0, s>>>(gathered, world, K, start, nt, t0, lo, hi, tile_state, cap, out, count_dev);
   prof_end(c, h, s);
-  c->launches += 4;
+  c->launches += 3;
   return cudaGetLastError();
 }
 
