@@ -124,6 +124,24 @@ def barrier(world):
         dist.barrier()
 
 
+def host_info():
+    """The host the oracle is timed on (model, sockets x cores, SMT, NUMA, nproc)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        txt = open("/proc/cpuinfo").read()
+        models = [ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("model name")]
+        info["model"] = models[0] if models else None
+        info["sockets"] = len({ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("physical id")}) or None
+        cores = {(a, b) for a, b in zip([ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("physical id")],
+                                        [ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("core id")])}
+        info["physical_cores"] = len(cores) or None
+        info["smt"] = (len(models) // len(cores)) if cores else None
+        info["numa_nodes"] = len([d for d in os.listdir("/sys/devices/system/node") if d.startswith("node")])
+    except (OSError, ValueError, ZeroDivisionError):
+        pass
+    return info
+
+
 def workload_config(args, sizes, K, world):
     """The `config` object both arms print (same workload keys)."""
     psi = sum(sizes)
@@ -197,7 +215,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, sizes, sum(ref.k_table(sizes, args.ppm)), args.gpus),
-            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "host": host_info(),
                              "sample": f"{args.workload} layers [{a},{b}) = {psi_s} params per step "
                                        "(compress + exchange + batch serialize, 1 rank)"},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -640,7 +658,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         t_o, sample, (a, b) = oracle_sample(sizes, args.ppm, args.cpu_budget)
-        cpu = {"value": 4 * sum(sample) / t_o / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+        cpu = {"value": 4 * sum(sample) / t_o / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle", "host": host_info(),
                "sample": f"{args.workload} layers [{a},{b}) = {sum(sample)} params, one iteration of compress "
                          f"+ exchange + batch serialize on 1 thread ({t_o:.1f} s)"}
 
