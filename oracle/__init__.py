@@ -14,7 +14,8 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liblowdiff_ref.so")
+# LOWDIFF_REF_LIB: load another build of the oracle (tests/test_oracle_mutants.py loads mutants)
+_LIB_PATH = os.environ.get("LOWDIFF_REF_LIB") or os.path.join(_HERE, "liblowdiff_ref.so")
 
 OK, E_INVALID, E_DIM, E_NUMERIC, E_IO, E_CORRUPT, E_GAP = 0, 1, 2, 3, 6, 7, 8
 SGD, ADAM = 0, 1
@@ -22,7 +23,8 @@ FLAG_EF, FLAG_MEAN = 1, 2
 
 
 def build() -> str:
-    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    if not os.environ.get("LOWDIFF_REF_LIB"):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return _LIB_PATH
 
 
