@@ -133,16 +133,25 @@ struct AdamK { float b1, c1, b2, c2, eps, nz; };   // nz = -0.0f (ieee_fast.cuh:
 // slots: the per-step fixed work (zeroing, entry loops) is amortised over 16 elements per thread
 // (measured 249 -> 214 ms for 100 GPT-2 XL steps against 256 x 2, 357 ms for 512 x 1).
 // MAXW >= min(world, 8): ranks whose first-round entries are prefetched in registers.
-constexpr int kWarpSpan = kReplayTile / (kReplayThreads / 32);
-static_assert(kWarpSpan == 128 * kReplaySlots, "one float4 per lane per slot");
+// SGD keeps only p per element and its step is a couple of operations, so the per-step fixed work
+// dominates: it runs 64 threads x 32 elements per tile instead (100 GPT-2 XL steps 69 -> 53 ms).
+template <int OPT> struct ReplayShape {
+  static constexpr int threads = OPT == LOWDIFF_SGD ? 64 : kReplayThreads;
+  static constexpr int slots = kReplayTile / (4 * threads);        // float4 slots per lane
+  static constexpr int span = kReplayTile / (threads / 32);         // elements per warp
+  static constexpr int minb = OPT == LOWDIFF_SGD ? 2 * LD_REPLAY_MINB : LD_REPLAY_MINB;
+};
 
 template <int OPT, int DIV, int MAXW>
-__global__ void __launch_bounds__(kReplayThreads, MAXW >= 8 ? LD_REPLAY_MINB * 3 / 4 : LD_REPLAY_MINB)
+__global__ void __launch_bounds__(ReplayShape<OPT>::threads,
+                                  MAXW >= 8 ? ReplayShape<OPT>::minb * 3 / 4 : ReplayShape<OPT>::minb)
 replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
               const uint32_t* __restrict__ start, int64_t n_tiles, const float* __restrict__ scal,
               AdamK ak, uint64_t lo, uint64_t hi, int64_t tile0, float* __restrict__ p, float* __restrict__ m,
               float* __restrict__ v) {
   // elements [lo, hi) are replayed; p, m, v hold exactly that range (p[0] is element lo)
+  constexpr int kReplaySlots = ReplayShape<OPT>::slots, kWarpSpan = ReplayShape<OPT>::span;
+  static_assert(kWarpSpan == 128 * kReplaySlots, "one float4 per lane per slot");
   __shared__ __align__(16) float G[kReplayTile];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t t = tile0 + blockIdx.x;
@@ -584,7 +593,8 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
   const unsigned grid = (unsigned)n_tiles;
   const int dm = div_mode(mean, world);
 #define LD_REPLAY(OPT, DIV, W) \
-  replay_kernel<OPT, DIV, W><<<grid, kReplayThreads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, scal_dev, \
+  replay_kernel<OPT, DIV, W><<<grid, ReplayShape<OPT>::threads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, \
+                                                                       scal_dev, \
                                                              ak, lo, hi, tile0, p, m, v)
 #define LD_REPLAY_W(OPT, DIV)                                  \
   do {                                                         \
