@@ -38,7 +38,10 @@ namespace {
 
 constexpr int kH0 = 2048, kH1 = 2048, kH2 = 512;   // digit sizes: key bits [30:20] [19:9] [8:0]
 constexpr int kHistRow = kH0 + kH1 + kH2;
-constexpr int kScanWarps = 4;                       // segments per scan CTA
+#ifndef LD_SCAN_WARPS
+#define LD_SCAN_WARPS 4
+#endif
+constexpr int kScanWarps = LD_SCAN_WARPS;           // segments per scan CTA
 constexpr int kPiecesPerChunk = kSegsPerChunk / kScanWarps;   // 4 scan CTAs per chunk
 constexpr int kJ = 1;                               // float4 per lane per scan round
 constexpr int kUnroll = 4;                          // candidate rounds in flight per warp
@@ -270,7 +273,7 @@ __device__ __forceinline__ float lazy_zero(float rv, uint32_t gidx, uint32_t T, 
 constexpr int kCandBuf = 32 + 32 * 4 * kJ;   // < 32 staged + one round's worst case
 
 template <bool EF, bool REFILL>
-__global__ void __launch_bounds__(kScanWarps * 32, 16)
+__global__ void __launch_bounds__(kScanWarps * 32, 64 / kScanWarps)
 scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int lazy) {
   __shared__ uint64_t sbuf_all[kScanWarps][kCandBuf];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
