@@ -286,6 +286,12 @@ lowdiff_status lowdiff_recover_union(lowdiff_ctx *ctx, int64_t target, float *p,
 lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx *ctx, int64_t iteration, int32_t first_layer,
                                       int32_t n_layers, const float *grad_bucket, void *producer);
 
+/* Sharded snapshots (enable != 0): lowdiff_snapshot_layer copies only this rank's shard
+ *    [floor(rank*Psi/world), floor((rank+1)*Psi/world)) of each bucket -- the part of the synced
+ *    gradient a data-parallel rank has to keep (PCIe bytes per rank / world); the rest of the host
+ *    buffer is not updated.  Always the case while a CPU replica is active. */
+lowdiff_status lowdiff_snapshot_shard(lowdiff_ctx *ctx, int32_t enable);
+
 /* Wait until every layer of `iteration` has been snapshotted; *host_grad = pinned
  *    f32[Psi] valid until iteration + 2 is first snapshotted.  LOWDIFF_E_STATE if some
  *    layer of that iteration was never submitted. */

@@ -1690,9 +1690,13 @@ lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx* c, int64_t iteration, int32_t
   CK(cudaEventRecord(c->ev_tmp, p));
   CK(cudaStreamWaitEvent(c->side, c->ev_tmp, 0));
   const uint64_t lo = c->off[first_layer], hi = c->off[first_layer + n_layers];
-  // with an active replica only its shard of the bucket crosses PCIe (the rest is not read)
-  const uint64_t a = c->rep_active ? std::max(lo, c->rep_sb) : lo;
-  const uint64_t z = c->rep_active ? std::min(hi, c->rep_se) : hi;
+  // with an active replica, or when sharded snapshots are on, only this rank's shard of the bucket
+  // crosses PCIe (the rest is not read)
+  const uint64_t psi = (uint64_t)c->psi, rk = (uint64_t)c->cfg.rank, wd = (uint64_t)c->cfg.world;
+  const bool shard = c->rep_active || c->snap_sharded;
+  const uint64_t sb = c->rep_active ? c->rep_sb : psi * rk / wd, se = c->rep_active ? c->rep_se : psi * (rk + 1) / wd;
+  const uint64_t a = shard ? std::max(lo, sb) : lo;
+  const uint64_t z = shard ? std::min(hi, se) : hi;
   int h;
   ld::prof_begin(c, "snapshot_d2h", c->side, &h);
   if (a < z)
@@ -1724,6 +1728,13 @@ lowdiff_status lowdiff_bucket_plan(int32_t n_layers, const int64_t* numel, int64
     first[n] = 0, count[n] = hi, ++n;
   }
   *n_buckets = n;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_snapshot_shard(lowdiff_ctx* c, int32_t enable) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  c->snap_sharded = enable != 0;
   return LOWDIFF_OK;
 }
 

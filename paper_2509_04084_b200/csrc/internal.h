@@ -198,6 +198,7 @@ struct lowdiff_ctx {
   int64_t snap_iter[2] = {-1, -1};
   std::vector<uint8_t> snap_seen[2];
   cudaEvent_t snap_done[2] = {nullptr, nullptr};
+  bool snap_sharded = false;          // lowdiff_snapshot_shard: copy only this rank's 1/N of each bucket
   // peer-memory exchange (NEXT-1; peer.cu): own slots = send u32[2K] | merge tile starts
   int peer_slots = 0;
   std::vector<uint32_t*> peer_own;

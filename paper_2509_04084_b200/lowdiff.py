@@ -97,6 +97,7 @@ def lib():
             "snapshot_layer": ([P, C.c_int64, C.c_int32, C.c_int32, P, P], S),
             "snapshot_wait": ([P, C.c_int64, C.POINTER(C.c_void_p)], S),
             "bucket_plan": ([C.c_int32, P, C.c_int64, P, P, C.c_int32, C.POINTER(C.c_int32)], S),
+            "snapshot_shard": ([P, C.c_int32], S),
             "union_compact": ([P, C.c_int32, P, C.c_int64, C.c_int64, P, C.c_int64, P, P], S),
             "union_persist": ([P, C.c_int64, C.POINTER(StepScalars), P, P], S),
             "recover_union": ([P, C.c_int64, P, P, P, C.c_int32, C.POINTER(C.c_int64), P], S),
@@ -140,7 +141,7 @@ def lib():
 
 EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_materialize", "exchange", "merge", "exchange_update", "peer_alloc", "ipc_open",
             "peer_set", "exchange_peer", "batch_persist",
-            "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "bucket_plan", "union_compact", "union_persist", "recover_union",
+            "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "snapshot_shard", "bucket_plan", "union_compact", "union_persist", "recover_union",
             "replica_init",
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
             "sync", "get_stats",
@@ -422,6 +423,10 @@ class Context:
     def snapshot_layer(self, iteration, first_layer, n_layers, grad_bucket, stream=None):
         self._c("snapshot_layer", lib().lowdiff_snapshot_layer(self._h, iteration, first_layer, n_layers,
                                                                _ptr(grad_bucket), _stream(stream)))
+
+    def snapshot_shard(self, on=True):
+        """Copy only this rank's 1/world shard of each snapshotted bucket."""
+        self._c("snapshot_shard", lib().lowdiff_snapshot_shard(self._h, int(bool(on))))
 
     def snapshot_wait(self, iteration):
         """Returns a CPU float32 tensor viewing the pinned snapshot buffer (valid until iteration + 2)."""
