@@ -502,6 +502,41 @@ def run_ours(args):
                            "fused_algorithmic_gbs_per_rank": (8 * S + n_rep * 8 * world * K) / (sms_ / 1e3) / 1e9}
         del diffs, p, m, v
 
+    # recovery end to end from files (opt-in, --recovery-files n): Full@0 + n differentials written
+    # by the library, then lowdiff_recover (chain scan, CRC checks, H2D, fused replay) timed by wall
+    # clock; storage + PCIe + replay, reported beside the resident replay (M2)
+    recovery_files = None
+    if args.recovery_files and rank == 0:
+        rdir = tempfile.mkdtemp(prefix="lowdiff_rf_")
+        try:
+            fctx = ld.Context(sizes, density_ppm=args.ppm, ckpt_dir=rdir, batch_size=4, optim=ld.ADAM)
+            pf = torch.randn(psi, device=dev) * 0.02
+            mf, vf = torch.zeros(psi, device=dev), torch.zeros(psi, device=dev)
+            t_w0 = time.perf_counter()
+            fctx.full_ckpt(0, pf, mf, vf)
+            rf = torch.zeros(psi, device=dev)
+            sf = torch.empty(2 * K, dtype=torch.int32, device=dev)
+            for t in range(1, args.recovery_files + 1):
+                fctx.compress(grads[t % 2], rf, sf)
+                fctx.batch_persist(t, scal[t - 1], sf)
+            fctx.sync()
+            t_w = time.perf_counter() - t_w0
+            del rf, sf
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            got = fctx.recover(pf, mf, vf)
+            torch.cuda.synchronize()
+            t_r = time.perf_counter() - t0
+            fbytes = sum(os.path.getsize(os.path.join(rdir, f)) for f in os.listdir(rdir))
+            recovery_files = {"steps": got, "seconds": t_r, "file_bytes": fbytes, "gbs": fbytes / t_r / 1e9,
+                              "write_seconds": t_w,
+                              "note": "lowdiff_recover from Full@0 + the .ldb chain on local storage (wall clock)"}
+            fctx.close()
+            del pf, mf, vf
+        except Exception as exc:   # storage limits on the box: report, do not fail the bench line
+            recovery_files = {"error": str(exc)[:200]}
+        subprocess.run(["rm", "-rf", rdir])
+
     # writer throughput (files, CRC-32C, rename) on this box's storage, reported separately
     writer = None
     if not args.no_writer and rank == 0:
@@ -693,7 +728,7 @@ def run_ours(args):
                        "cuda_graphs": not args.no_graphs},
             "roofline": roofline, "gate_bj5": gate, "kernels": kern, "per_step_ms": spread, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "recovery": recovery, "writer": writer, "full_ckpt": fullck, "update": update,
-            "replica": replica, "snapshot": snapshot, "union": union,
+            "replica": replica, "snapshot": snapshot, "union": union, "recovery_files": recovery_files,
             "spec": {"hits": st["spec_hits"], "misses": st["spec_misses"]}}
     print(json.dumps(line), flush=True)
 
@@ -717,6 +752,8 @@ def main():
     ap.add_argument("--no-update", action="store_true")
     ap.add_argument("--no-snapshot", action="store_true")
     ap.add_argument("--no-union", action="store_true")
+    ap.add_argument("--recovery-files", type=int, default=0,
+                    help="n > 0: also time lowdiff_recover from Full@0 + n differentials on local storage")
     ap.add_argument("--no-graphs", action="store_true", help="plain launches instead of captured CUDA graphs")
     ap.add_argument("--snapshot-reps", type=int, default=20,
                     help="proxy backward: HBM passes over each bucket (20 ~ 38 ms for GPT-2 XL, about the backward "

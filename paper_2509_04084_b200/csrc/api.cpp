@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <thread>
 
 #include "internal.h"
 
@@ -1092,23 +1093,36 @@ static lowdiff_status load_full_shards(lowdiff_ctx* c, const std::vector<std::st
                                        float* p, float* m, float* v, uint32_t* optim, float* consts, uint16_t* flags) {
   const uint32_t world = (uint32_t)c->cfg.world;
   const uint64_t psi = (uint64_t)c->psi;
+  const int threads = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
   for (uint32_t r = sharded ? (uint32_t)c->cfg.rank : 0; r < (sharded ? (uint32_t)c->cfg.rank + 1 : world); ++r) {
-    std::vector<uint8_t> buf;
-    if (!read_all(paths[r], buf)) return fail(c, LOWDIFF_E_IO, "cannot read " + paths[r]);
     const uint64_t sb = psi * r / world, se = psi * (r + 1) / world, S = se - sb;
-    if (buf.size() != 100 + 12 * S || std::memcmp(buf.data(), "LDF1", 4) != 0 ||
-        lowdiff_crc32c(buf.data(), buf.size() - 4) != rd<uint32_t>(buf.data() + buf.size() - 4) ||
-        rd<uint32_t>(buf.data() + 8) != r || rd<uint32_t>(buf.data() + 12) != world ||
-        (int64_t)rd<uint64_t>(buf.data() + 16) != F || rd<uint64_t>(buf.data() + 24) != psi ||
-        rd<uint64_t>(buf.data() + 32) != sb || rd<uint64_t>(buf.data() + 40) != se)
-      return fail(c, LOWDIFF_E_CORRUPT, "corrupt full checkpoint " + paths[r]);
-    *optim = rd<uint32_t>(buf.data() + 48);
-    *flags = rd<uint16_t>(buf.data() + 6);
-    std::memcpy(consts, buf.data() + 64, 20);
-    const float* body = reinterpret_cast<const float*>(buf.data() + 96);
-    CK(cudaMemcpy(p + sb, body, S * 4, cudaMemcpyHostToDevice));
-    if (m) CK(cudaMemcpy(m + sb, body + S, S * 4, cudaMemcpyHostToDevice));
-    if (v) CK(cudaMemcpy(v + sb, body + 2 * S, S * 4, cudaMemcpyHostToDevice));
+    const std::string& path = paths[r];
+    int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+    if (fd < 0) return fail(c, LOWDIFF_E_IO, "cannot read " + path);
+    struct stat stt;
+    uint8_t h[96];
+    uint32_t trailer = 0;
+    const bool ok = fstat(fd, &stt) == 0 && (uint64_t)stt.st_size == 100 + 12 * S &&
+                    ::pread(fd, h, 96, 0) == 96 && ::pread(fd, &trailer, 4, (off_t)(96 + 12 * S)) == 4 &&
+                    std::memcmp(h, "LDF1", 4) == 0 && rd<uint32_t>(h + 8) == r && rd<uint32_t>(h + 12) == world &&
+                    (int64_t)rd<uint64_t>(h + 16) == F && rd<uint64_t>(h + 24) == psi &&
+                    rd<uint64_t>(h + 32) == sb && rd<uint64_t>(h + 40) == se;
+    if (!ok) {
+      ::close(fd);
+      return fail(c, LOWDIFF_E_CORRUPT, "corrupt full checkpoint " + path);
+    }
+    *optim = rd<uint32_t>(h + 48);
+    *flags = rd<uint16_t>(h + 6);
+    std::memcpy(consts, h + 64, 20);
+    // body p | m | v streamed to the device through pinned chunks (read, CRC and H2D overlapped)
+    uint32_t crc_body = 0;
+    std::string err;
+    lowdiff_status st2 = ld::stream_to_device(fd, 96, {{p + sb, 4 * S}, {m ? m + sb : nullptr, 4 * S},
+                                                       {v ? v + sb : nullptr, 4 * S}}, threads, &crc_body, &err);
+    ::close(fd);
+    if (st2) return fail(c, st2, err + " (" + path + ")");
+    const uint32_t crc = ld::crc32c_combine(lowdiff_crc32c(h, 96), crc_body, 12 * S);
+    if (crc != trailer) return fail(c, LOWDIFF_E_CORRUPT, "corrupt full checkpoint " + path + " (CRC)");
   }
   if (*optim == LOWDIFF_ADAM && (!m || !v)) return fail(c, LOWDIFF_E_INVALID, "recover: Adam needs m and v");
   return LOWDIFF_OK;

@@ -17,6 +17,12 @@
 #include <cerrno>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+#include <algorithm>
 
 #include "internal.h"
 
@@ -153,6 +159,115 @@ lowdiff_status write_file_atomic(const std::string& path, const std::vector<std:
     *err = "rename " + tmp + ": " + std::strerror(errno);
     return LOWDIFF_E_IO;
   }
+  return LOWDIFF_OK;
+}
+
+// ---------------------------------------------------------------- CRC-32C combination
+// crc(A || B) from crc(A), crc(B) and |B|: appending |B| zero bytes to A is a linear map over GF(2)
+// on the 32-bit CRC register; it is applied by squaring the one-zero-bit operator (log |B| steps).
+static uint32_t gf2_times(const uint32_t* mat, uint32_t vec) {
+  uint32_t sum = 0;
+  for (int i = 0; vec; ++i, vec >>= 1)
+    if (vec & 1u) sum ^= mat[i];
+  return sum;
+}
+static void gf2_square(uint32_t* sq, const uint32_t* mat) {
+  for (int n = 0; n < 32; ++n) sq[n] = gf2_times(mat, mat[n]);
+}
+uint32_t crc32c_combine(uint32_t crc_a, uint32_t crc_b, uint64_t len_b) {
+  if (len_b == 0) return crc_a;
+  uint32_t even[32], odd[32];
+  odd[0] = 0x82F63B78u;   // one zero bit: the reflected Castagnoli polynomial
+  for (int n = 1; n < 32; ++n) odd[n] = 1u << (n - 1);
+  gf2_square(even, odd);   // two zero bits
+  gf2_square(odd, even);   // four zero bits
+  do {                     // one zero byte = eight zero bits, then doublings
+    gf2_square(even, odd);
+    if (len_b & 1u) crc_a = gf2_times(even, crc_a);
+    len_b >>= 1;
+    if (!len_b) break;
+    gf2_square(odd, even);
+    if (len_b & 1u) crc_a = gf2_times(odd, crc_a);
+    len_b >>= 1;
+  } while (len_b);
+  return crc_a ^ crc_b;
+}
+
+// ---------------------------------------------------------------- streamed file -> device
+// Bytes [off, off + total) of `fd` go to the device segments in order (a NULL segment is read and
+// checksummed but not copied), through pinned chunks: `threads` readers each pread a chunk, take
+// its CRC-32C and copy it H2D on their own stream, so storage, checksum and PCIe overlap.  *crc =
+// CRC-32C of the bytes (standard init/xorout), combined in file order.
+lowdiff_status stream_to_device(int fd, uint64_t off, const std::vector<std::pair<void*, uint64_t>>& segs,
+                                int threads, uint32_t* crc, std::string* err) {
+  uint64_t total = 0;
+  for (auto& sg : segs) total += sg.second;
+  const uint64_t CH = 64ull << 20;
+  const uint64_t n_chunks = (total + CH - 1) / CH;
+  if (n_chunks == 0) { *crc = 0; return LOWDIFF_OK; }
+  threads = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(1, threads), n_chunks));
+  std::vector<uint32_t> crcs(n_chunks, 0u);
+  std::vector<uint8_t*> bufs(threads, nullptr);
+  std::vector<cudaStream_t> streams(threads, nullptr);
+  std::atomic<int> failed{0};
+  std::string first_err;
+  std::mutex emu;
+  auto set_err = [&](const std::string& m) {
+    std::lock_guard<std::mutex> g(emu);
+    if (!failed.exchange(1)) first_err = m;
+  };
+  for (int t = 0; t < threads; ++t) {
+    if (cudaHostAlloc((void**)&bufs[t], CH, cudaHostAllocDefault) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&streams[t], cudaStreamNonBlocking) != cudaSuccess) {
+      set_err("pinned staging for the checkpoint read");
+      break;
+    }
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto worker = [&](int t) {
+    cudaSetDevice(dev);
+    for (uint64_t c = (uint64_t)t; c < n_chunks && !failed.load(); c += (uint64_t)threads) {
+      const uint64_t b0 = c * CH, len = std::min(CH, total - b0);
+      uint64_t got = 0;
+      while (got < len) {
+        const ssize_t r = ::pread(fd, bufs[t] + got, len - got, (off_t)(off + b0 + got));
+        if (r <= 0) { set_err(std::string("read: ") + (r < 0 ? std::strerror(errno) : "unexpected end of file")); return; }
+        got += (uint64_t)r;
+      }
+      crcs[c] = crc32c_update(0xFFFFFFFFu, bufs[t], len) ^ 0xFFFFFFFFu;
+      // copy the chunk into the segments it overlaps
+      uint64_t seg_start = 0;
+      for (auto& sg : segs) {
+        const uint64_t s0 = seg_start, s1 = seg_start + sg.second;
+        seg_start = s1;
+        const uint64_t a = std::max(s0, b0), z = std::min(s1, b0 + len);
+        if (a >= z || !sg.first) continue;
+        if (cudaMemcpyAsync(static_cast<uint8_t*>(sg.first) + (a - s0), bufs[t] + (a - b0), z - a,
+                            cudaMemcpyHostToDevice, streams[t]) != cudaSuccess) {
+          set_err("H2D of a checkpoint chunk");
+          return;
+        }
+      }
+      if (cudaStreamSynchronize(streams[t]) != cudaSuccess) { set_err("H2D of a checkpoint chunk"); return; }
+    }
+  };
+  if (!failed.load()) {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(worker, t);
+    for (auto& th : pool) th.join();
+  }
+  for (int t = 0; t < threads; ++t) {
+    if (streams[t]) cudaStreamDestroy(streams[t]);
+    if (bufs[t]) cudaFreeHost(bufs[t]);
+  }
+  if (failed.load()) {
+    *err = first_err;
+    return LOWDIFF_E_IO;
+  }
+  uint32_t acc = crcs[0];
+  for (uint64_t c = 1; c < n_chunks; ++c) acc = crc32c_combine(acc, crcs[c], std::min(CH, total - c * CH));
+  *crc = acc;
   return LOWDIFF_OK;
 }
 

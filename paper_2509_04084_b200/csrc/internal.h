@@ -307,4 +307,7 @@ void build_prefix(const lowdiff_config& cfg, const std::vector<int64_t>& numel, 
                   int64_t K, std::vector<uint8_t>& out);
 lowdiff_status write_file_atomic(const std::string& path, const std::vector<std::pair<const void*, size_t>>& parts,
                                  bool do_fsync, std::string* err);
+uint32_t crc32c_combine(uint32_t crc_a, uint32_t crc_b, uint64_t len_b);
+lowdiff_status stream_to_device(int fd, uint64_t off, const std::vector<std::pair<void*, uint64_t>>& segs,
+                                int threads, uint32_t* crc, std::string* err);
 }  // namespace ld
