@@ -518,7 +518,7 @@ def run_ours(args):
             sf = torch.empty(2 * K, dtype=torch.int32, device=dev)
             for t in range(1, args.recovery_files + 1):
                 fctx.compress(grads[t % 2], rf, sf)
-                fctx.batch_persist(t, scal[t - 1], sf)
+                fctx.batch_persist(t, ld.derive_step_scalars(t, 1e-3), sf)
             fctx.sync()
             t_w = time.perf_counter() - t_w0
             del rf, sf

@@ -663,6 +663,8 @@ lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
   for (auto e : {c->ev_tmp, c->ev_side_all, c->last_d2h, c->full_done, c->full_staged, c->snap_done[0], c->snap_done[1]})
     if (e) cudaEventDestroy(e);
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  for (auto* b : c->stage.bufs) cudaFreeHost(b);
+  for (auto st : c->stage.streams) cudaStreamDestroy(st);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->aux) cudaStreamDestroy(c->aux);
@@ -1093,7 +1095,6 @@ static lowdiff_status load_full_shards(lowdiff_ctx* c, const std::vector<std::st
                                        float* p, float* m, float* v, uint32_t* optim, float* consts, uint16_t* flags) {
   const uint32_t world = (uint32_t)c->cfg.world;
   const uint64_t psi = (uint64_t)c->psi;
-  const int threads = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
   for (uint32_t r = sharded ? (uint32_t)c->cfg.rank : 0; r < (sharded ? (uint32_t)c->cfg.rank + 1 : world); ++r) {
     const uint64_t sb = psi * r / world, se = psi * (r + 1) / world, S = se - sb;
     const std::string& path = paths[r];
@@ -1118,13 +1119,79 @@ static lowdiff_status load_full_shards(lowdiff_ctx* c, const std::vector<std::st
     uint32_t crc_body = 0;
     std::string err;
     lowdiff_status st2 = ld::stream_to_device(fd, 96, {{p + sb, 4 * S}, {m ? m + sb : nullptr, 4 * S},
-                                                       {v ? v + sb : nullptr, 4 * S}}, threads, &crc_body, &err);
+                                                       {v ? v + sb : nullptr, 4 * S}}, c->stage, &crc_body, &err);
     ::close(fd);
     if (st2) return fail(c, st2, err + " (" + path + ")");
     const uint32_t crc = ld::crc32c_combine(lowdiff_crc32c(h, 96), crc_body, 12 * S);
     if (crc != trailer) return fail(c, LOWDIFF_E_CORRUPT, "corrupt full checkpoint " + path + " (CRC)");
   }
   if (*optim == LOWDIFF_ADAM && (!m || !v)) return fail(c, LOWDIFF_E_INVALID, "recover: Adam needs m and v");
+  return LOWDIFF_OK;
+}
+
+// Differential blocks of steps [t0, t1] of every rank into d_diffs (block of (t, r) at
+// ((t - t0) world + r) 2K), file by file: header fields and block headers read with small preads
+// (scalars kept, ranks must agree), then the whole file streamed through pinned chunks by parallel
+// readers (payloads of the wanted blocks copied H2D, everything checksummed; ld::stream_to_device)
+// and its CRC-32C checked against the trailer.
+static lowdiff_status load_blocks_streamed(lowdiff_ctx* c, const Chain& ch, int64_t t0, int64_t t1, uint32_t optim,
+                                           uint32_t* d_diffs, std::vector<lowdiff_step_scalars>& scal) {
+  const uint32_t world = (uint32_t)c->cfg.world;
+  const uint64_t psi = (uint64_t)c->psi, K = (uint64_t)c->K, L = (uint64_t)c->cfg.n_layers;
+  const size_t pre = 96 + 16 * L, blk = 32 + 8 * K;
+  std::vector<char> have((size_t)(t1 - t0 + 1) * world, 0);
+  for (uint32_t r = 0; r < world; ++r) {
+    std::map<std::string, bool> files;   // the files holding this rank's blocks of [t0, t1]
+    for (int64_t t = t0; t <= t1; ++t) files[ch.where[r].at(t).first] = true;
+    for (auto& fe : files) {
+      const std::string& path = fe.first;
+      int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+      if (fd < 0) return fail(c, LOWDIFF_E_IO, "cannot read " + path);
+      struct stat stt;
+      uint8_t h[64];
+      bool ok = fstat(fd, &stt) == 0 && stt.st_size >= (off_t)(pre + 4) && ::pread(fd, h, 64, 0) == 64;
+      const uint32_t nit = ok ? rd<uint32_t>(h + 24) : 0;
+      ok = ok && (size_t)stt.st_size == pre + (size_t)nit * blk + 4 && std::memcmp(h, "LDB1", 4) == 0 &&
+           rd<uint32_t>(h + 8) == r && rd<uint32_t>(h + 12) == world && rd<uint32_t>(h + 28) == (uint32_t)L &&
+           rd<uint64_t>(h + 32) == psi && rd<uint64_t>(h + 40) == K && rd<uint32_t>(h + 48) == c->cfg.density_ppm &&
+           rd<uint32_t>(h + 52) == optim;
+      const int64_t first = ok ? (int64_t)rd<uint64_t>(h + 16) : 0;
+      std::vector<std::pair<void*, uint64_t>> segs{{nullptr, (uint64_t)pre}};
+      for (uint32_t i = 0; ok && i < nit; ++i) {
+        uint8_t bh[32];
+        ok = ::pread(fd, bh, 32, (off_t)(pre + i * blk)) == 32 && (int64_t)rd<uint64_t>(bh) == first + i;
+        const int64_t t = first + i;
+        void* dst = nullptr;
+        if (ok && t >= t0 && t <= t1 && ch.where[r].at(t).first == path) {
+          lowdiff_step_scalars sc;
+          std::memcpy(&sc, bh + 8, 12);
+          if (r == 0) scal[t - t0] = sc;
+          else if (std::memcmp(&sc, &scal[t - t0], 12) != 0) {
+            ::close(fd);
+            return fail(c, LOWDIFF_E_CORRUPT, "ranks disagree on the scalars of iteration " + std::to_string(t));
+          }
+          dst = d_diffs + ((size_t)(t - t0) * world + r) * 2 * K;
+          have[(size_t)(t - t0) * world + r] = 1;
+        }
+        segs.push_back({nullptr, 32});
+        segs.push_back({dst, 8 * K});
+      }
+      uint32_t trailer = 0;
+      ok = ok && ::pread(fd, &trailer, 4, stt.st_size - 4) == 4;
+      if (!ok) {
+        ::close(fd);
+        return fail(c, LOWDIFF_E_CORRUPT, "corrupt batch file " + path);
+      }
+      uint32_t crc = 0;
+      std::string err;
+      lowdiff_status st = ld::stream_to_device(fd, 0, segs, c->stage, &crc, &err);
+      ::close(fd);
+      if (st) return fail(c, st, err + " (" + path + ")");
+      if (crc != trailer) return fail(c, LOWDIFF_E_CORRUPT, "corrupt batch file " + path + " (CRC)");
+    }
+  }
+  for (char x : have)
+    if (!x) return fail(c, LOWDIFF_E_CORRUPT, "a block of the chain is missing from its file");
   return LOWDIFF_OK;
 }
 
@@ -1170,7 +1237,8 @@ static lowdiff_status recover_impl(lowdiff_ctx* c, int64_t target, float* p, flo
     const int64_t t1 = std::min<int64_t>(ch.last, t0 + chunk - 1);
     scal.assign((size_t)(t1 - t0 + 1), {0, 0, 0});
     ranges.assign((size_t)(t1 - t0 + 1) * world * 2, 0);
-    for (int64_t t = t0; t <= t1 && result == LOWDIFF_OK; ++t) {
+    if (!sharded) result = load_blocks_streamed(c, ch, t0, t1, optim, d_diffs, scal);
+    for (int64_t t = t0; sharded && t <= t1 && result == LOWDIFF_OK; ++t) {
       for (uint32_t r = 0; r < world; ++r) {
         const auto& w = ch.where[r][t];
         auto itc = cache.find(w.first);

@@ -199,16 +199,13 @@ uint32_t crc32c_combine(uint32_t crc_a, uint32_t crc_b, uint64_t len_b) {
 // its CRC-32C and copy it H2D on their own stream, so storage, checksum and PCIe overlap.  *crc =
 // CRC-32C of the bytes (standard init/xorout), combined in file order.
 lowdiff_status stream_to_device(int fd, uint64_t off, const std::vector<std::pair<void*, uint64_t>>& segs,
-                                int threads, uint32_t* crc, std::string* err) {
+                                Staging& stg, uint32_t* crc, std::string* err) {
   uint64_t total = 0;
   for (auto& sg : segs) total += sg.second;
-  const uint64_t CH = 64ull << 20;
+  const uint64_t CH = Staging::kChunk;
   const uint64_t n_chunks = (total + CH - 1) / CH;
   if (n_chunks == 0) { *crc = 0; return LOWDIFF_OK; }
-  threads = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(1, threads), n_chunks));
   std::vector<uint32_t> crcs(n_chunks, 0u);
-  std::vector<uint8_t*> bufs(threads, nullptr);
-  std::vector<cudaStream_t> streams(threads, nullptr);
   std::atomic<int> failed{0};
   std::string first_err;
   std::mutex emu;
@@ -216,13 +213,23 @@ lowdiff_status stream_to_device(int fd, uint64_t off, const std::vector<std::pai
     std::lock_guard<std::mutex> g(emu);
     if (!failed.exchange(1)) first_err = m;
   };
-  for (int t = 0; t < threads; ++t) {
-    if (cudaHostAlloc((void**)&bufs[t], CH, cudaHostAllocDefault) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&streams[t], cudaStreamNonBlocking) != cudaSuccess) {
-      set_err("pinned staging for the checkpoint read");
-      break;
-    }
+  // pinned chunks and streams are allocated once per context and reused (cudaHostAlloc is slow)
+  const int want = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  while ((int)stg.bufs.size() < want) {
+    uint8_t* b = nullptr;
+    cudaStream_t st = nullptr;
+    if (cudaHostAlloc((void**)&b, CH, cudaHostAllocDefault) != cudaSuccess) break;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) { cudaFreeHost(b); break; }
+    stg.bufs.push_back(b);
+    stg.streams.push_back(st);
   }
+  if (stg.bufs.empty()) {
+    *err = "pinned staging for the checkpoint read";
+    return LOWDIFF_E_CUDA;
+  }
+  const int threads = (int)std::min<uint64_t>(stg.bufs.size(), n_chunks);
+  std::vector<uint8_t*>& bufs = stg.bufs;
+  std::vector<cudaStream_t>& streams = stg.streams;
   int dev = 0;
   cudaGetDevice(&dev);
   auto worker = [&](int t) {
@@ -252,14 +259,12 @@ lowdiff_status stream_to_device(int fd, uint64_t off, const std::vector<std::pai
       if (cudaStreamSynchronize(streams[t]) != cudaSuccess) { set_err("H2D of a checkpoint chunk"); return; }
     }
   };
-  if (!failed.load()) {
+  if (threads == 1) {
+    worker(0);
+  } else {
     std::vector<std::thread> pool;
     for (int t = 0; t < threads; ++t) pool.emplace_back(worker, t);
     for (auto& th : pool) th.join();
-  }
-  for (int t = 0; t < threads; ++t) {
-    if (streams[t]) cudaStreamDestroy(streams[t]);
-    if (bufs[t]) cudaFreeHost(bufs[t]);
   }
   if (failed.load()) {
     *err = first_err;

@@ -105,6 +105,12 @@ struct Slot {
 // gradient of `iteration`, 2 = persist the replica as it stands after the preceding items
 struct RepJob { int kind; int64_t iteration; lowdiff_step_scalars sc; };
 struct UJob { int64_t iteration; lowdiff_step_scalars sc; int buf; };
+// pinned chunks + streams of the recovery loader (files.cpp stream_to_device), kept per context
+struct Staging {
+  static constexpr uint64_t kChunk = 64ull << 20;
+  std::vector<uint8_t*> bufs;
+  std::vector<cudaStream_t> streams;
+};
 // a captured CUDA graph of one call's kernels, keyed by the call kind and its buffers
 struct GraphEntry {
   int kind; const void *a, *b, *c; int flag; uint64_t gen;
@@ -198,7 +204,8 @@ struct lowdiff_ctx {
   int64_t snap_iter[2] = {-1, -1};
   std::vector<uint8_t> snap_seen[2];
   cudaEvent_t snap_done[2] = {nullptr, nullptr};
-  bool snap_sharded = false;          // lowdiff_snapshot_shard: copy only this rank's 1/N of each bucket
+  bool snap_sharded = false;
+  ld::Staging stage;                  // recovery loader's pinned chunks          // lowdiff_snapshot_shard: copy only this rank's 1/N of each bucket
   // peer-memory exchange (NEXT-1; peer.cu): own slots = send u32[2K] | merge tile starts
   int peer_slots = 0;
   std::vector<uint32_t*> peer_own;
@@ -309,5 +316,5 @@ lowdiff_status write_file_atomic(const std::string& path, const std::vector<std:
                                  bool do_fsync, std::string* err);
 uint32_t crc32c_combine(uint32_t crc_a, uint32_t crc_b, uint64_t len_b);
 lowdiff_status stream_to_device(int fd, uint64_t off, const std::vector<std::pair<void*, uint64_t>>& segs,
-                                int threads, uint32_t* crc, std::string* err);
+                                Staging& stg, uint32_t* crc, std::string* err);
 }  // namespace ld
