@@ -16,7 +16,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,
     python bench.py --steps 12 --warmup 8 --no-cpu --no-e2e --no-writer --no-replica --no-full --no-snapshot --no-union --replay-steps 10 \
     > $OUT/p_launches.out 2>&1
 tail -2 $OUT/p_launches.out
-for ks in scan_kernel:9 merge1_kernel:4 update_kernel:4 replay_kernel:1 emit_kernel:10 chunk_prep_kernel:9 union_emit_kernel:2; do
+for ks in scan_kernel:9 merge1_kernel:4 update_kernel:4 replay_kernel:1 emit_kernel:10 chunk_prep_kernel:9 union_tile_kernel:2; do
   k=${ks%%:*}; skip=${ks##*:}
   ncu --set full --clock-control none --import-source on -k regex:^$k -s $skip -c 1 -o $OUT/prof_$k $SHORT \
       > $OUT/p_$k.out 2>&1
