@@ -426,7 +426,7 @@ lowdiff_status lowdiff_optimal_config(const lowdiff_sys_params *p, double *f_sta
 lowdiff_status lowdiff_config_step(const lowdiff_sys_params *p, int64_t *fcf, int32_t *batch);
 /* Failure-injection simulator: failures of the N GPUs as a Poisson process of rate
  * N / M over the productive time [0, T) (inter-arrival -log(1 - u) M / N; u from splitmix64 over a
- * counter starting at `seed`, DESIGN.md §4.6), each "software" with probability sw_fraction.
+ * counter starting at `seed`, DESIGN.md §4.9), each "software" with probability sw_fraction.
  * Hardware failure at t: x = t mod (1/f); lost work x mod b; recovery R_F + R_D floor(x / b).
  * Software failure (LowDiff+ replica restore): recovery R_S, no lost work.
  * steady = N (S / W) floor(f T); wasted = lost + recovery + steady (the ledger of Eq. 3, whose

@@ -64,7 +64,7 @@ lowdiff_status lowdiff_config_step(const lowdiff_sys_params* p, int64_t* fcf, in
 // every failure with the wasted time Alg. 1's recovery implies for the configuration (f, b):
 // hardware -> lost work since the last persisted batch + R_F + R_D per persisted batch since the
 // last full checkpoint; software (LowDiff+) -> R_S for restoring the CPU replica.
-// Random numbers: splitmix64 over a counter (DESIGN.md §4.6), inter-arrival then kind per event.
+// Random numbers: splitmix64 over a counter (DESIGN.md §4.9), inter-arrival then kind per event.
 namespace {
 struct SplitMix {
   uint64_t seed, i = 0;
