@@ -184,6 +184,7 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   CK(cudaMemset(P.layer_total, 0, nl * 4));   // then kept zero between calls by layer_scan_kernel
   if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_cut = (uint32_t*)p;
   if ((st = dalloc(c, nl * 4, &p))) return st; P.thr_safe = (uint32_t*)p;
+  if ((st = dalloc(c, (size_t)nc * 8, &p))) return st; P.chunk_state = (unsigned long long*)p;
   CK(cudaMemset(P.thr, 0xFF, nl * 4));   // no speculative band before the first call
   CK(cudaMemset(P.thr_safe, 0xFF, nl * 4));
   CK(cudaMemset(P.sel_T, 0xFF, nl * 4));  // no previous k-th key (no drift estimate yet)

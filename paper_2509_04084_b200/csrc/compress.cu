@@ -23,9 +23,9 @@
 //              prediction.
 //     digits:  two more radix digits over the candidate lists -> exact k-th key T and the number
 //              of ties at T to take (lowest indices first).
-//     count / layer scan / emit: per-chunk counts of key > T and key == T, per-layer exclusive
-//              scans, then a warp per chunk writes its selected entries at their final position
-//              and zeroes residual' there.
+//     count+emit: a warp per chunk counts key > T and key == T, takes its layer offset and the
+//              ties taken before it by a decoupled look-back over the layer's earlier chunks, and
+//              writes its selected entries at their final position (residual' zeroing is lazy).
 //   HBM traffic in the steady state: 12 B/param + ~16 B per candidate (~1.5-2.5 k) + 8 B/entry.
 #include <cuda_runtime.h>
 
@@ -639,12 +639,20 @@ __global__ void __launch_bounds__(256) digit_kernel(DevPlan P, int d) {
   }
 }
 
-// per chunk: #(key > T) and #(key == T)
-__global__ void count_kernel(DevPlan P) {
+// count + layer scan + emit in one kernel (warp per chunk): the chunk's #(key > T) and #(key == T), then a
+// decoupled look-back over the earlier chunks of its layer (their published counts, 32 per round)
+// gives the ties taken before it and its output offset, then the ordered emit (the candidates are
+// read once from DRAM; the emit's second read hits L1/L2).  The layer's first chunk also does the
+// per-layer bookkeeping the layer scan did (sel_T, next thresholds, layer_total reset).
+__global__ void __launch_bounds__(256) count_emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K) {
+  const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
   const int lane = threadIdx.x & 31;
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (ch >= P.n_chunks) return;
-  const uint32_t T = P.sel[P.chunk_slot[ch]].prefix;
+  if (ch >= P.n_chunks) return;   // whole warps
+  const unsigned lt = (1u << lane) - 1u;
+  const int slot = P.chunk_slot[ch];
+  const int c0 = P.large_chunk0[slot];
+  const uint32_t T = P.sel[slot].prefix, need = P.sel[slot].kleft;
   const uint32_t cnt = P.chunk_count[ch];
   const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
   uint32_t gt = 0, eq = 0;
@@ -664,32 +672,38 @@ __global__ void count_kernel(DevPlan P) {
     gt += __shfl_xor_sync(0xFFFFFFFFu, gt, o);
     eq += __shfl_xor_sync(0xFFFFFFFFu, eq, o);
   }
-  if (lane == 0) { P.chunk_gt[ch] = gt; P.chunk_eq[ch] = eq; }
-}
-// per large layer (one CTA): exclusive scans over its chunks; next speculative threshold
-__global__ void __launch_bounds__(1024) layer_scan_kernel(DevPlan P) {
-  __shared__ uint32_t sh32[33];
-  const int slot = blockIdx.x;
-  const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
-  const uint32_t T = P.sel[slot].prefix, need = P.sel[slot].kleft;
-  uint32_t eq_carry = 0, out_carry = 0;
-  for (int cb = c0; cb < c1; cb += blockDim.x) {
-    const int c = cb + threadIdx.x;
-    const uint32_t eq = c < c1 ? P.chunk_eq[c] : 0, gt = c < c1 ? P.chunk_gt[c] : 0;
-    uint32_t tot;
-    const uint32_t eb = eq_carry + block_excl_scan(eq, sh32, &tot);
-    eq_carry += tot;
-    const uint32_t take = eb >= need ? 0u : min(eq, need - eb);
-    const uint32_t o = gt + take;
-    const uint32_t ob = out_carry + block_excl_scan(o, sh32, &tot);
-    out_carry += tot;
-    if (c < c1) {
-      P.chunk_out[c] = ob;
-      P.chunk_take[c] = take;
-      P.chunk_eq[c] = (take > 0 && eb + take == need) ? 1u : 0u;   // holds the layer's last taken tie
+  // per-layer counts < 2^31, so (eq << 31 | gt) words add without carries between the fields
+  const unsigned long long mine = ((unsigned long long)eq << 31) | gt;
+  unsigned long long before = 0;
+  if (ch == c0) {
+    if (lane == 0) atomicExch(P.chunk_state + ch, kInc | mine);
+  } else {
+    if (lane == 0) atomicExch(P.chunk_state + ch, kAgg | mine);
+    int p = ch - 1;
+    for (;;) {
+      const int q = p - lane;   // lane 0: the nearest earlier chunk
+      const unsigned long long w =
+          q >= c0 ? *reinterpret_cast<volatile unsigned long long*>(P.chunk_state + q) : kInc;
+      if (__any_sync(0xFFFFFFFFu, (w >> 62) == 0ull)) continue;   // not published yet
+      const unsigned inc = __ballot_sync(0xFFFFFFFFu, (w >> 62) == 2ull);
+      const int stop = inc ? __ffs(inc) - 1 : 31;
+      unsigned long long v = lane <= stop ? (w & kVal) : 0ull;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+      before += v;
+      if (inc) break;
+      p -= 32;
+    }
+    if (lane == 0) {
+      __threadfence();
+      atomicExch(P.chunk_state + ch, kInc | (before + mine));
     }
   }
-  if (threadIdx.x == 0) {
+  const uint32_t gt_b = (uint32_t)(before & 0x7FFFFFFFull), eq_b = (uint32_t)(before >> 31);
+  const uint32_t take_b = min(eq_b, need);       // ties are taken in chunk order, then index order
+  const uint32_t take = min(eq, need - take_b);
+  const bool last_tie_chunk = take > 0 && take_b + take == need;
+  if (ch == c0 && lane == 0) {
     P.layer_total[slot] = 0;   // zero for the next call's chunk_prep
     P.sel_T[slot] = T;
     // speculative band for the next call: the drift-led threshold (may exceed T)
@@ -699,22 +713,7 @@ __global__ void __launch_bounds__(1024) layer_scan_kernel(DevPlan P) {
     P.thr_safe[slot] = sf;
     P.thr[slot] = max(sf, P.sel[slot].next_thr);
   }
-}
-
-// warp per chunk: ordered emit of the selected candidates; the chunk holding the layer's last
-// taken tie records its index + 1 (sel_cut) for the lazy residual zeroing
-__global__ void emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K) {
-  const int lane = threadIdx.x & 31;
-  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (ch >= P.n_chunks) return;
-  const unsigned lt = (1u << lane) - 1u;
-  const int slot = P.chunk_slot[ch];
-  const uint32_t T = P.sel[slot].prefix;
-  const uint32_t take = P.chunk_take[ch];
-  const bool last_tie_chunk = P.chunk_eq[ch] != 0u;
-  const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + P.chunk_out[ch];
-  const uint32_t cnt = P.chunk_count[ch];
-  const uint64_t* cd = P.cand + (uint64_t)ch * kChunk;
+  const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + gt_b + take_b;
   uint32_t eq_run = 0, out_run = 0;
   for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
     uint64_t v[kUnroll];
@@ -819,6 +818,8 @@ cudaError_t compress_head(lowdiff_ctx* c, const float* grad, float* residual, ui
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(P.counters, 0, 8 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(P.chunk_state, 0, (size_t)P.n_chunks * sizeof(unsigned long long), s);   // look-back
+  if (e != cudaSuccess) return e;
   const int layer_blocks = (P.n_large * 32 + 255) / 256;     // warp per large layer
   const int chunk_blocks = (P.n_chunks + 7) / 8;              // warp per chunk
   const unsigned scan_grid = (unsigned)P.n_chunks * kPiecesPerChunk;   // full grid: no tail loop
@@ -862,15 +863,13 @@ cudaError_t compress_tail(lowdiff_ctx* c, float* residual, uint32_t* send, cudaS
     find_kernel<<<layer_blocks, 256, 0, s>>>(P, 2);
     digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 2);
     find_kernel<<<layer_blocks, 256, 0, s>>>(P, 3);
-    count_kernel<<<chunk_blocks, 256, 0, s>>>(P);
-    layer_scan_kernel<<<P.n_large, 1024, 0, s>>>(P);
     prof_end(c, sel_h, s);
     int h;
     prof_begin(c, "emit", s, &h);
-    emit_kernel<<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K);
+    count_emit_kernel<<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K);
     prof_end(c, h, s);
     if (P.n_small && c->aux && (e = cudaStreamWaitEvent(s, c->ev_join, 0)) != cudaSuccess) return e;   // join
-    c->launches += 7;
+    c->launches += 5;
   }
   c->lazy_residual = ef ? residual : nullptr;   // this call's large-layer selection is now pending
   return cudaGetLastError();

@@ -86,6 +86,7 @@ struct DevPlan {
   uint32_t* refill_list;         // [n_chunks] chunk ids to rescan at the safe threshold (level 1)
   uint32_t* refill_list2;        // [n_chunks] chunk ids to rescan at 0 (level 2)
   uint32_t* thr_safe;            // [n_large] the band without the drift lead
+  unsigned long long* chunk_state;  // [n_chunks] count_emit look-back: status | eq_incl | gt_incl
   uint32_t* counters;            // [0] level-1 refill chunks, [1] spec hits, [2] spec misses,
                                  // [3] candidates of hit layers, [4] level-2 refill chunks
   uint32_t* err;                 // [0] non-finite flag, [1] first bad layer
