@@ -1,6 +1,8 @@
-// C-ABI implementation of liblowdiff: context, NCCL exchange, reuse queue -> pinned ring ->
-// writer thread, full checkpoints, chain scan + recovery, LowDiff+ snapshots.
-// The GPU kernels live in compress.cu and merge_replay.cu.  See include/lowdiff.h.
+// C-ABI implementation of liblowdiff (part 1): context, compress / exchange (NCCL, peer memory,
+// CUDA graphs), reuse queue -> pinned ring -> writer thread, full checkpoints, stats, host writers,
+// and the shared helpers of api_util.h.  Recovery: recover.cpp; union-compacted differentials:
+// union_api.cpp; LowDiff+ snapshot and CPU replica: lowdiff_plus.cpp.  Kernels: *.cu.
+// See include/lowdiff.h.
 #include <dirent.h>
 #include <fcntl.h>
 #include <sys/stat.h>
@@ -14,11 +16,12 @@
 #include <map>
 #include <thread>
 
-#include "internal.h"
+#include "api_util.h"
 
 using ld::DevPlan;
 
-namespace {
+namespace ld {
+namespace api {
 
 int64_t now_ns() {
   return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
@@ -38,11 +41,6 @@ lowdiff_status cuda_fail(lowdiff_ctx* c, cudaError_t e, const char* what) {
   return fail(c, LOWDIFF_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define CK(call)                                          \
-  do {                                                    \
-    cudaError_t e_ = (call);                              \
-    if (e_ != cudaSuccess) return cuda_fail(c, e_, #call); \
-  } while (0)
 
 lowdiff_status entry(lowdiff_ctx* c) {
   if (!c) return LOWDIFF_E_INVALID;
@@ -300,11 +298,6 @@ void writer_loop(lowdiff_ctx* c) {
 }
 
 // ---------------------------------------------------------------- chain scan (recovery)
-struct Chain {
-  int64_t F = -1, last = -1;
-  std::vector<std::string> full_paths;                               // [world]
-  std::vector<std::map<int64_t, std::pair<std::string, uint32_t>>> where;  // rank -> t -> (file, block)
-};
 
 bool parse_name(const char* name, const char* kind, const char* ext, unsigned* rank, long long* it) {
   // ld_<kind>_r%03u_%012lld.<ext>
@@ -342,7 +335,6 @@ bool read_head(const std::string& path, uint8_t* buf, size_t n, size_t* fsize) {
   return ok;
 }
 
-template <class T> T rd(const uint8_t* p) { T v; std::memcpy(&v, p, sizeof v); return v; }
 
 lowdiff_status scan_chain(const lowdiff_config& cfg, int64_t target, Chain* ch, std::string* err) {
   const uint32_t world = (uint32_t)cfg.world;
@@ -399,7 +391,23 @@ lowdiff_status scan_chain(const lowdiff_config& cfg, int64_t target, Chain* ch, 
   return LOWDIFF_OK;
 }
 
-}  // namespace
+lowdiff_status validate_cfg(const lowdiff_config* cfg) {
+  if (!cfg || cfg->n_layers <= 0 || !cfg->numel) return LOWDIFF_E_INVALID;
+  if (cfg->density_ppm < 1 || cfg->density_ppm > 1000000) return LOWDIFF_E_INVALID;
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return LOWDIFF_E_INVALID;
+  if (cfg->optim != LOWDIFF_SGD && cfg->optim != LOWDIFF_ADAM) return LOWDIFF_E_INVALID;
+  uint64_t psi = 0;
+  for (int l = 0; l < cfg->n_layers; ++l) {
+    if (cfg->numel[l] <= 0) return LOWDIFF_E_DIM;
+    psi += (uint64_t)cfg->numel[l];
+  }
+  if (psi >= (1ull << 32)) return LOWDIFF_E_DIM;
+  return LOWDIFF_OK;
+}
+
+}  // namespace api
+}  // namespace ld
+using namespace ld::api;
 
 // ---------------------------------------------------------------- profiling helpers
 namespace ld {
@@ -519,19 +527,6 @@ uint32_t lowdiff_crc32c(const void* data, size_t len) {
   return ld::crc32c_update(0xFFFFFFFFu, data, len) ^ 0xFFFFFFFFu;
 }
 
-static lowdiff_status validate_cfg(const lowdiff_config* cfg) {
-  if (!cfg || cfg->n_layers <= 0 || !cfg->numel) return LOWDIFF_E_INVALID;
-  if (cfg->density_ppm < 1 || cfg->density_ppm > 1000000) return LOWDIFF_E_INVALID;
-  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return LOWDIFF_E_INVALID;
-  if (cfg->optim != LOWDIFF_SGD && cfg->optim != LOWDIFF_ADAM) return LOWDIFF_E_INVALID;
-  uint64_t psi = 0;
-  for (int l = 0; l < cfg->n_layers; ++l) {
-    if (cfg->numel[l] <= 0) return LOWDIFF_E_DIM;
-    psi += (uint64_t)cfg->numel[l];
-  }
-  if (psi >= (1ull << 32)) return LOWDIFF_E_DIM;
-  return LOWDIFF_OK;
-}
 
 lowdiff_status lowdiff_create(const lowdiff_config* cfg, lowdiff_ctx** out) {
   if (!out) return LOWDIFF_E_INVALID;
@@ -588,9 +583,6 @@ lowdiff_status lowdiff_create(const lowdiff_config* cfg, lowdiff_ctx** out) {
   return LOWDIFF_OK;
 }
 
-static void union_drain(lowdiff_ctx* c);
-static void union_shutdown(lowdiff_ctx* c);
-
 lowdiff_status lowdiff_sync(lowdiff_ctx* c) {
   lowdiff_status st = entry(c);
   if (st) return st;
@@ -622,9 +614,6 @@ lowdiff_status lowdiff_sync(lowdiff_ctx* c) {
   }
   return LOWDIFF_OK;
 }
-
-static void replica_drain(lowdiff_ctx* c);
-static void replica_shutdown(lowdiff_ctx* c);
 
 lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
   if (!c) return LOWDIFF_OK;
@@ -1027,999 +1016,6 @@ lowdiff_status lowdiff_full_ckpt(lowdiff_ctx* c, int64_t iteration, const float*
     else { c->files_written += 1; c->bytes_written += (int64_t)(100 + 12 * S); }
     c->writer_ns += now_ns() - t0;
   });
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_replay_range(lowdiff_ctx* c, int32_t optim, int32_t world, int64_t n_steps,
-                                    const uint32_t* diffs, const lowdiff_step_scalars* scalars, int64_t begin,
-                                    int64_t end, float* p, float* m, float* v, void* stream) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if (begin >= 0 && begin == end && end <= c->psi && n_steps >= 0) return LOWDIFF_OK;   // empty range
-  if (world < 1 || n_steps < 0 || (n_steps && (!diffs || !scalars)) || !p ||
-      (optim == LOWDIFF_ADAM && (!m || !v)) || (optim != LOWDIFF_ADAM && optim != LOWDIFF_SGD) || begin < 0 ||
-      end > c->psi || begin > end)
-    return fail(c, LOWDIFF_E_INVALID, "replay: bad argument");
-  if (!n_steps || begin == end) return LOWDIFF_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // per-step scalars to the device (tail of the replay scratch is not reused: own buffer)
-  float* scal_dev = nullptr;
-  CK(cudaMallocAsync((void**)&scal_dev, (size_t)n_steps * 12, s));
-  CK(cudaMemcpyAsync(scal_dev, scalars, (size_t)n_steps * 12, cudaMemcpyHostToDevice, s));
-  const float consts[5] = {c->cfg.adam.beta1, c->cfg.adam.one_minus_beta1, c->cfg.adam.beta2,
-                           c->cfg.adam.one_minus_beta2, c->cfg.adam.eps};
-  cudaError_t e = ld::launch_replay(c, optim, c->cfg.mean != 0, consts, world, n_steps, diffs, scal_dev,
-                                    (uint64_t)begin, (uint64_t)end, nullptr, p, m, v, s);
-  cudaFreeAsync(scal_dev, s);
-  if (e != cudaSuccess) return cuda_fail(c, e, "launch_replay");
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_replay(lowdiff_ctx* c, int32_t optim, int32_t world, int64_t n_steps, const uint32_t* diffs,
-                              const lowdiff_step_scalars* scalars, float* p, float* m, float* v, void* stream) {
-  if (!c) return LOWDIFF_E_INVALID;
-  return lowdiff_replay_range(c, optim, world, n_steps, diffs, scalars, 0, c->psi, p, m, v, stream);
-}
-
-lowdiff_status lowdiff_chain_scan(const lowdiff_config* cfg, int64_t target, int64_t* full_iter, int64_t* last_iter) {
-  if (validate_cfg(cfg) || !cfg->ckpt_dir) return LOWDIFF_E_INVALID;
-  Chain ch;
-  std::string err;
-  lowdiff_status st = scan_chain(*cfg, target, &ch, &err);
-  if (st) return st;
-  if (full_iter) *full_iter = ch.F;
-  if (last_iter) *last_iter = ch.last;
-  return LOWDIFF_OK;
-}
-
-// Every rank's shard [floor(q Psi / N), floor((q+1) Psi / N)) of each non-NULL dst array, broadcast
-// from its owner q (uneven shard sizes: one broadcast per owner, grouped).
-static lowdiff_status bcast_shards(lowdiff_ctx* c, float* dst[3], cudaStream_t s) {
-  ncclResult_t r = ncclGroupStart();
-  const uint64_t psi = (uint64_t)c->psi, W = (uint64_t)c->cfg.world;
-  for (int a = 0; a < 3 && r == ncclSuccess; ++a) {
-    if (!dst[a]) continue;
-    for (uint64_t q = 0; q < W && r == ncclSuccess; ++q) {
-      const uint64_t qb = psi * q / W, qe = psi * (q + 1) / W;
-      r = ncclBroadcast(dst[a] + qb, dst[a] + qb, qe - qb, ncclFloat, (int)q, c->comm, s);
-    }
-  }
-  ncclResult_t r2 = ncclGroupEnd();
-  if (r == ncclSuccess) r = r2;
-  if (r != ncclSuccess) return fail(c, LOWDIFF_E_NCCL, std::string("shard broadcast: ") + ncclGetErrorString(r));
-  return LOWDIFF_OK;
-}
-
-// Full checkpoint F -> p, m, v (every shard, or only this rank's when sharded): size, magic, CRC and
-// header fields verified (else E_CORRUPT); optim, Adam constants and flags from the file.
-static lowdiff_status load_full_shards(lowdiff_ctx* c, const std::vector<std::string>& paths, int64_t F, bool sharded,
-                                       float* p, float* m, float* v, uint32_t* optim, float* consts, uint16_t* flags) {
-  const uint32_t world = (uint32_t)c->cfg.world;
-  const uint64_t psi = (uint64_t)c->psi;
-  for (uint32_t r = sharded ? (uint32_t)c->cfg.rank : 0; r < (sharded ? (uint32_t)c->cfg.rank + 1 : world); ++r) {
-    const uint64_t sb = psi * r / world, se = psi * (r + 1) / world, S = se - sb;
-    const std::string& path = paths[r];
-    int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
-    if (fd < 0) return fail(c, LOWDIFF_E_IO, "cannot read " + path);
-    struct stat stt;
-    uint8_t h[96];
-    uint32_t trailer = 0;
-    const bool ok = fstat(fd, &stt) == 0 && (uint64_t)stt.st_size == 100 + 12 * S &&
-                    ::pread(fd, h, 96, 0) == 96 && ::pread(fd, &trailer, 4, (off_t)(96 + 12 * S)) == 4 &&
-                    std::memcmp(h, "LDF1", 4) == 0 && rd<uint32_t>(h + 8) == r && rd<uint32_t>(h + 12) == world &&
-                    (int64_t)rd<uint64_t>(h + 16) == F && rd<uint64_t>(h + 24) == psi &&
-                    rd<uint64_t>(h + 32) == sb && rd<uint64_t>(h + 40) == se;
-    if (!ok) {
-      ::close(fd);
-      return fail(c, LOWDIFF_E_CORRUPT, "corrupt full checkpoint " + path);
-    }
-    *optim = rd<uint32_t>(h + 48);
-    *flags = rd<uint16_t>(h + 6);
-    std::memcpy(consts, h + 64, 20);
-    // body p | m | v streamed to the device through pinned chunks (read, CRC and H2D overlapped)
-    uint32_t crc_body = 0;
-    std::string err;
-    lowdiff_status st2 = ld::stream_to_device(fd, 96, {{p + sb, 4 * S}, {m ? m + sb : nullptr, 4 * S},
-                                                       {v ? v + sb : nullptr, 4 * S}}, c->stage, &crc_body, &err);
-    ::close(fd);
-    if (st2) return fail(c, st2, err + " (" + path + ")");
-    const uint32_t crc = ld::crc32c_combine(lowdiff_crc32c(h, 96), crc_body, 12 * S);
-    if (crc != trailer) return fail(c, LOWDIFF_E_CORRUPT, "corrupt full checkpoint " + path + " (CRC)");
-  }
-  if (*optim == LOWDIFF_ADAM && (!m || !v)) return fail(c, LOWDIFF_E_INVALID, "recover: Adam needs m and v");
-  return LOWDIFF_OK;
-}
-
-// Differential blocks of steps [t0, t1] of every rank into d_diffs (block of (t, r) at
-// ((t - t0) world + r) 2K), file by file: header fields and block headers read with small preads
-// (scalars kept, ranks must agree), then the whole file streamed through pinned chunks by parallel
-// readers (payloads of the wanted blocks copied H2D, everything checksummed; ld::stream_to_device)
-// and its CRC-32C checked against the trailer.
-static lowdiff_status load_blocks_streamed(lowdiff_ctx* c, const Chain& ch, int64_t t0, int64_t t1, uint32_t optim,
-                                           uint32_t* d_diffs, std::vector<lowdiff_step_scalars>& scal) {
-  const uint32_t world = (uint32_t)c->cfg.world;
-  const uint64_t psi = (uint64_t)c->psi, K = (uint64_t)c->K, L = (uint64_t)c->cfg.n_layers;
-  const size_t pre = 96 + 16 * L, blk = 32 + 8 * K;
-  std::vector<char> have((size_t)(t1 - t0 + 1) * world, 0);
-  for (uint32_t r = 0; r < world; ++r) {
-    std::map<std::string, bool> files;   // the files holding this rank's blocks of [t0, t1]
-    for (int64_t t = t0; t <= t1; ++t) files[ch.where[r].at(t).first] = true;
-    for (auto& fe : files) {
-      const std::string& path = fe.first;
-      int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
-      if (fd < 0) return fail(c, LOWDIFF_E_IO, "cannot read " + path);
-      struct stat stt;
-      uint8_t h[64];
-      bool ok = fstat(fd, &stt) == 0 && stt.st_size >= (off_t)(pre + 4) && ::pread(fd, h, 64, 0) == 64;
-      const uint32_t nit = ok ? rd<uint32_t>(h + 24) : 0;
-      ok = ok && (size_t)stt.st_size == pre + (size_t)nit * blk + 4 && std::memcmp(h, "LDB1", 4) == 0 &&
-           rd<uint32_t>(h + 8) == r && rd<uint32_t>(h + 12) == world && rd<uint32_t>(h + 28) == (uint32_t)L &&
-           rd<uint64_t>(h + 32) == psi && rd<uint64_t>(h + 40) == K && rd<uint32_t>(h + 48) == c->cfg.density_ppm &&
-           rd<uint32_t>(h + 52) == optim;
-      const int64_t first = ok ? (int64_t)rd<uint64_t>(h + 16) : 0;
-      std::vector<std::pair<void*, uint64_t>> segs{{nullptr, (uint64_t)pre}};
-      for (uint32_t i = 0; ok && i < nit; ++i) {
-        uint8_t bh[32];
-        ok = ::pread(fd, bh, 32, (off_t)(pre + i * blk)) == 32 && (int64_t)rd<uint64_t>(bh) == first + i;
-        const int64_t t = first + i;
-        void* dst = nullptr;
-        if (ok && t >= t0 && t <= t1 && ch.where[r].at(t).first == path) {
-          lowdiff_step_scalars sc;
-          std::memcpy(&sc, bh + 8, 12);
-          if (r == 0) scal[t - t0] = sc;
-          else if (std::memcmp(&sc, &scal[t - t0], 12) != 0) {
-            ::close(fd);
-            return fail(c, LOWDIFF_E_CORRUPT, "ranks disagree on the scalars of iteration " + std::to_string(t));
-          }
-          dst = d_diffs + ((size_t)(t - t0) * world + r) * 2 * K;
-          have[(size_t)(t - t0) * world + r] = 1;
-        }
-        segs.push_back({nullptr, 32});
-        segs.push_back({dst, 8 * K});
-      }
-      uint32_t trailer = 0;
-      ok = ok && ::pread(fd, &trailer, 4, stt.st_size - 4) == 4;
-      if (!ok) {
-        ::close(fd);
-        return fail(c, LOWDIFF_E_CORRUPT, "corrupt batch file " + path);
-      }
-      uint32_t crc = 0;
-      std::string err;
-      lowdiff_status st = ld::stream_to_device(fd, 0, segs, c->stage, &crc, &err);
-      ::close(fd);
-      if (st) return fail(c, st, err + " (" + path + ")");
-      if (crc != trailer) return fail(c, LOWDIFF_E_CORRUPT, "corrupt batch file " + path + " (CRC)");
-    }
-  }
-  for (char x : have)
-    if (!x) return fail(c, LOWDIFF_E_CORRUPT, "a block of the chain is missing from its file");
-  return LOWDIFF_OK;
-}
-
-// Recovery of elements [lo, hi): lo = 0, hi = Psi loads every full shard and replays everything;
-// the sharded form (NEXT-2) loads only this rank's .ldf shard and replays only its element range,
-// uploading only the entries of each differential block that fall in it.
-static lowdiff_status recover_impl(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int64_t* recovered,
-                                   void* stream, bool sharded) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if (!c->cfg.ckpt_dir) return fail(c, LOWDIFF_E_INVALID, "recover: no ckpt_dir");
-  if (!p) return fail(c, LOWDIFF_E_INVALID, "recover: NULL p");
-  if ((st = lowdiff_sync(c))) return st;     // our own pending files first
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  Chain ch;
-  std::string err;
-  if ((st = scan_chain(c->cfg, target, &ch, &err))) return fail(c, st, err);
-  const uint32_t world = (uint32_t)c->cfg.world;
-  const uint64_t psi = (uint64_t)c->psi, K = (uint64_t)c->K;
-  const uint64_t lo = sharded ? psi * (uint64_t)c->cfg.rank / world : 0;
-  const uint64_t hi = sharded ? psi * ((uint64_t)c->cfg.rank + 1) / world : psi;
-  // 1. full checkpoint shards -> p, m, v
-  uint32_t optim = 0;
-  float consts[5] = {0, 0, 0, 0, 0};
-  uint16_t flags = 0;
-  if ((st = load_full_shards(c, ch.full_paths, ch.F, sharded, p, m, v, &optim, consts, &flags))) return st;
-  const int64_t n = ch.last - ch.F;
-  // 2. stream the differentials through the fused replay in chunks of steps that fit HBM
-  const size_t step_bytes = (size_t)world * 8 * K;
-  size_t free_b = 0, total_b = 0;
-  CK(cudaMemGetInfo(&free_b, &total_b));
-  const size_t per_step = step_bytes + ld::replay_scratch_bytes(c->psi, (int)world, 1);
-  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)(free_b / 2 / std::max<size_t>(1, per_step))));
-  uint32_t* d_diffs = nullptr;
-  uint32_t* d_ranges = nullptr;
-  std::vector<uint32_t> ranges;
-  if (n > 0) CK(cudaMalloc(&d_diffs, (size_t)chunk * step_bytes));
-  if (n > 0 && sharded) CK(cudaMalloc(&d_ranges, (size_t)chunk * world * 8));
-  std::map<std::string, std::vector<uint8_t>> cache;   // verified batch files in use
-  lowdiff_status result = LOWDIFF_OK;
-  std::vector<lowdiff_step_scalars> scal;
-  for (int64_t t0 = ch.F + 1; t0 <= ch.last && result == LOWDIFF_OK; t0 += chunk) {
-    const int64_t t1 = std::min<int64_t>(ch.last, t0 + chunk - 1);
-    scal.assign((size_t)(t1 - t0 + 1), {0, 0, 0});
-    ranges.assign((size_t)(t1 - t0 + 1) * world * 2, 0);
-    if (!sharded) result = load_blocks_streamed(c, ch, t0, t1, optim, d_diffs, scal);
-    for (int64_t t = t0; sharded && t <= t1 && result == LOWDIFF_OK; ++t) {
-      for (uint32_t r = 0; r < world; ++r) {
-        const auto& w = ch.where[r][t];
-        auto itc = cache.find(w.first);
-        if (itc == cache.end()) {
-          // drop files no longer needed by this rank (iterations are visited in order)
-          for (auto jt = cache.begin(); jt != cache.end();) {
-            bool used = false;
-            for (uint32_t q = 0; q < world && !used; ++q) {
-              auto f = ch.where[q].find(t);
-              used = f != ch.where[q].end() && f->second.first == jt->first;
-            }
-            jt = used ? std::next(jt) : cache.erase(jt);
-          }
-          std::vector<uint8_t> buf;
-          if (!read_all(w.first, buf)) { result = fail(c, LOWDIFF_E_IO, "cannot read " + w.first); break; }
-          const uint32_t nit = buf.size() >= 100 ? rd<uint32_t>(buf.data() + 24) : 0;
-          const size_t want = 100 + 16 * (size_t)c->cfg.n_layers + (size_t)nit * (32 + 8 * K);
-          if (buf.size() != want || std::memcmp(buf.data(), "LDB1", 4) != 0 ||
-              lowdiff_crc32c(buf.data(), buf.size() - 4) != rd<uint32_t>(buf.data() + buf.size() - 4) ||
-              rd<uint32_t>(buf.data() + 8) != r || rd<uint32_t>(buf.data() + 12) != world ||
-              rd<uint32_t>(buf.data() + 28) != (uint32_t)c->cfg.n_layers || rd<uint64_t>(buf.data() + 32) != psi ||
-              rd<uint64_t>(buf.data() + 40) != K || rd<uint32_t>(buf.data() + 48) != c->cfg.density_ppm ||
-              rd<uint32_t>(buf.data() + 52) != optim) {
-            result = fail(c, LOWDIFF_E_CORRUPT, "corrupt batch file " + w.first);
-            break;
-          }
-          itc = cache.emplace(w.first, std::move(buf)).first;
-        }
-        const uint8_t* blk = itc->second.data() + 96 + 16 * (size_t)c->cfg.n_layers + (size_t)w.second * (32 + 8 * K);
-        if ((int64_t)rd<uint64_t>(blk) != t) { result = fail(c, LOWDIFF_E_CORRUPT, "block iteration mismatch"); break; }
-        lowdiff_step_scalars sc;
-        std::memcpy(&sc, blk + 8, 12);
-        if (r == 0) scal[t - t0] = sc;
-        else if (std::memcmp(&sc, &scal[t - t0], 12) != 0) {
-          result = fail(c, LOWDIFF_E_CORRUPT, "ranks disagree on the scalars of iteration " + std::to_string(t));
-          break;
-        }
-        uint32_t* dst = d_diffs + ((size_t)(t - t0) * world + r) * 2 * K;
-        cudaError_t e;
-        if (!sharded) {
-          e = cudaMemcpy(dst, blk + 32, 8 * K, cudaMemcpyHostToDevice);
-        } else {
-          // the block's indices ascend: its entries inside [lo, hi) are one contiguous run [a, b)
-          // (Psi < 2^32, so lo and hi fit the u32 index type)
-          const uint32_t* idx = reinterpret_cast<const uint32_t*>(blk + 32);
-          const uint32_t a = (uint32_t)(std::lower_bound(idx, idx + K, (uint32_t)lo) - idx);
-          const uint32_t b = (uint32_t)(std::lower_bound(idx, idx + K, (uint32_t)hi) - idx);
-          ranges[((size_t)(t - t0) * world + r) * 2] = a;
-          ranges[((size_t)(t - t0) * world + r) * 2 + 1] = b;
-          e = cudaSuccess;
-          if (b > a) e = cudaMemcpy(dst + a, idx + a, (size_t)(b - a) * 4, cudaMemcpyHostToDevice);
-          if (e == cudaSuccess && b > a)
-            e = cudaMemcpy(dst + K + a, idx + K + a, (size_t)(b - a) * 4, cudaMemcpyHostToDevice);
-        }
-        if (e != cudaSuccess) { result = cuda_fail(c, e, "H2D differential"); break; }
-      }
-    }
-    if (result) break;
-    // per-step scalars to the device, then one fused replay launch for the chunk of steps
-    float* scal_dev = nullptr;
-    cudaError_t e2 = cudaMalloc((void**)&scal_dev, scal.size() * 12);
-    if (e2 == cudaSuccess) e2 = cudaMemcpy(scal_dev, scal.data(), scal.size() * 12, cudaMemcpyHostToDevice);
-    if (e2 == cudaSuccess && sharded)
-      e2 = cudaMemcpy(d_ranges, ranges.data(), ranges.size() * 4, cudaMemcpyHostToDevice);
-    if (e2 == cudaSuccess)
-      e2 = ld::launch_replay(c, (int)optim, (flags & 2) != 0, consts, (int)world, t1 - t0 + 1, d_diffs, scal_dev, lo,
-                             hi, sharded ? d_ranges : nullptr, p + lo, m ? m + lo : nullptr, v ? v + lo : nullptr, s);
-    if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(s);
-    if (scal_dev) cudaFree(scal_dev);
-    if (e2 != cudaSuccess) result = cuda_fail(c, e2, "replay");
-  }
-  if (d_diffs) cudaFree(d_diffs);
-  if (d_ranges) cudaFree(d_ranges);
-  if (result) return result;
-  CK(cudaStreamSynchronize(s));
-  if (recovered) *recovered = ch.last;
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_recover(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int64_t* recovered,
-                               void* stream) {
-  return recover_impl(c, target, p, m, v, recovered, stream, false);
-}
-
-lowdiff_status lowdiff_recover_sharded(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int32_t gather,
-                                       int64_t* recovered, void* stream) {
-  lowdiff_status st = recover_impl(c, target, p, m, v, recovered, stream, true);
-  if (st || !gather || c->cfg.world == 1) return st;
-  if (!c->comm) return fail(c, LOWDIFF_E_STATE, "recover_sharded: gather needs an NCCL context");
-  float* dst[3] = {p, m, v};
-  if ((st = bcast_shards(c, dst, static_cast<cudaStream_t>(stream)))) return st;
-  CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
-  return LOWDIFF_OK;
-}
-
-// ---------------------------------------------------------------- union-compacted differentials (NEXT-4)
-// C^U_t: this rank's shard of the synchronised compressed gradient as an index -> value dictionary
-// (R-29; union.cu).  .ldu layout: DESIGN.md §3.
-lowdiff_status lowdiff_union_compact(lowdiff_ctx* c, int32_t world, const uint32_t* gathered, int64_t begin,
-                                     int64_t end, uint32_t* out, int64_t cap, uint64_t* count_dev, void* stream) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if (!gathered || !out || !count_dev || world < 1 || world > 65535)
-    return fail(c, LOWDIFF_E_INVALID, "union_compact: bad argument");
-  if (begin < 0 || end < begin || end > c->psi) return fail(c, LOWDIFF_E_DIM, "union_compact: range outside [0, Psi]");
-  const int64_t worst = std::min<int64_t>((int64_t)world * c->K, end - begin);
-  if (cap < worst) return fail(c, LOWDIFF_E_INVALID, "union_compact: cap below min(world * K, end - begin)");
-  if ((reinterpret_cast<uintptr_t>(out) & 3u) || (reinterpret_cast<uintptr_t>(count_dev) & 7u))
-    return fail(c, LOWDIFF_E_INVALID, "union_compact: misaligned buffer");
-  CK(ld::launch_union(c, world, c->cfg.mean != 0, gathered, (uint64_t)begin, (uint64_t)end, out, (uint64_t)cap,
-                      reinterpret_cast<unsigned long long*>(count_dev), static_cast<cudaStream_t>(stream)));
-  return LOWDIFF_OK;
-}
-
-struct UBlock { int64_t it; lowdiff_step_scalars sc; std::vector<uint32_t> data; uint64_t n; };   // idx[n] | val[n]
-
-static std::string union_name(const std::string& dir, int rank, int64_t first) {
-  char buf[64];
-  std::snprintf(buf, sizeof buf, "/ld_union_r%03d_%012lld.ldu", rank, (long long)first);
-  return dir + buf;
-}
-
-// 80-byte header + hyper (32 B) + layer table (16 B per layer) of a .ldu file
-static std::vector<uint8_t> ldu_prefix(const lowdiff_ctx* c, int64_t first, uint32_t n_iters) {
-  std::vector<uint8_t> b(112 + 16 * (size_t)c->cfg.n_layers, 0);
-  const uint16_t ver = 1, flags = (uint16_t)((c->cfg.error_feedback ? 1 : 0) | (c->cfg.mean ? 2 : 0));
-  const uint32_t rk = (uint32_t)c->cfg.rank, wd = (uint32_t)c->cfg.world, nl = (uint32_t)c->cfg.n_layers;
-  const uint32_t ppm = c->cfg.density_ppm, opt = (uint32_t)c->cfg.optim;
-  const uint64_t psi = (uint64_t)c->psi, K = (uint64_t)c->K, sb = psi * rk / wd, se = psi * (rk + 1) / wd;
-  const uint64_t fi = (uint64_t)first;
-  std::memcpy(b.data(), "LDU1", 4);
-  std::memcpy(b.data() + 4, &ver, 2);
-  std::memcpy(b.data() + 6, &flags, 2);
-  std::memcpy(b.data() + 8, &rk, 4);
-  std::memcpy(b.data() + 12, &wd, 4);
-  std::memcpy(b.data() + 16, &fi, 8);
-  std::memcpy(b.data() + 24, &n_iters, 4);
-  std::memcpy(b.data() + 28, &nl, 4);
-  std::memcpy(b.data() + 32, &psi, 8);
-  std::memcpy(b.data() + 40, &K, 8);
-  std::memcpy(b.data() + 48, &ppm, 4);
-  std::memcpy(b.data() + 52, &opt, 4);
-  std::memcpy(b.data() + 56, &sb, 8);
-  std::memcpy(b.data() + 64, &se, 8);
-  std::memcpy(b.data() + 80, &c->cfg.adam, 20);
-  for (int l = 0; l < c->cfg.n_layers; ++l) {
-    const uint64_t n = (uint64_t)c->numel[l];
-    const uint32_t k = c->k[l];
-    std::memcpy(b.data() + 112 + 16 * (size_t)l, &n, 8);
-    std::memcpy(b.data() + 120 + 16 * (size_t)l, &k, 4);
-  }
-  return b;
-}
-
-static void union_write(lowdiff_ctx* c, std::vector<UBlock>& batch) {
-  if (batch.empty()) return;
-  if (c->cfg.ckpt_dir) {
-    const int64_t t0 = now_ns();
-    const std::vector<uint8_t> pre = ldu_prefix(c, batch[0].it, (uint32_t)batch.size());
-    std::vector<std::array<uint8_t, 32>> heads(batch.size());
-    std::vector<std::pair<const void*, size_t>> parts{{pre.data(), pre.size()}};
-    for (size_t i = 0; i < batch.size(); ++i) {
-      auto& h = heads[i];
-      h.fill(0);
-      const uint64_t it = (uint64_t)batch[i].it;
-      const uint32_t n = (uint32_t)batch[i].n;
-      std::memcpy(h.data(), &it, 8);
-      std::memcpy(h.data() + 8, &batch[i].sc, 12);
-      std::memcpy(h.data() + 20, &n, 4);
-      parts.push_back({h.data(), 32});
-      if (n) parts.push_back({batch[i].data.data(), 8 * (size_t)n});
-    }
-    uint32_t crc = 0xFFFFFFFFu;
-    size_t bytes = 4;
-    for (auto& q : parts) {
-      crc = ld::crc32c_update(crc, q.first, q.second);
-      bytes += q.second;
-    }
-    crc ^= 0xFFFFFFFFu;
-    parts.push_back({&crc, 4});
-    std::string err;
-    lowdiff_status st = ld::write_file_atomic(union_name(c->ckpt_dir, c->cfg.rank, batch[0].it), parts,
-                                              c->cfg.fsync != 0, &err);
-    if (st) set_deferred(c, st, err);
-    else { c->u_files += 1; c->u_bytes += (int64_t)bytes; }
-    c->writer_ns += now_ns() - t0;
-  }
-  batch.clear();
-}
-
-static void union_loop(lowdiff_ctx* c) {
-  cudaSetDevice(c->device);
-  std::vector<UBlock> batch;
-  for (;;) {
-    ld::UJob j{};
-    bool have = false, flush = false;
-    {
-      std::unique_lock<std::mutex> lk(c->u_mu);
-      c->u_cv.wait(lk, [&] { return c->u_stop || c->u_flush || !c->u_q.empty(); });
-      if (!c->u_q.empty()) {
-        j = c->u_q.front();
-        c->u_q.pop_front();
-        have = true;
-      } else if (c->u_flush) {
-        flush = true;
-      }
-      c->u_busy = 1;
-    }
-    if (have) {
-      UBlock B{j.iteration, j.sc, {}, 0};
-      cudaError_t e = cudaEventSynchronize(c->u_ready[j.buf]);
-      bool bad = false;
-      if (e == cudaSuccess) {
-        const unsigned long long n = c->u_cnt_host[2 * j.buf];
-        const uint32_t errc = (uint32_t)c->u_cnt_host[2 * j.buf + 1];
-        if (errc > c->u_err_seen) {   // a non-finite accumulated gradient reached this iteration
-          c->u_err_seen = errc;
-          bad = true;
-        } else {
-          B.n = n;
-          B.data.resize(2 * (size_t)n);
-          if (n) {
-            e = cudaMemcpyAsync(B.data.data(), c->u_buf[j.buf], 4 * (size_t)n, cudaMemcpyDeviceToHost, c->u_stream);
-            if (e == cudaSuccess)
-              e = cudaMemcpyAsync(B.data.data() + n, c->u_buf[j.buf] + c->u_cap, 4 * (size_t)n, cudaMemcpyDeviceToHost,
-                                  c->u_stream);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(c->u_stream);
-          }
-        }
-      }
-      {
-        std::lock_guard<std::mutex> g(c->u_mu);
-        c->u_inuse[j.buf] = false;
-        c->u_cv_free.notify_all();
-      }
-      if (e != cudaSuccess || bad) {
-        set_deferred(c, e != cudaSuccess ? LOWDIFF_E_CUDA : LOWDIFF_E_NUMERIC,
-                     e != cudaSuccess ? std::string("union differential copy: ") + cudaGetErrorString(e)
-                                      : "non-finite accumulated gradient before union iteration " +
-                                            std::to_string(j.iteration));
-        union_write(c, batch);   // the chain stops before this iteration
-      } else {
-        c->u_entries += (int64_t)B.n;
-        batch.push_back(std::move(B));
-        if ((int)batch.size() == c->b) union_write(c, batch);
-      }
-    } else if (flush) {
-      union_write(c, batch);
-      std::lock_guard<std::mutex> g(c->u_mu);
-      c->u_flush = false;
-    } else {
-      union_write(c, batch);
-      std::lock_guard<std::mutex> g(c->u_mu);
-      c->u_busy = 0;
-      c->u_cv_idle.notify_all();
-      return;
-    }
-    std::lock_guard<std::mutex> g(c->u_mu);
-    c->u_busy = 0;
-    c->u_cv_idle.notify_all();
-  }
-}
-
-// drain queued union blocks and write the partial batch (lowdiff_sync)
-static void union_drain(lowdiff_ctx* c) {
-  if (!c->u_writer.joinable()) return;
-  std::unique_lock<std::mutex> lk(c->u_mu);
-  c->u_flush = true;
-  c->u_cv.notify_all();
-  c->u_cv_idle.wait(lk, [&] { return c->u_q.empty() && !c->u_flush && !c->u_busy; });
-}
-
-static void union_shutdown(lowdiff_ctx* c) {
-  if (c->u_writer.joinable()) {
-    {
-      std::lock_guard<std::mutex> g(c->u_mu);
-      c->u_stop = true;
-      c->u_cv.notify_all();
-    }
-    c->u_writer.join();
-  }
-  for (auto*& b : c->u_buf) if (b) { cudaFree(b); b = nullptr; }
-  if (c->u_cnt_dev) cudaFree(c->u_cnt_dev);
-  if (c->u_cnt_host) cudaFreeHost(c->u_cnt_host);
-  for (auto e : c->u_ready) if (e) cudaEventDestroy(e);
-  if (c->u_stream) cudaStreamDestroy(c->u_stream);
-  if (c->union_scratch) cudaFree(c->union_scratch);
-}
-
-lowdiff_status lowdiff_union_persist(lowdiff_ctx* c, int64_t iteration, const lowdiff_step_scalars* scalars,
-                                     const uint32_t* gathered, void* producer) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if ((st = take_deferred(c))) return st;
-  if (!scalars || !gathered) return fail(c, LOWDIFF_E_INVALID, "union_persist: NULL argument");
-  if (c->u_next_iter >= 0 && iteration != c->u_next_iter)
-    return fail(c, LOWDIFF_E_STATE, "union_persist: iteration " + std::to_string(iteration) + " after " +
-                                        std::to_string(c->u_next_iter - 1) + " (must be consecutive)");
-  const uint64_t psi = (uint64_t)c->psi, rk = (uint64_t)c->cfg.rank, wd = (uint64_t)c->cfg.world;
-  const uint64_t sb = psi * rk / wd, se = psi * (rk + 1) / wd;
-  if (!c->u_buf[0]) {   // first call: buffers sized for the worst case min(N K, shard)
-    c->u_cap = std::max<uint64_t>(1, std::min<uint64_t>(wd * (uint64_t)c->K, se - sb));
-    for (auto*& b : c->u_buf) CK(cudaMalloc((void**)&b, 2 * c->u_cap * 4));
-    CK(cudaMalloc((void**)&c->u_cnt_dev, 2 * sizeof(unsigned long long)));
-    CK(cudaHostAlloc((void**)&c->u_cnt_host, 4 * sizeof(unsigned long long), cudaHostAllocDefault));
-    for (auto& e : c->u_ready) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CK(cudaStreamCreateWithFlags(&c->u_stream, cudaStreamNonBlocking));
-    c->u_err_seen = c->err_seen.load();
-    c->u_writer = std::thread(union_loop, c);
-  }
-  const int buf = (int)(iteration & 1);
-  {
-    std::unique_lock<std::mutex> lk(c->u_mu);
-    if (c->u_inuse[buf]) {   // the writer still copies iteration - 2 out of this buffer
-      const int64_t t0 = now_ns();
-      c->u_cv_free.wait(lk, [&] { return !c->u_inuse[buf]; });
-      c->stall_ns += now_ns() - t0;
-    }
-    c->u_inuse[buf] = true;
-  }
-  cudaStream_t s = static_cast<cudaStream_t>(producer);
-  c->u_cnt_host[2 * buf] = 0;
-  c->u_cnt_host[2 * buf + 1] = 0;
-  CK(ld::launch_union(c, c->cfg.world, c->cfg.mean != 0, gathered, sb, se, c->u_buf[buf], c->u_cap, c->u_cnt_dev + buf, s));
-  CK(cudaMemcpyAsync(&c->u_cnt_host[2 * buf], c->u_cnt_dev + buf, 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(&c->u_cnt_host[2 * buf + 1], c->plan.err, 4, cudaMemcpyDeviceToHost, s));
-  CK(cudaEventRecord(c->u_ready[buf], s));
-  c->u_next_iter = iteration + 1;
-  {
-    std::lock_guard<std::mutex> g(c->u_mu);
-    c->u_q.push_back(ld::UJob{iteration, *scalars, buf});
-    c->u_cv.notify_all();
-  }
-  return LOWDIFF_OK;
-}
-
-// recovery from .ldf + .ldu: the chain rules of lowdiff_recover; the replay is the fused kernel with
-// one "rank" per step (the union is already merged and divided: sum mode, G = +0 + value)
-static lowdiff_status union_recover_impl(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v,
-                                         bool sharded, int64_t* recovered, void* stream) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if (!c->cfg.ckpt_dir) return fail(c, LOWDIFF_E_INVALID, "recover_union: no ckpt_dir");
-  if (!p) return fail(c, LOWDIFF_E_INVALID, "recover_union: NULL p");
-  if ((st = lowdiff_sync(c))) return st;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const uint32_t world = (uint32_t)c->cfg.world;
-  const uint64_t psi = (uint64_t)c->psi, K = (uint64_t)c->K;
-  std::map<int64_t, std::map<uint32_t, std::string>> fulls;
-  std::vector<std::map<int64_t, std::string>> diffs(world);
-  DIR* d = opendir(c->cfg.ckpt_dir);
-  if (!d) return fail(c, LOWDIFF_E_IO, std::string("cannot open ") + c->cfg.ckpt_dir);
-  while (dirent* de = readdir(d)) {
-    unsigned r;
-    long long it;
-    if (parse_name(de->d_name, "full", "ldf", &r, &it) && r < world)
-      fulls[it][r] = std::string(c->cfg.ckpt_dir) + "/" + de->d_name;
-    else if (parse_name(de->d_name, "union", "ldu", &r, &it) && r < world)
-      diffs[r][it] = std::string(c->cfg.ckpt_dir) + "/" + de->d_name;
-  }
-  closedir(d);
-  int64_t F = -1;
-  std::vector<std::string> full_paths;
-  for (auto it = fulls.rbegin(); it != fulls.rend(); ++it) {
-    if (target >= 0 && it->first > target) continue;
-    if (it->second.size() == world) {
-      F = it->first;
-      for (uint32_t r = 0; r < world; ++r) full_paths.push_back(it->second[r]);
-      break;
-    }
-  }
-  if (F < 0) return fail(c, LOWDIFF_E_GAP, "no complete full checkpoint <= target");
-  uint32_t optim = 0;
-  float consts[5] = {0, 0, 0, 0, 0};
-  uint16_t flags = 0;
-  if ((st = load_full_shards(c, full_paths, F, sharded, p, m, v, &optim, consts, &flags))) return st;
-  // index every needed rank's .ldu files: iteration -> (file, byte offset of its block, count);
-  // files are verified (magic, CRC, header fields, block walk) when indexed
-  const uint32_t r0 = sharded ? (uint32_t)c->cfg.rank : 0, r1 = sharded ? (uint32_t)c->cfg.rank + 1 : world;
-  struct Where { std::string path; size_t off; uint64_t n; };
-  std::vector<std::map<int64_t, Where>> where(world);
-  for (uint32_t r = r0; r < r1; ++r) {
-    for (auto& fe : diffs[r]) {   // ascending first iteration: later files win
-      std::vector<uint8_t> buf;
-      if (!read_all(fe.second, buf)) return fail(c, LOWDIFF_E_IO, "cannot read " + fe.second);
-      const size_t L = (size_t)c->cfg.n_layers;
-      if (buf.size() < 116 + 16 * L || std::memcmp(buf.data(), "LDU1", 4) != 0 ||
-          lowdiff_crc32c(buf.data(), buf.size() - 4) != rd<uint32_t>(buf.data() + buf.size() - 4) ||
-          rd<uint32_t>(buf.data() + 8) != r || rd<uint32_t>(buf.data() + 12) != world ||
-          rd<uint32_t>(buf.data() + 28) != (uint32_t)L || rd<uint64_t>(buf.data() + 32) != psi ||
-          rd<uint64_t>(buf.data() + 40) != K || rd<uint32_t>(buf.data() + 48) != c->cfg.density_ppm ||
-          rd<uint32_t>(buf.data() + 52) != optim || rd<uint64_t>(buf.data() + 56) != psi * r / world ||
-          rd<uint64_t>(buf.data() + 64) != psi * (r + 1) / world)
-        return fail(c, LOWDIFF_E_CORRUPT, "corrupt union file " + fe.second);
-      const uint32_t n_it = rd<uint32_t>(buf.data() + 24);
-      size_t off = 112 + 16 * L;
-      for (uint32_t i = 0; i < n_it; ++i) {
-        if (off + 32 > buf.size() - 4 || (int64_t)rd<uint64_t>(buf.data() + off) != fe.first + i)
-          return fail(c, LOWDIFF_E_CORRUPT, "corrupt union file " + fe.second);
-        const uint64_t n = rd<uint32_t>(buf.data() + off + 20);
-        where[r][fe.first + i] = Where{fe.second, off, n};
-        off += 32 + 8 * n;
-      }
-      if (off != buf.size() - 4) return fail(c, LOWDIFF_E_CORRUPT, "corrupt union file " + fe.second);
-    }
-  }
-  int64_t last = F;
-  for (;;) {
-    const int64_t t = last + 1;
-    if (target >= 0 && t > target) break;
-    bool all = true;
-    for (uint32_t r = r0; r < r1 && all; ++r) all = where[r].count(t) > 0;
-    if (!all) break;
-    last = t;
-  }
-  if (target >= 0 && last < target) return fail(c, LOWDIFF_E_GAP, "union chain has a gap after " + std::to_string(last));
-  const uint64_t lo = sharded ? psi * c->cfg.rank / world : 0, hi = sharded ? psi * (c->cfg.rank + 1) / world : psi;
-  // replay in chunks of steps: block of step t = idx[Kc] | val[Kc], entries [0, U_t) valid
-  size_t free_b = 0, total_b = 0;
-  CK(cudaMemGetInfo(&free_b, &total_b));
-  std::map<std::string, std::vector<uint8_t>> cache;
-  lowdiff_status result = LOWDIFF_OK;
-  for (int64_t t0 = F + 1; t0 <= last && result == LOWDIFF_OK;) {
-    // grow the chunk while its padded size stays within a quarter of free memory
-    uint64_t Kc = 1;
-    int64_t t1 = t0;
-    for (int64_t t = t0; t <= last; ++t) {
-      uint64_t U = 0;
-      for (uint32_t r = r0; r < r1; ++r) U += where[r][t].n;
-      const uint64_t k2 = std::max<uint64_t>(Kc, U);
-      if (t > t0 && (uint64_t)(t - t0 + 1) * 8 * k2 > free_b / 4) break;
-      Kc = k2;
-      t1 = t;
-    }
-    const int64_t ns = t1 - t0 + 1;
-    std::vector<uint32_t> host((size_t)ns * 2 * Kc, 0u), ranges((size_t)ns * 2, 0u);
-    std::vector<lowdiff_step_scalars> scal((size_t)ns);
-    for (int64_t t = t0; t <= t1 && result == LOWDIFF_OK; ++t) {
-      uint64_t at = 0;
-      for (uint32_t r = r0; r < r1; ++r) {
-        const Where& w = where[r][t];
-        auto itc = cache.find(w.path);
-        if (itc == cache.end()) {
-          for (auto jt = cache.begin(); jt != cache.end();) {   // drop files this step no longer uses
-            bool used = false;
-            for (uint32_t q = r0; q < r1 && !used; ++q) used = where[q][t].path == jt->first;
-            jt = used ? std::next(jt) : cache.erase(jt);
-          }
-          std::vector<uint8_t> buf;
-          if (!read_all(w.path, buf)) { result = fail(c, LOWDIFF_E_IO, "cannot read " + w.path); break; }
-          itc = cache.emplace(w.path, std::move(buf)).first;
-        }
-        const uint8_t* blk = itc->second.data() + w.off;
-        lowdiff_step_scalars sc;
-        std::memcpy(&sc, blk + 8, 12);
-        if (r == r0) scal[t - t0] = sc;
-        else if (std::memcmp(&sc, &scal[t - t0], 12) != 0) {
-          result = fail(c, LOWDIFF_E_CORRUPT, "ranks disagree on the scalars of iteration " + std::to_string(t));
-          break;
-        }
-        const uint64_t sbr = psi * r / world, ser = psi * (r + 1) / world;
-        const uint32_t* idx = reinterpret_cast<const uint32_t*>(blk + 32);
-        for (uint64_t e = 0; e < w.n; ++e)
-          if (idx[e] < sbr || idx[e] >= ser || (e && idx[e] <= idx[e - 1])) {
-            result = fail(c, LOWDIFF_E_CORRUPT, "union entries outside their shard or not ascending in " + w.path);
-            break;
-          }
-        if (result) break;
-        uint32_t* dst = host.data() + (size_t)(t - t0) * 2 * Kc;
-        std::memcpy(dst + at, idx, 4 * w.n);
-        std::memcpy(dst + Kc + at, idx + w.n, 4 * w.n);
-        at += w.n;
-      }
-      ranges[2 * (size_t)(t - t0) + 1] = (uint32_t)at;
-    }
-    if (result) break;
-    uint32_t* d_diffs = nullptr;
-    uint32_t* d_ranges = nullptr;
-    float* scal_dev = nullptr;
-    cudaError_t e = cudaMalloc((void**)&d_diffs, host.size() * 4);
-    if (e == cudaSuccess) e = cudaMalloc((void**)&d_ranges, ranges.size() * 4);
-    if (e == cudaSuccess) e = cudaMalloc((void**)&scal_dev, scal.size() * 12);
-    if (e == cudaSuccess) e = cudaMemcpy(d_diffs, host.data(), host.size() * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d_ranges, ranges.data(), ranges.size() * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(scal_dev, scal.data(), scal.size() * 12, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-      e = ld::launch_replay(c, (int)optim, false, consts, 1, ns, d_diffs, scal_dev, lo, hi, d_ranges, p + lo,
-                            m ? m + lo : nullptr, v ? v + lo : nullptr, s, Kc);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (d_diffs) cudaFree(d_diffs);
-    if (d_ranges) cudaFree(d_ranges);
-    if (scal_dev) cudaFree(scal_dev);
-    if (e != cudaSuccess) result = cuda_fail(c, e, "union replay");
-    t0 = t1 + 1;
-  }
-  if (result) return result;
-  if (recovered) *recovered = last;
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_recover_union(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int32_t sharded,
-                                     int64_t* recovered, void* stream) {
-  return union_recover_impl(c, target, p, m, v, sharded != 0, recovered, stream);
-}
-
-lowdiff_status lowdiff_snapshot_layer(lowdiff_ctx* c, int64_t iteration, int32_t first_layer, int32_t n_layers,
-                                      const float* grad_bucket, void* producer) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if (!grad_bucket || first_layer < 0 || n_layers < 1 || first_layer + n_layers > c->cfg.n_layers || iteration < 0)
-    return fail(c, LOWDIFF_E_INVALID, "snapshot_layer: bad argument");
-  const int buf = (int)(iteration & 1);
-  if (!c->snap_host[buf]) {
-    CK(cudaHostAlloc((void**)&c->snap_host[buf], (size_t)c->psi * 4, cudaHostAllocDefault));
-  }
-  if (c->snap_iter[buf] != iteration) {
-    const int64_t old = c->snap_iter[buf];
-    if (c->rep_active && old >= 0 && old <= c->rep_tail) {
-      // the replica worker still has to read iteration `old` from this buffer
-      const int64_t t0 = now_ns();
-      std::unique_lock<std::mutex> lk(c->rep_mu);
-      c->rep_done_cv.wait(lk, [&] { return c->rep_iter.load() >= old; });
-      c->rep_stall_ns += now_ns() - t0;
-    }
-    CK(cudaEventSynchronize(c->snap_done[buf]));   // iteration - 2 finished with this buffer
-    c->snap_iter[buf] = iteration;
-    c->snap_seen[buf].assign(c->cfg.n_layers, 0);
-  }
-  for (int l = first_layer; l < first_layer + n_layers; ++l) c->snap_seen[buf][l] = 1;
-  cudaStream_t p = static_cast<cudaStream_t>(producer);
-  CK(cudaEventRecord(c->ev_tmp, p));
-  CK(cudaStreamWaitEvent(c->side, c->ev_tmp, 0));
-  const uint64_t lo = c->off[first_layer], hi = c->off[first_layer + n_layers];
-  // with an active replica, or when sharded snapshots are on, only this rank's shard of the bucket
-  // crosses PCIe (the rest is not read)
-  const uint64_t psi = (uint64_t)c->psi, rk = (uint64_t)c->cfg.rank, wd = (uint64_t)c->cfg.world;
-  const bool shard = c->rep_active || c->snap_sharded;
-  const uint64_t sb = c->rep_active ? c->rep_sb : psi * rk / wd, se = c->rep_active ? c->rep_se : psi * (rk + 1) / wd;
-  const uint64_t a = shard ? std::max(lo, sb) : lo;
-  const uint64_t z = shard ? std::min(hi, se) : hi;
-  int h;
-  ld::prof_begin(c, "snapshot_d2h", c->side, &h);
-  if (a < z)
-    CK(cudaMemcpyAsync(c->snap_host[buf] + a, grad_bucket + (a - lo), (z - a) * 4, cudaMemcpyDeviceToHost, c->side));
-  ld::prof_end(c, h, c->side);
-  CK(cudaEventRecord(c->snap_done[buf], c->side));
-  return LOWDIFF_OK;
-}
-
-// Backward-order buckets of >= min_bytes contiguous layers (LowDiff+ snapshot granularity).
-lowdiff_status lowdiff_bucket_plan(int32_t n_layers, const int64_t* numel, int64_t min_bytes, int32_t* first,
-                                   int32_t* count, int32_t cap, int32_t* n_buckets) {
-  if (n_layers < 1 || !numel || min_bytes < 0 || !first || !count || !n_buckets || cap < 0) return LOWDIFF_E_INVALID;
-  for (int32_t l = 0; l < n_layers; ++l)
-    if (numel[l] < 1) return LOWDIFF_E_INVALID;
-  int32_t n = 0, hi = n_layers;   // the bucket being formed ends (exclusive) at layer hi
-  int64_t bytes = 0;
-  for (int32_t l = n_layers - 1; l >= 0; --l) {
-    bytes += 4 * numel[l];
-    if (bytes >= min_bytes && l > 0) {
-      if (n == cap) return LOWDIFF_E_DIM;
-      first[n] = l, count[n] = hi - l, ++n;
-      hi = l, bytes = 0;
-    }
-  }
-  // the bucket holding layer 0 takes whatever is left (possibly below min_bytes)
-  if (bytes > 0 || n == 0) {
-    if (n == cap) return LOWDIFF_E_DIM;
-    first[n] = 0, count[n] = hi, ++n;
-  }
-  *n_buckets = n;
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_snapshot_shard(lowdiff_ctx* c, int32_t enable) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  c->snap_sharded = enable != 0;
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_snapshot_wait(lowdiff_ctx* c, int64_t iteration, const float** host_grad) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  const int buf = (int)(iteration & 1);
-  if (iteration < 0 || c->snap_iter[buf] != iteration) return fail(c, LOWDIFF_E_STATE, "snapshot_wait: unknown iteration");
-  for (uint8_t x : c->snap_seen[buf])
-    if (!x) return fail(c, LOWDIFF_E_STATE, "snapshot_wait: some layer of the iteration was not snapshotted");
-  CK(cudaEventSynchronize(c->snap_done[buf]));
-  if (host_grad) *host_grad = c->snap_host[buf];
-  return LOWDIFF_OK;
-}
-
-// ---------------------------------------------------------------- LowDiff+ CPU replica (NEXT-3)
-// Worker: applies queued snapshot gradients to the host shard in order (ld::host_adam/host_sgd,
-// replica.cpp), and hands persist requests to a writer thread through a staging copy.
-static void replica_loop(lowdiff_ctx* c) {
-  cudaSetDevice(c->device);
-  const uint64_t S = c->rep_se - c->rep_sb;
-  for (;;) {
-    ld::RepJob j;
-    {
-      std::unique_lock<std::mutex> lk(c->rep_mu);
-      c->rep_cv.wait(lk, [&] { return c->rep_stop || !c->rep_q.empty(); });
-      if (c->rep_q.empty()) return;
-      j = c->rep_q.front();
-      c->rep_q.pop_front();
-      c->rep_busy = 1;
-    }
-    cudaError_t e = cudaSuccess;
-    if (j.kind == 0) {
-      e = cudaEventSynchronize(c->rep_init_done);
-    } else if (j.kind == 1) {
-      const int buf = (int)(j.iteration & 1);
-      e = cudaEventSynchronize(c->snap_done[buf]);
-      if (e == cudaSuccess) {
-        const int64_t t0 = now_ns();
-        const float* G = c->snap_host[buf] + c->rep_sb;
-        if (c->cfg.optim == LOWDIFF_ADAM)
-          ld::host_adam((int64_t)S, G, c->cfg.adam, j.sc, c->rep_host, c->rep_host + S, c->rep_host + 2 * S,
-                        c->rep_threads);
-        else
-          ld::host_sgd((int64_t)S, G, j.sc.lr, c->rep_host, c->rep_threads);
-        c->rep_ns += now_ns() - t0;
-      }
-    } else if (c->cfg.ckpt_dir && c->cfg.write_files) {
-      if (c->rep_writer.joinable()) c->rep_writer.join();
-      c->rep_stage.assign(c->rep_host, c->rep_host + 3 * S);
-      const int64_t it = j.iteration;
-      c->rep_writer = std::thread([c, it]() {
-        const int64_t t0 = now_ns();
-        std::string err;
-        lowdiff_status s2 = write_ldf(c->cfg, c->ckpt_dir, it, (uint64_t)c->psi, c->rep_sb, c->rep_se,
-                                      c->rep_stage.data(), &err);
-        if (s2) set_deferred(c, s2, err);
-        else { c->files_written += 1; c->bytes_written += (int64_t)(100 + 12 * (c->rep_se - c->rep_sb)); }
-        c->writer_ns += now_ns() - t0;
-      });
-    }
-    if (e != cudaSuccess) set_deferred(c, LOWDIFF_E_CUDA, std::string("replica: ") + cudaGetErrorString(e));
-    {
-      std::lock_guard<std::mutex> g(c->rep_mu);
-      if (j.kind != 2) c->rep_iter = j.iteration;
-      c->rep_busy = 0;
-    }
-    c->rep_done_cv.notify_all();
-  }
-}
-
-// drain the queue and the persist writer (worker stays alive)
-static void replica_drain(lowdiff_ctx* c) {
-  if (!c->rep_active) return;
-  {
-    std::unique_lock<std::mutex> lk(c->rep_mu);
-    c->rep_done_cv.wait(lk, [&] { return c->rep_q.empty() && !c->rep_busy; });
-  }
-  // the writer is only joined by the worker or here; the worker is idle now
-  if (c->rep_writer.joinable()) c->rep_writer.join();
-}
-
-static void replica_shutdown(lowdiff_ctx* c) {
-  if (c->rep_thread.joinable()) {
-    {
-      std::lock_guard<std::mutex> g(c->rep_mu);
-      c->rep_stop = true;
-    }
-    c->rep_cv.notify_all();
-    c->rep_thread.join();
-  }
-  if (c->rep_writer.joinable()) c->rep_writer.join();
-  c->rep_stop = false;
-  c->rep_active = false;
-}
-
-static void replica_push(lowdiff_ctx* c, const ld::RepJob& j) {
-  {
-    std::lock_guard<std::mutex> g(c->rep_mu);
-    c->rep_q.push_back(j);
-  }
-  c->rep_cv.notify_one();
-}
-
-lowdiff_status lowdiff_replica_init(lowdiff_ctx* c, int64_t iteration, const float* p, const float* m, const float* v,
-                                    int32_t threads, void* producer) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if (!p || iteration < 0 || threads < 1) return fail(c, LOWDIFF_E_INVALID, "replica_init: bad argument");
-  if (c->cfg.optim == LOWDIFF_ADAM && (!m || !v)) return fail(c, LOWDIFF_E_INVALID, "replica_init: Adam needs m and v");
-  replica_drain(c);
-  replica_shutdown(c);
-  const uint64_t sb = (uint64_t)c->psi * c->cfg.rank / c->cfg.world;
-  const uint64_t se = (uint64_t)c->psi * (c->cfg.rank + 1) / c->cfg.world;
-  const uint64_t S = se - sb;
-  if (!c->rep_host || c->rep_se - c->rep_sb != S) {
-    if (c->rep_host) cudaFreeHost(c->rep_host);
-    c->rep_host = nullptr;
-    CK(cudaHostAlloc((void**)&c->rep_host, std::max<size_t>(1, 3 * S) * 4, cudaHostAllocDefault));
-  }
-  if (!c->rep_init_done) CK(cudaEventCreateWithFlags(&c->rep_init_done, cudaEventDisableTiming));
-  c->rep_sb = sb;
-  c->rep_se = se;
-  c->rep_threads = threads;
-  cudaStream_t pr = static_cast<cudaStream_t>(producer);
-  CK(cudaEventRecord(c->ev_tmp, pr));
-  CK(cudaStreamWaitEvent(c->side, c->ev_tmp, 0));
-  const float* src[3] = {p, m, v};
-  for (int a = 0; a < 3; ++a) {
-    if (src[a]) CK(cudaMemcpyAsync(c->rep_host + a * S, src[a] + sb, S * 4, cudaMemcpyDeviceToHost, c->side));
-    else std::memset(c->rep_host + a * S, 0, S * 4);
-  }
-  CK(cudaEventRecord(c->rep_init_done, c->side));
-  CK(cudaStreamWaitEvent(pr, c->rep_init_done, 0));
-  c->rep_iter = -1;
-  c->rep_tail = iteration;
-  c->rep_active = true;
-  c->rep_thread = std::thread(replica_loop, c);
-  replica_push(c, {0, iteration, {0.f, 0.f, 0.f}});
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_replica_step(lowdiff_ctx* c, int64_t iteration, const lowdiff_step_scalars* scalars) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if ((st = take_deferred(c))) return st;
-  if (!c->rep_active) return fail(c, LOWDIFF_E_STATE, "replica_step: no replica (call lowdiff_replica_init)");
-  if (!scalars) return fail(c, LOWDIFF_E_INVALID, "replica_step: NULL scalars");
-  if (iteration != c->rep_tail + 1)
-    return fail(c, LOWDIFF_E_STATE, "replica_step: expected iteration " + std::to_string(c->rep_tail + 1));
-  const int buf = (int)(iteration & 1);
-  if (c->snap_iter[buf] != iteration) return fail(c, LOWDIFF_E_STATE, "replica_step: iteration was not snapshotted");
-  for (uint8_t x : c->snap_seen[buf])
-    if (!x) return fail(c, LOWDIFF_E_STATE, "replica_step: some layer of the iteration was not snapshotted");
-  c->rep_tail = iteration;
-  replica_push(c, {1, iteration, *scalars});
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_replica_persist(lowdiff_ctx* c) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if ((st = take_deferred(c))) return st;
-  if (!c->rep_active) return fail(c, LOWDIFF_E_STATE, "replica_persist: no replica");
-  if (!c->cfg.ckpt_dir) return fail(c, LOWDIFF_E_INVALID, "replica_persist: no ckpt_dir");
-  replica_push(c, {2, c->rep_tail, {0.f, 0.f, 0.f}});
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_replica_wait(lowdiff_ctx* c, int64_t* iteration, const float** p, const float** m,
-                                    const float** v, int64_t* shard_begin, int64_t* shard_end) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if (!c->rep_active) return fail(c, LOWDIFF_E_STATE, "replica_wait: no replica");
-  replica_drain(c);
-  if ((st = take_deferred(c))) return st;
-  const uint64_t S = c->rep_se - c->rep_sb;
-  if (iteration) *iteration = c->rep_iter.load();
-  if (p) *p = c->rep_host;
-  if (m) *m = c->rep_host + S;
-  if (v) *v = c->rep_host + 2 * S;
-  if (shard_begin) *shard_begin = (int64_t)c->rep_sb;
-  if (shard_end) *shard_end = (int64_t)c->rep_se;
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_replica_restore(lowdiff_ctx* c, float* p, float* m, float* v, int64_t* iteration, void* stream) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if (!c->rep_active) return fail(c, LOWDIFF_E_STATE, "replica_restore: no replica");
-  if (!p || (c->cfg.optim == LOWDIFF_ADAM && (!m || !v))) return fail(c, LOWDIFF_E_INVALID, "replica_restore: bad argument");
-  if (c->cfg.world > 1 && !c->comm) return fail(c, LOWDIFF_E_STATE, "replica_restore: world > 1 needs an NCCL context");
-  replica_drain(c);
-  if ((st = take_deferred(c))) return st;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const uint64_t S = c->rep_se - c->rep_sb;
-  float* dst[3] = {p, m, v};
-  for (int a = 0; a < 3; ++a)
-    if (dst[a] && S) CK(cudaMemcpyAsync(dst[a] + c->rep_sb, c->rep_host + a * S, S * 4, cudaMemcpyHostToDevice, s));
-  if (c->cfg.world > 1 && (st = bcast_shards(c, dst, s))) return st;
-  CK(cudaStreamSynchronize(s));
-  if (iteration) *iteration = c->rep_iter.load();
   return LOWDIFF_OK;
 }
 
