@@ -7,7 +7,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 def build(verbose: bool = False) -> str:
     """Compile liblowdiff.so for sm_100a in-tree (nvcc cross-compiles without a GPU)."""
-    out = subprocess.run(["make", "-C", os.path.join(_HERE, "csrc")], capture_output=True, text=True)
+    jobs = str(max(1, min(8, os.cpu_count() or 1)))
+    out = subprocess.run(["make", "-j", jobs, "-C", os.path.join(_HERE, "csrc")], capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError("liblowdiff build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])
     if verbose:
