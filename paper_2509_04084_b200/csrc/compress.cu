@@ -273,7 +273,13 @@ __device__ __forceinline__ float lazy_zero(float rv, uint32_t gidx, uint32_t T, 
 constexpr int kCandBuf = 32 + 32 * 4 * kJ;   // < 32 staged + one round's worst case
 
 template <bool EF, bool REFILL>
-__global__ void __launch_bounds__(kScanWarps * 32, 64 / kScanWarps)
+#ifndef LD_SCAN_MINB
+#define LD_SCAN_MINB (64 / LD_SCAN_WARPS)
+#endif
+#ifndef LD_SCAN_PF
+#define LD_SCAN_PF 1   // issue round r+1's loads before round r is processed (31 registers: full occupancy kept)
+#endif
+__global__ void __launch_bounds__(kScanWarps * 32, LD_SCAN_MINB)
 scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int lazy) {
   __shared__ uint64_t sbuf_all[kScanWarps][kCandBuf];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -301,25 +307,38 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
     const uint32_t sb = (uint32_t)seg * kSeg;
     uint32_t run = 0, staged = 0, flushed = 0;   // run = flushed + staged
     bool bad = false;
+    // valid-lane mask and 128-bit loads of one round's float4 (j) of g and r
+    auto load = [&](int rd, int j, float4& gq, float4& rq, uint32_t& vq) {
+      const uint32_t e0 = sb + 4u * ((rd * kJ + j) * 32 + lane);
+      vq = 0;
+      if (e0 >= lo && e0 + 4 <= hi) vq = 0xF;
+      else if (e0 + 4 > lo && e0 < hi)
+        for (int k = 0; k < 4; ++k) vq |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
+      if (vq == 0xF) {
+        if (REFILL) {
+          gq = *reinterpret_cast<const float4*>((EF ? rc : gc) + e0);
+        } else {
+          gq = __ldcs(reinterpret_cast<const float4*>(gc + e0));
+          if (EF) rq = __ldcs(reinterpret_cast<const float4*>(rc + e0));
+        }
+      }
+    };
+    constexpr bool kPF = LD_SCAN_PF && !REFILL && kJ == 1;
+    float4 gn = make_float4(0.f, 0.f, 0.f, 0.f), rn = gn;
+    uint32_t vn = 0;
+    if (kPF) load(0, 0, gn, rn, vn);
 #pragma unroll 1
     for (int rd = 0; rd < kSeg / (128 * kJ); ++rd) {   // rounds of kJ float4 x 32 lanes
       float4 a[kJ], gv[kJ], rv[kJ];
       uint32_t vm[kJ];
+      if (kPF) {   // this round was loaded during the previous one; issue the next round now
+        gv[0] = gn;
+        rv[0] = rn;
+        vm[0] = vn;
+        if (rd + 1 < kSeg / (128 * kJ)) load(rd + 1, 0, gn, rn, vn);
+      } else {
 #pragma unroll
-      for (int j = 0; j < kJ; ++j) {
-        const uint32_t e0 = sb + 4u * ((rd * kJ + j) * 32 + lane);
-        vm[j] = 0;
-        if (e0 >= lo && e0 + 4 <= hi) vm[j] = 0xF;
-        else if (e0 + 4 > lo && e0 < hi)
-          for (int k = 0; k < 4; ++k) vm[j] |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
-        if (vm[j] == 0xF) {   // loads first: 4 x 128-bit in flight per lane
-          if (REFILL) {
-            gv[j] = *reinterpret_cast<const float4*>((EF ? rc : gc) + e0);
-          } else {
-            gv[j] = __ldcs(reinterpret_cast<const float4*>(gc + e0));
-            if (EF) rv[j] = __ldcs(reinterpret_cast<const float4*>(rc + e0));
-          }
-        }
+        for (int j = 0; j < kJ; ++j) load(rd, j, gv[j], rv[j], vm[j]);   // 128-bit loads in flight first
       }
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {

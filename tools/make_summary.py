@@ -95,9 +95,11 @@ Evolution of this kernel in round 1 (same workload, bench events):
 | full-grid streaming, 256-element warp segments, 2×32-bit candidate arrays | 3.96 | 0.72 |
 | 1024-element segments, 64-bit interleaved candidates | 3.62 | 0.79 |
 | + chunk-local 32-bit offsets, 1 float4/lane/round, 32 registers | 3.15 | 0.90 |
-| + candidates staged per warp in smem, 256-byte runs (L2 write sectors 308 M → 235 M) | **3.12** | **0.91** |
+| + candidates staged per warp in smem, 256-byte runs (L2 write sectors 308 M → 235 M) | 3.12 | 0.91 |
+| + round r+1's loads issued before round r is processed (31 registers) | **3.06** | **0.92** |
 | (tried) L2 prefetch of the warp's whole segment at its start | 3.18 | 0.90 |
 | (tried) 2 / 8 / 16 warps per CTA | 3.09 / 3.14 / 3.16 | ≤ 0.92 |
+| (tried) the prefetch with 40 / 48 registers (12 / 10 CTAs per SM) | 3.22 / 3.44 | 0.87 / 0.82 |
 
 The probes explain the ordering: a plain full-grid `r = r + g` reaches 7.1 TB/s, and everything
 that lowers resident warps (registers, block barriers, persistent CTAs with serial phases) costs
