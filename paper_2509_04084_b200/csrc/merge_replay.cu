@@ -108,6 +108,15 @@ merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __r
   const int64_t t = blockIdx.x;
   const uint64_t j0 = (uint64_t)t * kMergeTile;
   const int len = (int)min((uint64_t)kMergeTile, psi - j0);
+  // the tile's entry range and this thread's first entry are loaded before the fill, so their
+  // latency hides behind the stores instead of holding the CTA after them
+  const uint32_t a = __ldg(start + t), b = __ldg(start + t + 1);
+  const uint32_t e1 = a + threadIdx.x;
+  uint32_t j1 = 0, v1 = 0;
+  if (e1 < b) {
+    j1 = __ldg(send + e1);
+    v1 = __ldg(send + K + e1);
+  }
   if (len == kMergeTile) {
     float4* out = reinterpret_cast<float4*>(dense + j0);
     for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -115,8 +124,8 @@ merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __r
     for (int i = threadIdx.x; i < len; i += blockDim.x) dense[j0 + i] = 0.f;
   }
   __syncthreads();
-  const uint32_t a = __ldg(start + t), b = __ldg(start + t + 1);
-  for (uint32_t e = a + threadIdx.x; e < b; e += blockDim.x)
+  if (e1 < b) dense[j1] = __fadd_rn(0.f, __uint_as_float(v1));
+  for (uint32_t e = e1 + blockDim.x; e < b; e += blockDim.x)
     dense[__ldg(send + e)] = __fadd_rn(0.f, __uint_as_float(__ldg(send + K + e)));
 }
 
