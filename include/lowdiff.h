@@ -10,8 +10,11 @@
  *   lowdiff_full_ckpt      sharded full checkpoint C^F               Alg. 1 l.15
  *   lowdiff_recover        chain scan + fused replay onto C^F        Alg. 1 l.16-24 PAPER.md:248-259
  * plus the LowDiff+ layer-wise dense snapshot (Alg. 2 l.19), the LowDiff+ CPU
- * replica (Sec. 5.2), the checkpointing-configuration model (Eq. 3-5,
- * PAPER.md:318-350) and a device-resident replay entry point used by recover and the benchmark.
+ * replica (Sec. 5.2), union-compacted differentials (the synchronised G~_t as a
+ * per-shard dictionary), the peer-memory exchange and the live update
+ * (allgather fused into the merge / the optimizer), the checkpointing-configuration model
+ * (Eq. 3-5), CUDA-graph replay of compress / merge, and device-resident replay
+ * entry points used by recover and the benchmark.
  *
  * Conventions (all calls):
  *  - Every call returns lowdiff_status; none throws, aborts or exits.  A CUDA or NCCL
