@@ -268,12 +268,16 @@ def run_ours(args):
         t = it[0]
         sd = sends[t % 2]
         ctx.compress(grads[t % 2] if g is None else g, r, sd)
-        # the rank's own block is final after compress: its D2H (side stream) overlaps the exchange
-        ctx.batch_persist(t + 1, scal[t], sd)
+        if args.persist_first:
+            ctx.batch_persist(t + 1, scal[t], sd)   # D2H overlaps this exchange + the next compress
         if args.exchange == "peer":
             ctx.exchange_peer(t % 2, dense)
         else:
             ctx.exchange(sd, gathered, dense)
+        if not args.persist_first:
+            # Q.put after Sync (Alg. 1 l.5-6): the D2H overlaps the next compress, whose long scan
+            # kernel covers it (a copy-engine D2H costs each kernel boundary it overlaps)
+            ctx.batch_persist(t + 1, scal[t], sd)
         it[0] += 1
         return sd
 
@@ -755,6 +759,8 @@ def main():
     ap.add_argument("--recovery-files", type=int, default=0,
                     help="n > 0: also time lowdiff_recover from Full@0 + n differentials on local storage")
     ap.add_argument("--no-graphs", action="store_true", help="plain launches instead of captured CUDA graphs")
+    ap.add_argument("--persist-first", action="store_true",
+                    help="issue the block's D2H before the exchange instead of after it")
     ap.add_argument("--snapshot-reps", type=int, default=20,
                     help="proxy backward: HBM passes over each bucket (20 ~ 38 ms for GPT-2 XL, about the backward "
                          "of 8K tokens at ~1.2 PFLOP/s)")
