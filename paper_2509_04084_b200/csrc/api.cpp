@@ -645,6 +645,7 @@ lowdiff_status lowdiff_destroy(lowdiff_ctx* c) {
   for (auto* p : c->snap_host) if (p) cudaFreeHost(p);
   for (auto* p : c->dev_allocs) cudaFree(p);
   if (c->replay_scratch) cudaFree(c->replay_scratch);
+  if (c->scal_dev) cudaFree(c->scal_dev);
   if (c->merge_scratch) cudaFree(c->merge_scratch);
   if (c->full_stage) cudaFree(c->full_stage);
   for (void* q : c->peer_opened) cudaIpcCloseMemHandle(q);

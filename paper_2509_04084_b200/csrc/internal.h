@@ -243,6 +243,8 @@ struct lowdiff_ctx {
   size_t merge_scratch_bytes = 0;
   void* union_scratch = nullptr;
   size_t union_scratch_bytes = 0;
+  float* scal_dev = nullptr;          // lowdiff_replay(_range): per-step scalars on the device
+  size_t scal_cap = 0;
   uint64_t scratch_gen = 0;          // bumped when a scratch buffer a graph may bake in is reallocated
   // CUDA graphs of lowdiff_compress / merge (lowdiff_set_graphs)
   bool use_graphs = false;

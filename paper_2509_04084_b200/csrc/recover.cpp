@@ -92,15 +92,21 @@ lowdiff_status lowdiff_replay_range(lowdiff_ctx* c, int32_t optim, int32_t world
     return fail(c, LOWDIFF_E_INVALID, "replay: bad argument");
   if (!n_steps || begin == end) return LOWDIFF_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // per-step scalars to the device (tail of the replay scratch is not reused: own buffer)
-  float* scal_dev = nullptr;
-  CK(cudaMallocAsync((void**)&scal_dev, (size_t)n_steps * 12, s));
-  CK(cudaMemcpyAsync(scal_dev, scalars, (size_t)n_steps * 12, cudaMemcpyHostToDevice, s));
+  // per-step scalars to the device: a context buffer that only grows (a cudaMallocAsync / free
+  // pair per call returned the pool's memory at every synchronisation and re-mapped it: ~27 ms)
+  const size_t sbytes = (size_t)n_steps * 12;
+  if (c->scal_cap < sbytes) {
+    if (c->scal_dev) cudaFree(c->scal_dev);
+    c->scal_dev = nullptr;
+    c->scal_cap = 0;
+    CK(cudaMalloc((void**)&c->scal_dev, sbytes));
+    c->scal_cap = sbytes;
+  }
+  CK(cudaMemcpyAsync(c->scal_dev, scalars, sbytes, cudaMemcpyHostToDevice, s));
   const float consts[5] = {c->cfg.adam.beta1, c->cfg.adam.one_minus_beta1, c->cfg.adam.beta2,
                            c->cfg.adam.one_minus_beta2, c->cfg.adam.eps};
-  cudaError_t e = ld::launch_replay(c, optim, c->cfg.mean != 0, consts, world, n_steps, diffs, scal_dev,
+  cudaError_t e = ld::launch_replay(c, optim, c->cfg.mean != 0, consts, world, n_steps, diffs, c->scal_dev,
                                     (uint64_t)begin, (uint64_t)end, nullptr, p, m, v, s);
-  cudaFreeAsync(scal_dev, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "launch_replay");
   return LOWDIFF_OK;
 }
