@@ -219,3 +219,22 @@ def test_bucket_plan_errors():
     assert L.lowdiff_bucket_plan(3, sizes, 0, first, count, 3, C.byref(nb)) == 0 and nb.value == 3
     assert L.lowdiff_bucket_plan(3, sizes, 10**9, first, count, 1, C.byref(nb)) == 0
     assert nb.value == 1 and (first[0], count[0]) == (0, 3)
+
+
+def test_bench_reference_arm_prints_one_json_line():
+    """`bench.py --impl reference` (the oracle arm the driver runs) prints one JSON line with the
+    contract's keys, on the CPU (MLP workload to keep it short)."""
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "mlp",
+                        "--steps", "2", "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == "mlp@10000ppm"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
