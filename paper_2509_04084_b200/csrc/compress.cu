@@ -208,6 +208,7 @@ small_layer_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r
     if (tid < 32) {
       uint32_t bin, above;
       warp_find_bin(hist, nb, s_kleft, &bin, &above);
+      __syncwarp();   // every lane has read s_kleft before lane 0 updates it
       if (tid == 0) { s_prefix = (pre << bits[d]) | bin; s_kleft -= above; }
     }
     __syncthreads();
