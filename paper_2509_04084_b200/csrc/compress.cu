@@ -32,6 +32,7 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "pdl.cuh"
 
 namespace ld {
 namespace {
@@ -282,6 +283,8 @@ template <bool EF, bool REFILL>
 #endif
 __global__ void __launch_bounds__(kScanWarps * 32, LD_SCAN_MINB)
 scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int lazy) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint64_t sbuf_all[kScanWarps][kCandBuf];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -427,6 +430,8 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
 // when all chunks of the CTA belong to one layer (chunk slots are monotone), else directly.
 // only_refill: process just the chunks of refilled layers (after the rescan).
 __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_refill) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t sh[kH0];
   __shared__ uint32_t s_tot;
   if (only_refill && P.counters[only_refill == 2 ? 4 : 0] == 0) return;   // no refill at this level
@@ -517,6 +522,8 @@ __device__ void queue_refill(const DevPlan& P, int slot, int level, int c0, int 
 }
 
 __global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
+  pdl_wait();
+  pdl_trigger();
   const int slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (slot >= P.n_large) return;
@@ -615,6 +622,8 @@ __global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
 // digit d (1 or 2) histogram over candidates matching the prefix: warp per chunk, 8 chunks per
 // CTA aggregated in shared memory when they belong to one layer
 __global__ void __launch_bounds__(256) digit_kernel(DevPlan P, int d) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t sh[kH1];
   const int lane = threadIdx.x & 31;
   const int c_first = blockIdx.x * 8;
@@ -665,6 +674,8 @@ __global__ void __launch_bounds__(256) digit_kernel(DevPlan P, int d) {
 // read once from DRAM; the emit's second read hits L1/L2).  The layer's first chunk also does the
 // per-layer bookkeeping the layer scan did (sel_T, next thresholds, layer_total reset).
 __global__ void __launch_bounds__(256) count_emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K) {
+  pdl_wait();
+  pdl_trigger();
   const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
   const int lane = threadIdx.x & 31;
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -851,8 +862,9 @@ cudaError_t compress_head(lowdiff_ctx* c, const float* grad, float* residual, ui
   else scan_kernel<false, false><<<scan_grid, uK, 0, s>>>(P, grad, residual, 0);
   prof_end(c, h, s);
   prof_begin(c, "select", s, sel_h);
-  chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, 0);
-  find_kernel<<<layer_blocks, 256, 0, s>>>(P, 0);
+  const bool pdl = !c->prof;   // programmatic launches (pdl.cuh); profiling events sit between kernels
+  if ((e = launch_pdl(pdl, chunk_prep_kernel, chunk_blocks, 256, 0, s, P, 0)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 0)) != cudaSuccess) return e;
   c->launches += 3;
   return cudaGetLastError();
 }
@@ -864,10 +876,13 @@ cudaError_t compress_refill(lowdiff_ctx* c, const float* grad, float* residual, 
   const int layer_blocks = (P.n_large * 32 + 255) / 256;
   const int chunk_blocks = (P.n_chunks + 7) / 8;
   const int uK = kScanWarps * 32;
-  if (ef) scan_kernel<true, true><<<num_sms() * 16, uK, 0, s>>>(P, grad, residual, level);
-  else scan_kernel<false, true><<<num_sms() * 16, uK, 0, s>>>(P, grad, residual, level);
-  chunk_prep_kernel<<<chunk_blocks, 256, 0, s>>>(P, level);
-  find_kernel<<<layer_blocks, 256, 0, s>>>(P, level == 1 ? 1 : 4);
+  const bool pdl = !c->prof;
+  const unsigned rgrid = (unsigned)num_sms() * 16;
+  cudaError_t e = ef ? launch_pdl(pdl, scan_kernel<true, true>, rgrid, uK, 0, s, P, grad, residual, level)
+                     : launch_pdl(pdl, scan_kernel<false, true>, rgrid, uK, 0, s, P, grad, residual, level);
+  if (e != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, chunk_prep_kernel, chunk_blocks, 256, 0, s, P, level)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, level == 1 ? 1 : 4)) != cudaSuccess) return e;
   c->launches += 3;
   return cudaGetLastError();
 }
@@ -879,14 +894,16 @@ cudaError_t compress_tail(lowdiff_ctx* c, float* residual, uint32_t* send, cudaS
   if (P.n_large) {
     const int layer_blocks = (P.n_large * 32 + 255) / 256;
     const int chunk_blocks = (P.n_chunks + 7) / 8;
-    digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 1);
-    find_kernel<<<layer_blocks, 256, 0, s>>>(P, 2);
-    digit_kernel<<<chunk_blocks, 256, 0, s>>>(P, 2);
-    find_kernel<<<layer_blocks, 256, 0, s>>>(P, 3);
+    const bool pdl = !c->prof;
+    if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, 1)) != cudaSuccess) return e;
+    if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 2)) != cudaSuccess) return e;
+    if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, 2)) != cudaSuccess) return e;
+    if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 3)) != cudaSuccess) return e;
     prof_end(c, sel_h, s);
     int h;
     prof_begin(c, "emit", s, &h);
-    count_emit_kernel<<<chunk_blocks, 256, 0, s>>>(P, send, (uint64_t)c->K);
+    if ((e = launch_pdl(pdl, count_emit_kernel, chunk_blocks, 256, 0, s, P, send, (uint64_t)c->K)) != cudaSuccess)
+      return e;
     prof_end(c, h, s);
     if (P.n_small && c->aux && (e = cudaStreamWaitEvent(s, c->ev_join, 0)) != cudaSuccess) return e;   // join
     c->launches += 5;

@@ -20,6 +20,7 @@
 
 #include "ieee_fast.cuh"
 #include "internal.h"
+#include "pdl.cuh"
 
 namespace ld {
 namespace {
@@ -32,6 +33,7 @@ namespace {
 __global__ void tile_start_kernel(const uint32_t* __restrict__ blocks, int64_t n_blocks, uint64_t stride,
                                   uint32_t K, int tile_shift, uint32_t T0, uint32_t T1,
                                   const uint32_t* __restrict__ ranges, uint32_t* __restrict__ start) {
+  pdl_trigger();   // the merge may be scheduled now (it waits for this grid before reading start)
   const uint32_t W = T1 - T0 + 1;
   for (int64_t b = blockIdx.y; b < n_blocks; b += gridDim.y) {
     const uint32_t* idx = blocks + (uint64_t)b * stride;
@@ -73,6 +75,7 @@ merge_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const
   const int len = (int)min((uint64_t)kMergeTile, psi - j0);
   float4* acc4 = reinterpret_cast<float4*>(acc);
   for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) acc4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  pdl_wait();
   __syncthreads();
   for (int r = 0; r < world; ++r) {
     const uint32_t* idx = gathered + (uint64_t)r * 2 * K;
@@ -108,20 +111,21 @@ merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __r
   const int64_t t = blockIdx.x;
   const uint64_t j0 = (uint64_t)t * kMergeTile;
   const int len = (int)min((uint64_t)kMergeTile, psi - j0);
-  // the tile's entry range and this thread's first entry are loaded before the fill, so their
-  // latency hides behind the stores instead of holding the CTA after them
+  // the fill touches only dense, which tile_start (the programmatic predecessor, itself launched in
+  // plain stream order) does not: it runs before pdl_wait and overlaps tile_start
+  if (len == kMergeTile) {
+    float4* out = reinterpret_cast<float4*>(dense + j0);
+    for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  } else {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) dense[j0 + i] = 0.f;
+  }
+  pdl_wait();
   const uint32_t a = __ldg(start + t), b = __ldg(start + t + 1);
   const uint32_t e1 = a + threadIdx.x;
   uint32_t j1 = 0, v1 = 0;
   if (e1 < b) {
     j1 = __ldg(send + e1);
     v1 = __ldg(send + K + e1);
-  }
-  if (len == kMergeTile) {
-    float4* out = reinterpret_cast<float4*>(dense + j0);
-    for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-  } else {
-    for (int i = threadIdx.x; i < len; i += blockDim.x) dense[j0 + i] = 0.f;
   }
   __syncthreads();
   if (e1 < b) dense[j1] = __fadd_rn(0.f, __uint_as_float(v1));
@@ -511,16 +515,16 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
   }
   const unsigned grid = (unsigned)n_tiles;
   if (world == 1) {
-    merge1_kernel<<<grid, 256, 0, s>>>(gathered, K, start, n_tiles, (uint64_t)psi, dense);
+    cudaError_t e = launch_pdl(!c->prof, merge1_kernel, grid, 256, 0, s, gathered, K, start, n_tiles, (uint64_t)psi, dense);
+    if (e != cudaSuccess) return e;
     prof_end(c, h, s);
     c->launches += 2;
     return cudaGetLastError();
   }
-  switch (div_mode(c->cfg.mean != 0, world)) {
-    case 0: merge_kernel<0><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
-    case 1: merge_kernel<1><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
-    default: merge_kernel<2><<<grid, 256, 0, s>>>(gathered, world, K, start, n_tiles, (uint64_t)psi, dense); break;
-  }
+  const int dm = div_mode(c->cfg.mean != 0, world);
+  cudaError_t e = launch_pdl(!c->prof, dm == 0 ? merge_kernel<0> : dm == 1 ? merge_kernel<1> : merge_kernel<2>, grid, 256, 0,
+                             s, gathered, world, K, start, n_tiles, (uint64_t)psi, dense);
+  if (e != cudaSuccess) return e;
   prof_end(c, h, s);
   c->launches += 2;
   return cudaGetLastError();
