@@ -274,13 +274,145 @@ __device__ __forceinline__ float lazy_zero(float rv, uint32_t gidx, uint32_t T, 
 // ~0.3 GB of candidates per GPT-2 XL call).
 constexpr int kCandBuf = 32 + 32 * 4 * kJ;   // < 32 staged + one round's worst case
 
-template <bool EF, bool REFILL>
 #ifndef LD_SCAN_MINB
 #define LD_SCAN_MINB (64 / LD_SCAN_WARPS)
 #endif
 #ifndef LD_SCAN_PF
 #define LD_SCAN_PF 1   // issue round r+1's loads before round r is processed (31 registers: full occupancy kept)
 #endif
+// One warp's 1024-element segment.  FULL: the segment lies inside the layer (every chunk but a
+// layer's ragged first/last one), so the valid-lane masks and the scalar edge path compile away.
+// thr is pre-clamped to <= 0x7F800000, so every non-finite key is also a candidate and the
+// non-finite check runs only on the (rare) candidate path.  The lazy-zero index test (key == T_prev
+// and index < cut_prev) is taken only by a lane holding a key equal to T_prev.
+template <bool EF, bool REFILL, bool FULL>
+__device__ __forceinline__ uint32_t scan_segment(const float* __restrict__ gc, float* __restrict__ rc,
+                                                 uint64_t* __restrict__ cd, uint64_t* sbuf, uint32_t sb,
+                                                 uint32_t lo, uint32_t hi, uint32_t gbase, uint32_t thr,
+                                                 uint32_t lT, uint32_t lcut, int lane, unsigned lt, bool& bad) {
+  uint32_t run = 0, staged = 0, flushed = 0;   // run = flushed + staged
+  // valid-lane mask and 128-bit loads of one round's float4 (j) of g and r
+  auto load = [&](int rd, int j, float4& gq, float4& rq, uint32_t& vq) {
+    const uint32_t e0 = sb + 4u * ((rd * kJ + j) * 32 + lane);
+    if (FULL) {
+      vq = 0xF;
+    } else {
+      vq = 0;
+      if (e0 >= lo && e0 + 4 <= hi) vq = 0xF;
+      else if (e0 + 4 > lo && e0 < hi)
+        for (int k = 0; k < 4; ++k) vq |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
+    }
+    if (vq == 0xF) {
+      if (REFILL) {
+        gq = *reinterpret_cast<const float4*>((EF ? rc : gc) + e0);
+      } else {
+        gq = __ldcs(reinterpret_cast<const float4*>(gc + e0));
+        if (EF) rq = __ldcs(reinterpret_cast<const float4*>(rc + e0));
+      }
+    }
+  };
+  constexpr bool kPF = LD_SCAN_PF && !REFILL && kJ == 1;
+  float4 gn = make_float4(0.f, 0.f, 0.f, 0.f), rn = gn;
+  uint32_t vn = 0;
+  if (kPF) load(0, 0, gn, rn, vn);
+#pragma unroll 1
+  for (int rd = 0; rd < kSeg / (128 * kJ); ++rd) {   // rounds of kJ float4 x 32 lanes
+    float4 a[kJ], gv[kJ], rv[kJ];
+    uint32_t vm[kJ];
+    if (kPF) {   // this round was loaded during the previous one; issue the next round now
+      gv[0] = gn;
+      rv[0] = rn;
+      vm[0] = vn;
+      if (rd + 1 < kSeg / (128 * kJ)) load(rd + 1, 0, gn, rn, vn);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) load(rd, j, gv[j], rv[j], vm[j]);   // 128-bit loads in flight first
+    }
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const uint32_t e0 = sb + 4u * ((rd * kJ + j) * 32 + lane);
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (FULL || vm[j] == 0xF) {
+        if (!REFILL && EF) {
+          const float4 q = rv[j];
+          const uint32_t k0 = key_of(q.x), k1 = key_of(q.y), k2 = key_of(q.z), k3 = key_of(q.w);
+          if ((k0 == lT) | (k1 == lT) | (k2 == lT) | (k3 == lT)) {   // a tie with T_prev: exact rule
+            const uint32_t gi = gbase + e0;
+            x = make_float4(__fadd_rn(lazy_zero(q.x, gi, lT, lcut), gv[j].x),
+                            __fadd_rn(lazy_zero(q.y, gi + 1, lT, lcut), gv[j].y),
+                            __fadd_rn(lazy_zero(q.z, gi + 2, lT, lcut), gv[j].z),
+                            __fadd_rn(lazy_zero(q.w, gi + 3, lT, lcut), gv[j].w));
+          } else {
+            x = make_float4(__fadd_rn(k0 > lT ? 0.0f : q.x, gv[j].x), __fadd_rn(k1 > lT ? 0.0f : q.y, gv[j].y),
+                            __fadd_rn(k2 > lT ? 0.0f : q.z, gv[j].z), __fadd_rn(k3 > lT ? 0.0f : q.w, gv[j].w));
+          }
+        } else {
+          x = gv[j];
+        }
+        if (!REFILL && EF) __stcs(reinterpret_cast<float4*>(rc + e0), x);
+      } else if (vm[j]) {   // ragged edge of a layer: scalar
+        for (int k = 0; k < 4; ++k)
+          if ((vm[j] >> k) & 1u) {
+            float y;
+            if (REFILL) y = EF ? rc[e0 + k] : gc[e0 + k];
+            else y = EF ? __fadd_rn(lazy_zero(rc[e0 + k], gbase + e0 + k, lT, lcut), gc[e0 + k]) : gc[e0 + k];
+            f4set(x, k, y);
+            if (!REFILL && EF) rc[e0 + k] = y;
+          }
+      }
+      a[j] = x;
+    }
+    // flags + ordered compaction: (round, j, lane, k) order == index order
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      uint32_t fl = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool v = FULL || ((vm[j] >> k) & 1u);
+        fl |= (v && key_of(f4get(a[j], k)) >= thr) ? 1u << k : 0u;
+      }
+      unsigned bm[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) bm[k] = __ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u);
+      uint32_t pos = staged;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) pos += __popc(bm[k] & lt);
+      if (fl) {
+        const uint32_t e0 = gbase + sb + 4u * ((rd * kJ + j) * 32 + lane);   // global index (Psi < 2^32)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if ((fl >> k) & 1u) {
+            bad |= key_of(f4get(a[j], k)) >= 0x7F800000u;
+            sbuf[pos++] = ((uint64_t)__float_as_uint(f4get(a[j], k)) << 32) | (e0 + k);
+          }
+      }
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cnt += __popc(bm[k]);
+      run += cnt;
+      staged += cnt;
+    }
+    if (staged >= 32) {   // whole 32-entry runs out, coalesced; the remainder moves to the front
+      __syncwarp();
+      const uint32_t full = staged & ~31u;
+      for (uint32_t i = lane; i < full; i += 32) cd[flushed + i] = sbuf[i];
+      __syncwarp();
+      const uint32_t rest = staged - full;
+      uint64_t x = lane < rest ? sbuf[full + lane] : 0;
+      __syncwarp();
+      if (lane < rest) sbuf[lane] = x;
+      __syncwarp();
+      flushed += full;
+      staged = rest;
+    }
+  }
+  __syncwarp();
+  if (lane < staged) cd[flushed + lane] = sbuf[lane];
+  __syncwarp();
+  return run;
+}
+
+template <bool EF, bool REFILL>
 __global__ void __launch_bounds__(kScanWarps * 32, LD_SCAN_MINB)
 scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int lazy) {
   pdl_wait();
@@ -301,122 +433,17 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
     const uint64_t cbase = P.chunk_base[ch];
     const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
     const int slot = P.chunk_slot[ch];
-    const uint32_t thr = REFILL ? (lazy == 2 ? 0u : P.thr_safe[slot]) : P.thr[slot];
+    const uint32_t thr = min(REFILL ? (lazy == 2 ? 0u : P.thr_safe[slot]) : P.thr[slot], 0x7F800000u);
     const bool lz = !REFILL && EF && lazy;
     const uint32_t lT = lz ? P.sel_T[slot] : 0xFFFFFFFFu, lcut = lz ? P.sel_cut[slot] : 0u;
     const uint32_t gbase = (uint32_t)cbase;   // Psi < 2^32
-    const float* gc = g + cbase;
-    float* rc = r + cbase;
     uint64_t* cd = P.cand + ((uint64_t)ch * kSegsPerChunk + seg) * kSeg;
     const uint32_t sb = (uint32_t)seg * kSeg;
-    uint32_t run = 0, staged = 0, flushed = 0;   // run = flushed + staged
     bool bad = false;
-    // valid-lane mask and 128-bit loads of one round's float4 (j) of g and r
-    auto load = [&](int rd, int j, float4& gq, float4& rq, uint32_t& vq) {
-      const uint32_t e0 = sb + 4u * ((rd * kJ + j) * 32 + lane);
-      vq = 0;
-      if (e0 >= lo && e0 + 4 <= hi) vq = 0xF;
-      else if (e0 + 4 > lo && e0 < hi)
-        for (int k = 0; k < 4; ++k) vq |= (e0 + k >= lo && e0 + k < hi) ? 1u << k : 0u;
-      if (vq == 0xF) {
-        if (REFILL) {
-          gq = *reinterpret_cast<const float4*>((EF ? rc : gc) + e0);
-        } else {
-          gq = __ldcs(reinterpret_cast<const float4*>(gc + e0));
-          if (EF) rq = __ldcs(reinterpret_cast<const float4*>(rc + e0));
-        }
-      }
-    };
-    constexpr bool kPF = LD_SCAN_PF && !REFILL && kJ == 1;
-    float4 gn = make_float4(0.f, 0.f, 0.f, 0.f), rn = gn;
-    uint32_t vn = 0;
-    if (kPF) load(0, 0, gn, rn, vn);
-#pragma unroll 1
-    for (int rd = 0; rd < kSeg / (128 * kJ); ++rd) {   // rounds of kJ float4 x 32 lanes
-      float4 a[kJ], gv[kJ], rv[kJ];
-      uint32_t vm[kJ];
-      if (kPF) {   // this round was loaded during the previous one; issue the next round now
-        gv[0] = gn;
-        rv[0] = rn;
-        vm[0] = vn;
-        if (rd + 1 < kSeg / (128 * kJ)) load(rd + 1, 0, gn, rn, vn);
-      } else {
-#pragma unroll
-        for (int j = 0; j < kJ; ++j) load(rd, j, gv[j], rv[j], vm[j]);   // 128-bit loads in flight first
-      }
-#pragma unroll
-      for (int j = 0; j < kJ; ++j) {
-        const uint32_t e0 = sb + 4u * ((rd * kJ + j) * 32 + lane);
-        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (vm[j] == 0xF) {
-          if (!REFILL && EF) {
-            const uint32_t gi = gbase + e0;
-            x = make_float4(__fadd_rn(lazy_zero(rv[j].x, gi, lT, lcut), gv[j].x),
-                            __fadd_rn(lazy_zero(rv[j].y, gi + 1, lT, lcut), gv[j].y),
-                            __fadd_rn(lazy_zero(rv[j].z, gi + 2, lT, lcut), gv[j].z),
-                            __fadd_rn(lazy_zero(rv[j].w, gi + 3, lT, lcut), gv[j].w));
-          } else {
-            x = gv[j];
-          }
-          if (!REFILL && EF) __stcs(reinterpret_cast<float4*>(rc + e0), x);
-        } else if (vm[j]) {   // ragged edge of a layer: scalar
-          for (int k = 0; k < 4; ++k)
-            if ((vm[j] >> k) & 1u) {
-              float y;
-              if (REFILL) y = EF ? rc[e0 + k] : gc[e0 + k];
-              else y = EF ? __fadd_rn(lazy_zero(rc[e0 + k], gbase + e0 + k, lT, lcut), gc[e0 + k]) : gc[e0 + k];
-              f4set(x, k, y);
-              if (!REFILL && EF) rc[e0 + k] = y;
-            }
-        }
-        a[j] = x;
-      }
-      // flags + ordered compaction: (round, j, lane, k) order == index order
-#pragma unroll
-      for (int j = 0; j < kJ; ++j) {
-        uint32_t fl = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t key = key_of(f4get(a[j], k));
-          const bool v = (vm[j] >> k) & 1u;
-          bad |= v && key >= 0x7F800000u;
-          fl |= (v && key >= thr) ? 1u << k : 0u;
-        }
-        unsigned bm[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) bm[k] = __ballot_sync(0xFFFFFFFFu, (fl >> k) & 1u);
-        uint32_t pos = staged;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) pos += __popc(bm[k] & lt);
-        if (fl) {
-          const uint32_t e0 = (uint32_t)cbase + sb + 4u * ((rd * kJ + j) * 32 + lane);   // global index (Psi < 2^32)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if ((fl >> k) & 1u) sbuf[pos++] = ((uint64_t)__float_as_uint(f4get(a[j], k)) << 32) | (e0 + k);
-        }
-        uint32_t cnt = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) cnt += __popc(bm[k]);
-        run += cnt;
-        staged += cnt;
-      }
-      if (staged >= 32) {   // whole 32-entry runs out, coalesced; the remainder moves to the front
-        __syncwarp();
-        const uint32_t full = staged & ~31u;
-        for (uint32_t i = lane; i < full; i += 32) cd[flushed + i] = sbuf[i];
-        __syncwarp();
-        const uint32_t rest = staged - full;
-        uint64_t x = lane < rest ? sbuf[full + lane] : 0;
-        __syncwarp();
-        if (lane < rest) sbuf[lane] = x;
-        __syncwarp();
-        flushed += full;
-        staged = rest;
-      }
-    }
-    __syncwarp();
-    if (lane < staged) cd[flushed + lane] = sbuf[lane];
-    __syncwarp();
+    const uint32_t run =
+        (sb >= lo && sb + kSeg <= hi)
+            ? scan_segment<EF, REFILL, true>(g + cbase, r + cbase, cd, sbuf, sb, lo, hi, gbase, thr, lT, lcut, lane, lt, bad)
+            : scan_segment<EF, REFILL, false>(g + cbase, r + cbase, cd, sbuf, sb, lo, hi, gbase, thr, lT, lcut, lane, lt, bad);
     if (lane == 0) P.seg_count[(uint64_t)ch * kSegsPerChunk + seg] = run;
     if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
     if (!REFILL) break;
