@@ -112,10 +112,13 @@ merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __r
   const uint64_t j0 = (uint64_t)t * kMergeTile;
   const int len = (int)min((uint64_t)kMergeTile, psi - j0);
   // the fill touches only dense, which tile_start (the programmatic predecessor, itself launched in
-  // plain stream order) does not: it runs before pdl_wait and overlaps tile_start
-  if (len == kMergeTile) {
-    float4* out = reinterpret_cast<float4*>(dense + j0);
-    for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  // plain stream order) does not: its first half runs before pdl_wait and overlaps tile_start; the
+  // tile's entry range and this thread's first entry are loaded between the halves, so their
+  // latency hides behind the second half instead of holding the CTA after the fill
+  float4* out = reinterpret_cast<float4*>(dense + j0);
+  const bool whole = len == kMergeTile;
+  if (whole) {
+    for (int q = threadIdx.x; q < kMergeTile / 8; q += blockDim.x) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   } else {
     for (int i = threadIdx.x; i < len; i += blockDim.x) dense[j0 + i] = 0.f;
   }
@@ -127,6 +130,8 @@ merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __r
     j1 = __ldg(send + e1);
     v1 = __ldg(send + K + e1);
   }
+  if (whole)
+    for (int q = kMergeTile / 8 + threadIdx.x; q < kMergeTile / 4; q += blockDim.x) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncthreads();
   if (e1 < b) dense[j1] = __fadd_rn(0.f, __uint_as_float(v1));
   for (uint32_t e = e1 + blockDim.x; e < b; e += blockDim.x)
