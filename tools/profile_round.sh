@@ -8,15 +8,17 @@ mkdir -p $OUT
 timeout 1200 python -m pytest tests -m gpu -q > $OUT/p_gpu_tests.log 2>&1; tail -n 2 $OUT/p_gpu_tests.log
 python bench.py --steps 20 --warmup 8 > $OUT/p_bench.json 2> $OUT/p_bench.err
 tail -2 $OUT/p_bench.err
-SHORT="python bench.py --steps 8 --warmup 4 --no-cpu --no-e2e --no-writer --no-replica --no-full --no-snapshot --replay-steps 10"
-# our kernels only (the gradient generator's launches are torch's), steady state: skip the first 150
+SHORT="python bench.py --steps 4 --warmup 20 --no-cpu --no-e2e --no-writer --no-replica --no-full --no-snapshot --replay-steps 10"
+# our kernels only (the gradient generator's launches are torch's), steady state: skip the first 400
+# (~23 calls: the EF residual and the speculative band settle over the first ~10, see tools/spec_ratio.py)
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active \
     --clock-control none -k "regex:^(small|scan|chunk_prep|find|digit|count|tile_start|merge|update|replay|materialize|union)" \
-    -s 150 -c 200 --csv --log-file $OUT/launches.csv \
-    python bench.py --steps 12 --warmup 8 --no-cpu --no-e2e --no-writer --no-replica --no-full --no-snapshot --no-union --replay-steps 10 \
+    -s 400 -c 200 --csv --log-file $OUT/launches.csv \
+    python bench.py --steps 12 --warmup 24 --no-cpu --no-e2e --no-writer --no-replica --no-full --no-snapshot --no-union --replay-steps 10 \
     > $OUT/p_launches.out 2>&1
 tail -2 $OUT/p_launches.out
-for ks in scan_kernel:9 merge1_kernel:4 update_kernel:4 replay_kernel:1 count_emit_kernel:10 chunk_prep_kernel:9 union_tile_kernel:2; do
+# skips land on call 21 of the step loop (3 scan / chunk_prep launches per call: main + 2 refill levels)
+for ks in scan_kernel:63 merge1_kernel:21 update_kernel:4 replay_kernel:1 count_emit_kernel:21 chunk_prep_kernel:63 union_tile_kernel:2; do
   k=${ks%%:*}; skip=${ks##*:}
   ncu --set full --clock-control none --import-source on -k regex:^$k -s $skip -c 1 -o $OUT/prof_$k $SHORT \
       > $OUT/p_$k.out 2>&1
