@@ -309,9 +309,10 @@ def run_ours(args):
     e1.record()
     torch.cuda.synchronize()
     clk = clocks.stop()
-    per = [e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, args.steps)]
-    per.sort()
+    raw = [e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, args.steps)]
+    per = sorted(raw)
     spread = {"p10": per[len(per) // 10], "p50": per[len(per) // 2], "p90": per[(9 * len(per)) // 10],
+              "steps_ms": [round(x, 4) for x in raw],
               "note": "compute-stream time per step (event after each step); value uses the whole region"}
     barrier(world)
     ms = allmax(e0.elapsed_time(e1), world)

@@ -532,6 +532,11 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, int only_ref
 // mode 2/3: find digit 1/2 for every large layer (mode 2 also predicts the next band)
 // candidates admitted for the layer this call: summed by chunk_prep (one load instead of a walk
 // over up to ~5000 chunk counts per layer)
+#ifndef LD_L1_DROP
+#define LD_L1_DROP (1u << 21)
+#endif
+constexpr uint32_t kL1Drop = LD_L1_DROP;   // level-1 threshold step below a missed band (key units)
+
 __device__ __forceinline__ uint32_t layer_candidates(const DevPlan& P, int slot) {
   return *reinterpret_cast<volatile const uint32_t*>(P.layer_total + slot);
 }
@@ -577,8 +582,16 @@ __global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
       }
     } else {
       // missed.  Level 1 rescans at the safe threshold (this distribution's band, without the
-      // drift share) when that is lower than the one that missed; otherwise straight to level 2.
-      const int level = P.thr_safe[slot] < P.thr[slot] ? 1 : 2;
+      // drift share) when that is lower than the one that missed, else at the missed threshold
+      // lowered by a quarter binade (x0.75-0.875 in value); level 2 (every element a candidate)
+      // only when neither exists.  Without the second option a miss with no drift lead went
+      // straight to level 2, which for a large layer cost ~1 ms.
+      const uint32_t th = P.thr[slot], ts = P.thr_safe[slot];
+      uint32_t l1 = 0xFFFFFFFFu;
+      if (ts < th) l1 = ts;
+      else if (th != 0xFFFFFFFFu && th > kL1Drop) l1 = min(th, 0x7F800000u) - kL1Drop;
+      const int level = l1 != 0xFFFFFFFFu ? 1 : 2;
+      if (level == 1 && lane == 0) P.thr_safe[slot] = l1;   // read by the level-1 rescan
       queue_refill(P, slot, level, c0, c1, lane);
       if (lane == 0) {
         S.refill = (uint32_t)level;
@@ -631,16 +644,20 @@ __global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
         }
       }
       // drift share: under error feedback the k-th key moved from T_{t-1} (sel_T, still the previous
-      // call's) to T_t (>= the digit-1 prefix); lead the next band by alpha x that drift.
+      // call's) to T_t (>= the digit-1 prefix); lead the next band by alpha x the smaller of this
+      // drift and the previous call's, so a T that alternates (periodic inputs) gets no lead --
+      // leading by an up-step right before a down-step missed most layers at once.
       const uint32_t t_lo = ((S.prefix << 11) | bin) << 9;
       const uint32_t t_prev = P.sel_T[slot];
+      const uint32_t d_now = (t_prev != 0xFFFFFFFFu && t_lo > t_prev) ? t_lo - t_prev : 0u;
+      const uint32_t d = min(d_now, S.drift);
       uint32_t na = nt;
-      if (t_prev != 0xFFFFFFFFu && t_lo > t_prev && nt != 0xFFFFFFFFu) {
+      if (d > 0 && nt != 0xFFFFFFFFu) {
         const float a = fmaxf(0.f, fminf(0.5f, S.alpha));
-        na = nt + (uint32_t)(a * (float)(t_lo - t_prev));
+        na = nt + (uint32_t)(a * (float)d);
         na = min(na, 0x7F800000u);
       }
-      if (lane == 0) { S.next_thr = na; S.next_safe = nt; }
+      if (lane == 0) { S.next_thr = na; S.next_safe = nt; S.drift = d_now; }
     }
     if (lane == 0) { S.prefix = (S.prefix << (mode == 2 ? 11 : 9)) | bin; S.kleft -= above; }
   }

@@ -48,6 +48,7 @@ struct LayerSel {
   float band;        // band width as a multiple of k_l in this call's distribution (adaptive; 0 = unset)
   uint32_t next_safe;// the same band without the drift lead (level-1 refill threshold)
   float alpha;       // share of the last drift of T the next band leads by (adaptive)
+  uint32_t drift;    // this layer's last upward drift of T (key units; 0 = none or downward)
 };
 
 struct DevPlan {
