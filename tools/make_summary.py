@@ -129,7 +129,9 @@ bandwidth; TMA staging added barrier/latency structure without adding bytes in f
               f"{x['gate_bj5']['frac']:.2f} | {x['roofline']['frac']:.2f} | {x['recovery']['ms']:.1f} ms |\n")
     t += f"""| C4 GPT-2 XL 1% (default line) | {d['ms_per_step']:.3f} ({d['per_step_ms']['p10']:.3f}–{d['per_step_ms']['p90']:.3f}) | {d['gate_bj5']['frac']:.2f} | {d['roofline']['frac']:.2f} | {rec['ms']:.1f} ms |
 
-ResNet-50 sits at the gate (0.57–0.68 across runs): its ~20 dependent kernels take 3–50 µs each
+ResNet-50 sits just below the gate (0.53 with the PCIe rate timed by CUDA events, best of 10; earlier
+lines read 0.57–0.68 against a slower wall-clock PCIe sample, which inflated the floor): its 17
+dependent kernels per step take 3–50 µs each
 (latency, not bytes), the CUDA graphs remove the launch gaps (197 → 168–182 µs), and the block's
 D2H, which overlaps the next compress, adds a cost per kernel boundary while it is in flight
 (DESIGN.md §4.4). Its replay of 20 Adam steps at N = 8 (gate ≤ 3.15 ms) is far inside the bound.
