@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(256) digit_kernel(DevPlan P, int d) {
 // gives the ties taken before it and its output offset, then the ordered emit (the candidates are
 // read once from DRAM; the emit's second read hits L1/L2).  The layer's first chunk also does the
 // per-layer bookkeeping the layer scan did (sel_T, next thresholds, layer_total reset).
-__global__ void __launch_bounds__(256) count_emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K) {
+__global__ void __launch_bounds__(256, 8) count_emit_kernel(DevPlan P, uint32_t* __restrict__ send, uint64_t K) {
   pdl_wait();
   pdl_trigger();
   const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
