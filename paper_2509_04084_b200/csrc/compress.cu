@@ -45,7 +45,10 @@ constexpr int kHistRow = kH0 + kH1 + kH2;
 constexpr int kScanWarps = LD_SCAN_WARPS;           // segments per scan CTA
 constexpr int kPiecesPerChunk = kSegsPerChunk / kScanWarps;   // 4 scan CTAs per chunk
 constexpr int kJ = 1;                               // float4 per lane per scan round
-constexpr int kUnroll = 4;                          // candidate rounds in flight per warp
+#ifndef LD_UNROLL
+#define LD_UNROLL 4
+#endif
+constexpr int kUnroll = LD_UNROLL;                  // candidate rounds in flight per warp
 
 __device__ __forceinline__ float f4get(const float4& v, int q) {
   return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
