@@ -39,7 +39,7 @@ synthetic gradients, CUDA graphs on, unless a config says otherwise. Peaks from 
 (HBM copy {d['roofline']['peak']} GB/s, "of measured"). Regenerate with `python tools/make_summary.py`.
 
 Files (all from the same code, final refresh of round 1):
-- `r01_bench_gpt2xl.json` — the default `bench.py --steps 20 --warmup 8` line (every leg).
+- `r01_bench_gpt2xl.json` — the default `bench.py --steps 20` line (every leg; 20 warm-up iterations).
 - `r01_bench_{{resnet50,bert_large,gpt2_1000,gpt2_2500,gpt2_5000}}.json` — `tools/run_configs.sh`:
   C2, C3 and the C4 density sweep (0.1 / 0.25 / 0.5%); `r01_bench_snapshot_gpt2xl.json` — M3 leg;
   `r01_bench_recovery_files_gpt2xl.json` — `--recovery-files 100` (recovery from local files).
@@ -47,12 +47,14 @@ Files (all from the same code, final refresh of round 1):
   `--clock-control none`, serialised cold-cache launches; our kernels only, steady state);
   `r01_launches_gpt2xl_agg.txt` = its per-kernel aggregate (`python tools/launches.py … agg`).
 - `r01_ncu_full_summary.csv` — `ncu --set full` of scan / chunk_prep / emit / merge1 / update /
-  replay, one steady-state launch each (`python tools/ncu_summary.py …`).
+  replay / union, one steady-state launch each (call 21 of the step loop) (`python tools/ncu_summary.py …`).
 - `ncu_traffic.json` — DRAM bytes per scan launch (feeds `roofline.traffic`).
 - `r01_stream_probe*.txt` — achievable HBM bandwidth for the access patterns (copy 6.77 TB/s,
   `r += g` 7.11 TB/s, 2-stream read 7.40 TB/s with full grids).
 - `r01_d2h_interference_probe.txt` — what a concurrent D2H does to HBM-bound kernels (a cost per
-  kernel boundary, DESIGN.md §4.4); `r01_sanitizer.txt` — compute-sanitizer memcheck / racecheck.
+  kernel boundary, DESIGN.md §4.4); `r01_sanitizer.txt` — compute-sanitizer memcheck / racecheck /
+  synccheck / initcheck; `r01_pdl_ab.txt` — A/B records of the late variants (programmatic
+  dependent launch adopted; persistent merge, wider tile index grid, candidate unroll 8 dropped).
 
 ## Bench line (bench.py, N = 1)
 
