@@ -71,8 +71,12 @@ typedef struct {
   int32_t error_feedback;      /* 1: acc = residual + grad, residual' = unsent part (default)  */
   int32_t mean;                /* 1: merged G = sum / world (default); 0: sum                  */
   int32_t rank, world;         /* data-parallel rank and world size                            */
-  const void *nccl_unique_id;  /* 128-byte ncclUniqueId from rank 0 (world > 1).  NULL: no
-                                  communicator -- a recovery/merge-only context (exchange then
+  const void *nccl_unique_id;  /* 128-byte ncclUniqueId from rank 0 (lowdiff_nccl_unique_id,
+                                  broadcast by the caller).  Given: an NCCL communicator of
+                                  `world` ranks -- also at world 1 (a 1-rank communicator, so
+                                  the allgather / broadcasts run through NCCL).  NULL: no
+                                  communicator -- world 1 merges straight from the send block;
+                                  world > 1 is a recovery/merge-only context (exchange then
                                   returns LOWDIFF_E_STATE)                                     */
   int32_t device;              /* CUDA device ordinal this context drives                      */
   const char *ckpt_dir;        /* directory for .ldb/.ldf files; NULL disables persistence     */
@@ -87,7 +91,7 @@ typedef struct {
 typedef struct lowdiff_ctx lowdiff_ctx;
 
 /* Create a context: validates the layer table, builds the chunk plan, allocates device
- * scratch and the pinned ring, initialises NCCL (world > 1) and starts the writer thread.
+ * scratch and the pinned ring, initialises NCCL (when an id is given) and starts the writer thread.
  * Synchronous.  *out is NULL on failure. */
 lowdiff_status lowdiff_create(const lowdiff_config *cfg, lowdiff_ctx **out);
 
@@ -126,7 +130,8 @@ lowdiff_status lowdiff_compress(lowdiff_ctx *ctx, const float *grad, float *resi
 lowdiff_status lowdiff_residual_materialize(lowdiff_ctx *ctx, float *residual, void *stream);
 
 /* 2. Exchange (Alg. 1 lines 5 and 7): ncclAllGather of the fixed-size
- *    blocks (rank r's block lands at gathered + r*2K), then the merge
+ *    blocks (rank r's block lands at gathered + r*2K; with a communicator this also runs at
+ *    world 1 when `gathered` is given), then the merge
  *      G[j] = ((((+0 + v_0[j]) + v_1[j]) + ... ) + v_{N-1}[j]) / N   (rank order, IEEE divide)
  *    where v_r[j] is rank r's value when j is among its indices.  No atomics: deterministic.
  *    send: device u32[2K].  gathered: device u32[world*2K] (may be NULL when world == 1).
@@ -179,7 +184,10 @@ lowdiff_status lowdiff_exchange_update(lowdiff_ctx *ctx, const uint32_t *send, u
  *    rank's own send block (8K bytes) into a pinned-host ring slot.  The writer thread
  *    groups b consecutive iterations into one .ldb file written with one writev
  *    (`*.tmp`, then rename).  `iteration` must be the previous call's + 1 (else
- *    LOWDIFF_E_STATE).  Blocks on the host only while the ring is full (backpressure);
+ *    LOWDIFF_E_STATE), except for the first call of a context and the first after a recovery /
+ *    replica restore, which (re)start the sequence at `iteration` and first retire this rank's
+ *    files holding iterations >= `iteration` (lowdiff_retire_from kinds .ldb|.ldf; E_IO if that
+ *    fails).  Blocks on the host only while the ring is full (backpressure);
  *    the blocked time is reported by lowdiff_stats.  scalars: host pointer. */
 lowdiff_status lowdiff_batch_persist(lowdiff_ctx *ctx, int64_t iteration,
                                      const lowdiff_step_scalars *scalars, const uint32_t *send,
@@ -207,7 +215,10 @@ lowdiff_status lowdiff_full_ckpt(lowdiff_ctx *ctx, int64_t iteration, const floa
  *    (LOWDIFF_E_CORRUPT); target = -1 replays the longest gap-free chain.  Loads C^F into
  *    p, m, v (device f32[Psi]; m, v may be NULL for SGD), replays the blocks through the
  *    optimizer recorded in the files with the fused replay kernel, and stores the
- *    iteration reached in *recovered.  Synchronous (returns after the replay finished). */
+ *    iteration reached in *recovered.  Synchronous (returns after the replay finished).
+ *    Afterwards persisting may resume at *recovered + 1: the next lowdiff_batch_persist /
+ *    lowdiff_union_persist accepts any iteration t and first retires this rank's files holding
+ *    iterations >= t (lowdiff_retire_from), so blocks of the abandoned run never enter a chain. */
 lowdiff_status lowdiff_recover(lowdiff_ctx *ctx, int64_t target, float *p, float *m, float *v,
                                int64_t *recovered, void *stream);
 
@@ -228,7 +239,8 @@ lowdiff_status lowdiff_replay(lowdiff_ctx *ctx, int32_t optim, int32_t world, in
  *    floor((rank+1)*Psi/world)) only: reads only this rank's .ldf shard, uploads only the entries
  *    of each differential block that fall in the shard (the indices ascend, so they are one
  *    contiguous run per block), and replays only the shard into p, m, v (device f32[Psi];
- *    elements outside the shard are not touched).  gather != 0 (world > 1, NCCL context needed):
+ *    elements outside the shard are not touched).  gather != 0 (NCCL context needed if world > 1;
+ *    with a 1-rank communicator the broadcast runs too):
  *    then fills the other shards from their owners by NCCL broadcasts, so every rank ends with
  *    the full state.  Chain selection (F, last) is exactly that of lowdiff_recover (all ranks
  *    agree).  Synchronous. */
@@ -342,8 +354,10 @@ lowdiff_status lowdiff_replica_wait(lowdiff_ctx *ctx, int64_t *iteration, const 
                                     const float **v, int64_t *shard_begin, int64_t *shard_end);
 /* replica_restore: drain, then copy the replica into device p, m, v (f32[Psi]; m, v may be NULL
  *    for SGD): this rank's shard H2D, the other shards by an NCCL broadcast from their owners
- *    (world > 1: every rank must call it; needs an NCCL context).  Synchronous on `stream`;
- *    *iteration = the restored iteration. */
+ *    (world > 1: every rank must call it; needs an NCCL context; a 1-rank communicator also
+ *    broadcasts).  Synchronous on `stream`; *iteration = the restored iteration.  Persisting may
+ *    then resume at *iteration + 1 (its first lowdiff_batch_persist retires the abandoned run's
+ *    files, see lowdiff_retire_from). */
 lowdiff_status lowdiff_replica_restore(lowdiff_ctx *ctx, float *p, float *m, float *v, int64_t *iteration,
                                        void *stream);
 /* Host optimizer used by the replica (no context; element-wise over n, split over `threads`
@@ -411,6 +425,15 @@ lowdiff_status lowdiff_chain_scan(const lowdiff_config *cfg, int64_t target, int
 lowdiff_status lowdiff_write_batch_host(const lowdiff_config *cfg, int64_t first_iter,
                                         int32_t n_iters, const lowdiff_step_scalars *scalars,
                                         const uint32_t *blocks);
+/* Restart hygiene (host only): remove / truncate this rank's (cfg->rank) files in cfg->ckpt_dir that
+ * hold iterations >= `iteration` -- they belong to an abandoned run.  kinds: bit0 .ldb (files
+ * starting at >= iteration removed, a file straddling it rewritten atomically with its blocks <
+ * iteration), bit1 .ldu (same), bit2 .ldf (iterations >= iteration removed).  lowdiff_batch_persist
+ * (kinds .ldb|.ldf) and lowdiff_union_persist (.ldu|.ldf) call it on their first call of a context
+ * and on their first call after lowdiff_recover* / lowdiff_replica_restore, which re-open the
+ * iteration sequence (the next persisted iteration may then be any value).  E_IO if a file cannot
+ * be removed or rewritten. */
+lowdiff_status lowdiff_retire_from(const lowdiff_config *cfg, int64_t iteration, int32_t kinds);
 /* Serialise this rank's full-checkpoint shard from host arrays of length Psi (host only). */
 lowdiff_status lowdiff_write_full_host(const lowdiff_config *cfg, int64_t iteration, const float *p,
                                        const float *m, const float *v);
@@ -420,12 +443,20 @@ lowdiff_status lowdiff_write_full_host(const lowdiff_config *cfg, int64_t iterat
  * S full-checkpoint bytes, T total run time, R_F time to load a full checkpoint, R_D time to
  * merge one differential. */
 typedef struct { double N, M, W, S, T, R_F, R_D; } lowdiff_sys_params;
-/* Eq. 3: T_wasted(f, b) for f full checkpoints per time unit and b differentials per batch. */
+/* Eq. 3: T_wasted(f, b) for f full checkpoints per time unit and b differentials per batch.
+ * The model's domain is f b <= 1 (a batch inside one full-checkpoint interval): f b > 1 -> E_INVALID
+ * (also for lowdiff_simulate_failures). */
 lowdiff_status lowdiff_wasted_time(const lowdiff_sys_params *p, double f, double b, double *out);
 /* Eq. 5: the stationary point f* = cbrt(R_D W^2/(4 S^2 M^2)), b* = cbrt(2 S R_D M / W). */
 lowdiff_status lowdiff_optimal_config(const lowdiff_sys_params *p, double *f_star, double *b_star);
+/* Eq. 5 clamped to f b <= 1: (f*, b*) when f* b* <= 1 (*clamped = 0); else the minimum of Eq. 3 on
+ * the boundary f b = 1, f = sqrt(W / (2 M S)), b = 1/f (*clamped = 1).  f_unc / b_unc (optional)
+ * receive the unconstrained Eq. 5 point. */
+lowdiff_status lowdiff_optimal_config_feasible(const lowdiff_sys_params *p, double *f_opt, double *b_opt,
+                                               double *f_unc, double *b_unc, int32_t *clamped);
 /* One stepwise adaptation of the integer configuration (full-checkpoint interval *fcf in time
- * units, batch size *batch) toward the rounded optimum, applied only if it lowers Eq. 3. */
+ * units, batch size *batch <= *fcf) toward the rounded feasible optimum, applied only if it lowers
+ * Eq. 3; the step never leaves batch <= fcf. */
 lowdiff_status lowdiff_config_step(const lowdiff_sys_params *p, int64_t *fcf, int32_t *batch);
 /* Failure-injection simulator: failures of the N GPUs as a Poisson process of rate
  * N / M over the productive time [0, T) (inter-arrival -log(1 - u) M / N; u from splitmix64 over a

@@ -17,5 +17,5 @@ def build(verbose: bool = False) -> str:
 
 
 from .lowdiff import (ADAM, SGD, Context, LowDiffError, Options, StepScalars, bucket_plan, chain_scan,  # noqa: E402,F401
-                      crc32c, derive_adam_consts, derive_step_scalars, nccl_unique_id, write_batch_host,
+                      crc32c, derive_adam_consts, derive_step_scalars, nccl_unique_id, retire_from, write_batch_host,
                       write_full_host)

@@ -4,6 +4,7 @@
 // union_api.cpp; LowDiff+ snapshot and CPU replica: lowdiff_plus.cpp.  Kernels: *.cu.
 // See include/lowdiff.h.
 #include <dirent.h>
+#include <cerrno>
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
@@ -391,6 +392,71 @@ lowdiff_status scan_chain(const lowdiff_config& cfg, int64_t target, Chain* ch, 
   return LOWDIFF_OK;
 }
 
+// Restart hygiene: when persisting (re)starts at iteration t -- the first
+// batch_persist / union_persist of a context, or the first after a recovery -- every file of this
+// rank that holds iterations >= t belongs to an abandoned run (blocks t.. of the previous
+// trajectory, full checkpoints of states >= t).  Left in place, the chain rule "the file with the
+// later first iteration wins" could splice its blocks into the new run's chain (an old
+// ..._000000000008.ldb would override blocks 8.. of a new ..._000000000007.ldb), or extend the
+// chain past the new run's last block.  So: files starting at >= t are removed; a batch file
+// straddling t is rewritten (atomically) with only its blocks < t; .ldf files of iterations >= t
+// are removed.  kinds: bit0 .ldb, bit1 .ldu, bit2 .ldf.
+static bool rewrite_prefix_blocks(const std::string& path, size_t head, int64_t first, int64_t keep, bool ldu,
+                                  bool do_fsync, std::string* err) {
+  std::vector<uint8_t> buf;
+  if (!read_all(path, buf) || buf.size() < head + 4) return false;
+  if (lowdiff_crc32c(buf.data(), buf.size() - 4) != rd<uint32_t>(buf.data() + buf.size() - 4)) return false;
+  const uint64_t K = rd<uint64_t>(buf.data() + 40);
+  size_t off = head;
+  for (int64_t i = 0; i < keep; ++i) {
+    if (off + 32 > buf.size() - 4 || (int64_t)rd<uint64_t>(buf.data() + off) != first + i) return false;
+    const uint64_t n = ldu ? rd<uint32_t>(buf.data() + off + 20) : K;
+    off += 32 + 8 * n;
+  }
+  if (off > buf.size() - 4) return false;
+  const uint32_t n_it = (uint32_t)keep;
+  std::memcpy(buf.data() + 24, &n_it, 4);
+  const uint32_t crc = lowdiff_crc32c(buf.data(), off);
+  return ld::write_file_atomic(path, {{buf.data(), off}, {&crc, 4}}, do_fsync, err) == LOWDIFF_OK;
+}
+
+lowdiff_status retire_from(const lowdiff_config& cfg, int64_t t, int kinds, std::string* err) {
+  if (!cfg.ckpt_dir) return LOWDIFF_OK;
+  DIR* d = opendir(cfg.ckpt_dir);
+  if (!d) return LOWDIFF_OK;   // nothing persisted yet
+  std::vector<std::pair<std::string, int>> mine;   // (name, kind bit)
+  while (dirent* de = readdir(d)) {
+    unsigned r; long long it;
+    if ((kinds & 1) && parse_name(de->d_name, "diff", "ldb", &r, &it) && r == (unsigned)cfg.rank) mine.push_back({de->d_name, 1});
+    else if ((kinds & 2) && parse_name(de->d_name, "union", "ldu", &r, &it) && r == (unsigned)cfg.rank) mine.push_back({de->d_name, 2});
+    else if ((kinds & 4) && parse_name(de->d_name, "full", "ldf", &r, &it) && r == (unsigned)cfg.rank) mine.push_back({de->d_name, 4});
+  }
+  closedir(d);
+  for (auto& f : mine) {
+    unsigned r; long long it;
+    const char* kind = f.second == 1 ? "diff" : f.second == 2 ? "union" : "full";
+    const char* ext = f.second == 1 ? "ldb" : f.second == 2 ? "ldu" : "ldf";
+    parse_name(f.first.c_str(), kind, ext, &r, &it);
+    const std::string path = std::string(cfg.ckpt_dir) + "/" + f.first;
+    if (it >= t) {
+      if (::unlink(path.c_str()) != 0 && errno != ENOENT) { *err = "cannot remove stale " + path; return LOWDIFF_E_IO; }
+      continue;
+    }
+    if (f.second == 4) continue;
+    uint8_t h[32];
+    size_t fsz = 0;
+    if (!read_head(path, h, 32, &fsz)) continue;     // unreadable: recovery reports it as before
+    const int64_t n = rd<uint32_t>(h + 24);
+    if (it + n <= t) continue;                       // entirely before the restart
+    const size_t head = f.second == 1 ? 96 + 16 * (size_t)cfg.n_layers : 112 + 16 * (size_t)cfg.n_layers;
+    if (!rewrite_prefix_blocks(path, head, it, t - it, f.second == 2, cfg.fsync != 0, err)) {
+      if (err->empty()) *err = "cannot truncate stale blocks of " + path;
+      return LOWDIFF_E_IO;
+    }
+  }
+  return LOWDIFF_OK;
+}
+
 lowdiff_status validate_cfg(const lowdiff_config* cfg) {
   if (!cfg || cfg->n_layers <= 0 || !cfg->numel) return LOWDIFF_E_INVALID;
   if (cfg->density_ppm < 1 || cfg->density_ppm > 1000000) return LOWDIFF_E_INVALID;
@@ -558,7 +624,10 @@ lowdiff_status lowdiff_create(const lowdiff_config* cfg, lowdiff_ctx** out) {
     return bail(LOWDIFF_E_CUDA);
   for (int i = 0; i < 2; ++i)
     if (cudaEventCreateWithFlags(&c->snap_done[i], cudaEventDisableTiming) != cudaSuccess) return bail(LOWDIFF_E_CUDA);
-  if (cfg->world > 1 && cfg->nccl_unique_id) {   // no id: recovery / merge-only context
+  // An NCCL communicator whenever an id is given -- also at world 1 (a 1-rank communicator: the
+  // allgather is then a device copy, but every NCCL call site runs).  No id: world 1 merges straight
+  // from the send block; world > 1 without an id is a recovery / merge-only context.
+  if (cfg->nccl_unique_id) {
     ncclUniqueId id;
     std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
     if (ncclCommInitRank(&c->comm, cfg->world, id, cfg->rank) != ncclSuccess) return bail(LOWDIFF_E_NCCL);
@@ -842,7 +911,7 @@ lowdiff_status lowdiff_exchange(lowdiff_ctx* c, const uint32_t* send, uint32_t* 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!send || !dense_out || (c->cfg.world > 1 && !gathered)) return fail(c, LOWDIFF_E_INVALID, "exchange: NULL buffer");
   const size_t blk = 2 * (size_t)c->K;
-  if (c->cfg.world > 1) {
+  if (c->cfg.world > 1 || (c->comm && gathered)) {
     if (!c->comm) return fail(c, LOWDIFF_E_STATE, "exchange: context was created without an NCCL id");
     int h;
     ld::prof_begin(c, "allgather", s, &h);
@@ -867,7 +936,7 @@ lowdiff_status lowdiff_exchange_update(lowdiff_ctx* c, const uint32_t* send, uin
   if (!send || !scalars || (c->cfg.world > 1 && !gathered)) return fail(c, LOWDIFF_E_INVALID, "exchange_update: NULL buffer");
   const size_t blk = 2 * (size_t)c->K;
   const uint32_t* blocks = send;
-  if (c->cfg.world > 1) {
+  if (c->cfg.world > 1 || (c->comm && gathered)) {
     if (!c->comm) return fail(c, LOWDIFF_E_STATE, "exchange_update: context was created without an NCCL id");
     int h;
     ld::prof_begin(c, "allgather", s, &h);
@@ -893,6 +962,11 @@ lowdiff_status lowdiff_batch_persist(lowdiff_ctx* c, int64_t iteration, const lo
   if (c->next_iter >= 0 && iteration != c->next_iter)
     return fail(c, LOWDIFF_E_STATE, "batch_persist: iteration " + std::to_string(iteration) + " after " +
                                         std::to_string(c->next_iter - 1) + " (must be consecutive)");
+  if (c->next_iter < 0 && c->cfg.write_files) {   // persisting (re)starts here: retire the abandoned run
+    if (c->full_writer.joinable()) c->full_writer.join();
+    std::string err;
+    if ((st = retire_from(c->cfg, iteration, 1 | 4, &err))) return fail(c, st, err);
+  }
   int slot;
   {
     std::unique_lock<std::mutex> lk(c->mu);
@@ -976,9 +1050,6 @@ lowdiff_status lowdiff_full_ckpt(lowdiff_ctx* c, int64_t iteration, const float*
   // Without the device memory for the stage, the snapshot goes straight D2H.
   if (c->full_stage_cap < 3 * S) {
     if (c->full_stage) cudaFree(c->full_stage);
-  for (void* q : c->peer_opened) cudaIpcCloseMemHandle(q);
-  for (uint32_t* q : c->peer_own) cudaFree(q);
-  if (c->peer_flags) cudaFree(c->peer_flags);
     c->full_stage = nullptr;
     c->full_stage_cap = 0;
     if (cudaMalloc((void**)&c->full_stage, std::max<size_t>(1, 3 * S) * 4) == cudaSuccess) c->full_stage_cap = 3 * S;
@@ -1099,6 +1170,12 @@ lowdiff_status lowdiff_write_batch_host(const lowdiff_config* cfg, int64_t first
   std::string err;
   return ld::write_file_atomic(ld::batch_name(cfg->ckpt_dir, cfg->rank, first_iter),
                                {{pre.data(), pre.size()}, {body.data(), body.size()}, {&crc, 4}}, cfg->fsync != 0, &err);
+}
+
+lowdiff_status lowdiff_retire_from(const lowdiff_config* cfg, int64_t iteration, int32_t kinds) {
+  if (validate_cfg(cfg) || !cfg->ckpt_dir || iteration < 0 || kinds < 0 || kinds > 7) return LOWDIFF_E_INVALID;
+  std::string err;
+  return retire_from(*cfg, iteration, kinds, &err);
 }
 
 lowdiff_status lowdiff_write_full_host(const lowdiff_config* cfg, int64_t iteration, const float* p, const float* m,

@@ -41,6 +41,8 @@ bool read_all(const std::string& path, std::vector<uint8_t>& out);
 bool read_head(const std::string& path, uint8_t* buf, size_t n, size_t* fsize);
 template <class T> T rd(const uint8_t* p) { T v; std::memcpy(&v, p, sizeof v); return v; }
 lowdiff_status scan_chain(const lowdiff_config& cfg, int64_t target, Chain* ch, std::string* err);
+// remove / truncate this rank's files holding iterations >= t (kinds: bit0 .ldb, bit1 .ldu, bit2 .ldf)
+lowdiff_status retire_from(const lowdiff_config& cfg, int64_t t, int kinds, std::string* err);
 
 // recover.cpp
 lowdiff_status bcast_shards(lowdiff_ctx* c, float* dst[3], cudaStream_t s);

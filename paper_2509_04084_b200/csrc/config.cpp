@@ -17,8 +17,10 @@ extern "C" {
 
 // Eq. 3:
 //   T_wasted = (N T / M) (b/2 + R_F + R_D/2 (1/(f b) - 1)) + N T S f / W
+// The model needs f b <= 1 (a batch never spans more than one full-checkpoint interval; otherwise
+// the merge-count term R_D/2 (1/(f b) - 1) would be negative): f b > 1 is E_INVALID.
 lowdiff_status lowdiff_wasted_time(const lowdiff_sys_params* p, double f, double b, double* out) {
-  if (!valid(p) || !out || f <= 0 || b <= 0) return LOWDIFF_E_INVALID;
+  if (!valid(p) || !out || !(f > 0) || !(b > 0) || f * b > 1.0) return LOWDIFF_E_INVALID;
   const double failures = p->N * p->T / p->M;                      // N x (T / M)
   const double recovery = b / 2.0 + p->R_F + p->R_D / 2.0 * (1.0 / (f * b) - 1.0);
   const double steady = p->N * p->T * p->S * f / p->W;              // N x (S / W) x f T
@@ -35,14 +37,37 @@ lowdiff_status lowdiff_optimal_config(const lowdiff_sys_params* p, double* f_sta
   return LOWDIFF_OK;
 }
 
+// Eq. 5 restricted to the model's domain f b <= 1.  When the stationary point lies outside it,
+// Eq. 3 is minimised on the boundary f b = 1, where the merge term vanishes:
+//   T(f, 1/f) = (N T / M)(1/(2 f) + R_F) + N T S f / W  ->  f_c = sqrt(W / (2 M S)), b_c = 1 / f_c.
+lowdiff_status lowdiff_optimal_config_feasible(const lowdiff_sys_params* p, double* f_opt, double* b_opt,
+                                               double* f_unc, double* b_unc, int32_t* clamped) {
+  if (!valid(p) || !f_opt || !b_opt) return LOWDIFF_E_INVALID;
+  double fs, bs;
+  lowdiff_optimal_config(p, &fs, &bs);
+  if (f_unc) *f_unc = fs;
+  if (b_unc) *b_unc = bs;
+  const bool out = fs * bs > 1.0;
+  if (clamped) *clamped = out ? 1 : 0;
+  if (!out) {
+    *f_opt = fs;
+    *b_opt = bs;
+  } else {
+    *f_opt = std::sqrt(p->W / (2.0 * p->M * p->S));
+    *b_opt = 1.0 / *f_opt;
+  }
+  return LOWDIFF_OK;
+}
+
 // Stepwise runtime adaptation: move the integer configuration (full-checkpoint
 // interval in iterations, batch size) one step toward the rounded Eq. 5 optimum for the current
 // parameter estimates -- one iteration of FCF change per 10% of distance (at least 1), one batch
 // step -- but only while the step lowers Eq. 3.
 lowdiff_status lowdiff_config_step(const lowdiff_sys_params* p, int64_t* fcf, int32_t* batch) {
   if (!valid(p) || !fcf || !batch || *fcf < 1 || *batch < 1) return LOWDIFF_E_INVALID;
+  if (*batch > *fcf) return LOWDIFF_E_INVALID;   // f b <= 1: the batch fits the full interval
   double fs, bs;
-  lowdiff_optimal_config(p, &fs, &bs);
+  lowdiff_optimal_config_feasible(p, &fs, &bs, nullptr, nullptr, nullptr);
   const int64_t fcf_t = std::llround(std::fmax(1.0, 1.0 / fs));
   const int32_t b_t = (int32_t)std::lround(std::fmax(1.0, bs));
   int64_t nf = *fcf;
@@ -52,6 +77,7 @@ lowdiff_status lowdiff_config_step(const lowdiff_sys_params* p, int64_t* fcf, in
     nf += d > 0 ? stp : -stp;
   }
   int32_t nb = *batch + (b_t > *batch ? 1 : (b_t < *batch ? -1 : 0));
+  if (nb > nf) nb = (int32_t)nf;   // stay inside f b <= 1
   double cur, nxt;
   lowdiff_wasted_time(p, 1.0 / (double)*fcf, (double)*batch, &cur);
   lowdiff_wasted_time(p, 1.0 / (double)nf, (double)nb, &nxt);
@@ -80,7 +106,8 @@ struct SplitMix {
 
 lowdiff_status lowdiff_simulate_failures(const lowdiff_sys_params* p, double f, double b, double sw_fraction,
                                          double R_S, uint64_t seed, lowdiff_sim_report* out) {
-  if (!valid(p) || !out || !(f > 0) || !(b > 0) || !(sw_fraction >= 0 && sw_fraction <= 1) || !(R_S >= 0))
+  if (!valid(p) || !out || !(f > 0) || !(b > 0) || f * b > 1.0 || !(sw_fraction >= 0 && sw_fraction <= 1) ||
+      !(R_S >= 0))
     return LOWDIFF_E_INVALID;
   SplitMix rng{seed};
   const double mean_gap = p->M / p->N, interval = 1.0 / f;

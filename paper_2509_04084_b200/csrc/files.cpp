@@ -149,15 +149,29 @@ lowdiff_status write_file_atomic(const std::string& path, const std::vector<std:
   if (do_fsync && ::fsync(fd) != 0) {
     *err = "fsync " + tmp + ": " + std::strerror(errno);
     ::close(fd);
+    ::unlink(tmp.c_str());
     return LOWDIFF_E_IO;
   }
   if (::close(fd) != 0) {
     *err = "close " + tmp + ": " + std::strerror(errno);
+    ::unlink(tmp.c_str());
     return LOWDIFF_E_IO;
   }
   if (::rename(tmp.c_str(), path.c_str()) != 0) {
     *err = "rename " + tmp + ": " + std::strerror(errno);
+    ::unlink(tmp.c_str());
     return LOWDIFF_E_IO;
+  }
+  if (do_fsync) {   // the rename itself is durable only once the directory entry is on storage
+    const size_t slash = path.find_last_of('/');
+    const std::string dir = slash == std::string::npos ? "." : (slash == 0 ? "/" : path.substr(0, slash));
+    const int dfd = ::open(dir.c_str(), O_RDONLY | O_DIRECTORY | O_CLOEXEC);
+    if (dfd < 0 || ::fsync(dfd) != 0) {
+      *err = "fsync directory " + dir + ": " + std::strerror(errno);
+      if (dfd >= 0) ::close(dfd);
+      return LOWDIFF_E_IO;
+    }
+    ::close(dfd);
   }
   return LOWDIFF_OK;
 }
@@ -165,6 +179,8 @@ lowdiff_status write_file_atomic(const std::string& path, const std::vector<std:
 // ---------------------------------------------------------------- CRC-32C combination
 // crc(A || B) from crc(A), crc(B) and |B|: appending |B| zero bytes to A is a linear map over GF(2)
 // on the 32-bit CRC register; it is applied by squaring the one-zero-bit operator (log |B| steps).
+// Attribution: this is the standard zero-extension scheme of zlib's crc32_combine (Mark Adler,
+// zlib license) -- same odd/even operator squaring -- with the reflected Castagnoli polynomial.
 static uint32_t gf2_times(const uint32_t* mat, uint32_t vec) {
   uint32_t sum = 0;
   for (int i = 0; vec; ++i, vec >>= 1)

@@ -299,9 +299,14 @@ lowdiff_status lowdiff_replica_restore(lowdiff_ctx* c, float* p, float* m, float
   float* dst[3] = {p, m, v};
   for (int a = 0; a < 3; ++a)
     if (dst[a] && S) CK(cudaMemcpyAsync(dst[a] + c->rep_sb, c->rep_host + a * S, S * 4, cudaMemcpyHostToDevice, s));
-  if (c->cfg.world > 1 && (st = bcast_shards(c, dst, s))) return st;
+  if (c->comm && (st = bcast_shards(c, dst, s))) return st;   // world 1 with NCCL: a 1-rank broadcast
   CK(cudaStreamSynchronize(s));
   if (iteration) *iteration = c->rep_iter.load();
+  // training resumes at rep_iter + 1: drain the persistence of the abandoned steps, then let the next
+  // batch_persist start anywhere (its first call retires the abandoned run's files, api.cpp)
+  if ((st = lowdiff_sync(c))) return st;
+  c->next_iter = -1;
+  c->u_next_iter = -1;
   return LOWDIFF_OK;
 }
 

@@ -320,6 +320,8 @@ static lowdiff_status recover_impl(lowdiff_ctx* c, int64_t target, float* p, flo
   if (result) return result;
   CK(cudaStreamSynchronize(s));
   if (recovered) *recovered = ch.last;
+  c->next_iter = -1;     // persisting may resume at ch.last + 1; its first call retires the abandoned run
+  c->u_next_iter = -1;
   return LOWDIFF_OK;
 }
 
@@ -331,7 +333,7 @@ lowdiff_status lowdiff_recover(lowdiff_ctx* c, int64_t target, float* p, float* 
 lowdiff_status lowdiff_recover_sharded(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int32_t gather,
                                        int64_t* recovered, void* stream) {
   lowdiff_status st = recover_impl(c, target, p, m, v, recovered, stream, true);
-  if (st || !gather || c->cfg.world == 1) return st;
+  if (st || !gather || (c->cfg.world == 1 && !c->comm)) return st;   // world 1 without NCCL: nothing to gather
   if (!c->comm) return fail(c, LOWDIFF_E_STATE, "recover_sharded: gather needs an NCCL context");
   float* dst[3] = {p, m, v};
   if ((st = bcast_shards(c, dst, static_cast<cudaStream_t>(stream)))) return st;

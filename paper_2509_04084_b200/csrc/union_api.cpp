@@ -230,6 +230,11 @@ lowdiff_status lowdiff_union_persist(lowdiff_ctx* c, int64_t iteration, const lo
   if (c->u_next_iter >= 0 && iteration != c->u_next_iter)
     return fail(c, LOWDIFF_E_STATE, "union_persist: iteration " + std::to_string(iteration) + " after " +
                                         std::to_string(c->u_next_iter - 1) + " (must be consecutive)");
+  if (c->u_next_iter < 0 && c->cfg.write_files) {   // persisting (re)starts here: retire the abandoned run
+    if (c->full_writer.joinable()) c->full_writer.join();
+    std::string err;
+    if ((st = retire_from(c->cfg, iteration, 2 | 4, &err))) return fail(c, st, err);
+  }
   const uint64_t psi = (uint64_t)c->psi, rk = (uint64_t)c->cfg.rank, wd = (uint64_t)c->cfg.world;
   const uint64_t sb = psi * rk / wd, se = psi * (rk + 1) / wd;
   if (!c->u_buf[0]) {   // first call: buffers sized for the worst case min(N K, shard)
@@ -429,6 +434,8 @@ static lowdiff_status union_recover_impl(lowdiff_ctx* c, int64_t target, float* 
   }
   if (result) return result;
   if (recovered) *recovered = last;
+  c->u_next_iter = -1;   // persisting may resume at last + 1 (the abandoned run is retired then)
+  c->next_iter = -1;
   return LOWDIFF_OK;
 }
 

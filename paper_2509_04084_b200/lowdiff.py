@@ -123,10 +123,12 @@ def lib():
             "chain_scan": ([C.POINTER(Config), C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], S),
             "write_batch_host": ([C.POINTER(Config), C.c_int64, C.c_int32, C.POINTER(StepScalars), P], S),
             "write_full_host": ([C.POINTER(Config), C.c_int64, P, P, P], S),
+            "retire_from": ([C.POINTER(Config), C.c_int64, C.c_int32], S),
             "abi_version": ([], C.c_int32),
             "selftest": ([C.c_int32, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], S),
             "wasted_time": ([C.POINTER(SysParams), C.c_double, C.c_double, C.POINTER(C.c_double)], S),
             "optimal_config": ([C.POINTER(SysParams), C.POINTER(C.c_double), C.POINTER(C.c_double)], S),
+            "optimal_config_feasible": ([C.POINTER(SysParams)] + [C.POINTER(C.c_double)] * 4 + [C.POINTER(C.c_int32)], S),
             "config_step": ([C.POINTER(SysParams), C.POINTER(C.c_int64), C.POINTER(C.c_int32)], S),
             "simulate_failures": ([C.POINTER(SysParams), C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64,
                                    C.POINTER(SimReport)], S),
@@ -146,8 +148,8 @@ EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_mater
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
             "sync", "get_stats",
             "prof_enable", "prof_read", "kernel_launches", "set_graphs", "last_error", "nccl_unique_id",
-            "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host",
-            "write_full_host", "abi_version", "selftest", "wasted_time", "optimal_config", "config_step",
+            "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host", "retire_from",
+            "write_full_host", "abi_version", "selftest", "wasted_time", "optimal_config", "optimal_config_feasible", "config_step",
             "simulate_failures"]
 
 
@@ -163,6 +165,14 @@ def optimal_config(params: dict):
     f, b = C.c_double(), C.c_double()
     _check("optimal_config", lib().lowdiff_optimal_config(C.byref(SysParams(**params)), C.byref(f), C.byref(b)))
     return f.value, b.value
+
+
+def optimal_config_feasible(params: dict):
+    """Eq. 5 restricted to f b <= 1: (f, b, clamped, f_unconstrained, b_unconstrained)."""
+    f, b, fu, bu, cl = C.c_double(), C.c_double(), C.c_double(), C.c_double(), C.c_int32()
+    _check("optimal_config_feasible", lib().lowdiff_optimal_config_feasible(
+        C.byref(SysParams(**params)), C.byref(f), C.byref(b), C.byref(fu), C.byref(bu), C.byref(cl)))
+    return f.value, b.value, bool(cl.value), fu.value, bu.value
 
 
 def config_step(params: dict, fcf: int, batch: int):
@@ -540,6 +550,12 @@ def host_sgd_step(G, lr, p, threads=1):
     assert g.size == p.size
     _check("host_sgd_step", lib().lowdiff_host_sgd_step(p.size, g.ctypes.data_as(C.c_void_p), lr,
                                                         p.ctypes.data_as(C.c_void_p), threads))
+
+
+def retire_from(sizes, opts: Options, iteration, kinds=7):
+    """Remove / truncate opts.rank's files holding iterations >= iteration (restart hygiene)."""
+    cfg = make_config(sizes, opts)
+    _check("retire_from", lib().lowdiff_retire_from(C.byref(cfg), iteration, kinds))
 
 
 def write_full_host(sizes, opts: Options, iteration, p, m=None, v=None):

@@ -238,3 +238,57 @@ def test_bench_reference_arm_prints_one_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == "mlp@10000ppm"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+
+
+def _run_blocks(ref, sizes, ppm, seed, ts):
+    """Valid send blocks (oracle compress of seeded gradients, EF on) for iterations ts."""
+    psi = sum(sizes)
+    r = np.zeros(psi, np.float32)
+    out = []
+    for t in ts:
+        g = np.random.default_rng([seed, t]).standard_normal(psi).astype(np.float32)
+        blk, r = ref.compress(sizes, ppm, g, r, ef=True)
+        out.append(blk)
+    return np.stack(out)
+
+
+def test_restart_retires_the_abandoned_run(ref, tmp_path):
+    """after a recovery to iteration 6, persisting restarts at 7 with another batch
+    alignment.  The abandoned run's files holding iterations >= 7 (…05.ldb covers 5..8, …09.ldb
+    9..10) must not splice into the new chain.  lowdiff_retire_from(7) truncates …05 to 5..6 and
+    removes …09; the oracle then recovers exactly Full@0 + old 1..6 + new 7..12."""
+    o = _opts(tmp_path)
+    ppm, psi = o.density_ppm, sum(SIZES)
+    K = sum(ref.k_table(SIZES, ppm))
+    rng = np.random.default_rng(5)
+    p0 = rng.standard_normal(psi).astype(np.float32)
+    z = np.zeros(psi, np.float32)
+    ld.write_full_host(SIZES, o, 0, p0, z, z)
+    old = _run_blocks(ref, SIZES, ppm, 1, range(1, 11))
+    new = _run_blocks(ref, SIZES, ppm, 2, range(7, 13))
+    sc = lambda a, n: [ld.derive_step_scalars(t, 1e-3) for t in range(a, a + n)]
+    for a, n in ((1, 4), (5, 4), (9, 2)):                       # old run, b = 4
+        ld.write_batch_host(SIZES, o, a, sc(a, n), old[a - 1:a - 1 + n])
+    ld.write_full_host(SIZES, o, 8, z, z, z)                    # an old full checkpoint of a state >= 7
+    # without retiring, the old …09 file (first 9 > 7) would override blocks 9, 10 of the new …07 file
+    ld.retire_from(SIZES, o, 7)
+    names = sorted(os.listdir(tmp_path))
+    assert ref.batch_name(0, 9) not in names and ref.full_name(0, 8) not in names
+    raw = open(os.path.join(tmp_path, ref.batch_name(0, 5)), "rb").read()
+    assert raw == ref.batch_serialize(0, 1, 5, SIZES, ppm, ref.ADAM, ref.FLAG_EF | ref.FLAG_MEAN, ref.adam_consts(),
+                                      np.stack([ref.step_scalars(t, 1e-3) for t in (5, 6)]), old[4:6])
+    assert ld.chain_scan(SIZES, o) == (0, 6)
+    for a, n in ((7, 3), (10, 3)):                              # new run, b = 3
+        ld.write_batch_host(SIZES, o, a, sc(a, n), new[a - 7:a - 7 + n])
+    assert ld.chain_scan(SIZES, o) == (0, 12)
+    P, M, V = p0.copy(), z.copy(), z.copy()
+    blocks = list(old[:6]) + list(new)
+    for t, blk in zip(range(1, 13), blocks):
+        ref.adam_step(ref.exchange(blk, 1, K, psi), ref.adam_consts(), ref.step_scalars(t, 1e-3), P, M, V)
+    q, mq, vq, it = ref.recover(str(tmp_path), 1, SIZES, ppm)
+    assert it == 12 and np.array_equal(q, P) and np.array_equal(mq, M) and np.array_equal(vq, V)
+    # nothing at or after 13 exists: retiring there changes nothing; another rank's files are not touched
+    before = {n: open(os.path.join(tmp_path, n), "rb").read() for n in os.listdir(tmp_path)}
+    ld.retire_from(SIZES, o, 13)
+    ld.retire_from(SIZES, _opts(tmp_path, world=2, rank=1, nccl_id=b"\0" * 128), 0)
+    assert {n: open(os.path.join(tmp_path, n), "rb").read() for n in os.listdir(tmp_path)} == before

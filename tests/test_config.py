@@ -141,3 +141,39 @@ def test_sim_product_matches_oracle(ref):
             assert got["effective_ratio"] == SIM["T"] / (SIM["T"] + got["wasted"])
     with pytest.raises(ld.LowDiffError):
         B.simulate_failures(SIM, 0.0, 3.0)
+
+
+# ---------------------------------------------------------------- domain f b <= 1
+# a cluster where Eq. 5's stationary point leaves the model's domain: f* b* = cbrt(R_D^2 W / (2 S M)) > 1
+FAST = dict(N=8, M=100.0, W=1e10, S=1e9, T=1e5, R_F=2.0, R_D=10.0)
+
+
+def test_wasted_time_rejects_batch_beyond_full_interval():
+    with pytest.raises(ld.LowDiffError):
+        B.wasted_time(CASES[0], 0.5, 3.0)                  # f b = 1.5: the merge term would be negative
+    with pytest.raises(ld.LowDiffError):
+        B.simulate_failures(SIM, 0.5, 3.0)
+    assert B.wasted_time(CASES[0], 0.5, 2.0) > 0            # f b = 1 is inside
+
+
+def test_feasible_optimum_is_grid_minimum_on_the_domain(ref):
+    f, b, clamped, fu, bu = B.optimal_config_feasible(FAST)
+    rf, rb = ref.optimal_config(FAST["M"], FAST["W"], FAST["S"], FAST["R_D"])
+    assert (fu, bu) == (rf, rb) and fu * bu > 1 and clamped
+    assert math.isclose(f * b, 1.0, rel_tol=1e-12)
+    best = min(ref.wasted_time(*ref_args(FAST), ff, bb)
+               for ff in f * np.exp(np.linspace(-2, 2, 201)) for bb in b * np.exp(np.linspace(-2, 2, 201))
+               if ff * bb <= 1.0)
+    assert ref.wasted_time(*ref_args(FAST), f, b) <= best * (1 + 1e-9)
+    for p in CASES:                                        # inside the domain: the Eq. 5 point itself
+        f2, b2, cl2, fu2, bu2 = B.optimal_config_feasible(p)
+        assert not cl2 and (f2, b2) == (fu2, bu2) == ref.optimal_config(p["M"], p["W"], p["S"], p["R_D"])
+
+
+def test_stepwise_adaptation_stays_in_domain():
+    fcf, batch = 1, 1
+    for _ in range(100):
+        fcf, batch = B.config_step(FAST, fcf, batch)
+        assert 1 <= batch <= fcf
+    with pytest.raises(ld.LowDiffError):
+        B.config_step(FAST, 2, 3)
