@@ -105,7 +105,7 @@ def init_dist(gpus):
     else:
         torch.cuda.set_device(0)
     if world != gpus:
-        print(f"warning: --gpus {gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     return rank, world, local
 
 
@@ -147,8 +147,9 @@ def workload_config(args, sizes, K, world):
     psi = sum(sizes)
     return {"workload": f"{args.workload}@{args.ppm}ppm", "psi": psi, "layers": len(sizes), "k_total": K,
             "density_ppm": args.ppm, "batch_size": 4, "parallelism": f"dp{world}",
-            "inputs": "D4 row-sparse Gaussian, alpha=0.5 rank correlation; 2 gradient buffers of "
-                      f"{4 * psi / 1e9:.2f} GB alternate (> L2, no flush needed)",
+            "inputs": f"D4 row-sparse Gaussian, alpha=0.5 rank correlation; {N_GRADS} distinct gradient buffers of "
+                      f"{4 * psi / 1e9:.2f} GB used in rotation (GPT-2 XL / BERT-L: > L2, no flush needed; "
+                      "ResNet-50 / MLP: L2-resident, as the paper's small models would be)",
             "persist": "D2H of the rank's block into the pinned ring inside the timed region; "
                        "file writing measured separately (writer)"}
 
@@ -223,6 +224,7 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- our arm
+N_GRADS = 4      # distinct gradient buffers in rotation (a 2-periodic input biased the band)
 EF_SETTLE = 20   # 20 warm-up iterations, which error feedback needs to reach steady state
 
 
@@ -251,7 +253,7 @@ def run_ours(args):
     ctx = ld.Context(sizes, density_ppm=args.ppm, rank=rank, world=world, nccl_id=nid, device=local,
                      ckpt_dir=tmp, batch_size=4, ring_slots=8, write_files=False, optim=ld.ADAM)
     K = ctx.K
-    grads = [gradient(sizes, rank, i, dist="D4", alpha=0.5, model=args.workload, device=dev) for i in range(2)]
+    grads = [gradient(sizes, rank, i, dist="D4", alpha=0.5, model=args.workload, device=dev) for i in range(N_GRADS)]
     r = torch.zeros(psi, device=dev)
     dense = torch.empty(psi, device=dev)
     # double-buffered send blocks: the D2H of iteration t's block overlaps the
@@ -274,7 +276,7 @@ def run_ours(args):
     def step(g=None):
         t = it[0]
         sd = sends[t % 2]
-        ctx.compress(grads[t % 2] if g is None else g, r, sd)
+        ctx.compress(grads[t % N_GRADS] if g is None else g, r, sd)
         if args.persist_first:
             ctx.batch_persist(t + 1, scal[t], sd)   # D2H overlaps this exchange + the next compress
         if args.exchange == "peer":
@@ -467,10 +469,10 @@ def run_ours(args):
         rsend = torch.empty(2 * K, dtype=torch.int32, device=dev)   # not a peer slot
         for t in range(n_rep):
             if world > 1:
-                ctx.compress(grads[t % 2], r, rsend)
+                ctx.compress(grads[t % N_GRADS], r, rsend)
                 ctx.exchange(rsend, diffs[t], dn)
             else:
-                ctx.compress(grads[t % 2], r, diffs[t])
+                ctx.compress(grads[t % N_GRADS], r, diffs[t])
         del dn
         torch.cuda.synchronize()
         # sharded recovery (NEXT-2): every rank replays only its parameter range
@@ -753,6 +755,24 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: one rank per GPU via torch.distributed.run
+    on this node (the driver's own launch form), or a loud failure when the node has fewer GPUs."""
+    n_dev = torch.cuda.device_count()
+    if n_dev < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but this node has {n_dev} CUDA device(s); refusing to run "
+              f"{args.gpus} ranks on fewer GPUs", file=sys.stderr, flush=True)
+        sys.exit(2)
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -784,6 +804,8 @@ def main():
                     help="nccl: ncclAllGather + merge; peer: merge reading the peers' slots (NEXT-1)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        spawn_ranks(args)   # (the reference arm runs on rank 0 only: nothing to spawn)
     if args.impl == "reference":
         run_reference(args)
     else:
