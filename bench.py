@@ -270,7 +270,7 @@ def run_ours(args):
         sends = [torch.empty(2 * K, dtype=torch.int32, device=dev) for _ in range(2)]
     send = sends[0]
     gathered = torch.empty(world * 2 * K, dtype=torch.int32, device=dev) if world > 1 else None
-    scal = [ld.derive_step_scalars(t, 1e-3) for t in range(1, args.warmup + 2 * args.steps + 40)]
+    scal = [ld.derive_step_scalars(t, 1e-3) for t in range(1, args.warmup + 2 * args.steps + args.trace_calls + 60)]
     it = [0]
 
     def step(g=None):
@@ -333,6 +333,14 @@ def run_ours(args):
         if n:
             kern[name] = {"ms_per_launch": tot / n, "launches": n, "share_of_step": tot / n_prof / (ms / args.steps)}
     ctx.prof_enable(False)
+    # per-layer miss trace (lowdiff_compress_trace after each call of a further untimed run of the
+    # same loop): which large layers left the speculative band, and at which refill level
+    trace_calls = []
+    for _ in range(max(args.trace_calls, 0)):
+        step()
+        _, lev, cand, _ = ctx.compress_trace()
+        trace_calls.append({"level1": int((lev == 1).sum()), "level2": int((lev == 2).sum()),
+                            "direct_segments": ctx.stats()["direct_segments"]})
     ctx.sync()
     st = ctx.stats()
     ms_step = ms / args.steps
@@ -751,7 +759,17 @@ def run_ours(args):
             "roofline": roofline, "gate_bj5": gate, "kernels": kern, "per_step_ms": spread, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "recovery": recovery, "writer": writer, "full_ckpt": fullck, "update": update,
             "replica": replica, "snapshot": snapshot, "union": union, "recovery_files": recovery_files,
-            "spec": {"hits": st["spec_hits"], "misses": st["spec_misses"]}}
+            "spec": {"hits": st["spec_hits"], "misses": st["spec_misses"],
+                     "trace": {"calls": len(trace_calls),
+                               "calls_with_a_miss": sum(1 for t in trace_calls if t["level1"] + t["level2"]),
+                               "level1_layers": sum(t["level1"] for t in trace_calls),
+                               "level2_layers": sum(t["level2"] for t in trace_calls),
+                               "direct_segments_per_call": [t["direct_segments"] for t in trace_calls]}},
+            "scratch": {"compress_scratch_bytes": st["compress_scratch_bytes"],
+                        "compress_scratch_bytes_per_param": st["compress_scratch_bytes"] / psi,
+                        "library_device_bytes": st["device_bytes"],
+                        "note": "bounded candidate slots (DESIGN.md 4.1) + plan; library_device_bytes adds the "
+                                "merge/replay scratch and the full-checkpoint stage allocated so far"}}
     print(json.dumps(line), flush=True)
 
 
@@ -792,6 +810,8 @@ def main():
     ap.add_argument("--no-update", action="store_true")
     ap.add_argument("--no-snapshot", action="store_true")
     ap.add_argument("--no-union", action="store_true")
+    ap.add_argument("--trace-calls", type=int, default=40,
+                    help="untimed calls after the timed region whose per-layer refill trace is reported")
     ap.add_argument("--recovery-files", type=int, default=0,
                     help="n > 0: also time lowdiff_recover from Full@0 + n differentials on local storage")
     ap.add_argument("--no-graphs", action="store_true", help="plain launches instead of captured CUDA graphs")

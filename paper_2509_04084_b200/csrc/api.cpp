@@ -107,6 +107,7 @@ lowdiff_status upload(lowdiff_ctx* c, const std::vector<T>& h, T** d) {
   size_t bytes = std::max<size_t>(1, h.size()) * sizeof(T);
   CK(cudaMalloc(&p, bytes));
   c->dev_allocs.push_back(p);
+  c->plan_bytes += bytes;
   if (!h.empty()) CK(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
   *d = static_cast<T*>(p);
   return LOWDIFF_OK;
@@ -115,6 +116,7 @@ lowdiff_status upload(lowdiff_ctx* c, const std::vector<T>& h, T** d) {
 lowdiff_status dalloc(lowdiff_ctx* c, size_t bytes, void** d) {
   CK(cudaMalloc(d, std::max<size_t>(bytes, 16)));
   c->dev_allocs.push_back(*d);
+  c->plan_bytes += std::max<size_t>(bytes, 16);
   return LOWDIFF_OK;
 }
 
@@ -168,26 +170,29 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   P.chunk_slot = d_cslot; P.chunk_base = d_cb; P.chunk_lo = d_clo; P.chunk_hi = d_chi;
   const size_t nc = (size_t)std::max(1, P.n_chunks), nl = (size_t)std::max(1, P.n_large);
   void* p;
-  if ((st = dalloc(c, nc * ld::kChunk * sizeof(uint64_t), &p))) return st; P.cand = (uint64_t*)p;
+  // bounded candidate scratch: cs slots per 1024-element segment, O(K) in total
+  P.cs = ld::compress_seg_capacity(c->cfg.density_ppm);
+  if ((st = dalloc(c, nc * ld::kSegsPerChunk * (size_t)P.cs * sizeof(uint64_t), &p))) return st; P.cand = (uint64_t*)p;
   if ((st = dalloc(c, nc * ld::kSegsPerChunk * sizeof(uint32_t), &p))) return st; P.seg_count = (uint32_t*)p;
-  if ((st = dalloc(c, nc * 4 * 7, &p))) return st;
-  P.chunk_count = (uint32_t*)p; P.chunk_gt = P.chunk_count + nc; P.chunk_eq = P.chunk_gt + nc;
-  P.chunk_out = P.chunk_eq + nc; P.chunk_take = P.chunk_out + nc; P.refill_list = P.chunk_take + nc;
-  P.refill_list2 = P.refill_list + nc;
+  if ((st = dalloc(c, 3 * nc * ld::kSegsPerChunk * sizeof(uint32_t), &p))) return st; P.dlist = (uint32_t*)p;
   if ((st = dalloc(c, nl * (2048 + 2048 + 512) * 4, &p))) return st; P.hist = (uint32_t*)p;
   if ((st = dalloc(c, nl * sizeof(ld::LayerSel), &p))) return st; P.sel = (ld::LayerSel*)p;
   CK(cudaMemset(P.sel, 0, nl * sizeof(ld::LayerSel)));   // band = 0: not yet adapted
-  if ((st = dalloc(c, nl * 4, &p))) return st; P.thr = (uint32_t*)p;
-  if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_T = (uint32_t*)p;
-  if ((st = dalloc(c, nl * 4, &p))) return st; P.layer_total = (uint32_t*)p;
-  CK(cudaMemset(P.layer_total, 0, nl * 4));   // then kept zero between calls by layer_scan_kernel
-  if ((st = dalloc(c, nl * 4, &p))) return st; P.sel_cut = (uint32_t*)p;
-  if ((st = dalloc(c, nl * 4, &p))) return st; P.thr_safe = (uint32_t*)p;
-  if ((st = dalloc(c, (size_t)nc * 8, &p))) return st; P.chunk_state = (unsigned long long*)p;
+  if ((st = dalloc(c, nl * 4 * 9, &p))) return st;
+  P.thr = (uint32_t*)p; P.thr_used = P.thr + nl; P.sel_T = P.thr_used + nl; P.layer_total = P.sel_T + nl;
+  P.sel_cut = P.layer_total + nl; P.thr_safe = P.sel_cut + nl; P.refill_list = P.thr_safe + nl;
+  P.refill_list2 = P.refill_list + nl; P.trace = P.refill_list2 + nl;
+  CK(cudaMemset(P.layer_total, 0, nl * 4 * 6));
+  if ((st = dalloc(c, (size_t)nc * 24, &p))) return st; P.chunk_state = (unsigned long long*)p;
+  if ((st = dalloc(c, (size_t)ld::kMaxSelGrid * 12, &p))) return st;
+  P.tail_agg = (unsigned long long*)p; P.tail_slot = (uint32_t*)(P.tail_agg + ld::kMaxSelGrid);
   CK(cudaMemset(P.thr, 0xFF, nl * 4));   // no speculative band before the first call
   CK(cudaMemset(P.thr_safe, 0xFF, nl * 4));
   CK(cudaMemset(P.sel_T, 0xFF, nl * 4));  // no previous k-th key (no drift estimate yet)
+  CK(cudaMemset(P.thr_used, 0, nl * 4));
   if ((st = dalloc(c, 8 * 4, &p))) return st; P.counters = (uint32_t*)p;
+  if ((st = dalloc(c, 16 * 8, &p))) return st; P.phase_ns = (unsigned long long*)p;
+  CK(cudaMemset(P.phase_ns, 0, 16 * 8));
   if ((st = dalloc(c, 4 * 4, &p))) return st; P.err = (uint32_t*)p;
   CK(cudaMemset(P.err, 0, 16));
   CK(cudaMemset(P.err + 1, 0xFF, 4));
@@ -1098,18 +1103,51 @@ lowdiff_status lowdiff_get_stats(const lowdiff_ctx* c, lowdiff_stats* out) {
   out->ring_stall_ns = c->stall_ns;
   out->writer_busy_ns = c->writer_ns;
   uint32_t cnt[4] = {0, 0, 0, 0};
-  if (cudaMemcpy(cnt, c->plan.counters, 16, cudaMemcpyDeviceToHost) == cudaSuccess) {
+  if (cudaMemcpy(cnt, c->plan.counters, 16, cudaMemcpyDeviceToHost) == cudaSuccess) {   // of the last call
     out->spec_hits = cnt[1];
     out->spec_misses = cnt[2];
     out->spec_candidates = cnt[3];
   } else {
     out->spec_hits = out->spec_misses = out->spec_candidates = -1;
   }
+  uint32_t cnt2[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  out->direct_segments = cudaMemcpy(cnt2, c->plan.counters, 32, cudaMemcpyDeviceToHost) == cudaSuccess ? cnt2[5] : -1;
+  out->compress_scratch_bytes = (int64_t)c->plan_bytes;
+  out->device_bytes = (int64_t)(c->plan_bytes + c->merge_scratch_bytes + c->replay_scratch_bytes +
+                                c->full_stage_cap * 4 + c->union_scratch_bytes);
   out->replica_busy_ns = c->rep_ns;
   out->replica_stall_ns = c->rep_stall_ns;
   out->union_files_written = c->u_files;
   out->union_bytes_written = c->u_bytes;
   out->union_entries = c->u_entries;
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_compress_trace(lowdiff_ctx* c, int32_t cap, int32_t* n_large, int32_t* layer, int32_t* level,
+                                      uint32_t* candidates, uint32_t* threshold) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!n_large) return fail(c, LOWDIFF_E_INVALID, "compress_trace: NULL n_large");
+  const int nl = c->plan.n_large;
+  *n_large = nl;
+  if (!layer && !level && !candidates && !threshold) return LOWDIFF_OK;
+  if (cap < nl) return fail(c, LOWDIFF_E_INVALID, "compress_trace: arrays shorter than n_large");
+  CK(cudaDeviceSynchronize());
+  std::vector<int32_t> ids((size_t)nl);
+  if (nl) CK(cudaMemcpy(ids.data(), c->plan.large_layers, (size_t)nl * 4, cudaMemcpyDeviceToHost));
+  if (layer) std::copy(ids.begin(), ids.end(), layer);
+  if (level && nl) CK(cudaMemcpy(level, c->plan.trace, (size_t)nl * 4, cudaMemcpyDeviceToHost));
+  if (candidates && nl) CK(cudaMemcpy(candidates, c->plan.layer_total, (size_t)nl * 4, cudaMemcpyDeviceToHost));
+  if (threshold && nl) CK(cudaMemcpy(threshold, c->plan.thr_used, (size_t)nl * 4, cudaMemcpyDeviceToHost));
+  return LOWDIFF_OK;
+}
+
+lowdiff_status lowdiff_compress_phases(lowdiff_ctx* c, int64_t* ns16) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!ns16) return fail(c, LOWDIFF_E_INVALID, "compress_phases: NULL");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(ns16, c->plan.phase_ns, 16 * 8, cudaMemcpyDeviceToHost));
   return LOWDIFF_OK;
 }
 

@@ -37,6 +37,7 @@ constexpr int kReplayTile = 1 << kReplayTileShift;   // replay tile (elements pe
 constexpr int kReplayThreads = LD_REPLAY_THREADS;
 constexpr int kReplaySlots = kReplayTile / (4 * kReplayThreads);   // float4 slots per thread
 constexpr uint32_t kNoThreshold = 0xFFFFFFFFu;
+constexpr int kMaxSelGrid = 4096;      // upper bound of the persistent select grid (CTAs)
 
 // per-large-layer selection state (device)
 struct LayerSel {
@@ -68,29 +69,34 @@ struct DevPlan {
   const uint64_t* chunk_lo;      // [n_chunks] first element that belongs to the chunk
   const uint64_t* chunk_hi;      // [n_chunks] one past the last element
   // scratch
-  uint64_t* cand;                // [n_chunks * kChunk] candidates (acc bits << 32 | global index):
-                                 //   written per segment by the scan, compacted per chunk by prep
-  uint32_t* seg_count;           // [n_chunks * 16] candidates per segment (index-ordered inside)
-  uint32_t* chunk_count;         // [n_chunks]
+  int32_t cs;                    // candidate capacity of a segment (compress_seg_capacity)
+  uint64_t* cand;                // [n_chunks * 16] segment slots of cs candidates (acc bits << 32 | index);
+                                 //   the select compacts each window's lists in place
+  uint32_t* seg_count;           // [n_chunks * 16] candidates of the segment (| kDirect: not stored)
   uint32_t* layer_total;         // [n_large] candidates admitted per large layer (this call)
-  uint32_t* chunk_gt;            // [n_chunks]
-  uint32_t* chunk_eq;            // [n_chunks]
-  uint32_t* chunk_out;           // [n_chunks] output offset inside the layer
-  uint32_t* chunk_take;          // [n_chunks] ties taken from this chunk
   uint32_t* hist;                // [n_large * (2048 + 2048 + 512)]
   LayerSel* sel;                 // [n_large]
   uint32_t* thr;                 // [n_large] speculative threshold key (persistent across calls)
+  uint32_t* thr_used;            // [n_large] threshold this call's candidates were taken with
   // lazy residual zeroing: the previous call's selection of a large layer is
   // {key(r) > sel_T} U {key(r) == sel_T and index < sel_cut}; the next scan zeroes it on the fly
   uint32_t* sel_T;               // [n_large] previous call's exact k-th key
   uint32_t* sel_cut;             // [n_large] one past the global index of the last tie it took
-  uint32_t* refill_list;         // [n_chunks] chunk ids to rescan at the safe threshold (level 1)
-  uint32_t* refill_list2;        // [n_chunks] chunk ids to rescan at 0 (level 2)
+  uint32_t* refill_list;         // [n_large] layers to rescan at their safe threshold (level 1)
+  uint32_t* refill_list2;        // [n_large] layers to histogram directly (level 2)
+  uint32_t* trace;               // [n_large] this call's path per layer: 0 hit, 1 level-1, 2 level-2
+  uint32_t* dlist;               // [3 n_chunks 16] DIRECT segments of this call: segid | level << 30
   uint32_t* thr_safe;            // [n_large] the band without the drift lead
-  unsigned long long* chunk_state;  // [n_chunks] count_emit look-back: status | eq_incl | gt_incl
-  uint32_t* counters;            // [0] level-1 refill chunks, [1] spec hits, [2] spec misses,
-                                 // [3] candidates of hit layers, [4] level-2 refill chunks
+  unsigned long long* chunk_state;  // [3 n_chunks] select: per chunk u32 x 6 (compacted start and count,
+                                    //   gt, eq and their in-CTA prefixes)
+  unsigned long long* tail_agg;  // [kMaxSelGrid] select: (eq << 31 | gt) of each CTA's last layer run
+  uint32_t* tail_slot;           // [kMaxSelGrid] that run's layer (0xFFFFFFFE: the CTA had no chunks)
+  uint32_t* counters;            // [0] level-1 refills, [1] spec hits, [2] spec misses,
+                                 // [3] candidates of hit layers, [4] level-2 refills,
+                                 // [5] entries in dlist (DIRECT segments: more than cs candidates,
+                                 //     or every segment of a level-2 layer)
   uint32_t* err;                 // [0] non-finite flag, [1] first bad layer
+  unsigned long long* phase_ns;  // [16] select-kernel phase timestamps (block 0, %globaltimer)
 };
 
 // ---------------------------------------------------------------- context
@@ -156,6 +162,7 @@ struct lowdiff_ctx {
   // device plan + buffers
   ld::DevPlan plan{};
   std::vector<void*> dev_allocs;
+  size_t plan_bytes = 0;              // device memory of the plan + compress scratch (dev_allocs)
   // streams / events
   cudaStream_t side = nullptr;       // D2H copies
   cudaStream_t aux = nullptr;        // small-layer compress, forked from the caller's stream
@@ -278,11 +285,7 @@ namespace ld {
 cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send,
                             cudaStream_t s);
 cudaError_t launch_materialize(lowdiff_ctx* c, float* residual, cudaStream_t s);
-// the phases of launch_compress (compress.cu)
-cudaError_t compress_head(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send, cudaStream_t s,
-                          int* sel_h);
-cudaError_t compress_refill(lowdiff_ctx* c, const float* grad, float* residual, int level, cudaStream_t s);
-cudaError_t compress_tail(lowdiff_ctx* c, float* residual, uint32_t* send, cudaStream_t s, int sel_h);
+int compress_seg_capacity(uint32_t ppm);   // candidate slots per 1024-element segment
 cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, float* dense,
                          cudaStream_t s);
 // replays elements [lo, hi); p, m, v point at element lo.  ranges: NULL (every entry of every block

@@ -60,7 +60,8 @@ class Stats(C.Structure):
     _fields_ = [("files_written", C.c_int64), ("bytes_written", C.c_int64), ("ring_stall_ns", C.c_int64),
                 ("writer_busy_ns", C.c_int64), ("spec_hits", C.c_int64), ("spec_misses", C.c_int64),
                 ("spec_candidates", C.c_int64), ("replica_busy_ns", C.c_int64), ("replica_stall_ns", C.c_int64),
-                ("union_files_written", C.c_int64), ("union_bytes_written", C.c_int64), ("union_entries", C.c_int64)]
+                ("union_files_written", C.c_int64), ("union_bytes_written", C.c_int64), ("union_entries", C.c_int64),
+                ("direct_segments", C.c_int64), ("compress_scratch_bytes", C.c_int64), ("device_bytes", C.c_int64)]
 
 
 _lib = None
@@ -111,6 +112,8 @@ def lib():
             "host_sgd_step": ([C.c_int64, P, C.c_float, P, C.c_int32], S),
             "sync": ([P], S),
             "get_stats": ([P, C.POINTER(Stats)], S),
+            "compress_trace": ([P, C.c_int32, C.POINTER(C.c_int32), P, P, P, P], S),
+            "compress_phases": ([P, P], S),
             "prof_enable": ([P, C.c_int32], S),
             "prof_read": ([P, C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)], S),
             "kernel_launches": ([P], C.c_int64),
@@ -146,7 +149,7 @@ EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_mater
             "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "snapshot_shard", "bucket_plan", "union_compact", "union_persist", "recover_union",
             "replica_init",
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
-            "sync", "get_stats",
+            "sync", "get_stats", "compress_trace", "compress_phases",
             "prof_enable", "prof_read", "kernel_launches", "set_graphs", "last_error", "nccl_unique_id",
             "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host", "retire_from",
             "write_full_host", "abi_version", "selftest", "wasted_time", "optimal_config", "optimal_config_feasible", "config_step",
@@ -488,6 +491,24 @@ class Context:
         s = Stats()
         self._c("get_stats", lib().lowdiff_get_stats(self._h, C.byref(s)))
         return {f: getattr(s, f) for f, _ in Stats._fields_}
+
+    def compress_trace(self):
+        """Per large layer of the last compress: (layer ids, level 0/1/2, candidates, threshold key)."""
+        import numpy as np
+        n = C.c_int32()
+        self._c("compress_trace", lib().lowdiff_compress_trace(self._h, 0, C.byref(n), None, None, None, None))
+        L, lev = np.zeros(n.value, np.int32), np.zeros(n.value, np.int32)
+        cand, thr = np.zeros(n.value, np.uint32), np.zeros(n.value, np.uint32)
+        self._c("compress_trace", lib().lowdiff_compress_trace(self._h, n.value, C.byref(n), *[a.ctypes.data_as(C.c_void_p)
+                                                                                             for a in (L, lev, cand, thr)]))
+        return L, lev, cand, thr
+
+    def compress_phases(self):
+        """Select-kernel phase timestamps (ns) of the last compress (diagnostic)."""
+        import numpy as np
+        a = np.zeros(16, np.int64)
+        self._c("compress_phases", lib().lowdiff_compress_phases(self._h, a.ctypes.data_as(C.c_void_p)))
+        return a
 
     def set_graphs(self, on=True):
         """Replay compress / merge as captured CUDA graphs (fewer launch gaps for small models)."""
