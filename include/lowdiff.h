@@ -395,11 +395,6 @@ lowdiff_status lowdiff_get_stats(const lowdiff_ctx *ctx, lowdiff_stats *out);
  * may be NULL to query it): layer[i] = its layer id, level[i] = 0 selected from the speculative
  * band, 1 level-1 refill (rescan at the safe threshold), 2 level-2 refill (every element),
  * candidates[i] = keys admitted at the threshold finally used, threshold[i] = that threshold key. */
-/* Phase timestamps (ns, %globaltimer of CTA 0) of the last lowdiff_compress's persistent select
- * kernel: [0] start, [1] digit-0 histograms, [2] plan, [3..6] refill rescans / plans (0 when no
- * refill ran this call... stale values otherwise), [7..10] digit 1 / 2 histograms and searches,
- * [11] counts, [15] CTA 0 done.  Synchronises the device.  Diagnostic. */
-lowdiff_status lowdiff_compress_phases(lowdiff_ctx *ctx, int64_t *ns16);
 lowdiff_status lowdiff_compress_trace(lowdiff_ctx *ctx, int32_t cap, int32_t *n_large, int32_t *layer,
                                       int32_t *level, uint32_t *candidates, uint32_t *threshold);
 

@@ -174,25 +174,22 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   P.cs = ld::compress_seg_capacity(c->cfg.density_ppm);
   if ((st = dalloc(c, nc * ld::kSegsPerChunk * (size_t)P.cs * sizeof(uint64_t), &p))) return st; P.cand = (uint64_t*)p;
   if ((st = dalloc(c, nc * ld::kSegsPerChunk * sizeof(uint32_t), &p))) return st; P.seg_count = (uint32_t*)p;
-  if ((st = dalloc(c, 3 * nc * ld::kSegsPerChunk * sizeof(uint32_t), &p))) return st; P.dlist = (uint32_t*)p;
+  if ((st = dalloc(c, nc * 4 * 4, &p))) return st;
+  P.chunk_count = (uint32_t*)p; P.chunk_dm = P.chunk_count + nc; P.refill_list = P.chunk_dm + nc;
+  P.refill_list2 = P.refill_list + nc;
   if ((st = dalloc(c, nl * (2048 + 2048 + 512) * 4, &p))) return st; P.hist = (uint32_t*)p;
   if ((st = dalloc(c, nl * sizeof(ld::LayerSel), &p))) return st; P.sel = (ld::LayerSel*)p;
   CK(cudaMemset(P.sel, 0, nl * sizeof(ld::LayerSel)));   // band = 0: not yet adapted
-  if ((st = dalloc(c, nl * 4 * 9, &p))) return st;
+  if ((st = dalloc(c, nl * 4 * 7, &p))) return st;
   P.thr = (uint32_t*)p; P.thr_used = P.thr + nl; P.sel_T = P.thr_used + nl; P.layer_total = P.sel_T + nl;
-  P.sel_cut = P.layer_total + nl; P.thr_safe = P.sel_cut + nl; P.refill_list = P.thr_safe + nl;
-  P.refill_list2 = P.refill_list + nl; P.trace = P.refill_list2 + nl;
-  CK(cudaMemset(P.layer_total, 0, nl * 4 * 6));
-  if ((st = dalloc(c, (size_t)nc * 24, &p))) return st; P.chunk_state = (unsigned long long*)p;
-  if ((st = dalloc(c, (size_t)ld::kMaxSelGrid * 12, &p))) return st;
-  P.tail_agg = (unsigned long long*)p; P.tail_slot = (uint32_t*)(P.tail_agg + ld::kMaxSelGrid);
+  P.sel_cut = P.layer_total + nl; P.thr_safe = P.sel_cut + nl; P.trace = P.thr_safe + nl;
+  CK(cudaMemset(P.layer_total, 0, nl * 4 * 4));
+  if ((st = dalloc(c, (size_t)nc * 8, &p))) return st; P.chunk_state = (unsigned long long*)p;
   CK(cudaMemset(P.thr, 0xFF, nl * 4));   // no speculative band before the first call
   CK(cudaMemset(P.thr_safe, 0xFF, nl * 4));
   CK(cudaMemset(P.sel_T, 0xFF, nl * 4));  // no previous k-th key (no drift estimate yet)
   CK(cudaMemset(P.thr_used, 0, nl * 4));
   if ((st = dalloc(c, 8 * 4, &p))) return st; P.counters = (uint32_t*)p;
-  if ((st = dalloc(c, 16 * 8, &p))) return st; P.phase_ns = (unsigned long long*)p;
-  CK(cudaMemset(P.phase_ns, 0, 16 * 8));
   if ((st = dalloc(c, 4 * 4, &p))) return st; P.err = (uint32_t*)p;
   CK(cudaMemset(P.err, 0, 16));
   CK(cudaMemset(P.err + 1, 0xFF, 4));
@@ -1139,15 +1136,6 @@ lowdiff_status lowdiff_compress_trace(lowdiff_ctx* c, int32_t cap, int32_t* n_la
   if (level && nl) CK(cudaMemcpy(level, c->plan.trace, (size_t)nl * 4, cudaMemcpyDeviceToHost));
   if (candidates && nl) CK(cudaMemcpy(candidates, c->plan.layer_total, (size_t)nl * 4, cudaMemcpyDeviceToHost));
   if (threshold && nl) CK(cudaMemcpy(threshold, c->plan.thr_used, (size_t)nl * 4, cudaMemcpyDeviceToHost));
-  return LOWDIFF_OK;
-}
-
-lowdiff_status lowdiff_compress_phases(lowdiff_ctx* c, int64_t* ns16) {
-  lowdiff_status st = entry(c);
-  if (st) return st;
-  if (!ns16) return fail(c, LOWDIFF_E_INVALID, "compress_phases: NULL");
-  CK(cudaDeviceSynchronize());
-  CK(cudaMemcpy(ns16, c->plan.phase_ns, 16 * 8, cudaMemcpyDeviceToHost));
   return LOWDIFF_OK;
 }
 

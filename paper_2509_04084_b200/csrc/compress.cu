@@ -20,26 +20,24 @@
 //             marked DIRECT: its list is not kept and later passes re-read its 1024 acc values (4 KB)
 //             from HBM instead -- exactness never depends on the capacity, which only bounds the
 //             scratch at O(K) (cs ~ 12 x the expected candidates per segment: 1 B/param at 1%).
-//     select: ONE persistent cooperative kernel (grid barriers between phases, no launch gaps):
-//             plan -- per layer, #candidates >= k_l means the exact top-k lies inside the band (hit);
-//                     otherwise a refill: level 1 rescans the layer at a lower ("safe") threshold,
-//                     level 2 histograms all of its elements directly (no candidate storage);
-//             two more radix digits over the candidates (or the DIRECT segments' acc) -> the exact
-//             k-th key T and the number of ties at T to take (lowest indices first);
-//             count+emit -- a warp per chunk counts key > T and key == T, obtains its layer offset
-//             and the ties taken before it by a decoupled look-back over the layer's earlier chunks,
-//             and writes its selected entries at their final positions (residual' zeroing is lazy).
-//   HBM traffic in the steady state: 12 B/param + ~(4 + 4 + 4 + 8) B per candidate (~1.5-2 k per
-//   layer) + 8 B/entry.
-#include <cooperative_groups.h>
+//     prep:   warp per chunk: compacts its stored segment lists in place into one index-ordered
+//             chunk list, and histograms the first radix digit (key bits [30:20]) of its candidates.
+//     plan:   per layer, #candidates >= k_l means the exact top-k lies inside the band (hit);
+//             otherwise a refill: level 1 rescans the layer at a lower ("safe") threshold, level 2
+//             makes every segment DIRECT at threshold 0 (no candidate storage).
+//     digits: two more radix digits over the candidates -> the exact k-th key T and the number of
+//             ties at T to take (lowest indices first).
+//     count+emit: a warp per chunk counts key > T and key == T, takes its layer offset and the ties
+//             taken before it by a decoupled look-back over the layer's earlier chunks, and writes
+//             its selected entries at their final positions (residual' zeroing is lazy).
+//   HBM traffic in the steady state: 12 B/param + ~(16 + 8 + 8 + 8) B per candidate (~1.5-2 k per
+//   layer) + 8 B/entry (+ 4 KB per DIRECT segment and pass).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 
 #include "internal.h"
 #include "pdl.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace ld {
 namespace {
@@ -56,8 +54,6 @@ constexpr int kPiecesPerChunk = kSegsPerChunk / kScanWarps;   // 4 scan CTAs per
 #endif
 constexpr int kUnroll = LD_UNROLL;                  // candidate rounds in flight per warp
 constexpr uint32_t kDirect = 0x80000000u;           // seg_count flag: list not stored, read acc
-constexpr int kSelThreads = 256;                    // select kernel: 8 warps per CTA
-constexpr int kSelWarps = kSelThreads / 32;
 #ifndef LD_BAND_AIM
 #define LD_BAND_AIM 1.5f
 #endif
@@ -450,7 +446,7 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
                                                   (uint32_t)cbase, thr, lT, lcut, lane, lt, bad);
   if (lane == 0) {
     P.seg_count[segid] = run > cs ? (run | kDirect) : run;   // layer totals: the select's first pass
-    if (run > cs) P.dlist[atomicAdd(&P.counters[5], 1u)] = (uint32_t)segid;   // DIRECT, level 0
+    if (run > cs) atomicAdd(&P.counters[5], 1u);   // DIRECT segments (stats)
   }
   if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
 }
@@ -485,43 +481,193 @@ __device__ __forceinline__ void visit_direct(const DevPlan& P, const float* __re
   }
 }
 
+// Level-1 refill: the chunks of refill_list (count counters[0]) are rescanned at their layer's
+// thr_used (acc re-read: r when EF, else g); a persistent grid over 4 pieces x the listed chunks.
+template <bool EF>
+__global__ void __launch_bounds__(kScanWarps * 32, LD_SCAN_MINB)
+rescan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint64_t sbuf_all[kScanWarps][kCandBuf];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint32_t n_items = P.counters[0] * kPiecesPerChunk;
+  for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const int ch = (int)P.refill_list[w / kPiecesPerChunk];
+    const int seg = (int)(w % kPiecesPerChunk) * kScanWarps + warp;
+    const uint64_t cbase = P.chunk_base[ch];
+    const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
+    const int slot = P.chunk_slot[ch];
+    const uint64_t segid = (uint64_t)ch * kSegsPerChunk + seg;
+    const uint32_t cs = (uint32_t)P.cs;
+    bool bad = false;
+    const uint32_t run = scan_segment<EF, true, false, false>(g + cbase, r + cbase, seg_slot(P, segid), cs, nullptr,
+                                                              sbuf_all[warp], (uint32_t)seg * kSeg, lo, hi,
+                                                              (uint32_t)cbase, P.thr_used[slot], 0xFFFFFFFFu, 0u,
+                                                              lane, lt, bad);
+    if (lane == 0) P.seg_count[segid] = run > cs ? (run | kDirect) : run;
+  }
+}
+
+// ---------------------------------------------------------------- chunk prep (warp per chunk)
+// Compact the stored segment lists of a chunk in place into one index-ordered list at the chunk's
+// region start (a candidate never moves up -- the list offset of segment s is at most s cs -- and
+// each round loads before it stores), store its length and DIRECT mask, and histogram the first
+// radix digit (key bits [30:20]) of its candidates: the stored ones, and those of its DIRECT
+// segments read from acc (src) at the layer's threshold -- in shared memory when all chunks of the
+// CTA belong to one layer (chunk slots are monotone), else directly.
+// mode 0: every chunk (after the scan); 1: chunks of level-1 layers (after their rescan);
+// 2: chunks of level-2 layers -- every segment becomes DIRECT at threshold 0 (no storage).
+// Modes 1 / 2 walk their refill list (the layers' chunks, listed contiguously) with a small
+// persistent grid, so an empty list costs only the launch.
+__global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, const float* __restrict__ src, int mode) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint32_t sh[kH0];
+  __shared__ uint32_t s_tot;
+  const uint32_t n_items = mode == 0 ? (uint32_t)P.n_chunks : P.counters[mode == 1 ? 0 : 4];
+  const uint32_t* list = mode == 1 ? P.refill_list : P.refill_list2;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t i0 = blockIdx.x * 8u; i0 < n_items; i0 += gridDim.x * 8u) {
+  const uint32_t i_last = min(n_items, i0 + 8u) - 1u;
+  const int c_first = mode == 0 ? (int)i0 : (int)list[i0];
+  const int c_last = mode == 0 ? (int)i_last : (int)list[i_last];
+  const uint32_t item = i0 + (threadIdx.x >> 5);
+  const int ch = item <= i_last ? (mode == 0 ? (int)item : (int)list[item]) : c_last;
+  const bool uniform = P.chunk_slot[c_first] == P.chunk_slot[c_last];
+  if (uniform) {
+    __syncthreads();   // the previous round's flush has read sh
+    for (int b = threadIdx.x; b < kH0; b += 256) sh[b] = 0;
+    if (threadIdx.x == 0) s_tot = 0;
+    __syncthreads();
+  }
+  const int slot = P.chunk_slot[ch];
+  const bool active = item <= i_last;
+  if (active) {
+    uint32_t* h0 = uniform ? sh : P.hist + (uint64_t)slot * kHistRow;
+    // the threshold the chunk's candidates were taken with: the scan's band (mode 0) or the refill's
+    const uint32_t thr = mode == 0 ? min(P.thr[slot], 0x7F800000u) : P.thr_used[slot];
+    uint32_t sc = lane < kSegsPerChunk ? P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] : 0u;
+    if (mode == 2) {   // level 2: every segment DIRECT (count = its valid elements)
+      const uint64_t cb = P.chunk_base[ch];
+      const uint64_t s0 = cb + (uint64_t)lane * kSeg, s1 = s0 + kSeg;
+      const uint64_t lo = P.chunk_lo[ch], hi = P.chunk_hi[ch];
+      const uint64_t nv = (lane < kSegsPerChunk && s1 > lo && s0 < hi) ? min(s1, hi) - max(s0, lo) : 0;
+      sc = lane < kSegsPerChunk ? (kDirect | (uint32_t)nv) : 0u;
+      if (lane < kSegsPerChunk) P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] = sc;
+    }
+    const bool direct = (sc & kDirect) != 0u;
+    const uint32_t c = direct ? 0u : sc;
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const uint32_t so = inc - c;                                  // lanes 0..15: segment offsets
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    const unsigned dm = __ballot_sync(0xFFFFFFFFu, direct) & 0xFFFFu;
+    const uint32_t cs = (uint32_t)P.cs;
+    uint64_t* cd = seg_slot(P, (uint64_t)ch * kSegsPerChunk);
+    for (uint32_t base = 0; base < total; base += 32 * kUnroll) {
+      uint64_t v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t cc = base + u * 32 + lane;
+        int s = 0;   // segment of candidate cc: max{s : so[s] <= cc}, by shuffles over lanes 0..15
+#pragma unroll
+        for (int step = 8; step; step >>= 1) {
+          const uint32_t t = __shfl_sync(0xFFFFFFFFu, so, s + step);
+          if (t <= cc) s += step;
+        }
+        const uint32_t sos = __shfl_sync(0xFFFFFFFFu, so, s);
+        v[u] = cc < total ? cd[(uint32_t)s * cs + (cc - sos)] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t cc = base + u * 32 + lane;
+        if (cc < total) cd[cc] = v[u];
+        const uint32_t bin = (uint32_t)(v[u] >> 52) & 0x7FFu;   // key bits [30:20]
+        if (uniform) { if (cc < total) atomicAdd(&h0[bin], 1u); }
+        else warp_hist_add(h0, cc < total, bin);
+      }
+    }
+    uint32_t dcnt = 0;   // DIRECT segments: their candidates read from acc
+    for (unsigned m = dm; m; m &= m - 1) {
+      visit_direct(P, src, ch, __ffs(m) - 1, thr, lane, [&](bool ok, uint32_t bits, uint32_t) {
+        if (uniform) { if (ok) atomicAdd(&h0[(bits >> 20) & 0x7FFu], 1u); }
+        else warp_hist_add(h0, ok, (bits >> 20) & 0x7FFu);
+        dcnt += ok;
+      });
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dcnt += __shfl_xor_sync(0xFFFFFFFFu, dcnt, o);
+    if (lane == 0) {
+      P.chunk_count[ch] = total;
+      P.chunk_dm[ch] = dm;
+      if (uniform) atomicAdd(&s_tot, total + dcnt);
+      else atomicAdd(&P.layer_total[slot], total + dcnt);   // per-layer candidate count
+    }
+  }
+  if (uniform) {
+    __syncthreads();
+    uint32_t* hrow = P.hist + (uint64_t)P.chunk_slot[c_first] * kHistRow;
+    for (int b = threadIdx.x; b < kH0; b += 256)
+      if (sh[b]) atomicAdd(&hrow[b], sh[b]);
+    if (threadIdx.x == 0 && s_tot) atomicAdd(&P.layer_total[P.chunk_slot[c_first]], s_tot);
+  }
+  }
+}
+
 // ---------------------------------------------------------------- per-layer plan / digit search
 #ifndef LD_L1_DROP
 #define LD_L1_DROP (1u << 21)
 #endif
 constexpr uint32_t kL1Drop = LD_L1_DROP;   // level-1 threshold step below a missed band (key units)
 
-__device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpret_cast<volatile const uint32_t*>(p); }
+__device__ __forceinline__ uint32_t layer_candidates(const DevPlan& P, int slot) {
+  return *reinterpret_cast<volatile const uint32_t*>(P.layer_total + slot);
+}
 
-// queue a refill of the layer at `level` (1: rescan at thr_used, 2: every element, read directly)
-__device__ void queue_refill(const DevPlan& P, int slot, int level, int lane) {
+// queue every chunk of the layer for a refill at `level` (zeroes the layer's digit-0 histogram)
+__device__ void queue_refill(const DevPlan& P, int slot, int level, int c0, int c1, int lane) {
   uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
   for (int b = lane; b < kH0; b += 32) hrow[b] = 0;
   if (lane == 0) {
-    P.layer_total[slot] = 0;   // the rescan recounts
-    const uint32_t at = atomicAdd(&P.counters[level == 1 ? 0 : 4], 1u);
-    (level == 1 ? P.refill_list : P.refill_list2)[at] = (uint32_t)slot;
+    P.layer_total[slot] = 0;   // the refill's chunk_prep recounts every chunk
     P.trace[slot] = (uint32_t)level;
   }
+  uint32_t base = 0;
+  if (lane == 0) base = atomicAdd(&P.counters[level == 2 ? 4 : 0], (uint32_t)(c1 - c0));
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  uint32_t* list = level == 2 ? P.refill_list2 : P.refill_list;
+  for (int c = c0 + lane; c < c1; c += 32) list[base + (c - c0)] = (uint32_t)c;
 }
 
-// mode 0: after the first pass -- hit: digit 0; miss: queue a level-1 (or level-2) refill
-// mode 1: after a rescan -- level 1 hit: digit 0; level 1 still short: queue level 2; level 2: digit 0
-// mode 2/3: digit 1/2 (mode 2 also predicts the next call's band)
-__device__ void find_layer(const DevPlan& P, int slot, int mode, int lane) {
+// mode 0: after the scan -- hit: digit 0; miss: queue a level-1 (or level-2) refill
+// mode 1: after the level-1 rescan -- hit: digit 0; still short: queue level 2
+// mode 4: after the level-2 prep -- digit 0 (every element a candidate)
+// mode 2/3: digit 1/2 for every large layer (mode 2 also predicts the next call's band)
+__global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
+  pdl_wait();
+  pdl_trigger();
+  const int slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (slot >= P.n_large) return;
   const int li = P.large_layers[slot];
   const uint32_t k = P.layer_k[li];
   LayerSel& S = P.sel[slot];
   uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
+  const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
   if (mode == 0) {
-    const uint32_t tot = vload(P.layer_total + slot);
+    const uint32_t tot = layer_candidates(P, slot);
     if (tot >= k) {
       uint32_t bin, above;
       warp_find_bin(hrow, kH0, k, &bin, &above);
       if (lane == 0) {
         S.prefix = bin; S.kleft = k - above; S.total = tot; S.refill = 0;
-        P.thr_used[slot] = min(P.thr[slot], 0x7F800000u);
         P.trace[slot] = 0;
+        P.thr_used[slot] = min(P.thr[slot], 0x7F800000u);   // the scan's band (DIRECT re-reads)
         // adapt the band: the previous call chose it to admit `band` x k keys of ITS distribution;
         // under error feedback the accumulated values drift upward between calls, so the band
         // admitted tot / k x k now.  Aim the next band at kBandAim x k_l admitted.
@@ -535,36 +681,43 @@ __device__ void find_layer(const DevPlan& P, int slot, int mode, int lane) {
       // missed.  Level 1 rescans at the safe threshold (this distribution's band, without the
       // drift share) when that is lower than the one that missed, else at the missed threshold
       // lowered by a quarter binade (x0.75-0.875 in value); level 2 (every element) only when
-      // neither exists.
+      // neither exists.  Without the second option a miss with no drift lead went straight to
+      // level 2, which for a large layer cost ~1 ms.
       const uint32_t th = P.thr[slot], ts = P.thr_safe[slot];
       uint32_t l1 = 0xFFFFFFFFu;
       if (ts < th) l1 = ts;
       else if (th != 0xFFFFFFFFu && th > kL1Drop) l1 = min(th, 0x7F800000u) - kL1Drop;
       const int level = l1 != 0xFFFFFFFFu ? 1 : 2;
+      if (lane == 0) P.thr_used[slot] = level == 1 ? min(l1, 0x7F800000u) : 0u;   // read by the refill
+      queue_refill(P, slot, level, c0, c1, lane);
       if (lane == 0) {
-        P.thr_used[slot] = level == 1 ? min(l1, 0x7F800000u) : 0u;
         S.refill = (uint32_t)level;
         S.total = (uint32_t)(P.layer_off[li + 1] - P.layer_off[li]);
         S.alpha *= 0.5f;                          // the drift prediction overshot
         if (level == 2) S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : kBandAim;   // widen
         atomicAdd(&P.counters[2], 1u);
       }
-      queue_refill(P, slot, level, lane);
     }
   } else if (mode == 1) {
-    const uint32_t tot = vload(P.layer_total + slot);
-    if (S.refill == 1 && tot < k) {
-      if (lane == 0) {
-        P.thr_used[slot] = 0u;
-        S.refill = 2;
-        S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : kBandAim;
-      }
-      queue_refill(P, slot, 2, lane);
-    } else {
+    if (S.refill != 1) return;
+    const uint32_t tot = layer_candidates(P, slot);
+    if (tot >= k) {
       uint32_t bin, above;
       warp_find_bin(hrow, kH0, k, &bin, &above);
       if (lane == 0) { S.prefix = bin; S.kleft = k - above; S.total = tot; }
+    } else {
+      if (lane == 0) P.thr_used[slot] = 0u;
+      queue_refill(P, slot, 2, c0, c1, lane);
+      if (lane == 0) {
+        S.refill = 2;
+        S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : kBandAim;
+      }
     }
+  } else if (mode == 4) {
+    if (S.refill != 2) return;
+    uint32_t bin, above;
+    warp_find_bin(hrow, kH0, k, &bin, &above);
+    if (lane == 0) { S.prefix = bin; S.kleft = k - above; }
   } else {
     const int nb = mode == 2 ? kH1 : kH2;
     const uint32_t* h = hrow + (mode == 2 ? kH0 : kH0 + kH1);
@@ -590,7 +743,7 @@ __device__ void find_layer(const DevPlan& P, int slot, int mode, int lane) {
       }
       // drift share: under error feedback the k-th key moved from T_{t-1} (sel_T, still the previous
       // call's) to T_t (>= the digit-1 prefix); lead the next band by alpha x the smaller of this
-      // drift and the previous call's, so a T that alternates gets no lead
+      // drift and the previous call's, so a T that alternates (periodic inputs) gets no lead.
       const uint32_t t_lo = ((S.prefix << 11) | bin) << 9;
       const uint32_t t_prev = P.sel_T[slot];
       const uint32_t d_now = (t_prev != 0xFFFFFFFFu && t_lo > t_prev) ? t_lo - t_prev : 0u;
@@ -607,291 +760,65 @@ __device__ void find_layer(const DevPlan& P, int slot, int mode, int lane) {
   }
 }
 
-// Rescan one segment of a refilled layer: level 1 stores the candidates >= thr_used (bounded, as
-// the scan); level 2 stores nothing (every element is a candidate, read directly later).  Both add
-// the digit-0 bins and the count to the CTA's shared histogram h0 / counter cnt_sh.
-template <bool EF>
-__device__ void rescan_segment(const DevPlan& P, const float* __restrict__ g, float* __restrict__ r, int slot,
-                               int ch, int seg, int level, uint64_t* sbuf, uint32_t* h0, uint32_t* cnt_sh, int lane) {
-  const uint64_t segid = (uint64_t)ch * kSegsPerChunk + seg;
-  if (level == 2) {
-    uint32_t cnt = 0;
-    visit_direct(P, EF ? r : g, ch, seg, 0u, lane, [&](bool ok, uint32_t bits, uint32_t) {
-      warp_hist_add(h0, ok, (bits >> 20) & 0x7FFu);
-      cnt += ok;
-    });
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
-    if (lane == 0) {
-      P.seg_count[segid] = cnt | kDirect;
-      if (cnt) atomicAdd(cnt_sh, cnt);
-      P.dlist[atomicAdd(&P.counters[5], 1u)] = (uint32_t)segid | (2u << 30);   // DIRECT, level 2
-    }
-    return;
-  }
-  const uint64_t cbase = P.chunk_base[ch];
-  const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
-  const uint32_t cs = (uint32_t)P.cs;
-  const uint32_t sb = (uint32_t)seg * kSeg;
-  const unsigned lt = (1u << lane) - 1u;
-  bool bad = false;
-  const uint32_t run = scan_segment<EF, true, false, true>(g + cbase, r + cbase, seg_slot(P, segid), cs, h0, sbuf, sb,
-                                                           lo, hi, (uint32_t)cbase, P.thr_used[slot], 0xFFFFFFFFu, 0u,
-                                                           lane, lt, bad);
-  if (lane == 0) {
-    P.seg_count[segid] = run > cs ? (run | kDirect) : run;
-    if (run) atomicAdd(cnt_sh, run);
-    if (run > cs) P.dlist[atomicAdd(&P.counters[5], 1u)] = (uint32_t)segid | (1u << 30);   // DIRECT, level 1
-  }
-}
-
-// ---------------------------------------------------------------- the persistent select kernel
-// One cooperative launch after the scan (grid = co-resident CTAs), phases separated by grid
-// barriers.  CTA b owns the contiguous chunk range [cb, ce) for the streaming phases and walks it
-// in WINDOWS of at most kWin chunks of one layer.  The first pass COMPACTS each window in place:
-// its 16 kWin segment counts go to shared memory and are prefix-summed, the stored candidates are
-// read as one flat, index-ordered list (item j -> its segment by binary search over the prefix) and
-// written back contiguously at the window's start (a candidate never moves up; each round loads
-// before it stores), histogramming digit 0 on the way.  Every later pass then streams the window's
-// contiguous list with 128-bit loads, many in flight per thread.  DIRECT segments (more candidates
-// than their slot, or level-2 layers) stay out of the list and are read from acc by warps.
-// Histograms aggregate per window in shared memory; the per-chunk counts are prefix-summed per
-// layer run inside the CTA, and only the CTA's last run is published (tail) for later CTAs of the
-// same layer (reduce-then-scan); the ordered emit scans the window's flags block-wide.
-constexpr int kWin = kSelThreads;     // chunks per window (one per thread at setup)
-constexpr int kStreamV = 4;           // 128-bit loads (2 candidates each) in flight per thread and round
-constexpr int kStreamItems = 2 * kStreamV;
-
-struct SelShared {
-  uint32_t hist[kH0];
-  uint32_t pre[kWin * kSegsPerChunk];   // compaction: exclusive prefix of the window's stored segment counts
-  uint32_t cst[kWin + 1];               // window-relative start of each chunk's compacted candidates
-  uint32_t dm[kWin];                    // DIRECT-segment bitmask per chunk
-  uint32_t cw0[kWin], cw1[kWin];        // per chunk: counts (count pass) / window starts (emit)
-  uint32_t take[kWin];                  // emit: ties to take | 0x80000000 if the layer's last tie is here
-  uint32_t dst[kWin];                   // emit: output offset of the chunk's first entry
-  uint32_t sw[33];
-  uint32_t cnt, lvl;
-  unsigned long long head;
-};
-
-// per-chunk metadata written by the select kernel (global, [n_chunks] each): cpos = absolute offset
-// (in candidates) of the chunk's compacted stored list, ccnt its length, cgt / ceq its counts of
-// key > T / key == T (stored + DIRECT), cgtb / ceqb their exclusive prefixes inside the CTA's range
-struct ChunkMeta {
-  uint32_t *cpos, *ccnt, *cgt, *ceq, *cgtb, *ceqb;
-};
-__device__ __forceinline__ ChunkMeta chunk_meta(const DevPlan& P) {
-  uint32_t* b = reinterpret_cast<uint32_t*>(P.chunk_state);
-  const uint32_t n = (uint32_t)P.n_chunks;
-  return ChunkMeta{b, b + n, b + 2 * n, b + 3 * n, b + 4 * n, b + 5 * n};
-}
-
-// iterate the CTA's range in windows of one layer: body(a, n, slot)
-template <class B>
-__device__ __forceinline__ void for_windows(const DevPlan& P, int cb, int ce, B&& body) {
-  for (int a = cb; a < ce;) {
-    const int slot = P.chunk_slot[a];
-    const int z = min(min(ce, P.large_chunk0[slot + 1]), a + kWin);
-    body(a, z - a, slot);
-    a = z;
-  }
-}
-
-// window setup after compaction: sh.cst (window-relative chunk starts), sh.dm (DIRECT masks);
-// returns the window's stored total
-__device__ uint32_t win_meta(const DevPlan& P, const ChunkMeta& M, int a, int n, SelShared& sh) {
-  const int t = threadIdx.x;
-  const uint32_t wbase = (uint32_t)a * kSegsPerChunk * (uint32_t)P.cs;
-  if (t < n) {
-    sh.cst[t] = M.cpos[a + t] - wbase;
-    uint32_t dm = 0;
-    const uint4* q = reinterpret_cast<const uint4*>(P.seg_count + (uint64_t)(a + t) * kSegsPerChunk);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint4 v = q[i];
-      dm |= (((v.x & kDirect) ? 1u : 0u) | ((v.y & kDirect) ? 2u : 0u) | ((v.z & kDirect) ? 4u : 0u) |
-             ((v.w & kDirect) ? 8u : 0u)) << (4 * i);
-    }
-    sh.dm[t] = dm;
-    if (t == n - 1) sh.cst[n] = M.cpos[a + t] + M.ccnt[a + t] - wbase;
-  }
-  __syncthreads();
-  return sh.cst[n];
-}
-
-// chunk (window-relative) of compacted item j: the largest c with cst[c] <= j (a non-empty chunk)
-__device__ __forceinline__ int win_chunk(const SelShared& sh, int n, uint32_t j) {
-  int lo = 0, hi = n;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (sh.cst[mid] <= j) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
-// the window's compacted candidates L[0, total), kStreamItems contiguous per thread per round:
-// f(ok, val_bits, idx, j) -- all threads call f equally often (warp-convergent)
-template <class F>
-__device__ __forceinline__ void win_stream(const uint64_t* __restrict__ L, uint32_t total, F&& f) {
-  for (uint32_t r0 = 0; r0 < total; r0 += kSelThreads * kStreamItems) {
-    const uint32_t j0 = r0 + threadIdx.x * kStreamItems;
-    uint64_t v[kStreamItems];
-    if (j0 + kStreamItems <= total) {
-      const uint4* q = reinterpret_cast<const uint4*>(L + j0);
-#pragma unroll
-      for (int u = 0; u < kStreamV; ++u) {
-        const uint4 x = __ldcg(q + u);
-        v[2 * u] = ((uint64_t)x.y << 32) | x.x;
-        v[2 * u + 1] = ((uint64_t)x.w << 32) | x.z;
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < kStreamItems; ++u) v[u] = j0 + u < total ? L[j0 + u] : 0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < kStreamItems; ++u) f(j0 + u < total, (uint32_t)(v[u] >> 32), (uint32_t)v[u], j0 + u);
-  }
-}
-
-// Every valid DIRECT segment of the call, grid-wide, one segment per CTA round (thread t reads the
-// segment's float4 t): f(ok, key_bits, idx, chunk, slot) for each thread's 4 elements (CTA-uniform
-// control flow).  An entry is valid when its level equals the layer's final refill level (entries
-// of a layer that was rescanned afterwards are stale); any_level: every entry (the first pass, before
-// this call's plan).  thr: the layer's threshold of that level.
-static_assert(kSeg == 4 * kSelThreads, "direct_all: one float4 of the segment per thread");
-template <class F>
-__device__ __forceinline__ void direct_all(const DevPlan& P, const float* __restrict__ src, bool any_level, F&& f) {
-  const uint32_t nd = vload(P.counters + 5);
-  const int t = threadIdx.x;
-  for (uint32_t e = blockIdx.x; e < nd; e += gridDim.x) {
-    const uint32_t w = P.dlist[e];
-    const uint32_t segid = w & 0x3FFFFFFFu, lvl = w >> 30;
-    const int ch = (int)(segid / kSegsPerChunk), seg = (int)(segid % kSegsPerChunk);
-    const int slot = P.chunk_slot[ch];
-    if (!any_level && lvl != P.sel[slot].refill) continue;   // uniform over the CTA
-    const uint32_t thr = any_level ? min(P.thr[slot], 0x7F800000u) : P.thr_used[slot];
-    const uint64_t cbase = P.chunk_base[ch];
-    const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
-    const float* sp = src + cbase;
-    const uint32_t e0 = (uint32_t)seg * kSeg + 4u * (uint32_t)t;   // kSeg = 4 x kSelThreads
-    uint32_t vm = 0;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e0 >= lo && e0 + 4 <= hi) {
-      vm = 0xF;
-      a = *reinterpret_cast<const float4*>(sp + e0);
-    } else if (e0 + 4 > lo && e0 < hi) {
-      for (int k = 0; k < 4; ++k)
-        if (e0 + k >= lo && e0 + k < hi) { vm |= 1u << k; f4set(a, k, sp[e0 + k]); }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t bits = __float_as_uint(f4get(a, k));
-      f(((vm >> k) & 1u) && (bits & 0x7FFFFFFFu) >= thr, bits, (uint32_t)cbase + e0 + k, ch, slot);
-    }
-  }
-}
-
-// In-place compaction of window (a, n) + digit-0 histogram of its stored candidates into the
-// layer's global row and their count into layer_total; per-chunk cpos / ccnt (and cgt / ceq
-// zeroed).  The window's segment slots are contiguous, so its compacted list starts at
-// seg_slot(a * 16): a candidate never moves up, and each round loads before it stores.
-__device__ void compact_window(const DevPlan& P, const ChunkMeta& M, int a, int n, int slot, bool hist,
-                               SelShared& sh, int lane) {
-  const int t = threadIdx.x;
-  if (hist)
-    for (int i = t; i < kH0; i += kSelThreads) sh.hist[i] = 0;
-  if (t == 0) sh.cnt = 0;
-  uint32_t c[kSegsPerChunk], sum = 0;
-  if (t < n) {
-    const uint4* q = reinterpret_cast<const uint4*>(P.seg_count + (uint64_t)(a + t) * kSegsPerChunk);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint4 v = q[i];
-      c[4 * i] = v.x; c[4 * i + 1] = v.y; c[4 * i + 2] = v.z; c[4 * i + 3] = v.w;
-    }
-#pragma unroll
-    for (int i = 0; i < kSegsPerChunk; ++i) {
-      c[i] = (c[i] & kDirect) ? 0u : c[i];
-      sum += c[i];
-    }
-  }
-  uint32_t total;
-  uint32_t run = block_excl_scan(sum, sh.sw, &total);   // (its barriers also order the zeroing)
-  const uint32_t cs = (uint32_t)P.cs;
-  if (t < n) {
-    M.cpos[a + t] = (uint32_t)a * kSegsPerChunk * cs + run;
-    M.ccnt[a + t] = sum;
-    M.cgt[a + t] = 0;
-    M.ceq[a + t] = 0;
-#pragma unroll
-    for (int i = 0; i < kSegsPerChunk; ++i) { sh.pre[t * kSegsPerChunk + i] = run; run += c[i]; }
-  }
-  __syncthreads();
-  const int nseg = n * kSegsPerChunk;
-  uint64_t* L = seg_slot(P, (uint64_t)a * kSegsPerChunk);
-  constexpr int U = kStreamItems;
-  for (uint32_t r0 = 0; r0 < total; r0 += kSelThreads * U) {
-    const uint32_t j0 = r0 + t * U;
-    uint64_t v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = 0ull;
-    if (j0 < total) {
-      int lo = 0, hi = nseg;   // segment of j0: the largest s with pre[s] <= j0
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (sh.pre[mid] <= j0) lo = mid; else hi = mid;
-      }
-      int s = lo;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t j = j0 + u;
-        if (j < total) {
-          while (s + 1 < nseg && sh.pre[s + 1] <= j) ++s;
-          v[u] = L[(uint32_t)s * cs + (j - sh.pre[s])];
-        }
-      }
-    }
-    __syncthreads();   // every source of this round is read before any of its destinations is written
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const bool ok = j0 + u < total;
-      if (ok) L[j0 + u] = v[u];
-      if (hist) warp_hist_add(sh.hist, ok, (uint32_t)(v[u] >> 52) & 0x7FFu);
-    }
+// digit d (1 or 2) histogram over the candidates matching the prefix (the chunk list + its DIRECT
+// segments' acc): warp per chunk, 8 chunks per CTA aggregated in shared memory when they belong
+// to one layer
+__global__ void __launch_bounds__(256) digit_kernel(DevPlan P, const float* __restrict__ src, int d) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint32_t sh[kH1];
+  const int lane = threadIdx.x & 31;
+  const int c_first = blockIdx.x * 8;
+  const int c_last = min(P.n_chunks, c_first + 8) - 1;
+  const int ch = c_first + (threadIdx.x >> 5);
+  const bool uniform = P.chunk_slot[c_first] == P.chunk_slot[c_last];
+  const int nb = d == 1 ? kH1 : kH2;
+  if (uniform) {
+    for (int b = threadIdx.x; b < nb; b += 256) sh[b] = 0;
     __syncthreads();
   }
-  if (hist) {
-    uint32_t* hg = P.hist + (uint64_t)slot * kHistRow;
-    for (int i = t; i < kH0; i += kSelThreads)
-      if (sh.hist[i]) atomicAdd(&hg[i], sh.hist[i]);
-    if (t == 0 && total) atomicAdd(&P.layer_total[slot], total);   // stored candidates admitted
-    __syncthreads();
-  }
-}
-
-// digit d = 1 / 2 histogram (key bits [19:9] / [8:0]) of the window's stored candidates matching the prefix
-__device__ void digit_window(const DevPlan& P, const ChunkMeta& M, int d, int a, int n, int slot, SelShared& sh) {
-  const int nb = d == 1 ? kH1 : kH2, shift = d == 1 ? 9 : 0, hs = d == 1 ? 20 : 9;
+  const int shift = d == 1 ? 9 : 0;
+  const int hs = d == 1 ? 20 : 9;
   const uint32_t mask = d == 1 ? 0x7FFu : 0x1FFu;
-  for (int i = threadIdx.x; i < nb; i += kSelThreads) sh.hist[i] = 0;
-  const uint32_t total = win_meta(P, M, a, n, sh);
-  const uint32_t pre = P.sel[slot].prefix;
-  win_stream(seg_slot(P, (uint64_t)a * kSegsPerChunk), total, [&](bool ok, uint32_t bits, uint32_t, uint32_t) {
-    const uint32_t key = bits & 0x7FFFFFFFu;
-    warp_hist_add(sh.hist, ok && (key >> hs) == pre, (key >> shift) & mask);
-  });
-  __syncthreads();
-  uint32_t* hg = P.hist + (uint64_t)slot * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
-  for (int i = threadIdx.x; i < nb; i += kSelThreads)
-    if (sh.hist[i]) atomicAdd(&hg[i], sh.hist[i]);
-  __syncthreads();
+  if (ch <= c_last) {
+    const int slot = P.chunk_slot[ch];
+    const uint32_t pre = P.sel[slot].prefix;
+    uint32_t* h = uniform ? sh : P.hist + (uint64_t)slot * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
+    const uint32_t cnt = P.chunk_count[ch];
+    const uint64_t* cd = seg_slot(P, (uint64_t)ch * kSegsPerChunk);
+    auto add = [&](bool ok, uint32_t key) {
+      const bool m = ok && (key >> hs) == pre;
+      const uint32_t bin = (key >> shift) & mask;
+      if (uniform) { if (m) atomicAdd(&h[bin], 1u); }
+      else warp_hist_add(h, m, bin);
+    };
+    for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
+      uint32_t key[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t i = base + u * 32 + lane;
+        key[u] = i < cnt ? (uint32_t)(cd[i] >> 32) & 0x7FFFFFFFu : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) add(base + u * 32 + lane < cnt, key[u]);
+    }
+    const uint32_t thr = P.thr_used[slot];
+    for (unsigned m = P.chunk_dm[ch]; m; m &= m - 1)
+      visit_direct(P, src, ch, __ffs(m) - 1, thr, lane,
+                   [&](bool ok, uint32_t bits, uint32_t) { add(ok, bits & 0x7FFFFFFFu); });
+  }
+  if (uniform) {
+    __syncthreads();
+    uint32_t* hg = P.hist + (uint64_t)P.chunk_slot[c_first] * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
+    for (int b = threadIdx.x; b < nb; b += 256)
+      if (sh[b]) atomicAdd(&hg[b], sh[b]);
+  }
 }
 
 // Ordered emit of a chunk with a DIRECT segment (warp): its segments in index order -- the stored
 // ones from its compacted run Lc (segment after segment), the DIRECT ones from acc.  dst0 = output
 // offset of its first entry; it takes `take` of its ties (lowest index first).
-__device__ void emit_dirty_chunk(const DevPlan& P, const float* __restrict__ src, int ch, const uint64_t* Lc,
+__device__ __noinline__ void emit_dirty_chunk(const DevPlan& P, const float* __restrict__ src, int ch, const uint64_t* Lc,
                                  uint32_t* __restrict__ send, uint64_t K, uint64_t dst0, uint32_t T, uint32_t take,
                                  bool last_tie_chunk, int slot, int lane) {
   const unsigned lt = (1u << lane) - 1u;
@@ -991,376 +918,131 @@ __device__ void emit_dirty_chunk(const DevPlan& P, const float* __restrict__ src
   }
 }
 
-// phase timestamps of the select kernel (block 0, %globaltimer ns): lowdiff_compress_phases
-__device__ __forceinline__ void phase_mark(const DevPlan& P, int i) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    P.phase_ns[i] = t;
-  }
+// (key > T, key == T) counts of the chunk's DIRECT segments (dm), added to *gt / *eq (per lane);
+// out of line, so the common path of count_emit keeps its 32-register budget
+__device__ __noinline__ void count_direct(const DevPlan& P, const float* __restrict__ src, int ch, unsigned dm,
+                                          uint32_t T, int lane, uint32_t* gt, uint32_t* eq) {
+  uint32_t g = *gt, e = *eq;
+  for (unsigned m = dm; m; m &= m - 1)
+    visit_direct(P, src, ch, __ffs(m) - 1, 0u, lane, [&](bool ok, uint32_t bits, uint32_t) {
+      const uint32_t key = bits & 0x7FFFFFFFu;
+      g += ok && key > T;
+      e += ok && key == T;
+    });
+  *gt = g;
+  *eq = e;
 }
 
-// the CTA that owns chunk ch in the select's static partition (cb(b) = floor(n_chunks b / G))
-__device__ __forceinline__ int owner_cta(int ch, int n_chunks, int G) {
-  int b = (int)(((int64_t)ch * G) / n_chunks);
-  while (b + 1 < G && (int)((int64_t)n_chunks * (b + 1) / G) <= ch) ++b;
-  while (b > 0 && (int)((int64_t)n_chunks * b / G) > ch) --b;
-  return b;
-}
-
-#ifndef LD_SEL_MINB
-#define LD_SEL_MINB 3
-#endif
-
-template <bool EF>
-__global__ void __launch_bounds__(kSelThreads, LD_SEL_MINB)
-select_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, uint32_t* __restrict__ send, uint64_t K) {
-  __shared__ uint64_t sbuf_all[kSelWarps][kCandBuf];
-  __shared__ SelShared sh;
-  cg::grid_group grid = cg::this_grid();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, t = threadIdx.x;
-  const int gw = blockIdx.x * kSelWarps + warp, nw = gridDim.x * kSelWarps;
-  const float* src = EF ? r : g;
-  const ChunkMeta M = chunk_meta(P);
-  const int cb = (int)((int64_t)P.n_chunks * blockIdx.x / gridDim.x);
-  const int ce = (int)((int64_t)P.n_chunks * (blockIdx.x + 1) / gridDim.x);
-  if (blockIdx.x == 0 && t < 16) P.phase_ns[t] = 0;   // phases not run stay 0
-  __syncthreads();
-  phase_mark(P, 0);
-  // 1. compact every window in place + digit 0 of its stored candidates; digit 0 of the DIRECT
-  //    segments' candidates grid-wide
-  for_windows(P, cb, ce, [&](int a, int n, int slot) { compact_window(P, M, a, n, slot, true, sh, lane); });
-  {
-    uint32_t cnt = 0;
-    int cur_slot = -1;
-    direct_all(P, src, true, [&](bool ok, uint32_t bits, uint32_t, int, int slot) {
-      warp_hist_add(P.hist + (uint64_t)slot * kHistRow, ok, (bits >> 20) & 0x7FFu);
-      if (slot != cur_slot) {   // (uniform over the CTA: one segment per round)
-        if (cur_slot >= 0) {
+// count + layer scan + emit in one kernel (warp per chunk): the chunk's #(key > T) and #(key == T)
+// (list + DIRECT segments), then a decoupled look-back over the earlier chunks of its layer (their
+// published counts, 32 per round) gives the ties taken before it and its output offset, then the
+// ordered emit (the list's second read hits L1/L2; a chunk with a DIRECT segment is emitted
+// segment by segment).  The layer's first chunk also does the per-layer bookkeeping.
+__global__ void __launch_bounds__(256, 8) count_emit_kernel(DevPlan P, const float* __restrict__ src,
+                                                              uint32_t* __restrict__ send, uint64_t K) {
+  pdl_wait();
+  pdl_trigger();
+  const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
+  const int lane = threadIdx.x & 31;
+  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ch >= P.n_chunks) return;   // whole warps
+  const unsigned lt = (1u << lane) - 1u;
+  const int slot = P.chunk_slot[ch];
+  const int c0 = P.large_chunk0[slot];
+  const uint32_t T = P.sel[slot].prefix, need = P.sel[slot].kleft;
+  const uint32_t cnt = P.chunk_count[ch];
+  const unsigned dmask = P.chunk_dm[ch];
+  const uint64_t* cd = seg_slot(P, (uint64_t)ch * kSegsPerChunk);
+  uint32_t gt = 0, eq = 0;
+  for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
 #pragma unroll
-          for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
-          if (lane == 0 && cnt) atomicAdd(&P.layer_total[cur_slot], cnt);
-          cnt = 0;
-        }
-        cur_slot = slot;
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t i = base + u * 32 + lane;
+      if (i < cnt) {
+        const uint32_t key = (uint32_t)(cd[i] >> 32) & 0x7FFFFFFFu;
+        gt += key > T;
+        eq += key == T;
       }
-      cnt += ok;
-    });
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
-    if (lane == 0 && cnt && cur_slot >= 0) atomicAdd(&P.layer_total[cur_slot], cnt);
-  }
-  grid.sync();
-  phase_mark(P, 1);
-  // 2. plan: per large layer, hit or refill
-  for (int slot = gw; slot < P.n_large; slot += nw) find_layer(P, slot, 0, lane);
-  grid.sync();
-  phase_mark(P, 2);
-  // 3. refills: level 1 (rescan at the safe threshold, stored), then level 2 (every element, DIRECT).
-  // list 1: layers queued at level 1 by the plan; list 2: queued at level 2 by the plan, or still
-  // short after their level-1 rescan (appended by find_layer mode 1 in pass 0)
-  for (int pass = 0; pass < 2; ++pass) {
-    const uint32_t n_ref = vload(P.counters + (pass == 0 ? 0 : 4));
-    if (n_ref == 0) continue;   // uniform: every thread reads the same value after the barrier
-    const uint32_t* list = pass == 0 ? P.refill_list : P.refill_list2;
-    for (uint32_t i = 0; i < n_ref; ++i) {   // layer by layer; its segments over the whole grid
-      const int slot = (int)list[i];
-      const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
-      const int nseg = (c1 - c0) * kSegsPerChunk;
-      for (int b = t; b < kH0; b += kSelThreads) sh.hist[b] = 0;
-      if (t == 0) sh.cnt = 0;
-      __syncthreads();
-      for (int s = gw; s < nseg; s += nw)
-        rescan_segment<EF>(P, g, r, slot, c0 + s / kSegsPerChunk, s % kSegsPerChunk, pass + 1, sbuf_all[warp],
-                           sh.hist, &sh.cnt, lane);
-      __syncthreads();
-      uint32_t* hg = P.hist + (uint64_t)slot * kHistRow;
-      for (int b = t; b < kH0; b += kSelThreads)
-        if (sh.hist[b]) atomicAdd(&hg[b], sh.hist[b]);
-      if (t == 0 && sh.cnt) atomicAdd(&P.layer_total[slot], sh.cnt);
-      __syncthreads();
     }
-    grid.sync();
-    phase_mark(P, 3 + 2 * pass);
-    // re-compact the rescanned windows (their histogram is complete), then plan.  The level is read
-    // once per CTA: another CTA's plan below may already escalate the layer (1 -> 2), and every
-    // thread of the CTA must take the same branch; an escalated layer is re-compacted in pass 1.
-    for_windows(P, cb, ce, [&](int a, int n, int slot) {
-      if (t == 0) sh.lvl = P.sel[slot].refill;
-      __syncthreads();
-      const uint32_t lvl = sh.lvl;
-      __syncthreads();
-      if (lvl == (uint32_t)(pass + 1)) compact_window(P, M, a, n, slot, false, sh, lane);
-    });
-    for (uint32_t i = gw; i < n_ref; i += nw) find_layer(P, (int)list[i], 1, lane);
-    grid.sync();
-    phase_mark(P, 4 + 2 * pass);
   }
-  // 4. digits 1 and 2 over the candidates matching the prefix
-  for (int d = 1; d <= 2; ++d) {
-    const int shift = d == 1 ? 9 : 0, hs = d == 1 ? 20 : 9;
-    const uint32_t mask = d == 1 ? 0x7FFu : 0x1FFu;
-    for_windows(P, cb, ce, [&](int a, int n, int slot) { digit_window(P, M, d, a, n, slot, sh); });
-    direct_all(P, src, false, [&](bool ok, uint32_t bits, uint32_t, int, int slot) {
-      const uint32_t key = bits & 0x7FFFFFFFu;
-      warp_hist_add(P.hist + (uint64_t)slot * kHistRow + (d == 1 ? kH0 : kH0 + kH1),
-                    ok && (key >> hs) == P.sel[slot].prefix, (key >> shift) & mask);
-    });
-    grid.sync();
-    phase_mark(P, 5 + 2 * d);
-    for (int slot = gw; slot < P.n_large; slot += nw) find_layer(P, slot, d == 1 ? 2 : 3, lane);
-    grid.sync();
-    phase_mark(P, 6 + 2 * d);
-  }
-  // 5. counts per chunk (key > T, key == T): stored per window, DIRECT grid-wide (both add)
-  for_windows(P, cb, ce, [&](int a, int n, int slot) {
-    if (t < n) { sh.cw0[t] = 0; sh.cw1[t] = 0; }
-    const uint32_t total = win_meta(P, M, a, n, sh);
-    const uint32_t T = P.sel[slot].prefix;
-    int cc = 0;
-    uint32_t last_j0 = 0xFFFFFFFFu;
-    win_stream(seg_slot(P, (uint64_t)a * kSegsPerChunk), total, [&](bool ok, uint32_t bits, uint32_t, uint32_t j) {
-      if (ok) {   // items are contiguous per thread: the chunk of the first by binary search, then advance
-        const uint32_t j0 = j - (j % kStreamItems);
-        if (j0 != last_j0) { cc = win_chunk(sh, n, j); last_j0 = j0; }
-        while (cc + 1 < n && sh.cst[cc + 1] <= j) ++cc;
-      }
-      const uint32_t key = bits & 0x7FFFFFFFu;
-      const bool gt = ok && key > T, eq = ok && key == T;
-      const unsigned act = __ballot_sync(0xFFFFFFFFu, gt || eq);
-      if (gt || eq) {
-        const unsigned peers = __match_any_sync(act, cc);
-        const unsigned ng = __popc(__ballot_sync(act, gt) & peers), ne = __popc(__ballot_sync(act, eq) & peers);
-        if (lane == __ffs(peers) - 1) {
-          if (ng) atomicAdd(&sh.cw0[cc], ng);
-          if (ne) atomicAdd(&sh.cw1[cc], ne);
-        }
-      }
-    });
-    __syncthreads();
-    if (t < n) {
-      if (sh.cw0[t]) atomicAdd(&M.cgt[a + t], sh.cw0[t]);
-      if (sh.cw1[t]) atomicAdd(&M.ceq[a + t], sh.cw1[t]);
-    }
-    __syncthreads();
-  });
-  {
-    uint32_t gtc = 0, eqc = 0;
-    int cur = -1;
-    auto flush = [&]() {
+  if (dmask) count_direct(P, src, ch, dmask, T, lane, &gt, &eq);
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        gtc += __shfl_xor_sync(0xFFFFFFFFu, gtc, o);
-        eqc += __shfl_xor_sync(0xFFFFFFFFu, eqc, o);
-      }
-      if (lane == 0 && cur >= 0) {
-        if (gtc) atomicAdd(&M.cgt[cur], gtc);
-        if (eqc) atomicAdd(&M.ceq[cur], eqc);
-      }
-      gtc = eqc = 0;
-    };
-    direct_all(P, src, false, [&](bool ok, uint32_t bits, uint32_t, int ch, int slot) {
-      if (ch != cur) { flush(); cur = ch; }   // (uniform over the CTA)
-      const uint32_t key = bits & 0x7FFFFFFFu, T = P.sel[slot].prefix;
-      gtc += ok && key > T;
-      eqc += ok && key == T;
-    });
-    flush();
+  for (int o = 16; o; o >>= 1) {
+    gt += __shfl_xor_sync(0xFFFFFFFFu, gt, o);
+    eq += __shfl_xor_sync(0xFFFFFFFFu, eq, o);
   }
-  grid.sync();
-  phase_mark(P, 11);
-  // 6. in-CTA exclusive scan of the counts, restarting at every layer boundary; the CTA's last
-  //    run's total is published for the CTAs after it (reduce-then-scan)
-  if (warp == 0) {
-    unsigned long long carry = 0;
-    int cur = -1;
-    for (int a = cb; a < ce; a += 32) {
-      const int ch = a + lane;
-      const bool in = ch < ce;
-      const int slot = in ? P.chunk_slot[ch] : -1;
-      const unsigned long long v = in ? (((unsigned long long)M.ceq[ch] << 31) | M.cgt[ch]) : 0ull;
-      // segmented inclusive scan (segments = layer runs; slots ascend with the chunk index):
-      // (x, fx) + (y, fy) = (fy ? y : x + y, fx | fy)
-      const int prev = __shfl_up_sync(0xFFFFFFFFu, slot, 1);
-      bool f = in && (lane == 0 ? slot != cur : slot != prev);
-      unsigned long long inc = v;
+  // per-layer counts < 2^31, so (eq << 31 | gt) words add without carries between the fields
+  const unsigned long long mine = ((unsigned long long)eq << 31) | gt;
+  unsigned long long before = 0;
+  if (ch == c0) {
+    if (lane == 0) atomicExch(P.chunk_state + ch, kInc | mine);
+  } else {
+    if (lane == 0) atomicExch(P.chunk_state + ch, kAgg | mine);
+    int p = ch - 1;
+    for (;;) {
+      const int q = p - lane;   // lane 0: the nearest earlier chunk
+      const unsigned long long w =
+          q >= c0 ? *reinterpret_cast<volatile unsigned long long*>(P.chunk_state + q) : kInc;
+      if (__any_sync(0xFFFFFFFFu, (w >> 62) == 0ull)) continue;   // not published yet
+      const unsigned inc = __ballot_sync(0xFFFFFFFFu, (w >> 62) == 2ull);
+      const int stop = inc ? __ffs(inc) - 1 : 31;
+      unsigned long long v = lane <= stop ? (w & kVal) : 0ull;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-        const bool fy = __shfl_up_sync(0xFFFFFFFFu, f, o);
-        if (lane >= o) {
-          if (!f) inc += y;
-          f = f || fy;
-        }
-      }
-      if (!f) inc += carry;   // no run start in [round start, lane]: continues the previous round's run
-      const unsigned long long exc = inc - v;
-      if (in) {
-        M.cgtb[ch] = (uint32_t)(exc & 0x7FFFFFFFull);
-        M.ceqb[ch] = (uint32_t)(exc >> 31);
-      }
-      const int last = min(31, ce - 1 - a);
-      carry = __shfl_sync(0xFFFFFFFFu, inc, last);
-      cur = __shfl_sync(0xFFFFFFFFu, slot, last);
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+      before += v;
+      if (inc) break;
+      p -= 32;
     }
     if (lane == 0) {
-      P.tail_agg[blockIdx.x] = ce > cb ? carry : 0ull;        // the CTA's last run: its layer's partial sum
-      P.tail_slot[blockIdx.x] = ce > cb ? (uint32_t)cur : 0xFFFFFFFEu;   // no chunks: transparent
+      __threadfence();
+      atomicExch(P.chunk_state + ch, kInc | (before + mine));
     }
   }
-  grid.sync();
-  phase_mark(P, 12);
-  // the CTA's first layer may have started in earlier CTAs: their published tails of that layer;
-  // the full "before" counts of every chunk of the range are then written back (cgtb / ceqb)
-  if (warp == 0) {
-    unsigned long long head = 0;
-    if (ce > cb) {
-      const uint32_t slot0 = (uint32_t)P.chunk_slot[cb];
-      if (P.large_chunk0[slot0] < cb) {
-        for (int b = (int)blockIdx.x - 1; b >= 0; b -= 32) {
-          const int q = b - lane;
-          const uint32_t ts = q >= 0 ? P.tail_slot[q] : 0u;
-          const bool same = q >= 0 && (ts == slot0 || ts == 0xFFFFFFFEu);
-          const unsigned stop = __ballot_sync(0xFFFFFFFFu, !same);
-          const int n_same = stop ? __ffs(stop) - 1 : 32;
-          unsigned long long v = lane < n_same ? P.tail_agg[q] : 0ull;
-#pragma unroll
-          for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-          head += v;
-          if (stop) break;
-        }
-      }
-    }
-    if (lane == 0) sh.head = head;
+  const uint32_t gt_b = (uint32_t)(before & 0x7FFFFFFFull), eq_b = (uint32_t)(before >> 31);
+  const uint32_t take_b = min(eq_b, need);       // ties are taken in chunk order, then index order
+  const uint32_t take = min(eq, need - take_b);
+  const bool last_tie_chunk = take > 0 && take_b + take == need;
+  if (ch == c0 && lane == 0) {
+    P.sel_T[slot] = T;
+    // speculative band for the next call: the drift-led threshold (may exceed T)
+    // and the safe one (never above this call's T) that a level-1 refill falls back to
+    const uint32_t ns = P.sel[slot].next_safe;
+    const uint32_t sf = ns <= T ? ns : T;
+    P.thr_safe[slot] = sf;
+    P.thr[slot] = max(sf, P.sel[slot].next_thr);
   }
-  __syncthreads();
-  {
-    const unsigned long long head = sh.head;
-    const int first_run_end = ce > cb ? min(ce, P.large_chunk0[P.chunk_slot[cb] + 1]) : cb;
-    if (head)
-      for (int ch = cb + t; ch < first_run_end; ch += kSelThreads) {
-        const unsigned long long b = (((unsigned long long)M.ceqb[ch] << 31) | M.cgtb[ch]) + head;
-        M.cgtb[ch] = (uint32_t)(b & 0x7FFFFFFFull);
-        M.ceqb[ch] = (uint32_t)(b >> 31);
-      }
+  const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + gt_b + take_b;
+  if (dmask) {
+    emit_dirty_chunk(P, src, ch, cd, send, K, dst0, T, take, last_tie_chunk, slot, lane);
+    return;
   }
-  const bool any_direct = vload(P.counters + 5) != 0;
-  if (any_direct) grid.sync();   // the dirty-chunk emit below reads other CTAs' chunks (uniform)
-  // 7. ordered emit: clean chunks block-parallel over the window's compacted list (flags scanned
-  //    block-wide); chunks with a DIRECT segment by a warp each, grid-wide
-  for_windows(P, cb, ce, [&](int a, int n, int slot) {
-    const uint32_t T = P.sel[slot].prefix, need = P.sel[slot].kleft;
-    uint32_t wgt = 0, weq = 0;
-    if (t < n) {
-      const int ch = a + t;
-      const uint32_t gt_b = M.cgtb[ch], eq_b = M.ceqb[ch];
-      const uint32_t take_b = min(eq_b, need);       // ties are taken in chunk order, then index order
-      const uint32_t take = min(M.ceq[ch], need - take_b);
-      const bool last_tie = take > 0 && take_b + take == need;
-      sh.take[t] = take | (last_tie ? 0x80000000u : 0u);
-      sh.dst[t] = (uint32_t)(P.layer_koff[P.large_layers[slot]] + gt_b + take_b);
-      wgt = M.cgt[ch];
-      weq = M.ceq[ch];
-      if (ch == P.large_chunk0[slot]) {
-        P.sel_T[slot] = T;
-        // speculative band for the next call: the drift-led threshold (may exceed T)
-        // and the safe one (never above this call's T) that a level-1 refill falls back to
-        const uint32_t ns = P.sel[slot].next_safe;
-        const uint32_t sf = ns <= T ? ns : T;
-        P.thr_safe[slot] = sf;
-        P.thr[slot] = max(sf, P.sel[slot].next_thr);
-      }
+  uint32_t eq_run = 0, out_run = 0;
+  for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
+    uint64_t v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t i = base + u * 32 + lane;
+      v[u] = i < cnt ? cd[i] : 0ull;
     }
-    const uint32_t total = win_meta(P, M, a, n, sh);
-    if (t < n && sh.dm[t] != 0) { wgt = 0; weq = 0; }   // dirty chunks: emitted below
-    uint32_t tot2;
-    const uint32_t wsg = block_excl_scan(wgt, sh.sw, &tot2);
-    const uint32_t wse = block_excl_scan(weq, sh.sw, &tot2);
-    if (t < n) { sh.cw0[t] = wsg; sh.cw1[t] = wse; }
-    __syncthreads();
-    const uint64_t* L = seg_slot(P, (uint64_t)a * kSegsPerChunk);
-    uint32_t g_run = 0, e_run = 0;   // clean gt / eq items of the window before this round
-    for (uint32_t r0 = 0; r0 < total; r0 += kSelThreads * kStreamItems) {
-      const uint32_t j0 = r0 + t * kStreamItems;
-      uint64_t v[kStreamItems];
-      if (j0 + kStreamItems <= total) {
-        const uint4* q = reinterpret_cast<const uint4*>(L + j0);
 #pragma unroll
-        for (int u = 0; u < kStreamV; ++u) {
-          const uint4 x = __ldcg(q + u);
-          v[2 * u] = ((uint64_t)x.y << 32) | x.x;
-          v[2 * u + 1] = ((uint64_t)x.w << 32) | x.z;
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < kStreamItems; ++u) v[u] = j0 + u < total ? L[j0 + u] : 0ull;
+    for (int u = 0; u < kUnroll; ++u) {
+      const bool ok = base + u * 32 + lane < cnt;
+      const uint32_t val = (uint32_t)(v[u] >> 32), idx = (uint32_t)v[u];
+      const uint32_t key = val & 0x7FFFFFFFu;
+      const bool is_eq = ok && key == T;
+      const unsigned eqm = __ballot_sync(0xFFFFFFFFu, is_eq);
+      const bool sel = ok && (key > T || (is_eq && eq_run + __popc(eqm & lt) < take));
+      const unsigned sm = __ballot_sync(0xFFFFFFFFu, sel);
+      if (sel) {
+        const uint64_t o = dst0 + out_run + __popc(sm & lt);
+        send[o] = idx;
+        send[K + o] = val;
       }
-      const int c0 = j0 < total ? win_chunk(sh, n, j0) : 0;
-      int c = c0;
-      uint32_t lg = 0, le = 0, skip = 0;
-#pragma unroll
-      for (int u = 0; u < kStreamItems; ++u) {
-        const uint32_t j = j0 + u;
-        const bool ok = j < total;
-        if (ok)
-          while (c + 1 < n && sh.cst[c + 1] <= j) ++c;
-        const bool cl = ok && sh.dm[c] == 0;
-        skip |= cl ? 0u : 1u << u;
-        const uint32_t key = (uint32_t)(v[u] >> 32) & 0x7FFFFFFFu;
-        lg += cl && key > T;
-        le += cl && key == T;
-      }
-      uint32_t rtot;
-      const uint32_t rex = block_excl_scan((le << 16) | lg, sh.sw, &rtot);
-      uint32_t gbw = g_run + (rex & 0xFFFFu), ebw = e_run + (rex >> 16);   // before this thread's items
-      c = c0;
-#pragma unroll
-      for (int u = 0; u < kStreamItems; ++u) {
-        const uint32_t j = j0 + u;
-        if (j < total)
-          while (c + 1 < n && sh.cst[c + 1] <= j) ++c;
-        const bool ok = !((skip >> u) & 1u);
-        const uint32_t val = (uint32_t)(v[u] >> 32), key = val & 0x7FFFFFFFu;
-        const bool gt = ok && key > T, eq = ok && key == T;
-        if (gt || eq) {
-          const uint32_t gb = gbw - sh.cw0[c], eb = ebw - sh.cw1[c];   // before it, inside its chunk
-          const uint32_t tk = sh.take[c] & 0x7FFFFFFFu;
-          if (gt || eb < tk) {
-            const uint32_t o = sh.dst[c] + gb + min(eb, tk);
-            send[o] = (uint32_t)v[u];
-            send[K + o] = val;
-          }
-          if (eq && (sh.take[c] >> 31) && eb == tk - 1) P.sel_cut[slot] = (uint32_t)v[u] + 1;
-        }
-        gbw += gt;
-        ebw += eq;
-      }
-      g_run += rtot & 0xFFFFu;
-      e_run += rtot >> 16;
-    }
-    __syncthreads();
-  });
-  if (any_direct) {   // chunks with a DIRECT segment: the entry of the chunk's first DIRECT segment emits it
-    const uint32_t nd = vload(P.counters + 5);
-    for (uint32_t e = gw; e < nd; e += nw) {
-      const uint32_t w = P.dlist[e];
-      const uint32_t segid = w & 0x3FFFFFFFu, lvl = w >> 30;
-      const int ch = (int)(segid / kSegsPerChunk), seg = (int)(segid % kSegsPerChunk);
-      const int slot = P.chunk_slot[ch];
-      if (lvl != P.sel[slot].refill) continue;
-      const uint32_t sc = lane < kSegsPerChunk ? P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] : 0u;
-      const unsigned dmask = __ballot_sync(0xFFFFFFFFu, (sc & kDirect) != 0u) & 0xFFFFu;
-      if (__ffs(dmask) - 1 != seg) continue;
-      const uint32_t T = P.sel[slot].prefix, need = P.sel[slot].kleft;
-      const uint32_t take_b = min(M.ceqb[ch], need);
-      const uint32_t take = min(M.ceq[ch], need - take_b);
-      const bool last_tie = take > 0 && take_b + take == need;
-      const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + M.cgtb[ch] + take_b;
-      emit_dirty_chunk(P, src, ch, P.cand + M.cpos[ch], send, K, dst0, T, take, last_tie, slot, lane);
+      if (last_tie_chunk && is_eq && eq_run + __popc(eqm & lt) == take - 1) P.sel_cut[slot] = idx + 1;
+      eq_run += __popc(eqm);
+      out_run += __popc(sm);
     }
   }
-  __syncthreads();
-  phase_mark(P, 15);
 }
 
 // residual' = 0 at the last selection of the large layers (lowdiff_residual_materialize): a
@@ -1399,27 +1081,18 @@ int num_sms() {
 
 size_t compress_hist_bytes(int n_large) { return (size_t)n_large * kHistRow * sizeof(uint32_t); }
 
-// per-segment candidate capacity: ~12 x the expected candidates of a 1024-element segment at the
-// band's ~1.5 k_l (a power of two in [32, 1024]); 1 B/param of scratch at 1% density
+// per-segment candidate capacity: ~11.5 x the expected candidates of a 1024-element segment at the
+// band's ~1.5 k_l, a multiple of 8 in [32, 1024]: with the plan, <= 1 B/param of scratch at 1%
 int compress_seg_capacity(uint32_t ppm) {
-  const double want = 12.0 * kSeg * (double)ppm / 1e6;
-  int cs = 32;
-  while (cs < 1024 && cs < want) cs <<= 1;
-  return cs;
+  const double want = 11.5 * kSeg * (double)ppm / 1e6;   // 1% density: 120 slots (0.94 B/param)
+  int cs = ((int)want + 7) & ~7;
+  return cs < 32 ? 32 : cs > kSeg ? kSeg : cs;
 }
 
-// co-resident CTAs of the select kernel (cooperative launch), at most 4 per SM
-static unsigned select_grid(bool ef) {
-  static int occ[2] = {0, 0};
-  if (!occ[ef]) {
-    int o = 0;
-    if (ef) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, select_kernel<true>, kSelThreads, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, select_kernel<false>, kSelThreads, 0);
-    occ[ef] = std::max(1, std::min(4, o));
-  }
-  return (unsigned)std::min(kMaxSelGrid, num_sms() * occ[ef]);
-}
-
+// lowdiff_compress: small layers (forked stream) | scan -> chunk prep -> plan -> level-1 refill
+// (rescan, prep, plan) -> level-2 refill (prep, plan) -> digit 1 -> digit 2 -> count+emit, join.
+// The refill kernels exit at once when nothing was queued; the CUDA-graph form captures the same
+// sequence.  Short kernels use programmatic dependent launch (pdl.cuh).
 cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send, cudaStream_t s) {
   DevPlan& P = c->plan;
   const bool ef = c->cfg.error_feedback != 0;
@@ -1435,7 +1108,7 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
       attr_set[ef] = true;
     }
     // the small layers touch disjoint elements and send entries from the large-layer path, so
-    // they run on a forked stream, concurrently with the scan, and join before the select
+    // they run on a forked stream, concurrently with the scan, and join at the end
     const bool fork = P.n_large && c->aux;
     cudaStream_t ss = fork ? c->aux : s;
     if (fork) {
@@ -1453,36 +1126,48 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
     c->lazy_residual = nullptr;
     return cudaGetLastError();
   }
-  // per-call state: digit histograms, per-layer candidate totals, counters
+  // per-call state: digit histograms, candidate totals, counters, look-back states
   if ((e = cudaMemsetAsync(P.hist, 0, compress_hist_bytes(P.n_large), s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(P.layer_total, 0, (size_t)P.n_large * 4, s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(P.counters, 0, 8 * sizeof(uint32_t), s)) != cudaSuccess) return e;
-  const unsigned scan_grid = (unsigned)P.n_chunks * kPiecesPerChunk;
+  if ((e = cudaMemsetAsync(P.chunk_state, 0, (size_t)P.n_chunks * 8, s)) != cudaSuccess) return e;
+  const int layer_blocks = (P.n_large * 32 + 255) / 256;     // warp per large layer
+  const int chunk_blocks = (P.n_chunks + 7) / 8;              // warp per chunk
+  const unsigned scan_grid = (unsigned)P.n_chunks * kPiecesPerChunk;   // full grid: no tail loop
+  const int uK = kScanWarps * 32;
+  const float* src = ef ? residual : grad;   // where acc lives after the scan (DIRECT re-reads)
   // lazy residual zeroing applies only to the residual buffer whose selection is pending
   const int lazy = (ef && c->lazy_residual == residual) ? 1 : 0;
   prof_begin(c, "scan", s, &h);
-  if (ef) scan_kernel<true><<<scan_grid, kScanWarps * 32, 0, s>>>(P, grad, residual, lazy);
-  else scan_kernel<false><<<scan_grid, kScanWarps * 32, 0, s>>>(P, grad, residual, 0);
+  if (ef) scan_kernel<true><<<scan_grid, uK, 0, s>>>(P, grad, residual, lazy);
+  else scan_kernel<false><<<scan_grid, uK, 0, s>>>(P, grad, residual, 0);
+  prof_end(c, h, s);
+  int hs;
+  prof_begin(c, "select", s, &hs);
+  const bool pdl = !c->prof;   // programmatic launches (pdl.cuh); profiling events sit between kernels
+  if ((e = launch_pdl(pdl, chunk_prep_kernel, chunk_blocks, 256, 0, s, P, src, 0)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 0)) != cudaSuccess) return e;
+  // level-1 refill: rescan the queued chunks at the safe threshold, prep them, plan again
+  const unsigned rgrid = (unsigned)num_sms() * 4;   // refill kernels: persistent over their lists
+  e = ef ? launch_pdl(pdl, rescan_kernel<true>, 4 * rgrid, uK, 0, s, P, grad, residual)
+         : launch_pdl(pdl, rescan_kernel<false>, 4 * rgrid, uK, 0, s, P, grad, residual);
+  if (e != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, chunk_prep_kernel, rgrid, 256, 0, s, P, src, 1)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 1)) != cudaSuccess) return e;
+  // level-2 refill: every element of the queued layers, read directly
+  if ((e = launch_pdl(pdl, chunk_prep_kernel, rgrid, 256, 0, s, P, src, 2)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 4)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, src, 1)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 2)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, src, 2)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 3)) != cudaSuccess) return e;
+  prof_end(c, hs, s);
+  prof_begin(c, "emit", s, &h);
+  if ((e = launch_pdl(pdl, count_emit_kernel, chunk_blocks, 256, 0, s, P, src, send, (uint64_t)c->K)) != cudaSuccess)
+    return e;
   prof_end(c, h, s);
   if (P.n_small && c->aux && (e = cudaStreamWaitEvent(s, c->ev_join, 0)) != cudaSuccess) return e;   // join
-  prof_begin(c, "select", s, &h);
-  {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(select_grid(ef));
-    cfg.blockDim = dim3(kSelThreads);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const uint64_t K = (uint64_t)c->K;
-    e = ef ? cudaLaunchKernelEx(&cfg, select_kernel<true>, P, grad, residual, send, K)
-           : cudaLaunchKernelEx(&cfg, select_kernel<false>, P, grad, residual, send, K);
-    if (e != cudaSuccess) return e;
-  }
-  prof_end(c, h, s);
-  c->launches += 2;
+  c->launches += 13;
   c->lazy_residual = ef ? residual : nullptr;   // this call's large-layer selection is now pending
   return cudaGetLastError();
 }

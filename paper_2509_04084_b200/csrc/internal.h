@@ -37,7 +37,6 @@ constexpr int kReplayTile = 1 << kReplayTileShift;   // replay tile (elements pe
 constexpr int kReplayThreads = LD_REPLAY_THREADS;
 constexpr int kReplaySlots = kReplayTile / (4 * kReplayThreads);   // float4 slots per thread
 constexpr uint32_t kNoThreshold = 0xFFFFFFFFu;
-constexpr int kMaxSelGrid = 4096;      // upper bound of the persistent select grid (CTAs)
 
 // per-large-layer selection state (device)
 struct LayerSel {
@@ -71,8 +70,10 @@ struct DevPlan {
   // scratch
   int32_t cs;                    // candidate capacity of a segment (compress_seg_capacity)
   uint64_t* cand;                // [n_chunks * 16] segment slots of cs candidates (acc bits << 32 | index);
-                                 //   the select compacts each window's lists in place
+                                 //   chunk prep compacts each chunk's stored lists in place (chunk list)
   uint32_t* seg_count;           // [n_chunks * 16] candidates of the segment (| kDirect: not stored)
+  uint32_t* chunk_count;         // [n_chunks] length of the chunk's compacted (stored) list
+  uint32_t* chunk_dm;            // [n_chunks] its DIRECT segments (bit mask)
   uint32_t* layer_total;         // [n_large] candidates admitted per large layer (this call)
   uint32_t* hist;                // [n_large * (2048 + 2048 + 512)]
   LayerSel* sel;                 // [n_large]
@@ -82,21 +83,15 @@ struct DevPlan {
   // {key(r) > sel_T} U {key(r) == sel_T and index < sel_cut}; the next scan zeroes it on the fly
   uint32_t* sel_T;               // [n_large] previous call's exact k-th key
   uint32_t* sel_cut;             // [n_large] one past the global index of the last tie it took
-  uint32_t* refill_list;         // [n_large] layers to rescan at their safe threshold (level 1)
-  uint32_t* refill_list2;        // [n_large] layers to histogram directly (level 2)
+  uint32_t* refill_list;         // [n_chunks] chunks to rescan at their layer's safe threshold (level 1)
+  uint32_t* refill_list2;        // [n_chunks] chunks whose segments all become DIRECT (level 2)
   uint32_t* trace;               // [n_large] this call's path per layer: 0 hit, 1 level-1, 2 level-2
-  uint32_t* dlist;               // [3 n_chunks 16] DIRECT segments of this call: segid | level << 30
   uint32_t* thr_safe;            // [n_large] the band without the drift lead
-  unsigned long long* chunk_state;  // [3 n_chunks] select: per chunk u32 x 6 (compacted start and count,
-                                    //   gt, eq and their in-CTA prefixes)
-  unsigned long long* tail_agg;  // [kMaxSelGrid] select: (eq << 31 | gt) of each CTA's last layer run
-  uint32_t* tail_slot;           // [kMaxSelGrid] that run's layer (0xFFFFFFFE: the CTA had no chunks)
+  unsigned long long* chunk_state;  // [n_chunks] count_emit look-back: status | eq_incl | gt_incl
   uint32_t* counters;            // [0] level-1 refills, [1] spec hits, [2] spec misses,
                                  // [3] candidates of hit layers, [4] level-2 refills,
-                                 // [5] entries in dlist (DIRECT segments: more than cs candidates,
-                                 //     or every segment of a level-2 layer)
+                                 // [5] DIRECT segments of the scan (more than cs candidates)
   uint32_t* err;                 // [0] non-finite flag, [1] first bad layer
-  unsigned long long* phase_ns;  // [16] select-kernel phase timestamps (block 0, %globaltimer)
 };
 
 // ---------------------------------------------------------------- context

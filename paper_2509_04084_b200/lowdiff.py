@@ -113,7 +113,6 @@ def lib():
             "sync": ([P], S),
             "get_stats": ([P, C.POINTER(Stats)], S),
             "compress_trace": ([P, C.c_int32, C.POINTER(C.c_int32), P, P, P, P], S),
-            "compress_phases": ([P, P], S),
             "prof_enable": ([P, C.c_int32], S),
             "prof_read": ([P, C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)], S),
             "kernel_launches": ([P], C.c_int64),
@@ -149,7 +148,7 @@ EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_mater
             "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "snapshot_shard", "bucket_plan", "union_compact", "union_persist", "recover_union",
             "replica_init",
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
-            "sync", "get_stats", "compress_trace", "compress_phases",
+            "sync", "get_stats", "compress_trace",
             "prof_enable", "prof_read", "kernel_launches", "set_graphs", "last_error", "nccl_unique_id",
             "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host", "retire_from",
             "write_full_host", "abi_version", "selftest", "wasted_time", "optimal_config", "optimal_config_feasible", "config_step",
@@ -502,13 +501,6 @@ class Context:
         self._c("compress_trace", lib().lowdiff_compress_trace(self._h, n.value, C.byref(n), *[a.ctypes.data_as(C.c_void_p)
                                                                                              for a in (L, lev, cand, thr)]))
         return L, lev, cand, thr
-
-    def compress_phases(self):
-        """Select-kernel phase timestamps (ns) of the last compress (diagnostic)."""
-        import numpy as np
-        a = np.zeros(16, np.int64)
-        self._c("compress_phases", lib().lowdiff_compress_phases(self._h, a.ctypes.data_as(C.c_void_p)))
-        return a
 
     def set_graphs(self, on=True):
         """Replay compress / merge as captured CUDA graphs (fewer launch gaps for small models)."""
