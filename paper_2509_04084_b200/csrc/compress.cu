@@ -678,15 +678,14 @@ __global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
         atomicAdd(&P.counters[3], tot);
       }
     } else {
-      // missed.  Level 1 rescans at the safe threshold (this distribution's band, without the
-      // drift share) when that is lower than the one that missed, else at the missed threshold
-      // lowered by a quarter binade (x0.75-0.875 in value); level 2 (every element) only when
-      // neither exists.  Without the second option a miss with no drift lead went straight to
-      // level 2, which for a large layer cost ~1 ms.
+      // missed.  Level 1 rescans at the lower of the safe threshold (this distribution's band,
+      // without the drift share) and the missed threshold lowered by a quarter binade (x0.75-0.875
+      // in value); level 2 (every element) only when neither exists.  Rescanning at the safe
+      // threshold alone escalated most misses to level 2 (~4 passes over the layer's acc): the
+      // safe band sits only a few percent below the missed one.
       const uint32_t th = P.thr[slot], ts = P.thr_safe[slot];
-      uint32_t l1 = 0xFFFFFFFFu;
-      if (ts < th) l1 = ts;
-      else if (th != 0xFFFFFFFFu && th > kL1Drop) l1 = min(th, 0x7F800000u) - kL1Drop;
+      uint32_t l1 = ts < th ? ts : 0xFFFFFFFFu;
+      if (th != 0xFFFFFFFFu && th > kL1Drop) l1 = min(l1, min(th, 0x7F800000u) - kL1Drop);
       const int level = l1 != 0xFFFFFFFFu ? 1 : 2;
       if (lane == 0) P.thr_used[slot] = level == 1 ? min(l1, 0x7F800000u) : 0u;   // read by the refill
       queue_refill(P, slot, level, c0, c1, lane);
