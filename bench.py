@@ -387,6 +387,26 @@ def run_ours(args):
                   "frac_of_hbm": fused_b / (ums / 1e3) / B_HBM,
                   "unfused_model_bytes": unfused_b, "unfused_floor_ms": unfused_b / B_HBM * 1e3,
                   "note": "allgather + update_kernel (tile merge in smem + streaming Adam); p, m, v fp32 in HBM"}
+        if args.exchange == "peer":
+            # NEXT-1 fully fused: the peers' entries read over peer memory straight into the tile merge
+            # + Adam (lowdiff_exchange_peer_update): local HBM 24 B/param + this rank's own entries;
+            # the other ranks' entries of each tile arrive over NVLink ((N - 1) 8 K bytes per step)
+            for t in range(2):
+                ctx.exchange_peer_update(0, scal[t], p, m, v)
+            torch.cuda.synchronize()
+            barrier(world)
+            u0.record()
+            for t in range(n_u):
+                ctx.exchange_peer_update(0, scal[t + 2], p, m, v)
+            u1.record()
+            torch.cuda.synchronize()
+            pms = allmax(u0.elapsed_time(u1), world) / n_u
+            local_b = 24 * psi + 8 * K
+            update["peer_fused"] = {"ms_per_step": pms, "local_hbm_bytes": local_b,
+                                    "nvlink_bytes_in": 8 * K * (world - 1),
+                                    "local_gbs": local_b / (pms / 1e3) / 1e9,
+                                    "frac_of_hbm": local_b / (pms / 1e3) / B_HBM,
+                                    "note": "lowdiff_exchange_peer_update: no gathered buffer, no dense G"}
         del p, m, v
 
     # BJ:5 gate: T_floor / t_chain; PCIe D2H bandwidth measured here

@@ -168,6 +168,15 @@ lowdiff_status lowdiff_peer_alloc(lowdiff_ctx *ctx, int32_t n_slots, uint32_t **
 lowdiff_status lowdiff_ipc_open(lowdiff_ctx *ctx, const void *handle64, void **ptr);
 lowdiff_status lowdiff_peer_set(lowdiff_ctx *ctx, const void *const *ptrs);
 lowdiff_status lowdiff_exchange_peer(lowdiff_ctx *ctx, int32_t slot, float *dense_out, void *stream);
+/* Both halves of NEXT-1 fused (Alg. 1 lines 5-8): like lowdiff_exchange_peer, the
+ *    merge reads every rank's entries of its tile from their slots (peer memory), but instead of
+ *    writing G it applies the optimizer of cfg->optim (R-11 Adam / R-12 SGD, the scalars of this
+ *    step) to the tile's p, m, v in the same pass -- bitwise what lowdiff_exchange followed by the
+ *    oracle's step gives, with neither a gathered buffer nor a dense G in HBM.  p, m, v: device
+ *    f32[Psi] (m, v unused for SGD), 16-byte aligned.  Same ordering protocol as
+ *    lowdiff_exchange_peer (call it instead of exchange_peer for the slot).  Asynchronous. */
+lowdiff_status lowdiff_exchange_peer_update(lowdiff_ctx *ctx, int32_t slot, const lowdiff_step_scalars *scalars,
+                                            float *p, float *m, float *v, void *stream);
 
 /* Exchange + optimizer step without a dense gradient (Alg. 1 lines 5, 7, 8,
  *    PAPER.md:231-237): the allgather of lowdiff_exchange, then p, m, v <- Opt(G, scalars) with

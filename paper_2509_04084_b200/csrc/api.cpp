@@ -880,6 +880,43 @@ lowdiff_status lowdiff_exchange_peer(lowdiff_ctx* c, int32_t slot, float* dense_
   return LOWDIFF_OK;
 }
 
+// SURVEY NEXT-1, both halves fused: the allgather folded into the merge over peer memory AND the
+// merge folded into the optimizer step -- the peers' entries of each tile are read over NVLink,
+// merged in shared memory and applied to p, m, v in one pass (no gathered buffer, no dense G).
+lowdiff_status lowdiff_exchange_peer_update(lowdiff_ctx* c, int32_t slot, const lowdiff_step_scalars* scalars,
+                                            float* p, float* m, float* v, void* stream) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (!c->peer_set) return fail(c, LOWDIFF_E_STATE, "exchange_peer_update: call lowdiff_peer_set first");
+  const bool adam = c->cfg.optim == LOWDIFF_ADAM;
+  if (slot < 0 || slot >= c->peer_slots || !scalars || !p || !aligned16(p) || (adam && (!m || !v)) ||
+      (m && !aligned16(m)) || (v && !aligned16(v)))
+    return fail(c, LOWDIFF_E_INVALID, "exchange_peer_update: bad argument (p, m, v 16-byte aligned device arrays)");
+  if (!c->peer_epoch[slot]) return fail(c, LOWDIFF_E_STATE, "exchange_peer_update: nothing was compressed into the slot");
+  const int n = c->peer_slots;
+  ld::PeerTable T{};
+  T.world = c->cfg.world;
+  T.self = c->cfg.rank;
+  T.slot = slot;
+  T.n_slots = n;
+  T.epoch = c->peer_epoch[slot];
+  for (int q = 0; q < T.world; ++q) {
+    T.send[q] = static_cast<const uint32_t*>(c->peer_ptrs[q * (n + 1) + slot]);
+    T.start[q] = T.send[q] + 2 * c->K;
+    T.flags[q] = const_cast<unsigned long long*>(static_cast<const unsigned long long*>(c->peer_ptrs[q * (n + 1) + n]));
+  }
+  const ld::PeerOpt o{c->cfg.adam.beta1, c->cfg.adam.one_minus_beta1, c->cfg.adam.beta2, c->cfg.adam.one_minus_beta2,
+                      c->cfg.adam.eps, scalars->lr, scalars->bc1_inv, scalars->bc2_inv};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int h;
+  ld::prof_begin(c, "peer_update", s, &h);
+  cudaError_t e = ld::launch_peer_update(T, (uint64_t)c->K, c->psi, c->cfg.mean != 0, adam, o, p, m, v, s);
+  ld::prof_end(c, h, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "peer_update");
+  c->launches += 2;
+  return LOWDIFF_OK;
+}
+
 lowdiff_status lowdiff_residual_materialize(lowdiff_ctx* c, float* residual, void* stream) {
   lowdiff_status st = entry(c);
   if (st) return st;

@@ -135,6 +135,10 @@ cudaError_t launch_peer_ready(unsigned long long* own_flags, int slot, unsigned 
 cudaError_t launch_peer_wait_done(unsigned long long* own_flags, int n_slots, int slot, int world,
                                   unsigned long long epoch, cudaStream_t s);
 cudaError_t launch_peer_merge(const PeerTable& T, uint64_t K, int64_t psi, bool mean, float* dense, cudaStream_t s);
+// the optimizer constants and one step's scalars of lowdiff_exchange_peer_update
+struct PeerOpt { float b1, c1, b2, c2, eps, lr, r1, r2; };
+cudaError_t launch_peer_update(const PeerTable& T, uint64_t K, int64_t psi, bool mean, bool adam, const PeerOpt& o,
+                               float* p, float* m, float* v, cudaStream_t s);
 // merge_replay.cu: the merge's tile-start table of one block (n_tiles + 1 entries)
 cudaError_t launch_tile_start(const uint32_t* block, uint64_t K, int64_t psi, uint32_t* start, cudaStream_t s);
 

@@ -374,17 +374,7 @@ update_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, cons
   const float n = (float)world, inv = 1.0f / (float)world;
   const bool eps_ok = ak.eps >= 0x1p-60f && ak.eps <= 0x1p59f;
   auto step1 = [&](float g, float& P, float& M, float& V) {
-    if (OPT == LOWDIFF_ADAM) {
-      M = __fadd_rn(__fmul_rn(ak.b1, M), __fmul_rn(ak.c1, g));
-      V = __fadd_rn(__fmul_rn(ak.b2, V), __fmul_rn(ak.c2, __fmul_rn(g, g)));
-      const float mh = __fmul_rn(M, r1), vh = __fmul_rn(V, r2);
-      bool sl;
-      float u = adam_u_fast(mh, vh, ak.eps, &sl);
-      if (sl || !eps_ok) u = __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), ak.eps));
-      P = __fsub_rn(P, __fmul_rn(lr, u));
-    } else {
-      P = __fsub_rn(P, __fmul_rn(lr, g));
-    }
+    opt_step1<OPT == LOWDIFF_ADAM>(g, P, M, V, ak.b1, ak.c1, ak.b2, ak.c2, ak.eps, eps_ok, lr, r1, r2);
   };
   if (len == kMergeTile) {
     float4* p4 = reinterpret_cast<float4*>(p + j0);

@@ -17,6 +17,7 @@
 // continues, so a protocol misuse surfaces as LOWDIFF_E_STATE at lowdiff_sync instead of a hang.
 #include <cuda_runtime.h>
 
+#include "ieee_fast.cuh"
 #include "internal.h"
 
 namespace ld {
@@ -106,6 +107,67 @@ peer_merge_kernel(PeerTable T, uint64_t K, int64_t n_tiles, uint64_t psi, float*
   }
 }
 
+// The live optimizer step straight from the peers' blocks (lowdiff_exchange_peer_update, SURVEY
+// NEXT-1 second half): the tile's G is merged in shared memory from every rank's entries read over
+// NVLink (as peer_merge_kernel), then one streaming pass applies the R-11 Adam / R-12 SGD to the
+// tile's p, m, v (opt_step1: the replay's and update_kernel's operations) -- neither a gathered
+// buffer nor the dense G ever exists in HBM.  Local HBM: 24 B/param (Adam; 8 SGD); remote reads:
+// 8 B per peer entry falling in the tile.
+template <bool ADAM, int DIV>
+__global__ void __launch_bounds__(256)
+peer_update_kernel(PeerTable T, uint64_t K, int64_t n_tiles, uint64_t psi, PeerOpt o, float* __restrict__ p,
+                   float* __restrict__ m, float* __restrict__ v) {
+  __shared__ float acc[kMergeTile];
+  const int64_t t = blockIdx.x;
+  const uint64_t j0 = (uint64_t)t * kMergeTile;
+  const int len = (int)min((uint64_t)kMergeTile, psi - j0);
+  if (threadIdx.x < T.world)
+    wait_geq(T.flags[threadIdx.x] + T.slot, T.epoch, T.flags[T.self] + peer_err_word(T.n_slots));
+  float4* acc4 = reinterpret_cast<float4*>(acc);
+  for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) acc4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  for (int r = 0; r < T.world; ++r) {   // rank order from +0 (R-8): no conflicts within a rank
+    const uint32_t* idx = T.send[r];
+    const uint32_t* val = idx + K;
+    const uint32_t a = T.start[r][t], b = T.start[r][t + 1];
+    for (uint32_t e = a + threadIdx.x; e < b; e += blockDim.x) {
+      const uint32_t j = idx[e] - (uint32_t)j0;
+      acc[j] = __fadd_rn(acc[j], __uint_as_float(val[e]));
+    }
+    __syncthreads();
+  }
+  const float n = (float)T.world, inv = 1.0f / (float)T.world;
+  const bool eps_ok = o.eps >= 0x1p-60f && o.eps <= 0x1p59f;
+  auto step1 = [&](float g, float& P, float& M, float& V) {
+    opt_step1<ADAM>(mean_of<DIV>(g, n, inv), P, M, V, o.b1, o.c1, o.b2, o.c2, o.eps, eps_ok, o.lr, o.r1, o.r2);
+  };
+  if (len == kMergeTile) {
+    float4* p4 = reinterpret_cast<float4*>(p + j0);
+    float4* m4 = reinterpret_cast<float4*>(m + j0);
+    float4* v4 = reinterpret_cast<float4*>(v + j0);
+#pragma unroll 2
+    for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) {
+      float4 P = __ldcs(p4 + q), M = make_float4(0.f, 0.f, 0.f, 0.f), V = M;
+      if (ADAM) { M = __ldcs(m4 + q); V = __ldcs(v4 + q); }
+      const float4 gv = acc4[q];
+      step1(gv.x, P.x, M.x, V.x);
+      step1(gv.y, P.y, M.y, V.y);
+      step1(gv.z, P.z, M.z, V.z);
+      step1(gv.w, P.w, M.w, V.w);
+      __stcs(p4 + q, P);
+      if (ADAM) { __stcs(m4 + q, M); __stcs(v4 + q, V); }
+    }
+  } else {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      float P = p[j0 + i], M = 0.f, V = 0.f;
+      if (ADAM) { M = m[j0 + i]; V = v[j0 + i]; }
+      step1(acc[i], P, M, V);
+      p[j0 + i] = P;
+      if (ADAM) { m[j0 + i] = M; v[j0 + i] = V; }
+    }
+  }
+}
+
 // consumer side: tell every owner that this rank finished reading `slot` at `epoch`
 __global__ void peer_done_kernel(PeerTable T) {
   const int q = threadIdx.x;
@@ -113,6 +175,24 @@ __global__ void peer_done_kernel(PeerTable T) {
 }
 
 }  // namespace
+
+cudaError_t launch_peer_update(const PeerTable& T, uint64_t K, int64_t psi, bool mean, bool adam, const PeerOpt& o,
+                               float* p, float* m, float* v, cudaStream_t s) {
+  const int64_t n_tiles = (psi + kMergeTile - 1) / kMergeTile;
+  const unsigned grid = (unsigned)n_tiles;
+  const int dm = (!mean || T.world == 1) ? 0 : ((T.world & (T.world - 1)) == 0 ? 1 : 2);
+#define LD_PU(A, D) peer_update_kernel<A, D><<<grid, 256, 0, s>>>(T, K, n_tiles, (uint64_t)psi, o, p, m, v)
+  if (adam) {
+    if (dm == 0) LD_PU(true, 0); else if (dm == 1) LD_PU(true, 1); else LD_PU(true, 2);
+  } else {
+    if (dm == 0) LD_PU(false, 0); else if (dm == 1) LD_PU(false, 1); else LD_PU(false, 2);
+  }
+#undef LD_PU
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  peer_done_kernel<<<1, 32, 0, s>>>(T);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_peer_ready(unsigned long long* own_flags, int slot, unsigned long long epoch, cudaStream_t s) {
   peer_ready_kernel<<<1, 1, 0, s>>>(own_flags, slot, epoch);

@@ -88,6 +88,7 @@ def lib():
             "ipc_open": ([P, P, C.POINTER(C.c_void_p)], S),
             "peer_set": ([P, C.POINTER(C.c_void_p)], S),
             "exchange_peer": ([P, C.c_int32, P, P], S),
+            "exchange_peer_update": ([P, C.c_int32, C.POINTER(StepScalars), P, P, P, P], S),
             "batch_persist": ([P, C.c_int64, C.POINTER(StepScalars), P, P], S),
             "full_ckpt": ([P, C.c_int64, P, P, P, P], S),
             "wait_persist": ([P, P], S),
@@ -144,7 +145,7 @@ def lib():
 
 
 EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_materialize", "exchange", "merge", "exchange_update", "peer_alloc", "ipc_open",
-            "peer_set", "exchange_peer", "batch_persist",
+            "peer_set", "exchange_peer", "exchange_peer_update", "batch_persist",
             "full_ckpt", "wait_persist", "recover", "replay", "replay_range", "recover_sharded", "snapshot_layer", "snapshot_wait", "snapshot_shard", "bucket_plan", "union_compact", "union_persist", "recover_union",
             "replica_init",
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
@@ -381,6 +382,10 @@ class Context:
 
     def exchange_peer(self, slot, dense_out, stream=None):
         self._c("exchange_peer", lib().lowdiff_exchange_peer(self._h, slot, _ptr(dense_out), _stream(stream)))
+
+    def exchange_peer_update(self, slot, scalars: StepScalars, p, m=None, v=None, stream=None):
+        self._c("exchange_peer_update", lib().lowdiff_exchange_peer_update(self._h, slot, C.byref(scalars), _ptr(p),
+                                                                           _ptr(m), _ptr(v), _stream(stream)))
 
     def batch_persist(self, iteration, scalars: StepScalars, send, stream=None):
         self._c("batch_persist", lib().lowdiff_batch_persist(self._h, iteration, C.byref(scalars), _ptr(send),

@@ -12,6 +12,8 @@ from inputs import gradient, table
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
+# multi-rank peer tests: several tiles, chunks and small layers, but an oracle compress in ~0.1 s
+PEER_SIZES = [300000, 5000, 1048576, 70001, 4096, 600000, 7]
 
 
 def _np(t):
@@ -52,12 +54,13 @@ def test_exchange_update_equals_dense_path(ref, optim, model):
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
-def test_peer_exchange_equals_gathered_merge(world):
+def test_peer_exchange_equals_gathered_merge(ref, world):
     """Peer-memory exchange (NEXT-1) with `world` ranks simulated on one device (each rank a
     context; peers' slots passed as plain device pointers instead of IPC mappings): over several
     iterations with alternating slots (the write-after-read wait path included), every rank's
-    merged G equals lowdiff_merge of the concatenated blocks bit for bit."""
-    sizes = table("resnet50")
+    merged G equals the oracle's exchange (R-8) of the oracle's own compressed blocks bit for bit
+    (and lowdiff_merge of the concatenated slots)."""
+    sizes = PEER_SIZES
     psi = sum(sizes)
     ctxs = [ld.Context(sizes, density_ppm=10000, world=world, rank=q) for q in range(world)]
     K = ctxs[0].K
@@ -77,18 +80,80 @@ def test_peer_exchange_equals_gathered_merge(world):
     res = [torch.zeros(psi, device=DEV) for _ in range(world)]
     dense = [torch.empty(psi, device=DEV) for _ in range(world)]
     want = torch.empty(psi, device=DEV)
+    R = [np.zeros(psi, np.float32) for _ in range(world)]
     for t in range(5):
         sl = t % 2
+        blocks = []
         for q, c in enumerate(ctxs):
-            g = gradient(sizes, q, t, dist="D5", alpha=0.5, model="resnet50", device=DEV)
+            g = gradient(sizes, q, t, dist="D5", alpha=0.5, device=DEV)
             c.compress(g, res[q], slots[q][sl])
+            b, R[q] = ref.compress(sizes, 10000, _np(g), R[q], ef=True)
+            blocks.append(b)
         for q, c in enumerate(ctxs):
             c.exchange_peer(sl, dense[q])
         gathered = torch.cat([slots[q][sl] for q in range(world)])
         ctxs[0].merge(world, gathered, want)
         torch.cuda.synchronize()
+        G = ref.exchange(np.concatenate(blocks), world, K, psi)
         for q in range(world):
+            assert np.array_equal(_np(dense[q]).view(np.uint32), G.view(np.uint32)), (t, q)
             assert torch.equal(dense[q].view(torch.int32), want.view(torch.int32)), (t, q)
+    for c in ctxs:
+        c.sync()
+    for c in ctxs:
+        c.close()
+
+
+@pytest.mark.parametrize("world,optim", [(1, ld.ADAM), (2, ld.ADAM), (3, ld.SGD), (4, ld.ADAM), (8, ld.ADAM),
+                                         (8, ld.SGD)])
+def test_peer_update_equals_oracle(ref, world, optim):
+    """NEXT-1 fully fused (lowdiff_exchange_peer_update): every simulated rank reads all ranks'
+    entries of each tile from their slots, merges them in shared memory and applies the step to its
+    own p, m, v -- no gathered buffer, no dense G.  Every rank's p, m, v equal, bit for bit, the
+    oracle's exchange (R-8) of its own compressed blocks followed by its Adam (R-11) / SGD (R-12)
+    step, over several iterations with alternating slots and stored per-step scalars."""
+    sizes = PEER_SIZES
+    psi = sum(sizes)
+    ctxs = [ld.Context(sizes, density_ppm=10000, world=world, rank=q, optim=optim) for q in range(world)]
+    K = ctxs[0].K
+    slots = []
+    for c in ctxs:
+        sl, _ = c.peer_alloc(2, handles=False)
+        slots.append(sl)
+    tbl = [c.peer_ptrs + [c.peer_flags_ptr] for c in ctxs]
+    for c in ctxs:
+        c.peer_set(tbl)
+    gen = torch.Generator(device=DEV).manual_seed(9)
+    p0 = torch.randn(psi, generator=gen, device=DEV) * 0.05
+    ps = [p0.clone() for _ in range(world)]
+    ms = [torch.zeros(psi, device=DEV) for _ in range(world)]
+    vs = [torch.zeros(psi, device=DEV) for _ in range(world)]
+    P, M, V = _np(p0).copy(), np.zeros(psi, np.float32), np.zeros(psi, np.float32)
+    res = [torch.zeros(psi, device=DEV) for _ in range(world)]
+    R = [np.zeros(psi, np.float32) for _ in range(world)]
+    for t in range(1, 6):
+        sl = t % 2
+        blocks = []
+        for q, c in enumerate(ctxs):
+            g = gradient(sizes, q, t, dist="D5", alpha=0.5, device=DEV)
+            c.compress(g, res[q], slots[q][sl])
+            b, R[q] = ref.compress(sizes, 10000, _np(g), R[q], ef=True)
+            blocks.append(b)
+        sc = ld.derive_step_scalars(t, 1e-3 if optim == ld.ADAM else 0.1)
+        for q, c in enumerate(ctxs):
+            c.exchange_peer_update(sl, sc, ps[q], ms[q], vs[q])
+        torch.cuda.synchronize()
+        G = ref.exchange(np.concatenate(blocks), world, K, psi)
+        scal = np.array([sc.lr, sc.bc1_inv, sc.bc2_inv], np.float32)
+        if optim == ld.ADAM:
+            ref.adam_step(G, ref.adam_consts(), scal, P, M, V)
+        else:
+            ref.sgd_step(G, scal[0], P)
+        for q in range(world):
+            assert np.array_equal(_np(ps[q]).view(np.uint32), P.view(np.uint32)), (t, q)
+            if optim == ld.ADAM:
+                assert np.array_equal(_np(ms[q]).view(np.uint32), M.view(np.uint32)), (t, q)
+                assert np.array_equal(_np(vs[q]).view(np.uint32), V.view(np.uint32)), (t, q)
     for c in ctxs:
         c.sync()
     for c in ctxs:

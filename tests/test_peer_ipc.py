@@ -3,7 +3,9 @@ works between processes that share a device; the time-sliced contexts make the c
 waits real).  Each process maps the other's send slots and flag words through the IPC handles
 exchanged over torch.distributed (gloo), runs compress -> exchange_peer for several iterations
 with alternating slots, and returns its merged G and its send blocks; the parent checks that both
-ranks' G equal lowdiff_merge of the two blocks bit for bit."""
+ranks' G equal the oracle's exchange (R-8) of the oracle's own compressed blocks bit for bit, and
+that both ranks' p, m, v after the fused peer update (lowdiff_exchange_peer_update) equal the
+oracle's Adam step on that G."""
 import multiprocessing as mp
 import socket
 
@@ -28,13 +30,18 @@ def _worker(rank, world, port, q):
         slots = ctx.peer_setup(2)
         r = torch.zeros(psi, device="cuda")
         dense = torch.empty(psi, device="cuda")
+        p = torch.full((psi,), 0.5, device="cuda")
+        m = torch.zeros(psi, device="cuda")
+        v = torch.zeros(psi, device="cuda")
         out = []
         for t in range(T):
             g = gradient(sizes, rank, t, dist="D5", alpha=0.5, model="resnet50", device="cuda")
             ctx.compress(g, r, slots[t % 2])
             ctx.exchange_peer(t % 2, dense)
+            ctx.exchange_peer_update(t % 2, ld.derive_step_scalars(t + 1, 1e-3), p, m, v)
             torch.cuda.synchronize()
-            out.append((slots[t % 2].cpu().numpy().copy(), dense.cpu().numpy().copy()))
+            out.append((slots[t % 2].cpu().numpy().copy(), dense.cpu().numpy().copy(), p.cpu().numpy().copy(),
+                        v.cpu().numpy().copy()))
             dist.barrier()     # the peer's slot is re-used two iterations later; keep the copies consistent
         ctx.sync()
         dist.barrier()
@@ -45,7 +52,7 @@ def _worker(rank, world, port, q):
         q.put((rank, repr(e)))
 
 
-def test_two_process_ipc_peer_exchange():
+def test_two_process_ipc_peer_exchange(ref):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -65,12 +72,20 @@ def test_two_process_ipc_peer_exchange():
     for rank in (0, 1):
         assert not isinstance(res[rank], str), res[rank]
     sizes = table("resnet50")
-    ctx = ld.Context(sizes, density_ppm=10000, world=2, rank=0)
-    want = torch.empty(sum(sizes), device="cuda")
+    psi = sum(sizes)
+    K = sum(ref.k_table(sizes, 10000))
+    R = [np.zeros(psi, np.float32) for _ in range(2)]
+    P, M, V = np.full(psi, 0.5, np.float32), np.zeros(psi, np.float32), np.zeros(psi, np.float32)
     for t in range(T):
-        gathered = torch.from_numpy(np.concatenate([res[0][t][0], res[1][t][0]])).cuda()
-        ctx.merge(2, gathered, want)
-        w = want.cpu().numpy()
+        blocks = []
         for rank in (0, 1):
-            assert np.array_equal(res[rank][t][1].view(np.uint32), w.view(np.uint32)), (t, rank)
-    ctx.close()
+            g = gradient(sizes, rank, t, dist="D5", alpha=0.5, model="resnet50", device="cuda").cpu().numpy()
+            b, R[rank] = ref.compress(sizes, 10000, g, R[rank], ef=True)
+            blocks.append(b)
+            assert np.array_equal(res[rank][t][0].view(np.uint32), b), (t, rank)   # the slot = the oracle block
+        G = ref.exchange(np.concatenate(blocks), 2, K, psi)
+        ref.adam_step(G, ref.adam_consts(), ref.step_scalars(t + 1, 1e-3), P, M, V)
+        for rank in (0, 1):
+            assert np.array_equal(res[rank][t][1].view(np.uint32), G.view(np.uint32)), (t, rank)
+            assert np.array_equal(res[rank][t][2].view(np.uint32), P.view(np.uint32)), (t, rank)
+            assert np.array_equal(res[rank][t][3].view(np.uint32), V.view(np.uint32)), (t, rank)
