@@ -196,6 +196,33 @@ def _oracle_chain(ref, sizes, ppm):
     return time.perf_counter() - t0, K
 
 
+def _oracle_part(args_):
+    sizes, ppm = args_
+    import oracle as ref
+    return _oracle_chain(ref, sizes, ppm)[0]
+
+
+def oracle_all_cores(sample, ppm, cores=None):
+    """The same oracle work on every host core: the sample's layers in `cores` size-balanced parts
+    (compression is per layer, the merge per element), one process per part (the oracle is kept
+    single-threaded as written).  Returns (wall seconds, cores used)."""
+    import multiprocessing as mp
+    cores = max(1, min(cores or os.cpu_count() or 1, len(sample)))
+    parts = [[] for _ in range(cores)]
+    load = [0] * cores
+    for n in sorted(sample, reverse=True):   # greedy: largest layer to the least loaded part
+        i = load.index(min(load))
+        parts[i].append(n)
+        load[i] += n
+    parts = [p_ for p_ in parts if p_]
+    with mp.get_context("fork").Pool(len(parts)) as pool:
+        pool.map(_oracle_part, [([64], ppm)] * len(parts))       # workers up, oracle loaded
+        t0 = time.perf_counter()
+        pool.map(_oracle_part, [(p_, ppm) for p_ in parts])
+        t = time.perf_counter() - t0
+    return t, len(parts)
+
+
 def run_reference(args):
     """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -210,15 +237,23 @@ def run_reference(args):
     for _ in range(args.warmup):
         _oracle_chain(ref, sample, args.ppm)
     times = [_oracle_chain(ref, sample, args.ppm)[0] for _ in range(args.steps)]
-    t = sum(times) / len(times)
+    t1 = sum(times) / len(times)
+    # the host's cores: the same sample split over one oracle process per core
+    times_all = [oracle_all_cores(sample, args.ppm) for _ in range(args.steps)]
+    t = sum(x for x, _ in times_all) / len(times_all)
+    cores = times_all[0][1]
+    if t1 <= t:   # a sample too small to pay for the processes: the single thread is the baseline
+        t, cores = t1, 1
     value = 4 * psi_s / t / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, sizes, sum(ref.k_table(sizes, args.ppm)), args.gpus),
-            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "host": host_info(),
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "oracle", "host": host_info(),
+                             "one_thread": {"value": 4 * psi_s / t1 / 1e9, "ms_per_step": t1 * 1e3},
                              "sample": f"{args.workload} layers [{a},{b}) = {psi_s} params per step "
-                                       "(compress + exchange + batch serialize, 1 rank)"},
+                                       f"(compress + exchange + batch serialize, 1 rank), split over {cores} "
+                                       "single-threaded oracle processes by layer"},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -425,14 +460,18 @@ def run_ours(args):
         best = min(best, ca.elapsed_time(cb) / 1e3)
     b_pcie = 8 * K / best
     t_c = (12 * psi + 8 * K) / B_HBM
-    t_ag = (world - 1) * 8 * K / 770e9
+    nvl = float(peaks.get("nvlink_gbs", 770.0))   # MEASURED_PEAKS.json has none: B200_PROFILING.md's measured
+    t_ag = (world - 1) * 8 * K / (nvl * 1e9)       # peer copy, 770 GB/s per direction (unmeasurable on 1 GPU)
     t_m = (4 * psi + 8 * world * K) / B_HBM
     t_d2h = (8 * K + 32) / b_pcie
     t_floor = t_c + max(t_ag + t_m, t_d2h)
     t_pipe = max(t_c + t_ag + t_m, t_d2h)   # floor when the D2H of t overlaps the compress of t+1
     gate = {"t_floor_ms": t_floor * 1e3, "t_chain_ms": ms_step, "frac": t_floor / (ms_step / 1e3),
             "t_floor_pipelined_ms": t_pipe * 1e3, "frac_pipelined": t_pipe / (ms_step / 1e3),
-            "pcie_d2h_gbs_measured": b_pcie / 1e9, "nvlink_gbs": 770.0,
+            "pcie_d2h_gbs_measured": b_pcie / 1e9, "nvlink_gbs": nvl,
+            "nvlink_source": ("MEASURED_PEAKS.json" if "nvlink_gbs" in peaks else
+                              "B200_PROFILING.md measured peer copy (770 GB/s per direction); not measurable on the "
+                              "1-GPU boxes of this round"),
             "note": "send blocks double-buffered: D2H(t) overlaps compress(t+1)"}
 
     # e2e: the same chain through the C ABI with the gradient in pinned HOST memory
@@ -550,6 +589,38 @@ def run_ours(args):
                            "frac_of_hbm_unfused_model": unf_sgd / (sms_ / 1e3) / B_HBM,
                            "fused_algorithmic_gbs_per_rank": (8 * S + n_rep * 8 * world * K) / (sms_ / 1e3) / 1e9}
         del diffs, p, m, v
+        # C4's per-rank recovery work at N = 8 on this one GPU: every
+        # step carries 8 ranks' blocks and this rank replays only its 1/8 of Psi (lowdiff_replay_range)
+        if world == 1 and not args.no_c4_shape:
+            W8 = 8
+            torch.cuda.empty_cache()
+            free, _ = torch.cuda.mem_get_info()
+            n8 = int(max(1, min(args.replay_steps, (free - 4 * 2**30) * 0.85 // (W8 * 8 * K))))
+            blk8 = torch.empty((W8, 2 * K), dtype=torch.int32, device=dev)
+            for q in range(W8):   # 8 distinct blocks (the residual keeps evolving)
+                ctx.compress(grads[q % N_GRADS], r, blk8[q])
+            d8 = blk8.reshape(1, -1).expand(n8, -1).contiguous()   # the same 8 blocks at every step
+            del blk8
+            lo8, hi8 = 0, psi // W8
+            S8 = hi8 - lo8
+            p8 = torch.randn(S8, device=dev) * 0.02
+            m8, v8 = torch.zeros(S8, device=dev), torch.zeros(S8, device=dev)
+            sc8 = [ld.derive_step_scalars(t, 1e-3) for t in range(1, n8 + 1)]
+            ctx.replay_range(ld.ADAM, W8, n8, d8, sc8, lo8, hi8, p8, m8, v8)   # warm-up
+            torch.cuda.synchronize()
+            g0.record()
+            ctx.replay_range(ld.ADAM, W8, n8, d8, sc8, lo8, hi8, p8, m8, v8)
+            g1.record()
+            torch.cuda.synchronize()
+            ms8 = g0.elapsed_time(g1)
+            unf8 = n8 * (24 * S8 + 8 * W8 * K)
+            recovery["c4_shape_rank_of_8"] = {
+                "steps": n8, "ranks_per_step": W8, "range": [lo8, hi8], "ms": ms8,
+                "param_steps_per_s_per_rank": n8 * S8 / (ms8 / 1e3),
+                "param_steps_per_s_8_ranks": W8 * n8 * S8 / (ms8 / 1e3),
+                "effective_unfused_gbs": unf8 / (ms8 / 1e3) / 1e9, "frac_of_hbm_unfused_model": unf8 / (ms8 / 1e3) / B_HBM,
+                "note": "one rank's share of an 8-GPU recovery (8 ranks' blocks per step, 1/8 of Psi), timed on one GPU"}
+            del d8, p8, m8, v8
 
     # recovery end to end from files (opt-in, --recovery-files n): Full@0 + n differentials written
     # by the library, then lowdiff_recover (chain scan, CRC checks, H2D, fused replay) timed by wall
@@ -760,11 +831,16 @@ def run_ours(args):
                                        "note": "lowdiff_snapshot_shard: rank 0 of 8 copies its 1/8 of each bucket"}}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:   # (N > 1: rank 0 alone, on the same bounded sample)
         t_o, sample, (a, b) = oracle_sample(sizes, args.ppm, args.cpu_budget)
-        cpu = {"value": 4 * sum(sample) / t_o / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle", "host": host_info(),
+        t_all, cores = oracle_all_cores(sample, args.ppm)
+        if t_o <= t_all:
+            t_all, cores = t_o, 1
+        cpu = {"value": 4 * sum(sample) / t_all / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
+               "host": host_info(), "one_thread": {"value": 4 * sum(sample) / t_o / 1e9, "seconds": t_o},
                "sample": f"{args.workload} layers [{a},{b}) = {sum(sample)} params, one iteration of compress "
-                         f"+ exchange + batch serialize on 1 thread ({t_o:.1f} s)"}
+                         f"+ exchange + batch serialize: {t_o:.1f} s on 1 thread, {t_all:.1f} s split by layer "
+                         f"over {cores} single-threaded oracle processes (value)"}
 
     ctx.close()
     subprocess.run(["rm", "-rf", tmp])
@@ -814,7 +890,7 @@ def spawn_ranks(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="gpt2_xl", choices=["gpt2_xl", "bert_large", "resnet50", "mlp"])
@@ -823,6 +899,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-recovery", action="store_true")
+    ap.add_argument("--no-c4-shape", action="store_true", help="skip the 8-ranks-per-step replay leg")
     ap.add_argument("--no-writer", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-replica", action="store_true")

@@ -758,6 +758,7 @@ lowdiff_status lowdiff_set_graphs(lowdiff_ctx* c, int32_t enable) {
 }
 
 lowdiff_status lowdiff_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send, void* stream) {
+  NvtxRange nvtx_("lowdiff_compress");
   lowdiff_status st = entry(c);
   if (st) return st;
   if (!grad || !send || (c->cfg.error_feedback && !residual)) return fail(c, LOWDIFF_E_INVALID, "compress: NULL buffer");
@@ -852,6 +853,7 @@ lowdiff_status lowdiff_peer_set(lowdiff_ctx* c, const void* const* ptrs) {
 }
 
 lowdiff_status lowdiff_exchange_peer(lowdiff_ctx* c, int32_t slot, float* dense_out, void* stream) {
+  NvtxRange nvtx_("lowdiff_exchange_peer");
   lowdiff_status st = entry(c);
   if (st) return st;
   if (!c->peer_set) return fail(c, LOWDIFF_E_STATE, "exchange_peer: call lowdiff_peer_set first");
@@ -885,6 +887,7 @@ lowdiff_status lowdiff_exchange_peer(lowdiff_ctx* c, int32_t slot, float* dense_
 // merged in shared memory and applied to p, m, v in one pass (no gathered buffer, no dense G).
 lowdiff_status lowdiff_exchange_peer_update(lowdiff_ctx* c, int32_t slot, const lowdiff_step_scalars* scalars,
                                             float* p, float* m, float* v, void* stream) {
+  NvtxRange nvtx_("lowdiff_exchange_peer_update");
   lowdiff_status st = entry(c);
   if (st) return st;
   if (!c->peer_set) return fail(c, LOWDIFF_E_STATE, "exchange_peer_update: call lowdiff_peer_set first");
@@ -926,6 +929,7 @@ lowdiff_status lowdiff_residual_materialize(lowdiff_ctx* c, float* residual, voi
 }
 
 lowdiff_status lowdiff_merge(lowdiff_ctx* c, int32_t world, const uint32_t* gathered, float* dense_out, void* stream) {
+  NvtxRange nvtx_("lowdiff_merge");
   lowdiff_status st = entry(c);
   if (st) return st;
   if (world < 1 || !gathered || !dense_out) return fail(c, LOWDIFF_E_INVALID, "merge: bad argument");
@@ -945,6 +949,7 @@ lowdiff_status lowdiff_merge(lowdiff_ctx* c, int32_t world, const uint32_t* gath
 
 lowdiff_status lowdiff_exchange(lowdiff_ctx* c, const uint32_t* send, uint32_t* gathered, float* dense_out,
                                 void* stream) {
+  NvtxRange nvtx_("lowdiff_exchange");
   lowdiff_status st = entry(c);
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -969,6 +974,7 @@ lowdiff_status lowdiff_exchange(lowdiff_ctx* c, const uint32_t* send, uint32_t* 
 lowdiff_status lowdiff_exchange_update(lowdiff_ctx* c, const uint32_t* send, uint32_t* gathered,
                                        const lowdiff_step_scalars* scalars, float* p, float* m, float* v,
                                        void* stream) {
+  NvtxRange nvtx_("lowdiff_exchange_update");
   lowdiff_status st = entry(c);
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -994,6 +1000,7 @@ lowdiff_status lowdiff_exchange_update(lowdiff_ctx* c, const uint32_t* send, uin
 
 lowdiff_status lowdiff_batch_persist(lowdiff_ctx* c, int64_t iteration, const lowdiff_step_scalars* scalars,
                                      const uint32_t* send, void* producer) {
+  NvtxRange nvtx_("lowdiff_batch_persist");
   lowdiff_status st = entry(c);
   if (st) return st;
   if ((st = take_deferred(c))) return st;
@@ -1065,6 +1072,7 @@ lowdiff_status lowdiff_wait_persist(lowdiff_ctx* c, void* stream) {
 
 lowdiff_status lowdiff_full_ckpt(lowdiff_ctx* c, int64_t iteration, const float* p, const float* m, const float* v,
                                  void* producer) {
+  NvtxRange nvtx_("lowdiff_full_ckpt");
   lowdiff_status st = entry(c);
   if (st) return st;
   if ((st = take_deferred(c))) return st;

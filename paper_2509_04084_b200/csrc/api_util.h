@@ -7,7 +7,18 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
+
+// NVTX range over a C-ABI call (host timeline: nsys / ncu --nvtx); header-only NVTX v3, a no-op
+// unless a tool is attached (SURVEY §5 tracing)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // return a CUDA failure as LOWDIFF_E_CUDA (the context is poisoned); needs `c` in scope
 #define CK(call)                                          \

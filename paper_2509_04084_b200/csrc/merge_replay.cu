@@ -139,7 +139,7 @@ merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __r
 }
 
 #ifndef LD_REPLAY_MINB
-#define LD_REPLAY_MINB 8   // resident CTAs per SM the replay is compiled for (128 threads: 64 registers)
+#define LD_REPLAY_MINB 7   // resident CTAs per SM the replay is compiled for (128 threads: 72 registers)
 #endif
 
 struct AdamK { float b1, c1, b2, c2, eps, nz; };   // nz = -0.0f (ieee_fast.cuh: opaque -0 addend)
@@ -160,7 +160,9 @@ template <int OPT> struct ReplayShape {
   static constexpr int minb = OPT == LOWDIFF_SGD ? 2 * LD_REPLAY_MINB : LD_REPLAY_MINB;
 };
 
-template <int OPT, int DIV, int MAXW>
+// EPS: Adam's eps lies in adam_u_fast's window [2^-60, 2^59] (checked on the host; false: every
+// group takes the intrinsics) -- a template flag, so the per-group test needs no predicate register
+template <int OPT, int DIV, int MAXW, bool EPS>
 __global__ void __launch_bounds__(ReplayShape<OPT>::threads,
                                   MAXW >= 8 ? ReplayShape<OPT>::minb * 3 / 4 : ReplayShape<OPT>::minb)
 replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
@@ -201,7 +203,6 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
   }
   const AdamK2 k2 = make_adamk2(ak.b1, ak.c1, ak.b2, ak.c2, ak.eps, ak.nz);
   const float n = (float)world, inv = 1.0f / (float)world;
-  const bool eps_ok = ak.eps >= 0x1p-60f && ak.eps <= 0x1p59f;   // adam_u_fast's precondition
   const uint64_t tstride = (uint64_t)(n_tiles + 1);   // n_tiles = tiles in the window
   const int64_t tl = blockIdx.x;                       // tile relative to the window
   // Software pipeline over steps: lane r (< 32) holds rank r's entry range of this tile for the
@@ -305,7 +306,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
         bool s0, s1;
         u[0] = adam2_u(M2[2 * i], V2[2 * i], g01, k2, R1, R2, &s0);
         u[1] = adam2_u(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2, &s1);
-        if (s0 | s1 | !eps_ok) {   // rare: redo the group exactly with the intrinsics
+        if (s0 | s1 | !EPS) {   // rare: redo the group exactly with the intrinsics
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const f32x2 mh = mul2(M2[2 * i + h], R1), vh = mul2(V2[2 * i + h], R2);
@@ -600,10 +601,16 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
   prof_begin(c, "replay", s, &h);
   const unsigned grid = (unsigned)n_tiles;
   const int dm = div_mode(mean, world);
-#define LD_REPLAY(OPT, DIV, W) \
-  replay_kernel<OPT, DIV, W><<<grid, ReplayShape<OPT>::threads, 0, s>>>(diffs, world, K, n_steps, start, n_tiles, \
-                                                                       scal_dev, \
-                                                             ak, lo, hi, tile0, p, m, v)
+  const bool eps_ok = ak.eps >= 0x1p-60f && ak.eps <= 0x1p59f;   // adam_u_fast's precondition
+#define LD_REPLAY(OPT, DIV, W)                                                                                  \
+  do {                                                                                                        \
+    if (OPT == LOWDIFF_SGD || eps_ok)                                                                         \
+      replay_kernel<OPT, DIV, W, true><<<grid, ReplayShape<OPT>::threads, 0, s>>>(                            \
+          diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, lo, hi, tile0, p, m, v);                     \
+    else                                                                                                      \
+      replay_kernel<OPT, DIV, W, false><<<grid, ReplayShape<OPT>::threads, 0, s>>>(                           \
+          diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, lo, hi, tile0, p, m, v);                     \
+  } while (0)
 #define LD_REPLAY_W(OPT, DIV)                                  \
   do {                                                         \
     if (world == 1) LD_REPLAY(OPT, DIV, 1);                    \

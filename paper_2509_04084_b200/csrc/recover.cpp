@@ -83,6 +83,7 @@ extern "C" {
 lowdiff_status lowdiff_replay_range(lowdiff_ctx* c, int32_t optim, int32_t world, int64_t n_steps,
                                     const uint32_t* diffs, const lowdiff_step_scalars* scalars, int64_t begin,
                                     int64_t end, float* p, float* m, float* v, void* stream) {
+  NvtxRange nvtx_("lowdiff_replay_range");
   lowdiff_status st = entry(c);
   if (st) return st;
   if (begin >= 0 && begin == end && end <= c->psi && n_steps >= 0) return LOWDIFF_OK;   // empty range
@@ -205,6 +206,7 @@ static lowdiff_status load_blocks_streamed(lowdiff_ctx* c, const Chain& ch, int6
 // uploading only the entries of each differential block that fall in it.
 static lowdiff_status recover_impl(lowdiff_ctx* c, int64_t target, float* p, float* m, float* v, int64_t* recovered,
                                    void* stream, bool sharded) {
+  NvtxRange nvtx_(sharded ? "lowdiff_recover_sharded" : "lowdiff_recover");
   lowdiff_status st = entry(c);
   if (st) return st;
   if (!c->cfg.ckpt_dir) return fail(c, LOWDIFF_E_INVALID, "recover: no ckpt_dir");
