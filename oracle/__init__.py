@@ -66,6 +66,10 @@ def lib():
         L.lowdiff_ref_union_bytes.argtypes = [C.c_int, C.c_int, P]
         L.lowdiff_ref_union_serialize.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int, P,
                                                   C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P, C.c_uint64]
+        L.lowdiff_ref_accumulate.argtypes = [C.c_uint32, P, P, P, P, C.c_uint64, P]
+        L.lowdiff_ref_accum_serialize.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int, P,
+                                                  C.c_uint32, C.c_uint32, C.c_uint32, P, P, C.c_uint64, P, P,
+                                                  C.c_uint64]
         L.lowdiff_ref_recover_union.argtypes = [C.c_char_p, C.c_uint32, C.c_int, P, C.c_uint32, C.c_int64,
                                                 P, P, P, P]
         L.lowdiff_ref_wasted_time.restype = C.c_double
@@ -251,6 +255,36 @@ def union_serialize(rank, world, first_iter, sizes, ppm, optim, flags, consts, s
     _check("union_serialize", lib().lowdiff_ref_union_serialize(
         rank, world, first_iter, n, len(sizes), _p(numel), ppm, optim, flags, _p(_c(consts, np.float32)),
         _p(sc), _p(counts), _p(ent if ent.size else np.zeros(1, np.uint32)), _p(out), cap))
+    return out.tobytes()
+
+
+def accumulate(unions):
+    """Accumulated batch mode (R-30): tensor addition of the dictionaries [(idx, val), ...] of one
+    batch in iteration order -> (idx u32[A], val u32[A]) -- see lowdiff_ref.cpp."""
+    counts = np.array([len(u[0]) for u in unions], np.uint64)
+    ent = np.concatenate([np.concatenate([_c(i, np.uint32), _c(v, np.uint32)]) for i, v in unions]
+                         + [np.zeros(1, np.uint32)])
+    cap = int(counts.sum())
+    idx = np.zeros(max(cap, 1), np.uint32)
+    val = np.zeros(max(cap, 1), np.uint32)
+    cnt = np.zeros(1, np.uint64)
+    _check("accumulate", lib().lowdiff_ref_accumulate(len(unions), _p(counts if counts.size else np.zeros(1, np.uint64)),
+                                                      _p(ent), _p(idx), _p(val), cap, _p(cnt)))
+    n = int(cnt[0])
+    return idx[:n].copy(), val[:n].copy()
+
+
+def accum_serialize(rank, world, first_iter, n_iters, sizes, ppm, optim, flags, consts, last_scalars, acc) -> bytes:
+    """Accumulated .ldu of one batch of n_iters iterations: acc = (idx, val) from accumulate()."""
+    numel = _c(sizes, np.int64)
+    idx, val = acc
+    n = len(idx)
+    iv = np.concatenate([_c(idx, np.uint32), _c(val, np.uint32), np.zeros(1, np.uint32)])
+    cap = union_bytes(len(sizes), np.array([n], np.uint64))
+    out = np.zeros(cap, np.uint8)
+    _check("accum_serialize", lib().lowdiff_ref_accum_serialize(
+        rank, world, first_iter, n_iters, len(sizes), _p(numel), ppm, optim, flags, _p(_c(consts, np.float32)),
+        _p(_c(last_scalars, np.float32)), n, _p(iv), _p(out), cap))
     return out.tobytes()
 
 

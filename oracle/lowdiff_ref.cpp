@@ -16,6 +16,10 @@
 //   union      -- union-compacted differential C^U_t: the synchronised G~_t
 //                 (Alg. 1 lines 5-6) kept as a dictionary
 //                 (PAPER.md:452), its .ldu file and recovery from it (R-29)
+//   accumulate -- Accumulated batch mode: the b dictionaries of a batch added
+//                 into one ("tensor addition", PAPER.md:270/274/452), one
+//                 optimizer step per batch at recovery -- INEXACT for b > 1
+//                 by construction (R-30)
 //
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
 // load this library.  It shares no code, header, table or constant generator
@@ -545,11 +549,99 @@ int lowdiff_ref_union_serialize(uint32_t rank, uint32_t world, uint64_t first_it
   return OK;
 }
 
+// --------------------------------------------------------------------------
+// Accumulated batch mode (R-30).  PAPER.md:270: writes of compressed
+// gradients are batched "with the help of the widely-used gradient accumulation
+// technique ... where the gradients of the same shape and size can be
+// accumulated"; the CPU batching operation "mainly involves the
+// addition of compressed gradients"; "checkpoints are aggregated
+// (tensor addition or dictionary accumulation)".  Tensor addition of the b
+// dictionaries C^U_t of one batch, written out as a dictionary in iteration
+// order:
+//   A = {}
+//   for t in batch (ascending), for (j, x) in C^U_t:  A[j] = (j in A ? A[j] : +0) + x
+// The accumulated file holds A and the scalars of the batch's last iteration;
+// recovery applies it as ONE optimizer step (gradient-accumulation semantics).
+// In exact arithmetic this equals the b steps only for SGD at a constant lr.
+// --------------------------------------------------------------------------
+int lowdiff_ref_accumulate(uint32_t n_iters, const uint64_t* counts, const uint32_t* entries /* per iteration
+                           idx[count] then val[count], concatenated */, uint32_t* out_idx, uint32_t* out_val,
+                           uint64_t cap, uint64_t* count) {
+  if (!fp_env_ok()) return E_FPENV;
+  if (!count || (n_iters && (!counts || !entries))) return E_INVALID;
+  std::map<uint32_t, float> A;
+  const uint32_t* q = entries;
+  for (uint32_t it = 0; it < n_iters; ++it) {
+    const uint64_t n = counts[it];
+    for (uint64_t e = 0; e < n; ++e) {
+      const uint32_t j = q[e];
+      const float x = bits_float(q[n + e]);
+      auto f = A.find(j);
+      const float before = f == A.end() ? 0.0f : f->second;
+      A[j] = before + x;
+    }
+    q += 2 * n;
+  }
+  uint64_t n = 0;
+  for (const auto& kv : A) {
+    if (n < cap) {
+      out_idx[n] = kv.first;
+      out_val[n] = float_bits(kv.second);
+    }
+    ++n;
+  }
+  *count = n;
+  return n <= cap ? OK : E_DIM;
+}
+
+// Accumulated .ldu: the .ldu header with flags bit 2 (ACCUMULATED) and n_iters = b (the iterations
+// the batch covers, first_iter .. first_iter + b - 1), then ONE block {u64 first_iter + b - 1, the
+// scalars of that last iteration, u32 count, u64 0} + idx u32[count] + val u32[count], then CRC-32C.
+int lowdiff_ref_accum_serialize(uint32_t rank, uint32_t world, uint64_t first_iter, uint32_t n_iters,
+                                int n_layers, const int64_t* numel, uint32_t ppm, uint32_t optim, uint32_t flags,
+                                const float* consts5, const float* last_scalars3, uint64_t count,
+                                const uint32_t* idx_val /* idx[count] then val[count] */, uint8_t* out,
+                                uint64_t cap) {
+  if (n_iters < 1) return E_INVALID;
+  uint64_t psi = 0, K = 0;
+  for (int l = 0; l < n_layers; ++l) { psi += (uint64_t)numel[l]; K += k_of((uint64_t)numel[l], ppm); }
+  std::vector<uint8_t> b;
+  b.push_back('L'); b.push_back('D'); b.push_back('U'); b.push_back('1');
+  put_u16(b, 1); put_u16(b, (uint16_t)(flags | 4u));
+  put_u32(b, rank); put_u32(b, world);
+  put_u64(b, first_iter);
+  put_u32(b, n_iters); put_u32(b, (uint32_t)n_layers);
+  put_u64(b, psi); put_u64(b, K);
+  put_u32(b, ppm); put_u32(b, optim);
+  put_u64(b, psi * rank / world);
+  put_u64(b, psi * (rank + 1) / world);
+  put_u64(b, 0);
+  for (int i = 0; i < 5; ++i) put_f32(b, consts5[i]);
+  for (int i = 0; i < 3; ++i) put_u32(b, 0);
+  for (int l = 0; l < n_layers; ++l) {
+    put_u64(b, (uint64_t)numel[l]);
+    put_u32(b, (uint32_t)k_of((uint64_t)numel[l], ppm));
+    put_u32(b, 0);
+  }
+  put_u64(b, first_iter + n_iters - 1);
+  for (int i = 0; i < 3; ++i) put_f32(b, last_scalars3[i]);
+  put_u32(b, (uint32_t)count);
+  put_u64(b, 0);
+  for (uint64_t e = 0; e < 2 * count; ++e) put_u32(b, idx_val[e]);
+  put_u32(b, crc32c_bitwise(b.data(), b.size()));
+  if (b.size() > cap) return E_INVALID;
+  std::memcpy(out, b.data(), b.size());
+  return OK;
+}
+
 // Recovery from union-compacted differentials (Alg. 1 recovery, with C^U_t in
 // place of the gathered blocks): the same chain rules as lowdiff_ref_recover (.ldf shards of the
 // latest complete full F <= target; for t = F+1..target every rank's .ldu must hold iteration t,
 // later files winning), then per iteration G_t[j] = the stored value for every stored j (the ranks'
-// shards are disjoint), +0.0f elsewhere, and the optimizer step with the block's scalars.
+// shards are disjoint), +0.0f elsewhere, and the optimizer step with the block's scalars.  An
+// accumulated file (flags bit 2, R-30) is one replay unit covering its n_iters iterations: one
+// optimizer step with G[j] = the accumulated value and the stored scalars of its last iteration; a
+// target inside such a batch is not reachable (E_GAP).
 int lowdiff_ref_recover_union(const char* dir, uint32_t world, int n_layers, const int64_t* numel,
                               uint32_t ppm, int64_t target, float* p, float* m, float* v,
                               int64_t* recovered) {
@@ -595,8 +687,10 @@ int lowdiff_ref_recover_union(const char* dir, uint32_t world, int n_layers, con
     for (uint64_t j = 0; j < S; ++j) if (m) m[sb + j] = get_f32(q + 4 * (S + j));
     for (uint64_t j = 0; j < S; ++j) if (v) v[sb + j] = get_f32(q + 4 * (2 * S + j));
   }
-  // which file (and byte offset) holds iteration t of rank r; every used file is verified
-  std::vector<std::map<int64_t, std::pair<std::string, uint64_t>>> where(world);
+  // which file (and byte offset) holds the replay unit starting at iteration t of rank r, and how
+  // many iterations it covers (1; b for an accumulated batch); every used file is verified
+  struct Unit { std::string path; uint64_t off; int64_t span; };
+  std::vector<std::map<int64_t, Unit>> where(world);
   std::map<std::string, std::vector<uint8_t>> loaded;
   for (uint32_t r = 0; r < world; ++r) {
     for (auto& fe : diffs[r]) {   // ascending first_iter: later files override earlier ones
@@ -610,36 +704,52 @@ int lowdiff_ref_recover_union(const char* dir, uint32_t world, int n_layers, con
           get_u64(buf.data() + 56) != psi * r / world || get_u64(buf.data() + 64) != psi * (r + 1) / world)
         return E_CORRUPT;
       const uint32_t n_iters = get_u32(buf.data() + 24);
+      const bool accumulated = (get_u16(buf.data() + 6) & 4u) != 0;
       uint64_t off = 112 + 16 * (uint64_t)n_layers;
-      for (uint32_t i = 0; i < n_iters; ++i) {
+      if (accumulated) {   // one block for iterations fe.first .. fe.first + n_iters - 1
+        if (n_iters < 1 || off + 32 > buf.size() - 4) return E_CORRUPT;
+        const uint64_t cnt = get_u32(buf.data() + off + 20);
+        if ((int64_t)get_u64(buf.data() + off) != fe.first + n_iters - 1) return E_CORRUPT;
+        where[r][fe.first] = {fe.second, off, (int64_t)n_iters};
+        off += 32 + 8 * cnt;
+      }
+      for (uint32_t i = 0; i < n_iters && !accumulated; ++i) {
         if (off + 32 > buf.size() - 4) return E_CORRUPT;
         const uint64_t cnt = get_u32(buf.data() + off + 20);
         if ((int64_t)get_u64(buf.data() + off) != fe.first + i) return E_CORRUPT;
-        where[r][fe.first + i] = {fe.second, off};
+        where[r][fe.first + i] = {fe.second, off, 1};
         off += 32 + 8 * cnt;
       }
       if (off != buf.size() - 4) return E_CORRUPT;
       loaded[fe.second] = std::move(buf);
     }
   }
+  // the chain: units F+1 .., every rank holding a unit that starts there and covers the same
+  // iterations; an accumulated batch is recovered whole or not at all
   int64_t last = F;
+  std::vector<int64_t> starts;
   while (true) {
     const int64_t t = last + 1;
-    if (target >= 0 && t > target) break;
     bool all = true;
-    for (uint32_t r = 0; r < world; ++r) all = all && where[r].count(t);
-    if (!all) break;
-    last = t;
+    int64_t span = 0;
+    for (uint32_t r = 0; r < world && all; ++r) {
+      all = where[r].count(t) > 0;
+      if (all && r == 0) span = where[r][t].span;
+      else if (all && where[r][t].span != span) return E_CORRUPT;
+    }
+    if (!all || (target >= 0 && t + span - 1 > target)) break;
+    starts.push_back(t);
+    last = t + span - 1;
   }
   if (target >= 0 && last < target) return E_GAP;
   std::vector<float> G(psi);
-  for (int64_t t = F + 1; t <= last; ++t) {
+  for (int64_t t : starts) {
     float scal[3] = {0, 0, 0};
     float consts[5] = {0, 0, 0, 0, 0};
     std::fill(G.begin(), G.end(), 0.0f);
     for (uint32_t r = 0; r < world; ++r) {
-      const std::vector<uint8_t>& buf = loaded[where[r][t].first];
-      const uint8_t* blk = buf.data() + where[r][t].second;
+      const std::vector<uint8_t>& buf = loaded[where[r][t].path];
+      const uint8_t* blk = buf.data() + where[r][t].off;
       float s3[3] = {get_f32(blk + 8), get_f32(blk + 12), get_f32(blk + 16)};
       if (r == 0) {
         std::memcpy(scal, s3, sizeof scal);

@@ -12,6 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "oracle", "lowdiff_ref.cpp")
 C, X, F, U = ("tests/test_oracle_compress.py", "tests/test_oracle_exchange_optim.py", "tests/test_oracle_files.py",
               "tests/test_oracle_union.py")
+A = "tests/test_oracle_accumulate.py"
 
 MUTANTS = [
     ("ties go to the higher index", "      return a < b;\n    });", "      return a > b;\n    });", C),
@@ -33,6 +34,9 @@ MUTANTS = [
     ("union keeps only the first rank's support",
      "for (int r = 0; r < world; ++r)\n    for (uint64_t e = 0; e < K; ++e) member[gathered[(uint64_t)r * 2 * K + e]] = 1;",
      "for (int r = 0; r < 1; ++r)\n    for (uint64_t e = 0; e < K; ++e) member[gathered[(uint64_t)r * 2 * K + e]] = 1;", U),
+    ("accumulation overwrites instead of adding", "A[j] = before + x;", "A[j] = x;", A),
+    ("accumulated batch replayed with its first iteration's step", "where[r][fe.first] = {fe.second, off, (int64_t)n_iters};",
+     "where[r][fe.first] = {fe.second, off, 1};", A),
     ("CRC polynomial wrong", "(crc >> 1) ^ 0x82F63B78u", "(crc >> 1) ^ 0xEDB88320u", F),
 ]
 
