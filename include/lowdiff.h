@@ -288,6 +288,20 @@ lowdiff_status lowdiff_union_compact(lowdiff_ctx *ctx, int32_t world, const uint
  *    next call / lowdiff_sync).  lowdiff_sync flushes the final partial batch. */
 lowdiff_status lowdiff_union_persist(lowdiff_ctx *ctx, int64_t iteration, const lowdiff_step_scalars *scalars,
                                      const uint32_t *gathered, void *producer);
+/* Batch mode of union_persist (R-30).
+ *    LOWDIFF_BATCH_RECORD (default): a .ldu holds its b dictionaries verbatim; recovery is exact.
+ *    LOWDIFF_BATCH_ACCUMULATED: the paper's "gradient accumulation" batching, done by
+ *    the CPU as "the addition of compressed gradients" ("tensor addition or dictionary
+ *    accumulation"): the writer thread adds the b dictionaries of a batch into ONE,
+ *    in iteration order (A[j] = (j in A ? A[j] : +0.0f) + x, fp32), and writes it as a .ldu with
+ *    flags bit 2 set, n_iters = b and a single block tagged with the batch's last iteration and
+ *    its scalars.  recover_union replays such a batch as ONE optimizer step with G = A and those
+ *    scalars: the state after the batch is NOT the live state for b > 1 (exact in real arithmetic
+ *    only for SGD at a constant lr), and targets inside the batch are unreachable (E_GAP).
+ *    Switching modes first writes the batch in flight (partial) in the old mode; setting the
+ *    current mode is a no-op.  E_INVALID for another value. */
+enum { LOWDIFF_BATCH_RECORD = 0, LOWDIFF_BATCH_ACCUMULATED = 1 };
+lowdiff_status lowdiff_set_batch_mode(lowdiff_ctx *ctx, int32_t mode);
 /* recover_union: Alg. 1 recovery from full checkpoints and .ldu files with the
  *    chain rules of lowdiff_recover (latest complete Full F <= target; every needed rank's .ldu
  *    must hold each of F+1..target, later files winning; E_GAP / E_CORRUPT / E_IO as there).
@@ -295,7 +309,9 @@ lowdiff_status lowdiff_union_persist(lowdiff_ctx *ctx, int64_t iteration, const 
  *    sharded = 1: only this rank's .ldf shard and .ldu files, only its element range of p, m, v
  *    written (the arrays are still indexed by global element).  The replay is the fused kernel
  *    of lowdiff_replay; the result is bitwise the state lowdiff_recover reaches from the .ldb
- *    chain of the same run.  Synchronous on `stream`. */
+ *    chain of the same run (record mode).  An accumulated .ldu (see lowdiff_set_batch_mode) is one
+ *    replay step covering its b iterations; every rank must hold a batch covering the same
+ *    iterations (else E_CORRUPT).  Synchronous on `stream`. */
 lowdiff_status lowdiff_recover_union(lowdiff_ctx *ctx, int64_t target, float *p, float *m, float *v, int32_t sharded,
                                      int64_t *recovered, void *stream);
 

@@ -16,6 +16,6 @@ def build(verbose: bool = False) -> str:
     return os.path.join(_HERE, "_lib", "liblowdiff.so")
 
 
-from .lowdiff import (ADAM, SGD, Context, LowDiffError, Options, StepScalars, bucket_plan, chain_scan,  # noqa: E402,F401
+from .lowdiff import (ADAM, BATCH_ACCUMULATED, BATCH_RECORD, SGD, Context, LowDiffError, Options, StepScalars, bucket_plan, chain_scan,  # noqa: E402,F401
                       crc32c, derive_adam_consts, derive_step_scalars, nccl_unique_id, retire_from, write_batch_host,
                       write_full_host)

@@ -107,7 +107,7 @@ struct Slot {
 // work item of the LowDiff+ replica worker: 0 = initial copy landed, 1 = apply the snapshotted
 // gradient of `iteration`, 2 = persist the replica as it stands after the preceding items
 struct RepJob { int kind; int64_t iteration; lowdiff_step_scalars sc; };
-struct UJob { int64_t iteration; lowdiff_step_scalars sc; int buf; };
+struct UJob { int64_t iteration; lowdiff_step_scalars sc; int buf; bool accumulate; };
 // pinned chunks + streams of the recovery loader (files.cpp stream_to_device), kept per context
 struct Staging {
   static constexpr uint64_t kChunk = 64ull << 20;
@@ -277,6 +277,9 @@ struct lowdiff_ctx {
   std::thread u_writer;
   cudaStream_t u_stream = nullptr;
   std::atomic<int64_t> u_files{0}, u_bytes{0}, u_entries{0};
+  // Accumulated batch mode (R-30): the writer adds each iteration's dictionary into u_acc_* (host
+  // memory) and writes one accumulated .ldu per batch
+  int u_accumulate = 0;
 };
 
 namespace ld {

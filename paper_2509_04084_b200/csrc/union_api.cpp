@@ -77,10 +77,12 @@ static std::string union_name(const std::string& dir, int rank, int64_t first) {
   return dir + buf;
 }
 
-// 80-byte header + hyper (32 B) + layer table (16 B per layer) of a .ldu file
-static std::vector<uint8_t> ldu_prefix(const lowdiff_ctx* c, int64_t first, uint32_t n_iters) {
+// 80-byte header + hyper (32 B) + layer table (16 B per layer) of a .ldu file; flags bit 2 marks
+// an accumulated batch (one block covering n_iters iterations)
+static std::vector<uint8_t> ldu_prefix(const lowdiff_ctx* c, int64_t first, uint32_t n_iters, bool accumulated) {
   std::vector<uint8_t> b(112 + 16 * (size_t)c->cfg.n_layers, 0);
-  const uint16_t ver = 1, flags = (uint16_t)((c->cfg.error_feedback ? 1 : 0) | (c->cfg.mean ? 2 : 0));
+  const uint16_t ver = 1,
+                 flags = (uint16_t)((c->cfg.error_feedback ? 1 : 0) | (c->cfg.mean ? 2 : 0) | (accumulated ? 4 : 0));
   const uint32_t rk = (uint32_t)c->cfg.rank, wd = (uint32_t)c->cfg.world, nl = (uint32_t)c->cfg.n_layers;
   const uint32_t ppm = c->cfg.density_ppm, opt = (uint32_t)c->cfg.optim;
   const uint64_t psi = (uint64_t)c->psi, K = (uint64_t)c->K, sb = psi * rk / wd, se = psi * (rk + 1) / wd;
@@ -109,11 +111,99 @@ static std::vector<uint8_t> ldu_prefix(const lowdiff_ctx* c, int64_t first, uint
   return b;
 }
 
+// Accumulated batch mode (R-30): tensor addition of the batch's
+// dictionaries on the host, in iteration order: A[j] = (j in A ? A[j] : +0) + x.  Both lists are
+// index-ascending, so one merge pass per iteration.
+struct UAcc {
+  int64_t first = -1, last = -1;
+  uint32_t n_iters = 0;
+  lowdiff_step_scalars sc{};
+  std::vector<uint32_t> idx, val, tidx, tval;
+};
+
+static void accumulate_into(UAcc& A, const UBlock& B) {
+  const uint64_t n = B.n;
+  const uint32_t* bi = B.data.data();
+  const uint32_t* bv = B.data.data() + n;
+  A.tidx.clear();
+  A.tval.clear();
+  A.tidx.reserve(A.idx.size() + n);
+  A.tval.reserve(A.idx.size() + n);
+  size_t i = 0, e = 0;
+  while (i < A.idx.size() || e < n) {
+    if (e == n || (i < A.idx.size() && A.idx[i] < bi[e])) {
+      A.tidx.push_back(A.idx[i]);
+      A.tval.push_back(A.val[i]);
+      ++i;
+    } else {
+      const bool both = i < A.idx.size() && A.idx[i] == bi[e];
+      float before = 0.0f, x;
+      if (both) std::memcpy(&before, &A.val[i], 4);
+      std::memcpy(&x, &bv[e], 4);
+      const float sum = before + x;
+      uint32_t u;
+      std::memcpy(&u, &sum, 4);
+      A.tidx.push_back(bi[e]);
+      A.tval.push_back(u);
+      ++e;
+      if (both) ++i;
+    }
+  }
+  A.idx.swap(A.tidx);
+  A.val.swap(A.tval);
+  if (A.n_iters == 0) A.first = B.it;
+  A.last = B.it;
+  A.sc = B.sc;
+  A.n_iters += 1;
+}
+
+// CRC trailer, *.tmp + rename (parts: everything before the CRC)
+static void write_ldu(lowdiff_ctx* c, int64_t first, std::vector<std::pair<const void*, size_t>>& parts) {
+  const int64_t t0 = now_ns();
+  uint32_t crc = 0xFFFFFFFFu;
+  size_t bytes = 4;
+  for (auto& q : parts) {
+    crc = ld::crc32c_update(crc, q.first, q.second);
+    bytes += q.second;
+  }
+  crc ^= 0xFFFFFFFFu;
+  parts.push_back({&crc, 4});
+  std::string err;
+  lowdiff_status st =
+      ld::write_file_atomic(union_name(c->ckpt_dir, c->cfg.rank, first), parts, c->cfg.fsync != 0, &err);
+  if (st) set_deferred(c, st, err);
+  else { c->u_files += 1; c->u_bytes += (int64_t)bytes; }
+  c->writer_ns += now_ns() - t0;
+}
+
+static void union_write_accumulated(lowdiff_ctx* c, UAcc& A) {
+  if (A.n_iters == 0) return;
+  if (c->cfg.ckpt_dir) {
+    const std::vector<uint8_t> pre = ldu_prefix(c, A.first, A.n_iters, true);
+    std::array<uint8_t, 32> h;
+    h.fill(0);
+    const uint64_t it = (uint64_t)A.last;
+    const uint32_t n = (uint32_t)A.idx.size();
+    std::memcpy(h.data(), &it, 8);
+    std::memcpy(h.data() + 8, &A.sc, 12);
+    std::memcpy(h.data() + 20, &n, 4);
+    std::vector<std::pair<const void*, size_t>> parts{{pre.data(), pre.size()}, {h.data(), 32}};
+    if (n) {
+      parts.push_back({A.idx.data(), 4 * (size_t)n});
+      parts.push_back({A.val.data(), 4 * (size_t)n});
+    }
+    write_ldu(c, A.first, parts);
+  }
+  A.idx.clear();
+  A.val.clear();
+  A.n_iters = 0;
+  A.first = A.last = -1;
+}
+
 static void union_write(lowdiff_ctx* c, std::vector<UBlock>& batch) {
   if (batch.empty()) return;
   if (c->cfg.ckpt_dir) {
-    const int64_t t0 = now_ns();
-    const std::vector<uint8_t> pre = ldu_prefix(c, batch[0].it, (uint32_t)batch.size());
+    const std::vector<uint8_t> pre = ldu_prefix(c, batch[0].it, (uint32_t)batch.size(), false);
     std::vector<std::array<uint8_t, 32>> heads(batch.size());
     std::vector<std::pair<const void*, size_t>> parts{{pre.data(), pre.size()}};
     for (size_t i = 0; i < batch.size(); ++i) {
@@ -127,20 +217,7 @@ static void union_write(lowdiff_ctx* c, std::vector<UBlock>& batch) {
       parts.push_back({h.data(), 32});
       if (n) parts.push_back({batch[i].data.data(), 8 * (size_t)n});
     }
-    uint32_t crc = 0xFFFFFFFFu;
-    size_t bytes = 4;
-    for (auto& q : parts) {
-      crc = ld::crc32c_update(crc, q.first, q.second);
-      bytes += q.second;
-    }
-    crc ^= 0xFFFFFFFFu;
-    parts.push_back({&crc, 4});
-    std::string err;
-    lowdiff_status st = ld::write_file_atomic(union_name(c->ckpt_dir, c->cfg.rank, batch[0].it), parts,
-                                              c->cfg.fsync != 0, &err);
-    if (st) set_deferred(c, st, err);
-    else { c->u_files += 1; c->u_bytes += (int64_t)bytes; }
-    c->writer_ns += now_ns() - t0;
+    write_ldu(c, batch[0].it, parts);
   }
   batch.clear();
 }
@@ -148,6 +225,12 @@ static void union_write(lowdiff_ctx* c, std::vector<UBlock>& batch) {
 static void union_loop(lowdiff_ctx* c) {
   cudaSetDevice(c->device);
   std::vector<UBlock> batch;
+  UAcc acc;
+  // writes whatever is pending (record batch or accumulated batch)
+  auto write_pending = [&] {
+    union_write(c, batch);
+    union_write_accumulated(c, acc);
+  };
   for (;;) {
     ld::UJob j{};
     bool have = false, flush = false;
@@ -195,18 +278,27 @@ static void union_loop(lowdiff_ctx* c) {
                      e != cudaSuccess ? std::string("union differential copy: ") + cudaGetErrorString(e)
                                       : "non-finite accumulated gradient before union iteration " +
                                             std::to_string(j.iteration));
-        union_write(c, batch);   // the chain stops before this iteration
+        write_pending();   // the chain stops before this iteration
       } else {
         c->u_entries += (int64_t)B.n;
-        batch.push_back(std::move(B));
-        if ((int)batch.size() == c->b) union_write(c, batch);
+        if (j.accumulate) {
+          union_write(c, batch);   // a record batch in flight ends where accumulation starts
+          const int64_t t0 = now_ns();
+          accumulate_into(acc, B);
+          c->writer_ns += now_ns() - t0;
+          if ((int)acc.n_iters == c->b) union_write_accumulated(c, acc);
+        } else {
+          union_write_accumulated(c, acc);
+          batch.push_back(std::move(B));
+          if ((int)batch.size() == c->b) union_write(c, batch);
+        }
       }
     } else if (flush) {
-      union_write(c, batch);
+      write_pending();
       std::lock_guard<std::mutex> g(c->u_mu);
       c->u_flush = false;
     } else {
-      union_write(c, batch);
+      write_pending();
       std::lock_guard<std::mutex> g(c->u_mu);
       c->u_busy = 0;
       c->u_cv_idle.notify_all();
@@ -267,10 +359,22 @@ lowdiff_status lowdiff_union_persist(lowdiff_ctx* c, int64_t iteration, const lo
   c->u_next_iter = iteration + 1;
   {
     std::lock_guard<std::mutex> g(c->u_mu);
-    c->u_q.push_back(ld::UJob{iteration, *scalars, buf});
+    c->u_q.push_back(ld::UJob{iteration, *scalars, buf, c->u_accumulate != 0});
     c->u_cv.notify_all();
   }
   return LOWDIFF_OK;
+}
+
+// Accumulated batch mode switch (R-30): the union writer first writes the batch in flight
+lowdiff_status lowdiff_set_batch_mode(lowdiff_ctx* c, int32_t mode) {
+  lowdiff_status st = entry(c);
+  if (st) return st;
+  if (mode != LOWDIFF_BATCH_RECORD && mode != LOWDIFF_BATCH_ACCUMULATED)
+    return fail(c, LOWDIFF_E_INVALID, "set_batch_mode: unknown mode");
+  if ((mode == LOWDIFF_BATCH_ACCUMULATED) == (c->u_accumulate != 0)) return LOWDIFF_OK;
+  union_drain(c);
+  c->u_accumulate = mode == LOWDIFF_BATCH_ACCUMULATED;
+  return take_deferred(c);
 }
 
 // recovery from .ldf + .ldu: the chain rules of lowdiff_recover; the replay is the fused kernel with
@@ -316,7 +420,9 @@ static lowdiff_status union_recover_impl(lowdiff_ctx* c, int64_t target, float* 
   // index every needed rank's .ldu files: iteration -> (file, byte offset of its block, count);
   // files are verified (magic, CRC, header fields, block walk) when indexed
   const uint32_t r0 = sharded ? (uint32_t)c->cfg.rank : 0, r1 = sharded ? (uint32_t)c->cfg.rank + 1 : world;
-  struct Where { std::string path; size_t off; uint64_t n; };
+  // replay units: iteration -> (file, byte offset of its block, count, iterations covered: 1, or b
+  // for an accumulated batch keyed by its first iteration)
+  struct Where { std::string path; size_t off; uint64_t n; int64_t span; };
   std::vector<std::map<int64_t, Where>> where(world);
   for (uint32_t r = r0; r < r1; ++r) {
     for (auto& fe : diffs[r]) {   // ascending first iteration: later files win
@@ -332,49 +438,67 @@ static lowdiff_status union_recover_impl(lowdiff_ctx* c, int64_t target, float* 
           rd<uint64_t>(buf.data() + 64) != psi * (r + 1) / world)
         return fail(c, LOWDIFF_E_CORRUPT, "corrupt union file " + fe.second);
       const uint32_t n_it = rd<uint32_t>(buf.data() + 24);
+      const bool accumulated = (rd<uint16_t>(buf.data() + 6) & 4u) != 0;
       size_t off = 112 + 16 * L;
-      for (uint32_t i = 0; i < n_it; ++i) {
-        if (off + 32 > buf.size() - 4 || (int64_t)rd<uint64_t>(buf.data() + off) != fe.first + i)
+      const uint32_t n_blocks = accumulated ? 1u : n_it;
+      if (accumulated && n_it < 1) return fail(c, LOWDIFF_E_CORRUPT, "corrupt union file " + fe.second);
+      for (uint32_t i = 0; i < n_blocks; ++i) {
+        const int64_t it = accumulated ? fe.first + n_it - 1 : fe.first + i;
+        if (off + 32 > buf.size() - 4 || (int64_t)rd<uint64_t>(buf.data() + off) != it)
           return fail(c, LOWDIFF_E_CORRUPT, "corrupt union file " + fe.second);
         const uint64_t n = rd<uint32_t>(buf.data() + off + 20);
-        where[r][fe.first + i] = Where{fe.second, off, n};
+        where[r][accumulated ? fe.first : it] = Where{fe.second, off, n, accumulated ? (int64_t)n_it : 1};
         off += 32 + 8 * n;
       }
       if (off != buf.size() - 4) return fail(c, LOWDIFF_E_CORRUPT, "corrupt union file " + fe.second);
     }
   }
+  // the chain of replay units F+1, ...: every needed rank holds a unit starting there that covers
+  // the same iterations; an accumulated batch is recovered whole or not at all (R-30)
   int64_t last = F;
+  std::vector<int64_t> units;
   for (;;) {
     const int64_t t = last + 1;
-    if (target >= 0 && t > target) break;
     bool all = true;
-    for (uint32_t r = r0; r < r1 && all; ++r) all = where[r].count(t) > 0;
-    if (!all) break;
-    last = t;
+    int64_t span = 0;
+    for (uint32_t r = r0; r < r1 && all; ++r) {
+      auto f = where[r].find(t);
+      all = f != where[r].end();
+      if (!all) break;
+      if (r == r0) span = f->second.span;
+      else if (f->second.span != span)
+        return fail(c, LOWDIFF_E_CORRUPT, "ranks disagree on the batch starting at iteration " + std::to_string(t));
+    }
+    if (!all || (target >= 0 && t + span - 1 > target)) break;
+    units.push_back(t);
+    last = t + span - 1;
   }
-  if (target >= 0 && last < target) return fail(c, LOWDIFF_E_GAP, "union chain has a gap after " + std::to_string(last));
+  if (target >= 0 && last < target)
+    return fail(c, LOWDIFF_E_GAP, "union chain has a gap (or an accumulated batch boundary) after " + std::to_string(last));
   const uint64_t lo = sharded ? psi * c->cfg.rank / world : 0, hi = sharded ? psi * (c->cfg.rank + 1) / world : psi;
   // replay in chunks of steps: block of step t = idx[Kc] | val[Kc], entries [0, U_t) valid
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   std::map<std::string, std::vector<uint8_t>> cache;
   lowdiff_status result = LOWDIFF_OK;
-  for (int64_t t0 = F + 1; t0 <= last && result == LOWDIFF_OK;) {
-    // grow the chunk while its padded size stays within a quarter of free memory
+  const int64_t n_units = (int64_t)units.size();
+  for (int64_t u0 = 0; u0 < n_units && result == LOWDIFF_OK;) {
+    // grow the chunk of replay steps while its padded size stays within a quarter of free memory
     uint64_t Kc = 1;
-    int64_t t1 = t0;
-    for (int64_t t = t0; t <= last; ++t) {
+    int64_t u1 = u0;
+    for (int64_t u = u0; u < n_units; ++u) {
       uint64_t U = 0;
-      for (uint32_t r = r0; r < r1; ++r) U += where[r][t].n;
+      for (uint32_t r = r0; r < r1; ++r) U += where[r][units[u]].n;
       const uint64_t k2 = std::max<uint64_t>(Kc, U);
-      if (t > t0 && (uint64_t)(t - t0 + 1) * 8 * k2 > free_b / 4) break;
+      if (u > u0 && (uint64_t)(u - u0 + 1) * 8 * k2 > free_b / 4) break;
       Kc = k2;
-      t1 = t;
+      u1 = u;
     }
-    const int64_t ns = t1 - t0 + 1;
+    const int64_t ns = u1 - u0 + 1;
     std::vector<uint32_t> host((size_t)ns * 2 * Kc, 0u), ranges((size_t)ns * 2, 0u);
     std::vector<lowdiff_step_scalars> scal((size_t)ns);
-    for (int64_t t = t0; t <= t1 && result == LOWDIFF_OK; ++t) {
+    for (int64_t u = u0; u <= u1 && result == LOWDIFF_OK; ++u) {
+      const int64_t t = units[u];
       uint64_t at = 0;
       for (uint32_t r = r0; r < r1; ++r) {
         const Where& w = where[r][t];
@@ -392,8 +516,8 @@ static lowdiff_status union_recover_impl(lowdiff_ctx* c, int64_t target, float* 
         const uint8_t* blk = itc->second.data() + w.off;
         lowdiff_step_scalars sc;
         std::memcpy(&sc, blk + 8, 12);
-        if (r == r0) scal[t - t0] = sc;
-        else if (std::memcmp(&sc, &scal[t - t0], 12) != 0) {
+        if (r == r0) scal[u - u0] = sc;
+        else if (std::memcmp(&sc, &scal[u - u0], 12) != 0) {
           result = fail(c, LOWDIFF_E_CORRUPT, "ranks disagree on the scalars of iteration " + std::to_string(t));
           break;
         }
@@ -405,12 +529,12 @@ static lowdiff_status union_recover_impl(lowdiff_ctx* c, int64_t target, float* 
             break;
           }
         if (result) break;
-        uint32_t* dst = host.data() + (size_t)(t - t0) * 2 * Kc;
+        uint32_t* dst = host.data() + (size_t)(u - u0) * 2 * Kc;
         std::memcpy(dst + at, idx, 4 * w.n);
         std::memcpy(dst + Kc + at, idx + w.n, 4 * w.n);
         at += w.n;
       }
-      ranges[2 * (size_t)(t - t0) + 1] = (uint32_t)at;
+      ranges[2 * (size_t)(u - u0) + 1] = (uint32_t)at;
     }
     if (result) break;
     uint32_t* d_diffs = nullptr;
@@ -430,7 +554,7 @@ static lowdiff_status union_recover_impl(lowdiff_ctx* c, int64_t target, float* 
     if (d_ranges) cudaFree(d_ranges);
     if (scal_dev) cudaFree(scal_dev);
     if (e != cudaSuccess) result = cuda_fail(c, e, "union replay");
-    t0 = t1 + 1;
+    u0 = u1 + 1;
   }
   if (result) return result;
   if (recovered) *recovered = last;

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("LOWDIFF_LIB") or os.path.join(_HERE, "_lib", "liblowd
 
 OK, E_INVALID, E_DIM, E_NUMERIC, E_CUDA, E_NCCL, E_IO, E_CORRUPT, E_GAP, E_STATE = range(10)
 SGD, ADAM = 0, 1
+BATCH_RECORD, BATCH_ACCUMULATED = 0, 1   # lowdiff_set_batch_mode
 STATUS_NAMES = ["OK", "E_INVALID", "E_DIM", "E_NUMERIC", "E_CUDA", "E_NCCL", "E_IO", "E_CORRUPT",
                 "E_GAP", "E_STATE"]
 
@@ -118,6 +119,7 @@ def lib():
             "prof_read": ([P, C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)], S),
             "kernel_launches": ([P], C.c_int64),
             "set_graphs": ([P, C.c_int32], S),
+            "set_batch_mode": ([P, C.c_int32], S),
             "last_error": ([P], C.c_char_p),
             "nccl_unique_id": ([P], S),
             "derive_step_scalars": ([C.c_int64, C.c_double, C.c_double, C.c_double, C.POINTER(StepScalars)], S),
@@ -150,7 +152,7 @@ EXPORTED = ["create", "destroy", "query", "layer_k", "compress", "residual_mater
             "replica_init",
             "replica_step", "replica_persist", "replica_wait", "replica_restore", "host_adam_step", "host_sgd_step",
             "sync", "get_stats", "compress_trace",
-            "prof_enable", "prof_read", "kernel_launches", "set_graphs", "last_error", "nccl_unique_id",
+            "prof_enable", "prof_read", "kernel_launches", "set_graphs", "set_batch_mode", "last_error", "nccl_unique_id",
             "derive_step_scalars", "derive_adam_consts", "crc32c", "chain_scan", "write_batch_host", "retire_from",
             "write_full_host", "abi_version", "selftest", "wasted_time", "optimal_config", "optimal_config_feasible", "config_step",
             "simulate_failures"]
@@ -510,6 +512,11 @@ class Context:
     def set_graphs(self, on=True):
         """Replay compress / merge as captured CUDA graphs (fewer launch gaps for small models)."""
         self._c("set_graphs", lib().lowdiff_set_graphs(self._h, int(bool(on))))
+
+    def set_batch_mode(self, mode):
+        """BATCH_RECORD (exact) or BATCH_ACCUMULATED (the paper's tensor-addition batching of the
+        union dictionaries; one replay step per batch, inexact for b > 1) -- include/lowdiff.h."""
+        self._c("set_batch_mode", lib().lowdiff_set_batch_mode(self._h, int(mode)))
 
     def prof_enable(self, on=True):
         self._c("prof_enable", lib().lowdiff_prof_enable(self._h, int(on)))

@@ -212,3 +212,77 @@ def test_union_recover_gap(ref, tmp_path):
         rc.recover_union(q, mq, vq, target=5)
     assert e.value.code == ld.lowdiff.E_GAP
     rc.close()
+
+
+@pytest.mark.parametrize("world,b", [(1, 3), (2, 4), (4, 2)])
+def test_accumulated_batch_mode_files_and_recover(ref, tmp_path, world, b):
+    """Accumulated batch mode (R-30): the writer's tensor addition of each batch's dictionaries gives
+    .ldu files byte-identical to the oracle's accumulate + accum_serialize; recovery (all shards and
+    sharded) equals the oracle's recover_union over the same files -- and, for b > 1, differs from
+    the live state (the mode is inexact by construction).  A mode switch mid-run writes the batch in
+    flight in the old mode; the mixed chain recovers like the oracle."""
+    sizes, ppm, T, lr = [30000, 1600, 50000, 7], 10000, 9, 1e-2
+    psi = sum(sizes)
+    states, gath, scals = _oracle_live(ref, sizes, ppm, world, T, lr, seed=20 + world)
+    d = str(tmp_path)
+    flags = ref.FLAG_EF | ref.FLAG_MEAN
+    consts = ref.adam_consts()
+    for r in range(world):
+        with open(os.path.join(d, ref.full_name(r, 0)), "wb") as f:
+            f.write(ref.full_serialize(r, world, 0, ref.ADAM, flags, consts, *states[0]))
+    ctxs = [ld.Context(sizes, density_ppm=ppm, ckpt_dir=d, world=world, rank=r, batch_size=b, optim=ld.ADAM)
+            for r in range(world)]
+    switch_at = T - 1          # iterations T-1, T go in record mode (the accumulated batch in flight is cut)
+    for c in ctxs:
+        c.set_batch_mode(ld.BATCH_ACCUMULATED)
+    for t in range(1, T + 1):
+        gd = torch.from_numpy(gath[t].view(np.int32)).to(DEV)
+        if t == switch_at:
+            for c in ctxs:
+                c.set_batch_mode(ld.BATCH_RECORD)
+        for r in range(world):
+            ctxs[r].union_persist(t, ld.derive_step_scalars(t, lr), gd)
+    K = ctxs[0].K
+    batches = [list(range(f, min(switch_at - 1, f + b - 1) + 1)) for f in range(1, switch_at, b)]
+    for r in range(world):
+        ctxs[r].sync()
+        lo, hi = psi * r // world, psi * (r + 1) // world
+        for its in batches:
+            acc = ref.accumulate([ref.union_compact(gath[t], world, K, psi, lo, hi) for t in its])
+            want = ref.accum_serialize(r, world, its[0], len(its), sizes, ppm, ref.ADAM, flags, consts,
+                                       scals[its[-1]], acc)
+            got = open(os.path.join(d, ref.union_name(r, its[0])), "rb").read()
+            assert got == want, (r, its)
+        rec = [ref.union_compact(gath[t], world, K, psi, lo, hi) for t in (switch_at, T)]
+        want = ref.union_serialize(r, world, switch_at, sizes, ppm, ref.ADAM, flags, consts,
+                                   np.stack([scals[switch_at], scals[T]]), rec)
+        assert open(os.path.join(d, ref.union_name(r, switch_at)), "rb").read() == want
+    for c in ctxs:
+        c.close()
+    ends = [its[-1] for its in batches] + [switch_at, T]
+    rc = ld.Context(sizes, density_ppm=ppm, ckpt_dir=d, world=world, rank=0, optim=ld.ADAM)
+    for target in [-1, 0] + ends:
+        q, mq, vq = (torch.full((psi,), 5.0, device=DEV) for _ in range(3))
+        got_t = rc.recover_union(q, mq, vq, target=target)
+        po, mo, vo, to = ref.recover_union(d, world, sizes, ppm, target)
+        assert got_t == to == (T if target == -1 else target)
+        assert np.array_equal(q.cpu().numpy(), po) and np.array_equal(mq.cpu().numpy(), mo)
+        assert np.array_equal(vq.cpu().numpy(), vo)
+        if b > 1 and to >= b:
+            assert not np.array_equal(po, states[to][0])      # inexact (R-30)
+    inner = [t for t in range(1, switch_at) if t not in ends]
+    for target in inner[:2]:
+        with pytest.raises(ld.LowDiffError) as e:
+            rc.recover_union(q, mq, vq, target=target)
+        assert e.value.code == ld.lowdiff.E_GAP
+    rc.close()
+    po, _, vo, _ = ref.recover_union(d, world, sizes, ppm, -1)
+    for r in range(world):
+        sc_ctx = ld.Context(sizes, density_ppm=ppm, ckpt_dir=d, world=world, rank=r, optim=ld.ADAM)
+        q, mq, vq = (torch.full((psi,), 5.0, device=DEV) for _ in range(3))
+        assert sc_ctx.recover_union(q, mq, vq, sharded=True) == T
+        lo, hi = psi * r // world, psi * (r + 1) // world
+        qn = q.cpu().numpy()
+        assert np.array_equal(qn[lo:hi], po[lo:hi]) and np.array_equal(vq.cpu().numpy()[lo:hi], vo[lo:hi])
+        assert np.all(qn[:lo] == 5.0) and np.all(qn[hi:] == 5.0)
+        sc_ctx.close()
