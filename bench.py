@@ -369,13 +369,12 @@ def run_ours(args):
             kern[name] = {"ms_per_launch": tot / n, "launches": n, "share_of_step": tot / n_prof / (ms / args.steps)}
     ctx.prof_enable(False)
     # per-layer miss trace (lowdiff_compress_trace after each call of a further untimed run of the
-    # same loop): which large layers left the speculative band, and at which refill level
+    # same loop): which large layers left the speculative band and were refilled
     trace_calls = []
     for _ in range(max(args.trace_calls, 0)):
         step()
         _, lev, cand, _ = ctx.compress_trace()
-        trace_calls.append({"level1": int((lev == 1).sum()), "level2": int((lev == 2).sum()),
-                            "direct_segments": ctx.stats()["direct_segments"]})
+        trace_calls.append({"refilled": int((lev == 1).sum()), "direct_segments": ctx.stats()["direct_segments"]})
     ctx.sync()
     st = ctx.stats()
     ms_step = ms / args.steps
@@ -857,9 +856,8 @@ def run_ours(args):
             "replica": replica, "snapshot": snapshot, "union": union, "recovery_files": recovery_files,
             "spec": {"hits": st["spec_hits"], "misses": st["spec_misses"],
                      "trace": {"calls": len(trace_calls),
-                               "calls_with_a_miss": sum(1 for t in trace_calls if t["level1"] + t["level2"]),
-                               "level1_layers": sum(t["level1"] for t in trace_calls),
-                               "level2_layers": sum(t["level2"] for t in trace_calls),
+                               "calls_with_a_miss": sum(1 for t in trace_calls if t["refilled"]),
+                               "refilled_layers": sum(t["refilled"] for t in trace_calls),
                                "direct_segments_per_call": [t["direct_segments"] for t in trace_calls]}},
             "scratch": {"compress_scratch_bytes": st["compress_scratch_bytes"],
                         "compress_scratch_bytes_per_param": st["compress_scratch_bytes"] / psi,

@@ -418,7 +418,8 @@ lowdiff_status lowdiff_get_stats(const lowdiff_ctx *ctx, lowdiff_stats *out);
 /* Per-layer trace of the last lowdiff_compress (synchronises the device): for each of the
  * n_large layers above 4096 elements (in layer-table order; *n_large receives the count, arrays
  * may be NULL to query it): layer[i] = its layer id, level[i] = 0 selected from the speculative
- * band, 1 level-1 refill (rescan at the safe threshold), 2 level-2 refill (every element),
+ * band, 1 refilled (a histogram pass over the layer, then a rescan at the lower edge of the
+ * digit-0 bin (key bits [30:20]) holding the k-th key: at least k candidates by construction),
  * candidates[i] = keys admitted at the threshold finally used, threshold[i] = that threshold key. */
 lowdiff_status lowdiff_compress_trace(lowdiff_ctx *ctx, int32_t cap, int32_t *n_large, int32_t *layer,
                                       int32_t *level, uint32_t *candidates, uint32_t *threshold);

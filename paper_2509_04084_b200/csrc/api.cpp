@@ -174,19 +174,17 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   P.cs = ld::compress_seg_capacity(c->cfg.density_ppm);
   if ((st = dalloc(c, nc * ld::kSegsPerChunk * (size_t)P.cs * sizeof(uint64_t), &p))) return st; P.cand = (uint64_t*)p;
   if ((st = dalloc(c, nc * ld::kSegsPerChunk * sizeof(uint32_t), &p))) return st; P.seg_count = (uint32_t*)p;
-  if ((st = dalloc(c, nc * 4 * 4, &p))) return st;
+  if ((st = dalloc(c, nc * 4 * 3, &p))) return st;
   P.chunk_count = (uint32_t*)p; P.chunk_dm = P.chunk_count + nc; P.refill_list = P.chunk_dm + nc;
-  P.refill_list2 = P.refill_list + nc;
   if ((st = dalloc(c, nl * (2048 + 2048 + 512) * 4, &p))) return st; P.hist = (uint32_t*)p;
   if ((st = dalloc(c, nl * sizeof(ld::LayerSel), &p))) return st; P.sel = (ld::LayerSel*)p;
   CK(cudaMemset(P.sel, 0, nl * sizeof(ld::LayerSel)));   // band = 0: not yet adapted
-  if ((st = dalloc(c, nl * 4 * 7, &p))) return st;
+  if ((st = dalloc(c, nl * 4 * 6, &p))) return st;
   P.thr = (uint32_t*)p; P.thr_used = P.thr + nl; P.sel_T = P.thr_used + nl; P.layer_total = P.sel_T + nl;
-  P.sel_cut = P.layer_total + nl; P.thr_safe = P.sel_cut + nl; P.trace = P.thr_safe + nl;
-  CK(cudaMemset(P.layer_total, 0, nl * 4 * 4));
+  P.sel_cut = P.layer_total + nl; P.trace = P.sel_cut + nl;
+  CK(cudaMemset(P.layer_total, 0, nl * 4 * 3));   // layer_total, sel_cut, trace
   if ((st = dalloc(c, (size_t)nc * 8, &p))) return st; P.chunk_state = (unsigned long long*)p;
   CK(cudaMemset(P.thr, 0xFF, nl * 4));   // no speculative band before the first call
-  CK(cudaMemset(P.thr_safe, 0xFF, nl * 4));
   CK(cudaMemset(P.sel_T, 0xFF, nl * 4));  // no previous k-th key (no drift estimate yet)
   CK(cudaMemset(P.thr_used, 0, nl * 4));
   if ((st = dalloc(c, 8 * 4, &p))) return st; P.counters = (uint32_t*)p;

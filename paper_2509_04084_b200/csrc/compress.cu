@@ -23,8 +23,9 @@
 //     prep:   warp per chunk: compacts its stored segment lists in place into one index-ordered
 //             chunk list, and histograms the first radix digit (key bits [30:20]) of its candidates.
 //     plan:   per layer, #candidates >= k_l means the exact top-k lies inside the band (hit);
-//             otherwise a refill: level 1 rescans the layer at a lower ("safe") threshold, level 2
-//             makes every segment DIRECT at threshold 0 (no candidate storage).
+//             otherwise a refill: a histogram pass over the layer's acc finds the digit-0 bin of
+//             the k-th key, and the layer is rescanned at that bin's lower edge (>= k candidates
+//             by construction, about k + the bin's population).
 //     digits: two more radix digits over the candidates -> the exact k-th key T and the number of
 //             ties at T to take (lowest indices first).
 //     count+emit: a warp per chunk counts key > T and key == T, takes its layer offset and the ties
@@ -481,7 +482,34 @@ __device__ __forceinline__ void visit_direct(const DevPlan& P, const float* __re
   }
 }
 
-// Level-1 refill: the chunks of refill_list (count counters[0]) are rescanned at their layer's
+// Refill, pass 1: the digit-0 histogram (key bits [30:20]) of EVERY element of the listed chunks'
+// acc (r when EF, else g), one CTA per listed chunk at a time (persistent grid), 8 warps x 2
+// segments, aggregated in shared memory and added to the layer's histogram row (zeroed by the
+// plan).  Find mode 5 then picks the bin of the k-th key.
+__global__ void __launch_bounds__(256) refill_hist_kernel(DevPlan P, const float* __restrict__ src) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint32_t sh[kH0];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n_items = P.counters[0];
+  for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const int ch = (int)P.refill_list[w];
+    for (int b = threadIdx.x; b < kH0; b += 256) sh[b] = 0;
+    __syncthreads();
+#pragma unroll 1
+    for (int seg = warp; seg < kSegsPerChunk; seg += 8)
+      visit_direct(P, src, ch, seg, 0u, lane, [&](bool ok, uint32_t bits, uint32_t) {
+        warp_hist_add(sh, ok, (bits >> 20) & 0x7FFu);
+      });
+    __syncthreads();
+    uint32_t* hrow = P.hist + (uint64_t)P.chunk_slot[ch] * kHistRow;
+    for (int b = threadIdx.x; b < kH0; b += 256)
+      if (sh[b]) atomicAdd(&hrow[b], sh[b]);
+    __syncthreads();
+  }
+}
+
+// Refill, pass 2: the chunks of refill_list (count counters[0]) are rescanned at their layer's
 // thr_used (acc re-read: r when EF, else g); a persistent grid over 4 pieces x the listed chunks.
 template <bool EF>
 __global__ void __launch_bounds__(kScanWarps * 32, LD_SCAN_MINB)
@@ -505,7 +533,10 @@ rescan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
                                                               sbuf_all[warp], (uint32_t)seg * kSeg, lo, hi,
                                                               (uint32_t)cbase, P.thr_used[slot], 0xFFFFFFFFu, 0u,
                                                               lane, lt, bad);
-    if (lane == 0) P.seg_count[segid] = run > cs ? (run | kDirect) : run;
+    if (lane == 0) {
+      P.seg_count[segid] = run > cs ? (run | kDirect) : run;
+      if (run > cs) atomicAdd(&P.counters[5], 1u);   // DIRECT segments (stats)
+    }
   }
 }
 
@@ -516,17 +547,16 @@ rescan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
 // radix digit (key bits [30:20]) of its candidates: the stored ones, and those of its DIRECT
 // segments read from acc (src) at the layer's threshold -- in shared memory when all chunks of the
 // CTA belong to one layer (chunk slots are monotone), else directly.
-// mode 0: every chunk (after the scan); 1: chunks of level-1 layers (after their rescan);
-// 2: chunks of level-2 layers -- every segment becomes DIRECT at threshold 0 (no storage).
-// Modes 1 / 2 walk their refill list (the layers' chunks, listed contiguously) with a small
-// persistent grid, so an empty list costs only the launch.
+// mode 0: every chunk (after the scan); 1: chunks of refilled layers (after their rescan), walking
+// the refill list (the layers' chunks, listed contiguously) with a small persistent grid, so an
+// empty list costs only the launch.
 __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, const float* __restrict__ src, int mode) {
   pdl_wait();
   pdl_trigger();
   __shared__ uint32_t sh[kH0];
   __shared__ uint32_t s_tot;
-  const uint32_t n_items = mode == 0 ? (uint32_t)P.n_chunks : P.counters[mode == 1 ? 0 : 4];
-  const uint32_t* list = mode == 1 ? P.refill_list : P.refill_list2;
+  const uint32_t n_items = mode == 0 ? (uint32_t)P.n_chunks : P.counters[0];
+  const uint32_t* list = P.refill_list;
   const int lane = threadIdx.x & 31;
   for (uint32_t i0 = blockIdx.x * 8u; i0 < n_items; i0 += gridDim.x * 8u) {
   const uint32_t i_last = min(n_items, i0 + 8u) - 1u;
@@ -547,15 +577,7 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, const float*
     uint32_t* h0 = uniform ? sh : P.hist + (uint64_t)slot * kHistRow;
     // the threshold the chunk's candidates were taken with: the scan's band (mode 0) or the refill's
     const uint32_t thr = mode == 0 ? min(P.thr[slot], 0x7F800000u) : P.thr_used[slot];
-    uint32_t sc = lane < kSegsPerChunk ? P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] : 0u;
-    if (mode == 2) {   // level 2: every segment DIRECT (count = its valid elements)
-      const uint64_t cb = P.chunk_base[ch];
-      const uint64_t s0 = cb + (uint64_t)lane * kSeg, s1 = s0 + kSeg;
-      const uint64_t lo = P.chunk_lo[ch], hi = P.chunk_hi[ch];
-      const uint64_t nv = (lane < kSegsPerChunk && s1 > lo && s0 < hi) ? min(s1, hi) - max(s0, lo) : 0;
-      sc = lane < kSegsPerChunk ? (kDirect | (uint32_t)nv) : 0u;
-      if (lane < kSegsPerChunk) P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] = sc;
-    }
+    const uint32_t sc = lane < kSegsPerChunk ? P.seg_count[(uint64_t)ch * kSegsPerChunk + lane] : 0u;
     const bool direct = (sc & kDirect) != 0u;
     const uint32_t c = direct ? 0u : sc;
     uint32_t inc = c;
@@ -620,33 +642,29 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, const float*
 }
 
 // ---------------------------------------------------------------- per-layer plan / digit search
-#ifndef LD_L1_DROP
-#define LD_L1_DROP (1u << 21)
-#endif
-constexpr uint32_t kL1Drop = LD_L1_DROP;   // level-1 threshold step below a missed band (key units)
-
 __device__ __forceinline__ uint32_t layer_candidates(const DevPlan& P, int slot) {
   return *reinterpret_cast<volatile const uint32_t*>(P.layer_total + slot);
 }
 
-// queue every chunk of the layer for a refill at `level` (zeroes the layer's digit-0 histogram)
-__device__ void queue_refill(const DevPlan& P, int slot, int level, int c0, int c1, int lane) {
+// queue every chunk of the layer for a refill (zeroes the layer's digit-0 histogram, which the
+// refill's histogram pass then fills with every element of the layer)
+__device__ void queue_refill(const DevPlan& P, int slot, int c0, int c1, int lane) {
   uint32_t* hrow = P.hist + (uint64_t)slot * kHistRow;
   for (int b = lane; b < kH0; b += 32) hrow[b] = 0;
   if (lane == 0) {
     P.layer_total[slot] = 0;   // the refill's chunk_prep recounts every chunk
-    P.trace[slot] = (uint32_t)level;
+    P.trace[slot] = 1u;
   }
   uint32_t base = 0;
-  if (lane == 0) base = atomicAdd(&P.counters[level == 2 ? 4 : 0], (uint32_t)(c1 - c0));
+  if (lane == 0) base = atomicAdd(&P.counters[0], (uint32_t)(c1 - c0));
   base = __shfl_sync(0xFFFFFFFFu, base, 0);
-  uint32_t* list = level == 2 ? P.refill_list2 : P.refill_list;
-  for (int c = c0 + lane; c < c1; c += 32) list[base + (c - c0)] = (uint32_t)c;
+  for (int c = c0 + lane; c < c1; c += 32) P.refill_list[base + (c - c0)] = (uint32_t)c;
 }
 
-// mode 0: after the scan -- hit: digit 0; miss: queue a level-1 (or level-2) refill
-// mode 1: after the level-1 rescan -- hit: digit 0; still short: queue level 2
-// mode 4: after the level-2 prep -- digit 0 (every element a candidate)
+// mode 0: after the scan -- hit: digit 0; miss: queue a refill
+// mode 5: after the refill's histogram pass -- the refill threshold: the lower edge of the digit-0
+//         bin holding the k-th key (every element at or above it is a candidate: >= k of them)
+// mode 1: after the refill's rescan + prep -- digit 0 (a hit by construction)
 // mode 2/3: digit 1/2 for every large layer (mode 2 also predicts the next call's band)
 __global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
   pdl_wait();
@@ -678,45 +696,33 @@ __global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
         atomicAdd(&P.counters[3], tot);
       }
     } else {
-      // missed.  Level 1 rescans at the lower of the safe threshold (this distribution's band,
-      // without the drift share) and the missed threshold lowered by a quarter binade (x0.75-0.875
-      // in value); level 2 (every element) only when neither exists.  Rescanning at the safe
-      // threshold alone escalated most misses to level 2 (~4 passes over the layer's acc): the
-      // safe band sits only a few percent below the missed one.
-      const uint32_t th = P.thr[slot], ts = P.thr_safe[slot];
-      uint32_t l1 = ts < th ? ts : 0xFFFFFFFFu;
-      if (th != 0xFFFFFFFFu && th > kL1Drop) l1 = min(l1, min(th, 0x7F800000u) - kL1Drop);
-      const int level = l1 != 0xFFFFFFFFu ? 1 : 2;
-      if (lane == 0) P.thr_used[slot] = level == 1 ? min(l1, 0x7F800000u) : 0u;   // read by the refill
-      queue_refill(P, slot, level, c0, c1, lane);
+      // missed: the exact top-k is not inside the band.  The refill histograms every element of
+      // the layer (refill_hist_kernel), then rescans at the digit-0 bin of the k-th key (mode 5).
+      queue_refill(P, slot, c0, c1, lane);
       if (lane == 0) {
-        S.refill = (uint32_t)level;
+        S.refill = 1;
         S.total = (uint32_t)(P.layer_off[li + 1] - P.layer_off[li]);
         S.alpha *= 0.5f;                          // the drift prediction overshot
-        if (level == 2) S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : kBandAim;   // widen
         atomicAdd(&P.counters[2], 1u);
       }
     }
+  } else if (mode == 5) {
+    if (S.refill != 1) return;
+    uint32_t bin, above;
+    warp_find_bin(hrow, kH0, k, &bin, &above);   // the full digit-0 histogram of the layer
+    __syncwarp();
+    for (int b = lane; b < kH0; b += 32) hrow[b] = 0;   // chunk_prep (mode 1) histograms the candidates
+    if (lane == 0) P.thr_used[slot] = bin << 20;        // keys >= bin << 20: above + h[bin] >= k of them
   } else if (mode == 1) {
     if (S.refill != 1) return;
     const uint32_t tot = layer_candidates(P, slot);
-    if (tot >= k) {
-      uint32_t bin, above;
-      warp_find_bin(hrow, kH0, k, &bin, &above);
-      if (lane == 0) { S.prefix = bin; S.kleft = k - above; S.total = tot; }
-    } else {
-      if (lane == 0) P.thr_used[slot] = 0u;
-      queue_refill(P, slot, 2, c0, c1, lane);
-      if (lane == 0) {
-        S.refill = 2;
-        S.band = S.band > 0.f ? fminf(4.f, S.band * 2.f) : kBandAim;
-      }
+    if (tot < k) {   // impossible: the rescan admits exactly the elements the histogram counted
+      if (lane == 0) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)li); }
+      return;
     }
-  } else if (mode == 4) {
-    if (S.refill != 2) return;
     uint32_t bin, above;
     warp_find_bin(hrow, kH0, k, &bin, &above);
-    if (lane == 0) { S.prefix = bin; S.kleft = k - above; }
+    if (lane == 0) { S.prefix = bin; S.kleft = k - above; S.total = tot; }
   } else {
     const int nb = mode == 2 ? kH1 : kH2;
     const uint32_t* h = hrow + (mode == 2 ? kH0 : kH0 + kH1);
@@ -728,7 +734,8 @@ __global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
       // bin).  Only a prediction -- the next call checks #candidates >= k_l and refills otherwise.
       const float band = S.band > 0.f ? S.band : kBandAim;
       const uint32_t C = max(k + 32u, (uint32_t)fminf((float)k * band, 4.0e9f));
-      uint32_t nt = P.thr[slot];
+      // (a refilled layer's fallback is its refill threshold, which admitted >= k_l this call)
+      uint32_t nt = S.refill ? P.thr_used[slot] : P.thr[slot];
       if (S.total >= C) {
         uint32_t b0, a0;
         warp_find_bin(hrow, kH0, C, &b0, &a0);
@@ -1003,11 +1010,10 @@ __global__ void __launch_bounds__(256, 8) count_emit_kernel(DevPlan P, const flo
   const bool last_tie_chunk = take > 0 && take_b + take == need;
   if (ch == c0 && lane == 0) {
     P.sel_T[slot] = T;
-    // speculative band for the next call: the drift-led threshold (may exceed T)
-    // and the safe one (never above this call's T) that a level-1 refill falls back to
+    // speculative band for the next call: the drift-led threshold (may exceed T),
+    // never below the band without the lead capped at this call's T
     const uint32_t ns = P.sel[slot].next_safe;
     const uint32_t sf = ns <= T ? ns : T;
-    P.thr_safe[slot] = sf;
     P.thr[slot] = max(sf, P.sel[slot].next_thr);
   }
   const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + gt_b + take_b;
@@ -1088,8 +1094,8 @@ int compress_seg_capacity(uint32_t ppm) {
   return cs < 32 ? 32 : cs > kSeg ? kSeg : cs;
 }
 
-// lowdiff_compress: small layers (forked stream) | scan -> chunk prep -> plan -> level-1 refill
-// (rescan, prep, plan) -> level-2 refill (prep, plan) -> digit 1 -> digit 2 -> count+emit, join.
+// lowdiff_compress: small layers (forked stream) | scan -> chunk prep -> plan -> refill (histogram,
+// threshold, rescan, prep, plan) -> digit 1 -> digit 2 -> count+emit, join.
 // The refill kernels exit at once when nothing was queued; the CUDA-graph form captures the same
 // sequence.  Short kernels use programmatic dependent launch (pdl.cuh).
 cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, uint32_t* send, cudaStream_t s) {
@@ -1146,16 +1152,15 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   const bool pdl = !c->prof;   // programmatic launches (pdl.cuh); profiling events sit between kernels
   if ((e = launch_pdl(pdl, chunk_prep_kernel, chunk_blocks, 256, 0, s, P, src, 0)) != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 0)) != cudaSuccess) return e;
-  // level-1 refill: rescan the queued chunks at the safe threshold, prep them, plan again
+  // refill of the missed layers: histogram pass, threshold, rescan at it, prep, plan
   const unsigned rgrid = (unsigned)num_sms() * 4;   // refill kernels: persistent over their lists
+  if ((e = launch_pdl(pdl, refill_hist_kernel, rgrid, 256, 0, s, P, src)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 5)) != cudaSuccess) return e;
   e = ef ? launch_pdl(pdl, rescan_kernel<true>, 4 * rgrid, uK, 0, s, P, grad, residual)
          : launch_pdl(pdl, rescan_kernel<false>, 4 * rgrid, uK, 0, s, P, grad, residual);
   if (e != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, chunk_prep_kernel, rgrid, 256, 0, s, P, src, 1)) != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 1)) != cudaSuccess) return e;
-  // level-2 refill: every element of the queued layers, read directly
-  if ((e = launch_pdl(pdl, chunk_prep_kernel, rgrid, 256, 0, s, P, src, 2)) != cudaSuccess) return e;
-  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 4)) != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, src, 1)) != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 2)) != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, src, 2)) != cudaSuccess) return e;

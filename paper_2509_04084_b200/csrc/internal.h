@@ -43,10 +43,10 @@ struct LayerSel {
   uint32_t prefix;   // key bits fixed by the digits done so far
   uint32_t kleft;    // entries still to take among those matching prefix
   uint32_t total;    // candidate count
-  uint32_t refill;   // 1: speculative band too narrow, whole layer became candidates
+  uint32_t refill;   // 1: speculative band too narrow, the layer was refilled (histogram + rescan)
   uint32_t next_thr; // speculative band for the next call (drift-led)
   float band;        // band width as a multiple of k_l in this call's distribution (adaptive; 0 = unset)
-  uint32_t next_safe;// the same band without the drift lead (level-1 refill threshold)
+  uint32_t next_safe;// the same band without the drift lead
   float alpha;       // share of the last drift of T the next band leads by (adaptive)
   uint32_t drift;    // this layer's last upward drift of T (key units; 0 = none or downward)
 };
@@ -83,14 +83,12 @@ struct DevPlan {
   // {key(r) > sel_T} U {key(r) == sel_T and index < sel_cut}; the next scan zeroes it on the fly
   uint32_t* sel_T;               // [n_large] previous call's exact k-th key
   uint32_t* sel_cut;             // [n_large] one past the global index of the last tie it took
-  uint32_t* refill_list;         // [n_chunks] chunks to rescan at their layer's safe threshold (level 1)
-  uint32_t* refill_list2;        // [n_chunks] chunks whose segments all become DIRECT (level 2)
-  uint32_t* trace;               // [n_large] this call's path per layer: 0 hit, 1 level-1, 2 level-2
-  uint32_t* thr_safe;            // [n_large] the band without the drift lead
+  uint32_t* refill_list;         // [n_chunks] chunks of the missed layers (histogram pass + rescan)
+  uint32_t* trace;               // [n_large] this call's path per layer: 0 hit, 1 refill
   unsigned long long* chunk_state;  // [n_chunks] count_emit look-back: status | eq_incl | gt_incl
-  uint32_t* counters;            // [0] level-1 refills, [1] spec hits, [2] spec misses,
-                                 // [3] candidates of hit layers, [4] level-2 refills,
-                                 // [5] DIRECT segments of the scan (more than cs candidates)
+  uint32_t* counters;            // [0] chunks queued for a refill, [1] spec hits, [2] spec misses,
+                                 // [3] candidates of hit layers, [4] unused,
+                                 // [5] DIRECT segments of the scan and the rescan (more than cs candidates)
   uint32_t* err;                 // [0] non-finite flag, [1] first bad layer
 };
 
