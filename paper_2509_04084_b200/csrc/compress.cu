@@ -325,7 +325,7 @@ __device__ __forceinline__ uint32_t scan_segment(const float* __restrict__ gc, f
     }
     __syncwarp();
   };
-  constexpr bool kPF = !RESCAN;   // issue round r+1's loads before round r is processed
+  constexpr bool kPF = true;   // issue round r+1's loads before round r is processed
   float4 gn = make_float4(0.f, 0.f, 0.f, 0.f), rn = gn;
   uint32_t vn = 0;
   if (kPF) load(0, gn, rn, vn);
@@ -483,24 +483,46 @@ __device__ __forceinline__ void visit_direct(const DevPlan& P, const float* __re
 }
 
 // Refill, pass 1: the digit-0 histogram (key bits [30:20]) of EVERY element of the listed chunks'
-// acc (r when EF, else g), one CTA per listed chunk at a time (persistent grid), 8 warps x 2
-// segments, aggregated in shared memory and added to the layer's histogram row (zeroed by the
-// plan).  Find mode 5 then picks the bin of the k-th key.
+// acc (r when EF, else g), one CTA per listed chunk at a time (persistent grid).  Each thread keeps
+// four 128-bit loads in flight (16 per chunk); the counts go straight to a shared-memory histogram
+// (same-bin lanes serialise in the atomic unit, cheaper than aggregating them first) that is added
+// to the layer's histogram row (zeroed by the plan).  Find mode 5 then picks the k-th key's bin.
 __global__ void __launch_bounds__(256) refill_hist_kernel(DevPlan P, const float* __restrict__ src) {
   pdl_wait();
   pdl_trigger();
   __shared__ uint32_t sh[kH0];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kV = kChunk / 4 / 256;   // float4 per thread per chunk (16)
   const uint32_t n_items = P.counters[0];
   for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x) {
     const int ch = (int)P.refill_list[w];
+    const uint64_t cbase = P.chunk_base[ch];
+    const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
+    const float* sp = src + cbase;
     for (int b = threadIdx.x; b < kH0; b += 256) sh[b] = 0;
     __syncthreads();
 #pragma unroll 1
-    for (int seg = warp; seg < kSegsPerChunk; seg += 8)
-      visit_direct(P, src, ch, seg, 0u, lane, [&](bool ok, uint32_t bits, uint32_t) {
-        warp_hist_add(sh, ok, (bits >> 20) & 0x7FFu);
-      });
+    for (int v0 = 0; v0 < kV; v0 += 4) {
+      float4 a[4];
+      uint32_t vm[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t e0 = 4u * ((v0 + u) * 256 + threadIdx.x);
+        vm[u] = 0;
+        a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e0 >= lo && e0 + 4 <= hi) {
+          vm[u] = 0xF;
+          a[u] = *reinterpret_cast<const float4*>(sp + e0);
+        } else if (e0 + 4 > lo && e0 < hi) {
+          for (int k = 0; k < 4; ++k)
+            if (e0 + k >= lo && e0 + k < hi) { vm[u] |= 1u << k; f4set(a[u], k, sp[e0 + k]); }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if ((vm[u] >> k) & 1u) atomicAdd(&sh[(__float_as_uint(f4get(a[u], k)) >> 20) & 0x7FFu], 1u);
+    }
     __syncthreads();
     uint32_t* hrow = P.hist + (uint64_t)P.chunk_slot[ch] * kHistRow;
     for (int b = threadIdx.x; b < kH0; b += 256)
