@@ -487,14 +487,11 @@ __device__ __forceinline__ void visit_direct(const DevPlan& P, const float* __re
 // four 128-bit loads in flight (16 per chunk); the counts go straight to a shared-memory histogram
 // (same-bin lanes serialise in the atomic unit, cheaper than aggregating them first) that is added
 // to the layer's histogram row (zeroed by the plan).  Find mode 5 then picks the k-th key's bin.
-__global__ void __launch_bounds__(256) refill_hist_kernel(DevPlan P, const float* __restrict__ src) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ uint32_t sh[kH0];
+// CTA-level (256 threads); sh: kH0 words of shared memory.
+__device__ __forceinline__ void refill_hist_chunk(const DevPlan& P, const float* __restrict__ src, int ch,
+                                                  uint32_t* sh) {
   constexpr int kV = kChunk / 4 / 256;   // float4 per thread per chunk (16)
-  const uint32_t n_items = P.counters[0];
-  for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-    const int ch = (int)P.refill_list[w];
+  {
     const uint64_t cbase = P.chunk_base[ch];
     const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
     const float* sp = src + cbase;
@@ -531,20 +528,13 @@ __global__ void __launch_bounds__(256) refill_hist_kernel(DevPlan P, const float
   }
 }
 
-// Refill, pass 2: the chunks of refill_list (count counters[0]) are rescanned at their layer's
-// thr_used (acc re-read: r when EF, else g); a persistent grid over 4 pieces x the listed chunks.
+// Refill, pass 2: segment `seg` of chunk ch is rescanned at its layer's thr_used (acc re-read: r
+// when EF, else g) into its slot (warp-level; sbuf: the warp's kCandBuf staging entries).
 template <bool EF>
-__global__ void __launch_bounds__(kScanWarps * 32, LD_SCAN_MINB)
-rescan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ uint64_t sbuf_all[kScanWarps][kCandBuf];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ void rescan_segment(const DevPlan& P, const float* __restrict__ g, float* __restrict__ r,
+                                               int ch, int seg, uint64_t* sbuf, int lane) {
   const unsigned lt = (1u << lane) - 1u;
-  const uint32_t n_items = P.counters[0] * kPiecesPerChunk;
-  for (uint32_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-    const int ch = (int)P.refill_list[w / kPiecesPerChunk];
-    const int seg = (int)(w % kPiecesPerChunk) * kScanWarps + warp;
+  {
     const uint64_t cbase = P.chunk_base[ch];
     const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
     const int slot = P.chunk_slot[ch];
@@ -552,7 +542,7 @@ rescan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
     const uint32_t cs = (uint32_t)P.cs;
     bool bad = false;
     const uint32_t run = scan_segment<EF, true, false, false>(g + cbase, r + cbase, seg_slot(P, segid), cs, nullptr,
-                                                              sbuf_all[warp], (uint32_t)seg * kSeg, lo, hi,
+                                                              sbuf, (uint32_t)seg * kSeg, lo, hi,
                                                               (uint32_t)cbase, P.thr_used[slot], 0xFFFFFFFFu, 0u,
                                                               lane, lt, bad);
     if (lane == 0) {
@@ -570,17 +560,13 @@ rescan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r) {
 // segments read from acc (src) at the layer's threshold -- in shared memory when all chunks of the
 // CTA belong to one layer (chunk slots are monotone), else directly.
 // mode 0: every chunk (after the scan); 1: chunks of refilled layers (after their rescan), walking
-// the refill list (the layers' chunks, listed contiguously) with a small persistent grid, so an
-// empty list costs only the launch.
-__global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, const float* __restrict__ src, int mode) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ uint32_t sh[kH0];
-  __shared__ uint32_t s_tot;
-  const uint32_t n_items = mode == 0 ? (uint32_t)P.n_chunks : P.counters[0];
+// the refill list (the layers' chunks, listed contiguously).  One round = items i0 .. i0 + 7 (a warp
+// each), CTA-level (256 threads); sh: kH0 words of shared memory, s_tot one more.
+__device__ __forceinline__ void chunk_prep_round(const DevPlan& P, const float* __restrict__ src, int mode,
+                                                 uint32_t i0, uint32_t n_items, uint32_t* sh, uint32_t* s_tot) {
   const uint32_t* list = P.refill_list;
   const int lane = threadIdx.x & 31;
-  for (uint32_t i0 = blockIdx.x * 8u; i0 < n_items; i0 += gridDim.x * 8u) {
+  {
   const uint32_t i_last = min(n_items, i0 + 8u) - 1u;
   const int c_first = mode == 0 ? (int)i0 : (int)list[i0];
   const int c_last = mode == 0 ? (int)i_last : (int)list[i_last];
@@ -590,7 +576,7 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, const float*
   if (uniform) {
     __syncthreads();   // the previous round's flush has read sh
     for (int b = threadIdx.x; b < kH0; b += 256) sh[b] = 0;
-    if (threadIdx.x == 0) s_tot = 0;
+    if (threadIdx.x == 0) *s_tot = 0;
     __syncthreads();
   }
   const int slot = P.chunk_slot[ch];
@@ -649,7 +635,7 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, const float*
     if (lane == 0) {
       P.chunk_count[ch] = total;
       P.chunk_dm[ch] = dm;
-      if (uniform) atomicAdd(&s_tot, total + dcnt);
+      if (uniform) atomicAdd(s_tot, total + dcnt);
       else atomicAdd(&P.layer_total[slot], total + dcnt);   // per-layer candidate count
     }
   }
@@ -658,9 +644,19 @@ __global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, const float*
     uint32_t* hrow = P.hist + (uint64_t)P.chunk_slot[c_first] * kHistRow;
     for (int b = threadIdx.x; b < kH0; b += 256)
       if (sh[b]) atomicAdd(&hrow[b], sh[b]);
-    if (threadIdx.x == 0 && s_tot) atomicAdd(&P.layer_total[P.chunk_slot[c_first]], s_tot);
+    if (threadIdx.x == 0 && *s_tot) atomicAdd(&P.layer_total[P.chunk_slot[c_first]], *s_tot);
   }
   }
+}
+
+// chunk prep of every chunk after the scan (mode 0)
+__global__ void __launch_bounds__(256) chunk_prep_kernel(DevPlan P, const float* __restrict__ src) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint32_t sh[kH0];
+  __shared__ uint32_t s_tot;
+  for (uint32_t i0 = blockIdx.x * 8u; i0 < (uint32_t)P.n_chunks; i0 += gridDim.x * 8u)
+    chunk_prep_round(P, src, 0, i0, (uint32_t)P.n_chunks, sh, &s_tot);
 }
 
 // ---------------------------------------------------------------- per-layer plan / digit search
@@ -688,12 +684,8 @@ __device__ void queue_refill(const DevPlan& P, int slot, int c0, int c1, int lan
 //         bin holding the k-th key (every element at or above it is a candidate: >= k of them)
 // mode 1: after the refill's rescan + prep -- digit 0 (a hit by construction)
 // mode 2/3: digit 1/2 for every large layer (mode 2 also predicts the next call's band)
-__global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
-  pdl_wait();
-  pdl_trigger();
-  const int slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (slot >= P.n_large) return;
+// (warp-level: one large layer per warp)
+__device__ void find_layer(const DevPlan& P, int slot, int mode, int lane) {
   const int li = P.large_layers[slot];
   const uint32_t k = P.layer_k[li];
   LayerSel& S = P.sel[slot];
@@ -787,6 +779,61 @@ __global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
     if (lane == 0) { S.prefix = (S.prefix << (mode == 2 ? 11 : 9)) | bin; S.kleft -= above; }
   }
 }
+
+__global__ void __launch_bounds__(256) find_kernel(DevPlan P, int mode) {
+  pdl_wait();
+  pdl_trigger();
+  const int slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (slot < P.n_large) find_layer(P, slot, mode, threadIdx.x & 31);
+}
+
+// Grid-wide barrier of a co-resident grid (refill_kernel): counter `bar` is zeroed per call with the
+// other counters; barrier n (1, 2, ...) releases when every CTA has arrived n times.
+__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t n) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    const uint32_t target = n * gridDim.x;
+    uint32_t v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+// The refill of the layers find mode 0 queued, one launch for the whole sequence:
+// histogram pass -> refill threshold (find mode 5) -> rescan at it -> chunk prep -> find mode 1,
+// phases separated by grid barriers (the grid is co-resident: a cooperative launch sized by the
+// occupancy).  Nothing queued -- the steady state -- is one early exit, not five empty launches.
+template <bool EF>
+__global__ void __launch_bounds__(256) refill_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r,
+                                                     const float* __restrict__ src) {
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t n = P.counters[0];   // chunks queued (written by find mode 0, before this grid)
+  if (n == 0) return;
+  __shared__ __align__(16) uint64_t smem[8 * kCandBuf];   // 10 KB: staging (rescan) or histogram
+  __shared__ uint32_t s_tot;
+  uint32_t* sh = reinterpret_cast<uint32_t*>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * 8 + warp, nw = gridDim.x * 8;
+  uint32_t* bar = P.counters + 6;
+  for (uint32_t w = blockIdx.x; w < n; w += gridDim.x) refill_hist_chunk(P, src, (int)P.refill_list[w], sh);
+  grid_barrier(bar, 1);
+  for (int slot = gw; slot < P.n_large; slot += nw) find_layer(P, slot, 5, lane);
+  grid_barrier(bar, 2);
+  for (uint32_t w = blockIdx.x; w < 2 * n; w += gridDim.x)   // half a chunk (8 segments) per CTA round
+    rescan_segment<EF>(P, g, r, (int)P.refill_list[w >> 1], (int)(w & 1) * 8 + warp, smem + warp * kCandBuf, lane);
+  grid_barrier(bar, 3);
+  for (uint32_t i0 = blockIdx.x * 8u; i0 < n; i0 += gridDim.x * 8u) chunk_prep_round(P, src, 1, i0, n, sh, &s_tot);
+  grid_barrier(bar, 4);
+  for (int slot = gw; slot < P.n_large; slot += nw) find_layer(P, slot, 1, lane);
+}
+
 
 // digit d (1 or 2) histogram over the candidates matching the prefix (the chunk list + its DIRECT
 // segments' acc): warp per chunk, 8 chunks per CTA aggregated in shared memory when they belong
@@ -1172,17 +1219,20 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   int hs;
   prof_begin(c, "select", s, &hs);
   const bool pdl = !c->prof;   // programmatic launches (pdl.cuh); profiling events sit between kernels
-  if ((e = launch_pdl(pdl, chunk_prep_kernel, chunk_blocks, 256, 0, s, P, src, 0)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, chunk_prep_kernel, chunk_blocks, 256, 0, s, P, src)) != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 0)) != cudaSuccess) return e;
-  // refill of the missed layers: histogram pass, threshold, rescan at it, prep, plan
-  const unsigned rgrid = (unsigned)num_sms() * 4;   // refill kernels: persistent over their lists
-  if ((e = launch_pdl(pdl, refill_hist_kernel, rgrid, 256, 0, s, P, src)) != cudaSuccess) return e;
-  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 5)) != cudaSuccess) return e;
-  e = ef ? launch_pdl(pdl, rescan_kernel<true>, 4 * rgrid, uK, 0, s, P, grad, residual)
-         : launch_pdl(pdl, rescan_kernel<false>, 4 * rgrid, uK, 0, s, P, grad, residual);
+  // refill of the missed layers: histogram pass, threshold, rescan at it, prep, plan (one launch)
+  static int refill_grid[2] = {0, 0};
+  if (!refill_grid[ef]) {
+    int per_sm = 0;
+    e = ef ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refill_kernel<true>, 256, 0)
+           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refill_kernel<false>, 256, 0);
+    if (e != cudaSuccess) return e;
+    refill_grid[ef] = num_sms() * std::max(1, std::min(per_sm, 4));
+  }
+  e = ef ? launch_pdl_ex(pdl, true, refill_kernel<true>, refill_grid[1], 256, 0, s, P, grad, residual, src)
+         : launch_pdl_ex(pdl, true, refill_kernel<false>, refill_grid[0], 256, 0, s, P, grad, residual, src);
   if (e != cudaSuccess) return e;
-  if ((e = launch_pdl(pdl, chunk_prep_kernel, rgrid, 256, 0, s, P, src, 1)) != cudaSuccess) return e;
-  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 1)) != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, src, 1)) != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 2)) != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, src, 2)) != cudaSuccess) return e;
@@ -1193,7 +1243,7 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
     return e;
   prof_end(c, h, s);
   if (P.n_small && c->aux && (e = cudaStreamWaitEvent(s, c->ev_join, 0)) != cudaSuccess) return e;   // join
-  c->launches += 13;
+  c->launches += 9;
   c->lazy_residual = ef ? residual : nullptr;   // this call's large-layer selection is now pending
   return cudaGetLastError();
 }

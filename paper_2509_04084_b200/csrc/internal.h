@@ -88,7 +88,8 @@ struct DevPlan {
   unsigned long long* chunk_state;  // [n_chunks] count_emit look-back: status | eq_incl | gt_incl
   uint32_t* counters;            // [0] chunks queued for a refill, [1] spec hits, [2] spec misses,
                                  // [3] candidates of hit layers, [4] unused,
-                                 // [5] DIRECT segments of the scan and the rescan (more than cs candidates)
+                                 // [5] DIRECT segments of the scan and the rescan (more than cs candidates),
+                                 // [6] grid-barrier counter of the refill kernel
   uint32_t* err;                 // [0] non-finite flag, [1] first bad layer
 };
 
