@@ -139,7 +139,7 @@ merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __r
 }
 
 #ifndef LD_REPLAY_MINB
-#define LD_REPLAY_MINB 7   // resident CTAs per SM the replay is compiled for (128 threads: 72 registers)
+#define LD_REPLAY_MINB 6   // resident CTAs per SM the replay is compiled for (128 threads: 80 registers)
 #endif
 
 struct AdamK { float b1, c1, b2, c2, eps, nz; };   // nz = -0.0f (ieee_fast.cuh: opaque -0 addend)
@@ -157,32 +157,56 @@ template <int OPT> struct ReplayShape {
   static constexpr int threads = OPT == LOWDIFF_SGD ? 64 : kReplayThreads;
   static constexpr int slots = kReplayTile / (4 * threads);        // float4 slots per lane
   static constexpr int span = kReplayTile / (threads / 32);         // elements per warp
-  static constexpr int minb = OPT == LOWDIFF_SGD ? 2 * LD_REPLAY_MINB : LD_REPLAY_MINB;
+  static constexpr int minb = OPT == LOWDIFF_SGD ? 14 : LD_REPLAY_MINB;
 };
 
-// EPS: Adam's eps lies in adam_u_fast's window [2^-60, 2^59] (checked on the host; false: every
-// group takes the intrinsics) -- a template flag, so the per-group test needs no predicate register
-template <int OPT, int DIV, int MAXW, bool EPS>
-__global__ void __launch_bounds__(ReplayShape<OPT>::threads,
-                                  MAXW >= 8 ? ReplayShape<OPT>::minb * 3 / 4 : ReplayShape<OPT>::minb)
-replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t n_steps,
-              const uint32_t* __restrict__ start, int64_t n_tiles, const float* __restrict__ scal,
-              AdamK ak, uint64_t lo, uint64_t hi, int64_t tile0, float* __restrict__ p, float* __restrict__ m,
-              float* __restrict__ v) {
+struct ReplayArgs {
+  const uint32_t* diffs;
+  int world;
+  uint64_t K;
+  int64_t n_steps;
+  const uint32_t* start;
+  int64_t n_tiles;
+  const float* scal;
+  AdamK ak;
+  uint64_t lo, hi;
+  int64_t tile0;
+  float *p, *m, *v;
+  uint32_t* fix_list;        // [n_tiles * warps] (tile << 8 | region) of regions to re-run exactly
+  unsigned int* fix_count;
+};
+
+// The replay of one warp's region (region `wreg` of tile tl of the window), G_t built in the warp's
+// shared-memory slice Gw.  SAFE = false: Adam's sqrt / division take the branch-free fast
+// sequences (ieee_fast.cuh) with their operand windows folded into a WinAcc; if any operand of any
+// step left the windows, nothing is written and the region is queued for an exact re-run
+// (replay_fix_kernel).  SAFE = true: the intrinsics throughout (that re-run, or an eps outside the
+// fast window).  Either way the written bits are the sequential R-11 recurrence.
+template <int OPT, int DIV, int MAXW, bool SAFE>
+__device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, int wreg, float* Gw, int lane) {
   // elements [lo, hi) are replayed; p, m, v hold exactly that range (p[0] is element lo)
   constexpr int kReplaySlots = ReplayShape<OPT>::slots, kWarpSpan = ReplayShape<OPT>::span;
   static_assert(kWarpSpan == 128 * kReplaySlots, "one float4 per lane per slot");
-  __shared__ __align__(16) float G[kReplayTile];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t t = tile0 + blockIdx.x;
+  const uint32_t* __restrict__ diffs = A.diffs;
+  const int world = A.world;
+  const uint64_t K = A.K;
+  const int64_t n_steps = A.n_steps;
+  const uint32_t* __restrict__ start = A.start;
+  const float* __restrict__ scal = A.scal;
+  const AdamK ak = A.ak;
+  const uint64_t lo = A.lo, hi = A.hi;
+  float* __restrict__ p = A.p;
+  float* __restrict__ m = A.m;
+  float* __restrict__ v = A.v;
+  const int64_t t = A.tile0 + tl;
   const uint64_t j0 = (uint64_t)t * kReplayTile;
-  const uint32_t wb = (uint32_t)warp * kWarpSpan;           // the warp's region: [j0 + wb, j0 + wb + span)
+  const uint32_t wb = (uint32_t)wreg * kWarpSpan;           // the warp's region: [j0 + wb, j0 + wb + span)
   const uint32_t jw = (uint32_t)j0 + wb;                    // Psi < 2^32
-  float* Gw = G + wb;
   float4* G4w = reinterpret_cast<float4*>(Gw);
   // state in element pairs (f32x2: FADD2/FMUL2/FFMA2 do both halves in one instruction, each
   // rounded exactly like the scalar operation): pair x = 2 i + h holds elements 2h, 2h+1 of slot i
   f32x2 P2[2 * kReplaySlots], M2[2 * kReplaySlots], V2[2 * kReplaySlots];
+  bool neg_v = false;   // a negative initial v (not -0) is outside the fast windows
 #pragma unroll
   for (int i = 0; i < kReplaySlots; ++i) {
 #pragma unroll
@@ -195,6 +219,7 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
         pe[e] = in ? p[j - lo] : 0.f;
         me[e] = (OPT == LOWDIFF_ADAM && in) ? m[j - lo] : 0.f;
         ve[e] = (OPT == LOWDIFF_ADAM && in) ? v[j - lo] : 0.f;
+        neg_v |= __float_as_uint(ve[e]) > 0x80000000u;
       }
       P2[2 * i + h] = pk2(pe[0], pe[1]);
       M2[2 * i + h] = pk2(me[0], me[1]);
@@ -203,8 +228,8 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
   }
   const AdamK2 k2 = make_adamk2(ak.b1, ak.c1, ak.b2, ak.c2, ak.eps, ak.nz);
   const float n = (float)world, inv = 1.0f / (float)world;
-  const uint64_t tstride = (uint64_t)(n_tiles + 1);   // n_tiles = tiles in the window
-  const int64_t tl = blockIdx.x;                       // tile relative to the window
+  const uint64_t tstride = (uint64_t)(A.n_tiles + 1);   // n_tiles = tiles in the window
+  WinAcc win = win_init();
   // Software pipeline over steps: lane r (< 32) holds rank r's entry range of this tile for the
   // current step (ra_c, rb_c) and the next (ra_n, rb_n); the ranges of step s+2 and the first
   // round of step s+1's entries (pj, pv: entry a_r + lane of every rank < MAXW) are loaded while
@@ -220,9 +245,13 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       rb_n = __ldg(st1 + 1);
     }
   }
+  // per-step strides, advanced incrementally (no 64-bit products in the step loop)
+  const uint64_t bstride = (uint64_t)world * 2 * K;          // u32 of the blocks of one step
+  const uint64_t sstride = (uint64_t)world * tstride;        // u32 of the start table of one step
+  const uint32_t* st2 = start + 2 * sstride + (uint64_t)lane * tstride + tl;   // step s + 2, rank `lane`
+  const float* sc_n = scal + 3;                              // scalars of step s + 1
   uint32_t pj[MAXW], pv[MAXW];
-  auto load_entries = [&](int64_t x, uint32_t ra, uint32_t rb) {   // first round of step x
-    const uint32_t* blk = diffs + (uint64_t)x * world * 2 * K;
+  auto load_entries = [&](const uint32_t* blk, uint32_t ra, uint32_t rb) {   // first round of a step
 #pragma unroll
     for (int r = 0; r < MAXW; ++r) {
       pj[r] = 0xFFFFFFFFu;
@@ -238,14 +267,14 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       }
     }
   };
-  load_entries(0, ra_c, rb_c);
+  const uint32_t* blk = diffs;                               // step s
+  load_entries(blk, ra_c, rb_c);
   float lr = __ldg(scal), r1 = __ldg(scal + 1), r2 = __ldg(scal + 2);
 #pragma unroll 1
   for (int64_t s = 0; s < n_steps; ++s) {
 #pragma unroll
     for (int i = 0; i < kReplaySlots; ++i) G4w[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
-    const uint32_t* blk = diffs + (uint64_t)s * world * 2 * K;
     // rank by rank from +0: the rank-order sum of DESIGN.md R-8 (indices unique within a rank)
 #pragma unroll
     for (int r = 0; r < MAXW; ++r) {
@@ -281,16 +310,18 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
     const float slr = lr, sr1 = r1, sr2 = r2;
     uint32_t na = 0, nb = 0;
     if (s + 1 < n_steps) {
-      load_entries(s + 1, ra_n, rb_n);
-      lr = __ldg(scal + 3 * (s + 1));
-      r1 = __ldg(scal + 3 * (s + 1) + 1);
-      r2 = __ldg(scal + 3 * (s + 1) + 2);
+      load_entries(blk + bstride, ra_n, rb_n);
+      lr = __ldg(sc_n);
+      r1 = __ldg(sc_n + 1);
+      r2 = __ldg(sc_n + 2);
+      sc_n += 3;
     }
     if (lane < wr && s + 2 < n_steps) {
-      const uint32_t* st2 = start + ((uint64_t)(s + 2) * world + lane) * tstride + tl;
       na = __ldg(st2);
       nb = __ldg(st2 + 1);
     }
+    st2 += sstride;
+    blk += bstride;
     const f32x2 LR = pk2(slr, slr), R1 = pk2(sr1, sr1), R2 = pk2(sr2, sr2);
 #pragma unroll
     for (int i = 0; i < kReplaySlots; ++i) {   // float4 slots: 2 independent element pairs each
@@ -300,22 +331,16 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
       if (OPT == LOWDIFF_ADAM) {
         // m = b1*m + c1*g ; v = b2*v + c2*(g*g) ; mh = m*r1 ; vh = v*r2
         // d = sqrt(vh) + eps ; u = mh / d ; p = p - lr*u          (R-11)
-        // Correctly rounded sqrt / divide take the exact fast sequence (ieee_fast.cuh) for every
-        // lane; a warp-rare fix-up redoes out-of-window operands with the intrinsics.
-        f32x2 u[2];
-        bool s0, s1;
-        u[0] = adam2_u(M2[2 * i], V2[2 * i], g01, k2, R1, R2, &s0);
-        u[1] = adam2_u(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2, &s1);
-        if (s0 | s1 | !EPS) {   // rare: redo the group exactly with the intrinsics
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const f32x2 mh = mul2(M2[2 * i + h], R1), vh = mul2(V2[2 * i + h], R2);
-            u[h] = pk2(__fdiv_rn(lo2(mh), __fadd_rn(__fsqrt_rn(lo2(vh)), ak.eps)),
-                       __fdiv_rn(hi2(mh), __fadd_rn(__fsqrt_rn(hi2(vh)), ak.eps)));
-          }
+        f32x2 u0, u1;
+        if (SAFE) {
+          u0 = adam2_u_exact(M2[2 * i], V2[2 * i], g01, k2, R1, R2, ak.eps);
+          u1 = adam2_u_exact(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2, ak.eps);
+        } else {
+          u0 = adam2_u_agg(M2[2 * i], V2[2 * i], g01, k2, R1, R2, win);
+          u1 = adam2_u_agg(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2, win);
         }
-        P2[2 * i] = sub_prod2(P2[2 * i], LR, u[0], k2.nz);
-        P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, u[1], k2.nz);
+        P2[2 * i] = sub_prod2(P2[2 * i], LR, u0, k2.nz);
+        P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, u1, k2.nz);
       } else {
         P2[2 * i] = sub_prod2(P2[2 * i], LR, g01, k2.nz);
         P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, g23, k2.nz);
@@ -326,6 +351,12 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
     ra_n = na;
     rb_n = nb;
     __syncwarp();   // every lane has read this step's G before the next step zeroes and adds
+  }
+  if (OPT == LOWDIFF_ADAM && !SAFE) {
+    if (__any_sync(0xFFFFFFFFu, neg_v | win_bad(win))) {   // rare: re-run the region exactly
+      if (lane == 0) A.fix_list[atomicAdd(A.fix_count, 1u)] = (uint32_t)(tl << 8) | (uint32_t)wreg;
+      return;
+    }
   }
 #pragma unroll
   for (int i = 0; i < kReplaySlots; ++i) {
@@ -341,6 +372,31 @@ replay_kernel(const uint32_t* __restrict__ diffs, int world, uint64_t K, int64_t
         }
       }
     }
+  }
+}
+
+// Measured (B200, 100 GPT-2 XL steps): Adam 6 CTAs/SM (80 registers) 198 ms, 7 (72, spills) 203 ms,
+// 5 (96) 207 ms, 8 (64) 216 ms; with 8 ranks per step (MAXW 8) 6 CTAs/SM 97 ms, 5 CTAs 108 ms.
+template <int OPT, int DIV, int MAXW, bool SAFE>
+__global__ void __launch_bounds__(ReplayShape<OPT>::threads, ReplayShape<OPT>::minb)
+replay_kernel(ReplayArgs A) {
+  __shared__ __align__(16) float G[kReplayTile];
+  const int warp = threadIdx.x >> 5;
+  replay_region<OPT, DIV, MAXW, SAFE>(A, blockIdx.x, warp, G + warp * ReplayShape<OPT>::span, threadIdx.x & 31);
+}
+
+// the exact re-run of the regions replay_kernel queued (Adam only): one warp per queued region
+template <int DIV, int MAXW>
+__global__ void __launch_bounds__(ReplayShape<LOWDIFF_ADAM>::threads)
+replay_fix_kernel(ReplayArgs A) {
+  __shared__ __align__(16) float G[kReplayTile];
+  const int warp = threadIdx.x >> 5;
+  constexpr int kWarps = ReplayShape<LOWDIFF_ADAM>::threads / 32;
+  const unsigned n = *A.fix_count;
+  for (unsigned i = blockIdx.x * kWarps + warp; i < n; i += gridDim.x * kWarps) {
+    const uint32_t item = A.fix_list[i];
+    replay_region<LOWDIFF_ADAM, DIV, MAXW, true>(A, (int64_t)(item >> 8), (int)(item & 0xFFu),
+                                                 G + warp * ReplayShape<LOWDIFF_ADAM>::span, threadIdx.x & 31);
   }
 }
 
@@ -423,7 +479,8 @@ size_t merge_scratch_bytes(int64_t psi, int world, int64_t n_blocks) {
 
 size_t replay_scratch_bytes(int64_t psi, int world, int64_t n_steps) {
   const int64_t n_tiles = (psi + kReplayTile - 1) / kReplayTile;
-  return (size_t)n_steps * world * (n_tiles + 1) * sizeof(uint32_t) + (size_t)n_steps * 3 * sizeof(float) + 256;
+  return (size_t)n_steps * world * (n_tiles + 1) * sizeof(uint32_t) + (size_t)n_steps * 3 * sizeof(float) + 256 +
+         (size_t)n_tiles * 4 * sizeof(uint32_t);   // + the exact-re-run queue
 }
 
 cudaError_t launch_tile_start(const uint32_t* block, uint64_t K, int64_t psi, uint32_t* start, cudaStream_t s) {
@@ -576,7 +633,10 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
   // the window of tiles that hold [lo, hi): tile0 .. tile0 + n_tiles - 1 (start table: n_tiles + 1)
   const int64_t tile0 = (int64_t)(lo >> kReplayTileShift);
   const int64_t n_tiles = (int64_t)((hi - 1) >> kReplayTileShift) - tile0 + 1;
-  const size_t tbytes = (size_t)n_steps * world * (n_tiles + 1) * sizeof(uint32_t);
+  // scratch: the start table, then the exact-re-run queue (a count and one word per warp region)
+  const size_t sbytes = ((size_t)n_steps * world * (n_tiles + 1) * sizeof(uint32_t) + 15) & ~(size_t)15;
+  const size_t fix_words = (size_t)n_tiles * (kReplayTile / (128 * ReplayShape<LOWDIFF_ADAM>::slots));
+  const size_t tbytes = sbytes + 16 + fix_words * sizeof(uint32_t);
   if (c->replay_scratch_bytes < tbytes) {
     if (c->replay_scratch) cudaFree(c->replay_scratch);
     c->replay_scratch = nullptr;
@@ -586,6 +646,8 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
     c->replay_scratch_bytes = tbytes;
   }
   uint32_t* start = static_cast<uint32_t*>(c->replay_scratch);
+  unsigned int* fix_count = reinterpret_cast<unsigned int*>(static_cast<char*>(c->replay_scratch) + sbytes);
+  uint32_t* fix_list = reinterpret_cast<uint32_t*>(static_cast<char*>(c->replay_scratch) + sbytes + 16);
   const int sms = num_sms2();
   AdamK ak{consts5[0], consts5[1], consts5[2], consts5[3], consts5[4], -0.0f};
   int h;
@@ -602,14 +664,21 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
   const unsigned grid = (unsigned)n_tiles;
   const int dm = div_mode(mean, world);
   const bool eps_ok = ak.eps >= 0x1p-60f && ak.eps <= 0x1p59f;   // adam_u_fast's precondition
-#define LD_REPLAY(OPT, DIV, W)                                                                                  \
-  do {                                                                                                        \
-    if (OPT == LOWDIFF_SGD || eps_ok)                                                                         \
-      replay_kernel<OPT, DIV, W, true><<<grid, ReplayShape<OPT>::threads, 0, s>>>(                            \
-          diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, lo, hi, tile0, p, m, v);                     \
-    else                                                                                                      \
-      replay_kernel<OPT, DIV, W, false><<<grid, ReplayShape<OPT>::threads, 0, s>>>(                           \
-          diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, lo, hi, tile0, p, m, v);                     \
+  const ReplayArgs A{diffs, world, K, n_steps, start, n_tiles, scal_dev, ak, lo, hi, tile0, p, m, v, fix_list,
+                     fix_count};
+  const bool fix = optim == LOWDIFF_ADAM && eps_ok;   // the fast path may queue regions for a re-run
+  if (fix) {
+    cudaError_t e = cudaMemsetAsync(fix_count, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+  }
+#define LD_REPLAY(OPT, DIV, W)                                                                         \
+  do {                                                                                               \
+    if (OPT == LOWDIFF_SGD || eps_ok)                                                                \
+      replay_kernel<OPT, DIV, W, false><<<grid, ReplayShape<OPT>::threads, 0, s>>>(A);               \
+    else                                                                                             \
+      replay_kernel<OPT, DIV, W, true><<<grid, ReplayShape<OPT>::threads, 0, s>>>(A);                \
+    if (OPT == LOWDIFF_ADAM && eps_ok)                                                               \
+      replay_fix_kernel<DIV, W><<<sms * 4, ReplayShape<LOWDIFF_ADAM>::threads, 0, s>>>(A);           \
   } while (0)
 #define LD_REPLAY_W(OPT, DIV)                                  \
   do {                                                         \
@@ -626,7 +695,7 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
 #undef LD_REPLAY_W
 #undef LD_REPLAY
   prof_end(c, h, s);
-  c->launches += 2;
+  c->launches += fix ? 3 : 2;
   return cudaGetLastError();
 }
 

@@ -101,7 +101,7 @@ __global__ void adam_check_kernel(uint64_t n, uint64_t seed, unsigned long long*
   }
 }
 
-// which = 3: the paired Adam step (adam2_u + the exact fallback, then p - lr*u) on random states vs
+// which = 3: the paired Adam step (adam2_u_agg, the exact form when its window test fails, then p - lr*u) on random states vs
 // the scalar R-11 sequence written with the CUDA intrinsics
 __global__ void adam2_check_kernel(uint64_t n, uint64_t seed, float neg0, unsigned long long* bad,
                                    unsigned long long* first) {
@@ -130,10 +130,10 @@ __global__ void adam2_check_kernel(uint64_t n, uint64_t seed, float neg0, unsign
     }
     const AdamK2 k2 = make_adamk2(b1, c1, b2, c2, eps, neg0);
     f32x2 P = pk2(p[0], p[1]), M = pk2(m[0], m[1]), V = pk2(v[0], v[1]);
-    bool sl;
-    f32x2 u = adam2_u(M, V, pk2(g[0], g[1]), k2, pk2(r1, r1), pk2(r2, r2), &sl);
+    WinAcc w = win_init();
+    f32x2 u = adam2_u_agg(M, V, pk2(g[0], g[1]), k2, pk2(r1, r1), pk2(r2, r2), w);
     const f32x2 mh = mul2(M, pk2(r1, r1)), vh = mul2(V, pk2(r2, r2));
-    if (sl)
+    if (win_bad(w))
       u = pk2(__fdiv_rn(lo2(mh), __fadd_rn(__fsqrt_rn(lo2(vh)), eps)),
               __fdiv_rn(hi2(mh), __fadd_rn(__fsqrt_rn(hi2(vh)), eps)));
     P = sub_prod2(P, pk2(lr, lr), u, k2.nz);
