@@ -375,10 +375,12 @@ __device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, i
   }
 }
 
-// Measured (B200, 100 GPT-2 XL steps): Adam 6 CTAs/SM (80 registers) 198 ms, 7 (72, spills) 203 ms,
-// 5 (96) 207 ms, 8 (64) 216 ms; with 8 ranks per step (MAXW 8) 6 CTAs/SM 97 ms, 5 CTAs 108 ms.
+// Measured (B200, 100 GPT-2 XL steps, tools/run_replay_ab.sh): Adam, 1 rank per step: 6 CTAs/SM
+// (80 registers) 196 ms, 7 (72, spills) 199 ms, 5 (96) 207 ms, 8 (64) 216 ms, 256 threads x 8
+// elements 227-245 ms; 8 ranks per step (MAXW 8): 7 CTAs/SM 96.5 ms, 6 99.5 ms, 5 108 ms.
 template <int OPT, int DIV, int MAXW, bool SAFE>
-__global__ void __launch_bounds__(ReplayShape<OPT>::threads, ReplayShape<OPT>::minb)
+__global__ void __launch_bounds__(ReplayShape<OPT>::threads,
+                                  OPT == LOWDIFF_ADAM && MAXW >= 8 ? ReplayShape<OPT>::minb + 1 : ReplayShape<OPT>::minb)
 replay_kernel(ReplayArgs A) {
   __shared__ __align__(16) float G[kReplayTile];
   const int warp = threadIdx.x >> 5;
