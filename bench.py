@@ -31,6 +31,12 @@ import torch  # noqa: E402
 from inputs import gradient, table  # noqa: E402
 
 METRIC = "compress+exchange+persist GB/s per iteration"
+T_START = time.time()
+
+
+def log(msg):
+    """progress on stderr (elapsed wall seconds), so a slow leg is visible in the driver's log"""
+    print(f"[bench {time.time() - T_START:7.1f}s] {msg}", file=sys.stderr, flush=True)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "note": "fallback (B200_PROFILING.md)"}
 
 
@@ -198,16 +204,26 @@ def _oracle_chain(ref, sizes, ppm):
 
 def _oracle_part(args_):
     sizes, ppm = args_
+    torch.set_num_threads(1)   # one core per worker process
     import oracle as ref
     return _oracle_chain(ref, sizes, ppm)[0]
 
 
-def oracle_all_cores(sample, ppm, cores=None):
+def oracle_pool(n_sample_layers):
+    """Worker processes for oracle_all_cores, one per host core (at most one per sample layer).
+    spawn, not fork: a child forked from a process whose torch/OpenMP thread pool is live can
+    deadlock on a lock held at the fork (seen on the GPU box: the leg never returned)."""
+    import multiprocessing as mp
+    cores = max(1, min(os.cpu_count() or 1, n_sample_layers))
+    pool = mp.get_context("spawn").Pool(cores)
+    pool.map(_oracle_part, [([64], 10000)] * cores)   # workers up, oracle loaded
+    return pool, cores
+
+
+def oracle_all_cores(sample, ppm, pool, cores):
     """The same oracle work on every host core: the sample's layers in `cores` size-balanced parts
     (compression is per layer, the merge per element), one process per part (the oracle is kept
     single-threaded as written).  Returns (wall seconds, cores used)."""
-    import multiprocessing as mp
-    cores = max(1, min(cores or os.cpu_count() or 1, len(sample)))
     parts = [[] for _ in range(cores)]
     load = [0] * cores
     for n in sorted(sample, reverse=True):   # greedy: largest layer to the least loaded part
@@ -215,12 +231,9 @@ def oracle_all_cores(sample, ppm, cores=None):
         parts[i].append(n)
         load[i] += n
     parts = [p_ for p_ in parts if p_]
-    with mp.get_context("fork").Pool(len(parts)) as pool:
-        pool.map(_oracle_part, [([64], ppm)] * len(parts))       # workers up, oracle loaded
-        t0 = time.perf_counter()
-        pool.map(_oracle_part, [(p_, ppm) for p_ in parts])
-        t = time.perf_counter() - t0
-    return t, len(parts)
+    t0 = time.perf_counter()
+    pool.map(_oracle_part, [(p_, ppm) for p_ in parts])
+    return time.perf_counter() - t0, len(parts)
 
 
 def run_reference(args):
@@ -239,7 +252,9 @@ def run_reference(args):
     times = [_oracle_chain(ref, sample, args.ppm)[0] for _ in range(args.steps)]
     t1 = sum(times) / len(times)
     # the host's cores: the same sample split over one oracle process per core
-    times_all = [oracle_all_cores(sample, args.ppm) for _ in range(args.steps)]
+    pool, ncores = oracle_pool(len(sample))
+    with pool:
+        times_all = [oracle_all_cores(sample, args.ppm, pool, ncores) for _ in range(args.steps)]
     t = sum(x for x, _ in times_all) / len(times_all)
     cores = times_all[0][1]
     if t1 <= t:   # a sample too small to pay for the processes: the single thread is the baseline
@@ -325,6 +340,7 @@ def run_ours(args):
         it[0] += 1
         return sd
 
+    log("warm-up + timed steps")
     if not args.no_graphs:
         ctx.set_graphs(True)          # compress + merge replayed as captured CUDA graphs
     for _ in range(args.warmup):
@@ -398,6 +414,7 @@ def run_ours(args):
     # live optimizer step from the gathered blocks (NEXT-1 second half): exchange_update never
     # materialises G; compared with exchange (merge) + a dense Adam step in the algorithmic-byte model
     update = None
+    log("update (live merge + Adam)")
     if not args.no_update:
         p = torch.randn(psi, device=dev) * 0.02
         m = torch.zeros(psi, device=dev)
@@ -475,6 +492,7 @@ def run_ours(args):
 
     # e2e: the same chain through the C ABI with the gradient in pinned HOST memory
     e2e = None
+    log("e2e (host buffers)")
     if not args.no_e2e:
         hg = torch.empty(psi, dtype=torch.float32, pin_memory=True)
         hg.copy_(grads[0].cpu())
@@ -503,6 +521,7 @@ def run_ours(args):
     # full checkpoint (a7): the producer waits only for the D2D stage of the rank's 12 Psi / N shard;
     # the D2H from the stage follows on the side stream (p, m, v stand-ins: the gradient buffers)
     fullck = None
+    log("full checkpoint")
     if not args.no_full:
         fs = (psi * (rank + 1) // world) - (psi * rank // world)
         ctx.full_ckpt(0, grads[0], grads[1], grads[0])   # warm-up: allocates the stage and pinned host
@@ -525,6 +544,7 @@ def run_ours(args):
     # recovery replay (M2): n steps of gathered blocks resident in HBM, fused Adam replay
     recovery = None
     ctx.set_graphs(False)   # the recovery leg compresses into 100 different blocks: plain launches
+    log("recovery replay")
     if not args.no_recovery:
         del dense
         step_bytes = world * 8 * K
@@ -658,6 +678,7 @@ def run_ours(args):
 
     # writer throughput (files, CRC-32C, rename) on this box's storage, reported separately
     writer = None
+    log("writer")
     if not args.no_writer and rank == 0:
         wdir = tempfile.mkdtemp(prefix="lowdiff_w_")
         wctx = ld.Context(sizes, density_ppm=args.ppm, ckpt_dir=wdir, batch_size=2, ring_slots=4, write_files=True)
@@ -675,6 +696,7 @@ def run_ours(args):
     # LowDiff+ CPU replica: host Adam over one rank's shard of an 8-GPU job,
     # fed by the snapshot of the synced gradient (only the shard crosses PCIe); reported separately
     replica = None
+    log("replica")
     if not args.no_replica and rank == 0:
         rw = 8
         rctx = ld.Context(sizes, density_ppm=args.ppm, world=rw, rank=0)
@@ -714,6 +736,7 @@ def run_ours(args):
     # union-compacted differentials (NEXT-4): the union of 8 ranks' blocks (8 simulated ranks with
     # rank-correlated gradients, D4 with alpha = 0.5) compacted over rank 0's shard and over all of Psi
     union = None
+    log("union")
     if not args.no_union and rank == 0:
         NU = 8
         uctx = ld.Context(sizes, density_ppm=args.ppm, world=NU, rank=0, device=local)
@@ -757,6 +780,7 @@ def run_ours(args):
     # its D2H.  M3 = dense bytes / (last D2H done - first bucket ready); interference = slowdown of
     # the proxy backward while the snapshots stream out over PCIe.
     snapshot = None
+    log("snapshot")
     if not args.no_snapshot:
         plan = ld.bucket_plan(sizes, 4 << 20)
         offs = [0]
@@ -829,10 +853,13 @@ def run_ours(args):
                                        "interference": statistics.median(with_s) / t_a - 1.0,
                                        "note": "lowdiff_snapshot_shard: rank 0 of 8 copies its 1/8 of each bucket"}}
 
+    log("cpu baseline (oracle)")
     cpu = None
     if rank == 0 and not args.no_cpu:   # (N > 1: rank 0 alone, on the same bounded sample)
         t_o, sample, (a, b) = oracle_sample(sizes, args.ppm, args.cpu_budget)
-        t_all, cores = oracle_all_cores(sample, args.ppm)
+        pool, ncores = oracle_pool(len(sample))
+        with pool:
+            t_all, cores = oracle_all_cores(sample, args.ppm, pool, ncores)
         if t_o <= t_all:
             t_all, cores = t_o, 1
         cpu = {"value": 4 * sum(sample) / t_all / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
