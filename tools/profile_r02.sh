@@ -17,13 +17,13 @@ timeout 300 python bench.py --workload resnet50 --steps 200 --no-cpu --no-snapsh
 SHORT="python bench.py --steps 4 --warmup 20 --no-cpu --no-e2e --no-writer --no-replica --no-full --no-snapshot --no-union --no-c4-shape --replay-steps 10"
 # our kernels only (the gradient generator's launches are torch's), steady state
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
-    --clock-control none -k "regex:^(small|scan|rescan|chunk_prep|find|digit|count|tile_start|merge|update|replay|materialize|union)" \
+    --clock-control none -k "regex:^(small|scan|refill|chunk_prep|find|digit|count|tile_start|merge|update|replay|materialize|union)" \
     -s 300 -c 200 --csv --log-file $OUT/${TAG}_launches.csv \
     python bench.py --steps 12 --warmup 24 --no-cpu --no-e2e --no-writer --no-replica --no-full --no-snapshot --no-union --no-c4-shape --replay-steps 10 \
     > $OUT/${TAG}_launches.out 2>&1
 tail -2 $OUT/${TAG}_launches.out
-# per call: 1 scan, 1 rescan, 3 chunk_prep, 5 find, 2 digit, 1 count_emit -> skip 20 = call 21
-for ks in scan_kernel:20 count_emit_kernel:20 chunk_prep_kernel:60 digit_kernel:40 merge1_kernel:20 update_kernel:4 replay_kernel:1; do
+# per call: 1 scan, 1 chunk_prep, 1 refill, 3 find, 2 digit, 1 count_emit -> skip 20 = call 21
+for ks in scan_kernel:20 count_emit_kernel:20 chunk_prep_kernel:20 digit_kernel:40 merge1_kernel:20 update_kernel:4 replay_kernel:1; do
   k=${ks%%:*}; skip=${ks##*:}
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:^$k -s $skip -c 1 -o $OUT/${TAG}_prof_$k $SHORT \
       > $OUT/${TAG}_p_$k.out 2>&1
