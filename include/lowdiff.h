@@ -515,7 +515,11 @@ int32_t lowdiff_abi_version(void);
  * __fsqrt_rn/__fdiv_rn (which = 0: all 2^31+1 non-negative floats; which = 1: n pseudo-random
  * operand pairs from `seed`; which = 2: Adam's fused u = mh / (sqrt(vh) + eps) on n random
  * triples; which = 3: the paired (f32x2) Adam step of the replay / update kernels on n random
- * element pairs against the scalar R-11 sequence).  Needs a GPU (current device); synchronous. */
+ * element pairs against the scalar R-11 sequence; which = 4: the division on every exponent pair
+ * of [2^-70, 2^67]^2 (the fast window and ten binades around each edge: extreme mantissas and
+ * n / 138^2 - 4 random ones per pair, all signs); which = 5: the paired Adam direction
+ * mh / (sqrt(vh) + eps) with its window test on every exponent pair of mh in [2^-90, 2^87] and vh
+ * over the whole float range).  Needs a GPU (current device); synchronous. */
 lowdiff_status lowdiff_selftest(int32_t which, uint64_t n, uint64_t seed, uint64_t *mismatches,
                                 uint64_t *first_bad);
 

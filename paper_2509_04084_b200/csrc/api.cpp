@@ -555,7 +555,7 @@ extern "C" {
 int32_t lowdiff_abi_version(void) { return 1; }
 
 lowdiff_status lowdiff_selftest(int32_t which, uint64_t n, uint64_t seed, uint64_t* mismatches, uint64_t* first_bad) {
-  if (!mismatches || !first_bad || which < 0 || which > 3) return LOWDIFF_E_INVALID;
+  if (!mismatches || !first_bad || which < 0 || which > 5) return LOWDIFF_E_INVALID;
   return ld::run_selftest(which, n, seed, mismatches, first_bad) == cudaSuccess ? LOWDIFF_OK : LOWDIFF_E_CUDA;
 }
 

@@ -1,4 +1,5 @@
-// lowdiff_selftest: device-side proofs for the branch-free IEEE helpers of ieee_fast.cuh.
+// lowdiff_selftest: device-side proofs for the branch-free IEEE helpers of ieee_fast.cuh
+// (modes 0-3 below; 4 and 5: every exponent pair of the division / Adam-direction windows).
 //   which = 0: sqrt_rn_nb vs __fsqrt_rn over every non-negative float and -0 (2^31 + 1 inputs)
 //   which = 1: div_rn_nb vs __fdiv_rn on n pseudo-random operand pairs: raw 32-bit patterns
 //              (NaN, Inf, denormals, zeros included) and pairs drawn from the replay's domain
@@ -156,6 +157,63 @@ __global__ void adam2_check_kernel(uint64_t n, uint64_t seed, float neg0, unsign
   }
 }
 
+// which = 4: division, every exponent pair: for each pair (ea, eb) of biased exponents in
+// [57, 194] (|a|, |b| from 2^-70 to 2^67: the window [2^-60, 2^61) of div_rn_fast and ten binades
+// around each edge) the four extreme mantissa combinations and n / 138^2 - 4 random mantissa pairs,
+// all four sign combinations -- div_rn_nb vs __fdiv_rn.  Item i: pair = i % 138^2, k = i / 138^2.
+// which = 5: the paired Adam direction adam2_u_agg (+ the exact form when win_bad) vs the scalar
+// R-11 sequence, every exponent pair of (mh, vh) in [37, 214] x [0, 254] (vh down to denormals),
+// extreme and random mantissas, eps in {1e-8, 1e-6, 2^-60, 1}, zeros mixed in.
+__global__ void pair_sweep_kernel(int which, uint64_t n, uint64_t seed, float neg0, unsigned long long* bad,
+                                  unsigned long long* first) {
+  const uint32_t A0 = which == 4 ? 57u : 37u, NA = which == 4 ? 138u : 178u;
+  const uint32_t B0 = which == 4 ? 57u : 0u, NB = which == 4 ? 138u : 255u;
+  const uint64_t npairs = (uint64_t)NA * NB;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pr = i % npairs, k = i / npairs;
+    const uint32_t ea = A0 + (uint32_t)(pr % NA), eb = B0 + (uint32_t)(pr / NA);
+    const uint64_t h = mix64(seed ^ mix64(i));
+    uint32_t ma, mb;
+    if (k < 4) {   // extreme mantissas
+      ma = (k & 1) ? 0x7FFFFFu : 0u;
+      mb = (k & 2) ? 0x7FFFFFu : 0u;
+    } else {
+      ma = (uint32_t)h & 0x7FFFFFu;
+      mb = (uint32_t)(h >> 23) & 0x7FFFFFu;
+    }
+    const uint32_t sa = (uint32_t)(h >> 62) & 1u, sb = which == 4 ? (uint32_t)(h >> 63) : 0u;
+    const float a = __uint_as_float((sa << 31) | (ea << 23) | ma);
+    const float b = __uint_as_float((sb << 31) | (eb << 23) | mb);
+    uint32_t x, y;
+    if (which == 4) {
+      x = __float_as_uint(div_rn_nb(a, b));
+      y = __float_as_uint(__fdiv_rn(a, b));
+    } else {
+      const float eps_set[4] = {1e-8f, 1e-6f, 0x1p-60f, 1.0f};
+      const float eps = eps_set[(h >> 48) & 3];
+      const float mh = ((h >> 50) & 15) == 0 ? 0.0f : a, vh = ((h >> 54) & 15) == 0 ? 0.0f : b;
+      // one Adam step from m = mh, v = vh with g = 0, b1 = b2 = 1, c1 = c2 = 0, r1 = r2 = 1: the
+      // moments pass through unchanged, so the direction is exactly mh / (sqrt(vh) + eps)
+      const AdamK2 k2 = make_adamk2(1.f, 0.f, 1.f, 0.f, eps, neg0);
+      f32x2 M = pk2(mh, -mh), V = pk2(vh, vh);
+      WinAcc w = win_init();
+      f32x2 u = adam2_u_agg(M, V, pk2(0.f, 0.f), k2, pk2(1.f, 1.f), pk2(1.f, 1.f), w);
+      if (win_bad(w))
+        u = pk2(__fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), eps)), __fdiv_rn(-mh, __fadd_rn(__fsqrt_rn(vh), eps)));
+      const float want = __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), eps));
+      const float want_n = __fdiv_rn(-mh, __fadd_rn(__fsqrt_rn(vh), eps));
+      const uint32_t x1 = __float_as_uint(hi2(u)), y1 = __float_as_uint(want_n);
+      const bool hi_ok = x1 == y1 || ((x1 & 0x7FFFFFFFu) > 0x7F800000u && (y1 & 0x7FFFFFFFu) > 0x7F800000u);
+      x = hi_ok ? __float_as_uint(lo2(u)) : ~__float_as_uint(want);   // a wrong high half fails too
+      y = __float_as_uint(want);
+    }
+    if (x != y && !((x & 0x7FFFFFFFu) > 0x7F800000u && (y & 0x7FFFFFFFu) > 0x7F800000u)) {
+      atomicAdd(bad, 1ull);
+      atomicMin(first, (unsigned long long)i);
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches, uint64_t* first) {
@@ -167,7 +225,8 @@ cudaError_t run_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatc
   if (which == 0) sqrt_check_kernel<<<148 * 16, 256>>>(d, d + 1);
   else if (which == 1) div_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
   else if (which == 2) adam_check_kernel<<<148 * 16, 256>>>(n, seed, d, d + 1);
-  else adam2_check_kernel<<<148 * 16, 256>>>(n, seed, -0.0f, d, d + 1);
+  else if (which == 3) adam2_check_kernel<<<148 * 16, 256>>>(n, seed, -0.0f, d, d + 1);
+  else pair_sweep_kernel<<<148 * 16, 256>>>(which, n, seed, -0.0f, d, d + 1);
   e = cudaDeviceSynchronize();
   unsigned long long h[2] = {0, 0};
   if (e == cudaSuccess) e = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);

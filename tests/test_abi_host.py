@@ -121,6 +121,40 @@ def test_chain_scan_rules(ref, tmp_path):
     assert ld.chain_scan(SIZES, o, 129) == (100, 129)
 
 
+def test_crash_mid_write_leaves_only_tmp_files_which_recovery_ignores(ref, tmp_path):
+    """Writer crash consistency (SPEC.md:287 atomic persist): a file is written
+    as *.tmp and renamed, so a crash mid-write leaves a partial *.tmp at most.  Partial *.tmp files
+    of the next batch and of a newer full checkpoint change neither the library's chain scan nor
+    the oracle's recovery, and a complete file written later under the same name supersedes them."""
+    o = _opts(tmp_path)
+    K = sum(ref.k_table(SIZES, o.density_ppm))
+    psi = sum(SIZES)
+    rng = np.random.default_rng(3)
+    p0 = rng.standard_normal(psi).astype(np.float32)
+    z = np.zeros(psi, np.float32)
+    sc = lambda a, n: [ld.derive_step_scalars(t, 1e-3) for t in range(a, a + n)]
+    blocks = []
+    for _ in range(6):
+        idx = np.sort(rng.choice(psi, K, replace=False)).astype(np.uint32)
+        blocks.append(np.concatenate([idx, (rng.standard_normal(K) * 1e-2).astype(np.float32).view(np.uint32)]))
+    blocks = np.stack(blocks)
+    ld.write_full_host(SIZES, o, 0, p0, z, z)
+    ld.write_batch_host(SIZES, o, 1, sc(1, 4), blocks[:4])
+    want = ref.recover(tmp_path, 1, SIZES, o.density_ppm, -1)
+    assert ld.chain_scan(SIZES, o) == (0, 4) and want[3] == 4
+    # the crash: a partial next batch and a partial newer full checkpoint, as *.tmp
+    full_bytes = open(tmp_path / ref.full_name(0, 0), "rb").read()
+    (tmp_path / (ref.batch_name(0, 5) + ".tmp")).write_bytes(b"LDB1" + bytes(100))
+    (tmp_path / (ref.full_name(0, 4) + ".tmp")).write_bytes(full_bytes[: len(full_bytes) // 3])
+    assert ld.chain_scan(SIZES, o) == (0, 4)
+    got = ref.recover(tmp_path, 1, SIZES, o.density_ppm, -1)
+    assert got[3] == 4 and np.array_equal(got[0], want[0]) and np.array_equal(got[2], want[2])
+    # after the restart the batch is written again, completely: the chain extends past the crash
+    ld.write_batch_host(SIZES, o, 5, sc(5, 2), blocks[4:6])
+    assert ld.chain_scan(SIZES, o) == (0, 6)
+    assert ref.recover(tmp_path, 1, SIZES, o.density_ppm, -1)[3] == 6
+
+
 def _gloo_worker(rank, world, port, tmp, q):
     import torch.distributed as dist
     import paper_2509_04084_b200 as ld2

@@ -238,3 +238,47 @@ def test_nccl_multi_gpu_exchange_update_recovery(tmp_path):
     for pr in procs:
         pr.join(timeout=120)
     assert all(ok for _, ok, _ in res), res
+
+
+def test_ring_backpressure_blocks_after_exactly_ring_slots(tmp_path):
+    """Backpressure: with the consumer stalled, the producer's
+    lowdiff_batch_persist returns for the first R = ring_slots iterations and blocks on the next one
+    until the consumer frees a slot.  The writer is stalled without a test hook: the first file's
+    *.tmp name is a FIFO, so the writer's open() blocks until a reader opens the other end."""
+    import threading
+    import time
+
+    sizes = [5000, 300]
+    ctx = ld.Context(sizes, density_ppm=10000, ckpt_dir=str(tmp_path), batch_size=1, ring_slots=2,
+                     write_files=True, fsync=False, optim=ld.ADAM)
+    K = ctx.K
+    fifo = tmp_path / "ld_diff_r000_000000000001.ldb.tmp"
+    os.mkfifo(fifo)
+    g = torch.randn(sum(sizes), device=DEV)
+    r = torch.zeros(sum(sizes), device=DEV)
+    sends = [torch.empty(2 * K, dtype=torch.int32, device=DEV) for _ in range(3)]
+    rd = None
+    try:
+        for t in (1, 2):                          # iteration 1 -> the (stalled) writer, 2 -> the second slot
+            ctx.compress(g, r, sends[t - 1])
+            ctx.batch_persist(t, ld.derive_step_scalars(t, 1e-3), sends[t - 1])
+        ctx.compress(g, r, sends[2])
+        torch.cuda.synchronize()
+        done = threading.Event()
+        th = threading.Thread(target=lambda: (ctx.batch_persist(3, ld.derive_step_scalars(3, 1e-3), sends[2]),
+                                              done.set()), daemon=True)
+        th.start()
+        time.sleep(1.0)
+        assert not done.is_set(), "the third persist should block: both ring slots are held"
+        rd = os.open(fifo, os.O_RDONLY | os.O_NONBLOCK)   # release the writer
+        th.join(timeout=30)
+        assert done.is_set(), "the blocked persist never resumed after the writer was released"
+        assert ctx.stats()["ring_stall_ns"] >= 0.5e9
+    finally:
+        if rd is None:
+            rd = os.open(fifo, os.O_RDONLY | os.O_NONBLOCK)
+        os.close(rd)
+    try:
+        ctx.close()
+    except ld.LowDiffError:
+        pass   # the first file went into the pipe; later files are regular
