@@ -421,6 +421,15 @@ template <bool EF>
 __global__ void __launch_bounds__(kScanWarps * 32, LD_SCAN_MINB)
 scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int lazy) {
   __shared__ uint64_t sbuf_all[kScanWarps][kCandBuf];
+  {  // the select chain's per-call state (histograms, candidate totals, counters, look-back states):
+     // zeroed here -- it is first read after this grid -- instead of by four memset graph nodes
+    const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t nh = (uint64_t)P.n_large * kHistRow;
+    for (uint64_t i = gid; i < nh; i += nthr) P.hist[i] = 0u;
+    if (gid < (uint64_t)P.n_large) P.layer_total[gid] = 0u;
+    if (gid < 8) P.counters[gid] = 0u;
+    for (uint64_t i = gid; i < (uint64_t)P.n_chunks; i += nthr) P.chunk_state[i] = 0ull;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t w = blockIdx.x;
@@ -447,7 +456,6 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
                                                   (uint32_t)cbase, thr, lT, lcut, lane, lt, bad);
   if (lane == 0) {
     P.seg_count[segid] = run > cs ? (run | kDirect) : run;   // layer totals: the select's first pass
-    if (run > cs) atomicAdd(&P.counters[5], 1u);   // DIRECT segments (stats)
   }
   if (bad) { atomicAdd(&P.err[0], 1u); atomicMin(&P.err[1], (uint32_t)P.large_layers[slot]); }
 }
@@ -635,6 +643,7 @@ __device__ __forceinline__ void chunk_prep_round(const DevPlan& P, const float* 
     if (lane == 0) {
       P.chunk_count[ch] = total;
       P.chunk_dm[ch] = dm;
+      if (dm && mode == 0) atomicAdd(&P.counters[5], (uint32_t)__popc(dm));   // DIRECT segments (stats)
       if (uniform) atomicAdd(s_tot, total + dcnt);
       else atomicAdd(&P.layer_total[slot], total + dcnt);   // per-layer candidate count
     }
@@ -1200,11 +1209,8 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
     c->lazy_residual = nullptr;
     return cudaGetLastError();
   }
-  // per-call state: digit histograms, candidate totals, counters, look-back states
-  if ((e = cudaMemsetAsync(P.hist, 0, compress_hist_bytes(P.n_large), s)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(P.layer_total, 0, (size_t)P.n_large * 4, s)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(P.counters, 0, 8 * sizeof(uint32_t), s)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(P.chunk_state, 0, (size_t)P.n_chunks * 8, s)) != cudaSuccess) return e;
+  // (the per-call state -- digit histograms, candidate totals, counters, look-back states -- is
+  // zeroed by the scan kernel itself)
   const int layer_blocks = (P.n_large * 32 + 255) / 256;     // warp per large layer
   const int chunk_blocks = (P.n_chunks + 7) / 8;              // warp per chunk
   const unsigned scan_grid = (unsigned)P.n_chunks * kPiecesPerChunk;   // full grid: no tail loop
