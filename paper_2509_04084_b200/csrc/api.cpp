@@ -171,7 +171,11 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   const size_t nc = (size_t)std::max(1, P.n_chunks), nl = (size_t)std::max(1, P.n_large);
   void* p;
   // bounded candidate scratch: cs slots per 1024-element segment, O(K) in total
-  P.cs = ld::compress_seg_capacity(c->cfg.density_ppm);
+  P.cs = ld::compress_seg_capacity(c->cfg.density_ppm, (uint64_t)P.n_chunks * ld::kSegsPerChunk);
+  if (const char* v = std::getenv("LOWDIFF_SEG_SLOTS")) {   // tests / tuning: force the slot capacity
+    const int f = std::atoi(v);
+    if (f >= 8 && f <= ld::kSeg) P.cs = f & ~7;
+  }
   if ((st = dalloc(c, nc * ld::kSegsPerChunk * (size_t)P.cs * sizeof(uint64_t), &p))) return st; P.cand = (uint64_t*)p;
   if ((st = dalloc(c, nc * ld::kSegsPerChunk * sizeof(uint32_t), &p))) return st; P.seg_count = (uint32_t*)p;
   if ((st = dalloc(c, nc * 4 * 3, &p))) return st;

@@ -1165,10 +1165,15 @@ int num_sms() {
 size_t compress_hist_bytes(int n_large) { return (size_t)n_large * kHistRow * sizeof(uint32_t); }
 
 // per-segment candidate capacity: ~11.5 x the expected candidates of a 1024-element segment at the
-// band's ~1.5 k_l, a multiple of 8 in [32, 1024]: with the plan, <= 1 B/param of scratch at 1%
-int compress_seg_capacity(uint32_t ppm) {
+// band's ~1.5 k_l, a multiple of 8 in [32, 1024]: <= 1 B/param of scratch at 1 % -- unless the whole
+// slot array fits in kSlotFloorBytes anyway (small models), then up to a whole segment, so that a
+// segment never overflows into the slower DIRECT path (ResNet-50: 25 K segments -> 1024 slots,
+// 205 MB; GPT-2 XL and BERT-large keep the O(K) bound)
+constexpr double kSlotFloorBytes = 256.0 * (1 << 20);
+int compress_seg_capacity(uint32_t ppm, uint64_t n_segments) {
   const double want = 11.5 * kSeg * (double)ppm / 1e6;   // 1% density: 120 slots (0.94 B/param)
-  int cs = ((int)want + 7) & ~7;
+  const double floor_cs = n_segments ? kSlotFloorBytes / (8.0 * (double)n_segments) : (double)kSeg;
+  int cs = ((int)std::max(want, std::min(floor_cs, (double)kSeg)) + 7) & ~7;
   return cs < 32 ? 32 : cs > kSeg ? kSeg : cs;
 }
 
