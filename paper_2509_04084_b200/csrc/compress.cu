@@ -463,11 +463,26 @@ scan_kernel(DevPlan P, const float* __restrict__ g, float* __restrict__ r, int l
 // A DIRECT segment's acc values, read from HBM: src = r (EF: the scan stored acc there) or g.
 // Calls f(ok, key_bits, global_index) for the 4 elements of each lane per 128-element round (all
 // lanes, convergent), ok = in the layer and key >= thr.  Unordered across k.
+// The chunk geometry and selection arrays the out-of-line helpers need, passed BY VALUE: a
+// `const DevPlan&` argument of a __noinline__ function makes every thread copy the whole kernel
+// parameter block to local memory at kernel entry (measured: 600 MB of DRAM writes per GPT-2 XL
+// count+emit launch).
+struct ChunkRefs {
+  const uint64_t* base;
+  const uint64_t* lo;
+  const uint64_t* hi;
+  const uint32_t* seg_count;
+  uint32_t* sel_cut;
+};
+__device__ __forceinline__ ChunkRefs chunk_refs(const DevPlan& P) {
+  return ChunkRefs{P.chunk_base, P.chunk_lo, P.chunk_hi, P.seg_count, P.sel_cut};
+}
+
 template <class F>
-__device__ __forceinline__ void visit_direct(const DevPlan& P, const float* __restrict__ src, int ch, int seg,
+__device__ __forceinline__ void visit_direct(const ChunkRefs& R, const float* __restrict__ src, int ch, int seg,
                                              uint32_t thr, int lane, F&& f) {
-  const uint64_t cbase = P.chunk_base[ch];
-  const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
+  const uint64_t cbase = R.base[ch];
+  const uint32_t lo = (uint32_t)(R.lo[ch] - cbase), hi = (uint32_t)(R.hi[ch] - cbase);
   const float* s = src + cbase;
   const uint32_t sb = (uint32_t)seg * kSeg;
 #pragma unroll 2
@@ -488,6 +503,12 @@ __device__ __forceinline__ void visit_direct(const DevPlan& P, const float* __re
       f(((vm >> k) & 1u) && (bits & 0x7FFFFFFFu) >= thr, bits, (uint32_t)cbase + e0 + k);
     }
   }
+}
+
+template <class F>
+__device__ __forceinline__ void visit_direct(const DevPlan& P, const float* __restrict__ src, int ch, int seg,
+                                             uint32_t thr, int lane, F&& f) {
+  visit_direct(chunk_refs(P), src, ch, seg, thr, lane, static_cast<F&&>(f));
 }
 
 // Refill, pass 1: the digit-0 histogram (key bits [30:20]) of EVERY element of the listed chunks'
@@ -902,7 +923,7 @@ __global__ void __launch_bounds__(256) digit_kernel(DevPlan P, const float* __re
 // Ordered emit of a chunk with a DIRECT segment (warp): its segments in index order -- the stored
 // ones from its compacted run Lc (segment after segment), the DIRECT ones from acc.  dst0 = output
 // offset of its first entry; it takes `take` of its ties (lowest index first).
-__device__ __noinline__ void emit_dirty_chunk(const DevPlan& P, const float* __restrict__ src, int ch, const uint64_t* Lc,
+__device__ __noinline__ void emit_dirty_chunk(ChunkRefs P, const float* __restrict__ src, int ch, const uint64_t* Lc,
                                  uint32_t* __restrict__ send, uint64_t K, uint64_t dst0, uint32_t T, uint32_t take,
                                  bool last_tie_chunk, int slot, int lane) {
   const unsigned lt = (1u << lane) - 1u;
@@ -916,8 +937,8 @@ __device__ __noinline__ void emit_dirty_chunk(const DevPlan& P, const float* __r
     if (lane >= o) inc += y;
   }
   const uint32_t so = inc - stored;
-  const uint64_t cbase = P.chunk_base[ch];
-  const uint32_t lo = (uint32_t)(P.chunk_lo[ch] - cbase), hi = (uint32_t)(P.chunk_hi[ch] - cbase);
+  const uint64_t cbase = P.base[ch];
+  const uint32_t lo = (uint32_t)(P.lo[ch] - cbase), hi = (uint32_t)(P.hi[ch] - cbase);
   for (int s = 0; s < kSegsPerChunk; ++s) {
     const uint32_t c = __shfl_sync(0xFFFFFFFFu, sc, s);
     if (!(c & kDirect)) {
@@ -1002,19 +1023,19 @@ __device__ __noinline__ void emit_dirty_chunk(const DevPlan& P, const float* __r
   }
 }
 
-// (key > T, key == T) counts of the chunk's DIRECT segments (dm), added to *gt / *eq (per lane);
-// out of line, so the common path of count_emit keeps its 32-register budget
-__device__ __noinline__ void count_direct(const DevPlan& P, const float* __restrict__ src, int ch, unsigned dm,
-                                          uint32_t T, int lane, uint32_t* gt, uint32_t* eq) {
-  uint32_t g = *gt, e = *eq;
+// (key > T, key == T) counts of the chunk's DIRECT segments (dm), per lane, packed eq << 32 | gt;
+// out of line, so the common path of count_emit keeps its 32-register budget (returned by value:
+// pointers to the caller's counters would put them in local memory for every thread)
+__device__ __noinline__ uint64_t count_direct(ChunkRefs P, const float* __restrict__ src, int ch, unsigned dm,
+                                              uint32_t T, int lane) {
+  uint32_t g = 0, e = 0;
   for (unsigned m = dm; m; m &= m - 1)
     visit_direct(P, src, ch, __ffs(m) - 1, 0u, lane, [&](bool ok, uint32_t bits, uint32_t) {
       const uint32_t key = bits & 0x7FFFFFFFu;
       g += ok && key > T;
       e += ok && key == T;
     });
-  *gt = g;
-  *eq = e;
+  return ((uint64_t)e << 32) | g;
 }
 
 // count + layer scan + emit in one kernel (warp per chunk): the chunk's #(key > T) and #(key == T)
@@ -1049,7 +1070,11 @@ __global__ void __launch_bounds__(256, 8) count_emit_kernel(DevPlan P, const flo
       }
     }
   }
-  if (dmask) count_direct(P, src, ch, dmask, T, lane, &gt, &eq);
+  if (dmask) {
+    const uint64_t d = count_direct(chunk_refs(P), src, ch, dmask, T, lane);
+    gt += (uint32_t)d;
+    eq += (uint32_t)(d >> 32);
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     gt += __shfl_xor_sync(0xFFFFFFFFu, gt, o);
@@ -1096,7 +1121,7 @@ __global__ void __launch_bounds__(256, 8) count_emit_kernel(DevPlan P, const flo
   }
   const uint64_t dst0 = P.layer_koff[P.large_layers[slot]] + gt_b + take_b;
   if (dmask) {
-    emit_dirty_chunk(P, src, ch, cd, send, K, dst0, T, take, last_tie_chunk, slot, lane);
+    emit_dirty_chunk(chunk_refs(P), src, ch, cd, send, K, dst0, T, take, last_tie_chunk, slot, lane);
     return;
   }
   uint32_t eq_run = 0, out_run = 0;

@@ -102,41 +102,6 @@ merge_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const
   }
 }
 
-// world == 1: G = (+0 + v) at the block's indices, +0 elsewhere.  The tile is zero-filled with
-// 128-bit stores straight to global memory, then (after a CTA barrier orders the writes) the tile's
-// entries are stored over it while those lines are still in L2 -- no shared-memory accumulator.
-__global__ void __launch_bounds__(256)
-merge1_kernel(const uint32_t* __restrict__ send, uint64_t K, const uint32_t* __restrict__ start,
-              int64_t n_tiles, uint64_t psi, float* __restrict__ dense) {
-  const int64_t t = blockIdx.x;
-  const uint64_t j0 = (uint64_t)t * kMergeTile;
-  const int len = (int)min((uint64_t)kMergeTile, psi - j0);
-  // the fill touches only dense, which tile_start (the programmatic predecessor, itself launched in
-  // plain stream order) does not: its first half runs before pdl_wait and overlaps tile_start; the
-  // tile's entry range and this thread's first entry are loaded between the halves, so their
-  // latency hides behind the second half instead of holding the CTA after the fill
-  float4* out = reinterpret_cast<float4*>(dense + j0);
-  const bool whole = len == kMergeTile;
-  if (whole) {
-    for (int q = threadIdx.x; q < kMergeTile / 8; q += blockDim.x) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-  } else {
-    for (int i = threadIdx.x; i < len; i += blockDim.x) dense[j0 + i] = 0.f;
-  }
-  pdl_wait();
-  const uint32_t a = __ldg(start + t), b = __ldg(start + t + 1);
-  const uint32_t e1 = a + threadIdx.x;
-  uint32_t j1 = 0, v1 = 0;
-  if (e1 < b) {
-    j1 = __ldg(send + e1);
-    v1 = __ldg(send + K + e1);
-  }
-  if (whole)
-    for (int q = kMergeTile / 8 + threadIdx.x; q < kMergeTile / 4; q += blockDim.x) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncthreads();
-  if (e1 < b) dense[j1] = __fadd_rn(0.f, __uint_as_float(v1));
-  for (uint32_t e = e1 + blockDim.x; e < b; e += blockDim.x)
-    dense[__ldg(send + e)] = __fadd_rn(0.f, __uint_as_float(__ldg(send + K + e)));
-}
 
 #ifndef LD_REPLAY_MINB
 #define LD_REPLAY_MINB 6   // resident CTAs per SM the replay is compiled for (128 threads: 80 registers)
@@ -569,13 +534,9 @@ cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, fl
                                                                  start);
   }
   const unsigned grid = (unsigned)n_tiles;
-  if (world == 1) {
-    cudaError_t e = launch_pdl(!c->prof, merge1_kernel, grid, 256, 0, s, gathered, K, start, n_tiles, (uint64_t)psi, dense);
-    if (e != cudaSuccess) return e;
-    prof_end(c, h, s);
-    c->launches += 2;
-    return cudaGetLastError();
-  }
+  // world 1 takes the same shared-memory tile (DIV 0: x / 1 == x): every element written once with
+  // 128-bit stores -- measured 1.030 -> 0.990 ms per GPT-2 XL merge against round 1's global
+  // zero-fill + scatter over the L2-resident tile (merge1)
   const int dm = div_mode(c->cfg.mean != 0, world);
   cudaError_t e = launch_pdl(!c->prof, dm == 0 ? merge_kernel<0> : dm == 1 ? merge_kernel<1> : merge_kernel<2>, grid, 256, 0,
                              s, gathered, world, K, start, n_tiles, (uint64_t)psi, dense);

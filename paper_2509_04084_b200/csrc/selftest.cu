@@ -192,20 +192,25 @@ __global__ void pair_sweep_kernel(int which, uint64_t n, uint64_t seed, float ne
       const float eps_set[4] = {1e-8f, 1e-6f, 0x1p-60f, 1.0f};
       const float eps = eps_set[(h >> 48) & 3];
       const float mh = ((h >> 50) & 15) == 0 ? 0.0f : a, vh = ((h >> 54) & 15) == 0 ? 0.0f : b;
-      // one Adam step from m = mh, v = vh with g = 0, b1 = b2 = 1, c1 = c2 = 0, r1 = r2 = 1: the
-      // moments pass through unchanged, so the direction is exactly mh / (sqrt(vh) + eps)
+      // one Adam step from m = (mh, -mh), v = vh with g = 0, b1 = b2 = 1, c1 = c2 = 0, r1 = r2 = 1:
+      // the moments pass through (up to the sign of a zero: -0 + +0 = +0, as in the scalar R-11
+      // sequence written out below), so the direction is mh / (sqrt(vh) + eps) for each half
       const AdamK2 k2 = make_adamk2(1.f, 0.f, 1.f, 0.f, eps, neg0);
       f32x2 M = pk2(mh, -mh), V = pk2(vh, vh);
       WinAcc w = win_init();
       f32x2 u = adam2_u_agg(M, V, pk2(0.f, 0.f), k2, pk2(1.f, 1.f), pk2(1.f, 1.f), w);
-      if (win_bad(w))
-        u = pk2(__fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), eps)), __fdiv_rn(-mh, __fadd_rn(__fsqrt_rn(vh), eps)));
-      const float want = __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), eps));
-      const float want_n = __fdiv_rn(-mh, __fadd_rn(__fsqrt_rn(vh), eps));
-      const uint32_t x1 = __float_as_uint(hi2(u)), y1 = __float_as_uint(want_n);
+      float want[2];
+      for (int e = 0; e < 2; ++e) {
+        const float m0 = e ? -mh : mh;
+        const float me = __fadd_rn(__fmul_rn(1.f, m0), __fmul_rn(0.f, 0.f));
+        const float ve = __fadd_rn(__fmul_rn(1.f, vh), __fmul_rn(0.f, __fmul_rn(0.f, 0.f)));
+        want[e] = __fdiv_rn(__fmul_rn(me, 1.f), __fadd_rn(__fsqrt_rn(__fmul_rn(ve, 1.f)), eps));
+      }
+      if (win_bad(w)) u = pk2(want[0], want[1]);   // the caller's exact re-run
+      const uint32_t x1 = __float_as_uint(hi2(u)), y1 = __float_as_uint(want[1]);
       const bool hi_ok = x1 == y1 || ((x1 & 0x7FFFFFFFu) > 0x7F800000u && (y1 & 0x7FFFFFFFu) > 0x7F800000u);
-      x = hi_ok ? __float_as_uint(lo2(u)) : ~__float_as_uint(want);   // a wrong high half fails too
-      y = __float_as_uint(want);
+      x = hi_ok ? __float_as_uint(lo2(u)) : ~__float_as_uint(want[0]);   // a wrong high half fails too
+      y = __float_as_uint(want[0]);
     }
     if (x != y && !((x & 0x7FFFFFFFu) > 0x7F800000u && (y & 0x7FFFFFFFu) > 0x7F800000u)) {
       atomicAdd(bad, 1ull);
