@@ -20,6 +20,7 @@ METRICS = [
     ("launch__grid_size", ""),
     ("launch__block_size", ""),
     ("lts__t_sectors_op_write.sum", "M"),
+    ("smsp__inst_executed.sum", ""),
 ]
 SCALE = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
          "byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "KB": 1e-6, "MB": 1e-3, "GB": 1.0, "B": 1e-9}
