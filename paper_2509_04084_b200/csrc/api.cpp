@@ -180,7 +180,7 @@ lowdiff_status build_plan(lowdiff_ctx* c) {
   if ((st = dalloc(c, nc * ld::kSegsPerChunk * sizeof(uint32_t), &p))) return st; P.seg_count = (uint32_t*)p;
   if ((st = dalloc(c, nc * 4 * 3, &p))) return st;
   P.chunk_count = (uint32_t*)p; P.chunk_dm = P.chunk_count + nc; P.refill_list = P.chunk_dm + nc;
-  if ((st = dalloc(c, nl * (2048 + 2048 + 512) * 4, &p))) return st; P.hist = (uint32_t*)p;
+  if ((st = dalloc(c, ld::compress_hist_bytes((int)nl), &p))) return st; P.hist = (uint32_t*)p;
   if ((st = dalloc(c, nl * sizeof(ld::LayerSel), &p))) return st; P.sel = (ld::LayerSel*)p;
   CK(cudaMemset(P.sel, 0, nl * sizeof(ld::LayerSel)));   // band = 0: not yet adapted
   if ((st = dalloc(c, nl * 4 * 6, &p))) return st;

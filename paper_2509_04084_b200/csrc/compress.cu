@@ -43,8 +43,17 @@
 namespace ld {
 namespace {
 
-constexpr int kH0 = 2048, kH1 = 2048, kH2 = 512;   // digit sizes: key bits [30:20] [19:9] [8:0]
-constexpr int kHistRow = kH0 + kH1 + kH2;
+// Large layers select in two windowed digits: all candidates have key >= W (the threshold they
+// were taken with), so digit 0 is bin(key) = min(2047, (key - W) >> 11) -- 2047 bins of 2^11 key
+// units (half a binade above W) and an overflow bin -- and digit 1 the low 11 bits of key - W:
+// the k-th key exactly after two passes (a third, absolute digit of round 1 is gone).  A k-th key in
+// the overflow bin (the band was far too low) is treated as a miss and refilled.  (The refill's
+// histogram pass and the small layers keep absolute digits: key bits [30:20], [19:9], [8:0].)
+constexpr int kH0 = 2048, kH1 = 2048, kH2 = 512;
+constexpr int kHistRow = kH0 + kH1;
+constexpr int kWinShift = 11;
+constexpr uint32_t kWinOver = (uint32_t)kH0 - 1;   // the overflow bin
+__device__ __forceinline__ uint32_t win_bin(uint32_t key, uint32_t W) { return min(kWinOver, (key - W) >> kWinShift); }
 #ifndef LD_SCAN_WARPS
 #define LD_SCAN_WARPS 4
 #endif
@@ -646,7 +655,7 @@ __device__ __forceinline__ void chunk_prep_round(const DevPlan& P, const float* 
       for (int u = 0; u < kUnroll; ++u) {
         const uint32_t cc = base + u * 32 + lane;
         if (cc < total) cd[cc] = v[u];
-        const uint32_t bin = (uint32_t)(v[u] >> 52) & 0x7FFu;   // key bits [30:20]
+        const uint32_t bin = win_bin((uint32_t)(v[u] >> 32) & 0x7FFFFFFFu, thr);   // windowed digit 0
         if (uniform) { if (cc < total) atomicAdd(&h0[bin], 1u); }
         else warp_hist_add(h0, cc < total, bin);
       }
@@ -654,8 +663,9 @@ __device__ __forceinline__ void chunk_prep_round(const DevPlan& P, const float* 
     uint32_t dcnt = 0;   // DIRECT segments: their candidates read from acc
     for (unsigned m = dm; m; m &= m - 1) {
       visit_direct(P, src, ch, __ffs(m) - 1, thr, lane, [&](bool ok, uint32_t bits, uint32_t) {
-        if (uniform) { if (ok) atomicAdd(&h0[(bits >> 20) & 0x7FFu], 1u); }
-        else warp_hist_add(h0, ok, (bits >> 20) & 0x7FFu);
+        const uint32_t bin = win_bin(bits & 0x7FFFFFFFu, thr);
+        if (uniform) { if (ok) atomicAdd(&h0[bin], 1u); }
+        else warp_hist_add(h0, ok, bin);
         dcnt += ok;
       });
     }
@@ -713,7 +723,7 @@ __device__ void queue_refill(const DevPlan& P, int slot, int c0, int c1, int lan
 // mode 5: after the refill's histogram pass -- the refill threshold: the lower edge of the digit-0
 //         bin holding the k-th key (every element at or above it is a candidate: >= k of them)
 // mode 1: after the refill's rescan + prep -- digit 0 (a hit by construction)
-// mode 2/3: digit 1/2 for every large layer (mode 2 also predicts the next call's band)
+// mode 2: digit 1 for every large layer -> the exact k-th key, and the next call's band
 // (warp-level: one large layer per warp)
 __device__ void find_layer(const DevPlan& P, int slot, int mode, int lane) {
   const int li = P.large_layers[slot];
@@ -723,9 +733,9 @@ __device__ void find_layer(const DevPlan& P, int slot, int mode, int lane) {
   const int c0 = P.large_chunk0[slot], c1 = P.large_chunk0[slot + 1];
   if (mode == 0) {
     const uint32_t tot = layer_candidates(P, slot);
-    if (tot >= k) {
-      uint32_t bin, above;
-      warp_find_bin(hrow, kH0, k, &bin, &above);
+    uint32_t bin = kWinOver, above = 0;
+    if (tot >= k) warp_find_bin(hrow, kH0, k, &bin, &above);
+    if (tot >= k && bin < kWinOver) {   // a k-th key in the overflow bin is refilled like a miss
       if (lane == 0) {
         S.prefix = bin; S.kleft = k - above; S.total = tot; S.refill = 0;
         P.trace[slot] = 0;
@@ -740,8 +750,9 @@ __device__ void find_layer(const DevPlan& P, int slot, int mode, int lane) {
         atomicAdd(&P.counters[3], tot);
       }
     } else {
-      // missed: the exact top-k is not inside the band.  The refill histograms every element of
-      // the layer (refill_hist_kernel), then rescans at the digit-0 bin of the k-th key (mode 5).
+      // missed (or the k-th key lies in the window's overflow bin): the refill histograms every
+      // element of the layer (refill_hist_kernel), then rescans at the digit-0 bin of the k-th key
+      // (mode 5): the new window base W = that bin's lower edge, so T lies within 2^20 above W.
       queue_refill(P, slot, c0, c1, lane);
       if (lane == 0) {
         S.refill = 1;
@@ -767,46 +778,46 @@ __device__ void find_layer(const DevPlan& P, int slot, int mode, int lane) {
     uint32_t bin, above;
     warp_find_bin(hrow, kH0, k, &bin, &above);
     if (lane == 0) { S.prefix = bin; S.kleft = k - above; S.total = tot; }
-  } else {
-    const int nb = mode == 2 ? kH1 : kH2;
-    const uint32_t* h = hrow + (mode == 2 ? kH0 : kH0 + kH1);
+  } else {   // mode 2: digit 1 -> the exact k-th key T and the ties to take; the next call's band
+    const uint32_t* h = hrow + kH0;
     uint32_t bin, above;
-    warp_find_bin(h, nb, S.kleft, &bin, &above);
-    if (mode == 2) {
-      // Speculative band for the next call: the key with C = band x k_l candidate keys at or above
-      // it (digit-0 resolution, refined with the digit-1 histogram when C falls in T's digit-0
-      // bin).  Only a prediction -- the next call checks #candidates >= k_l and refills otherwise.
-      const float band = S.band > 0.f ? S.band : kBandAim;
-      const uint32_t C = max(k + 32u, (uint32_t)fminf((float)k * band, 4.0e9f));
-      // (a refilled layer's fallback is its refill threshold, which admitted >= k_l this call)
-      uint32_t nt = S.refill ? P.thr_used[slot] : P.thr[slot];
-      if (S.total >= C) {
-        uint32_t b0, a0;
-        warp_find_bin(hrow, kH0, C, &b0, &a0);
-        if (b0 == S.prefix) {
-          uint32_t b1, a1;
-          warp_find_bin(h, nb, C - a0, &b1, &a1);
-          nt = (b0 << 20) | (b1 << 9);
-        } else {
-          nt = b0 << 20;
-        }
+    warp_find_bin(h, kH1, S.kleft, &bin, &above);
+    const uint32_t W = P.thr_used[slot];
+    const uint32_t T = W + (S.prefix << kWinShift) + bin;
+    // Speculative band for the next call: the key with C = band x k_l candidate keys at or above
+    // it (digit-0 resolution, refined with the digit-1 histogram when C falls in T's digit-0 bin).
+    // Only a prediction -- the next call checks #candidates >= k_l and refills otherwise.
+    const float band = S.band > 0.f ? S.band : kBandAim;
+    const uint32_t C = max(k + 32u, (uint32_t)fminf((float)k * band, 4.0e9f));
+    // (a refilled layer's fallback is its refill threshold, which admitted >= k_l this call)
+    uint32_t nt = S.refill ? W : P.thr[slot];
+    if (S.total >= C) {
+      uint32_t b0, a0;
+      warp_find_bin(hrow, kH0, C, &b0, &a0);
+      if (b0 == S.prefix) {
+        uint32_t b1, a1;
+        warp_find_bin(h, kH1, C - a0, &b1, &a1);
+        nt = W + (b0 << kWinShift) + b1;
+      } else {
+        nt = W + (b0 << kWinShift);
       }
-      // drift share: under error feedback the k-th key moved from T_{t-1} (sel_T, still the previous
-      // call's) to T_t (>= the digit-1 prefix); lead the next band by alpha x the smaller of this
-      // drift and the previous call's, so a T that alternates (periodic inputs) gets no lead.
-      const uint32_t t_lo = ((S.prefix << 11) | bin) << 9;
-      const uint32_t t_prev = P.sel_T[slot];
-      const uint32_t d_now = (t_prev != 0xFFFFFFFFu && t_lo > t_prev) ? t_lo - t_prev : 0u;
-      const uint32_t d = min(d_now, S.drift);
-      uint32_t na = nt;
-      if (d > 0 && nt != 0xFFFFFFFFu) {
-        const float a = fmaxf(0.f, fminf(0.5f, S.alpha));
-        na = nt + (uint32_t)(a * (float)d);
-        na = min(na, 0x7F800000u);
-      }
-      if (lane == 0) { S.next_thr = na; S.next_safe = nt; S.drift = d_now; }
     }
-    if (lane == 0) { S.prefix = (S.prefix << (mode == 2 ? 11 : 9)) | bin; S.kleft -= above; }
+    // drift share: under error feedback the k-th key moved from T_{t-1} (sel_T, still the previous
+    // call's) to T_t; lead the next band by alpha x the smaller of this drift and the previous
+    // call's, so a T that alternates (periodic inputs) gets no lead.
+    const uint32_t t_prev = P.sel_T[slot];
+    const uint32_t d_now = (t_prev != 0xFFFFFFFFu && T > t_prev) ? T - t_prev : 0u;
+    const uint32_t d = min(d_now, S.drift);
+    uint32_t na = nt;
+    if (d > 0 && nt != 0xFFFFFFFFu) {
+      const float a = fmaxf(0.f, fminf(0.5f, S.alpha));
+      na = nt + (uint32_t)(a * (float)d);
+      na = min(na, 0x7F800000u);
+    }
+    if (lane == 0) {
+      S.next_thr = na; S.next_safe = nt; S.drift = d_now;
+      S.prefix = T; S.kleft -= above;
+    }
   }
 }
 
@@ -865,10 +876,10 @@ __global__ void __launch_bounds__(256) refill_kernel(DevPlan P, const float* __r
 }
 
 
-// digit d (1 or 2) histogram over the candidates matching the prefix (the chunk list + its DIRECT
-// segments' acc): warp per chunk, 8 chunks per CTA aggregated in shared memory when they belong
-// to one layer
-__global__ void __launch_bounds__(256) digit_kernel(DevPlan P, const float* __restrict__ src, int d) {
+// digit 1 histogram (the low 11 bits of key - W) over the candidates in the k-th key's windowed
+// digit-0 bin (the chunk list + its DIRECT segments' acc): warp per chunk, 8 chunks per CTA
+// aggregated in shared memory when they belong to one layer
+__global__ void __launch_bounds__(256) digit_kernel(DevPlan P, const float* __restrict__ src) {
   pdl_wait();
   pdl_trigger();
   __shared__ uint32_t sh[kH1];
@@ -877,23 +888,20 @@ __global__ void __launch_bounds__(256) digit_kernel(DevPlan P, const float* __re
   const int c_last = min(P.n_chunks, c_first + 8) - 1;
   const int ch = c_first + (threadIdx.x >> 5);
   const bool uniform = P.chunk_slot[c_first] == P.chunk_slot[c_last];
-  const int nb = d == 1 ? kH1 : kH2;
   if (uniform) {
-    for (int b = threadIdx.x; b < nb; b += 256) sh[b] = 0;
+    for (int b = threadIdx.x; b < kH1; b += 256) sh[b] = 0;
     __syncthreads();
   }
-  const int shift = d == 1 ? 9 : 0;
-  const int hs = d == 1 ? 20 : 9;
-  const uint32_t mask = d == 1 ? 0x7FFu : 0x1FFu;
   if (ch <= c_last) {
     const int slot = P.chunk_slot[ch];
     const uint32_t pre = P.sel[slot].prefix;
-    uint32_t* h = uniform ? sh : P.hist + (uint64_t)slot * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
+    const uint32_t W = P.thr_used[slot];
+    uint32_t* h = uniform ? sh : P.hist + (uint64_t)slot * kHistRow + kH0;
     const uint32_t cnt = P.chunk_count[ch];
     const uint64_t* cd = seg_slot(P, (uint64_t)ch * kSegsPerChunk);
     auto add = [&](bool ok, uint32_t key) {
-      const bool m = ok && (key >> hs) == pre;
-      const uint32_t bin = (key >> shift) & mask;
+      const bool m = ok && win_bin(key, W) == pre;
+      const uint32_t bin = (key - W) & 0x7FFu;
       if (uniform) { if (m) atomicAdd(&h[bin], 1u); }
       else warp_hist_add(h, m, bin);
     };
@@ -907,15 +915,14 @@ __global__ void __launch_bounds__(256) digit_kernel(DevPlan P, const float* __re
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) add(base + u * 32 + lane < cnt, key[u]);
     }
-    const uint32_t thr = P.thr_used[slot];
     for (unsigned m = P.chunk_dm[ch]; m; m &= m - 1)
-      visit_direct(P, src, ch, __ffs(m) - 1, thr, lane,
+      visit_direct(P, src, ch, __ffs(m) - 1, W, lane,
                    [&](bool ok, uint32_t bits, uint32_t) { add(ok, bits & 0x7FFFFFFFu); });
   }
   if (uniform) {
     __syncthreads();
-    uint32_t* hg = P.hist + (uint64_t)P.chunk_slot[c_first] * kHistRow + (d == 1 ? kH0 : kH0 + kH1);
-    for (int b = threadIdx.x; b < nb; b += 256)
+    uint32_t* hg = P.hist + (uint64_t)P.chunk_slot[c_first] * kHistRow + kH0;
+    for (int b = threadIdx.x; b < kH1; b += 256)
       if (sh[b]) atomicAdd(&hg[b], sh[b]);
   }
 }
@@ -1269,17 +1276,15 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
   e = ef ? launch_pdl_ex(pdl, true, refill_kernel<true>, refill_grid[1], 256, 0, s, P, grad, residual, src)
          : launch_pdl_ex(pdl, true, refill_kernel<false>, refill_grid[0], 256, 0, s, P, grad, residual, src);
   if (e != cudaSuccess) return e;
-  if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, src, 1)) != cudaSuccess) return e;
+  if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, src)) != cudaSuccess) return e;
   if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 2)) != cudaSuccess) return e;
-  if ((e = launch_pdl(pdl, digit_kernel, chunk_blocks, 256, 0, s, P, src, 2)) != cudaSuccess) return e;
-  if ((e = launch_pdl(pdl, find_kernel, layer_blocks, 256, 0, s, P, 3)) != cudaSuccess) return e;
   prof_end(c, hs, s);
   prof_begin(c, "emit", s, &h);
   if ((e = launch_pdl(pdl, count_emit_kernel, chunk_blocks, 256, 0, s, P, src, send, (uint64_t)c->K)) != cudaSuccess)
     return e;
   prof_end(c, h, s);
   if (P.n_small && c->aux && (e = cudaStreamWaitEvent(s, c->ev_join, 0)) != cudaSuccess) return e;   // join
-  c->launches += 9;
+  c->launches += 7;
   c->lazy_residual = ef ? residual : nullptr;   // this call's large-layer selection is now pending
   return cudaGetLastError();
 }

@@ -287,6 +287,7 @@ cudaError_t launch_compress(lowdiff_ctx* c, const float* grad, float* residual, 
                             cudaStream_t s);
 cudaError_t launch_materialize(lowdiff_ctx* c, float* residual, cudaStream_t s);
 int compress_seg_capacity(uint32_t ppm, uint64_t n_segments);   // candidate slots per 1024-element segment
+size_t compress_hist_bytes(int n_large);   // the select chain's per-layer radix histograms
 cudaError_t launch_merge(lowdiff_ctx* c, int world, const uint32_t* gathered, float* dense,
                          cudaStream_t s);
 // replays elements [lo, hi); p, m, v point at element lo.  ranges: NULL (every entry of every block
