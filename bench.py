@@ -593,6 +593,17 @@ def run_ours(args):
                     "frac_of_hbm_unfused_model": unfused / t_rep / B_HBM,
                     "fused_algorithmic_gbs_per_rank": fused / t_rep / 1e9,
                     "alu_lane_instr_per_param_step_at_peak": alu_peak * t_rep / (n_rep * S)}
+        # ncu's executed instructions of the same kernel (this round's capture, profiles/): the issue
+        # bound at that count, and this run's fraction of it
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                ipp = json.load(f).get(f"replay_instr_per_param_step@{args.workload}")
+        except (OSError, ValueError):
+            ipp = None
+        if ipp:
+            recovery["ncu_thread_instr_per_param_step"] = ipp
+            recovery["issue_bound_param_steps_per_s"] = alu_peak / ipp
+            recovery["frac_of_issue_bound"] = (n_rep * psi / t_rep) / (alu_peak / ipp) if world == 1 else None
         # SGD replay of the same blocks (SURVEY §8(d) M2, C4 SGD row): HBM model n (8 S + 8 N K)
         ctx.replay_range(ld.SGD, world, n_rep, diffs, rscal, lo, hi, p)   # warm-up
         torch.cuda.synchronize()

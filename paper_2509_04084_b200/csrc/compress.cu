@@ -1050,7 +1050,10 @@ __device__ __noinline__ uint64_t count_direct(ChunkRefs P, const float* __restri
 // published counts, 32 per round) gives the ties taken before it and its output offset, then the
 // ordered emit (the list's second read hits L1/L2; a chunk with a DIRECT segment is emitted
 // segment by segment).  The layer's first chunk also does the per-layer bookkeeping.
-__global__ void __launch_bounds__(256, 8) count_emit_kernel(DevPlan P, const float* __restrict__ src,
+#ifndef LD_EMIT_MINB
+#define LD_EMIT_MINB 8
+#endif
+__global__ void __launch_bounds__(256, LD_EMIT_MINB) count_emit_kernel(DevPlan P, const float* __restrict__ src,
                                                               uint32_t* __restrict__ send, uint64_t K) {
   pdl_wait();
   pdl_trigger();
