@@ -22,8 +22,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     python bench.py --steps 12 --warmup 24 --no-cpu --no-e2e --no-writer --no-replica --no-full --no-snapshot --no-union --no-c4-shape --replay-steps 10 \
     > $OUT/${TAG}_launches.out 2>&1
 tail -2 $OUT/${TAG}_launches.out
-# per call: 1 scan, 1 chunk_prep, 1 refill, 3 find, 2 digit, 1 count_emit -> skip 20 = call 21
-for ks in scan_kernel:20 count_emit_kernel:20 chunk_prep_kernel:20 digit_kernel:40 merge_kernel:20 update_kernel:4 replay_kernel:1; do
+# per call: 1 scan, 1 chunk_prep, 1 refill, 2 find, 1 digit, 1 count_emit -> skip 20 = call 21
+for ks in scan_kernel:20 count_emit_kernel:20 chunk_prep_kernel:20 digit_kernel:20 merge_kernel:20 update_kernel:4 replay_kernel:1; do
   k=${ks%%:*}; skip=${ks##*:}
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:^$k -s $skip -c 1 -o $OUT/${TAG}_prof_$k $SHORT \
       > $OUT/${TAG}_p_$k.out 2>&1
