@@ -301,7 +301,7 @@ __device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, i
     }
     st2 += sstride;
     blk += bstride;
-    const f32x2 LR = pk2(slr, slr), R1 = pk2(sr1, sr1), R2 = pk2(sr2, sr2);
+    const f32x2 LR = pk2(slr, slr), R1 = pk2(sr1, sr1), R2 = pk2(sr2, sr2), R2N = pk2(-sr2, -sr2);
 #pragma unroll
     for (int i = 0; i < kReplaySlots; ++i) {   // float4 slots: 2 independent element pairs each
       const float4 gv = G4w[lane + 32 * i];
@@ -315,8 +315,8 @@ __device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, i
           u0 = adam2_u_exact(M2[2 * i], V2[2 * i], g01, k2, R1, R2, ak.eps);
           u1 = adam2_u_exact(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2, ak.eps);
         } else {
-          u0 = adam2_u_agg(M2[2 * i], V2[2 * i], g01, k2, R1, R2, win);
-          u1 = adam2_u_agg(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2, win);
+          u0 = adam2_u_agg(M2[2 * i], V2[2 * i], g01, k2, R1, R2N, win);
+          u1 = adam2_u_agg(M2[2 * i + 1], V2[2 * i + 1], g23, k2, R1, R2N, win);
         }
         P2[2 * i] = sub_prod2(P2[2 * i], LR, u0, k2.nz);
         P2[2 * i + 1] = sub_prod2(P2[2 * i + 1], LR, u1, k2.nz);

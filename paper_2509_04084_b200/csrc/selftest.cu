@@ -132,7 +132,7 @@ __global__ void adam2_check_kernel(uint64_t n, uint64_t seed, float neg0, unsign
     const AdamK2 k2 = make_adamk2(b1, c1, b2, c2, eps, neg0);
     f32x2 P = pk2(p[0], p[1]), M = pk2(m[0], m[1]), V = pk2(v[0], v[1]);
     WinAcc w = win_init();
-    f32x2 u = adam2_u_agg(M, V, pk2(g[0], g[1]), k2, pk2(r1, r1), pk2(r2, r2), w);
+    f32x2 u = adam2_u_agg(M, V, pk2(g[0], g[1]), k2, pk2(r1, r1), pk2(-r2, -r2), w);
     const f32x2 mh = mul2(M, pk2(r1, r1)), vh = mul2(V, pk2(r2, r2));
     if (win_bad(w))
       u = pk2(__fdiv_rn(lo2(mh), __fadd_rn(__fsqrt_rn(lo2(vh)), eps)),
@@ -198,7 +198,7 @@ __global__ void pair_sweep_kernel(int which, uint64_t n, uint64_t seed, float ne
       const AdamK2 k2 = make_adamk2(1.f, 0.f, 1.f, 0.f, eps, neg0);
       f32x2 M = pk2(mh, -mh), V = pk2(vh, vh);
       WinAcc w = win_init();
-      f32x2 u = adam2_u_agg(M, V, pk2(0.f, 0.f), k2, pk2(1.f, 1.f), pk2(1.f, 1.f), w);
+      f32x2 u = adam2_u_agg(M, V, pk2(0.f, 0.f), k2, pk2(1.f, 1.f), pk2(-1.f, -1.f), w);
       float want[2];
       for (int e = 0; e < 2; ++e) {
         const float m0 = e ? -mh : mh;
