@@ -155,14 +155,25 @@ struct ReplayArgs {
   unsigned int* fix_count;
 };
 
+// cp.async of one 32-bit word global -> shared (LDGSTS): the prefetched entries of the next step land
+// in shared memory without holding registers (a register prefetch was spilled by ptxas right after its
+// load -- an STL waiting on the LDG, 11% of the kernel's stall samples)
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
 // The replay of one warp's region (region `wreg` of tile tl of the window), G_t built in the warp's
 // shared-memory slice Gw.  SAFE = false: Adam's sqrt / division take the branch-free fast
 // sequences (ieee_fast.cuh) with their operand windows folded into a WinAcc; if any operand of any
 // step left the windows, nothing is written and the region is queued for an exact re-run
 // (replay_fix_kernel).  SAFE = true: the intrinsics throughout (that re-run, or an eps outside the
 // fast window).  Either way the written bits are the sequential R-11 recurrence.
+// Sw: the warp's staging words in shared memory, u32[2 * MAXW * 32 + 4] (first-round idx | val |
+// the step's lr, r1, r2)
 template <int OPT, int DIV, int MAXW, bool SAFE>
-__device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, int wreg, float* Gw, int lane) {
+__device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, int wreg, float* Gw, uint32_t* Sw,
+                                              int lane) {
   // elements [lo, hi) are replayed; p, m, v hold exactly that range (p[0] is element lo)
   constexpr int kReplaySlots = ReplayShape<OPT>::slots, kWarpSpan = ReplayShape<OPT>::span;
   static_assert(kWarpSpan == 128 * kReplaySlots, "one float4 per lane per slot");
@@ -211,8 +222,8 @@ __device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, i
   WinAcc win = win_init();
   // Software pipeline over steps: lane r (< 32) holds rank r's entry range of this tile for the
   // current step (ra_c, rb_c) and the next (ra_n, rb_n); the ranges of step s+2 and the first
-  // round of step s+1's entries (pj, pv: entry a_r + lane of every rank < MAXW) are loaded while
-  // step s computes.
+  // round of step s+1's entries (entry a_r + lane of every rank < MAXW, by cp.async into the warp's
+  // staging words Sw) are loaded while step s computes.
   const int wr = world < 32 ? world : 32;
   uint32_t ra_c = 0, rb_c = 0, ra_n = 0, rb_n = 0;
   if (lane < wr) {
@@ -228,38 +239,67 @@ __device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, i
   const uint64_t bstride = (uint64_t)world * 2 * K;          // u32 of the blocks of one step
   const uint64_t sstride = (uint64_t)world * tstride;        // u32 of the start table of one step
   const uint32_t* st2 = start + 2 * sstride + (uint64_t)lane * tstride + tl;   // step s + 2, rank `lane`
-  const float* sc_n = scal + 3;                              // scalars of step s + 1
-  uint32_t pj[MAXW], pv[MAXW];
-  auto load_entries = [&](const uint32_t* blk, uint32_t ra, uint32_t rb) {   // first round of a step
+  const float* sc_n = scal + 3;                              // scalars of step s + 1 (then s + 2 ...)
+  // kCpa (several ranks per step): the prefetched first round and the step's three scalars go to the
+  // warp's staging words Sw by cp.async -- with 2 x MAXW prefetch registers ptxas spilled each
+  // prefetched word right after its load (an STL waiting on the LDG: 11% of the stall samples) and
+  // moved the scalars to uniform registers right after theirs.  Measured, 100 GPT-2 XL steps: 8 ranks
+  // per step over 1/8 of Psi 95.9 -> 77.8 ms; 1 rank 189.5 -> 193.7 ms, so one rank keeps registers.
+  constexpr bool kCpa = MAXW > 1;
+  uint32_t* Ssc = Sw + 2 * MAXW * 32;
+  uint32_t pj[MAXW], pv[MAXW];          // !kCpa: the first round in registers
+  float lr = 0.f, r1 = 0.f, r2 = 0.f;   // !kCpa: the scalars of the prefetched step
+  auto load_entries = [&](const uint32_t* blk, uint32_t ra, uint32_t rb, const float* sc) {   // first round of a step
+    if (kCpa) {
+      if (lane < 3) cp_async4(Ssc + lane, reinterpret_cast<const uint32_t*>(sc) + lane);
+    } else {
+      lr = __ldg(sc);
+      r1 = __ldg(sc + 1);
+      r2 = __ldg(sc + 2);
+    }
 #pragma unroll
     for (int r = 0; r < MAXW; ++r) {
-      pj[r] = 0xFFFFFFFFu;
-      pv[r] = 0u;
+      if (!kCpa) {
+        pj[r] = 0xFFFFFFFFu;
+        pv[r] = 0u;
+      }
       if (r < world) {
         const uint32_t e = __shfl_sync(0xFFFFFFFFu, ra, r) + lane;
         const uint32_t eb = __shfl_sync(0xFFFFFFFFu, rb, r);
         if (e < eb) {
           const uint32_t* idx = blk + (uint64_t)r * 2 * K;
-          pj[r] = __ldg(idx + e) - jw;   // >= kWarpSpan (wrapped) when outside the warp's region
-          pv[r] = __ldg(idx + K + e);
+          if (kCpa) {
+            cp_async4(Sw + r * 32 + lane, idx + e);
+            cp_async4(Sw + (MAXW + r) * 32 + lane, idx + K + e);
+          } else {
+            pj[r] = __ldg(idx + e) - jw;   // >= kWarpSpan (wrapped) when outside the warp's region
+            pv[r] = __ldg(idx + K + e);
+          }
         }
       }
     }
+    if (kCpa) asm volatile("cp.async.commit_group;" ::: "memory");
   };
   const uint32_t* blk = diffs;                               // step s
-  load_entries(blk, ra_c, rb_c);
-  float lr = __ldg(scal), r1 = __ldg(scal + 1), r2 = __ldg(scal + 2);
+  load_entries(blk, ra_c, rb_c, scal);
 #pragma unroll 1
   for (int64_t s = 0; s < n_steps; ++s) {
 #pragma unroll
     for (int i = 0; i < kReplaySlots; ++i) G4w[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kCpa) asm volatile("cp.async.wait_all;" ::: "memory");   // this step's first round and scalars are in Sw
     __syncwarp();
+    const float slr = kCpa ? __uint_as_float(Ssc[0]) : lr, sr1 = kCpa ? __uint_as_float(Ssc[1]) : r1,
+                sr2 = kCpa ? __uint_as_float(Ssc[2]) : r2;
     // rank by rank from +0: the rank-order sum of DESIGN.md R-8 (indices unique within a rank)
 #pragma unroll
     for (int r = 0; r < MAXW; ++r) {
       if (r < world) {
-        if (pj[r] < (uint32_t)kWarpSpan) Gw[pj[r]] = __fadd_rn(Gw[pj[r]], __uint_as_float(pv[r]));
+        if (!kCpa && pj[r] < (uint32_t)kWarpSpan) Gw[pj[r]] = __fadd_rn(Gw[pj[r]], __uint_as_float(pv[r]));
         const uint32_t a = __shfl_sync(0xFFFFFFFFu, ra_c, r), b = __shfl_sync(0xFFFFFFFFu, rb_c, r);
+        if (kCpa && a + lane < b) {
+          const uint32_t jl = Sw[r * 32 + lane] - jw;   // >= kWarpSpan (wrapped) outside the region
+          if (jl < (uint32_t)kWarpSpan) Gw[jl] = __fadd_rn(Gw[jl], __uint_as_float(Sw[(MAXW + r) * 32 + lane]));
+        }
         const uint32_t* idx = blk + (uint64_t)r * 2 * K;
         for (uint32_t e = a + 32 + lane; e < b; e += 32) {
           const uint32_t jl = __ldg(idx + e) - jw;
@@ -286,13 +326,9 @@ __device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, i
       __syncwarp();
     }
     // prefetch for the next steps while this one computes
-    const float slr = lr, sr1 = r1, sr2 = r2;
     uint32_t na = 0, nb = 0;
     if (s + 1 < n_steps) {
-      load_entries(blk + bstride, ra_n, rb_n);
-      lr = __ldg(sc_n);
-      r1 = __ldg(sc_n + 1);
-      r2 = __ldg(sc_n + 2);
+      load_entries(blk + bstride, ra_n, rb_n, sc_n);
       sc_n += 3;
     }
     if (lane < wr && s + 2 < n_steps) {
@@ -362,8 +398,10 @@ __global__ void __launch_bounds__(ReplayShape<OPT>::threads,
                                   OPT == LOWDIFF_ADAM && MAXW >= 8 ? ReplayShape<OPT>::minb + 1 : ReplayShape<OPT>::minb)
 replay_kernel(ReplayArgs A) {
   __shared__ __align__(16) float G[kReplayTile];
+  __shared__ uint32_t S[ReplayShape<OPT>::threads / 32][2 * MAXW * 32 + 4];
   const int warp = threadIdx.x >> 5;
-  replay_region<OPT, DIV, MAXW, SAFE>(A, blockIdx.x, warp, G + warp * ReplayShape<OPT>::span, threadIdx.x & 31);
+  replay_region<OPT, DIV, MAXW, SAFE>(A, blockIdx.x, warp, G + warp * ReplayShape<OPT>::span, S[warp],
+                                      threadIdx.x & 31);
 }
 
 // the exact re-run of the regions replay_kernel queued (Adam only): one warp per queued region
@@ -371,13 +409,14 @@ template <int DIV, int MAXW>
 __global__ void __launch_bounds__(ReplayShape<LOWDIFF_ADAM>::threads)
 replay_fix_kernel(ReplayArgs A) {
   __shared__ __align__(16) float G[kReplayTile];
-  const int warp = threadIdx.x >> 5;
   constexpr int kWarps = ReplayShape<LOWDIFF_ADAM>::threads / 32;
+  __shared__ uint32_t S[kWarps][2 * MAXW * 32 + 4];
+  const int warp = threadIdx.x >> 5;
   const unsigned n = *A.fix_count;
   for (unsigned i = blockIdx.x * kWarps + warp; i < n; i += gridDim.x * kWarps) {
     const uint32_t item = A.fix_list[i];
     replay_region<LOWDIFF_ADAM, DIV, MAXW, true>(A, (int64_t)(item >> 8), (int)(item & 0xFFu),
-                                                 G + warp * ReplayShape<LOWDIFF_ADAM>::span, threadIdx.x & 31);
+                                                 G + warp * ReplayShape<LOWDIFF_ADAM>::span, S[warp], threadIdx.x & 31);
   }
 }
 

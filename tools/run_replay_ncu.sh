@@ -1,0 +1,6 @@
+# replay ncu capture (not product): one 10-step GPT-2 XL Adam replay kernel, full set + source
+set -u
+O=gpurun_out/rncu_${1:-x}
+mkdir -p $O
+timeout 300 python tools/replay_probe.py 100 1 > $O/time.txt 2>&1; cat $O/time.txt
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:replay_kernel -c 1 -o $O/replay python tools/replay_probe.py 10 1 > $O/ncu.log 2>&1; tail -n 2 $O/ncu.log
