@@ -245,12 +245,18 @@ __device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, i
   // prefetched word right after its load (an STL waiting on the LDG: 11% of the stall samples) and
   // moved the scalars to uniform registers right after theirs.  Measured, 100 GPT-2 XL steps: 8 ranks
   // per step over 1/8 of Psi 95.9 -> 77.8 ms; 1 rank 189.5 -> 193.7 ms, so one rank keeps registers.
-  constexpr bool kCpa = MAXW > 1;
+#ifndef LD_CPA_E_MIN
+#define LD_CPA_E_MIN 2
+#endif
+#ifndef LD_CPA_S_MIN
+#define LD_CPA_S_MIN 2
+#endif
+  constexpr bool kCpa = MAXW >= LD_CPA_E_MIN, kCpaS = MAXW >= LD_CPA_S_MIN;
   uint32_t* Ssc = Sw + 2 * MAXW * 32;
   uint32_t pj[MAXW], pv[MAXW];          // !kCpa: the first round in registers
   float lr = 0.f, r1 = 0.f, r2 = 0.f;   // !kCpa: the scalars of the prefetched step
   auto load_entries = [&](const uint32_t* blk, uint32_t ra, uint32_t rb, const float* sc) {   // first round of a step
-    if (kCpa) {
+    if (kCpaS) {
       if (lane < 3) cp_async4(Ssc + lane, reinterpret_cast<const uint32_t*>(sc) + lane);
     } else {
       lr = __ldg(sc);
@@ -278,7 +284,7 @@ __device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, i
         }
       }
     }
-    if (kCpa) asm volatile("cp.async.commit_group;" ::: "memory");
+    if (kCpa || kCpaS) asm volatile("cp.async.commit_group;" ::: "memory");
   };
   const uint32_t* blk = diffs;                               // step s
   load_entries(blk, ra_c, rb_c, scal);
@@ -286,10 +292,10 @@ __device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, i
   for (int64_t s = 0; s < n_steps; ++s) {
 #pragma unroll
     for (int i = 0; i < kReplaySlots; ++i) G4w[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (kCpa) asm volatile("cp.async.wait_all;" ::: "memory");   // this step's first round and scalars are in Sw
+    if (kCpa || kCpaS) asm volatile("cp.async.wait_all;" ::: "memory");   // this step's first round and scalars are in Sw
     __syncwarp();
-    const float slr = kCpa ? __uint_as_float(Ssc[0]) : lr, sr1 = kCpa ? __uint_as_float(Ssc[1]) : r1,
-                sr2 = kCpa ? __uint_as_float(Ssc[2]) : r2;
+    const float slr = kCpaS ? __uint_as_float(Ssc[0]) : lr, sr1 = kCpaS ? __uint_as_float(Ssc[1]) : r1,
+                sr2 = kCpaS ? __uint_as_float(Ssc[2]) : r2;
     // rank by rank from +0: the rank-order sum of DESIGN.md R-8 (indices unique within a rank)
 #pragma unroll
     for (int r = 0; r < MAXW; ++r) {
