@@ -418,7 +418,10 @@ __device__ __forceinline__ void replay_region(const ReplayArgs& A, int64_t tl, i
 
 // Measured (B200, 100 GPT-2 XL steps, tools/run_replay_ab.sh): Adam, 1 rank per step: 6 CTAs/SM
 // (80 registers) 196 ms, 7 (72, spills) 199 ms, 5 (96) 207 ms, 8 (64) 216 ms, 256 threads x 8
-// elements 227-245 ms; 8 ranks per step (MAXW 8): 7 CTAs/SM 96.5 ms, 6 99.5 ms, 5 108 ms.
+// elements 227-245 ms; 8 ranks per step (MAXW 8): 7 CTAs/SM 96.5 ms, 6 99.5 ms, 5 108 ms.  Re-run
+// on the final code (cp.async staging, chained window minima): 1 rank 6 / 7 / 5 CTAs/SM 185.4 /
+// 190.2 / 198.1 ms; 8 ranks 7 / 8 / 6 CTAs/SM 78.6 / 79.8 / 79.0 ms (before the index-pass change;
+// DESIGN.md 4.3).
 template <int OPT, int DIV, int MAXW, bool SAFE>
 __global__ void __launch_bounds__(ReplayShape<OPT>::threads,
                                   OPT == LOWDIFF_ADAM && MAXW >= 8 ? ReplayShape<OPT>::minb + 1 : ReplayShape<OPT>::minb)
