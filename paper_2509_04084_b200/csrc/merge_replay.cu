@@ -50,23 +50,45 @@ __global__ void tile_start_kernel(const uint32_t* __restrict__ blocks, int64_t n
       t_hi = min(t_hi, T1);
       for (uint32_t t = t_lo; t <= t_hi; ++t) st[t - T0] = e;
     };
-    const uint32_t stride = gridDim.x * blockDim.x;
-    uint32_t e = ea + blockIdx.x * blockDim.x + threadIdx.x;
-    // LD_TS_UNROLL entries per thread in flight (one at a time left the replay's index pass
-    // latency-bound: 4.7 ms for 100 GPT-2 XL blocks, 1.3 TB/s; 4 in flight: 3.1 ms; 8: the same;
-    // a one-wave grid instead of the 2.03-wave one measured slower)
-    for (; e + (LD_TS_UNROLL - 1) * stride <= eb; e += LD_TS_UNROLL * stride) {
-      uint32_t prev[LD_TS_UNROLL], cur[LD_TS_UNROLL];
+    const uint32_t nthr = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+    // entries [ea, eb) are real, eb is the sentinel (the tiles after the last entry).  The 16-byte
+    // aligned middle [p0, p1) goes four entries per 128-bit load, LD_TS_UNROLL groups in flight per
+    // thread (one 32-bit entry at a time left the replay's index pass latency-bound: 4.7 ms for 100
+    // GPT-2 XL blocks, 1.3 TB/s; four 32-bit loads in flight 3.1 ms); the unaligned head (< 4
+    // entries), the tail and the sentinel go one entry per thread.
+    const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(idx + ea) >> 2) & 3u);
+    const uint32_t p0 = min(eb, ea + ((4u - mis) & 3u));
+    const uint32_t ng = (eb - p0) / 4u, p1 = p0 + 4u * ng;
+    for (uint32_t e = ea + tid; e < p0; e += nthr) owned(e, e == ea ? 0u : __ldg(idx + e - 1), __ldg(idx + e));
+    for (uint32_t e = p1 + tid; e <= eb; e += nthr) owned(e, e == ea ? 0u : __ldg(idx + e - 1), e == eb ? 0u : __ldg(idx + e));
+    const uint4* v4 = reinterpret_cast<const uint4*>(idx + p0);
+    uint32_t gi = tid;
+    for (; gi + (LD_TS_UNROLL - 1) * nthr < ng; gi += LD_TS_UNROLL * nthr) {
+      uint4 cur[LD_TS_UNROLL];
+      uint32_t prev[LD_TS_UNROLL];
 #pragma unroll
       for (int q = 0; q < LD_TS_UNROLL; ++q) {
-        const uint32_t x = e + q * stride;
-        prev[q] = x == ea ? 0u : __ldg(idx + x - 1);
-        cur[q] = x == eb ? 0u : __ldg(idx + x);
+        const uint32_t g = gi + q * nthr, e = p0 + 4u * g;
+        cur[q] = __ldg(v4 + g);
+        prev[q] = e == ea ? 0u : __ldg(idx + e - 1);
       }
 #pragma unroll
-      for (int q = 0; q < LD_TS_UNROLL; ++q) owned(e + q * stride, prev[q], cur[q]);
+      for (int q = 0; q < LD_TS_UNROLL; ++q) {
+        const uint32_t e = p0 + 4u * (gi + q * nthr);
+        owned(e, prev[q], cur[q].x);
+        owned(e + 1, cur[q].x, cur[q].y);
+        owned(e + 2, cur[q].y, cur[q].z);
+        owned(e + 3, cur[q].z, cur[q].w);
+      }
     }
-    for (; e <= eb; e += stride) owned(e, e == ea ? 0u : __ldg(idx + e - 1), e == eb ? 0u : __ldg(idx + e));
+    for (; gi < ng; gi += nthr) {
+      const uint4 c = __ldg(v4 + gi);
+      const uint32_t e = p0 + 4u * gi;
+      owned(e, e == ea ? 0u : __ldg(idx + e - 1), c.x);
+      owned(e + 1, c.x, c.y);
+      owned(e + 2, c.y, c.z);
+      owned(e + 3, c.z, c.w);
+    }
   }
 }
 
