@@ -722,7 +722,9 @@ cudaError_t launch_replay(lowdiff_ctx* c, int optim, bool mean, const float* con
   {
     const int64_t nb = n_steps * world;
     const unsigned gy = (unsigned)std::min<int64_t>(nb, 65535);
-    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((K + 256) / 256, (int64_t)sms * 16 / gy + 1));
+    // ~96 CTAs per SM in total over the blocks: several waves, so the last one's tail is short
+    // (measured, C4 shape: 16 per SM 60.5 ms, 48 58.4, 96 58.2, 160 58.0; one wave, 8: 63.7)
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((K + 256) / 256, (int64_t)sms * 96 / gy + 1));
     tile_start_kernel<<<dim3(gx, gy), 256, 0, s>>>(diffs, nb, 2 * K, (uint32_t)K, kReplayTileShift, (uint32_t)tile0,
                                                    (uint32_t)(tile0 + n_tiles), ranges, start);
   }
