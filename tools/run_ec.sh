@@ -1,4 +1,4 @@
-# early-clear check (not product): parity tests + bench A/B with and without the overlapped clear
+# early-clear check (not product; needs tools/ab/early_clear.patch applied): parity tests + bench A/B with and without the overlapped clear
 set -u
 O=gpurun_out/ec_${1:-x}
 mkdir -p $O
